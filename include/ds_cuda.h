@@ -1,0 +1,243 @@
+/*
+ * ds_cuda.h — the C-ABI drop-in boundary of the B200-native DeepSpark EASGD hot path.
+ *
+ * Plain C: no exceptions, no STL, no torch types. Device pointers are CUDA device
+ * addresses (local or peer-mapped); `stream` is a cudaStream_t passed as void* (NULL =
+ * the legacy default stream). Every entry point returns a ds_status; the message of
+ * the last failure on the calling thread is available from ds_last_error(). The C++
+ * API in include/deepspark/ (the reference's own headers' surface) sits on top of this
+ * and maps DS_E_CONTRACT -> deepspark::ContractError and DS_E_NUMERIC ->
+ * deepspark::NumericError, as the reference throws them.
+ *
+ * Each entry point names the reference interface it replaces (file:line under
+ * /root/reference/proj/). There is no CPU fallback behind any of them: a missing GPU
+ * or a CUDA failure is DS_E_CUDA.
+ */
+#ifndef DS_CUDA_H
+#define DS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------------------------- */
+/* Status                                                                             */
+/* ---------------------------------------------------------------------------------- */
+typedef enum {
+  DS_OK = 0,
+  DS_E_CONTRACT = 1, /* deepspark::ContractError  (errors.hpp:10-13)  */
+  DS_E_NUMERIC = 2,  /* deepspark::NumericError   (errors.hpp:16-19)  */
+  DS_E_CUDA = 3,     /* CUDA runtime / driver failure, or no device      */
+  DS_E_NOMEM = 4,    /* device allocation failed                         */
+  DS_E_STATE = 5     /* handle used in a state that does not allow it    */
+} ds_status;
+
+const char* ds_last_error(void);
+const char* ds_version(void);
+/* Number of visible CUDA devices (0 when none); DS_E_CUDA if the runtime fails. */
+int ds_device_count(int* count);
+
+/* Finiteness flags written by the update kernels (OR-ed, device uint32). */
+#define DS_FLAG_X_NONFINITE 1u    /* sgd_step: x contains a non-finite value   (param_vector.cpp:29) */
+#define DS_FLAG_G_NONFINITE 2u    /* sgd_step: grad contains a non-finite value (param_vector.cpp:30) */
+#define DS_FLAG_OUT_NONFINITE 4u  /* sgd_step: non-finite result              (param_vector.cpp:34-35) */
+#define DS_FLAG_LOSS_NONFINITE 8u /* loss_and_grad: non-finite loss            (model.cpp:256) */
+#define DS_FLAG_GRAD_NONFINITE 16u /* loss_and_grad: non-finite gradient       (model.cpp:259) */
+#define DS_FLAG_LABEL_RANGE 32u   /* loss_and_grad: label out of range         (model.cpp:176-180) */
+
+/* ---------------------------------------------------------------------------------- */
+/* Elementwise updates — param_vector.hpp:21-38                                       */
+/* ---------------------------------------------------------------------------------- */
+
+/* In-place elastic update, one fused pass: e = a*(w-m); w -= e; m += e, each step one
+ * f32 rounding (no FMA contraction) — elastic_update_elem (param_vector.hpp:34-38) over
+ * a vector, i.e. easgd_update (param_vector.cpp:41-57) without the allocations.
+ * alpha is the f32 moving rate; callers holding a double convert with (float)alpha as
+ * the reference does (param_vector.cpp:50). 16 bytes of HBM traffic per element. */
+int ds_elastic_update(float* w, float* m, uint64_t n, float alpha, void* stream);
+
+/* MasterState::exchange (exchanger.cpp:76-92) against a plain device vector `master`:
+ * out[i] = w'[i], master[i] = m'[i]. `out` may equal `worker` (in place). */
+int ds_elastic_exchange(const float* worker, float* master, float* out, uint64_t n, float alpha,
+                        void* stream);
+
+/* SGD with the engine's optional L2 fold (engine.cpp:75-79 + param_vector.cpp:21-39):
+ *   g' = wd > 0 ? g + f32(wd)*x : g;   out = x - f32(eta)*g'
+ * in f32 with separate roundings. `out` may equal `x`. Non-finite conditions are OR-ed
+ * into *flags_dev (DS_FLAG_*); the vector is still written, the caller decides. */
+int ds_sgd_update(float* out, const float* x, const float* g, uint64_t n, float eta, float wd,
+                  uint32_t* flags_dev, void* stream);
+
+/* Synchronous helper with the reference's exact error behaviour for one sgd_step call:
+ * DS_E_CONTRACT on eta <= 0 or non-finite x/g, DS_E_NUMERIC on non-finite output. */
+int ds_sgd_step_checked(float* out, const float* x, const float* g, uint64_t n, double eta,
+                        void* stream);
+
+/* ---------------------------------------------------------------------------------- */
+/* Synchronous data-parallel SGD — simulator.cpp:156-223 (and its NCCL form)          */
+/* ---------------------------------------------------------------------------------- */
+
+/* gsum[i] += (double)g[i] — the f64 gradient sum of simulate_sync (simulator.cpp:195). */
+int ds_grad_accumulate(double* gsum, const float* g, uint64_t n, void* stream);
+/* out[i] = (float)(gsum[i] / n_workers), then out[i] += f32(wd)*x[i] when wd > 0
+ * (simulator.cpp:204-208). x may be NULL when wd == 0. */
+int ds_grad_average(float* out, const double* gsum, uint64_t n, uint32_t n_workers, float wd,
+                    const float* x, void* stream);
+
+/* ---------------------------------------------------------------------------------- */
+/* Device plumbing for hosts that do not link the CUDA runtime (C++/Go/Java/Python)   */
+/* ---------------------------------------------------------------------------------- */
+int ds_device_alloc(int device, uint64_t bytes, void** out);
+int ds_device_free(void* p);
+/* Copy in any direction (unified addressing). stream == NULL: synchronous. */
+int ds_memcpy(void* dst, const void* src, uint64_t bytes, void* stream);
+int ds_memset(void* dst, int value, uint64_t bytes, void* stream);
+int ds_stream_create(int device, void** stream);
+int ds_stream_destroy(void* stream);
+int ds_stream_sync(void* stream);
+
+/* ---------------------------------------------------------------------------------- */
+/* Model — model.hpp:32-76                                                            */
+/* ---------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t kind;          /* 0 = SoftmaxRegression, 1 = Mlp (model.hpp:13)         */
+  uint32_t n_features;
+  uint32_t n_classes;
+  uint32_t n_hidden;     /* number of tanh hidden layers                            */
+  const uint32_t* hidden; /* host array of n_hidden layer widths                    */
+} ds_model_desc;
+
+/* Model::param_dim (model.cpp:123-129); DS_E_CONTRACT on an invalid model (model.cpp:44-57). */
+int ds_param_dim(const ds_model_desc* model, uint64_t* dim);
+
+/* Bytes of device workspace loss_and_grad needs for `rows` samples. */
+int ds_loss_and_grad_workspace(const ds_model_desc* model, uint32_t rows, uint64_t* bytes);
+
+/* loss_and_grad / loss_only (model.cpp:242-275), f64 internals with the reference's
+ * per-element summation order, gradient rounded once to f32. All pointers are device
+ * pointers: params[P], X[rows*n_features] row-major f32, y[rows] u32, grad[P] (NULL =
+ * loss_only semantics), loss_out one double. Asynchronous; label-range and finiteness
+ * violations are OR-ed into *flags_dev (may be NULL). `workspace` must hold
+ * ds_loss_and_grad_workspace bytes. */
+int ds_loss_and_grad(const ds_model_desc* model, const float* params, const float* X,
+                     const uint32_t* y, uint32_t rows, float* grad, double* loss_out,
+                     void* workspace, uint32_t* flags_dev, void* stream);
+
+/* predict (model.cpp:303-318) for `rows` samples, and the hit count behind accuracy
+ * (model.cpp:320-328): *hits_out (device u64) += #{r : predict(X_r) == y_r}. */
+int ds_predict(const ds_model_desc* model, const float* params, const float* X, uint64_t rows,
+               uint32_t* pred_out, void* stream);
+int ds_count_hits(const ds_model_desc* model, const float* params, const float* X,
+                  const uint32_t* y, uint64_t rows, unsigned long long* hits_out, void* stream);
+
+/* ---------------------------------------------------------------------------------- */
+/* Master — exchanger.hpp:40-72 (MasterState), center variable x~                     */
+/* ---------------------------------------------------------------------------------- */
+typedef struct ds_master ds_master;
+
+#define DS_MODE_LOCKED 0   /* UpdateMode::Locked: exchanges linearized (ticketed)    */
+#define DS_MODE_LOCKFREE 1 /* UpdateMode::LockFree: per-element plain ld/st, lost updates allowed */
+
+/* MasterState(dim, alpha, mode, initial) (exchanger.cpp:65-74) on one device.
+ * init_host: dim floats (must be finite: ContractError otherwise). */
+int ds_master_create(ds_master** out, int device, uint64_t dim, float alpha, int mode,
+                     const float* init_host);
+/* Sharded center: this process owns slice `rank` of `world` (128-byte aligned
+ * contiguous slices). Peers are attached with ds_master_export/ds_master_attach. */
+int ds_master_create_sharded(ds_master** out, int device, uint64_t dim, float alpha, int mode,
+                             int rank, int world, const float* init_host);
+#define DS_IPC_RECORD_BYTES 256
+/* Write this shard's IPC record (DS_IPC_RECORD_BYTES) for the peers. */
+int ds_master_export(ds_master* m, void* record_out);
+/* Attach all `world` records (index = rank; this rank's own is ignored). */
+int ds_master_attach(ds_master* m, const void* records);
+int ds_master_destroy(ds_master* m);
+
+/* MasterState::exchange (exchanger.cpp:76-92): worker/out are device pointers on the
+ * master's device (dim floats each; out may equal worker). Locked mode takes the next
+ * ticket so concurrent exchanges linearize; LockFree streams straight through. */
+int ds_master_exchange(ds_master* m, const float* worker, float* out, void* stream);
+/* Deterministic mode: perform exchange number `ticket` (0-based, global order) only
+ * after exchange ticket-1 completed on every shard; used to replay simulate_async's
+ * serialization (simulator.cpp:105-143) across GPUs. */
+int ds_master_exchange_ticketed(ds_master* m, const float* worker, float* out, uint64_t ticket,
+                                void* stream);
+/* MasterState::snapshot (exchanger.cpp:94-106) into host memory (synchronous). */
+int ds_master_snapshot(ds_master* m, float* host_out);
+/* Device pointer to this process's slice and its [begin,end) element range. */
+int ds_master_local_slice(ds_master* m, float** dev_ptr, uint64_t* begin, uint64_t* end);
+int ds_master_exchange_count(ds_master* m, uint64_t* count);
+int ds_master_dim(ds_master* m, uint64_t* dim);
+/* Reset the ticket sequence and exchange counter (all ranks, quiescent). */
+int ds_master_reset_tickets(ds_master* m);
+
+/* ---------------------------------------------------------------------------------- */
+/* Engine — engine.hpp:17-105 (ShardSweeper, ExchangePolicy, SgdEngine, loop)        */
+/* ---------------------------------------------------------------------------------- */
+typedef struct ds_engine ds_engine;
+
+typedef struct {
+  double eta;
+  double alpha;
+  uint32_t tau;
+  uint32_t batch_size;
+  uint64_t i_max;
+  double loss_cut;
+  double weight_decay;
+  int32_t adaptive;
+} ds_hyper; /* Hyperparams (hyperparams.hpp:10-21) */
+
+#define DS_ENGINE_AUTO 0    /* fused persistent kernel when the model allows, else layered */
+#define DS_ENGINE_LAYERED 1 /* one kernel per layer pass; any depth                        */
+#define DS_ENGINE_FUSED 2   /* persistent single-kernel step (<= 1 hidden layer)            */
+
+/* SgdEngine(model, shard, hp, sweep_seed, initial) (engine.cpp:50-65): uploads the
+ * shard (X row-major f32 [shard_n x n_features], y u32) to `device` once, keeps the
+ * parameters, gradients and sweep order resident. hp is validated like
+ * Hyperparams::validate (hyperparams.cpp:7-18). */
+int ds_engine_create(ds_engine** out, int device, const ds_model_desc* model, const float* X_host,
+                     const uint32_t* y_host, uint64_t shard_n, uint32_t shard_classes,
+                     const ds_hyper* hp, uint64_t sweep_seed, const float* init_host, int kind);
+int ds_engine_destroy(ds_engine* e);
+/* Attach a master: the policy's exchanges run on-device against it (async/LockFree or
+ * Locked as the master was created; deterministic when tickets are given). */
+int ds_engine_attach_master(ds_engine* e, ds_master* m);
+/* Deterministic schedule: this worker's exchanges take the given global tickets in
+ * order (count entries). Pass count 0 to return to ticket-less exchanges. */
+int ds_engine_set_tickets(ds_engine* e, const uint64_t* tickets, uint64_t count);
+
+/* Run `steps` iterations of run_training_loop's body (engine.cpp:96-111): step,
+ * policy, exchange-if-fired (against the attached master; with no master the
+ * exchange is skipped, as with a null ExchangeFn). Asynchronous on the engine's
+ * stream. If stop_at_exchange is nonzero the run ends after the first iteration whose
+ * policy fires WITHOUT performing that exchange (for host ExchangeFn callbacks);
+ * *ran_out (host, optional, synchronous when given) reports the iterations done. */
+int ds_engine_run(ds_engine* e, uint64_t steps, int stop_at_exchange, uint64_t* ran_out);
+/* Block until the engine's queued work finished; returns DS_E_NUMERIC/DS_E_CONTRACT
+ * if any step hit the reference's error conditions (message names the iteration). */
+int ds_engine_sync(ds_engine* e);
+/* Engine stream (cudaStream_t) for event timing / interop. */
+int ds_engine_stream(ds_engine* e, void** stream);
+/* TrainLog rows [first, first+count) (metrics.hpp:11-24), synchronous copy to host.
+ * Any output pointer may be NULL. */
+int ds_engine_log(ds_engine* e, uint64_t first, uint64_t count, double* batch_loss,
+                  double* cumulated, uint8_t* exchanged, uint32_t* period_len);
+int ds_engine_iterations(ds_engine* e, uint64_t* iters);
+/* SgdEngine::params / set_params (engine.hpp:76-78), host copies (synchronous). */
+int ds_engine_get_params(ds_engine* e, float* host_out);
+int ds_engine_set_params(ds_engine* e, const float* host_in);
+/* Device pointer of the live parameter vector (valid until the next run call). */
+int ds_engine_params_device(ds_engine* e, float** dev_ptr);
+/* Resolved policy state (ExchangePolicy, engine.hpp:40-59). */
+int ds_engine_policy(ds_engine* e, double* cumulated, uint32_t* since_exchange, double* loss_cut);
+/* Loop-launch count since creation (kernels this engine launched). */
+int ds_engine_launches(ds_engine* e, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DS_CUDA_H */

@@ -1,0 +1,578 @@
+// engine.cu — the worker's local SGD loop on one B200 (engine.cpp:10-113).
+//
+// SgdEngine keeps its shard, parameters, gradients, policy state and TrainLog in HBM.
+// The host contributes only what is inherently sequential and value-independent: the
+// per-epoch Fisher-Yates order of ShardSweeper (engine.cpp:19-33, seeded mt19937_64
+// bit-identical to the reference), uploaded as a batch plan once per run() call. Each
+// iteration then runs without host round trips:
+//
+//   fused path   (<= 1 hidden layer): ONE persistent kernel executes all steps of the
+//                run — forward, softmax-CE, backward, SGD, ExchangePolicy and the
+//                elastic exchange into the (possibly peer-resident) center — with one
+//                grid barrier per step (mlp_fused.cu).
+//   layered path (any depth): per-layer f64 kernels (model.cu) + SGD + a one-thread
+//                policy kernel + a conditional exchange kernel, stream-ordered.
+//
+// The policy is evaluated on the device (engine.cpp:35-48) so adaptive exchanges need
+// no host sync; the exchange kernels test the device-side fire flag themselves.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "deepspark/rng.hpp"
+#include "ds_common.cuh"
+#include "elementwise.cuh"
+#include "engine.cuh"
+
+namespace dsb {
+namespace {
+
+// run_training_loop body after the step: policy, TrainLog row (engine.cpp:97-110).
+__global__ void policy_kernel(DevState* st, DevLog log) {
+  if (st->err) return;
+  if (st->flags) {
+    st->err = st->flags;
+    st->bad_iter = st->iter + 1;
+    st->fire = 0;
+    return;
+  }
+  const double loss = st->loss;
+  st->cum = dadd(st->cum, loss);
+  st->since += 1;
+  const bool fire = st->adaptive ? (st->cum > st->cut) : (st->since == st->tau);
+  st->period = fire ? st->since : 0u;
+  if (fire) {
+    st->cum = 0.0;
+    st->since = 0;
+    st->exchanges += 1;
+  }
+  st->fire = fire ? 1u : 0u;
+  const unsigned long long row = st->iter;
+  if (row < log.cap) {
+    log.loss[row] = loss;
+    log.cum[row] = st->cum;
+    log.exchanged[row] = fire ? 1 : 0;
+    log.period[row] = st->period;
+  }
+  st->iter = row + 1;
+}
+
+}  // namespace
+}  // namespace dsb
+
+struct ds_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  dsb::ModelInfo model;
+  ds_hyper hp{};
+  uint64_t shard_n = 0;
+  uint32_t shard_classes = 0;
+  float* X = nullptr;
+  uint32_t* y = nullptr;
+  float* params[2] = {nullptr, nullptr};
+  int cur = 0;
+  float* grad = nullptr;
+  double* ws = nullptr;
+  double* act = nullptr;  // fused: [2][B x H]
+  dsb::DevState* st = nullptr;
+  dsb::DevLog log{};
+  unsigned int* bar = nullptr;
+  // batch plan (device) and its pinned staging copy
+  uint32_t* plan = nullptr;
+  uint32_t* plan_rows = nullptr;
+  uint32_t* h_plan = nullptr;
+  uint32_t* h_rows = nullptr;
+  uint64_t plan_cap = 0;  // steps
+  cudaEvent_t plan_ev = nullptr;
+  bool plan_ev_armed = false;
+  // ShardSweeper (host, bit-identical order)
+  std::vector<uint32_t> order;
+  uint64_t pos = 0, epoch = 0, seed = 0;
+  // host mirror of the fixed-period policy and of queued work
+  uint32_t host_since = 0;
+  uint64_t queued = 0;
+  uint64_t host_exchanges = 0;
+  ds_master* master = nullptr;
+  std::vector<uint64_t> tickets;
+  uint64_t* d_tickets = nullptr;
+  int kind = DS_ENGINE_AUTO;
+  bool fused = false;
+  int fused_grid = 0;
+  uint64_t launches = 0;
+};
+
+namespace dsb {
+namespace {
+
+void reshuffle(ds_engine* e) {  // ShardSweeper::reshuffle (engine.cpp:19-23)
+  deepspark::Rng rng(deepspark::mix_seed(e->seed, e->epoch));
+  rng.shuffle(e->order);
+  e->pos = 0;
+}
+
+uint32_t sweeper_next(ds_engine* e, uint32_t* dst) {  // ShardSweeper::next (engine.cpp:25-33)
+  if (e->pos >= e->order.size()) {
+    ++e->epoch;
+    reshuffle(e);
+  }
+  const uint64_t take = std::min<uint64_t>(e->hp.batch_size, e->order.size() - e->pos);
+  std::memcpy(dst, e->order.data() + e->pos, take * sizeof(uint32_t));
+  e->pos += take;
+  return static_cast<uint32_t>(take);
+}
+
+int ensure_plan(ds_engine* e, uint64_t steps) {
+  if (steps <= e->plan_cap) return DS_OK;
+  uint64_t cap = std::max<uint64_t>(steps, 2 * e->plan_cap);
+  if (e->plan_ev_armed) cudaEventSynchronize(e->plan_ev);
+  DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  cudaFree(e->plan);
+  cudaFree(e->plan_rows);
+  cudaFreeHost(e->h_plan);
+  cudaFreeHost(e->h_rows);
+  e->plan = nullptr;
+  e->plan_rows = nullptr;
+  e->h_plan = nullptr;
+  e->h_rows = nullptr;
+  const uint64_t B = e->hp.batch_size;
+  DS_CUDA_TRY(cudaMalloc(&e->plan, cap * B * sizeof(uint32_t)));
+  DS_CUDA_TRY(cudaMalloc(&e->plan_rows, cap * sizeof(uint32_t)));
+  DS_CUDA_TRY(cudaMallocHost(&e->h_plan, cap * B * sizeof(uint32_t)));
+  DS_CUDA_TRY(cudaMallocHost(&e->h_rows, cap * sizeof(uint32_t)));
+  e->plan_cap = cap;
+  e->plan_ev_armed = false;
+  return DS_OK;
+}
+
+int ensure_log(ds_engine* e, uint64_t rows) {
+  if (rows <= e->log.cap) return DS_OK;
+  uint64_t cap = std::max<uint64_t>(rows, 2 * e->log.cap);
+  cap = std::max<uint64_t>(cap, 1024);
+  DevLog n{};
+  DS_CUDA_TRY(cudaMalloc(&n.loss, cap * sizeof(double)));
+  DS_CUDA_TRY(cudaMalloc(&n.cum, cap * sizeof(double)));
+  DS_CUDA_TRY(cudaMalloc(&n.exchanged, cap));
+  DS_CUDA_TRY(cudaMalloc(&n.period, cap * sizeof(uint32_t)));
+  n.cap = cap;
+  if (e->log.cap) {
+    const uint64_t c = e->log.cap;
+    DS_CUDA_TRY(cudaMemcpyAsync(n.loss, e->log.loss, c * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+    DS_CUDA_TRY(cudaMemcpyAsync(n.cum, e->log.cum, c * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+    DS_CUDA_TRY(cudaMemcpyAsync(n.exchanged, e->log.exchanged, c, cudaMemcpyDeviceToDevice, e->stream));
+    DS_CUDA_TRY(cudaMemcpyAsync(n.period, e->log.period, c * sizeof(uint32_t), cudaMemcpyDeviceToDevice, e->stream));
+    DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    cudaFree(e->log.loss);
+    cudaFree(e->log.cum);
+    cudaFree(e->log.exchanged);
+    cudaFree(e->log.period);
+  }
+  e->log = n;
+  return DS_OK;
+}
+
+// Upload the sweep plan for `steps` iterations; returns per-step row counts on host.
+int upload_plan(ds_engine* e, uint64_t steps) {
+  DS_TRY(ensure_plan(e, steps));
+  if (e->plan_ev_armed) DS_CUDA_TRY(cudaEventSynchronize(e->plan_ev));  // staging buffer free again
+  const uint64_t B = e->hp.batch_size;
+  for (uint64_t j = 0; j < steps; ++j) e->h_rows[j] = sweeper_next(e, e->h_plan + j * B);
+  DS_CUDA_TRY(cudaMemcpyAsync(e->plan, e->h_plan, steps * B * sizeof(uint32_t), cudaMemcpyHostToDevice, e->stream));
+  DS_CUDA_TRY(cudaMemcpyAsync(e->plan_rows, e->h_rows, steps * sizeof(uint32_t), cudaMemcpyHostToDevice, e->stream));
+  DS_CUDA_TRY(cudaEventRecord(e->plan_ev, e->stream));
+  e->plan_ev_armed = true;
+  return DS_OK;
+}
+
+// Next exchange ticket of this worker, or kNoTicket.
+uint64_t next_ticket(ds_engine* e) {
+  if (e->tickets.empty()) return kNoTicket;
+  return e->host_exchanges < e->tickets.size() ? e->tickets[e->host_exchanges] : kNoTicket;
+}
+
+bool in_kernel_ok(const ds_engine* e) {
+  // the fused kernel may exchange itself when no host-side ordering is needed
+  const ds_master* m = e->master;
+  return m && (m->sharded || (m->mode == DS_MODE_LOCKFREE && e->tickets.empty()));
+}
+
+int enqueue_exchange(ds_engine* e, float* p) {
+  const uint64_t tk = next_ticket(e);
+  if (!e->tickets.empty() && tk == kNoTicket)
+    return set_error(DS_E_STATE, "engine: ran out of deterministic exchange tickets");
+  DS_TRY(master_enqueue_exchange(e->master, p, p, tk, &e->st->fire, &e->st->err, e->stream));
+  e->launches += (e->master->sharded && e->master->mode == DS_MODE_LOCKED && tk == kNoTicket) ? 2 : 1;
+  return DS_OK;
+}
+
+// Layered iterations; with_master = perform fired exchanges against e->master.
+int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
+  DS_TRY(upload_plan(e, steps));
+  const uint64_t B = e->hp.batch_size;
+  const float eta = static_cast<float>(e->hp.eta);
+  const float wd = static_cast<float>(e->hp.weight_decay);
+  float* p = e->params[e->cur];
+  const bool xm = with_master && e->master;
+  for (uint64_t j = 0; j < steps; ++j) {
+    const uint32_t R = e->h_rows[j];
+    DS_TRY(launch_loss_and_grad(e->model, p, e->X, e->plan + j * B, e->y, R, e->grad, &e->st->loss, e->ws,
+                                &e->st->flags, &e->st->err, e->stream));
+    e->launches += 3 * e->model.layers.size() + 1;
+    DS_TRY(launch_sgd(p, p, e->grad, e->model.P, eta, wd, &e->st->flags, e->stream, &e->st->err));
+    policy_kernel<<<1, 1, 0, e->stream>>>(e->st, e->log);
+    e->launches += 2;
+    if (e->hp.adaptive) {
+      if (xm) DS_TRY(enqueue_exchange(e, p));  // conditional on the device fire flag
+    } else if (++e->host_since == e->hp.tau) {
+      e->host_since = 0;
+      if (xm) DS_TRY(enqueue_exchange(e, p));
+      ++e->host_exchanges;
+    }
+  }
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
+  DS_TRY(upload_plan(e, steps));
+  FusedArgs a{};
+  a.F = e->model.n_features;
+  a.H = e->model.hidden.empty() ? 0 : e->model.hidden[0];
+  a.C = e->model.n_classes;
+  a.P = e->model.P;
+  a.X = e->X;
+  a.y = e->y;
+  a.plan = e->plan;
+  a.plan_rows = e->plan_rows;
+  a.B = e->hp.batch_size;
+  a.steps = steps;
+  a.params[0] = e->params[0];
+  a.params[1] = e->params[1];
+  a.cur = e->cur;
+  a.act = e->act;
+  a.eta = static_cast<float>(e->hp.eta);
+  a.wd = static_cast<float>(e->hp.weight_decay);
+  a.alpha = e->master ? e->master->alpha : static_cast<float>(e->hp.alpha);
+  a.st = e->st;
+  a.log = e->log;
+  a.bar = e->bar;
+  a.has_master = (e->master && in_kernel_exchange) ? 1 : 0;
+  if (a.has_master) {
+    a.table = e->master->table;
+    a.lockfree = e->master->mode == DS_MODE_LOCKFREE && e->tickets.empty();
+    a.tickets = e->tickets.empty() ? nullptr : e->d_tickets + e->host_exchanges;
+    a.ticket_src = (!a.lockfree && !a.tickets) ? &e->master->table.flags[0]->next_ticket : nullptr;
+  }
+  DS_TRY(launch_fused(a, e->fused_grid, e->stream));
+  e->launches += 1;
+  e->cur ^= static_cast<int>(steps & 1);
+  return DS_OK;
+}
+
+}  // namespace
+}  // namespace dsb
+
+using dsb::set_error;
+
+extern "C" int ds_engine_create(ds_engine** out, int device, const ds_model_desc* model, const float* X_host,
+                                const uint32_t* y_host, uint64_t shard_n, uint32_t shard_classes, const ds_hyper* hp,
+                                uint64_t sweep_seed, const float* init_host, int kind) {
+  if (!out || !hp || !X_host || !y_host || !init_host) return set_error(DS_E_CONTRACT, "engine: null argument");
+  dsb::ModelInfo m;
+  DS_TRY(dsb::model_from_desc(model, m));
+  // Hyperparams::validate (hyperparams.cpp:7-18)
+  if (!(hp->eta > 0.0)) return set_error(DS_E_CONTRACT, "hyperparams: eta must be positive");
+  if (!(hp->alpha > 0.0 && hp->alpha < 1.0)) return set_error(DS_E_CONTRACT, "hyperparams: alpha must lie in (0,1)");
+  if (hp->batch_size == 0) return set_error(DS_E_CONTRACT, "hyperparams: batch_size must be positive");
+  if (hp->i_max == 0) return set_error(DS_E_CONTRACT, "hyperparams: i_max must be positive");
+  if (hp->weight_decay < 0.0) return set_error(DS_E_CONTRACT, "hyperparams: weight_decay must be nonnegative");
+  if (!hp->adaptive && hp->tau == 0) return set_error(DS_E_CONTRACT, "hyperparams: tau must be positive in Fixed mode");
+  if (hp->adaptive && !(hp->loss_cut > 0.0))
+    return set_error(DS_E_CONTRACT, "hyperparams: loss_cut must be positive in Adaptive mode");
+  if (shard_n == 0) return set_error(DS_E_CONTRACT, "dataset: no samples");
+  if (shard_n > 0xFFFFFFFFull) return set_error(DS_E_CONTRACT, "engine: shard too large for u32 row indices");
+  if (shard_classes == 0) return set_error(DS_E_CONTRACT, "dataset: n_classes must be positive");
+  if (shard_classes > m.n_classes) return set_error(DS_E_CONTRACT, "engine: shard dims do not match model");
+  for (uint64_t i = 0; i < shard_n; ++i)
+    if (y_host[i] >= shard_classes) return set_error(DS_E_CONTRACT, "dataset: label out of range");
+  for (uint64_t i = 0; i < m.P; ++i)
+    if (!std::isfinite(init_host[i])) {
+      // sgd_step's require_finite(x) would reject the first step (param_vector.cpp:29)
+      break;
+    }
+  if (hp->batch_size > 65535) return set_error(DS_E_CONTRACT, "engine: batch_size above 65535");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return set_error(DS_E_CUDA, "engine: no CUDA device");
+  if (device < 0 || device >= ndev) return set_error(DS_E_CONTRACT, "engine: bad device %d", device);
+  dsb::DeviceScope ds(device);
+  auto* e = new ds_engine();
+  e->device = device;
+  e->model = m;
+  e->hp = *hp;
+  e->shard_n = shard_n;
+  e->shard_classes = shard_classes;
+  e->seed = sweep_seed;
+  e->kind = kind;
+  auto fail = [&](int rc) {
+    ds_engine_destroy(e);
+    return rc;
+  };
+  const uint64_t F = m.n_features, B = hp->batch_size;
+  cudaError_t err = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
+  if (err == cudaSuccess) err = cudaMalloc(&e->X, shard_n * F * sizeof(float));
+  if (err == cudaSuccess) err = cudaMalloc(&e->y, shard_n * sizeof(uint32_t));
+  if (err == cudaSuccess) err = cudaMalloc(&e->params[0], m.P * sizeof(float));
+  if (err == cudaSuccess) err = cudaMalloc(&e->params[1], m.P * sizeof(float));
+  if (err == cudaSuccess) err = cudaMalloc(&e->grad, m.P * sizeof(float));
+  if (err == cudaSuccess) err = cudaMalloc(&e->ws, dsb::layered_workspace_doubles(m, static_cast<uint32_t>(B)) * sizeof(double));
+  if (err == cudaSuccess) err = cudaMalloc(&e->st, sizeof(dsb::DevState));
+  if (err == cudaSuccess) err = cudaMalloc(&e->bar, 64 * sizeof(unsigned int));
+  if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->plan_ev, cudaEventDisableTiming);
+  if (err == cudaSuccess) err = cudaMemcpy(e->X, X_host, shard_n * F * sizeof(float), cudaMemcpyDefault);
+  if (err == cudaSuccess) err = cudaMemcpy(e->y, y_host, shard_n * sizeof(uint32_t), cudaMemcpyDefault);
+  if (err == cudaSuccess) err = cudaMemcpy(e->params[0], init_host, m.P * sizeof(float), cudaMemcpyDefault);
+  if (err == cudaSuccess) err = cudaMemcpy(e->params[1], init_host, m.P * sizeof(float), cudaMemcpyDefault);
+  if (err == cudaSuccess) err = cudaMemset(e->bar, 0, 64 * sizeof(unsigned int));
+  if (err != cudaSuccess)
+    return fail(set_error(err == cudaErrorMemoryAllocation ? DS_E_NOMEM : DS_E_CUDA, "engine: %s", cudaGetErrorString(err)));
+  dsb::DevState s0{};
+  s0.cut = hp->loss_cut;
+  s0.tau = hp->tau;
+  s0.adaptive = hp->adaptive ? 1 : 0;
+  err = cudaMemcpy(e->st, &s0, sizeof(s0), cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) return fail(set_error(DS_E_CUDA, "engine: %s", cudaGetErrorString(err)));
+  // ShardSweeper ctor: identity order, reshuffled for epoch 0 (engine.cpp:10-17)
+  e->order.resize(shard_n);
+  std::iota(e->order.begin(), e->order.end(), 0u);
+  dsb::reshuffle(e);
+  int rc = dsb::ensure_log(e, hp->i_max);
+  if (rc != DS_OK) return fail(rc);
+  const char* why = nullptr;
+  const bool can_fuse = dsb::fused_supported(m, static_cast<uint32_t>(B), device, &why) == DS_OK;
+  if (kind == DS_ENGINE_FUSED && !can_fuse) return fail(set_error(DS_E_CONTRACT, "engine: fused path unavailable: %s", why));
+  e->fused = (kind == DS_ENGINE_FUSED) || (kind == DS_ENGINE_AUTO && can_fuse);
+  if (e->fused) {
+    e->fused_grid = dsb::fused_grid(m, device);
+    const uint64_t H = m.hidden.empty() ? 0 : m.hidden[0];
+    err = cudaMalloc(&e->act, 2 * B * (H ? H : 1) * sizeof(double));
+    if (err != cudaSuccess) return fail(set_error(DS_E_NOMEM, "engine: %s", cudaGetErrorString(err)));
+  }
+  *out = e;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_destroy(ds_engine* e) {
+  if (!e) return DS_OK;
+  dsb::DeviceScope ds(e->device);
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  cudaFree(e->X);
+  cudaFree(e->y);
+  cudaFree(e->params[0]);
+  cudaFree(e->params[1]);
+  cudaFree(e->grad);
+  cudaFree(e->ws);
+  cudaFree(e->act);
+  cudaFree(e->st);
+  cudaFree(e->bar);
+  cudaFree(e->plan);
+  cudaFree(e->plan_rows);
+  cudaFree(e->d_tickets);
+  if (e->h_plan) cudaFreeHost(e->h_plan);
+  if (e->h_rows) cudaFreeHost(e->h_rows);
+  cudaFree(e->log.loss);
+  cudaFree(e->log.cum);
+  cudaFree(e->log.exchanged);
+  cudaFree(e->log.period);
+  if (e->plan_ev) cudaEventDestroy(e->plan_ev);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_attach_master(ds_engine* e, ds_master* m) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine: null");
+  if (m) {
+    uint64_t dim = 0;
+    ds_master_dim(m, &dim);
+    if (dim != e->model.P) return set_error(DS_E_CONTRACT, "engine: master dim %llu != model dim %llu",
+                                            (unsigned long long)dim, (unsigned long long)e->model.P);
+    if (m->device != e->device) return set_error(DS_E_CONTRACT, "engine: master lives on another device");
+  }
+  e->master = m;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_set_tickets(ds_engine* e, const uint64_t* tickets, uint64_t count) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine: null");
+  if (count && e->hp.adaptive)
+    return set_error(DS_E_CONTRACT, "engine: deterministic tickets need a Fixed period (adaptive order is value-dependent)");
+  dsb::DeviceScope ds(e->device);
+  DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  cudaFree(e->d_tickets);
+  e->d_tickets = nullptr;
+  e->tickets.assign(tickets, tickets + count);
+  if (count) {
+    DS_CUDA_TRY(cudaMalloc(&e->d_tickets, count * sizeof(uint64_t)));
+    DS_CUDA_TRY(cudaMemcpy(e->d_tickets, tickets, count * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  }
+  e->host_exchanges = 0;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_run(ds_engine* e, uint64_t steps, int stop_at_exchange, uint64_t* ran_out) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine: null");
+  dsb::DeviceScope ds(e->device);
+  uint64_t done = 0;
+  DS_TRY(dsb::ensure_log(e, e->queued + steps));
+  const bool ik = dsb::in_kernel_ok(e);
+  if (e->hp.adaptive) {
+    if (stop_at_exchange) {
+      // value-dependent: one iteration at a time, stop once the device policy fired
+      while (done < steps) {
+        DS_TRY(e->fused ? dsb::run_fused(e, 1, false) : dsb::run_layered(e, 1, false));
+        ++done;
+        ++e->queued;
+        uint32_t fire = 0;
+        DS_CUDA_TRY(cudaMemcpyAsync(&fire, &e->st->fire, sizeof(fire), cudaMemcpyDeviceToHost, e->stream));
+        DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+        if (fire) break;
+      }
+    } else if (e->fused && e->master && !ik) {
+      for (; done < steps; ++done, ++e->queued) {  // host-ordered master: exchange between launches
+        DS_TRY(dsb::run_fused(e, 1, false));
+        DS_TRY(dsb::enqueue_exchange(e, e->params[e->cur]));
+      }
+    } else {
+      DS_TRY(e->fused ? dsb::run_fused(e, steps, e->master != nullptr) : dsb::run_layered(e, steps, true));
+      done = steps;
+      e->queued += steps;
+    }
+  } else if (!stop_at_exchange && (!e->fused || !e->master || ik)) {
+    if (e->fused) {
+      DS_TRY(dsb::run_fused(e, steps, e->master != nullptr));
+      const uint64_t total = e->host_since + steps;
+      e->host_exchanges += total / e->hp.tau;
+      e->host_since = static_cast<uint32_t>(total % e->hp.tau);
+    } else {
+      DS_TRY(dsb::run_layered(e, steps, true));
+    }
+    done = steps;
+    e->queued += steps;
+  } else {
+    // fixed period, split at the exchange points the host can predict
+    while (done < steps) {
+      const uint64_t to_fire = e->hp.tau - e->host_since;
+      const uint64_t chunk = std::min<uint64_t>(to_fire, steps - done);
+      const bool fires = chunk == to_fire;
+      if (e->fused) {
+        DS_TRY(dsb::run_fused(e, chunk, false));
+        e->host_since = fires ? 0 : e->host_since + static_cast<uint32_t>(chunk);
+        if (fires) {
+          if (!stop_at_exchange && e->master) DS_TRY(dsb::enqueue_exchange(e, e->params[e->cur]));
+          ++e->host_exchanges;
+        }
+      } else {
+        DS_TRY(dsb::run_layered(e, chunk, !stop_at_exchange));
+      }
+      done += chunk;
+      e->queued += chunk;
+      if (fires && stop_at_exchange) break;
+    }
+  }
+  if (ran_out) *ran_out = done;
+  return DS_OK;
+}
+
+namespace {
+int engine_error(ds_engine* e) {
+  dsb::DevState s;
+  DS_CUDA_TRY(cudaMemcpy(&s, e->st, sizeof(s), cudaMemcpyDeviceToHost));
+  if (!s.err) return DS_OK;
+  const unsigned long long it = s.bad_iter;
+  const uint32_t f = s.err;
+  // the reference's check order: check_inputs, loss/grad finiteness, then sgd_step
+  if (f & DS_FLAG_LABEL_RANGE) return set_error(DS_E_CONTRACT, "loss_and_grad: label out of range (iteration %llu)", it);
+  if (f & DS_FLAG_LOSS_NONFINITE) return set_error(DS_E_NUMERIC, "loss_and_grad: non-finite loss (iteration %llu)", it);
+  if (f & DS_FLAG_GRAD_NONFINITE) return set_error(DS_E_NUMERIC, "loss_and_grad: non-finite gradient (iteration %llu)", it);
+  if (f & DS_FLAG_X_NONFINITE) return set_error(DS_E_CONTRACT, "sgd_step: x contains a non-finite value (iteration %llu)", it);
+  if (f & DS_FLAG_G_NONFINITE) return set_error(DS_E_CONTRACT, "sgd_step: grad contains a non-finite value (iteration %llu)", it);
+  if (f & DS_FLAG_OUT_NONFINITE) return set_error(DS_E_NUMERIC, "sgd_step: non-finite result (iteration %llu)", it);
+  return set_error(DS_E_NUMERIC, "engine: failure flags 0x%x (iteration %llu)", f, it);
+}
+}  // namespace
+
+extern "C" int ds_engine_sync(ds_engine* e) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine: null");
+  dsb::DeviceScope ds(e->device);
+  DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return engine_error(e);
+}
+
+extern "C" int ds_engine_stream(ds_engine* e, void** stream) {
+  if (!e || !stream) return set_error(DS_E_CONTRACT, "engine: null");
+  *stream = e->stream;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_log(ds_engine* e, uint64_t first, uint64_t count, double* batch_loss, double* cumulated,
+                             uint8_t* exchanged, uint32_t* period_len) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine: null");
+  dsb::DeviceScope ds(e->device);
+  DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  if (first + count > e->log.cap) return set_error(DS_E_CONTRACT, "engine_log: rows beyond the log");
+  if (batch_loss) DS_CUDA_TRY(cudaMemcpy(batch_loss, e->log.loss + first, count * sizeof(double), cudaMemcpyDeviceToHost));
+  if (cumulated) DS_CUDA_TRY(cudaMemcpy(cumulated, e->log.cum + first, count * sizeof(double), cudaMemcpyDeviceToHost));
+  if (exchanged) DS_CUDA_TRY(cudaMemcpy(exchanged, e->log.exchanged + first, count, cudaMemcpyDeviceToHost));
+  if (period_len) DS_CUDA_TRY(cudaMemcpy(period_len, e->log.period + first, count * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return DS_OK;
+}
+
+extern "C" int ds_engine_iterations(ds_engine* e, uint64_t* iters) {
+  if (!e || !iters) return set_error(DS_E_CONTRACT, "engine: null");
+  dsb::DeviceScope ds(e->device);
+  DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  dsb::DevState s;
+  DS_CUDA_TRY(cudaMemcpy(&s, e->st, sizeof(s), cudaMemcpyDeviceToHost));
+  *iters = s.iter;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_get_params(ds_engine* e, float* host_out) {
+  if (!e || !host_out) return set_error(DS_E_CONTRACT, "engine: null");
+  dsb::DeviceScope ds(e->device);
+  DS_CUDA_TRY(cudaMemcpyAsync(host_out, e->params[e->cur], e->model.P * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+  DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return DS_OK;
+}
+
+extern "C" int ds_engine_set_params(ds_engine* e, const float* host_in) {
+  if (!e || !host_in) return set_error(DS_E_CONTRACT, "engine: null");
+  dsb::DeviceScope ds(e->device);
+  DS_CUDA_TRY(cudaMemcpyAsync(e->params[e->cur], host_in, e->model.P * sizeof(float), cudaMemcpyDefault, e->stream));
+  DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return DS_OK;
+}
+
+extern "C" int ds_engine_params_device(ds_engine* e, float** dev_ptr) {
+  if (!e || !dev_ptr) return set_error(DS_E_CONTRACT, "engine: null");
+  *dev_ptr = e->params[e->cur];
+  return DS_OK;
+}
+
+extern "C" int ds_engine_policy(ds_engine* e, double* cumulated, uint32_t* since_exchange, double* loss_cut) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine: null");
+  dsb::DeviceScope ds(e->device);
+  DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  dsb::DevState s;
+  DS_CUDA_TRY(cudaMemcpy(&s, e->st, sizeof(s), cudaMemcpyDeviceToHost));
+  if (cumulated) *cumulated = s.cum;
+  if (since_exchange) *since_exchange = s.since;
+  if (loss_cut) *loss_cut = s.cut;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_launches(ds_engine* e, uint64_t* launches) {
+  if (!e || !launches) return set_error(DS_E_CONTRACT, "engine: null");
+  *launches = e->launches;
+  return DS_OK;
+}

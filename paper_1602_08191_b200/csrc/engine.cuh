@@ -1,0 +1,72 @@
+// engine.cuh — device-resident SgdEngine / run_training_loop state (engine.hpp:17-105).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "ds_cuda.h"
+#include "master.cuh"
+#include "model.cuh"
+
+namespace dsb {
+
+// ExchangePolicy + loop bookkeeping, resident on the device (engine.hpp:40-59).
+struct DevState {
+  double cum;              // cumulated loss L since the last exchange
+  double cut;              // resolved loss_cut (Adaptive)
+  double loss;             // batch loss of the step in flight
+  unsigned long long iter; // completed iterations (TrainRecord.iter of the last row)
+  unsigned long long bad_iter;  // first failing iteration (1-based); 0 = none
+  unsigned long long exchanges; // exchanges this worker performed
+  uint32_t since;          // iterations since the last exchange
+  uint32_t fire;           // the policy fired on the step in flight
+  uint32_t flags;          // DS_FLAG_* raised by the step in flight
+  uint32_t err;            // sticky copy of the first failing step's flags (gate)
+  uint32_t tau;
+  int32_t adaptive;
+  uint32_t period;
+  uint32_t pad;
+};
+
+struct DevLog {
+  double* loss;
+  double* cum;
+  uint8_t* exchanged;
+  uint32_t* period;
+  unsigned long long cap;
+};
+
+// Arguments of the fused persistent step kernel (mlp_fused.cu).
+struct FusedArgs {
+  // model: n_hidden == 0 (softmax) or 1 (one tanh layer)
+  uint32_t F, H, C;     // features, hidden width (0 = softmax regression), classes
+  uint64_t P;
+  const float* X;       // shard, row-major [shard_n x F]
+  const uint32_t* y;
+  const uint32_t* plan; // steps x B shard-local row indices
+  const uint32_t* plan_rows;  // rows per step
+  uint32_t B;           // batch stride of the plan
+  uint64_t steps;
+  float* params[2];     // ping-pong parameter buffers; step s reads [cur], writes [cur^1]
+  int cur;
+  double* act;          // [2][B x H] hidden activations (ping-pong), f64
+  float eta, wd, alpha;
+  DevState* st;
+  DevLog log;
+  // exchange
+  int has_master;
+  ShardTable table;
+  int lockfree;               // plain stores, no tickets
+  const uint64_t* tickets;    // per-exchange global tickets (deterministic), or null
+  unsigned long long* ticket_src;  // Locked: dispenser (shard 0 flags.next_ticket)
+  int stop_at_exchange;
+  unsigned int* bar;          // grid barrier words [2]
+};
+
+int fused_supported(const ModelInfo& m, uint32_t batch, int device, const char** why);
+int launch_fused(const FusedArgs& a, int grid, cudaStream_t s);
+int fused_grid(const ModelInfo& m, int device);
+size_t fused_smem_bytes(const ModelInfo& m, uint32_t batch);
+
+}  // namespace dsb

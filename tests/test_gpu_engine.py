@@ -1,0 +1,183 @@
+"""GPU parity of the device-resident SgdEngine / run_training_loop (C-ABI) against the
+CPU oracle's restatement of engine.cpp:50-113, with and without a device master.
+
+Bar: per-iteration batch losses equal to 1e-13 relative, final parameters and master
+within 1 ulp per element (the only non-bit-identical operations are CUDA's double
+tanh/exp/log); in practice the trajectories come out bit-identical and the test reports
+the fraction.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle, ModelSpec, Hyper
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_1602_08191_b200 import _lib
+    return _lib
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle("dso")
+
+
+def ulps(a, b):
+    a = np.asarray(a, np.float32).view(np.int32).astype(np.int64)
+    b = np.asarray(b, np.float32).view(np.int32).astype(np.int64)
+    ka = np.where(a < 0, np.int64(-2**31) - a, a)
+    kb = np.where(b < 0, np.int64(-2**31) - b, b)
+    return np.abs(ka - kb)
+
+
+def desc_of(L, m):
+    h = (C.c_uint32 * max(1, len(m.hidden)))(*m.hidden)
+    d = L.ds_model_desc(0 if m.kind == "softmax" else 1, m.n_features, m.n_classes, len(m.hidden), h)
+    d._keep = h
+    return d
+
+
+def make_engine(L, m, X, y, ncls, hp: Hyper, seed, init, kind):
+    d = desc_of(L, m)
+    h = L.ds_hyper(hp.eta, hp.alpha, hp.tau, hp.batch_size, hp.i_max, hp.loss_cut, hp.weight_decay,
+                   1 if hp.adaptive else 0)
+    X = np.ascontiguousarray(X, np.float32)
+    y = np.ascontiguousarray(y, np.uint32)
+    init = np.ascontiguousarray(init, np.float32)
+    e = C.c_void_p()
+    L.check(L.lib.ds_engine_create(C.byref(e), 0, C.byref(d), X.ctypes.data, y.ctypes.data, len(y), ncls,
+                                   C.byref(h), seed, init.ctypes.data, kind))
+    return e
+
+
+def engine_log(L, e, n):
+    loss = np.zeros(n)
+    cum = np.zeros(n)
+    ex = np.zeros(n, np.uint8)
+    per = np.zeros(n, np.uint32)
+    L.check(L.lib.ds_engine_log(e, 0, n, loss.ctypes.data, cum.ctypes.data, ex.ctypes.data, per.ctypes.data))
+    return loss, cum, ex, per
+
+
+def engine_params(L, e, P):
+    out = np.zeros(P, np.float32)
+    L.check(L.lib.ds_engine_get_params(e, out.ctypes.data))
+    return out
+
+
+CASES = [
+    ("softmax20x2", ModelSpec.softmax(20, 2), 300, 16, Hyper(eta=0.05, tau=5, batch_size=16, i_max=40)),
+    ("mlp20-16-3", ModelSpec.mlp(20, [16], 3), 300, 16, Hyper(eta=0.05, tau=5, batch_size=16, i_max=40)),
+    ("mlp-wd", ModelSpec.mlp(20, [16], 3), 300, 16, Hyper(eta=0.05, tau=7, batch_size=16, i_max=40, weight_decay=0.01)),
+    ("mlp2layers", ModelSpec.mlp(12, [8, 6], 4), 200, 10, Hyper(eta=0.1, tau=3, batch_size=10, i_max=30)),
+    ("mlp784", ModelSpec.mlp(784, [256], 10), 600, 32, Hyper(eta=0.05, tau=10, batch_size=32, i_max=60)),
+    ("short-batch", ModelSpec.mlp(20, [33], 3), 70, 32, Hyper(eta=0.05, tau=4, batch_size=32, i_max=12)),
+]
+
+
+@pytest.mark.parametrize("kind", [1, 2])  # layered, fused
+@pytest.mark.parametrize("name,m,n,b,hp", CASES, ids=[c[0] for c in CASES])
+@pytest.mark.parametrize("with_master", [False, True])
+def test_engine_matches_oracle(L, orc, kind, name, m, n, b, hp, with_master):
+    if kind == 2 and len(m.hidden) > 1:
+        pytest.skip("fused path covers <= 1 hidden layer")
+    X, y = orc.gen_synthetic(n, m.n_features, m.n_classes, 2.0, 1.5, 3)
+    init = orc.init_params(m, 9)
+    P = len(init)
+    master0 = orc.init_params(m, 10)
+    ref = orc.run_training_loop(m, X, y, m.n_classes, hp, 31, init, 2 if with_master else 0, master0)
+    e = make_engine(L, m, X, y, m.n_classes, hp, 31, init, kind)
+    mh = None
+    try:
+        if with_master:
+            mh = C.c_void_p()
+            L.check(L.lib.ds_master_create(C.byref(mh), 0, P, C.c_float(np.float32(hp.alpha)), L.DS_MODE_LOCKED,
+                                           master0.ctypes.data))
+            L.check(L.lib.ds_engine_attach_master(e, mh))
+        L.check(L.lib.ds_engine_run(e, hp.i_max, 0, None))
+        L.check(L.lib.ds_engine_sync(e))
+        loss, cum, ex, per = engine_log(L, e, hp.i_max)
+        params = engine_params(L, e, P)
+        np.testing.assert_allclose(loss, ref["batch_loss"], rtol=1e-13, atol=0)
+        assert np.array_equal(ex, ref["exchanged"])
+        assert np.array_equal(per, ref["period_len"])
+        d = ulps(params, ref["final_params"])
+        assert d.max() <= 1, f"params max ulp {d.max()}"
+        if with_master:
+            snap = np.zeros(P, np.float32)
+            L.check(L.lib.ds_master_snapshot(mh, snap.ctypes.data))
+            dm = ulps(snap, ref["master"])
+            assert dm.max() <= 1, f"master max ulp {dm.max()}"
+            cnt = C.c_uint64()
+            L.check(L.lib.ds_master_exchange_count(mh, C.byref(cnt)))
+            assert cnt.value == int(ref["exchanged"].sum())
+        print(f"{name} kind={kind} master={with_master}: params bit-identical {np.mean(d == 0):.6f}")
+    finally:
+        L.lib.ds_engine_destroy(e)
+        if mh:
+            L.lib.ds_master_destroy(mh)
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_engine_adaptive_stop_at_exchange(L, orc, kind):
+    """Adaptive policy with the host ExchangeFn path: run stops where the policy fires."""
+    m = ModelSpec.mlp(20, [16], 3)
+    X, y = orc.gen_synthetic(300, 20, 3, 2.0, 1.5, 3)
+    init = orc.init_params(m, 9)
+    hp = Hyper(eta=0.05, batch_size=16, i_max=40, adaptive=True)
+    cut = orc.resolve_loss_cut(m, X, y, 3, hp, 31, init)
+    hp.loss_cut = cut / 10.0  # fire every few iterations
+    ref = orc.run_training_loop(m, X, y, 3, hp, 31, init, 1, None)  # identity ExchangeFn
+    e = make_engine(L, m, X, y, 3, hp, 31, init, kind)
+    try:
+        done_total = 0
+        fires = []
+        while done_total < hp.i_max:
+            ran = C.c_uint64()
+            L.check(L.lib.ds_engine_run(e, hp.i_max - done_total, 1, C.byref(ran)))
+            done_total += ran.value
+            fires.append(done_total)
+        L.check(L.lib.ds_engine_sync(e))
+        loss, cum, ex, per = engine_log(L, e, hp.i_max)
+        np.testing.assert_allclose(loss, ref["batch_loss"], rtol=1e-13)
+        np.testing.assert_allclose(cum, ref["cumulated"], rtol=1e-12)
+        assert np.array_equal(ex, ref["exchanged"])
+        assert np.array_equal(per, ref["period_len"])
+        exp_fires = [i + 1 for i in np.nonzero(ref["exchanged"])[0]]
+        assert fires[:len(exp_fires)] == exp_fires
+    finally:
+        L.lib.ds_engine_destroy(e)
+
+
+def test_engine_contract_errors(L, orc):
+    m = ModelSpec.softmax(2, 2)
+    X = np.zeros((8, 2), np.float32)
+    y = np.zeros(8, np.uint32)
+    init = np.zeros(6, np.float32)
+    for hp in (Hyper(eta=0.0), Hyper(alpha=1.0), Hyper(tau=0), Hyper(batch_size=0), Hyper(i_max=0),
+               Hyper(weight_decay=-0.1), Hyper(adaptive=True, loss_cut=-1.0)):
+        with pytest.raises(L.ContractError):
+            make_engine(L, m, X, y, 2, hp, 1, init, 0)
+    with pytest.raises(L.ContractError):  # shard has more classes than the model
+        make_engine(L, m, X, y, 3, Hyper(), 1, init, 0)
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_engine_numeric_error(L, orc, kind):
+    """A diverging run reports NumericError/ContractError naming the iteration."""
+    m = ModelSpec.softmax(4, 2)
+    X = np.full((16, 4), 1e30, np.float32)
+    y = (np.arange(16) % 2).astype(np.uint32)
+    init = np.ones(10, np.float32)
+    e = make_engine(L, m, X, y, 2, Hyper(eta=1e30, batch_size=4, i_max=10, tau=100), 1, init, kind)
+    try:
+        L.check(L.lib.ds_engine_run(e, 10, 0, None))
+        with pytest.raises((L.NumericError, L.ContractError)):
+            L.check(L.lib.ds_engine_sync(e))
+    finally:
+        L.lib.ds_engine_destroy(e)
