@@ -1,0 +1,412 @@
+#!/usr/bin/env python3
+"""bench.py — throughput of the B200 EASGD hot path (BASELINE.json metric).
+
+Workload (config 1 shapes, one worker per GPU): MLP 784-256-10 (tanh), batch 32 per
+worker, async EASGD with tau=10, alpha=0.1, eta=0.05, on synthetic MNIST-shaped data
+made by the reference's own generator (gen_synthetic N=60000, sep 0.1, sigma 1.0; each
+GPU draws its own partition with seed 1+rank, the holdout split of the reference's
+simulator is removed, 48,000 rows = 150 MB stay resident per GPU, larger than L2).
+
+A "step" is one local SGD iteration on every GPU; every tau-th step also performs the
+elastic exchange with the center, which is sharded over all GPUs (LockFree, in-kernel
+P2P read-modify-write over NVLink). value = all samples processed / max-over-ranks
+device time. e2e = the same loop through the C-ABI with host buffers: every step
+copies its gathered batch from pinned host memory and reads the batch loss back.
+
+  python bench.py [--gpus N --steps K --warmup W]          # our B200 arm
+  python bench.py --impl reference [...]                   # the reference CPU arm
+  torchrun --nproc-per-node N bench.py --gpus N ...        # N > 1
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train samples/sec @1/2/4/8 B200; EASGD exchange GB/s vs HBM/NVLink peak"
+F, H, NCLS = 784, 256, 10
+N_SAMPLES, SEP, SIGMA = 60000, 0.1, 1.0
+INIT_SEED, DATA_SEED = 2, 3
+FLOP_PER_SAMPLE = 818_176  # fwd 203,264 MAC + dW 203,264 MAC + dX 2,560 MAC, x2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--tau", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=500)
+    ap.add_argument("--exchange-params", type=int, default=256 * 1024 * 1024)
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / exchange sweep / cpu baseline (profiling)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p.get("hbm_gbs", 6552.3), p.get("bf16_tflops", 1646.8), p.get("bf16_tflops_sustained", 1400.2), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def worker_data(rank, api):
+    """Rank's synthetic partition: gen_synthetic (seed 1+rank) minus the simulator's holdout."""
+    X, y = api.gen_synthetic(N_SAMPLES, F, NCLS, SEP, SIGMA, 1 + rank)
+    order, nh = api.split_holdout_order(N_SAMPLES, 0.2, api.mix_seed(DATA_SEED, 0x484f4c44))
+    tr = order[nh:]
+    return np.ascontiguousarray(X[tr]), np.ascontiguousarray(y[tr])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.rows = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = [n for i, n in enumerate(names) if any(r[3 + i].lower() == "active" for r in self.rows)]
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def run_reference(args):
+    """The reference's own CPU path: n worker threads (SgdEngine + ExchangePolicy +
+    in-process MasterState), timed on the host cores of this box."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle.oracle import Oracle, ModelSpec, Hyper, available
+    kind = "reference" if available("dsref") else "port"
+    orc = Oracle("dsref" if kind == "reference" else "dso")
+    n = max(1, args.gpus)
+    m = ModelSpec.mlp(F, [H], NCLS)
+    hp = Hyper(eta=0.05, alpha=0.1, tau=args.tau, batch_size=args.batch, i_max=10 ** 9)
+    shards = [worker_data(k, orc) for k in range(n)]
+    init = orc.init_params(m, INIT_SEED)
+    if kind == "reference":
+        probe = orc.workers_time(m, shards, NCLS, hp, init, True, 1, 5)  # calibrate: ~5 steps
+        per = max(probe / 5, 1e-4)
+        steps = int(min(args.steps, max(20, 60.0 / per)))  # bounded: <= ~1 min of CPU
+        warm = int(min(args.warmup, max(3, 5.0 / per)))
+        secs = orc.workers_time(m, shards, NCLS, hp, init, True, warm, steps)
+    else:  # C restatement, single worker only
+        t0 = time.perf_counter()
+        orc.engine_steps(m, shards[0][0], shards[0][1], NCLS, hp, 7, init, 5)
+        per = (time.perf_counter() - t0) / 5
+        steps = int(min(args.steps, max(20, 60.0 / per)))
+        warm = 0
+        t0 = time.perf_counter()
+        orc.engine_steps(m, shards[0][0], shards[0][1], NCLS, hp, 7, init, steps)
+        secs = time.perf_counter() - t0
+        n = 1
+    value = n * args.batch * steps / secs
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": steps,
+            "warmup": warm, "ms_per_step": 1000.0 * secs / steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference gen_synthetic, per-worker seeds)",
+            "impl": "reference",
+            "config": config_block(args, n),
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": n, "kind": kind,
+                             "sample": f"{steps} timed iterations per worker x {n} worker thread(s) "
+                                       f"(+{warm} warmup), LockFree in-process MasterState, tau={args.tau}"},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(args, n):
+    return {"workload": "mlp784-256-10 async EASGD (BASELINE config 1 shapes, one worker per GPU)",
+            "model": "mlp:784:256:10 (tanh hidden, softmax CE)", "global_batch": args.batch * n,
+            "batch_per_worker": args.batch, "seq_len": None, "tau": args.tau, "alpha": 0.1, "eta": 0.05,
+            "workers": n, "parallelism": f"easgd-dp{n}",
+            "exchange": "LockFree, center sharded over the GPUs, in-kernel P2P RMW" if n > 1 else
+                        "LockFree, center on the same GPU, in-kernel",
+            "l2_policy": "inputs larger than L2: 48,000-row (150 MB) shard per GPU, random batches",
+            "numerics": "f64 accumulation in the reference's summation order, f32 params"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1602_08191_b200 import _lib as L
+    from paper_1602_08191_b200.deepspark import DeepSpark
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    api = DeepSpark()
+    n = world
+    hbm, bf16, bf16_sus, peak_kind = peaks()
+
+    # ---- data, init (NCCL broadcast), master, engine --------------------------------
+    X, y = worker_data(rank, api)
+    P = (H * F + H) + (NCLS * H + NCLS)
+    init = torch.empty(P, dtype=torch.float32, device="cuda")
+    if rank == 0:
+        from paper_1602_08191_b200.deepspark import Model
+        init.copy_(torch.from_numpy(api.init_params(Model.mlp(F, [H], NCLS), INIT_SEED)))
+    if world > 1:
+        dist.broadcast(init, 0)  # replaces FETCH_INIT (exchanger.cpp:266-270)
+    torch.cuda.synchronize()
+
+    master = C.c_void_p()
+    if world == 1:
+        L.check(L.lib.ds_master_create(C.byref(master), local, P, C.c_float(0.1), L.DS_MODE_LOCKFREE,
+                                       C.c_void_p(init.data_ptr())))
+    else:
+        L.check(L.lib.ds_master_create_sharded(C.byref(master), local, P, C.c_float(0.1), L.DS_MODE_LOCKFREE,
+                                               rank, world, C.c_void_p(init.data_ptr())))
+        rec = (C.c_uint8 * L.DS_IPC_RECORD_BYTES)()
+        L.check(L.lib.ds_master_export(master, rec))
+        recs = [None] * world
+        dist.all_gather_object(recs, bytes(rec))
+        allrec = (C.c_uint8 * (L.DS_IPC_RECORD_BYTES * world)).from_buffer_copy(b"".join(recs))
+        L.check(L.lib.ds_master_attach(master, allrec))
+        dist.barrier()
+
+    hidden = (C.c_uint32 * 1)(H)
+    desc = L.ds_model_desc(1, F, NCLS, 1, hidden)
+    hp = L.ds_hyper(0.05, 0.1, args.tau, args.batch, 10 ** 9, 0.0, 0.0, 0)
+    sweep_seed = api.mix_seed(api.mix_seed(DATA_SEED, 0x53574550), rank)
+    eng = C.c_void_p()
+    L.check(L.lib.ds_engine_create(C.byref(eng), local, C.byref(desc), X.ctypes.data, y.ctypes.data, len(y), NCLS,
+                                   C.byref(hp), sweep_seed, C.c_void_p(init.data_ptr()), L.DS_ENGINE_AUTO))
+    L.check(L.lib.ds_engine_attach_master(eng, master))
+    sptr = C.c_void_p()
+    L.check(L.lib.ds_engine_stream(eng, C.byref(sptr)))
+    stream = torch.cuda.ExternalStream(sptr.value)
+
+    # ---- warmup, then K timed steps in one device run -----------------------------------
+    W, K = max(3, args.warmup), args.steps
+    L.check(L.lib.ds_engine_run(eng, W, 0, None))
+    L.check(L.lib.ds_engine_sync(eng))
+    launches0 = C.c_uint64()
+    L.check(L.lib.ds_engine_launches(eng, C.byref(launches0)))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        L.check(L.lib.ds_engine_run(eng, K, 0, None))
+        ev1.record(stream)
+        L.check(L.lib.ds_engine_sync(eng))
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches1 = C.c_uint64()
+    L.check(L.lib.ds_engine_launches(eng, C.byref(launches1)))
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    value = n * args.batch * K / (ms_max / 1e3)
+
+    # roofline of the dominant (and only) kernel of the timed region: the fused step
+    flop_launch = FLOP_PER_SAMPLE * args.batch * K
+    achieved = flop_launch / (ms / 1e3) / 1e12
+    roof = {"bound": "tensor", "achieved": achieved, "peak": bf16_sus, "unit": "TFLOP/s", "frac": achieved / bf16_sus,
+            "traffic": None, "peak_kind": f"{peak_kind} bf16 dense, sustained",
+            "kernel": "fused_kernel<true> (persistent: forward, softmax-CE, backward, SGD, policy, exchange)",
+            "algorithmic": f"{FLOP_PER_SAMPLE} FLOP/sample x {args.batch} x {K} steps per launch",
+            "note": "f64 CUDA-core chains in the reference's sequential order; latency-bound "
+                    "(784-long dependent DADD chains + 1 grid barrier per step), not a tensor-core kernel"}
+
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n, "steps": K, "warmup": W,
+            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (reference gen_synthetic, per-GPU seeds)",
+            "config": config_block(args, n), "roofline": roof, "clocks": clk.summary(),
+            "gpu_launches": int(launches1.value - launches0.value)}
+
+    if not args.no_extras:
+        line["e2e"] = e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n)
+        line["exchange"] = exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind)
+        if rank == 0 and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args, X, y)
+    L.lib.ds_engine_destroy(eng)
+    if world > 1:
+        dist.barrier()
+    L.lib.ds_master_destroy(master)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n):
+    """Same loop through the C-ABI with HOST buffers: per step, the batch rows are gathered
+    on the host (the reference's ShardSweeper order) into pinned memory, copied in, one
+    iteration runs (exchange every tau), and the batch loss is read back."""
+    import torch
+    import torch.distributed as dist
+    K = min(args.e2e_steps, args.steps)
+    B = args.batch
+    idx, sizes = api.sweep_batches(len(y), B, sweep_seed + 1, K)
+    Xp = torch.empty((B, F), dtype=torch.float32, pin_memory=True)
+    yp = torch.empty(B, dtype=torch.int32, pin_memory=True)
+    Xn, yn = Xp.numpy(), yp.numpy().view(np.uint32)
+    loss = C.c_double()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for s in range(K):
+        r = int(sizes[s])
+        np.take(X, idx[s, :r], axis=0, out=Xn[:r])
+        np.take(y, idx[s, :r], out=yn[:r])
+        L.check(L.lib.ds_engine_step_host(eng, C.c_void_p(Xp.data_ptr()), C.c_void_p(yp.data_ptr()), r,
+                                          C.byref(loss)))
+    secs = time.perf_counter() - t0
+    t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"value": n * B * K / t.item(), "unit": "samples/s", "h2d_bytes_per_step": B * F * 4 + B * 4 + 4,
+            "d2h_bytes_per_step": 8, "steps": K,
+            "path": "ds_engine_step_host: pinned-host batch H2D + fused step (+exchange) + loss D2H, per step"}
+
+
+def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind):
+    """Standalone elastic exchange (config 5 shape): fused in-place update streaming w and
+    the center once, 16 B/param; with N>1 the center is sharded and the RMW crosses NVLink."""
+    Pn = args.exchange_params
+    g = torch.Generator(device="cuda").manual_seed(11 + rank)
+    w = torch.rand(Pn, device="cuda", generator=g) * 2 - 1
+    m = torch.rand(Pn, device="cuda", generator=g) * 2 - 1
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        L.check(L.lib.ds_elastic_update(C.c_void_p(w.data_ptr()), C.c_void_p(m.data_ptr()), Pn, C.c_float(0.1),
+                                        C.c_void_p(s.cuda_stream)))
+    iters = 10
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(iters):
+        L.check(L.lib.ds_elastic_update(C.c_void_p(w.data_ptr()), C.c_void_p(m.data_ptr()), Pn, C.c_float(0.1),
+                                        C.c_void_p(s.cuda_stream)))
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    gbs = 16.0 * Pn / (ms / 1e3) / 1e9
+    out = {"params": Pn, "bytes_per_param": 16, "local_gbs": gbs, "local_frac_hbm": gbs / hbm,
+           "hbm_peak_gbs": hbm, "peak_kind": peak_kind, "ms": ms}
+    del w, m
+    if world > 1:
+        # sharded center: every rank exchanges its own worker vector concurrently (LockFree)
+        Ps = min(Pn, 64 * 1024 * 1024)
+        init = torch.zeros(Ps, device="cuda")
+        mh = C.c_void_p()
+        L.check(L.lib.ds_master_create_sharded(C.byref(mh), local, Ps, C.c_float(0.1), L.DS_MODE_LOCKFREE, rank,
+                                               world, C.c_void_p(init.data_ptr())))
+        rec = (C.c_uint8 * L.DS_IPC_RECORD_BYTES)()
+        L.check(L.lib.ds_master_export(mh, rec))
+        recs = [None] * world
+        dist.all_gather_object(recs, bytes(rec))
+        allrec = (C.c_uint8 * (L.DS_IPC_RECORD_BYTES * world)).from_buffer_copy(b"".join(recs))
+        L.check(L.lib.ds_master_attach(mh, allrec))
+        wv = torch.rand(Ps, device="cuda", generator=g)
+        for _ in range(2):
+            L.check(L.lib.ds_master_exchange(mh, C.c_void_p(wv.data_ptr()), C.c_void_p(wv.data_ptr()),
+                                             C.c_void_p(s.cuda_stream)))
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record(s)
+        for _ in range(iters):
+            L.check(L.lib.ds_master_exchange(mh, C.c_void_p(wv.data_ptr()), C.c_void_p(wv.data_ptr()),
+                                             C.c_void_p(s.cuda_stream)))
+        e1.record(s)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / iters], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sms = t.item()
+        remote = 8.0 * Ps * (world - 1) / world  # bytes each rank moves over NVLink per exchange, per direction x2
+        out.update({"sharded_params": Ps, "sharded_ms": sms, "sharded_gbs_per_gpu": 16.0 * Ps / (sms / 1e3) / 1e9,
+                    "nvlink_gbs_per_gpu": remote / (sms / 1e3) / 1e9,
+                    "nvlink_note": "(G-1)/G x 8 B/param over NVLink per exchange, all ranks concurrent"})
+        dist.barrier()
+        L.lib.ds_master_destroy(mh)
+    return out
+
+
+def cpu_baseline(args, X, y):
+    """The reference's own SgdEngine loop (oracle/_ref, unmodified) on this box's host,
+    one worker thread, a bounded sample (~15 s) of the same workload."""
+    try:
+        from oracle.oracle import Oracle, ModelSpec, Hyper, available
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unavailable": str(e)}
+    kind = "reference" if available("dsref") else "port"
+    orc = Oracle("dsref" if kind == "reference" else "dso")
+    m = ModelSpec.mlp(F, [H], NCLS)
+    hp = Hyper(eta=0.05, alpha=0.1, tau=args.tau, batch_size=args.batch, i_max=10 ** 9)
+    init = orc.init_params(m, INIT_SEED)
+    if kind == "reference":
+        probe = orc.workers_time(m, [(X, y)], NCLS, hp, init, True, 1, 5)
+        steps = int(max(20, min(2000, 15.0 / max(probe / 5, 1e-4))))
+        secs = orc.workers_time(m, [(X, y)], NCLS, hp, init, True, 3, steps)
+    else:
+        steps = 200
+        t0 = time.perf_counter()
+        orc.engine_steps(m, X, y, NCLS, hp, 7, init, steps)
+        secs = time.perf_counter() - t0
+    return {"value": args.batch * steps / secs, "unit": "samples/s", "cores": 1, "kind": kind,
+            "sample": f"{steps} SgdEngine iterations (b={args.batch}, tau={args.tau} exchanges with an "
+                      f"in-process MasterState) on 1 host core of {os.cpu_count()}"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -216,6 +216,14 @@ int ds_engine_set_tickets(ds_engine* e, const uint64_t* tickets, uint64_t count)
  * policy fires WITHOUT performing that exchange (for host ExchangeFn callbacks);
  * *ran_out (host, optional, synchronous when given) reports the iterations done. */
 int ds_engine_run(ds_engine* e, uint64_t steps, int stop_at_exchange, uint64_t* ran_out);
+/* Host-fed iteration (a data pipeline that owns the rows, like the reference worker's
+ * ShardSweeper + gather_batch, engine.cpp:25-33 / model.cpp:12-21): copies `rows`
+ * gathered rows (X_host row-major, y_host) from host memory — pinned for full speed —
+ * into the engine's staging area, runs one iteration of run_training_loop on exactly
+ * that batch (policy and exchange included), and, when loss_host is given, reads the
+ * batch loss back (synchronous). The engine's own sweep position is not advanced. */
+int ds_engine_step_host(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows,
+                        double* loss_host);
 /* Block until the engine's queued work finished; returns DS_E_NUMERIC/DS_E_CONTRACT
  * if any step hit the reference's error conditions (message names the iteration). */
 int ds_engine_sync(ds_engine* e);

@@ -154,6 +154,11 @@ DSO_DECLARE(dsref)
 /* MasterState::exchange (exchanger.cpp:76-92) on `threads` host threads, each doing
  * `iters` exchanges of a P-float worker vector; returns seconds elapsed. */
 double dsref_master_exchange_time(uint64_t P, int lockfree, int threads, int iters);
+/* n worker threads (SgdEngine + ExchangePolicy + one in-process MasterState): wall
+ * seconds of `steps` timed iterations per worker after `warmup`; -1 on error. */
+double dsref_workers_time(const dso_model* m, const dso_data* shards, uint32_t n_workers,
+                          const dso_hyper* hp, const float* init, int lockfree, uint64_t warmup,
+                          uint64_t steps, double* losses_out);
 
 #ifdef __cplusplus
 }

@@ -411,6 +411,31 @@ class Oracle:
         assert self.prefix == "dsref"
         return self.lib.dsref_master_exchange_time(P, 1 if lockfree else 0, threads, iters)
 
+    def workers_time(self, m: ModelSpec, shards, n_classes: int, hp: Hyper, init, lockfree: bool, warmup: int,
+                     steps: int) -> float:
+        """Reference n-worker loop (threads) — wall seconds of `steps` iterations per worker."""
+        assert self.prefix == "dsref"
+        L = self.lib
+        L.dsref_workers_time.restype = C.c_double
+        L.dsref_workers_time.argtypes = [C.POINTER(dso_model), C.POINTER(dso_data), C.c_uint32,
+                                         C.POINTER(dso_hyper), C.POINTER(C.c_float), C.c_int, C.c_uint64,
+                                         C.c_uint64, C.POINTER(C.c_double)]
+        cm, _h = m.c()
+        keep = []
+        arr = (dso_data * len(shards))()
+        for k, (X, y) in enumerate(shards):
+            d, kk = self._data(X, y, n_classes)
+            keep.append(kk)
+            arr[k] = d
+        ch = hp.c()
+        init = np.ascontiguousarray(init, np.float32)
+        losses = np.zeros(len(shards))
+        s = L.dsref_workers_time(C.byref(cm), arr, len(shards), C.byref(ch), _p(init, C.c_float),
+                                 1 if lockfree else 0, warmup, steps, _p(losses, C.c_double))
+        if s < 0:
+            raise OracleError(3, self._last_error().decode())
+        return s
+
 
 def available(prefix: str) -> bool:
     return os.path.exists(LIBS[prefix])

@@ -355,3 +355,57 @@ double dsref_master_exchange_time(uint64_t P, int lockfree, int threads, int ite
 }
 
 }  // extern "C"
+
+// The reference's n-worker EASGD loop (the launch-local shape, main.cpp:443-570, minus
+// the TCP wire): one std::thread per worker running SgdEngine::step + ExchangePolicy
+// and MasterState::exchange against one in-process master (the exchanger's own
+// update rule, exchanger.cpp:76-92). Used by bench.py --impl reference / cpu_baseline.
+// Returns the wall seconds of the `steps` timed iterations (after `warmup`), all
+// workers started and stopped together; losses_out[k] gets worker k's last loss.
+#include <barrier>
+extern "C" double dsref_workers_time(const dso_model* m, const dso_data* shards, uint32_t n_workers,
+                                     const dso_hyper* hp, const float* init, int lockfree, uint64_t warmup,
+                                     uint64_t steps, double* losses_out) {
+  try {
+    const Model model = to_model(m);
+    const size_t P = model.param_dim();
+    const Hyperparams h = to_hyper(hp);
+    std::vector<Dataset> ds;
+    for (uint32_t k = 0; k < n_workers; ++k) ds.push_back(to_dataset(&shards[k]));
+    MasterState master(static_cast<uint32_t>(P), static_cast<float>(h.alpha),
+                       lockfree ? UpdateMode::LockFree : UpdateMode::Locked, ParamVector(init, init + P));
+    std::barrier sync(static_cast<std::ptrdiff_t>(n_workers) + 1);
+    std::vector<std::thread> pool;
+    for (uint32_t k = 0; k < n_workers; ++k) {
+      pool.emplace_back([&, k] {
+        SgdEngine eng(model, ds[k], h, mix_seed(1234, k), ParamVector(init, init + P));
+        ExchangePolicy pol(h);
+        ParamVector out(P);
+        double loss = 0.0;
+        auto iterate = [&](uint64_t n) {
+          for (uint64_t i = 0; i < n; ++i) {
+            loss = eng.step();
+            if (pol.on_iteration(loss).exchange) {
+              master.exchange(eng.params().data(), out.data());
+              eng.set_params(out);
+            }
+          }
+        };
+        iterate(warmup);
+        sync.arrive_and_wait();
+        iterate(steps);
+        sync.arrive_and_wait();
+        if (losses_out) losses_out[k] = loss;
+      });
+    }
+    sync.arrive_and_wait();
+    const auto t0 = std::chrono::steady_clock::now();
+    sync.arrive_and_wait();
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (auto& t : pool) t.join();
+    return s;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}

@@ -99,6 +99,15 @@ _sig("ds_elastic_update", VP, VP, U64, C.c_float, VP)
 _sig("ds_elastic_exchange", VP, VP, VP, U64, C.c_float, VP)
 _sig("ds_sgd_update", VP, VP, VP, U64, C.c_float, C.c_float, VP, VP)
 _sig("ds_sgd_step_checked", VP, VP, VP, U64, C.c_double, VP)
+_sig("ds_grad_accumulate", VP, VP, U64, VP)
+_sig("ds_grad_average", VP, VP, U64, U32, C.c_float, VP, VP)
+_sig("ds_device_alloc", C.c_int, U64, C.POINTER(VP))
+_sig("ds_device_free", VP)
+_sig("ds_memcpy", VP, VP, U64, VP)
+_sig("ds_memset", VP, C.c_int, U64, VP)
+_sig("ds_stream_create", C.c_int, C.POINTER(VP))
+_sig("ds_stream_destroy", VP)
+_sig("ds_stream_sync", VP)
 _sig("ds_param_dim", C.POINTER(ds_model_desc), P_U64)
 _sig("ds_loss_and_grad_workspace", C.POINTER(ds_model_desc), U32, P_U64)
 _sig("ds_loss_and_grad", C.POINTER(ds_model_desc), VP, VP, VP, U32, VP, VP, VP, VP, VP)
@@ -122,6 +131,7 @@ _sig("ds_engine_destroy", VP)
 _sig("ds_engine_attach_master", VP, VP)
 _sig("ds_engine_set_tickets", VP, VP, U64)
 _sig("ds_engine_run", VP, U64, C.c_int, P_U64)
+_sig("ds_engine_step_host", VP, VP, VP, U32, VP)
 _sig("ds_engine_sync", VP)
 _sig("ds_engine_stream", VP, C.POINTER(VP))
 _sig("ds_engine_log", VP, U64, U64, VP, VP, VP, VP)
@@ -134,12 +144,14 @@ _sig("ds_engine_launches", VP, P_U64)
 
 EXPORTED = [
     "ds_last_error", "ds_version", "ds_device_count", "ds_elastic_update", "ds_elastic_exchange",
-    "ds_sgd_update", "ds_sgd_step_checked", "ds_param_dim", "ds_loss_and_grad_workspace",
+    "ds_sgd_update", "ds_sgd_step_checked", "ds_grad_accumulate", "ds_grad_average", "ds_device_alloc",
+    "ds_device_free", "ds_memcpy", "ds_memset", "ds_stream_create", "ds_stream_destroy", "ds_stream_sync",
+    "ds_param_dim", "ds_loss_and_grad_workspace",
     "ds_loss_and_grad", "ds_predict", "ds_count_hits", "ds_master_create", "ds_master_create_sharded",
     "ds_master_export", "ds_master_attach", "ds_master_destroy", "ds_master_exchange",
     "ds_master_exchange_ticketed", "ds_master_snapshot", "ds_master_local_slice",
     "ds_master_exchange_count", "ds_master_dim", "ds_master_reset_tickets", "ds_engine_create",
-    "ds_engine_destroy", "ds_engine_attach_master", "ds_engine_set_tickets", "ds_engine_run",
+    "ds_engine_destroy", "ds_engine_attach_master", "ds_engine_set_tickets", "ds_engine_run", "ds_engine_step_host",
     "ds_engine_sync", "ds_engine_stream", "ds_engine_log", "ds_engine_iterations",
     "ds_engine_get_params", "ds_engine_set_params", "ds_engine_params_device", "ds_engine_policy",
     "ds_engine_launches",

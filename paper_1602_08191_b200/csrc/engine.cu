@@ -100,6 +100,13 @@ struct ds_engine {
   bool fused = false;
   int fused_grid = 0;
   uint64_t launches = 0;
+  // host-fed batches (ds_engine_step_host): staging rows, identity plan, row count
+  float* Xb = nullptr;
+  uint32_t* yb = nullptr;
+  uint32_t* iota = nullptr;
+  uint32_t* rows_dev = nullptr;
+  uint32_t hostfed_rows = 0;
+  bool hostfed = false;
 };
 
 namespace dsb {
@@ -207,15 +214,18 @@ int enqueue_exchange(ds_engine* e, float* p) {
 
 // Layered iterations; with_master = perform fired exchanges against e->master.
 int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
-  DS_TRY(upload_plan(e, steps));
+  if (!e->hostfed) DS_TRY(upload_plan(e, steps));
   const uint64_t B = e->hp.batch_size;
+  const float* X = e->hostfed ? e->Xb : e->X;
+  const uint32_t* y = e->hostfed ? e->yb : e->y;
   const float eta = static_cast<float>(e->hp.eta);
   const float wd = static_cast<float>(e->hp.weight_decay);
   float* p = e->params[e->cur];
   const bool xm = with_master && e->master;
   for (uint64_t j = 0; j < steps; ++j) {
-    const uint32_t R = e->h_rows[j];
-    DS_TRY(launch_loss_and_grad(e->model, p, e->X, e->plan + j * B, e->y, R, e->grad, &e->st->loss, e->ws,
+    const uint32_t R = e->hostfed ? e->hostfed_rows : e->h_rows[j];
+    const uint32_t* idx = e->hostfed ? e->iota : e->plan + j * B;
+    DS_TRY(launch_loss_and_grad(e->model, p, X, idx, y, R, e->grad, &e->st->loss, e->ws,
                                 &e->st->flags, &e->st->err, e->stream));
     e->launches += 3 * e->model.layers.size() + 1;
     DS_TRY(launch_sgd(p, p, e->grad, e->model.P, eta, wd, &e->st->flags, e->stream, &e->st->err));
@@ -234,16 +244,16 @@ int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
 }
 
 int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
-  DS_TRY(upload_plan(e, steps));
+  if (!e->hostfed) DS_TRY(upload_plan(e, steps));
   FusedArgs a{};
   a.F = e->model.n_features;
   a.H = e->model.hidden.empty() ? 0 : e->model.hidden[0];
   a.C = e->model.n_classes;
   a.P = e->model.P;
-  a.X = e->X;
-  a.y = e->y;
-  a.plan = e->plan;
-  a.plan_rows = e->plan_rows;
+  a.X = e->hostfed ? e->Xb : e->X;
+  a.y = e->hostfed ? e->yb : e->y;
+  a.plan = e->hostfed ? e->iota : e->plan;
+  a.plan_rows = e->hostfed ? e->rows_dev : e->plan_rows;
   a.B = e->hp.batch_size;
   a.steps = steps;
   a.params[0] = e->params[0];
@@ -328,6 +338,15 @@ extern "C" int ds_engine_create(ds_engine** out, int device, const ds_model_desc
   if (err == cudaSuccess) err = cudaMalloc(&e->st, sizeof(dsb::DevState));
   if (err == cudaSuccess) err = cudaMalloc(&e->bar, 64 * sizeof(unsigned int));
   if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->plan_ev, cudaEventDisableTiming);
+  if (err == cudaSuccess) err = cudaMalloc(&e->Xb, B * F * sizeof(float));
+  if (err == cudaSuccess) err = cudaMalloc(&e->yb, B * sizeof(uint32_t));
+  if (err == cudaSuccess) err = cudaMalloc(&e->iota, B * sizeof(uint32_t));
+  if (err == cudaSuccess) err = cudaMalloc(&e->rows_dev, sizeof(uint32_t));
+  if (err == cudaSuccess) {
+    std::vector<uint32_t> id(B);
+    std::iota(id.begin(), id.end(), 0u);
+    err = cudaMemcpy(e->iota, id.data(), B * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  }
   if (err == cudaSuccess) err = cudaMemcpy(e->X, X_host, shard_n * F * sizeof(float), cudaMemcpyDefault);
   if (err == cudaSuccess) err = cudaMemcpy(e->y, y_host, shard_n * sizeof(uint32_t), cudaMemcpyDefault);
   if (err == cudaSuccess) err = cudaMemcpy(e->params[0], init_host, m.P * sizeof(float), cudaMemcpyDefault);
@@ -377,6 +396,10 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->plan);
   cudaFree(e->plan_rows);
   cudaFree(e->d_tickets);
+  cudaFree(e->Xb);
+  cudaFree(e->yb);
+  cudaFree(e->iota);
+  cudaFree(e->rows_dev);
   if (e->h_plan) cudaFreeHost(e->h_plan);
   if (e->h_rows) cudaFreeHost(e->h_rows);
   cudaFree(e->log.loss);
@@ -574,5 +597,29 @@ extern "C" int ds_engine_policy(ds_engine* e, double* cumulated, uint32_t* since
 extern "C" int ds_engine_launches(ds_engine* e, uint64_t* launches) {
   if (!e || !launches) return set_error(DS_E_CONTRACT, "engine: null");
   *launches = e->launches;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_step_host(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows,
+                                   double* loss_host) {
+  if (!e || !X_host || !y_host) return set_error(DS_E_CONTRACT, "engine_step_host: null");
+  if (rows == 0) return set_error(DS_E_CONTRACT, "loss_and_grad: empty batch");
+  if (rows > e->hp.batch_size) return set_error(DS_E_CONTRACT, "engine_step_host: more rows than batch_size");
+  dsb::DeviceScope ds(e->device);
+  const uint64_t F = e->model.n_features;
+  DS_CUDA_TRY(cudaMemcpyAsync(e->Xb, X_host, rows * F * sizeof(float), cudaMemcpyDefault, e->stream));
+  DS_CUDA_TRY(cudaMemcpyAsync(e->yb, y_host, rows * sizeof(uint32_t), cudaMemcpyDefault, e->stream));
+  DS_CUDA_TRY(cudaMemcpyAsync(e->rows_dev, &rows, sizeof(uint32_t), cudaMemcpyHostToDevice, e->stream));
+  e->hostfed = true;
+  e->hostfed_rows = rows;
+  const int rc = ds_engine_run(e, 1, 0, nullptr);
+  e->hostfed = false;
+  if (rc != DS_OK) return rc;
+  if (loss_host) {
+    // the loss row of this iteration: st->iter was advanced by the step
+    DS_CUDA_TRY(cudaMemcpyAsync(loss_host, e->log.loss + (e->queued - 1), sizeof(double), cudaMemcpyDeviceToHost,
+                                e->stream));
+    DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  }
   return DS_OK;
 }
