@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 
 #include "deepspark/rng.hpp"
@@ -273,9 +275,41 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
     a.tickets = e->tickets.empty() ? nullptr : e->d_tickets + e->host_exchanges;
     a.ticket_src = (!a.lockfree && !a.tickets) ? &e->master->table.flags[0]->next_ticket : nullptr;
   }
+  // DS_FUSED_PROFILE=<file>: per-phase globaltimer stamps of CTA 0, medians appended
+  const char* prof_path = std::getenv("DS_FUSED_PROFILE");
+  unsigned long long* prof = nullptr;
+  if (prof_path && steps >= 8) DS_CUDA_TRY(cudaMalloc(&prof, steps * kProfSlots * sizeof(unsigned long long)));
+  if (prof) DS_CUDA_TRY(cudaMemsetAsync(prof, 0, steps * kProfSlots * sizeof(unsigned long long), e->stream));
+  a.prof = prof;
   DS_TRY(launch_fused(a, e->fused_grid, e->stream));
   e->launches += 1;
   e->cur ^= static_cast<int>(steps & 1);
+  if (prof) {
+    std::vector<unsigned long long> h(steps * kProfSlots);
+    DS_CUDA_TRY(cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream));
+    DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    cudaFree(prof);
+    const char* names[] = {"x_staged", "forward", "grid_barrier", "acts_staged", "logits", "softmax_loss",
+                           "backward_update", "policy_exchange"};
+    const int pairs[][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}};
+    if (FILE* f = std::fopen(prof_path, "a")) {
+      std::fprintf(f, "steps=%llu", (unsigned long long)steps);
+      for (int k = 0; k < 8; ++k) {
+        std::vector<double> d;
+        for (uint64_t s = 2; s < steps; ++s) {
+          const unsigned long long t0 = h[s * kProfSlots + pairs[k][0]], t1 = h[s * kProfSlots + pairs[k][1]];
+          if (t0 && t1 >= t0) d.push_back(static_cast<double>(t1 - t0));
+        }
+        std::sort(d.begin(), d.end());
+        std::fprintf(f, " %s=%.0fns", names[k], d.empty() ? -1.0 : d[d.size() / 2]);
+      }
+      std::vector<double> tot;
+      for (uint64_t s = 3; s < steps; ++s) tot.push_back(static_cast<double>(h[s * kProfSlots] - h[(s - 1) * kProfSlots]));
+      std::sort(tot.begin(), tot.end());
+      std::fprintf(f, " step=%.0fns\n", tot.empty() ? -1.0 : tot[tot.size() / 2]);
+      std::fclose(f);
+    }
+  }
   return DS_OK;
 }
 

@@ -62,7 +62,10 @@ struct FusedArgs {
   unsigned long long* ticket_src;  // Locked: dispenser (shard 0 flags.next_ticket)
   int stop_at_exchange;
   unsigned int* bar;          // grid barrier words [2]
+  unsigned long long* prof;   // optional: kProfSlots globaltimer stamps per step (CTA 0)
 };
+
+constexpr int kProfSlots = 10;
 
 int fused_supported(const ModelInfo& m, uint32_t batch, int device, const char** why);
 int launch_fused(const FusedArgs& a, int grid, cudaStream_t s);
