@@ -119,6 +119,11 @@ int dsx_run_training_loop(const dsx_model* m, const dsx_data* shard, const dsx_h
 int dsx_resolve_loss_cut(const dsx_model* m, const dsx_data* shard, const dsx_hyper* hp, uint64_t sweep_seed,
                          const float* init, double* cut);
 int dsx_simulate(const dsx_sim_cfg* cfg, dsx_sim_out* out);
+/* exchange_order (simulator.hpp): the global (worker, iteration) exchange sequence of
+ * simulate_async for a Fixed period; *count = total (entries beyond cap not written). */
+int dsx_exchange_order(uint32_t n_workers, double batch_cost_C, double comm_cost_S, const double* mults,
+                       uint32_t tau, uint64_t i_max, uint64_t schedule_seed, uint32_t* worker, uint64_t* iteration,
+                       uint64_t cap, uint64_t* count);
 
 #ifdef __cplusplus
 }

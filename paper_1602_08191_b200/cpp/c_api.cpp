@@ -311,4 +311,25 @@ int dsx_simulate(const dsx_sim_cfg* c, dsx_sim_out* o) {
   });
 }
 
+int dsx_exchange_order(uint32_t n_workers, double batch_cost_C, double comm_cost_S, const double* mults, uint32_t tau,
+                       uint64_t i_max, uint64_t schedule_seed, uint32_t* worker, uint64_t* iteration, uint64_t cap,
+                       uint64_t* count) {
+  return guard([&] {
+    SimConfig cfg;
+    cfg.n_workers = n_workers;
+    cfg.batch_cost_C = batch_cost_C;
+    cfg.comm_cost_S = comm_cost_S;
+    if (mults) cfg.cost_multipliers.assign(mults, mults + n_workers);
+    cfg.hyper.tau = tau;
+    cfg.hyper.i_max = i_max;
+    cfg.schedule_seed = schedule_seed;
+    const auto ev = exchange_order(cfg);
+    *count = ev.size();
+    for (size_t j = 0; j < ev.size() && j < cap; ++j) {
+      if (worker) worker[j] = ev[j].worker;
+      if (iteration) iteration[j] = ev[j].iteration;
+    }
+  });
+}
+
 }  // extern "C"

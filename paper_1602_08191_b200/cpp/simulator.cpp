@@ -273,6 +273,33 @@ SimResult simulate(const SimConfig& cfg) {
                                          : simulate_sync(cfg, shards, holdout, std::move(master));
 }
 
+std::vector<ExchangeEvent> exchange_order(const SimConfig& cfg) {
+  if (cfg.n_workers < 1) throw ContractError("sim: n_workers must be >= 1");
+  if (cfg.hyper.period_mode != PeriodMode::Fixed || cfg.hyper.tau == 0)
+    throw ContractError("exchange_order: needs a Fixed period (adaptive order is value-dependent)");
+  if (!cfg.cost_multipliers.empty() && cfg.cost_multipliers.size() != cfg.n_workers)
+    throw ContractError("sim: cost_multipliers must have one entry per worker");
+  const uint32_t n = cfg.n_workers;
+  Rng sched(cfg.schedule_seed);
+  std::priority_queue<Event, std::vector<Event>, std::greater<Event>> pq;
+  std::vector<uint64_t> done(n, 0);
+  for (uint32_t k = 0; k < n; ++k) pq.push({cfg.batch_cost_C * mult(cfg, k), sched.next_u64(), k});
+  std::vector<ExchangeEvent> out;
+  while (!pq.empty()) {
+    const Event ev = pq.top();
+    pq.pop();
+    const uint32_t k = ev.worker;
+    const uint64_t it = ++done[k];
+    double next_t = ev.t + cfg.batch_cost_C * mult(cfg, k);
+    if (it % cfg.hyper.tau == 0) {  // ExchangePolicy Fixed: since == tau, reset on fire
+      out.push_back({k, it, ev.t});
+      next_t += cfg.comm_cost_S;
+    }
+    if (it < cfg.hyper.i_max) pq.push({next_t, sched.next_u64(), k});
+  }
+  return out;
+}
+
 std::optional<uint64_t> iterations_to_accuracy(const SimResult& result, double target) {
   for (const EvalPoint& p : result.eval_curve)
     if (p.accuracy >= target) return p.per_worker_iter;

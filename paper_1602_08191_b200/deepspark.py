@@ -104,6 +104,8 @@ _SIGS = {
     "dsx_resolve_loss_cut": (C.c_int, [P(dsx_model), P(dsx_data), P(dsx_hyper), C.c_uint64, P(C.c_float),
                                        P(C.c_double)]),
     "dsx_simulate": (C.c_int, [P(dsx_sim_cfg), P(dsx_sim_out)]),
+    "dsx_exchange_order": (C.c_int, [C.c_uint32, C.c_double, C.c_double, P(C.c_double), C.c_uint32, C.c_uint64,
+                                     C.c_uint64, P(C.c_uint32), P(C.c_uint64), C.c_uint64, P(C.c_uint64)]),
 }
 for _n, (_r, _a) in _SIGS.items():
     _f = getattr(lib, _n)
@@ -301,6 +303,18 @@ class DeepSpark:
         _check(lib.dsx_resolve_loss_cut(C.byref(d), C.byref(dd), C.byref(ch), sweep_seed, _p(init, C.c_float),
                                         C.byref(cut)))
         return cut.value
+
+    def exchange_order(self, n_workers, tau, i_max, schedule_seed, batch_cost_C=1.0, comm_cost_S=0.0,
+                       cost_multipliers=None):
+        """Global (worker, iteration) exchange order of simulate_async (Fixed period)."""
+        cap = n_workers * (i_max // tau) + 1
+        w = np.zeros(cap, np.uint32)
+        it = np.zeros(cap, np.uint64)
+        cnt = C.c_uint64()
+        mults = None if cost_multipliers is None else np.ascontiguousarray(cost_multipliers, np.float64)
+        _check(lib.dsx_exchange_order(n_workers, batch_cost_C, comm_cost_S, _p(mults, C.c_double), tau, i_max,
+                                      schedule_seed, _p(w, C.c_uint32), _p(it, C.c_uint64), cap, C.byref(cnt)))
+        return w[:cnt.value], it[:cnt.value]
 
     def simulate(self, s, snap_cap: Optional[int] = None, eval_cap: int = 100000):
         """simulate(SimConfig) — s carries SimConfig's fields (+ X, y, n_classes for the dataset)."""
