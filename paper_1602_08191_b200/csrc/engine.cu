@@ -76,7 +76,8 @@ struct ds_engine {
   int cur = 0;
   float* grad = nullptr;
   double* ws = nullptr;
-  double* act = nullptr;  // fused: [2][B x H]
+  double* act = nullptr;   // fused: [2][H x B]
+  double* xb64 = nullptr;  // fused MLP: [3][chunks][B][CW] f64 batch rows
   dsb::DevState* st = nullptr;
   dsb::DevLog log{};
   unsigned int* bar = nullptr;
@@ -262,6 +263,7 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
   a.params[1] = e->params[1];
   a.cur = e->cur;
   a.act = e->act;
+  a.xb64 = e->xb64;
   a.eta = static_cast<float>(e->hp.eta);
   a.wd = static_cast<float>(e->hp.weight_decay);
   a.alpha = e->master ? e->master->alpha : static_cast<float>(e->hp.alpha);
@@ -290,11 +292,11 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
     DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
     cudaFree(prof);
     const char* names[] = {"x_staged", "forward", "grid_barrier", "acts_staged", "logits", "softmax_loss",
-                           "backward_update", "policy_exchange"};
-    const int pairs[][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}};
+                           "backward_update", "policy_exchange", "bwd_head", "bwd_dW1"};
+    const int pairs[][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}, {6, 9}, {9, 7}};
     if (FILE* f = std::fopen(prof_path, "a")) {
       std::fprintf(f, "steps=%llu", (unsigned long long)steps);
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < 10; ++k) {
         std::vector<double> d;
         for (uint64_t s = 2; s < steps; ++s) {
           const unsigned long long t0 = h[s * kProfSlots + pairs[k][0]], t1 = h[s * kProfSlots + pairs[k][1]];
@@ -408,6 +410,8 @@ extern "C" int ds_engine_create(ds_engine** out, int device, const ds_model_desc
     e->fused_grid = dsb::fused_grid(m, device);
     const uint64_t H = m.hidden.empty() ? 0 : m.hidden[0];
     err = cudaMalloc(&e->act, 2 * B * (H ? H : 1) * sizeof(double));
+    const size_t xbd = dsb::fused_xb_doubles(m, static_cast<uint32_t>(B), device);
+    if (err == cudaSuccess && xbd) err = cudaMalloc(&e->xb64, xbd * sizeof(double));
     if (err != cudaSuccess) return fail(set_error(DS_E_NOMEM, "engine: %s", cudaGetErrorString(err)));
   }
   *out = e;
@@ -425,6 +429,7 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->grad);
   cudaFree(e->ws);
   cudaFree(e->act);
+  cudaFree(e->xb64);
   cudaFree(e->st);
   cudaFree(e->bar);
   cudaFree(e->plan);

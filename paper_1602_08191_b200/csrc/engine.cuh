@@ -50,7 +50,8 @@ struct FusedArgs {
   uint64_t steps;
   float* params[2];     // ping-pong parameter buffers; step s reads [cur], writes [cur^1]
   int cur;
-  double* act;          // [2][B x H] hidden activations (ping-pong), f64
+  double* act;          // [2][H x B] hidden activations (ping-pong), f64, unit-major
+  double* xb64;         // [3][nck][B][CW] f64 copies of the batch rows (MLP kernel)
   float eta, wd, alpha;
   DevState* st;
   DevLog log;
@@ -68,6 +69,8 @@ struct FusedArgs {
 constexpr int kProfSlots = 10;
 
 int fused_supported(const ModelInfo& m, uint32_t batch, int device, const char** why);
+// Doubles of the f64 batch buffer (A.xb64) the MLP kernel needs.
+size_t fused_xb_doubles(const ModelInfo& m, uint32_t batch, int device);
 int launch_fused(const FusedArgs& a, int grid, cudaStream_t s);
 int fused_grid(const ModelInfo& m, int device);
 size_t fused_smem_bytes(const ModelInfo& m, uint32_t batch);

@@ -27,6 +27,8 @@
 // rounded to f32 once, and the update rounds like param_vector.cpp:33. The chains are
 // what bounds this kernel (latency, not bandwidth): 784 dependent DADDs per hidden
 // unit, 256 per logit.
+#include <cstdlib>
+
 #include "ds_common.cuh"
 #include "engine.cuh"
 
@@ -199,9 +201,13 @@ struct SmemPlan {
   uint32_t Fs;     // X row stride (floats): 16-byte multiple when bulk copies apply
   uint32_t Hs;     // activation row stride (doubles)
   uint32_t H2;     // W2 row stride (doubles)
+  uint32_t CW;     // X columns per f64 chunk (converted once per element, see below)
+  uint32_t CWs;    // f64 chunk row stride (doubles)
   bool bulk_x;     // X rows by TMA bulk copies and 128-bit loads (F % 4 == 0)
   bool bulk_a;     // activation rows by TMA bulk copies (H % 2 == 0)
-  size_t x, w, w2, as, z, e, d1, lr, rs, bars, total;
+  // Region `un` is time-shared: f64 X chunks during the forward and the dW1 phase,
+  // activations (as) + W2 in f64 (w2) in between.
+  size_t x, w, wd, un, w2, as, z, e, d1, lr, rs, bars, total;
 };
 
 __host__ __device__ inline SmemPlan make_plan(uint32_t F, uint32_t H, uint32_t C, uint32_t B, uint32_t G) {
@@ -210,15 +216,30 @@ __host__ __device__ inline SmemPlan make_plan(uint32_t F, uint32_t H, uint32_t C
   const uint32_t U = hidden ? (H + G - 1) / G : 0;
   p.bulk_x = (F % 4) == 0;
   p.Fs = p.bulk_x ? F + 4 : (F | 1u);
-  p.bulk_a = hidden && (H % 2) == 0;
-  p.Hs = hidden ? (p.bulk_a ? H + 2 : (H | 1u)) : 0;
+  // activations are unit-major [H][B] in global and shared memory: one contiguous
+  // block (TMA), and lane == row reads are conflict-free in the logits
+  p.bulk_a = hidden && (static_cast<size_t>(H) * B) % 2 == 0;
+  p.Hs = B;
   p.H2 = hidden ? ((H % 2) == 0 ? H + 2 : H + 1) : 0;
   auto al = [](size_t v) { return (v + 127) & ~static_cast<size_t>(127); };
+  const size_t as_bytes = hidden ? al(static_cast<size_t>(H) * B * 8) : 0;
+  const size_t w2_bytes = hidden ? al(static_cast<size_t>(C) * p.H2 * 8) : 0;
+  // widest chunk (multiple of 16 columns, <= 256) that fits where as + w2 live
+  uint32_t cw = 256;
+  if (hidden) {
+    while (cw > 16 && static_cast<size_t>(B) * (cw + 2) * 8 > as_bytes + w2_bytes) cw -= 16;
+  }
+  p.CW = cw;
+  p.CWs = cw + 2;
+  const size_t chunk_bytes = al(static_cast<size_t>(B) * p.CWs * 8);
   size_t off = 0;
   p.x = off;   off = al(off + static_cast<size_t>(B) * p.Fs * 4);
   p.w = off;   off = al(off + static_cast<size_t>(hidden ? U : C) * F * 4);
-  p.w2 = off;  off = al(off + (hidden ? static_cast<size_t>(C) * p.H2 * 8 : 0));
-  p.as = off;  off = al(off + (hidden ? static_cast<size_t>(B) * p.Hs * 8 : 0));
+  p.wd = off;  off = al(off + (hidden ? static_cast<size_t>(U) * F * 8 : 0));
+  p.un = off;
+  p.as = off;
+  p.w2 = off + as_bytes;
+  off = al(off + (hidden ? (as_bytes + w2_bytes > chunk_bytes ? as_bytes + w2_bytes : chunk_bytes) : 0));
   p.z = off;   off = al(off + static_cast<size_t>(B) * C * 8);
   p.e = off;   off = al(off + static_cast<size_t>(B) * C * 8);
   p.d1 = off;  off = al(off + (hidden ? static_cast<size_t>(B) * U * 8 : 0));
@@ -315,6 +336,28 @@ __device__ __forceinline__ double dot_f64_exact(double z, const double* __restri
   return z;
 }
 
+// Xd[r, 0:cw] = (double) Xs[r, c0:c0+cw] for r < R: one warp per row, float4 -> 2 x
+// double2 (no per-element index arithmetic; F2F is the only real cost).
+__device__ __forceinline__ void convert_chunk(double* Xd, uint32_t CWs, const float* Xs, uint32_t Fs, uint32_t R,
+                                              uint32_t c0, uint32_t cw, bool vec) {
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = kFT / 32;
+  for (uint32_t r = warp; r < R; r += nwarps) {
+    const float* src = Xs + static_cast<size_t>(r) * Fs + c0;
+    double* dst = Xd + static_cast<size_t>(r) * CWs;
+    if (vec) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      double2* d2 = reinterpret_cast<double2*>(dst);
+      for (uint32_t q = lane; q < cw / 4; q += 32) {
+        const float4 v = s4[q];
+        d2[2 * q] = make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
+        d2[2 * q + 1] = make_double2(static_cast<double>(v.z), static_cast<double>(v.w));
+      }
+    } else {
+      for (uint32_t j = lane; j < cw; j += 32) dst[j] = static_cast<double>(src[j]);
+    }
+  }
+}
+
 template <bool kHidden>
 __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -329,6 +372,8 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
 
   float* Xs = reinterpret_cast<float*>(smem_raw + sp.x);     // B x Fs batch rows
   float* Ws = reinterpret_cast<float*>(smem_raw + sp.w);     // own W1 rows (U x F) | softmax W (C x F)
+  double* Wd = reinterpret_cast<double*>(smem_raw + sp.wd);  // own W1 rows as f64 (exact copy of Ws)
+  double* Xd = reinterpret_cast<double*>(smem_raw + sp.un);  // B x CWs f64 chunk of X (time-shared)
   double* W2d = reinterpret_cast<double*>(smem_raw + sp.w2); // C x H2, W2 as f64 (exact)
   double* As = reinterpret_cast<double*>(smem_raw + sp.as);  // B x Hs activations
   double* Z = reinterpret_cast<double*>(smem_raw + sp.z);    // B x C logits, then deltas
@@ -385,7 +430,11 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
     const float* P0 = A.params[cur];
     const uint32_t nW = kHidden ? Uo * F : (blockIdx.x == 0 ? C * F : 0);
     const float* src = P0 + (kHidden ? w1 + static_cast<uint64_t>(u0) * F : 0);
-    for (uint32_t e = tid; e < nW; e += kFT) Ws[e] = ldcg(src + e);
+    for (uint32_t e = tid; e < nW; e += kFT) {
+      const float v = ldcg(src + e);
+      Ws[e] = v;
+      if constexpr (kHidden) Wd[e] = static_cast<double>(v);
+    }
   }
   // L2 prefetch of the first batch's rows
   if (tid < B && A.steps > 0 && sp.bulk_x) {
@@ -436,11 +485,21 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
 
     if constexpr (kHidden) {
       double* act = A.act + static_cast<size_t>(step & 1) * B * H;
-      for (uint32_t t = tid; t < R * Uo; t += kFT) {
-        const uint32_t r = t / Uo, uu = t - r * Uo, u = u0 + uu;
-        const double z = dot_f32_exact(static_cast<double>(ldcg(P + b1 + u)), Ws + uu * F, Xs + r * Fs, F, sp.bulk_x);
-        act[static_cast<size_t>(r) * H + u] = tanh(z);
+      // Forward in f64 chunks of CW columns: every X element is converted to f64 once
+      // (F2F runs at a quarter of the FP64 rate on B200) by all threads, then the chain
+      // threads (one per (row, unit), R*Uo <= kFT) continue their reference-order sums.
+      const uint32_t t_ch = tid;
+      const bool chain = t_ch < R * Uo;
+      const uint32_t cr = chain ? t_ch / Uo : 0, cuu = chain ? t_ch - cr * Uo : 0;
+      double zc = chain ? static_cast<double>(ldcg(P + b1 + u0 + cuu)) : 0.0;
+      for (uint32_t c0 = 0; c0 < F; c0 += sp.CW) {
+        const uint32_t cw = F - c0 < sp.CW ? F - c0 : sp.CW;
+        __syncthreads();  // previous chunk consumed
+        convert_chunk(Xd, sp.CWs, Xs, Fs, R, c0, cw, sp.bulk_x && (cw % 4) == 0);
+        __syncthreads();
+        if (chain) zc = dot_f64_exact(zc, Wd + cuu * F + c0, Xd + cr * sp.CWs, cw, (cw % 2) == 0 && (F % 2) == 0);
       }
+      if (chain) act[static_cast<size_t>(u0 + cuu) * B + cr] = tanh(zc);
       stamp(A.prof, step, 2);
       // grid barrier; thread 0 also samples the failure flags of the previous iteration
       __syncthreads();
@@ -459,9 +518,11 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
         s_flags = *reinterpret_cast<volatile uint32_t*>(&st->flags);
         fence_proxy_async();  // other CTAs' generic writes (act, W2) before our async reads
         if (sp.bulk_a && !s_flags) {
-          mbar_arrive_expect_tx(bar_a, R * H * 8);
-          for (uint32_t r = 0; r < R; ++r)
-            bulk_g2s(As + static_cast<size_t>(r) * Hs, act + static_cast<size_t>(r) * H, H * 8, bar_a);
+          const uint32_t total = H * B * 8;  // [H][B] block, rows >= R unused
+          mbar_arrive_expect_tx(bar_a, total);
+          for (uint32_t off = 0; off < total; off += 32768)
+            bulk_g2s(reinterpret_cast<unsigned char*>(As) + off, reinterpret_cast<const unsigned char*>(act) + off,
+                     total - off < 32768 ? total - off : 32768, bar_a);
         }
       }
       __syncthreads();
@@ -475,21 +536,25 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
       }
       // ---- B: activations (TMA), W2 as f64, logits, softmax-CE ---------------------------
       if (!sp.bulk_a) {
-        for (uint32_t e = tid; e < R * H; e += kFT) {
-          const uint32_t r = e / H, u = e - r * H;
-          As[static_cast<size_t>(r) * Hs + u] = __ldcg(act + e);
-        }
+        for (uint32_t e = tid; e < H * B; e += kFT) As[e] = __ldcg(act + e);
       }
-      for (uint32_t e0 = tid; e0 < C * H; e0 += 4 * kFT) {
-        float v[4];
+      {  // W2 -> f64 rows: one warp per class row, coalesced, all loads issued first
+        const uint32_t warp = tid >> 5, lane = tid & 31;
+        for (uint32_t c = warp; c < C; c += kFT / 32) {
+          const float* src = P + w2 + static_cast<size_t>(c) * H;
+          double* dst = W2d + static_cast<size_t>(c) * H2;
+          for (uint32_t u0c = 0; u0c < H; u0c += 8 * 32) {
+            float v[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = (e0 + k * kFT < C * H) ? ldcg(P + w2 + e0 + k * kFT) : 0.0f;
+            for (int k = 0; k < 8; ++k) {
+              const uint32_t u = u0c + k * 32 + lane;
+              v[k] = u < H ? ldcg(src + u) : 0.0f;
+            }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t e = e0 + k * kFT;
-          if (e < C * H) {
-            const uint32_t c = e / H, u = e - c * H;
-            W2d[static_cast<size_t>(c) * H2 + u] = static_cast<double>(v[k]);
+            for (int k = 0; k < 8; ++k) {
+              const uint32_t u = u0c + k * 32 + lane;
+              if (u < H) dst[u] = static_cast<double>(v[k]);
+            }
           }
         }
       }
@@ -499,11 +564,60 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
       }
       __syncthreads();
       stamp(A.prof, step, 4);
-      const bool v2 = (H % 2) == 0;
-      for (uint32_t t = tid; t < R * C; t += kFT) {
-        const uint32_t r = t / C, c = t - r * C;
-        Z[t] = dot_f64_exact(static_cast<double>(ldcg(P + b2 + c)), W2d + static_cast<size_t>(c) * H2,
-                             As + static_cast<size_t>(r) * Hs, H, v2);
+      // Logits, lane == batch row, each warp two classes (two interleaved chains): the
+      // activation loads are conflict-free ([H][B] layout) and shared by both chains,
+      // the W2 loads are warp broadcasts. Reference order: b2[c] + sum_u in u order.
+      {
+        const uint32_t warp = tid >> 5, lane = tid & 31;
+        const uint32_t nwl = (C + 1) / 2 < kFT / 32 ? (C + 1) / 2 : kFT / 32;
+        for (uint32_t r0 = 0; r0 < R; r0 += 32) {
+          const uint32_t r = r0 + lane;
+          if (warp >= nwl || r >= R) continue;
+          for (uint32_t c = warp; c < C; c += 2 * nwl) {
+            const uint32_t c2 = c + nwl;
+            const bool has2 = c2 < C;
+            const double* wa = W2d + static_cast<size_t>(c) * H2;
+            const double* wb = W2d + static_cast<size_t>(has2 ? c2 : c) * H2;
+            const double* a = As + r;
+            double za = static_cast<double>(ldcg(P + b2 + c));
+            double zb = has2 ? static_cast<double>(ldcg(P + b2 + c2)) : 0.0;
+            double pa[8], pb[8], qa[8], qb[8];
+            const uint32_t nb = H / 8;
+            auto prod = [&](uint32_t blk, double (&xa)[8], double (&xb)[8]) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const double av = a[static_cast<size_t>(blk * 8 + k) * B];
+                xa[k] = dmul(wa[blk * 8 + k], av);
+                xb[k] = dmul(wb[blk * 8 + k], av);
+              }
+            };
+            if (nb) {
+              prod(0, pa, pb);
+              for (uint32_t blk = 1; blk < nb; ++blk) {
+                prod(blk, qa, qb);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  za = dadd(za, pa[k]);
+                  zb = dadd(zb, pb[k]);
+                  pa[k] = qa[k];
+                  pb[k] = qb[k];
+                }
+              }
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                za = dadd(za, pa[k]);
+                zb = dadd(zb, pb[k]);
+              }
+            }
+            for (uint32_t u = nb * 8; u < H; ++u) {
+              const double av = a[static_cast<size_t>(u) * B];
+              za = dadd(za, dmul(wa[u], av));
+              zb = dadd(zb, dmul(wb[u], av));
+            }
+            Z[static_cast<size_t>(r) * C + c] = za;
+            if (has2) Z[static_cast<size_t>(r) * C + c2] = zb;
+          }
+        }
       }
     } else {
       if (blockIdx.x == 0) {
@@ -563,62 +677,17 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
         const double* d = Z + static_cast<size_t>(r) * C;
         double p = 0.0;
         for (uint32_t c = 0; c < C; ++c) p = dadd(p, dmul(d[c], W2d[static_cast<size_t>(c) * H2 + u]));
-        const double a = As[static_cast<size_t>(r) * Hs + u];
+        const double a = As[static_cast<size_t>(u) * Hs + r];
         D1[r * U + uu] = dmul(p, dsub(1.0, dmul(a, a)));
       }
       __syncthreads();
-      // own W1 rows and b1 (the bias is the column x == 1: dmul(d, 1.0) == d exactly),
-      // four independent batch chains per thread for ILP
-      const uint32_t nOut = Uo * (F + 1);
-      for (uint32_t e0 = tid; e0 < nOut; e0 += 4 * kFT) {
-        uint32_t uu[4], ii[4];
-        bool ok[4];
-        double acc[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t e = e0 + k * kFT;
-          ok[k] = e < nOut;
-          uu[k] = ok[k] ? e / (F + 1) : 0;
-          ii[k] = ok[k] ? e - uu[k] * (F + 1) : 0;
-          acc[k] = 0.0;
-        }
-        // pipelined: the products of row r+1 are formed before row r's adds
-        double pc[4], pn[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          pc[k] = dmul(D1[uu[k]], ii[k] == F ? 1.0 : static_cast<double>(Xs[ii[k]]));
-        for (uint32_t r = 1; r < R; ++r) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            pn[k] = dmul(D1[r * U + uu[k]], ii[k] == F ? 1.0 : static_cast<double>(Xs[r * Fs + ii[k]]));
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            acc[k] = dadd(acc[k], pc[k]);
-            pc[k] = pn[k];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[k] = dadd(acc[k], pc[k]);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (!ok[k]) continue;
-          const uint32_t u = u0 + uu[k];
-          if (ii[k] == F) {
-            const uint64_t g = b1 + u;
-            Pn[g] = sgd_apply(acc[k], inv_b, ldcg(P + g), A.eta, A.wd, bad);
-          } else {
-            const float o = sgd_apply(acc[k], inv_b, Ws[uu[k] * F + ii[k]], A.eta, A.wd, bad);
-            Ws[uu[k] * F + ii[k]] = o;
-            Pn[w1 + static_cast<uint64_t>(u) * F + ii[k]] = o;
-          }
-        }
-      }
-      // own W2 columns
+      // own W2 columns and b2 first: they read As / W2d, whose shared region the f64
+      // X chunks of the dW1 phase reuse next
       for (uint32_t e = tid; e < C * Uo; e += kFT) {
         const uint32_t c = e / Uo, uu = e - c * Uo, u = u0 + uu;
         double acc = 0.0;
         for (uint32_t r = 0; r < R; ++r)
-          acc = dadd(acc, dmul(Z[static_cast<size_t>(r) * C + c], As[static_cast<size_t>(r) * Hs + u]));
+          acc = dadd(acc, dmul(Z[static_cast<size_t>(r) * C + c], As[static_cast<size_t>(u) * Hs + r]));
         const uint64_t g = w2 + static_cast<uint64_t>(c) * H + u;
         Pn[g] = sgd_apply(acc, inv_b, static_cast<float>(W2d[static_cast<size_t>(c) * H2 + u]), A.eta, A.wd, bad);
       }
@@ -628,6 +697,57 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
           for (uint32_t r = 0; r < R; ++r) acc = dadd(acc, Z[static_cast<size_t>(r) * C + c]);
           const uint64_t g = b2 + c;
           Pn[g] = sgd_apply(acc, inv_b, ldcg(P + g), A.eta, A.wd, bad);
+        }
+      }
+      // own b1: row-order sums of delta1 (model.cpp:218)
+      for (uint32_t uu = tid; uu < Uo; uu += kFT) {
+        double acc = 0.0;
+        for (uint32_t r = 0; r < R; ++r) acc = dadd(acc, D1[r * U + uu]);
+        const uint64_t g = b1 + u0 + uu;
+        Pn[g] = sgd_apply(acc, inv_b, ldcg(P + g), A.eta, A.wd, bad);
+      }
+      stamp(A.prof, step, 9);
+      // own W1 rows, f64 X chunks again: dW1[u,i] = sum_r delta1[r,u] * x[r,i] in row
+      // order (model.cpp:219-221), four independent chains per thread, products of row
+      // r+1 formed before the adds of row r
+      for (uint32_t c0 = 0; c0 < F; c0 += sp.CW) {
+        const uint32_t cw = F - c0 < sp.CW ? F - c0 : sp.CW;
+        __syncthreads();
+        convert_chunk(Xd, sp.CWs, Xs, Fs, R, c0, cw, sp.bulk_x && (cw % 4) == 0);
+        __syncthreads();
+        // one thread per column j: one Xd load feeds the chains of every owned unit
+        // (up to kMaxU interleaved), products of row r+1 formed before row r's adds
+        constexpr uint32_t kMaxU = 4;
+        for (uint32_t j = tid; j < cw; j += kFT) {
+          for (uint32_t ub = 0; ub < Uo; ub += kMaxU) {
+            const uint32_t nu = Uo - ub < kMaxU ? Uo - ub : kMaxU;
+            double acc[kMaxU], pc[kMaxU], pn[kMaxU];
+#pragma unroll
+            for (uint32_t k = 0; k < kMaxU; ++k) {
+              acc[k] = 0.0;
+              pc[k] = k < nu ? dmul(D1[ub + k], Xd[j]) : 0.0;
+            }
+            for (uint32_t r = 1; r < R; ++r) {
+              const double x = Xd[r * sp.CWs + j];
+#pragma unroll
+              for (uint32_t k = 0; k < kMaxU; ++k) pn[k] = k < nu ? dmul(D1[r * U + ub + k], x) : 0.0;
+#pragma unroll
+              for (uint32_t k = 0; k < kMaxU; ++k) {
+                acc[k] = dadd(acc[k], pc[k]);
+                pc[k] = pn[k];
+              }
+            }
+#pragma unroll
+            for (uint32_t k = 0; k < kMaxU; ++k) {
+              if (k >= nu) continue;
+              acc[k] = dadd(acc[k], pc[k]);
+              const uint32_t uu = ub + k, i = c0 + j;
+              const float o = sgd_apply(acc[k], inv_b, Ws[uu * F + i], A.eta, A.wd, bad);
+              Ws[uu * F + i] = o;
+              Wd[uu * F + i] = static_cast<double>(o);
+              Pn[w1 + static_cast<uint64_t>(u0 + uu) * F + i] = o;
+            }
+          }
         }
       }
     } else if (blockIdx.x == 0) {
@@ -713,7 +833,11 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
       // the exchange moved the resident rows too: refresh them from params[cur^1]
       const uint32_t nW = kHidden ? Uo * F : C * F;
       const float* src = Pn + (kHidden ? w1 + static_cast<uint64_t>(u0) * F : 0);
-      for (uint32_t e = tid; e < nW; e += kFT) Ws[e] = src[e];
+      for (uint32_t e = tid; e < nW; e += kFT) {
+        const float v = src[e];
+        Ws[e] = v;
+        if constexpr (kHidden) Wd[e] = static_cast<double>(v);
+      }
       ++xcount;
     }
     cur ^= 1;
@@ -742,22 +866,527 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
   }
 }
 
+
+// ======================================================================================
+// One-hidden-layer MLP: the persistent step kernel with f64 batch staging.
+//
+// X rows are converted to f64 ONCE per GPU per step: while the chain warps of every CTA
+// run step s's forward, its helper warps convert a 1/G share of batch s+1 (chunk-major
+// [chunk][row][CW] layout, triple-buffered in global memory so a fast CTA never
+// overwrites rows a slow CTA is still reading). Both passes that need X (the forward
+// dot products and dW1) then stream f64 chunks into shared memory with double-buffered
+// TMA bulk copies — no per-CTA F2F.F64.F32 (quarter-rate on B200) and no f32 X tile.
+// ======================================================================================
+struct MlpPlan {
+  uint32_t CW, CWs, nck, H2;  // CWs = CW + 2: padded chunk rows (bank-conflict-free row walks)
+  size_t w, wd, un, as, w2, z, e, d1, lr, rs, bars, chunk, total;
+};
+
+__host__ __device__ inline MlpPlan make_mlp_plan(uint32_t F, uint32_t H, uint32_t C, uint32_t B, uint32_t G) {
+  MlpPlan p{};
+  const uint32_t U = (H + G - 1) / G;
+  p.H2 = (H % 2) == 0 ? H + 2 : H + 1;
+  auto al = [](size_t v) { return (v + 127) & ~static_cast<size_t>(127); };
+  const size_t as_bytes = al(static_cast<size_t>(H) * B * 8);
+  const size_t w2_bytes = al(static_cast<size_t>(C) * p.H2 * 8);
+  for (uint32_t cw = 256;; cw -= 16) {
+    p.CW = cw;
+    p.CWs = cw + 2;
+    p.nck = (F + cw - 1) / cw;
+    p.chunk = al(static_cast<size_t>(B) * (cw + 2) * 8);
+    const size_t un = 2 * p.chunk > as_bytes + w2_bytes ? 2 * p.chunk : as_bytes + w2_bytes;
+    size_t off = 0;
+    p.w = off;   off = al(off + static_cast<size_t>(U) * F * 4);
+    p.wd = off;  off = al(off + static_cast<size_t>(U) * F * 8);
+    p.un = off;  p.as = off;  p.w2 = off + as_bytes;  off = al(off + un);
+    p.z = off;   off = al(off + static_cast<size_t>(B) * C * 8);
+    p.e = off;   off = al(off + static_cast<size_t>(B) * C * 8);
+    p.d1 = off;  off = al(off + static_cast<size_t>(B) * U * 8);
+    p.lr = off;  off = al(off + static_cast<size_t>(B) * 8);
+    p.rs = off;  off = al(off + static_cast<size_t>(B) * 8 * 2 + static_cast<size_t>(B) * 4 * 2);
+    p.bars = off; off = al(off + 8 * 8);
+    p.total = off;
+    if (p.total <= 212 * 1024 || cw == 16) break;
+  }
+  return p;
+}
+
+// This CTA's share of batch `idx` (R rows) converted to f64 into buffer `dst`
+// ([chunk][row][CW]); threads [t0, t0 + nthr) take part.
+__device__ __forceinline__ void convert_share(double* dst, const float* __restrict__ X, const uint32_t* idx, uint32_t R,
+                                              uint32_t F, uint32_t B, uint32_t CW, uint32_t nck, uint32_t t0,
+                                              uint32_t nthr) {
+  const uint32_t G = gridDim.x;
+  for (uint32_t q = blockIdx.x; q < R * nck; q += G) {
+    const uint32_t r = q / nck, k = q - r * nck;
+    const uint32_t c0 = k * CW, cw = F - c0 < CW ? F - c0 : CW;
+    const float* src = X + static_cast<uint64_t>(idx[r]) * F + c0;
+    double* d = dst + static_cast<size_t>(k) * B * (CW + 2) + static_cast<size_t>(r) * (CW + 2);
+    for (uint32_t j = threadIdx.x - t0; j < cw; j += nthr) d[j] = static_cast<double>(__ldg(src + j));
+  }
+}
+
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const unsigned int G = gridDim.x;
+  const uint32_t F = A.F, H = A.H, C = A.C, B = A.B;
+  const MlpPlan sp = make_mlp_plan(F, H, C, B, G);
+  const uint32_t CW = sp.CW, nck = sp.nck, H2 = sp.H2;
+  const uint32_t U = (H + G - 1) / G;
+  const uint32_t u0 = blockIdx.x * U;
+  const uint32_t Uo = u0 < H ? (u0 + U <= H ? U : H - u0) : 0;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t cwarps = (B * U + 31) / 32;  // forward chain warps (B*U <= kFT - 32)
+  const uint32_t nct = cwarps * 32;
+
+  float* Ws = reinterpret_cast<float*>(smem_raw + sp.w);     // own W1 rows f32 (the parameters)
+  double* Wd = reinterpret_cast<double*>(smem_raw + sp.wd);  // same rows as f64 (exact)
+  double* XD0 = reinterpret_cast<double*>(smem_raw + sp.un); // 2 x [B][CW] f64 chunk buffers ...
+  double* XD1 = reinterpret_cast<double*>(smem_raw + sp.un + sp.chunk);
+  double* As = reinterpret_cast<double*>(smem_raw + sp.as);  // ... time-shared with [H][B] activations
+  double* W2d = reinterpret_cast<double*>(smem_raw + sp.w2); // ... and [C][H2] W2 in f64
+  double* Z = reinterpret_cast<double*>(smem_raw + sp.z);
+  double* E = reinterpret_cast<double*>(smem_raw + sp.e);
+  double* D1 = reinterpret_cast<double*>(smem_raw + sp.d1);
+  double* Lr = reinterpret_cast<double*>(smem_raw + sp.lr);
+  double* Zmax = reinterpret_cast<double*>(smem_raw + sp.rs);
+  double* Lse = Zmax + B;
+  uint32_t* Lab = reinterpret_cast<uint32_t*>(Lse + B);
+  uint64_t* fbar = reinterpret_cast<uint64_t*>(smem_raw + sp.bars);  // forward chunks [2]
+  uint64_t* bbar = fbar + 2;                                          // dW1 chunks [2]
+  uint64_t* abar = fbar + 4;                                          // activations
+  __shared__ double s_loss;
+  __shared__ uint32_t s_bad, s_stop, s_flags;
+  __shared__ PolicyLocal s_pol;
+  __shared__ unsigned long long s_ticket;
+
+  const uint64_t w1 = 0, b1 = static_cast<uint64_t>(H) * F;
+  const uint64_t w2 = b1 + H, b2 = w2 + static_cast<uint64_t>(C) * H;
+  Slice sl;
+  sl.n = 0;
+  slice_add(sl, w1 + static_cast<uint64_t>(u0) * F, 1, Uo * F, 0);  // own W1 rows
+  slice_add(sl, b1 + u0, 1, Uo, 0);                                  // own b1
+  slice_add(sl, w2 + u0, C, Uo, H);                                  // own W2 columns
+  if (blockIdx.x == 0) slice_add(sl, b2, 1, C, 0);                   // b2
+
+  DevState* st = A.st;
+  if (tid == 0) {
+    s_pol.cum = st->cum;
+    s_pol.since = st->since;
+    s_pol.fire = 0;
+    s_pol.period = 0;
+    s_stop = st->err ? 1u : 0u;
+    for (int k = 0; k < 5; ++k) mbar_init(fbar + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (s_stop) return;
+  int cur = A.cur;
+  uint64_t xcount = 0;
+  uint32_t fph0 = 0, fph1 = 0, bph0 = 0, bph1 = 0, aph = 0;
+  const unsigned long long it0 = st->iter;
+  const size_t xb_stride = static_cast<size_t>(nck) * B * sp.CWs;
+  auto xbuf = [&](uint64_t it) { return A.xb64 + (it % 3) * xb_stride; };
+
+  // own W1 rows: resident for the whole launch (f32 and f64)
+  {
+    const float* src = A.params[cur] + w1 + static_cast<uint64_t>(u0) * F;
+    for (uint32_t e = tid; e < Uo * F; e += kFT) {
+      const float v = ldcg(src + e);
+      Ws[e] = v;
+      Wd[e] = static_cast<double>(v);
+    }
+  }
+  // prologue: the first batch in f64, visible to every CTA after one barrier
+  if (A.steps > 0) convert_share(xbuf(it0), A.X, A.plan, A.plan_rows[0], F, B, CW, nck, 0, kFT);
+  grid_barrier(A.bar, G);
+
+  for (uint64_t step = 0; step < A.steps; ++step) {
+    const uint32_t R = A.plan_rows[step];
+    const uint32_t* idx = A.plan + step * B;
+    const float* P = A.params[cur];
+    float* Pn = A.params[cur ^ 1];
+    const double inv_b = 1.0 / static_cast<double>(R);
+    const double* xb = xbuf(it0 + step);
+    stamp(A.prof, step, 0);
+    if (tid == 0) s_bad = 0;
+    if (tid < R) Lab[tid] = A.y[idx[tid]];
+
+    // ---- A: forward (chain warps) || f64 conversion of the next batch (helpers) ------
+    double* act = A.act + static_cast<size_t>(step & 1) * H * B;
+    if (warp < cwarps) {
+      auto issue = [&](uint32_t k) {
+        uint64_t* bar = fbar + (k & 1);
+        mbar_arrive_expect_tx(bar, R * sp.CWs * 8);
+        bulk_g2s((k & 1) ? XD1 : XD0, xb + static_cast<size_t>(k) * B * sp.CWs, R * sp.CWs * 8, bar);
+      };
+      if (tid == 0) {
+        fence_proxy_async();
+        issue(0);
+        if (nck > 1) issue(1);
+      }
+      const bool chain = tid < R * Uo;
+      const uint32_t cr = chain ? tid / Uo : 0, cuu = chain ? tid - cr * Uo : 0;
+      double zc = chain ? static_cast<double>(ldcg(P + b1 + u0 + cuu)) : 0.0;
+      for (uint32_t k = 0; k < nck; ++k) {
+        const uint32_t cw = F - k * CW < CW ? F - k * CW : CW;
+        if (k & 1) {
+          mbar_wait(fbar + 1, fph1);
+          fph1 ^= 1;
+        } else {
+          mbar_wait(fbar, fph0);
+          fph0 ^= 1;
+        }
+        if (k == 0) stamp(A.prof, step, 1);
+        const double* xd = ((k & 1) ? XD1 : XD0) + static_cast<size_t>(cr) * sp.CWs;
+        if (chain) zc = dot_f64_exact(zc, Wd + cuu * F + k * CW, xd, cw, (cw % 2) == 0 && (F % 2) == 0);
+        if (k + 2 < nck) {
+          named_sync(1, nct);  // both buffers' readers are the chain warps only
+          if (tid == 0) {
+            fence_proxy_async();
+            issue(k + 2);
+          }
+        }
+      }
+      if (chain) act[static_cast<size_t>(u0 + cuu) * B + cr] = tanh(zc);
+    } else if (step + 1 < A.steps) {
+      convert_share(xbuf(it0 + step + 1), A.X, idx + B, A.plan_rows[step + 1], F, B, CW, nck, nct, kFT - nct);
+    }
+    stamp(A.prof, step, 2);
+    // grid barrier; thread 0 samples the failure flags and starts the activation copy
+    __syncthreads();
+    if (tid == 0) {
+      volatile unsigned int* gen = A.bar + 1;
+      const unsigned int g = *gen;
+      __threadfence();
+      if (atomicAdd(A.bar, 1u) == G - 1) {
+        A.bar[0] = 0;
+        __threadfence();
+        atomicExch(A.bar + 1, g + 1);
+      } else {
+        while (*gen == g) __nanosleep(20);
+      }
+      __threadfence();
+      s_flags = *reinterpret_cast<volatile uint32_t*>(&st->flags);
+      fence_proxy_async();
+      if (!s_flags) {
+        const uint32_t total = H * B * 8;
+        mbar_arrive_expect_tx(abar, total);
+        for (uint32_t off = 0; off < total; off += 32768)
+          bulk_g2s(reinterpret_cast<unsigned char*>(As) + off, reinterpret_cast<const unsigned char*>(act) + off,
+                   total - off < 32768 ? total - off : 32768, abar);
+      }
+    }
+    __syncthreads();
+    stamp(A.prof, step, 3);
+    if (s_flags) {
+      if (blockIdx.x == 0 && tid == 0) {
+        st->err = s_flags;
+        st->bad_iter = it0 + step;
+      }
+      return;
+    }
+    // ---- B: W2 in f64, logits, softmax-CE ---------------------------------------------
+    for (uint32_t c = warp; c < C; c += kFT / 32) {
+      const float* src = P + w2 + static_cast<size_t>(c) * H;
+      double* dst = W2d + static_cast<size_t>(c) * H2;
+      for (uint32_t ub = 0; ub < H; ub += 8 * 32) {
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t u = ub + k * 32 + lane;
+          v[k] = u < H ? ldcg(src + u) : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t u = ub + k * 32 + lane;
+          if (u < H) dst[u] = static_cast<double>(v[k]);
+        }
+      }
+    }
+    mbar_wait(abar, aph);
+    aph ^= 1;
+    __syncthreads();
+    stamp(A.prof, step, 4);
+    {  // logits: lane == row, two classes per warp (see fused_kernel)
+      const uint32_t nwl = (C + 1) / 2 < kFT / 32 ? (C + 1) / 2 : kFT / 32;
+      for (uint32_t r0 = 0; r0 < R; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        if (warp >= nwl || r >= R) continue;
+        for (uint32_t c = warp; c < C; c += 2 * nwl) {
+          const uint32_t c2 = c + nwl;
+          const bool has2 = c2 < C;
+          const double* wa = W2d + static_cast<size_t>(c) * H2;
+          const double* wb = W2d + static_cast<size_t>(has2 ? c2 : c) * H2;
+          const double* a = As + r;
+          double za = static_cast<double>(ldcg(P + b2 + c));
+          double zb = has2 ? static_cast<double>(ldcg(P + b2 + c2)) : 0.0;
+          double pa[8], pb[8], qa[8], qb[8];
+          const uint32_t nb = H / 8;
+          auto prod = [&](uint32_t blk, double (&xa)[8], double (&xb2)[8]) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const double av = a[static_cast<size_t>(blk * 8 + k) * B];
+              xa[k] = dmul(wa[blk * 8 + k], av);
+              xb2[k] = dmul(wb[blk * 8 + k], av);
+            }
+          };
+          if (nb) {
+            prod(0, pa, pb);
+            for (uint32_t blk = 1; blk < nb; ++blk) {
+              prod(blk, qa, qb);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                za = dadd(za, pa[k]);
+                zb = dadd(zb, pb[k]);
+                pa[k] = qa[k];
+                pb[k] = qb[k];
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              za = dadd(za, pa[k]);
+              zb = dadd(zb, pb[k]);
+            }
+          }
+          for (uint32_t u = nb * 8; u < H; ++u) {
+            const double av = a[static_cast<size_t>(u) * B];
+            za = dadd(za, dmul(wa[u], av));
+            zb = dadd(zb, dmul(wb[u], av));
+          }
+          Z[static_cast<size_t>(r) * C + c] = za;
+          if (has2) Z[static_cast<size_t>(r) * C + c2] = zb;
+        }
+      }
+    }
+    __syncthreads();
+    stamp(A.prof, step, 5);
+    for (uint32_t r = tid; r < R; r += kFT) {
+      const double* z = Z + static_cast<size_t>(r) * C;
+      double zmax = z[0];
+      for (uint32_t c = 1; c < C; ++c) zmax = z[c] > zmax ? z[c] : zmax;
+      Zmax[r] = zmax;
+    }
+    __syncthreads();
+    for (uint32_t t = tid; t < R * C; t += kFT) E[t] = exp(dsub(Z[t], Zmax[t / C]));
+    __syncthreads();
+    for (uint32_t r = tid; r < R; r += kFT) {
+      const double* e = E + static_cast<size_t>(r) * C;
+      double sum = 0.0;
+      for (uint32_t c = 0; c < C; ++c) sum = dadd(sum, e[c]);
+      const double lse = dadd(Zmax[r], log(sum));
+      Lse[r] = lse;
+      const uint32_t label = Lab[r];
+      if (label >= C) {
+        atomicOr(&s_bad, DS_FLAG_LABEL_RANGE);
+        Lr[r] = 0.0;
+      } else {
+        Lr[r] = dsub(lse, Z[static_cast<size_t>(r) * C + label]);
+      }
+    }
+    __syncthreads();
+    if (tid == kFT - 1) {
+      double s = 0.0;
+      for (uint32_t r = 0; r < R; ++r) s = dadd(s, Lr[r]);
+      s_loss = dmul(s, inv_b);
+      if (!isfinite(s_loss)) atomicOr(&s_bad, DS_FLAG_LOSS_NONFINITE);
+    }
+    for (uint32_t t = tid; t < R * C; t += kFT) {
+      const uint32_t r = t / C, c = t - r * C;
+      Z[t] = dsub(exp(dsub(Z[t], Lse[r])), c == Lab[r] ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    // ---- C: backward. delta1 (chain warps) || W2 columns + b2 (next warps) ----------------
+    stamp(A.prof, step, 6);
+    uint32_t bad = 0;
+    if (tid < R * Uo) {  // delta1 (model.cpp:225-233)
+      const uint32_t r = tid / Uo, uu = tid - r * Uo, u = u0 + uu;
+      const double* d = Z + static_cast<size_t>(r) * C;
+      double p = 0.0;
+      for (uint32_t c = 0; c < C; ++c) p = dadd(p, dmul(d[c], W2d[static_cast<size_t>(c) * H2 + u]));
+      const double a = As[static_cast<size_t>(u) * B + r];
+      D1[r * U + uu] = dmul(p, dsub(1.0, dmul(a, a)));
+    } else if (tid >= nct && tid < nct + C * Uo) {  // own W2 columns (model.cpp:219-221)
+      const uint32_t e = tid - nct, c = e / Uo, uu = e - c * Uo, u = u0 + uu;
+      double acc = 0.0;
+      for (uint32_t r = 0; r < R; ++r) acc = dadd(acc, dmul(Z[static_cast<size_t>(r) * C + c], As[static_cast<size_t>(u) * B + r]));
+      const uint64_t g = w2 + static_cast<uint64_t>(c) * H + u;
+      Pn[g] = sgd_apply(acc, inv_b, static_cast<float>(W2d[static_cast<size_t>(c) * H2 + u]), A.eta, A.wd, bad);
+    } else if (blockIdx.x == 0 && tid >= nct + C * Uo && tid < nct + C * Uo + C) {  // b2
+      const uint32_t c = tid - nct - C * Uo;
+      double acc = 0.0;
+      for (uint32_t r = 0; r < R; ++r) acc = dadd(acc, Z[static_cast<size_t>(r) * C + c]);
+      const uint64_t g = b2 + c;
+      Pn[g] = sgd_apply(acc, inv_b, ldcg(P + g), A.eta, A.wd, bad);
+    }
+    __syncthreads();
+    stamp(A.prof, step, 9);
+    // ---- dW1 (+ b1): stream the f64 chunks again, one thread per column ------------------
+    {
+      auto issue = [&](uint32_t k) {
+        uint64_t* bar = bbar + (k & 1);
+        mbar_arrive_expect_tx(bar, R * sp.CWs * 8);
+        bulk_g2s((k & 1) ? XD1 : XD0, xb + static_cast<size_t>(k) * B * sp.CWs, R * sp.CWs * 8, bar);
+      };
+      if (tid == 0) {
+        fence_proxy_async();  // generic reads of As/W2d before the async overwrite
+        issue(0);
+        if (nck > 1) issue(1);
+      }
+      if (tid >= kFT - Uo) {  // own b1: row-order sums of delta1 (model.cpp:218)
+        const uint32_t uu = tid - (kFT - Uo);
+        double acc = 0.0;
+        for (uint32_t r = 0; r < R; ++r) acc = dadd(acc, D1[r * U + uu]);
+        const uint64_t g = b1 + u0 + uu;
+        Pn[g] = sgd_apply(acc, inv_b, ldcg(P + g), A.eta, A.wd, bad);
+      }
+      constexpr uint32_t kMaxU = 4;
+      for (uint32_t k = 0; k < nck; ++k) {
+        const uint32_t c0 = k * CW, cw = F - c0 < CW ? F - c0 : CW;
+        if (k & 1) {
+          mbar_wait(bbar + 1, bph1);
+          bph1 ^= 1;
+        } else {
+          mbar_wait(bbar, bph0);
+          bph0 ^= 1;
+        }
+        const double* xd = (k & 1) ? XD1 : XD0;
+        for (uint32_t j = tid; j < cw; j += kFT) {
+          for (uint32_t ub = 0; ub < Uo; ub += kMaxU) {
+            const uint32_t nu = Uo - ub < kMaxU ? Uo - ub : kMaxU;
+            double acc[kMaxU], pc[kMaxU], pn[kMaxU];
+#pragma unroll
+            for (uint32_t q = 0; q < kMaxU; ++q) {
+              acc[q] = 0.0;
+              pc[q] = q < nu ? dmul(D1[ub + q], xd[j]) : 0.0;
+            }
+            for (uint32_t r = 1; r < R; ++r) {
+              const double x = xd[static_cast<size_t>(r) * sp.CWs + j];
+#pragma unroll
+              for (uint32_t q = 0; q < kMaxU; ++q) pn[q] = q < nu ? dmul(D1[r * U + ub + q], x) : 0.0;
+#pragma unroll
+              for (uint32_t q = 0; q < kMaxU; ++q) {
+                acc[q] = dadd(acc[q], pc[q]);
+                pc[q] = pn[q];
+              }
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < kMaxU; ++q) {
+              if (q >= nu) continue;
+              acc[q] = dadd(acc[q], pc[q]);
+              const uint32_t uu = ub + q, i = c0 + j;
+              const float o = sgd_apply(acc[q], inv_b, Ws[uu * F + i], A.eta, A.wd, bad);
+              Ws[uu * F + i] = o;
+              Wd[uu * F + i] = static_cast<double>(o);
+              Pn[w1 + static_cast<uint64_t>(u0 + uu) * F + i] = o;
+            }
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && k + 2 < nck) {
+          fence_proxy_async();
+          issue(k + 2);
+        }
+      }
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && lane == 0) atomicOr(&s_bad, bad);
+    __syncthreads();
+    // ---- D: policy + exchange ------------------------------------------------------------
+    stamp(A.prof, step, 7);
+    if (s_bad && tid == 0) atomicOr(&st->flags, s_bad);  // all CTAs stop after the next barrier
+    if (tid == 0) {
+      policy_update(s_pol, s_loss, st);
+      if (blockIdx.x == 0) {
+        const unsigned long long row = it0 + step;
+        if (row < A.log.cap) {
+          A.log.loss[row] = s_loss;
+          A.log.cum[row] = s_pol.cum;
+          A.log.exchanged[row] = static_cast<uint8_t>(s_pol.fire);
+          A.log.period[row] = s_pol.period;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_pol.fire && A.has_master) {
+      uint64_t tk = kNoTicket;
+      if (A.tickets) {
+        tk = A.tickets[xcount];
+      } else if (A.ticket_src) {
+        unsigned long long* slot = reinterpret_cast<unsigned long long*>(A.bar + 4);
+        if (blockIdx.x == 0 && tid == 0) *slot = atomicAdd_system(A.ticket_src, 1ull);
+        grid_barrier(A.bar, G);
+        if (tid == 0) s_ticket = __ldcg(slot);
+        __syncthreads();
+        tk = s_ticket;
+      }
+      do_exchange(A, Pn, sl, tk, G);
+      const float* src = Pn + w1 + static_cast<uint64_t>(u0) * F;
+      for (uint32_t e = tid; e < Uo * F; e += kFT) {
+        const float v = src[e];
+        Ws[e] = v;
+        Wd[e] = static_cast<double>(v);
+      }
+      ++xcount;
+    }
+    cur ^= 1;
+    __syncthreads();
+    stamp(A.prof, step, 8);
+  }
+  grid_barrier(A.bar, G);
+  const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&st->flags);
+  if (fl) {
+    if (blockIdx.x == 0 && tid == 0) {
+      st->err = fl;
+      st->bad_iter = it0 + A.steps;
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    st->cum = s_pol.cum;
+    st->since = s_pol.since;
+    st->fire = s_pol.fire;
+    st->period = s_pol.period;
+    st->loss = s_loss;
+    st->iter = it0 + A.steps;
+    st->exchanges += xcount;
+  }
+}
+
 int grid_for(const ModelInfo& m, int device) {
   if (m.hidden.empty()) return 1;
   const uint32_t H = m.hidden[0];
   const uint32_t sms = static_cast<uint32_t>(sm_count(device));
   const uint32_t cap = H < sms ? H : sms;
-  const uint32_t U = (H + cap - 1) / cap;
+  uint32_t U = (H + cap - 1) / cap;
+  // Units per CTA: more units per CTA = fewer CTAs pulling the same batch chunks
+  // through L2 (the broadcast traffic is what bounds the X passes), at the cost of
+  // more chains per SM. DS_FUSED_UNITS overrides the default.
+  if (const char* env = std::getenv("DS_FUSED_UNITS")) {
+    const int v = std::atoi(env);
+    if (v > 0) U = static_cast<uint32_t>(v) > U ? static_cast<uint32_t>(v) : U;
+  }
   return static_cast<int>((H + U - 1) / U);
 }
 
 size_t smem_for(uint32_t F, uint32_t H, uint32_t C, uint32_t B, uint32_t G) {
-  return make_plan(F, H, C, B, G).total;
+  return H > 0 ? make_mlp_plan(F, H, C, B, G).total : make_plan(F, H, C, B, G).total;
 }
 
 }  // namespace
 
 int fused_grid(const ModelInfo& m, int device) { return grid_for(m, device); }
+
+size_t fused_xb_doubles(const ModelInfo& m, uint32_t batch, int device) {
+  if (m.hidden.empty()) return 0;
+  const MlpPlan p = make_mlp_plan(m.n_features, m.hidden[0], m.n_classes, batch,
+                                  static_cast<uint32_t>(grid_for(m, device)));
+  return 3ull * p.nck * batch * p.CWs;
+}
 
 size_t fused_smem_bytes(const ModelInfo& m, uint32_t batch) {
   const uint32_t H = m.hidden.empty() ? 0 : m.hidden[0];
@@ -772,6 +1401,14 @@ int fused_supported(const ModelInfo& m, uint32_t batch, int device, const char**
   if (batch > 1024) {
     if (why) *why = "batch_size above 1024";
     return DS_E_CONTRACT;
+  }
+  if (!m.hidden.empty()) {
+    const uint32_t G = static_cast<uint32_t>(grid_for(m, device));
+    const uint32_t U = (m.hidden[0] + G - 1) / G;
+    if (batch * U > static_cast<uint32_t>(kFT) - 64) {  // one forward chain per thread + helper warps
+      if (why) *why = "batch x hidden units per CTA exceeds the block";
+      return DS_E_CONTRACT;
+    }
   }
   const uint32_t H = m.hidden.empty() ? 0 : m.hidden[0];
   const size_t need = smem_for(m.n_features, H, m.n_classes, batch, static_cast<uint32_t>(grid_for(m, device)));
@@ -794,8 +1431,8 @@ int launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
   const size_t smem = smem_for(a.F, a.H, a.C, a.B, static_cast<uint32_t>(grid));
   void* args[] = {const_cast<FusedArgs*>(&a)};
   if (a.H > 0) {
-    DS_CUDA_TRY(cudaFuncSetAttribute(fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    DS_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fused_kernel<true>), dim3(grid), dim3(kFT), args, smem, s));
+    DS_CUDA_TRY(cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    DS_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mlp_kernel), dim3(grid), dim3(kFT), args, smem, s));
   } else {
     DS_CUDA_TRY(cudaFuncSetAttribute(fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DS_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fused_kernel<false>), dim3(1), dim3(kFT), args, smem, s));
