@@ -84,12 +84,19 @@ class ClockSampler:
         self.rows = []
 
     def __enter__(self):
+        if os.environ.get("DS_BENCH_NO_CLOCKS"):
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (NVML init) stalls the device for a moment: let it
+            # finish before the caller records its start event
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -234,6 +241,7 @@ def main():
 
     # ---- warmup, then K timed steps in one device run -----------------------------------
     W, K = max(3, args.warmup), args.steps
+    L.check(L.lib.ds_engine_reserve(eng, W + K))  # no allocation inside the timed region
     L.check(L.lib.ds_engine_run(eng, W, 0, None))
     L.check(L.lib.ds_engine_sync(eng))
     launches0 = C.c_uint64()

@@ -216,6 +216,10 @@ int ds_engine_set_tickets(ds_engine* e, const uint64_t* tickets, uint64_t count)
  * policy fires WITHOUT performing that exchange (for host ExchangeFn callbacks);
  * *ran_out (host, optional, synchronous when given) reports the iterations done. */
 int ds_engine_run(ds_engine* e, uint64_t steps, int stop_at_exchange, uint64_t* ran_out);
+/* Pre-size the engine's batch-plan and TrainLog buffers for the next `steps`
+ * iterations so a following ds_engine_run(steps) allocates nothing (no implicit
+ * device synchronisation inside a timed or latency-sensitive region). */
+int ds_engine_reserve(ds_engine* e, uint64_t steps);
 /* Host-fed iteration (a data pipeline that owns the rows, like the reference worker's
  * ShardSweeper + gather_batch, engine.cpp:25-33 / model.cpp:12-21): copies `rows`
  * gathered rows (X_host row-major, y_host) from host memory — pinned for full speed —

@@ -307,8 +307,23 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
       }
       std::vector<double> tot;
       for (uint64_t s = 3; s < steps; ++s) tot.push_back(static_cast<double>(h[s * kProfSlots] - h[(s - 1) * kProfSlots]));
+      uint64_t worst = 3;
+      double sum = 0.0, wmax = 0.0;
+      for (uint64_t s = 3; s < steps; ++s) {
+        const double d = static_cast<double>(h[s * kProfSlots] - h[(s - 1) * kProfSlots]);
+        sum += d;
+        if (d > wmax) wmax = d, worst = s - 1;
+      }
       std::sort(tot.begin(), tot.end());
-      std::fprintf(f, " step=%.0fns\n", tot.empty() ? -1.0 : tot[tot.size() / 2]);
+      std::fprintf(f, " step=%.0fns", tot.empty() ? -1.0 : tot[tot.size() / 2]);
+      if (!tot.empty())
+        std::fprintf(f, " step_mean=%.0fns step_p90=%.0fns step_max=%.0fns worst_step=%llu worst_phases:", sum / tot.size(),
+                     tot[tot.size() * 9 / 10], wmax, (unsigned long long)worst);
+      for (int k = 0; k < 10 && !tot.empty(); ++k) {
+        const unsigned long long t0 = h[worst * kProfSlots + pairs[k][0]], t1 = h[worst * kProfSlots + pairs[k][1]];
+        std::fprintf(f, " %s=%lld", names[k], static_cast<long long>(t1 - t0));
+      }
+      std::fprintf(f, "\n");
       std::fclose(f);
     }
   }
@@ -478,6 +493,14 @@ extern "C" int ds_engine_set_tickets(ds_engine* e, const uint64_t* tickets, uint
     DS_CUDA_TRY(cudaMemcpy(e->d_tickets, tickets, count * sizeof(uint64_t), cudaMemcpyHostToDevice));
   }
   e->host_exchanges = 0;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_reserve(ds_engine* e, uint64_t steps) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine: null");
+  dsb::DeviceScope ds(e->device);
+  DS_TRY(dsb::ensure_log(e, e->queued + steps));
+  if (!e->hostfed) DS_TRY(dsb::ensure_plan(e, steps));
   return DS_OK;
 }
 

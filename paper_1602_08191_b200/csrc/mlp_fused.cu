@@ -68,6 +68,15 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+// 16-byte LDGSTS (no register staging) and its completion hook on an mbarrier: the
+// arrive fires when every cp.async this thread issued so far has landed (.noinc: the
+// barrier's expected count already includes these arrivals).
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int G) {
   __syncthreads();
@@ -868,84 +877,142 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
 
 
 // ======================================================================================
-// One-hidden-layer MLP: the persistent step kernel with f64 batch staging.
+// One-hidden-layer MLP: the persistent step kernel.
 //
-// X rows are converted to f64 ONCE per GPU per step: while the chain warps of every CTA
-// run step s's forward, its helper warps convert a 1/G share of batch s+1 (chunk-major
-// [chunk][row][CW] layout, triple-buffered in global memory so a fast CTA never
-// overwrites rows a slow CTA is still reading). Both passes that need X (the forward
-// dot products and dW1) then stream f64 chunks into shared memory with double-buffered
-// TMA bulk copies — no per-CTA F2F.F64.F32 (quarter-rate on B200) and no f32 X tile.
+// Per iteration the batch rows land once in shared memory as f32 (TMA bulk copies, the
+// next batch prefetched into L2). Both passes that need X in f64 — the forward dot
+// products and dW1 — run as producer/consumer pipelines inside the CTA: producer warps
+// convert 128-column chunks to f64 (F2F.F64.F32 is quarter-rate on B200, so each
+// element is converted once per pass, off the consumers' critical path) into a double
+// buffer while consumer warps run the reference-order chains on the previous chunk;
+// named barriers (bar.sync / bar.arrive) hand the buffers back and forth.
 // ======================================================================================
 struct MlpPlan {
-  uint32_t CW, CWs, nck, H2;  // CWs = CW + 2: padded chunk rows (bank-conflict-free row walks)
-  size_t w, wd, un, as, w2, z, e, d1, lr, rs, bars, chunk, total;
+  uint32_t Fs, Fd, CW, CWs, nck, H2;
+  size_t xs, w, wd, un, as, w2, z, e, d1, lr, rs, bars, chunk, total;
 };
 
 __host__ __device__ inline MlpPlan make_mlp_plan(uint32_t F, uint32_t H, uint32_t C, uint32_t B, uint32_t G) {
   MlpPlan p{};
   const uint32_t U = (H + G - 1) / G;
+  p.Fs = (F % 4) == 0 ? F + 4 : (F | 1u);  // f32 rows: 16-byte multiple for TMA and float4
+  p.Fd = F + ((F % 2) == 0 ? 2 : 1);        // f64 W1 rows: shifted banks between units
   p.H2 = (H % 2) == 0 ? H + 2 : H + 1;
   auto al = [](size_t v) { return (v + 127) & ~static_cast<size_t>(127); };
   const size_t as_bytes = al(static_cast<size_t>(H) * B * 8);
   const size_t w2_bytes = al(static_cast<size_t>(C) * p.H2 * 8);
-  for (uint32_t cw = 256;; cw -= 16) {
+  for (uint32_t cw = 128;; cw -= 16) {
     p.CW = cw;
     p.CWs = cw + 2;
     p.nck = (F + cw - 1) / cw;
-    p.chunk = al(static_cast<size_t>(B) * (cw + 2) * 8);
+    p.chunk = al(static_cast<size_t>(B) * p.CWs * 8);
     const size_t un = 2 * p.chunk > as_bytes + w2_bytes ? 2 * p.chunk : as_bytes + w2_bytes;
     size_t off = 0;
+    p.xs = off;  off = al(off + static_cast<size_t>(B) * p.Fs * 4);
     p.w = off;   off = al(off + static_cast<size_t>(U) * F * 4);
-    p.wd = off;  off = al(off + static_cast<size_t>(U) * F * 8);
+    p.wd = off;  off = al(off + static_cast<size_t>(U) * p.Fd * 8);
     p.un = off;  p.as = off;  p.w2 = off + as_bytes;  off = al(off + un);
     p.z = off;   off = al(off + static_cast<size_t>(B) * C * 8);
     p.e = off;   off = al(off + static_cast<size_t>(B) * C * 8);
     p.d1 = off;  off = al(off + static_cast<size_t>(B) * U * 8);
     p.lr = off;  off = al(off + static_cast<size_t>(B) * 8);
     p.rs = off;  off = al(off + static_cast<size_t>(B) * 8 * 2 + static_cast<size_t>(B) * 4 * 2);
-    p.bars = off; off = al(off + 8 * 8);
+    p.bars = off; off = al(off + 8 * (p.nck + 2));
     p.total = off;
-    if (p.total <= 212 * 1024 || cw == 16) break;
+    if (p.total <= 216 * 1024 || cw == 16) break;
   }
   return p;
-}
-
-// This CTA's share of batch `idx` (R rows) converted to f64 into buffer `dst`
-// ([chunk][row][CW]); threads [t0, t0 + nthr) take part.
-__device__ __forceinline__ void convert_share(double* dst, const float* __restrict__ X, const uint32_t* idx, uint32_t R,
-                                              uint32_t F, uint32_t B, uint32_t CW, uint32_t nck, uint32_t t0,
-                                              uint32_t nthr) {
-  const uint32_t G = gridDim.x;
-  for (uint32_t q = blockIdx.x; q < R * nck; q += G) {
-    const uint32_t r = q / nck, k = q - r * nck;
-    const uint32_t c0 = k * CW, cw = F - c0 < CW ? F - c0 : CW;
-    const float* src = X + static_cast<uint64_t>(idx[r]) * F + c0;
-    double* d = dst + static_cast<size_t>(k) * B * (CW + 2) + static_cast<size_t>(r) * (CW + 2);
-    for (uint32_t j = threadIdx.x - t0; j < cw; j += nthr) d[j] = static_cast<double>(__ldg(src + j));
-  }
 }
 
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Producer side of one chunk: rows R of Xs columns [c0, c0+cw) -> dst (f64, row stride
+// CWs). Warps [w0, w0+nw) take rows round-robin, lanes take column pairs (LDS.64 in,
+// STS.128 out: both at the shared-memory wavefront minimum).
+__device__ __forceinline__ void produce_chunk(double* dst, uint32_t CWs, const float* Xs, uint32_t Fs, uint32_t R,
+                                              uint32_t c0, uint32_t cw, bool vec, uint32_t w0, uint32_t nw) {
+  const uint32_t warp = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+  for (uint32_t r = warp; r < R; r += nw) {
+    const float* src = Xs + static_cast<size_t>(r) * Fs + c0;
+    double* d = dst + static_cast<size_t>(r) * CWs;
+    if (vec) {
+      const float2* s2 = reinterpret_cast<const float2*>(src);
+      double2* d2 = reinterpret_cast<double2*>(d);
+#pragma unroll 2
+      for (uint32_t q = lane; q < cw / 2; q += 32) {
+        const float2 v = s2[q];
+        d2[q] = make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
+      }
+    } else {
+      for (uint32_t j = lane; j < cw; j += 32) d[j] = static_cast<double>(src[j]);
+    }
+  }
+}
+
+// dW1 for NU units [ub, ub+NU) of this CTA: thread tid owns columns j = tid + k*kFT.
+// Rows are unrolled by 4 with the loads of the next group issued before the current
+// group's chain adds (in-order issue would otherwise expose the LDS latency per row).
+template <int NU>
+__device__ __forceinline__ void dw1_columns(const FusedArgs& A, const float* Xs, uint32_t Fs, const double* D1,
+                                            uint32_t U, uint32_t ub, uint32_t u0, uint32_t R, double inv_b,
+                                            float* Ws, double* Wd, uint32_t Fd, float* Pn, uint64_t w1,
+                                            uint32_t& bad) {
+  const uint32_t F = A.F;
+  for (uint32_t j = threadIdx.x; j < F; j += kFT) {
+    double acc[NU];
+#pragma unroll
+    for (int q = 0; q < NU; ++q) acc[q] = 0.0;
+    const float* xc = Xs + j;
+    uint32_t r = 0;
+    for (; r + 4 <= R; r += 4) {
+      double x[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) x[t] = static_cast<double>(xc[static_cast<size_t>(r + t) * Fs]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int q = 0; q < NU; ++q) acc[q] = dadd(acc[q], dmul(D1[(r + t) * U + ub + q], x[t]));
+    }
+    for (; r < R; ++r) {
+      const double x = static_cast<double>(xc[static_cast<size_t>(r) * Fs]);
+#pragma unroll
+      for (int q = 0; q < NU; ++q) acc[q] = dadd(acc[q], dmul(D1[r * U + ub + q], x));
+    }
+#pragma unroll
+    for (int q = 0; q < NU; ++q) {
+      const uint32_t uu = ub + q;
+      const float o = sgd_apply(acc[q], inv_b, Ws[uu * F + j], A.eta, A.wd, bad);
+      Ws[uu * F + j] = o;
+      Wd[uu * Fd + j] = static_cast<double>(o);
+      Pn[w1 + static_cast<uint64_t>(u0 + uu) * F + j] = o;
+    }
+  }
+}
+
+constexpr uint32_t kBarFull = 2, kBarEmpty = 4;  // named barrier ids (+ buffer index)
 
 __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const unsigned int G = gridDim.x;
   const uint32_t F = A.F, H = A.H, C = A.C, B = A.B;
   const MlpPlan sp = make_mlp_plan(F, H, C, B, G);
-  const uint32_t CW = sp.CW, nck = sp.nck, H2 = sp.H2;
+  const uint32_t CW = sp.CW, CWs = sp.CWs, nck = sp.nck, H2 = sp.H2, Fs = sp.Fs, Fd = sp.Fd;
   const uint32_t U = (H + G - 1) / G;
   const uint32_t u0 = blockIdx.x * U;
   const uint32_t Uo = u0 < H ? (u0 + U <= H ? U : H - u0) : 0;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t cwarps = (B * U + 31) / 32;  // forward chain warps (B*U <= kFT - 32)
-  const uint32_t nct = cwarps * 32;
+  const uint32_t cwarps = (B * U + 31) / 32;  // forward consumer (chain) warps
+  const bool vecx = (F % 4) == 0 && (CW % 4) == 0;
 
+  float* Xs = reinterpret_cast<float*>(smem_raw + sp.xs);    // B x Fs batch rows (f32)
   float* Ws = reinterpret_cast<float*>(smem_raw + sp.w);     // own W1 rows f32 (the parameters)
-  double* Wd = reinterpret_cast<double*>(smem_raw + sp.wd);  // same rows as f64 (exact)
-  double* XD0 = reinterpret_cast<double*>(smem_raw + sp.un); // 2 x [B][CW] f64 chunk buffers ...
+  double* Wd = reinterpret_cast<double*>(smem_raw + sp.wd);  // same rows as f64, row stride Fd
+  double* XD0 = reinterpret_cast<double*>(smem_raw + sp.un); // 2 x [B][CWs] f64 chunk buffers ...
   double* XD1 = reinterpret_cast<double*>(smem_raw + sp.un + sp.chunk);
   double* As = reinterpret_cast<double*>(smem_raw + sp.as);  // ... time-shared with [H][B] activations
   double* W2d = reinterpret_cast<double*>(smem_raw + sp.w2); // ... and [C][H2] W2 in f64
@@ -956,9 +1023,8 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   double* Zmax = reinterpret_cast<double*>(smem_raw + sp.rs);
   double* Lse = Zmax + B;
   uint32_t* Lab = reinterpret_cast<uint32_t*>(Lse + B);
-  uint64_t* fbar = reinterpret_cast<uint64_t*>(smem_raw + sp.bars);  // forward chunks [2]
-  uint64_t* bbar = fbar + 2;                                          // dW1 chunks [2]
-  uint64_t* abar = fbar + 4;                                          // activations
+  uint64_t* abar = reinterpret_cast<uint64_t*>(smem_raw + sp.bars);  // activations
+  uint64_t* xbar = abar + 1;  // [nck]: column chunk k of the batch rows landed
   __shared__ double s_loss;
   __shared__ uint32_t s_bad, s_stop, s_flags;
   __shared__ PolicyLocal s_pol;
@@ -980,30 +1046,45 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     s_pol.fire = 0;
     s_pol.period = 0;
     s_stop = st->err ? 1u : 0u;
-    for (int k = 0; k < 5; ++k) mbar_init(fbar + k, 1);
+    for (uint32_t k = 0; k < nck; ++k) mbar_init(xbar + k, kFT);
+    mbar_init(abar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (s_stop) return;
   int cur = A.cur;
   uint64_t xcount = 0;
-  uint32_t fph0 = 0, fph1 = 0, bph0 = 0, bph1 = 0, aph = 0;
+  uint32_t xph = 0, aph = 0;
   const unsigned long long it0 = st->iter;
-  const size_t xb_stride = static_cast<size_t>(nck) * B * sp.CWs;
-  auto xbuf = [&](uint64_t it) { return A.xb64 + (it % 3) * xb_stride; };
 
-  // own W1 rows: resident for the whole launch (f32 and f64)
-  {
-    const float* src = A.params[cur] + w1 + static_cast<uint64_t>(u0) * F;
-    for (uint32_t e = tid; e < Uo * F; e += kFT) {
-      const float v = ldcg(src + e);
-      Ws[e] = v;
-      Wd[e] = static_cast<double>(v);
+  auto load_own_rows = [&](const float* P0) {  // Ws / Wd <- own W1 rows
+    const float* src = P0 + w1 + static_cast<uint64_t>(u0) * F;
+    for (uint32_t uu = warp; uu < Uo; uu += kFT / 32)
+      for (uint32_t i = lane; i < F; i += 32) {
+        const float v = ldcg(src + static_cast<size_t>(uu) * F + i);
+        Ws[uu * F + i] = v;
+        Wd[uu * Fd + i] = static_cast<double>(v);
+      }
+  };
+  // Batch rows -> Xs, column-chunk-major so the forward starts on chunk 0 while the rest
+  // lands: every thread issues 16-byte LDGSTS pieces, then arrives on chunk k's barrier.
+  // (One bulk copy per row-chunk would put ~R*nck serialized TMA issues on one warp.)
+  // The caller has synced the block since the last generic access of Xs.
+  auto issue_x = [&](uint64_t s) {
+    const uint32_t R = A.plan_rows[s];
+    const uint32_t* idx = A.plan + s * B;
+    for (uint32_t k = 0; k < nck; ++k) {
+      const uint32_t cw = F - k * CW < CW ? F - k * CW : CW, pr = cw / 4;
+      for (uint32_t p = tid; p < R * pr; p += kFT) {
+        const uint32_t r = p / pr, c = k * CW + 4 * (p - r * pr);
+        cp_async16(Xs + static_cast<size_t>(r) * Fs + c, A.X + static_cast<uint64_t>(__ldg(idx + r)) * F + c);
+      }
+      cp_async_arrive(xbar + k);
     }
-  }
-  // prologue: the first batch in f64, visible to every CTA after one barrier
-  if (A.steps > 0) convert_share(xbuf(it0), A.X, A.plan, A.plan_rows[0], F, B, CW, nck, 0, kFT);
-  grid_barrier(A.bar, G);
+  };
+  load_own_rows(A.params[cur]);
+  __syncthreads();
+  if (vecx && A.steps > 0) issue_x(0);
 
   for (uint64_t step = 0; step < A.steps; ++step) {
     const uint32_t R = A.plan_rows[step];
@@ -1011,51 +1092,43 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     const float* P = A.params[cur];
     float* Pn = A.params[cur ^ 1];
     const double inv_b = 1.0 / static_cast<double>(R);
-    const double* xb = xbuf(it0 + step);
     stamp(A.prof, step, 0);
     if (tid == 0) s_bad = 0;
     if (tid < R) Lab[tid] = A.y[idx[tid]];
 
-    // ---- A: forward (chain warps) || f64 conversion of the next batch (helpers) ------
+    // ---- A: batch rows (TMA issued at the end of the previous step; generic path here) --
+    if (!vecx) {
+      __syncthreads();
+      for (uint32_t r = warp; r < R; r += kFT / 32)
+        for (uint32_t i = lane; i < F; i += 32) Xs[static_cast<size_t>(r) * Fs + i] = __ldg(A.X + static_cast<uint64_t>(idx[r]) * F + i);
+      __syncthreads();
+    }
+    stamp(A.prof, step, 1);
+
+    // ---- forward: consumers (chain warps) || producers (f64 chunk conversion) -----------
     double* act = A.act + static_cast<size_t>(step & 1) * H * B;
     if (warp < cwarps) {
-      auto issue = [&](uint32_t k) {
-        uint64_t* bar = fbar + (k & 1);
-        mbar_arrive_expect_tx(bar, R * sp.CWs * 8);
-        bulk_g2s((k & 1) ? XD1 : XD0, xb + static_cast<size_t>(k) * B * sp.CWs, R * sp.CWs * 8, bar);
-      };
-      if (tid == 0) {
-        fence_proxy_async();
-        issue(0);
-        if (nck > 1) issue(1);
-      }
       const bool chain = tid < R * Uo;
       const uint32_t cr = chain ? tid / Uo : 0, cuu = chain ? tid - cr * Uo : 0;
       double zc = chain ? static_cast<double>(ldcg(P + b1 + u0 + cuu)) : 0.0;
       for (uint32_t k = 0; k < nck; ++k) {
-        const uint32_t cw = F - k * CW < CW ? F - k * CW : CW;
-        if (k & 1) {
-          mbar_wait(fbar + 1, fph1);
-          fph1 ^= 1;
-        } else {
-          mbar_wait(fbar, fph0);
-          fph0 ^= 1;
-        }
-        if (k == 0) stamp(A.prof, step, 1);
-        const double* xd = ((k & 1) ? XD1 : XD0) + static_cast<size_t>(cr) * sp.CWs;
-        if (chain) zc = dot_f64_exact(zc, Wd + cuu * F + k * CW, xd, cw, (cw % 2) == 0 && (F % 2) == 0);
-        if (k + 2 < nck) {
-          named_sync(1, nct);  // both buffers' readers are the chain warps only
-          if (tid == 0) {
-            fence_proxy_async();
-            issue(k + 2);
-          }
-        }
+        const uint32_t b = k & 1, cw = F - k * CW < CW ? F - k * CW : CW;
+        named_sync(kBarFull + b, kFT);
+        const double* xd = (b ? XD1 : XD0) + static_cast<size_t>(cr) * CWs;
+        if (chain) zc = dot_f64_exact(zc, Wd + cuu * Fd + k * CW, xd, cw, (cw % 2) == 0);
+        if (k + 2 < nck) named_arrive(kBarEmpty + b, kFT);
       }
       if (chain) act[static_cast<size_t>(u0 + cuu) * B + cr] = tanh(zc);
-    } else if (step + 1 < A.steps) {
-      convert_share(xbuf(it0 + step + 1), A.X, idx + B, A.plan_rows[step + 1], F, B, CW, nck, nct, kFT - nct);
+    } else {
+      for (uint32_t k = 0; k < nck; ++k) {
+        const uint32_t b = k & 1, c0 = k * CW, cw = F - c0 < CW ? F - c0 : CW;
+        if (k >= 2) named_sync(kBarEmpty + b, kFT);
+        if (vecx) mbar_wait(xbar + k, xph);
+        produce_chunk(b ? XD1 : XD0, CWs, Xs, Fs, R, c0, cw, vecx, cwarps, kFT / 32 - cwarps);
+        named_arrive(kBarFull + b, kFT);
+      }
     }
+    xph ^= 1;
     stamp(A.prof, step, 2);
     // grid barrier; thread 0 samples the failure flags and starts the activation copy
     __syncthreads();
@@ -1112,7 +1185,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     aph ^= 1;
     __syncthreads();
     stamp(A.prof, step, 4);
-    {  // logits: lane == row, two classes per warp (see fused_kernel)
+    {  // logits: lane == row, two classes per warp (two interleaved chains)
       const uint32_t nwl = (C + 1) / 2 < kFT / 32 ? (C + 1) / 2 : kFT / 32;
       for (uint32_t r0 = 0; r0 < R; r0 += 32) {
         const uint32_t r = r0 + lane;
@@ -1128,11 +1201,27 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
           double pa[8], pb[8], qa[8], qb[8];
           const uint32_t nb = H / 8;
           auto prod = [&](uint32_t blk, double (&xa)[8], double (&xb2)[8]) {
+            double2 w2a[4], w2b[4];
+            if ((H2 % 2) == 0) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                w2a[k] = reinterpret_cast<const double2*>(wa)[blk * 4 + k];
+                w2b[k] = reinterpret_cast<const double2*>(wb)[blk * 4 + k];
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                w2a[k] = make_double2(wa[blk * 8 + 2 * k], wa[blk * 8 + 2 * k + 1]);
+                w2b[k] = make_double2(wb[blk * 8 + 2 * k], wb[blk * 8 + 2 * k + 1]);
+              }
+            }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const double av = a[static_cast<size_t>(blk * 8 + k) * B];
-              xa[k] = dmul(wa[blk * 8 + k], av);
-              xb2[k] = dmul(wb[blk * 8 + k], av);
+              const double wva = (k & 1) ? w2a[k >> 1].y : w2a[k >> 1].x;
+              const double wvb = (k & 1) ? w2b[k >> 1].y : w2b[k >> 1].x;
+              xa[k] = dmul(wva, av);
+              xb2[k] = dmul(wvb, av);
             }
           };
           if (nb) {
@@ -1200,9 +1289,10 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
       Z[t] = dsub(exp(dsub(Z[t], Lse[r])), c == Lab[r] ? 1.0 : 0.0);
     }
     __syncthreads();
-    // ---- C: backward. delta1 (chain warps) || W2 columns + b2 (next warps) ----------------
+    // ---- C: backward. delta1 || W2 columns + b2 (different warps) ---------------------------
     stamp(A.prof, step, 6);
     uint32_t bad = 0;
+    const uint32_t nct = cwarps * 32;
     if (tid < R * Uo) {  // delta1 (model.cpp:225-233)
       const uint32_t r = tid / Uo, uu = tid - r * Uo, u = u0 + uu;
       const double* d = Z + static_cast<size_t>(r) * C;
@@ -1213,7 +1303,8 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     } else if (tid >= nct && tid < nct + C * Uo) {  // own W2 columns (model.cpp:219-221)
       const uint32_t e = tid - nct, c = e / Uo, uu = e - c * Uo, u = u0 + uu;
       double acc = 0.0;
-      for (uint32_t r = 0; r < R; ++r) acc = dadd(acc, dmul(Z[static_cast<size_t>(r) * C + c], As[static_cast<size_t>(u) * B + r]));
+      for (uint32_t r = 0; r < R; ++r)
+        acc = dadd(acc, dmul(Z[static_cast<size_t>(r) * C + c], As[static_cast<size_t>(u) * B + r]));
       const uint64_t g = w2 + static_cast<uint64_t>(c) * H + u;
       Pn[g] = sgd_apply(acc, inv_b, static_cast<float>(W2d[static_cast<size_t>(c) * H2 + u]), A.eta, A.wd, bad);
     } else if (blockIdx.x == 0 && tid >= nct + C * Uo && tid < nct + C * Uo + C) {  // b2
@@ -1225,77 +1316,29 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     }
     __syncthreads();
     stamp(A.prof, step, 9);
-    // ---- dW1 (+ b1): stream the f64 chunks again, one thread per column ------------------
-    {
-      auto issue = [&](uint32_t k) {
-        uint64_t* bar = bbar + (k & 1);
-        mbar_arrive_expect_tx(bar, R * sp.CWs * 8);
-        bulk_g2s((k & 1) ? XD1 : XD0, xb + static_cast<size_t>(k) * B * sp.CWs, R * sp.CWs * 8, bar);
-      };
-      if (tid == 0) {
-        fence_proxy_async();  // generic reads of As/W2d before the async overwrite
-        issue(0);
-        if (nck > 1) issue(1);
-      }
-      if (tid >= kFT - Uo) {  // own b1: row-order sums of delta1 (model.cpp:218)
-        const uint32_t uu = tid - (kFT - Uo);
-        double acc = 0.0;
-        for (uint32_t r = 0; r < R; ++r) acc = dadd(acc, D1[r * U + uu]);
-        const uint64_t g = b1 + u0 + uu;
-        Pn[g] = sgd_apply(acc, inv_b, ldcg(P + g), A.eta, A.wd, bad);
-      }
-      constexpr uint32_t kMaxU = 4;
-      for (uint32_t k = 0; k < nck; ++k) {
-        const uint32_t c0 = k * CW, cw = F - c0 < CW ? F - c0 : CW;
-        if (k & 1) {
-          mbar_wait(bbar + 1, bph1);
-          bph1 ^= 1;
-        } else {
-          mbar_wait(bbar, bph0);
-          bph0 ^= 1;
-        }
-        const double* xd = (k & 1) ? XD1 : XD0;
-        for (uint32_t j = tid; j < cw; j += kFT) {
-          for (uint32_t ub = 0; ub < Uo; ub += kMaxU) {
-            const uint32_t nu = Uo - ub < kMaxU ? Uo - ub : kMaxU;
-            double acc[kMaxU], pc[kMaxU], pn[kMaxU];
-#pragma unroll
-            for (uint32_t q = 0; q < kMaxU; ++q) {
-              acc[q] = 0.0;
-              pc[q] = q < nu ? dmul(D1[ub + q], xd[j]) : 0.0;
-            }
-            for (uint32_t r = 1; r < R; ++r) {
-              const double x = xd[static_cast<size_t>(r) * sp.CWs + j];
-#pragma unroll
-              for (uint32_t q = 0; q < kMaxU; ++q) pn[q] = q < nu ? dmul(D1[r * U + ub + q], x) : 0.0;
-#pragma unroll
-              for (uint32_t q = 0; q < kMaxU; ++q) {
-                acc[q] = dadd(acc[q], pc[q]);
-                pc[q] = pn[q];
-              }
-            }
-#pragma unroll
-            for (uint32_t q = 0; q < kMaxU; ++q) {
-              if (q >= nu) continue;
-              acc[q] = dadd(acc[q], pc[q]);
-              const uint32_t uu = ub + q, i = c0 + j;
-              const float o = sgd_apply(acc[q], inv_b, Ws[uu * F + i], A.eta, A.wd, bad);
-              Ws[uu * F + i] = o;
-              Wd[uu * F + i] = static_cast<double>(o);
-              Pn[w1 + static_cast<uint64_t>(u0 + uu) * F + i] = o;
-            }
-          }
-        }
-        __syncthreads();
-        if (tid == 0 && k + 2 < nck) {
-          fence_proxy_async();
-          issue(k + 2);
-        }
+    // ---- dW1 (+ b1): every thread owns whole columns j (all rows, its CTA's units) -----
+    // Each X element is converted to f64 once, by the one thread that uses it for all
+    // units; the row order of the sums is the reference's (model.cpp:219-221).
+    if (tid >= kFT - Uo) {  // own b1: row-order sums of delta1
+      const uint32_t uu = tid - (kFT - Uo);
+      double acc = 0.0;
+      for (uint32_t r = 0; r < R; ++r) acc = dadd(acc, D1[r * U + uu]);
+      const uint64_t g = b1 + u0 + uu;
+      Pn[g] = sgd_apply(acc, inv_b, ldcg(P + g), A.eta, A.wd, bad);
+    }
+    for (uint32_t ub = 0; ub < Uo; ub += 4) {
+      const uint32_t nu = Uo - ub < 4 ? Uo - ub : 4;
+      switch (nu) {
+        case 1: dw1_columns<1>(A, Xs, Fs, D1, U, ub, u0, R, inv_b, Ws, Wd, Fd, Pn, w1, bad); break;
+        case 2: dw1_columns<2>(A, Xs, Fs, D1, U, ub, u0, R, inv_b, Ws, Wd, Fd, Pn, w1, bad); break;
+        case 3: dw1_columns<3>(A, Xs, Fs, D1, U, ub, u0, R, inv_b, Ws, Wd, Fd, Pn, w1, bad); break;
+        default: dw1_columns<4>(A, Xs, Fs, D1, U, ub, u0, R, inv_b, Ws, Wd, Fd, Pn, w1, bad); break;
       }
     }
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) atomicOr(&s_bad, bad);
     __syncthreads();
+    if (vecx && step + 1 < A.steps) issue_x(step + 1);  // Xs is free: overlap the exchange
     // ---- D: policy + exchange ------------------------------------------------------------
     stamp(A.prof, step, 7);
     if (s_bad && tid == 0) atomicOr(&st->flags, s_bad);  // all CTAs stop after the next barrier
@@ -1325,12 +1368,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
         tk = s_ticket;
       }
       do_exchange(A, Pn, sl, tk, G);
-      const float* src = Pn + w1 + static_cast<uint64_t>(u0) * F;
-      for (uint32_t e = tid; e < Uo * F; e += kFT) {
-        const float v = src[e];
-        Ws[e] = v;
-        Wd[e] = static_cast<double>(v);
-      }
+      load_own_rows(Pn);  // the exchange moved the resident rows too
       ++xcount;
     }
     cur ^= 1;
@@ -1381,12 +1419,7 @@ size_t smem_for(uint32_t F, uint32_t H, uint32_t C, uint32_t B, uint32_t G) {
 
 int fused_grid(const ModelInfo& m, int device) { return grid_for(m, device); }
 
-size_t fused_xb_doubles(const ModelInfo& m, uint32_t batch, int device) {
-  if (m.hidden.empty()) return 0;
-  const MlpPlan p = make_mlp_plan(m.n_features, m.hidden[0], m.n_classes, batch,
-                                  static_cast<uint32_t>(grid_for(m, device)));
-  return 3ull * p.nck * batch * p.CWs;
-}
+size_t fused_xb_doubles(const ModelInfo&, uint32_t, int) { return 0; }  // X stays f32 in shared memory
 
 size_t fused_smem_bytes(const ModelInfo& m, uint32_t batch) {
   const uint32_t H = m.hidden.empty() ? 0 : m.hidden[0];
@@ -1405,7 +1438,7 @@ int fused_supported(const ModelInfo& m, uint32_t batch, int device, const char**
   if (!m.hidden.empty()) {
     const uint32_t G = static_cast<uint32_t>(grid_for(m, device));
     const uint32_t U = (m.hidden[0] + G - 1) / G;
-    if (batch * U > static_cast<uint32_t>(kFT) - 64) {  // one forward chain per thread + helper warps
+    if (batch * U > static_cast<uint32_t>(kFT) - 128) {  // one forward chain per thread + producer warps
       if (why) *why = "batch x hidden units per CTA exceeds the block";
       return DS_E_CONTRACT;
     }
