@@ -280,14 +280,17 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
   // DS_FUSED_PROFILE=<file>: per-phase globaltimer stamps of CTA 0, medians appended
   const char* prof_path = std::getenv("DS_FUSED_PROFILE");
   unsigned long long* prof = nullptr;
-  if (prof_path && steps >= 8) DS_CUDA_TRY(cudaMalloc(&prof, steps * kProfSlots * sizeof(unsigned long long)));
-  if (prof) DS_CUDA_TRY(cudaMemsetAsync(prof, 0, steps * kProfSlots * sizeof(unsigned long long), e->stream));
+  const uint64_t G = static_cast<uint64_t>(e->fused_grid);
+  const uint64_t prof_n = steps * (kProfSlots + 2 * G);
+  if (prof_path && steps >= 8) DS_CUDA_TRY(cudaMalloc(&prof, prof_n * sizeof(unsigned long long)));
+  if (prof) DS_CUDA_TRY(cudaMemsetAsync(prof, 0, prof_n * sizeof(unsigned long long), e->stream));
   a.prof = prof;
+  a.prof_cta = prof ? prof + steps * kProfSlots : nullptr;
   DS_TRY(launch_fused(a, e->fused_grid, e->stream));
   e->launches += 1;
   e->cur ^= static_cast<int>(steps & 1);
   if (prof) {
-    std::vector<unsigned long long> h(steps * kProfSlots);
+    std::vector<unsigned long long> h(prof_n);
     DS_CUDA_TRY(cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream));
     DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
     cudaFree(prof);
@@ -322,6 +325,26 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
       for (int k = 0; k < 10 && !tot.empty(); ++k) {
         const unsigned long long t0 = h[worst * kProfSlots + pairs[k][0]], t1 = h[worst * kProfSlots + pairs[k][1]];
         std::fprintf(f, " %s=%lld", names[k], static_cast<long long>(t1 - t0));
+      }
+      {  // grid-barrier anatomy: CTA skew at the forward's end vs the barrier itself
+        std::vector<double> skew, mech;
+        const unsigned long long* hc = h.data() + steps * kProfSlots;
+        for (uint64_t s = 2; s < steps; ++s) {
+          unsigned long long lo = ~0ull, hi = 0, exit0 = hc[(s * G) * 2 + 1];
+          for (uint64_t g = 0; g < G; ++g) {
+            const unsigned long long t = hc[(s * G + g) * 2];
+            lo = t < lo ? t : lo;
+            hi = t > hi ? t : hi;
+          }
+          if (lo && exit0 >= hi) {
+            skew.push_back(static_cast<double>(hi - lo));
+            mech.push_back(static_cast<double>(exit0 - hi));
+          }
+        }
+        std::sort(skew.begin(), skew.end());
+        std::sort(mech.begin(), mech.end());
+        if (!skew.empty())
+          std::fprintf(f, " | fwd_end_skew=%.0fns barrier_after_last=%.0fns", skew[skew.size() / 2], mech[mech.size() / 2]);
       }
       std::fprintf(f, "\n");
       std::fclose(f);

@@ -64,6 +64,7 @@ struct FusedArgs {
   int stop_at_exchange;
   unsigned int* bar;          // grid barrier words [2]
   unsigned long long* prof;   // optional: kProfSlots globaltimer stamps per step (CTA 0)
+  unsigned long long* prof_cta;  // optional: [step][CTA][2] forward-done / grid-barrier-exit stamps
 };
 
 constexpr int kProfSlots = 10;

@@ -78,27 +78,37 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int G) {
+// Grid-wide barrier over a monotonic arrival counter (zeroed before each launch, see
+// launch_fused): the k-th barrier of a launch completes when the counter reaches k*G.
+// One release-add per CTA after the CTA barrier (cumulative over the CTA's writes) and
+// acquire polling; no reset, no generation flag, no full fences. `nbar` is the calling
+// kernel's __shared__ barrier count (touched by thread 0 only).
+constexpr int kBarCounter = 32;  // word of A.bar holding the counter (own 128-byte line)
+__device__ __forceinline__ void grid_arrive_wait(unsigned int* bar, unsigned int& nbar, unsigned int G) {
+  unsigned int* ctr = bar + kBarCounter;
+  const unsigned int target = (++nbar) * G;
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+  unsigned int v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  } while (static_cast<int>(v - target) < 0);
+}
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& nbar, unsigned int G) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int* gen = bar + 1;
-    const unsigned int g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == G - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicExch(bar + 1, g + 1);
-    } else {
-      while (*gen == g) __nanosleep(20);
-    }
-    __threadfence();
-  }
+  if (threadIdx.x == 0) grid_arrive_wait(bar, nbar, G);
   __syncthreads();
 }
 
 __device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
 
 // Optional phase timestamps (CTA 0, thread 0) for DS_FUSED_PROFILE runs.
+__device__ __forceinline__ void stamp_cta(unsigned long long* prof_cta, uint64_t step, int slot) {
+  if (prof_cta && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    prof_cta[(step * gridDim.x + blockIdx.x) * 2 + slot] = t;
+  }
+}
 __device__ __forceinline__ void stamp(unsigned long long* prof, uint64_t step, int slot) {
   if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
@@ -189,14 +199,17 @@ __device__ void do_exchange(const FusedArgs& A, float* p, const Slice& sl, uint6
 
 struct PolicyLocal {
   double cum;
+  double cut;       // launch constants (DevState), cached so the per-step update
+  uint32_t tau;     // touches no global memory
+  int32_t adaptive;
   uint32_t since;
   uint32_t fire, period;
 };
 
-__device__ __forceinline__ void policy_update(PolicyLocal& pl, double loss, const DevState* st) {
+__device__ __forceinline__ void policy_update(PolicyLocal& pl, double loss) {
   pl.cum = dadd(pl.cum, loss);
   pl.since += 1;
-  const bool fire = st->adaptive ? (pl.cum > st->cut) : (pl.since == st->tau);
+  const bool fire = pl.adaptive ? (pl.cum > pl.cut) : (pl.since == pl.tau);
   pl.period = fire ? pl.since : 0u;
   pl.fire = fire ? 1u : 0u;
   if (fire) {
@@ -397,6 +410,7 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
   uint64_t* bar_a = bar_x + 1;
   __shared__ double s_loss;
   __shared__ uint32_t s_bad, s_stop, s_flags;
+  __shared__ unsigned int s_nbar;
   __shared__ PolicyLocal s_pol;
   __shared__ unsigned long long s_ticket;
 
@@ -417,7 +431,11 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
 
   DevState* st = A.st;
   if (tid == 0) {
+    s_nbar = 0;
     s_pol.cum = st->cum;
+    s_pol.cut = st->cut;
+    s_pol.tau = st->tau;
+    s_pol.adaptive = st->adaptive;
     s_pol.since = st->since;
     s_pol.fire = 0;
     s_pol.period = 0;
@@ -513,17 +531,7 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
       // grid barrier; thread 0 also samples the failure flags of the previous iteration
       __syncthreads();
       if (tid == 0) {
-        volatile unsigned int* gen = A.bar + 1;
-        const unsigned int g = *gen;
-        __threadfence();
-        if (atomicAdd(A.bar, 1u) == G - 1) {
-          A.bar[0] = 0;
-          __threadfence();
-          atomicExch(A.bar + 1, g + 1);
-        } else {
-          while (*gen == g) __nanosleep(20);
-        }
-        __threadfence();
+        grid_arrive_wait(A.bar, s_nbar, G);
         s_flags = *reinterpret_cast<volatile uint32_t*>(&st->flags);
         fence_proxy_async();  // other CTAs' generic writes (act, W2) before our async reads
         if (sp.bulk_a && !s_flags) {
@@ -812,7 +820,7 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
       }
     }
     if (tid == 0) {
-      policy_update(s_pol, s_loss, st);
+      policy_update(s_pol, s_loss);
       if (blockIdx.x == 0) {
         const unsigned long long row = it0 + step;
         if (row < A.log.cap) {
@@ -832,7 +840,7 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
         // Locked: take the next global ticket once, share it through the barrier
         unsigned long long* slot = reinterpret_cast<unsigned long long*>(A.bar + 4);
         if (blockIdx.x == 0 && tid == 0) *slot = atomicAdd_system(A.ticket_src, 1ull);
-        if (kHidden) grid_barrier(A.bar, G);
+        if (kHidden) grid_barrier(A.bar, s_nbar, G);
         else __syncthreads();
         if (tid == 0) s_ticket = __ldcg(slot);
         __syncthreads();
@@ -854,7 +862,7 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
     stamp(A.prof, step, 8);
   }
   if constexpr (kHidden) {
-    grid_barrier(A.bar, G);  // failures of the last iteration become visible here
+    grid_barrier(A.bar, s_nbar, G);  // failures of the last iteration become visible here
     const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&st->flags);
     if (fl) {
       if (blockIdx.x == 0 && tid == 0) {
@@ -994,6 +1002,63 @@ __device__ __forceinline__ void dw1_columns(const FusedArgs& A, const float* Xs,
   }
 }
 
+// Logits z[r][c] = b2[c] + sum_u W2[c][u] * a[r][u] in the reference's order (model.cpp:
+// 205-209) for NC classes cb, cb+4, ... of row r: NC interleaved chains per thread, the
+// activation loaded once for all of them, products one 4-element block ahead.
+constexpr uint32_t kLogitChains = 3;
+template <int NC>
+__device__ __forceinline__ void logit_chains(double* Z, const double* W2d, uint32_t H2, const double* As, uint32_t B,
+                                             uint32_t H, const float* b2, uint32_t r, uint32_t C, uint32_t cb) {
+  const double2* w[NC];
+  double z[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    w[i] = reinterpret_cast<const double2*>(W2d + static_cast<size_t>(cb + 4 * i) * H2);
+    z[i] = static_cast<double>(ldcg(b2 + cb + 4 * i));
+  }
+  const double* a = As + r;
+  double p[NC][4], q[NC][4];
+  auto prod = [&](uint32_t blk, double (&x)[NC][4]) {
+    double av[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) av[k] = a[static_cast<size_t>(blk * 4 + k) * B];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const double2 w01 = w[i][blk * 2], w23 = w[i][blk * 2 + 1];
+      x[i][0] = dmul(w01.x, av[0]);
+      x[i][1] = dmul(w01.y, av[1]);
+      x[i][2] = dmul(w23.x, av[2]);
+      x[i][3] = dmul(w23.y, av[3]);
+    }
+  };
+  const uint32_t nb = H / 4;
+  if (nb) {
+    prod(0, p);
+    for (uint32_t blk = 1; blk < nb; ++blk) {
+      prod(blk, q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          z[i] = dadd(z[i], p[i][k]);
+          p[i][k] = q[i][k];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int i = 0; i < NC; ++i) z[i] = dadd(z[i], p[i][k]);
+  }
+  for (uint32_t u = nb * 4; u < H; ++u) {
+    const double av = a[static_cast<size_t>(u) * B];
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+      z[i] = dadd(z[i], dmul(W2d[static_cast<size_t>(cb + 4 * i) * H2 + u], av));
+  }
+#pragma unroll
+  for (int i = 0; i < NC; ++i) Z[static_cast<size_t>(r) * C + cb + 4 * i] = z[i];
+}
+
 constexpr uint32_t kBarFull = 2, kBarEmpty = 4;  // named barrier ids (+ buffer index)
 
 __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
@@ -1027,6 +1092,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   uint64_t* xbar = abar + 1;  // [nck]: column chunk k of the batch rows landed
   __shared__ double s_loss;
   __shared__ uint32_t s_bad, s_stop, s_flags;
+  __shared__ unsigned int s_nbar;
   __shared__ PolicyLocal s_pol;
   __shared__ unsigned long long s_ticket;
 
@@ -1041,7 +1107,11 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
 
   DevState* st = A.st;
   if (tid == 0) {
+    s_nbar = 0;
     s_pol.cum = st->cum;
+    s_pol.cut = st->cut;
+    s_pol.tau = st->tau;
+    s_pol.adaptive = st->adaptive;
     s_pol.since = st->since;
     s_pol.fire = 0;
     s_pol.period = 0;
@@ -1074,11 +1144,10 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     const uint32_t R = A.plan_rows[s];
     const uint32_t* idx = A.plan + s * B;
     for (uint32_t k = 0; k < nck; ++k) {
-      const uint32_t cw = F - k * CW < CW ? F - k * CW : CW, pr = cw / 4;
-      for (uint32_t p = tid; p < R * pr; p += kFT) {
-        const uint32_t r = p / pr, c = k * CW + 4 * (p - r * pr);
-        cp_async16(Xs + static_cast<size_t>(r) * Fs + c, A.X + static_cast<uint64_t>(__ldg(idx + r)) * F + c);
-      }
+      const uint32_t c = k * CW + 4 * lane;
+      if (4 * lane < (F - k * CW < CW ? F - k * CW : CW))
+        for (uint32_t r = warp; r < R; r += kFT / 32)
+          cp_async16(Xs + static_cast<size_t>(r) * Fs + c, A.X + static_cast<uint64_t>(__ldg(idx + r)) * F + c);
       cp_async_arrive(xbar + k);
     }
   };
@@ -1132,18 +1201,9 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     stamp(A.prof, step, 2);
     // grid barrier; thread 0 samples the failure flags and starts the activation copy
     __syncthreads();
+    stamp_cta(A.prof_cta, step, 0);
     if (tid == 0) {
-      volatile unsigned int* gen = A.bar + 1;
-      const unsigned int g = *gen;
-      __threadfence();
-      if (atomicAdd(A.bar, 1u) == G - 1) {
-        A.bar[0] = 0;
-        __threadfence();
-        atomicExch(A.bar + 1, g + 1);
-      } else {
-        while (*gen == g) __nanosleep(20);
-      }
-      __threadfence();
+      grid_arrive_wait(A.bar, s_nbar, G);
       s_flags = *reinterpret_cast<volatile uint32_t*>(&st->flags);
       fence_proxy_async();
       if (!s_flags) {
@@ -1156,6 +1216,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     }
     __syncthreads();
     stamp(A.prof, step, 3);
+    stamp_cta(A.prof_cta, step, 1);
     if (s_flags) {
       if (blockIdx.x == 0 && tid == 0) {
         st->err = s_flags;
@@ -1185,70 +1246,19 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     aph ^= 1;
     __syncthreads();
     stamp(A.prof, step, 4);
-    {  // logits: lane == row, two classes per warp (two interleaved chains)
-      const uint32_t nwl = (C + 1) / 2 < kFT / 32 ? (C + 1) / 2 : kFT / 32;
-      for (uint32_t r0 = 0; r0 < R; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        if (warp >= nwl || r >= R) continue;
-        for (uint32_t c = warp; c < C; c += 2 * nwl) {
-          const uint32_t c2 = c + nwl;
-          const bool has2 = c2 < C;
-          const double* wa = W2d + static_cast<size_t>(c) * H2;
-          const double* wb = W2d + static_cast<size_t>(has2 ? c2 : c) * H2;
-          const double* a = As + r;
-          double za = static_cast<double>(ldcg(P + b2 + c));
-          double zb = has2 ? static_cast<double>(ldcg(P + b2 + c2)) : 0.0;
-          double pa[8], pb[8], qa[8], qb[8];
-          const uint32_t nb = H / 8;
-          auto prod = [&](uint32_t blk, double (&xa)[8], double (&xb2)[8]) {
-            double2 w2a[4], w2b[4];
-            if ((H2 % 2) == 0) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                w2a[k] = reinterpret_cast<const double2*>(wa)[blk * 4 + k];
-                w2b[k] = reinterpret_cast<const double2*>(wb)[blk * 4 + k];
-              }
-            } else {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                w2a[k] = make_double2(wa[blk * 8 + 2 * k], wa[blk * 8 + 2 * k + 1]);
-                w2b[k] = make_double2(wb[blk * 8 + 2 * k], wb[blk * 8 + 2 * k + 1]);
-              }
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const double av = a[static_cast<size_t>(blk * 8 + k) * B];
-              const double wva = (k & 1) ? w2a[k >> 1].y : w2a[k >> 1].x;
-              const double wvb = (k & 1) ? w2b[k >> 1].y : w2b[k >> 1].x;
-              xa[k] = dmul(wva, av);
-              xb2[k] = dmul(wvb, av);
-            }
-          };
-          if (nb) {
-            prod(0, pa, pb);
-            for (uint32_t blk = 1; blk < nb; ++blk) {
-              prod(blk, qa, qb);
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                za = dadd(za, pa[k]);
-                zb = dadd(zb, pb[k]);
-                pa[k] = qa[k];
-                pb[k] = qb[k];
-              }
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              za = dadd(za, pa[k]);
-              zb = dadd(zb, pb[k]);
-            }
+    {  // logits: lane == row; a warp runs the chains of classes w, w+4, w+8, ... for its
+       // rows (4 class sets, one per SM sub-partition: the As reads stay 4x, not Cx)
+      const uint32_t ngroups = (R + 31) / 32;
+      for (uint32_t item = warp; item < ngroups * 4; item += kFT / 32) {
+        const uint32_t r = (item >> 2) * 32 + lane, cs = item & 3;
+        if (r >= R) continue;
+        for (uint32_t cb = cs; cb < C; cb += 4 * kLogitChains) {
+          const uint32_t nc = (C - cb + 3) / 4 < kLogitChains ? (C - cb + 3) / 4 : kLogitChains;
+          switch (nc) {
+            case 1: logit_chains<1>(Z, W2d, H2, As, B, H, P + b2, r, C, cb); break;
+            case 2: logit_chains<2>(Z, W2d, H2, As, B, H, P + b2, r, C, cb); break;
+            default: logit_chains<3>(Z, W2d, H2, As, B, H, P + b2, r, C, cb); break;
           }
-          for (uint32_t u = nb * 8; u < H; ++u) {
-            const double av = a[static_cast<size_t>(u) * B];
-            za = dadd(za, dmul(wa[u], av));
-            zb = dadd(zb, dmul(wb[u], av));
-          }
-          Z[static_cast<size_t>(r) * C + c] = za;
-          if (has2) Z[static_cast<size_t>(r) * C + c2] = zb;
         }
       }
     }
@@ -1343,7 +1353,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     stamp(A.prof, step, 7);
     if (s_bad && tid == 0) atomicOr(&st->flags, s_bad);  // all CTAs stop after the next barrier
     if (tid == 0) {
-      policy_update(s_pol, s_loss, st);
+      policy_update(s_pol, s_loss);
       if (blockIdx.x == 0) {
         const unsigned long long row = it0 + step;
         if (row < A.log.cap) {
@@ -1362,7 +1372,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
       } else if (A.ticket_src) {
         unsigned long long* slot = reinterpret_cast<unsigned long long*>(A.bar + 4);
         if (blockIdx.x == 0 && tid == 0) *slot = atomicAdd_system(A.ticket_src, 1ull);
-        grid_barrier(A.bar, G);
+        grid_barrier(A.bar, s_nbar, G);
         if (tid == 0) s_ticket = __ldcg(slot);
         __syncthreads();
         tk = s_ticket;
@@ -1375,7 +1385,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     __syncthreads();
     stamp(A.prof, step, 8);
   }
-  grid_barrier(A.bar, G);
+  grid_barrier(A.bar, s_nbar, G);
   const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(&st->flags);
   if (fl) {
     if (blockIdx.x == 0 && tid == 0) {
@@ -1462,6 +1472,7 @@ int fused_supported(const ModelInfo& m, uint32_t batch, int device, const char**
 
 int launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
   const size_t smem = smem_for(a.F, a.H, a.C, a.B, static_cast<uint32_t>(grid));
+  DS_CUDA_TRY(cudaMemsetAsync(a.bar + kBarCounter, 0, sizeof(unsigned int), s));  // grid_barrier counter
   void* args[] = {const_cast<FusedArgs*>(&a)};
   if (a.H > 0) {
     DS_CUDA_TRY(cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
