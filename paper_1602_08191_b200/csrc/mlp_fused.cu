@@ -897,7 +897,7 @@ __global__ void __launch_bounds__(kFT, 1) fused_kernel(FusedArgs A) {
 // ======================================================================================
 struct MlpPlan {
   uint32_t Fs, Fd, CW, CWs, nck, H2;
-  size_t xs, w, wd, un, as, w2, z, e, d1, lr, rs, bars, chunk, total;
+  size_t xs, w, wd, un, as, w2, z, e, d1, lr, rs, ri, bars, chunk, total;
 };
 
 __host__ __device__ inline MlpPlan make_mlp_plan(uint32_t F, uint32_t H, uint32_t C, uint32_t B, uint32_t G) {
@@ -925,6 +925,7 @@ __host__ __device__ inline MlpPlan make_mlp_plan(uint32_t F, uint32_t H, uint32_
     p.d1 = off;  off = al(off + static_cast<size_t>(B) * U * 8);
     p.lr = off;  off = al(off + static_cast<size_t>(B) * 8);
     p.rs = off;  off = al(off + static_cast<size_t>(B) * 8 * 2 + static_cast<size_t>(B) * 4 * 2);
+    p.ri = off;  off = al(off + static_cast<size_t>(B) * 4);
     p.bars = off; off = al(off + 8 * (p.nck + 2));
     p.total = off;
     if (p.total <= 216 * 1024 || cw == 16) break;
@@ -1088,6 +1089,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   double* Zmax = reinterpret_cast<double*>(smem_raw + sp.rs);
   double* Lse = Zmax + B;
   uint32_t* Lab = reinterpret_cast<uint32_t*>(Lse + B);
+  uint32_t* Ri = reinterpret_cast<uint32_t*>(smem_raw + sp.ri);      // next batch's shard rows
   uint64_t* abar = reinterpret_cast<uint64_t*>(smem_raw + sp.bars);  // activations
   uint64_t* xbar = abar + 1;  // [nck]: column chunk k of the batch rows landed
   __shared__ double s_loss;
@@ -1140,18 +1142,20 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   // lands: every thread issues 16-byte LDGSTS pieces, then arrives on chunk k's barrier.
   // (One bulk copy per row-chunk would put ~R*nck serialized TMA issues on one warp.)
   // The caller has synced the block since the last generic access of Xs.
+  // Ri holds the batch's shard rows (staged earlier, so no global load sits in this loop).
   auto issue_x = [&](uint64_t s) {
     const uint32_t R = A.plan_rows[s];
-    const uint32_t* idx = A.plan + s * B;
     for (uint32_t k = 0; k < nck; ++k) {
       const uint32_t c = k * CW + 4 * lane;
       if (4 * lane < (F - k * CW < CW ? F - k * CW : CW))
         for (uint32_t r = warp; r < R; r += kFT / 32)
-          cp_async16(Xs + static_cast<size_t>(r) * Fs + c, A.X + static_cast<uint64_t>(__ldg(idx + r)) * F + c);
+          cp_async16(Xs + static_cast<size_t>(r) * Fs + c, A.X + static_cast<uint64_t>(Ri[r]) * F + c);
       cp_async_arrive(xbar + k);
     }
   };
   load_own_rows(A.params[cur]);
+  if (A.steps > 0)
+    for (uint32_t r = tid; r < A.plan_rows[0]; r += kFT) Ri[r] = A.plan[r];
   __syncthreads();
   if (vecx && A.steps > 0) issue_x(0);
 
@@ -1299,6 +1303,8 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
       Z[t] = dsub(exp(dsub(Z[t], Lse[r])), c == Lab[r] ? 1.0 : 0.0);
     }
     __syncthreads();
+    if (step + 1 < A.steps)  // next batch's rows for issue_x (latency hidden by the backward)
+      for (uint32_t r = tid; r < A.plan_rows[step + 1]; r += kFT) Ri[r] = A.plan[(step + 1) * B + r];
     // ---- C: backward. delta1 || W2 columns + b2 (different warps) ---------------------------
     stamp(A.prof, step, 6);
     uint32_t bad = 0;
@@ -1348,9 +1354,9 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) atomicOr(&s_bad, bad);
     __syncthreads();
+    stamp(A.prof, step, 7);
     if (vecx && step + 1 < A.steps) issue_x(step + 1);  // Xs is free: overlap the exchange
     // ---- D: policy + exchange ------------------------------------------------------------
-    stamp(A.prof, step, 7);
     if (s_bad && tid == 0) atomicOr(&st->flags, s_bad);  // all CTAs stop after the next barrier
     if (tid == 0) {
       policy_update(s_pol, s_loss);
