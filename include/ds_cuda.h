@@ -87,6 +87,30 @@ int ds_grad_accumulate(double* gsum, const float* g, uint64_t n, void* stream);
 int ds_grad_average(float* out, const double* gsum, uint64_t n, uint32_t n_workers, float wd,
                     const float* x, void* stream);
 
+/* Multi-GPU synchronous SGD, one process per GPU (simulate_sync, simulator.cpp:156-223,
+ * as the reference's "allreduce each iteration"). Each rank owns two peer-mapped f32
+ * gradient slots; ds_sync_reduce_update reads every rank's slot over NVLink and sums in
+ * f64 in worker order (simulator.cpp:192-200), divides by world, folds f32(wd)*x
+ * (205-207) and applies sgd_step to `params` (the rank's replica of the master) in ONE
+ * kernel — bit-identical to the single-process reference and identical on all ranks.
+ *   create -> export (256-byte record) -> all-gather records -> attach
+ *   per round: ds_sync_begin (slot free?) -> write the local gradient into *grad_slot on
+ *   `stream` -> ds_sync_reduce_update(params, ...) on the same stream.
+ * Non-finite conditions are OR-ed into *flags_dev (DS_FLAG_*). world <= 8. */
+typedef struct ds_sync ds_sync;
+int ds_sync_create(ds_sync** out, int device, uint64_t dim, int rank, int world);
+int ds_sync_export(ds_sync* s, void* record_out);
+int ds_sync_attach(ds_sync* s, const void* records);
+int ds_sync_begin(ds_sync* s, float** grad_slot, void* stream);
+int ds_sync_reduce_update(ds_sync* s, float* params, float eta, float wd, uint32_t* flags_dev, void* stream);
+int ds_sync_rounds(ds_sync* s, uint64_t* out);
+int ds_sync_destroy(ds_sync* s);
+
+/* Row gather for host-free minibatches (model.cpp:12-21 gather_batch on the device):
+ * dst[r, :] = X[idx[r], :] for r < rows, f32 rows of `features`; y_dst[r] = y[idx[r]]. */
+int ds_gather_rows(float* dst, uint32_t* y_dst, const float* X, const uint32_t* y, const uint32_t* idx,
+                   uint32_t rows, uint32_t features, void* stream);
+
 /* ---------------------------------------------------------------------------------- */
 /* Device plumbing for hosts that do not link the CUDA runtime (C++/Go/Java/Python)   */
 /* ---------------------------------------------------------------------------------- */

@@ -142,6 +142,14 @@ _sig("ds_engine_set_params", VP, VP)
 _sig("ds_engine_params_device", VP, C.POINTER(VP))
 _sig("ds_engine_policy", VP, P_D, P_U32, P_D)
 _sig("ds_engine_launches", VP, P_U64)
+_sig("ds_sync_create", C.POINTER(VP), C.c_int, U64, C.c_int, C.c_int)
+_sig("ds_sync_export", VP, VP)
+_sig("ds_sync_attach", VP, VP)
+_sig("ds_sync_begin", VP, C.POINTER(VP), VP)
+_sig("ds_sync_reduce_update", VP, VP, C.c_float, C.c_float, VP, VP)
+_sig("ds_sync_rounds", VP, P_U64)
+_sig("ds_sync_destroy", VP)
+_sig("ds_gather_rows", VP, VP, VP, VP, VP, U32, U32, VP)
 
 EXPORTED = [
     "ds_last_error", "ds_version", "ds_device_count", "ds_elastic_update", "ds_elastic_exchange",
@@ -155,7 +163,8 @@ EXPORTED = [
     "ds_engine_destroy", "ds_engine_attach_master", "ds_engine_set_tickets", "ds_engine_run", "ds_engine_reserve", "ds_engine_step_host",
     "ds_engine_sync", "ds_engine_stream", "ds_engine_log", "ds_engine_iterations",
     "ds_engine_get_params", "ds_engine_set_params", "ds_engine_params_device", "ds_engine_policy",
-    "ds_engine_launches",
+    "ds_engine_launches", "ds_sync_create", "ds_sync_export", "ds_sync_attach", "ds_sync_begin",
+    "ds_sync_reduce_update", "ds_sync_rounds", "ds_sync_destroy", "ds_gather_rows",
 ]
 
 

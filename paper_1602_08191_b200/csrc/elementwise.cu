@@ -245,6 +245,25 @@ __global__ void __launch_bounds__(256) grad_average_kernel(float* __restrict__ o
   }
 }
 
+// gather_batch (model.cpp:12-21) on the device: one warp per row, float4 when aligned.
+__global__ void __launch_bounds__(256) gather_rows_kernel(float* __restrict__ dst, uint32_t* __restrict__ y_dst,
+                                                          const float* __restrict__ X, const uint32_t* __restrict__ y,
+                                                          const uint32_t* __restrict__ idx, uint32_t rows,
+                                                          uint32_t F, bool vec) {
+  const uint32_t warp = (blockIdx.x * 256 + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const uint32_t src = idx[warp];
+  if (lane == 0 && y_dst) y_dst[warp] = y[src];
+  const float* s = X + static_cast<uint64_t>(src) * F;
+  float* d = dst + static_cast<uint64_t>(warp) * F;
+  if (vec) {
+    for (uint32_t q = lane; q < F / 4; q += 32)
+      reinterpret_cast<float4*>(d)[q] = __ldg(reinterpret_cast<const float4*>(s) + q);
+  } else {
+    for (uint32_t i = lane; i < F; i += 32) d[i] = __ldg(s + i);
+  }
+}
+
 unsigned grid_n(uint64_t n) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -269,6 +288,17 @@ extern "C" int ds_grad_average(float* out, const double* gsum, uint64_t n, uint3
     return dsb::set_error(DS_E_CONTRACT, "grad_average: bad arguments");
   grad_average_kernel<<<grid_n(n), 256, 0, dsb::as_stream(stream)>>>(out, gsum, n, static_cast<double>(n_workers),
                                                                     wd, x);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+extern "C" int ds_gather_rows(float* dst, uint32_t* y_dst, const float* X, const uint32_t* y, const uint32_t* idx,
+                              uint32_t rows, uint32_t features, void* stream) {
+  if (rows == 0) return DS_OK;
+  if (!dst || !X || !idx || features == 0 || (y_dst && !y)) return dsb::set_error(DS_E_CONTRACT, "gather_rows: bad arguments");
+  const bool vec = (features % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, dsb::as_stream(stream)>>>(dst, y_dst, X, y, idx, rows, features, vec);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }

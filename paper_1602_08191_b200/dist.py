@@ -72,3 +72,58 @@ def sim_shards(api, X, y, n_workers: int, holdout_frac: float, data_seed: int, r
 
 def sweep_seed(api, data_seed: int, worker: int, replicate: bool = False) -> int:
     return api.mix_seed(api.mix_seed(data_seed, SWEEP_TAG), 0 if replicate else worker)
+
+
+def sync_group(L, device: int, dim: int, rank: int, world: int, group=None):
+    """This rank's member of a synchronous-SGD group (ds_sync), attached to every peer."""
+    s = C.c_void_p()
+    L.check(L.lib.ds_sync_create(C.byref(s), device, dim, rank, world))
+    rec = (C.c_uint8 * L.DS_IPC_RECORD_BYTES)()
+    L.check(L.lib.ds_sync_export(s, rec))
+    recs = gather_bytes(bytes(rec), world, group)
+    allrec = (C.c_uint8 * (L.DS_IPC_RECORD_BYTES * world)).from_buffer_copy(b"".join(recs))
+    L.check(L.lib.ds_sync_attach(s, allrec))
+    return s
+
+
+def run_sync_worker(L, api, model_desc, Xk, yk, n_classes: int, hp, sweep_seed_k: int, params_dev, sg,
+                    device: int, stream=None):
+    """One rank of simulate_sync (simulator.cpp:156-223) on its own GPU: every round the
+    rank's ShardSweeper batch (gathered on the device from the resident shard) gives a
+    gradient at the current master replica; ds_sync_reduce_update sums all ranks' gradients
+    in worker order over NVLink and applies the SGD step. Returns this worker's per-round
+    batch losses (f64). `params_dev` (device f32[P]) holds the replica in and out."""
+    import torch
+    B, i_max = hp.batch_size, hp.i_max
+    idx, rows = api.sweep_batches(len(yk), B, sweep_seed_k, i_max)
+    dev = torch.device("cuda", device)
+    Xd = torch.from_numpy(np.ascontiguousarray(Xk)).to(dev)
+    yd = torch.from_numpy(np.ascontiguousarray(yk).astype(np.uint32).view(np.int32)).to(dev)
+    idx_d = torch.from_numpy(np.ascontiguousarray(idx).astype(np.uint32).view(np.int32)).to(dev)
+    F = Xk.shape[1]
+    bX = torch.empty((B, F), dtype=torch.float32, device=dev)
+    by = torch.empty(B, dtype=torch.int32, device=dev)
+    ws_bytes = C.c_uint64()
+    L.check(L.lib.ds_loss_and_grad_workspace(C.byref(model_desc), B, C.byref(ws_bytes)))
+    ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device=dev)
+    losses = torch.zeros(i_max, dtype=torch.float64, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = C.c_void_p(stream) if stream is not None else None
+    slot = C.c_void_p()
+    for r in range(i_max):
+        nr = int(rows[r])
+        src = idx_d[r, :nr]  # sweep_batches: [i_max, B] shard rows, `rows[r]` valid
+        L.check(L.lib.ds_gather_rows(C.c_void_p(bX.data_ptr()), C.c_void_p(by.data_ptr()), C.c_void_p(Xd.data_ptr()),
+                                     C.c_void_p(yd.data_ptr()), C.c_void_p(src.data_ptr()), nr, F, st))
+        L.check(L.lib.ds_sync_begin(sg, C.byref(slot), st))
+        L.check(L.lib.ds_loss_and_grad(C.byref(model_desc), C.c_void_p(params_dev.data_ptr()),
+                                       C.c_void_p(bX.data_ptr()), C.c_void_p(by.data_ptr()), nr, slot,
+                                       C.c_void_p(losses.data_ptr() + 8 * r), C.c_void_p(ws.data_ptr()),
+                                       C.c_void_p(flags.data_ptr()), st))
+        L.check(L.lib.ds_sync_reduce_update(sg, C.c_void_p(params_dev.data_ptr()), C.c_float(hp.eta),
+                                            C.c_float(hp.weight_decay), C.c_void_p(flags.data_ptr()), st))
+    torch.cuda.synchronize(dev)
+    fl = int(flags.item())
+    if fl:
+        raise RuntimeError(f"simulate_sync: device flags 0x{fl:x} (non-finite loss/grad/update or label range)")
+    return losses.cpu().numpy()
