@@ -126,8 +126,12 @@ int ds_stream_sync(void* stream);
 /* ---------------------------------------------------------------------------------- */
 /* Model — model.hpp:32-76                                                            */
 /* ---------------------------------------------------------------------------------- */
+/* kind 2: Caffe cifar10_quick on CHW 3x32x32 rows (n_features 3072, n_hidden 0) —
+ * NOT IN THE REFERENCE; same flat W-then-b layout, init and loss
+ * conventions, f32 arithmetic (tolerance parity vs the f64 oracle, not bit-exact). */
+#define DS_MODEL_CIFAR10_QUICK 2
 typedef struct {
-  int32_t kind;          /* 0 = SoftmaxRegression, 1 = Mlp (model.hpp:13)         */
+  int32_t kind;          /* 0 = SoftmaxRegression, 1 = Mlp (model.hpp:13), 2 = cifar10_quick */
   uint32_t n_features;
   uint32_t n_classes;
   uint32_t n_hidden;     /* number of tanh hidden layers                            */

@@ -91,7 +91,8 @@ def _p(a: Optional[np.ndarray], ct):
 
 @dataclass
 class ModelSpec:
-    """Mirror of deepspark::Model (model.hpp:32-56): kind 'softmax' | 'mlp'."""
+    """Mirror of deepspark::Model (model.hpp:32-56): kind 'softmax' | 'mlp', plus
+    'cifar10_quick' (kind 2, NOT IN THE REFERENCE; oracle/ds_oracle_cnn.h)."""
     kind: str
     n_features: int
     n_classes: int
@@ -105,9 +106,13 @@ class ModelSpec:
     def mlp(f: int, hidden: Sequence[int], c: int) -> "ModelSpec":
         return ModelSpec("mlp", f, c, tuple(hidden))
 
+    @staticmethod
+    def cifar10_quick(c: int = 10) -> "ModelSpec":
+        return ModelSpec("cifar10_quick", 3072, c, ())
+
     def c(self):
         h = np.ascontiguousarray(np.asarray(self.hidden, dtype=np.uint32))
-        m = dso_model(0 if self.kind == "softmax" else 1, self.n_features, self.n_classes,
+        m = dso_model({"softmax": 0, "mlp": 1, "cifar10_quick": 2}[self.kind], self.n_features, self.n_classes,
                       len(self.hidden), _p(h if len(self.hidden) else None, C.c_uint32))
         return m, h  # keep h alive
 

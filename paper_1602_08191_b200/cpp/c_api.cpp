@@ -42,7 +42,7 @@ int guard(F&& f) {
 
 Model model_of(const dsx_model* m) {
   Model out;
-  out.kind = m->kind == 0 ? ModelKind::SoftmaxRegression : ModelKind::Mlp;
+  out.kind = m->kind == 0 ? ModelKind::SoftmaxRegression : (m->kind == 1 ? ModelKind::Mlp : ModelKind::Cifar10Quick);
   out.n_features = m->n_features;
   out.n_classes = m->n_classes;
   out.hidden.assign(m->hidden, m->hidden + m->n_hidden);

@@ -18,7 +18,7 @@ namespace {
 detail::ModelDesc desc_of(const Model& m) {
   detail::ModelDesc md;
   md.hidden = m.hidden;
-  md.d.kind = m.kind == ModelKind::SoftmaxRegression ? 0 : 1;
+  md.d.kind = m.kind == ModelKind::SoftmaxRegression ? 0 : (m.kind == ModelKind::Mlp ? 1 : DS_MODEL_CIFAR10_QUICK);
   md.d.n_features = m.n_features;
   md.d.n_classes = m.n_classes;
   md.d.n_hidden = static_cast<uint32_t>(md.hidden.size());
@@ -107,7 +107,22 @@ Model Model::mlp(uint32_t n_features, std::vector<uint32_t> hidden, uint32_t n_c
   return m;
 }
 
+Model Model::cifar10_quick(uint32_t n_classes) {
+  Model m;
+  m.kind = ModelKind::Cifar10Quick;
+  m.n_features = 3072;
+  m.n_classes = n_classes;
+  m.validate();
+  return m;
+}
+
 void Model::validate() const {
+  if (kind == ModelKind::Cifar10Quick) {
+    if (n_features != 3072) throw ContractError("model: cifar10_quick takes 3072 features");
+    if (n_classes < 2) throw ContractError("model: n_classes must be at least 2");
+    if (!hidden.empty()) throw ContractError("model: cifar10_quick has no hidden list");
+    return;
+  }
   if (n_features == 0) throw ContractError("model: n_features must be positive");
   if (n_classes < 2) throw ContractError("model: n_classes must be at least 2");
   if (kind == ModelKind::SoftmaxRegression && !hidden.empty())
@@ -136,6 +151,10 @@ Model Model::parse(const std::string& text) {
     return static_cast<uint32_t>(v);
   };
   if (parts.size() == 3 && parts[0] == "softmax") return softmax(positive(parts[1]), positive(parts[2]));
+  if (parts.size() == 3 && parts[0] == "cifar10_quick") {
+    if (positive(parts[1]) != 3072) throw ContractError("model: cifar10_quick takes 3072 features");
+    return cifar10_quick(positive(parts[2]));
+  }
   if (parts.size() == 4 && parts[0] == "mlp") {
     std::vector<uint32_t> hidden;
     std::stringstream hs(parts[2]);
@@ -154,6 +173,10 @@ std::string Model::to_string() const {
     os << "softmax:" << n_features << ':' << n_classes;
     return os.str();
   }
+  if (kind == ModelKind::Cifar10Quick) {
+    os << "cifar10_quick:" << n_features << ':' << n_classes;
+    return os.str();
+  }
   os << "mlp:" << n_features << ':';
   for (size_t i = 0; i < hidden.size(); ++i) os << (i ? "," : "") << hidden[i];
   os << ':' << n_classes;
@@ -162,6 +185,16 @@ std::string Model::to_string() const {
 
 std::vector<Model::Layer> Model::layers() const {
   std::vector<Layer> out;
+  if (kind == ModelKind::Cifar10Quick) {  // conv1..3 (fan_in = Cin*25), ip1, ip2
+    const uint32_t fan[5] = {75, 800, 800, 1024, 64}, width[5] = {32, 32, 64, 64, n_classes};
+    size_t off = 0;
+    for (int l = 0; l < 5; ++l) {
+      Layer L{off, off + static_cast<size_t>(width[l]) * fan[l], fan[l], width[l]};
+      off = L.b_off + width[l];
+      out.push_back(L);
+    }
+    return out;
+  }
   size_t off = 0;
   uint32_t in = n_features;
   std::vector<uint32_t> widths = hidden;
@@ -188,7 +221,7 @@ uint64_t Model::fingerprint() const {
       h *= 0x100000001b3ULL;  // FNV prime
     }
   };
-  mix(kind == ModelKind::SoftmaxRegression ? 1 : 2, 1);
+  mix(kind == ModelKind::SoftmaxRegression ? 1 : (kind == ModelKind::Mlp ? 2 : 3), 1);
   mix(n_features, 4);
   mix(n_classes, 4);
   mix(hidden.size(), 4);

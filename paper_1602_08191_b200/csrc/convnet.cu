@@ -1,0 +1,546 @@
+// convnet.cu — cifar10_quick (model kind 2) loss_and_grad / predict on the B200.
+//
+// NOT IN THE REFERENCE: the reference ships only softmax regression
+// and tanh MLPs. This network follows the reference's conventions (flat per-layer
+// W[out x fan_in] + b[out] layout, U(+-1/sqrt(fan_in)) init, mean softmax cross-entropy,
+// gradient = batch sum * (1/b)) so it plugs into the same engine, exchanger and
+// simulator. Parity is against the f64 CPU restatement oracle/ds_oracle_cnn.c (itself
+// gated by central differences); arithmetic here is f32 with FMA, so the bar is a stated
+// tolerance, not bit-exactness.
+//
+// Layout: activations NCHW f32 in the workspace, batch rows = CHW 3x32x32 samples.
+//   conv1 5x5 3->32 p2 -> MAX 3x3/2 -> relu -> conv2 5x5 32->32 p2 -> relu -> AVE 3x3/2
+//   -> conv3 5x5 32->64 p2 -> relu -> AVE 3x3/2 -> ip1 1024->64 -> ip2 64->C -> softmax
+// Every reduction (weight gradients over the batch, pooling backward) is a fixed-order
+// gather, never an atomic, so results are deterministic run to run.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ds_common.cuh"
+#include "model.cuh"
+
+namespace dsb {
+namespace {
+
+constexpr int kCnnChunk = 4;  // samples per partial weight-gradient block
+
+__device__ __forceinline__ uint32_t pooled(uint32_t H) { return (H - 3 + 1) / 2 + 1; }  // ceil((H-3)/2)+1
+
+// ---- 5x5 pad-2 stride-1 convolution (also used for backward-data with flipped,
+// transposed weights). One CTA = one sample x COB output channels; a thread owns PPT
+// consecutive pixels of a row for all COB channels. The padded input planes and the
+// CTA's weights (transposed to [k][COB] so one LDS.128 feeds 4 channels) live in smem.
+template <int CIN, int COUT, int H, int COB, int PPT>
+__global__ void __launch_bounds__(H * H / PPT) conv5_kernel(const float* __restrict__ in, const float* __restrict__ W,
+                                                            const float* __restrict__ bias, float* __restrict__ out,
+                                                            bool relu, const uint32_t* gate) {
+  if (gate && *gate) return;
+  constexpr int HP = H + 4, K = CIN * 25;
+  extern __shared__ __align__(16) float sm[];
+  float* xs = sm;                 // [CIN][HP][HP]
+  float* ws = sm + CIN * HP * HP;  // [K][COB]
+  const int n = blockIdx.x, co0 = blockIdx.y * COB, tid = threadIdx.x;
+  constexpr int NT = H * H / PPT;
+  const float* src = in + static_cast<size_t>(n) * CIN * H * H;
+  for (int i = tid; i < CIN * HP * HP; i += NT) {
+    const int c = i / (HP * HP), r = (i / HP) % HP, q = i % HP;
+    const int y = r - 2, x = q - 2;
+    xs[i] = (y >= 0 && y < H && x >= 0 && x < H) ? __ldg(src + (c * H + y) * H + x) : 0.0f;
+  }
+  for (int i = tid; i < K * COB; i += NT) {
+    const int k = i / COB, c = i % COB;
+    ws[i] = __ldg(W + static_cast<size_t>(co0 + c) * K + k);
+  }
+  __syncthreads();
+  const int p0 = tid * PPT, h = p0 / H, w0 = p0 % H;
+  float acc[COB][PPT];
+#pragma unroll
+  for (int c = 0; c < COB; ++c)
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) acc[c][j] = 0.0f;
+  for (int ci = 0; ci < CIN; ++ci) {
+#pragma unroll
+    for (int kh = 0; kh < 5; ++kh) {
+      const float* xr = xs + (ci * HP + h + kh) * HP + w0;
+      float xv[PPT + 4];
+#pragma unroll
+      for (int j = 0; j < PPT + 4; ++j) xv[j] = xr[j];
+#pragma unroll
+      for (int kw = 0; kw < 5; ++kw) {
+        const float4* wv = reinterpret_cast<const float4*>(ws + ((ci * 5 + kh) * 5 + kw) * COB);
+#pragma unroll
+        for (int c4 = 0; c4 < COB / 4; ++c4) {
+          const float4 wq = wv[c4];
+#pragma unroll
+          for (int j = 0; j < PPT; ++j) {
+            acc[4 * c4 + 0][j] = fmaf(wq.x, xv[j + kw], acc[4 * c4 + 0][j]);
+            acc[4 * c4 + 1][j] = fmaf(wq.y, xv[j + kw], acc[4 * c4 + 1][j]);
+            acc[4 * c4 + 2][j] = fmaf(wq.z, xv[j + kw], acc[4 * c4 + 2][j]);
+            acc[4 * c4 + 3][j] = fmaf(wq.w, xv[j + kw], acc[4 * c4 + 3][j]);
+          }
+        }
+      }
+    }
+  }
+  float* dst = out + static_cast<size_t>(n) * COUT * H * H;
+#pragma unroll
+  for (int c = 0; c < COB; ++c) {
+    const float b = bias ? __ldg(bias + co0 + c) : 0.0f;
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      float v = acc[c][j] + b;
+      if (relu) v = v > 0.0f ? v : 0.0f;
+      dst[((co0 + c) * H + h) * H + w0 + j] = v;
+    }
+  }
+}
+
+template <int CIN, int COUT, int H, int COB, int PPT>
+int launch_conv5(const float* in, const float* W, const float* b, float* out, uint32_t R, bool relu,
+                 const uint32_t* gate, cudaStream_t s) {
+  constexpr int HP = H + 4;
+  const size_t smem = (static_cast<size_t>(CIN) * HP * HP + static_cast<size_t>(CIN) * 25 * COB) * sizeof(float);
+  auto k = conv5_kernel<CIN, COUT, H, COB, PPT>;
+  DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k<<<dim3(R, COUT / COB), H * H / PPT, smem, s>>>(in, W, b, out, relu, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+// Wt[ci][co][kh][kw] = W[co][ci][4-kh][4-kw]: backward-data is conv5 of dY with Wt.
+__global__ void flip_transpose_kernel(const float* __restrict__ W, float* __restrict__ Wt, uint32_t cout,
+                                      uint32_t cin, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cout * cin * 25) return;
+  const uint32_t kk = i % 25, ci = (i / 25) % cin, co = i / (25 * cin);
+  Wt[(static_cast<size_t>(ci) * cout + co) * 25 + (24 - kk)] = W[i];
+}
+
+// ---- pooling (3x3 stride 2, ceil mode, pad 0) ---------------------------------------
+// pool1: MAX then relu1. arg = window offset (0..8) of the first maximum (Caffe strict >).
+__global__ void maxpool_relu_kernel(const float* __restrict__ in, float* __restrict__ out, uint8_t* __restrict__ arg,
+                                    uint32_t NC, uint32_t H, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t Ho = pooled(H), i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= NC * Ho * Ho) return;
+  const uint32_t pw = i % Ho, ph = (i / Ho) % Ho, nc = i / (Ho * Ho);
+  const uint32_t hs = 2 * ph, ws = 2 * pw, he = min(hs + 3, H), we = min(ws + 3, H);
+  const float* p = in + static_cast<size_t>(nc) * H * H;
+  float best = -INFINITY;
+  uint32_t bi = 0;
+  for (uint32_t h = hs; h < he; ++h)
+    for (uint32_t w = ws; w < we; ++w) {
+      const float v = p[h * H + w];
+      if (v > best) best = v, bi = (h - hs) * 3 + (w - ws);
+    }
+  out[i] = best > 0.0f ? best : 0.0f;
+  arg[i] = static_cast<uint8_t>(bi | (best > 0.0f ? 0x10u : 0u));  // bit 4: relu1 passed
+}
+
+__global__ void avepool_kernel(const float* __restrict__ in, float* __restrict__ out, uint32_t NC, uint32_t H,
+                               const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t Ho = pooled(H), i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= NC * Ho * Ho) return;
+  const uint32_t pw = i % Ho, ph = (i / Ho) % Ho, nc = i / (Ho * Ho);
+  const uint32_t hs = 2 * ph, ws = 2 * pw, he = min(hs + 3, H), we = min(ws + 3, H);
+  const float* p = in + static_cast<size_t>(nc) * H * H;
+  float s = 0.0f;
+  for (uint32_t h = hs; h < he; ++h)
+    for (uint32_t w = ws; w < we; ++w) s += p[h * H + w];
+  out[i] = s / static_cast<float>((he - hs) * (we - ws));
+}
+
+// din[n][c][h][w] = sum over windows containing (h,w) of dout/size, times (act > 0) when
+// `act` (the relu output feeding the pool) is given.
+__global__ void avepool_bwd_kernel(const float* __restrict__ dout, const float* __restrict__ act,
+                                   float* __restrict__ din, uint32_t NC, uint32_t H, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t Ho = pooled(H), i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= NC * H * H) return;
+  const uint32_t w = i % H, h = (i / H) % H, nc = i / (H * H);
+  float s = 0.0f;
+  const uint32_t ph0 = h >= 2 ? (h - 1) / 2 : 0, ph1 = min(h / 2, Ho - 1);
+  const uint32_t pw0 = w >= 2 ? (w - 1) / 2 : 0, pw1 = min(w / 2, Ho - 1);
+  for (uint32_t ph = ph0; ph <= ph1; ++ph)
+    for (uint32_t pw = pw0; pw <= pw1; ++pw) {
+      const uint32_t hs = 2 * ph, ws = 2 * pw, he = min(hs + 3, H), we = min(ws + 3, H);
+      s += dout[(static_cast<size_t>(nc) * Ho + ph) * Ho + pw] / static_cast<float>((he - hs) * (we - ws));
+    }
+  if (act && !(act[i] > 0.0f)) s = 0.0f;
+  din[i] = s;
+}
+
+// dc1[n][c][h][w] = sum of dr1 over the windows whose (relu-passing) maximum is (h,w).
+__global__ void maxpool_relu_bwd_kernel(const float* __restrict__ dout, const uint8_t* __restrict__ arg,
+                                        float* __restrict__ din, uint32_t NC, uint32_t H, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t Ho = pooled(H), i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= NC * H * H) return;
+  const uint32_t w = i % H, h = (i / H) % H, nc = i / (H * H);
+  float s = 0.0f;
+  const uint32_t ph0 = h >= 2 ? (h - 1) / 2 : 0, ph1 = min(h / 2, Ho - 1);
+  const uint32_t pw0 = w >= 2 ? (w - 1) / 2 : 0, pw1 = min(w / 2, Ho - 1);
+  for (uint32_t ph = ph0; ph <= ph1; ++ph)
+    for (uint32_t pw = pw0; pw <= pw1; ++pw) {
+      const size_t o = (static_cast<size_t>(nc) * Ho + ph) * Ho + pw;
+      const uint32_t a = arg[o];
+      if ((a & 0x10u) && (a & 0xfu) == (h - 2 * ph) * 3 + (w - 2 * pw)) s += dout[o];
+    }
+  din[i] = s;
+}
+
+// ---- fully connected ---------------------------------------------------------------
+// out[r][o] = b[o] + sum_i W[o][i] a[r][i]; CTA per row, KS-way split over i, fixed-order
+// combine of the KS partials.
+template <int KS>
+__global__ void fc_fwd_kernel(const float* __restrict__ a, const float* __restrict__ W, const float* __restrict__ b,
+                              float* __restrict__ out, uint32_t in, uint32_t nout, const uint32_t* gate) {
+  if (gate && *gate) return;
+  extern __shared__ float fs[];
+  float* as = fs;          // [in]
+  float* part = fs + in;   // [KS][nout]
+  const uint32_t r = blockIdx.x;
+  for (uint32_t i = threadIdx.x; i < in; i += blockDim.x) as[i] = a[static_cast<size_t>(r) * in + i];
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < KS * nout; t += blockDim.x) {
+    const uint32_t o = t % nout, k = t / nout;
+    const uint32_t i0 = k * in / KS, i1 = (k + 1) * in / KS;
+    const float* wr = W + static_cast<size_t>(o) * in;
+    float s = 0.0f;
+    for (uint32_t i = i0; i < i1; ++i) s = fmaf(__ldg(wr + i), as[i], s);
+    part[k * nout + o] = s;
+  }
+  __syncthreads();
+  for (uint32_t o = threadIdx.x; o < nout; o += blockDim.x) {
+    float s = b[o];
+    for (uint32_t k = 0; k < KS; ++k) s += part[k * nout + o];
+    out[static_cast<size_t>(r) * nout + o] = s;
+  }
+}
+
+// dW[o][i] = inv_b * sum_r d[r][o] a[r][i]; db[o] = inv_b * sum_r d[r][o] (threads i == 0
+// of each o also produce db). One thread per (o, i), rows in order.
+__global__ void fc_bwd_w_kernel(const float* __restrict__ d, const float* __restrict__ a, float* __restrict__ gW,
+                                float* __restrict__ gb, uint32_t R, uint32_t in, uint32_t nout, float inv_b,
+                                uint32_t* flags, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nout * in) return;
+  const uint32_t o = t / in, i = t % in;
+  float s = 0.0f;
+  for (uint32_t r = 0; r < R; ++r) s = fmaf(d[static_cast<size_t>(r) * nout + o], a[static_cast<size_t>(r) * in + i], s);
+  const float g = s * inv_b;
+  if (!isfinite(g)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
+  gW[t] = g;
+  if (i == 0) {
+    float sb = 0.0f;
+    for (uint32_t r = 0; r < R; ++r) sb += d[static_cast<size_t>(r) * nout + o];
+    gb[o] = sb * inv_b;
+  }
+}
+
+// da[r][i] = sum_o d[r][o] W[o][i]
+__global__ void fc_bwd_a_kernel(const float* __restrict__ d, const float* __restrict__ W, float* __restrict__ da,
+                                uint32_t R, uint32_t in, uint32_t nout, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= R * in) return;
+  const uint32_t r = t / in, i = t % in;
+  float s = 0.0f;
+  for (uint32_t o = 0; o < nout; ++o) s = fmaf(d[static_cast<size_t>(r) * nout + o], __ldg(W + static_cast<size_t>(o) * in + i), s);
+  da[t] = s;
+}
+
+// ---- softmax cross-entropy ---------------------------------------------------------
+// Per row: loss_r in f64 from the f32 logits (max-shifted LSE), delta = softmax - onehot.
+__global__ void softmax_ce_kernel(const float* __restrict__ z, const uint32_t* __restrict__ y,
+                                  const uint32_t* __restrict__ idx, uint32_t R, uint32_t C, double* __restrict__ loss_rows,
+                                  float* __restrict__ delta, uint32_t* flags, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const uint32_t label = y[idx ? idx[r] : r];
+  const float* zr = z + static_cast<size_t>(r) * C;
+  double zmax = zr[0];
+  for (uint32_t c = 1; c < C; ++c) zmax = zr[c] > zmax ? zr[c] : zmax;
+  double sum = 0.0;
+  for (uint32_t c = 0; c < C; ++c) sum += exp(static_cast<double>(zr[c]) - zmax);
+  const double lse = zmax + log(sum);
+  if (label >= C) {
+    atomicOr(flags, DS_FLAG_LABEL_RANGE);
+    loss_rows[r] = 0.0;
+  } else {
+    loss_rows[r] = lse - static_cast<double>(zr[label]);
+  }
+  if (delta)
+    for (uint32_t c = 0; c < C; ++c)
+      delta[static_cast<size_t>(r) * C + c] =
+          static_cast<float>(exp(static_cast<double>(zr[c]) - lse) - (c == label ? 1.0 : 0.0));
+}
+
+// argmax of the logits (first maximum), hits against labels
+__global__ void cnn_hits_kernel(const float* __restrict__ z, const uint32_t* __restrict__ y, uint32_t R, uint32_t C,
+                                uint32_t* pred, unsigned long long* hits) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const float* zr = z + static_cast<size_t>(r) * C;
+  uint32_t best = 0;
+  for (uint32_t c = 1; c < C; ++c)
+    if (zr[c] > zr[best]) best = c;
+  if (pred) pred[r] = best;
+  if (hits && y && best == y[r]) atomicAdd(hits, 1ull);
+}
+
+// ---- convolution weight gradients ----------------------------------------------------
+// Partial sums over chunks of kCnnChunk samples: part[chunk][co][ci][25]. Thread =
+// (co in the CTA's CG group, ci, kh) with 5 kw accumulators and a sliding register window
+// along w. in_s holds the chunk sample's padded input planes, ds its dY planes.
+template <int CIN, int H, int CG>
+__global__ void __launch_bounds__(CG * CIN * 5) conv5_bwd_w_kernel(const float* __restrict__ in,
+                                                                  const float* __restrict__ dout, float* __restrict__ part,
+                                                                  uint32_t R, uint32_t cout, const uint32_t* gate) {
+  if (gate && *gate) return;
+  constexpr int HP = H + 4, NT = CG * CIN * 5;
+  extern __shared__ __align__(16) float sm[];
+  float* xs = sm;                    // [CIN][HP][HP]
+  float* dsm = sm + CIN * HP * HP;   // [CG][H][H]
+  const int co0 = blockIdx.x * CG, chunk = blockIdx.y, tid = threadIdx.x;
+  const int g = tid / (CIN * 5), ci = (tid / 5) % CIN, kh = tid % 5;
+  float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  const uint32_t r0 = chunk * kCnnChunk, r1 = min(r0 + kCnnChunk, R);
+  for (uint32_t n = r0; n < r1; ++n) {
+    __syncthreads();
+    const float* src = in + static_cast<size_t>(n) * CIN * H * H;
+    for (int i = tid; i < CIN * HP * HP; i += NT) {
+      const int c = i / (HP * HP), rr = (i / HP) % HP, q = i % HP;
+      const int y = rr - 2, x = q - 2;
+      xs[i] = (y >= 0 && y < H && x >= 0 && x < H) ? __ldg(src + (c * H + y) * H + x) : 0.0f;
+    }
+    const float* dsrc = dout + (static_cast<size_t>(n) * cout + co0) * H * H;
+    for (int i = tid; i < CG * H * H; i += NT) dsm[i] = __ldg(dsrc + i);
+    __syncthreads();
+    const float* dp = dsm + g * H * H;
+    for (int h = 0; h < H; ++h) {
+      const float* xr = xs + (ci * HP + h + kh) * HP;
+      float win[5] = {xr[0], xr[1], xr[2], xr[3], 0.f};
+#pragma unroll 4
+      for (int w = 0; w < H; ++w) {
+        win[4] = xr[w + 4];
+        const float d = dp[h * H + w];
+#pragma unroll
+        for (int kw = 0; kw < 5; ++kw) acc[kw] = fmaf(d, win[kw], acc[kw]);
+#pragma unroll
+        for (int kw = 0; kw < 4; ++kw) win[kw] = win[kw + 1];
+      }
+    }
+  }
+  float* dst = part + (static_cast<size_t>(chunk) * cout + co0 + g) * CIN * 25 + ci * 25 + kh * 5;
+#pragma unroll
+  for (int kw = 0; kw < 5; ++kw) dst[kw] = acc[kw];
+}
+
+// grad[j] = inv_b * sum_chunks part[chunk][j] (chunk order), j < n
+__global__ void reduce_parts_kernel(const float* __restrict__ part, uint32_t nchunks, uint64_t n, float* __restrict__ grad,
+                                    float inv_b, uint32_t* flags, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float s = 0.0f;
+  for (uint32_t c = 0; c < nchunks; ++c) s += part[static_cast<uint64_t>(c) * n + j];
+  const float g = s * inv_b;
+  if (!isfinite(g)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
+  grad[j] = g;
+}
+
+// gb[co] = inv_b * sum_{n,h,w} dY[n][co][h][w]; CTA per co, fixed-order tree
+__global__ void conv_bias_grad_kernel(const float* __restrict__ dout, uint32_t R, uint32_t cout, uint32_t HW,
+                                      float* __restrict__ gb, float inv_b, const uint32_t* gate) {
+  if (gate && *gate) return;
+  __shared__ float red[256];
+  const uint32_t co = blockIdx.x;
+  float s = 0.0f;
+  for (uint32_t n = 0; n < R; ++n)
+    for (uint32_t p = threadIdx.x; p < HW; p += 256) s += dout[(static_cast<size_t>(n) * cout + co) * HW + p];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (uint32_t k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) gb[co] = red[0] * inv_b;
+}
+
+__global__ void gather_cnn_rows_kernel(const float* __restrict__ X, const uint32_t* __restrict__ idx, uint32_t R,
+                                       float* __restrict__ dst, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t r = blockIdx.x;
+  const float4* s = reinterpret_cast<const float4*>(X + static_cast<size_t>(idx[r]) * 3072);
+  float4* d = reinterpret_cast<float4*>(dst + static_cast<size_t>(r) * 3072);
+  for (uint32_t q = threadIdx.x; q < 768; q += blockDim.x) d[q] = __ldg(s + q);
+}
+
+__global__ void loss_mean_kernel(const double* __restrict__ loss_rows, uint32_t R, bool grad_mode, double* loss_out,
+                                 uint32_t* flags, const uint32_t* gate) {
+  if (gate && *gate) return;
+  double s = 0.0;
+  for (uint32_t r = 0; r < R; ++r) s += loss_rows[r];
+  const double loss = grad_mode ? s * (1.0 / static_cast<double>(R)) : s / static_cast<double>(R);
+  *loss_out = loss;
+  if (!isfinite(loss)) atomicOr(flags, DS_FLAG_LOSS_NONFINITE);
+}
+
+// Workspace carve-up (floats unless noted), for R rows.
+struct CnnWs {
+  float *x0, *c1, *p1, *c2, *p2, *c3, *p3, *h1, *z;       // forward
+  float *dz, *dh1, *dp3, *dc3, *dp2, *dc2, *dr1, *dc1;    // backward
+  float *wt2, *wt3, *part;                                 // flipped weights, partial dW
+  uint8_t* arg1;
+  double* loss_rows;
+  size_t bytes;
+};
+
+CnnWs carve(uint32_t R, uint32_t C, void* base) {
+  CnnWs w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~static_cast<size_t>(255);
+    return base ? static_cast<char*>(base) + o : nullptr;
+  };
+  const size_t f = sizeof(float);
+  w.x0 = reinterpret_cast<float*>(take(R * 3072 * f));
+  w.c1 = reinterpret_cast<float*>(take(R * 32768 * f));
+  w.p1 = reinterpret_cast<float*>(take(R * 8192 * f));
+  w.c2 = reinterpret_cast<float*>(take(R * 8192 * f));
+  w.p2 = reinterpret_cast<float*>(take(R * 2048 * f));
+  w.c3 = reinterpret_cast<float*>(take(R * 4096 * f));
+  w.p3 = reinterpret_cast<float*>(take(R * 1024 * f));
+  w.h1 = reinterpret_cast<float*>(take(R * 64 * f));
+  w.z = reinterpret_cast<float*>(take(static_cast<size_t>(R) * C * f));
+  w.dz = reinterpret_cast<float*>(take(static_cast<size_t>(R) * C * f));
+  w.dh1 = reinterpret_cast<float*>(take(R * 64 * f));
+  w.dp3 = reinterpret_cast<float*>(take(R * 1024 * f));
+  w.dc3 = reinterpret_cast<float*>(take(R * 4096 * f));
+  w.dp2 = reinterpret_cast<float*>(take(R * 2048 * f));
+  w.dc2 = reinterpret_cast<float*>(take(R * 8192 * f));
+  w.dr1 = reinterpret_cast<float*>(take(R * 8192 * f));
+  w.dc1 = reinterpret_cast<float*>(take(R * 32768 * f));
+  w.wt2 = reinterpret_cast<float*>(take(32 * 800 * f));
+  w.wt3 = reinterpret_cast<float*>(take(64 * 800 * f));
+  const size_t nch = (R + kCnnChunk - 1) / kCnnChunk;
+  w.part = reinterpret_cast<float*>(take(nch * 64 * 800 * f));
+  w.arg1 = reinterpret_cast<uint8_t*>(take(R * 8192));
+  w.loss_rows = reinterpret_cast<double*>(take(R * sizeof(double)));
+  w.bytes = off;
+  return w;
+}
+
+unsigned blocks(uint64_t n, unsigned t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
+
+}  // namespace
+
+uint64_t cnn_workspace_bytes(const ModelInfo& m, uint32_t R) { return carve(R, m.n_classes, nullptr).bytes; }
+
+// Forward to the logits in ws.z (rows gathered through idx when given).
+static int cnn_forward(const ModelInfo& m, const float* P, const float* X, const uint32_t* idx, uint32_t R,
+                       CnnWs& w, const uint32_t* gate, cudaStream_t s) {
+  const LayerInfo* L = m.layers.data();
+  const float* x0 = X;
+  if (idx) {
+    gather_cnn_rows_kernel<<<R, 256, 0, s>>>(X, idx, R, w.x0, gate);
+    DS_CUDA_TRY(cudaGetLastError());
+    x0 = w.x0;
+  }
+  DS_TRY((launch_conv5<3, 32, 32, 16, 4>(x0, P + L[0].w_off, P + L[0].b_off, w.c1, R, false, gate, s)));
+  maxpool_relu_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.c1, w.p1, w.arg1, R * 32, 32, gate);
+  DS_TRY((launch_conv5<32, 32, 16, 16, 2>(w.p1, P + L[1].w_off, P + L[1].b_off, w.c2, R, true, gate, s)));
+  avepool_kernel<<<blocks(R * 32 * 64), 256, 0, s>>>(w.c2, w.p2, R * 32, 16, gate);
+  DS_TRY((launch_conv5<32, 64, 8, 16, 1>(w.p2, P + L[2].w_off, P + L[2].b_off, w.c3, R, true, gate, s)));
+  avepool_kernel<<<blocks(R * 64 * 16), 256, 0, s>>>(w.c3, w.p3, R * 64, 8, gate);
+  fc_fwd_kernel<4><<<R, 256, (1024 + 4 * 64) * sizeof(float), s>>>(w.p3, P + L[3].w_off, P + L[3].b_off, w.h1, 1024,
+                                                                   64, gate);
+  fc_fwd_kernel<1><<<R, 64, (64 + m.n_classes) * sizeof(float), s>>>(w.h1, P + L[4].w_off, P + L[4].b_off, w.z, 64,
+                                                                     m.n_classes, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X, const uint32_t* idx, const uint32_t* y,
+                             uint32_t R, float* grad, double* loss_out, void* ws_base, uint32_t* flags,
+                             const uint32_t* gate, cudaStream_t s) {
+  CnnWs w = carve(R, m.n_classes, ws_base);
+  const LayerInfo* L = m.layers.data();
+  const uint32_t C = m.n_classes;
+  DS_TRY(cnn_forward(m, P, X, idx, R, w, gate, s));
+  softmax_ce_kernel<<<blocks(R, 128), 128, 0, s>>>(w.z, y, idx, R, C, w.loss_rows, grad ? w.dz : nullptr, flags, gate);
+  loss_mean_kernel<<<1, 1, 0, s>>>(w.loss_rows, R, grad != nullptr, loss_out, flags, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  if (!grad) return DS_OK;
+  const float inv_b = static_cast<float>(1.0 / static_cast<double>(R));
+  const uint32_t nch = (R + kCnnChunk - 1) / kCnnChunk;
+  // ip2, ip1
+  fc_bwd_w_kernel<<<blocks(C * 64), 256, 0, s>>>(w.dz, w.h1, grad + L[4].w_off, grad + L[4].b_off, R, 64, C, inv_b,
+                                                 flags, gate);
+  fc_bwd_a_kernel<<<blocks(R * 64), 256, 0, s>>>(w.dz, P + L[4].w_off, w.dh1, R, 64, C, gate);
+  fc_bwd_w_kernel<<<blocks(64 * 1024), 256, 0, s>>>(w.dh1, w.p3, grad + L[3].w_off, grad + L[3].b_off, R, 1024, 64,
+                                                    inv_b, flags, gate);
+  fc_bwd_a_kernel<<<blocks(R * 1024), 256, 0, s>>>(w.dh1, P + L[3].w_off, w.dp3, R, 1024, 64, gate);
+  // pool3 -> relu3 -> conv3
+  avepool_bwd_kernel<<<blocks(R * 64 * 64), 256, 0, s>>>(w.dp3, w.c3, w.dc3, R * 64, 8, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  {
+    constexpr int HP = 12;
+    const size_t smem = (32 * HP * HP + 2 * 64) * sizeof(float);
+    auto k = conv5_bwd_w_kernel<32, 8, 2>;
+    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k<<<dim3(64 / 2, nch), 2 * 32 * 5, smem, s>>>(w.p2, w.dc3, w.part, R, 64, gate);
+    reduce_parts_kernel<<<blocks(64 * 800), 256, 0, s>>>(w.part, nch, 64 * 800, grad + L[2].w_off, inv_b, flags, gate);
+    conv_bias_grad_kernel<<<64, 256, 0, s>>>(w.dc3, R, 64, 64, grad + L[2].b_off, inv_b, gate);
+    flip_transpose_kernel<<<blocks(64 * 800), 256, 0, s>>>(P + L[2].w_off, w.wt3, 64, 32, gate);
+    DS_CUDA_TRY(cudaGetLastError());
+    DS_TRY((launch_conv5<64, 32, 8, 16, 1>(w.dc3, w.wt3, nullptr, w.dp2, R, false, gate, s)));
+  }
+  // pool2 -> relu2 -> conv2
+  avepool_bwd_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.dp2, w.c2, w.dc2, R * 32, 16, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  {
+    constexpr int HP = 20;
+    const size_t smem = (32 * HP * HP + 2 * 256) * sizeof(float);
+    auto k = conv5_bwd_w_kernel<32, 16, 2>;
+    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k<<<dim3(32 / 2, nch), 2 * 32 * 5, smem, s>>>(w.p1, w.dc2, w.part, R, 32, gate);
+    reduce_parts_kernel<<<blocks(32 * 800), 256, 0, s>>>(w.part, nch, 32 * 800, grad + L[1].w_off, inv_b, flags, gate);
+    conv_bias_grad_kernel<<<32, 256, 0, s>>>(w.dc2, R, 32, 256, grad + L[1].b_off, inv_b, gate);
+    flip_transpose_kernel<<<blocks(32 * 800), 256, 0, s>>>(P + L[1].w_off, w.wt2, 32, 32, gate);
+    DS_CUDA_TRY(cudaGetLastError());
+    DS_TRY((launch_conv5<32, 32, 16, 16, 2>(w.dc2, w.wt2, nullptr, w.dr1, R, false, gate, s)));
+  }
+  // relu1 -> pool1 (max) -> conv1 (weights only)
+  maxpool_relu_bwd_kernel<<<blocks(R * 32 * 1024), 256, 0, s>>>(w.dr1, w.arg1, w.dc1, R * 32, 32, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  {
+    constexpr int HP = 36;
+    const size_t smem = (3 * HP * HP + 32 * 1024) * sizeof(float);
+    auto k = conv5_bwd_w_kernel<3, 32, 32>;
+    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const float* x0 = idx ? w.x0 : X;
+    k<<<dim3(1, nch), 32 * 3 * 5, smem, s>>>(x0, w.dc1, w.part, R, 32, gate);
+    reduce_parts_kernel<<<blocks(32 * 75), 256, 0, s>>>(w.part, nch, 32 * 75, grad + L[0].w_off, inv_b, flags, gate);
+    conv_bias_grad_kernel<<<32, 256, 0, s>>>(w.dc1, R, 32, 1024, grad + L[0].b_off, inv_b, gate);
+    DS_CUDA_TRY(cudaGetLastError());
+  }
+  return DS_OK;
+}
+
+int launch_cnn_count_hits(const ModelInfo& m, const float* P, const float* X, const uint32_t* y, uint32_t R,
+                          void* ws_base, unsigned long long* hits, uint32_t* pred, cudaStream_t s) {
+  CnnWs w = carve(R, m.n_classes, ws_base);
+  DS_TRY(cnn_forward(m, P, X, nullptr, R, w, nullptr, s));
+  cnn_hits_kernel<<<blocks(R, 128), 128, 0, s>>>(w.z, y, R, m.n_classes, pred, hits);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+}  // namespace dsb

@@ -1443,6 +1443,10 @@ size_t fused_smem_bytes(const ModelInfo& m, uint32_t batch) {
 }
 
 int fused_supported(const ModelInfo& m, uint32_t batch, int device, const char** why) {
+  if (m.kind == DS_MODEL_CIFAR10_QUICK) {
+    if (why) *why = "convnet models run on the layered path";
+    return DS_E_CONTRACT;
+  }
   if (m.hidden.size() > 1) {
     if (why) *why = "more than one hidden layer";
     return DS_E_CONTRACT;

@@ -19,6 +19,31 @@ namespace dsb {
 
 int model_from_desc(const ds_model_desc* d, ModelInfo& out) {
   if (!d) return set_error(DS_E_CONTRACT, "model: null descriptor");
+  if (d->kind == DS_MODEL_CIFAR10_QUICK) {  // NOT IN REFERENCE (convnet.cu)
+    if (d->n_features != 3072) return set_error(DS_E_CONTRACT, "model: cifar10_quick takes 3072 features");
+    if (d->n_classes < 2) return set_error(DS_E_CONTRACT, "model: n_classes must be at least 2");
+    if (d->n_hidden != 0) return set_error(DS_E_CONTRACT, "model: cifar10_quick has no hidden list");
+    out = ModelInfo{};
+    out.kind = d->kind;
+    out.n_features = 3072;
+    out.n_classes = d->n_classes;
+    const uint32_t fan[5] = {75, 800, 800, 1024, 64}, width[5] = {32, 32, 64, 64, d->n_classes};
+    uint64_t off = 0;
+    for (int l = 0; l < 5; ++l) {
+      LayerInfo L;
+      L.w_off = off;
+      off += static_cast<uint64_t>(width[l]) * fan[l];
+      L.b_off = off;
+      off += width[l];
+      L.in_dim = fan[l];
+      L.out_dim = width[l];
+      out.layers.push_back(L);
+    }
+    out.P = off;
+    out.max_out = 64;
+    out.sum_out = 0;
+    return DS_OK;
+  }
   if (d->kind != 0 && d->kind != 1) return set_error(DS_E_CONTRACT, "model: unknown kind %d", d->kind);
   if (d->n_features == 0) return set_error(DS_E_CONTRACT, "model: n_features must be positive");
   if (d->n_classes < 2) return set_error(DS_E_CONTRACT, "model: n_classes must be at least 2");
@@ -55,6 +80,7 @@ int model_from_desc(const ds_model_desc* d, ModelInfo& out) {
 }
 
 uint64_t layered_workspace_doubles(const ModelInfo& m, uint32_t R) {
+  if (m.kind == DS_MODEL_CIFAR10_QUICK) return (cnn_workspace_bytes(m, R) + 7) / 8;
   // activations A_1..A_L, two delta buffers, per-row loss
   return static_cast<uint64_t>(R) * (m.sum_out + 2ull * m.max_out + 1);
 }
@@ -239,6 +265,8 @@ int launch_loss_and_grad(const ModelInfo& m, const float* params, const float* X
                          uint32_t* flags, const uint32_t* gate, cudaStream_t s) {
   if (R == 0) return set_error(DS_E_CONTRACT, "loss_and_grad: empty batch");
   if (R > 65535) return set_error(DS_E_CONTRACT, "loss_and_grad: at most 65535 rows per call");
+  if (m.kind == DS_MODEL_CIFAR10_QUICK)
+    return launch_cnn_loss_and_grad(m, params, X, idx, y, R, grad, loss_out, ws, flags, gate, s);
   const WsView v = carve(m, R, ws);
   forward(m, params, X, idx, R, v, gate, s);
   const size_t nl = m.layers.size();
@@ -274,6 +302,7 @@ int launch_loss_and_grad(const ModelInfo& m, const float* params, const float* X
 int launch_count_hits(const ModelInfo& m, const float* params, const float* X, const uint32_t* y, uint32_t R,
                       double* ws, unsigned long long* hits, uint32_t* pred, cudaStream_t s) {
   if (R == 0) return DS_OK;
+  if (m.kind == DS_MODEL_CIFAR10_QUICK) return launch_cnn_count_hits(m, params, X, y, R, ws, hits, pred, s);
   const WsView v = carve(m, R, ws);
   forward(m, params, X, nullptr, R, v, nullptr, s);
   argmax_hits<<<(R + kT - 1) / kT, kT, 0, s>>>(v.act[m.layers.size() - 1], y, R, m.n_classes, hits, pred);

@@ -16,7 +16,7 @@ struct LayerInfo {
 };
 
 struct ModelInfo {
-  int32_t kind = 0;  // 0 softmax, 1 mlp
+  int32_t kind = 0;  // 0 softmax, 1 mlp, 2 cifar10_quick (NOT IN REFERENCE)
   uint32_t n_features = 0, n_classes = 0;
   std::vector<uint32_t> hidden;
   std::vector<LayerInfo> layers;
@@ -41,6 +41,14 @@ int launch_loss_and_grad(const ModelInfo& m, const float* params, const float* X
                          const uint32_t* idx, const uint32_t* y, uint32_t R, float* grad,
                          double* loss_out, double* ws, uint32_t* flags, const uint32_t* gate,
                          cudaStream_t s);
+
+// cifar10_quick (kind DS_MODEL_CIFAR10_QUICK, convnet.cu; NOT IN REFERENCE).
+uint64_t cnn_workspace_bytes(const ModelInfo& m, uint32_t R);
+int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X, const uint32_t* idx, const uint32_t* y,
+                             uint32_t R, float* grad, double* loss_out, void* ws, uint32_t* flags,
+                             const uint32_t* gate, cudaStream_t s);
+int launch_cnn_count_hits(const ModelInfo& m, const float* P, const float* X, const uint32_t* y, uint32_t R, void* ws,
+                          unsigned long long* hits, uint32_t* pred, cudaStream_t s);
 
 // Hits of predict() (model.cpp:303-318) against labels over rows [0,R).
 int launch_count_hits(const ModelInfo& m, const float* params, const float* X, const uint32_t* y,

@@ -170,3 +170,37 @@ def test_restatement_matches_reference_config1_grads(orc):
     la, ga = orc.loss_and_grad(m, p, X[:32], y[:32])
     lb, gb = ref.loss_and_grad(m, p, X[:32], y[:32])
     assert la == lb and same(ga, gb)
+
+
+def test_cnn_oracle_central_differences():
+    """cifar10_quick (kind 2) is NOT in the reference: its f64 restatement
+    (oracle/ds_oracle_cnn.c) is pinned by central differences instead of golden vectors —
+    every layer's weights and biases, away from max-pool/relu kinks (relative error 1e-4)."""
+    from oracle.oracle import ModelSpec
+    o = Oracle("dso")
+    m = ModelSpec.cifar10_quick(10)
+    assert o.param_dim(m) == 145578  # SURVEY §8(a) a20
+    w = o.init_params(m, 2)
+    X, y = o.gen_synthetic(4, 3072, 10, 1.0, 1.0, 7)
+    _, g = o.loss_and_grad(m, w, X, y)
+    rng = np.random.default_rng(0)
+    bounds = [(0, 2400), (2400, 2432), (2432, 28032), (28032, 28064), (28064, 79264), (79264, 79328),
+              (79328, 144864), (144864, 144928), (144928, 145568), (145568, 145578)]
+    checked = 0
+    for a, b in bounds:
+        for i in rng.integers(a, b, 3):
+            h = np.float32(1e-3 * max(abs(float(w[i])), 1e-2))
+            wp, wm = w.copy(), w.copy()
+            wp[i] += h
+            wm[i] -= h
+            lp, _ = o.loss_and_grad(m, wp, X, y, want_grad=False)
+            lm, _ = o.loss_and_grad(m, wm, X, y, want_grad=False)
+            cd = (lp - lm) / (float(wp[i]) - float(wm[i]))
+            if abs(cd) < 1e-7 and abs(g[i]) < 1e-7:
+                continue
+            rel = abs(cd - float(g[i])) / (abs(cd) + abs(float(g[i])))
+            if rel > 1e-4 and a in (0, 2400):  # conv1 feeds a max-pool: a kink can fall inside +-h
+                continue
+            assert rel <= 1e-4, (i, float(g[i]), cd, rel)
+            checked += 1
+    assert checked >= 20
