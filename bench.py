@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=500)
     ap.add_argument("--exchange-params", type=int, default=256 * 1024 * 1024)
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / exchange sweep / cpu baseline (profiling)")
+    ap.add_argument("--cifar-steps", type=int, default=200, help="timed steps of the cifar10_quick leg (0 = skip)")
     return ap.parse_args()
 
 
@@ -284,6 +285,8 @@ def main():
     if not args.no_extras:
         line["e2e"] = e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n)
         line["exchange"] = exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind)
+        if args.cifar_steps > 0:
+            line["cifar10_quick"] = cifar_leg(args, L, api, torch, dist, world, rank, local)
         if rank == 0 and world == 1:
             line["cpu_baseline"] = cpu_baseline(args, X, y)
     L.lib.ds_engine_destroy(eng)
@@ -298,34 +301,41 @@ def main():
 
 
 def e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n):
-    """Same loop through the C-ABI with HOST buffers: per step, the batch rows are gathered
+    """Same loop through the C-ABI with HOST buffers: per step the batch rows are gathered
     on the host (the reference's ShardSweeper order) into pinned memory, copied in, one
-    iteration runs (exchange every tau), and the batch loss is read back."""
+    iteration runs (exchange every tau), and the batch loss is copied back — pipelined
+    (ds_engine_step_host_async, double-buffered staging) so step s+1's host gather and H2D
+    overlap step s on the device. Every step's H2D and loss D2H are inside the timed region."""
     import torch
     import torch.distributed as dist
     K = min(args.e2e_steps, args.steps)
     B = args.batch
     idx, sizes = api.sweep_batches(len(y), B, sweep_seed + 1, K)
-    Xp = torch.empty((B, F), dtype=torch.float32, pin_memory=True)
-    yp = torch.empty(B, dtype=torch.int32, pin_memory=True)
-    Xn, yn = Xp.numpy(), yp.numpy().view(np.uint32)
-    loss = C.c_double()
+    Xp = [torch.empty((B, F), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    yp = [torch.empty(B, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    Xn = [t.numpy() for t in Xp]
+    yn = [t.numpy().view(np.uint32) for t in yp]
+    losses = torch.zeros(K, dtype=torch.float64, pin_memory=True)
+    lbase = losses.data_ptr()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for s in range(K):
-        r = int(sizes[s])
-        np.take(X, idx[s, :r], axis=0, out=Xn[:r])
-        np.take(y, idx[s, :r], out=yn[:r])
-        L.check(L.lib.ds_engine_step_host(eng, C.c_void_p(Xp.data_ptr()), C.c_void_p(yp.data_ptr()), r,
-                                          C.byref(loss)))
+        r, k = int(sizes[s]), s & 1
+        np.take(X, idx[s, :r], axis=0, out=Xn[k][:r])
+        np.take(y, idx[s, :r], out=yn[k][:r])
+        L.check(L.lib.ds_engine_step_host_async(eng, C.c_void_p(Xp[k].data_ptr()), C.c_void_p(yp[k].data_ptr()), r,
+                                                C.c_void_p(lbase + 8 * s)))
+    L.check(L.lib.ds_engine_sync(eng))
     secs = time.perf_counter() - t0
+    ok = bool(np.isfinite(losses.numpy()).all())
     t = torch.tensor([secs], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return {"value": n * B * K / t.item(), "unit": "samples/s", "h2d_bytes_per_step": B * F * 4 + B * 4 + 4,
-            "d2h_bytes_per_step": 8, "steps": K,
-            "path": "ds_engine_step_host: pinned-host batch H2D + fused step (+exchange) + loss D2H, per step"}
+            "d2h_bytes_per_step": 8, "steps": K, "losses_finite": ok,
+            "path": "ds_engine_step_host_async: host gather into pinned memory + H2D + fused step (+exchange) + "
+                    "loss D2H every step, double-buffered; wall clock from first enqueue to final sync"}
 
 
 def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind):
@@ -388,6 +398,75 @@ def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind):
         dist.barrier()
         L.lib.ds_master_destroy(mh)
     return out
+
+
+def cifar_leg(args, L, api, torch, dist, world, rank, local):
+    """BASELINE config 2 shape: Caffe cifar10_quick on synthetic 3x32x32 CIFAR-10-shaped
+    data, async EASGD tau=10, batch 100 per worker, one worker per GPU, center sharded
+    over the GPUs (LockFree). NOT IN THE REFERENCE (no conv layers): f32 layered kernels
+    (csrc/convnet.cu), no CPU reference arm. Device-timed, max over ranks."""
+    from paper_1602_08191_b200 import dist as D
+    B, K, N = 100, args.cifar_steps, 10000
+    Xc, yc = api.gen_synthetic(N, 3072, 10, 1.0, 1.0, 101 + rank)
+    Pc = 145578
+    init = torch.empty(Pc, dtype=torch.float32, device="cuda")
+    if rank == 0:
+        from paper_1602_08191_b200.deepspark import Model
+        init.copy_(torch.from_numpy(api.init_params(Model.cifar10_quick(10), INIT_SEED)))
+    if world > 1:
+        dist.broadcast(init, 0)
+    torch.cuda.synchronize()
+    if world == 1:
+        m = C.c_void_p()
+        L.check(L.lib.ds_master_create(C.byref(m), local, Pc, C.c_float(0.1), L.DS_MODE_LOCKFREE,
+                                       C.c_void_p(init.data_ptr())))
+    else:
+        m = D.sharded_master(L, local, Pc, 0.1, L.DS_MODE_LOCKFREE, init.data_ptr(), rank, world)
+    hidden = (C.c_uint32 * 1)(0)
+    desc = L.ds_model_desc(2, 3072, 10, 0, hidden)
+    hp = L.ds_hyper(0.01, 0.1, 10, B, 10 ** 9, 0.0, 0.0, 0)
+    eng = C.c_void_p()
+    L.check(L.lib.ds_engine_create(C.byref(eng), local, C.byref(desc), Xc.ctypes.data, yc.ctypes.data, len(yc), 10,
+                                   C.byref(hp), api.mix_seed(5, rank), C.c_void_p(init.data_ptr()), L.DS_ENGINE_AUTO))
+    L.check(L.lib.ds_engine_attach_master(eng, m))
+    L.check(L.lib.ds_engine_reserve(eng, K + 5))
+    L.check(L.lib.ds_engine_run(eng, 5, 0, None))
+    L.check(L.lib.ds_engine_sync(eng))
+    sp = C.c_void_p()
+    L.check(L.lib.ds_engine_stream(eng, C.byref(sp)))
+    st = torch.cuda.ExternalStream(sp.value)
+    n0 = C.c_uint64()
+    L.check(L.lib.ds_engine_launches(eng, C.byref(n0)))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    L.check(L.lib.ds_engine_run(eng, K, 0, None))
+    e1.record(st)
+    L.check(L.lib.ds_engine_sync(eng))
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n1 = C.c_uint64()
+    L.check(L.lib.ds_engine_launches(eng, C.byref(n1)))
+    loss = np.zeros(K + 5)
+    L.check(L.lib.ds_engine_log(eng, 0, K + 5, loss.ctypes.data, None, None, None))
+    L.lib.ds_engine_destroy(eng)
+    if world > 1:
+        dist.barrier()
+    L.lib.ds_master_destroy(m)
+    ms = t.item()
+    flop = 3 * 2 * 12_350_000 * B * K  # ~3x forward (fwd + dgrad + wgrad), 2 FLOP/MAC
+    return {"metric": "train samples/s (cifar10_quick, BASELINE config 2 shape)", "value": world * B * K / (ms / 1e3),
+            "unit": "samples/s", "ms_per_step": ms / K, "steps": K, "batch_per_worker": B, "tau": 10, "alpha": 0.1,
+            "eta": 0.01, "workers": world, "exchange": "LockFree, center sharded over the GPUs" if world > 1 else
+            "LockFree, center on the same GPU", "dtype": "f32 (CUDA-core FFMA)", "data": "synthetic gen_synthetic "
+            "3072 features (3x32x32 CHW), 10 classes, 10,000 rows per GPU",
+            "achieved_tflops": flop / (ms / 1e3) / 1e12, "gpu_launches": int(n1.value - n0.value),
+            "loss_first_last": [float(loss[0]), float(loss[-1])],
+            "reference_arm": "none: the reference has no conv layers (SURVEY §8 a20)"}
 
 
 def cpu_baseline(args, X, y):

@@ -256,6 +256,12 @@ int ds_engine_reserve(ds_engine* e, uint64_t steps);
  * batch loss back (synchronous). The engine's own sweep position is not advanced. */
 int ds_engine_step_host(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows,
                         double* loss_host);
+/* Pipelined form of ds_engine_step_host: the same iteration, enqueued without waiting.
+ * Staging is double-buffered: X_host/y_host may be refilled two calls later, and
+ * *loss_host (pinned for an asynchronous copy) is valid after ds_engine_sync or two
+ * calls later. The host blocks only when it runs two iterations ahead of the device. */
+int ds_engine_step_host_async(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows,
+                              double* loss_host);
 /* Block until the engine's queued work finished; returns DS_E_NUMERIC/DS_E_CONTRACT
  * if any step hit the reference's error conditions (message names the iteration). */
 int ds_engine_sync(ds_engine* e);

@@ -16,31 +16,36 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "ds_common.cuh"
 #include "model.cuh"
 
 namespace dsb {
 namespace {
 
-constexpr int kCnnChunk = 4;  // samples per partial weight-gradient block
 
 __device__ __forceinline__ uint32_t pooled(uint32_t H) { return (H - 3 + 1) / 2 + 1; }  // ceil((H-3)/2)+1
 
 // ---- 5x5 pad-2 stride-1 convolution (also used for backward-data with flipped,
 // transposed weights). One CTA = one sample x COB output channels; a thread owns PPT
-// consecutive pixels of a row for all COB channels. The padded input planes and the
-// CTA's weights (transposed to [k][COB] so one LDS.128 feeds 4 channels) live in smem.
-template <int CIN, int COUT, int H, int COB, int PPT>
-__global__ void __launch_bounds__(H * H / PPT) conv5_kernel(const float* __restrict__ in, const float* __restrict__ W,
-                                                            const float* __restrict__ bias, float* __restrict__ out,
-                                                            bool relu, const uint32_t* gate) {
+// consecutive pixels of a row for all COB channels over a 1/KS slice of the input
+// channels (the KS partial sums are combined in a fixed order through smem). The padded
+// input planes and the CTA's weights (transposed to [k][COB] so one LDS.128 feeds 4
+// channels) live in smem.
+template <int CIN, int COUT, int H, int COB, int PPT, int KS>
+__global__ void __launch_bounds__(H * H / PPT * KS) conv5_kernel(const float* __restrict__ in,
+                                                                 const float* __restrict__ W,
+                                                                 const float* __restrict__ bias,
+                                                                 float* __restrict__ out, bool relu,
+                                                                 const uint32_t* gate) {
   if (gate && *gate) return;
-  constexpr int HP = H + 4, K = CIN * 25;
+  constexpr int HP = H + 4, K = CIN * 25, NPT = H * H / PPT, NT = NPT * KS, CPK = CIN / KS;
+  static_assert(CIN % KS == 0 && COB % 4 == 0, "conv5 tiling");
   extern __shared__ __align__(16) float sm[];
   float* xs = sm;                 // [CIN][HP][HP]
   float* ws = sm + CIN * HP * HP;  // [K][COB]
   const int n = blockIdx.x, co0 = blockIdx.y * COB, tid = threadIdx.x;
-  constexpr int NT = H * H / PPT;
   const float* src = in + static_cast<size_t>(n) * CIN * H * H;
   for (int i = tid; i < CIN * HP * HP; i += NT) {
     const int c = i / (HP * HP), r = (i / HP) % HP, q = i % HP;
@@ -52,13 +57,14 @@ __global__ void __launch_bounds__(H * H / PPT) conv5_kernel(const float* __restr
     ws[i] = __ldg(W + static_cast<size_t>(co0 + c) * K + k);
   }
   __syncthreads();
-  const int p0 = tid * PPT, h = p0 / H, w0 = p0 % H;
+  const int ks = tid / NPT, pt = tid % NPT;
+  const int p0 = pt * PPT, h = p0 / H, w0 = p0 % H;
   float acc[COB][PPT];
 #pragma unroll
   for (int c = 0; c < COB; ++c)
 #pragma unroll
     for (int j = 0; j < PPT; ++j) acc[c][j] = 0.0f;
-  for (int ci = 0; ci < CIN; ++ci) {
+  for (int ci = ks * CPK; ci < (ks + 1) * CPK; ++ci) {
 #pragma unroll
     for (int kh = 0; kh < 5; ++kh) {
       const float* xr = xs + (ci * HP + h + kh) * HP + w0;
@@ -82,6 +88,24 @@ __global__ void __launch_bounds__(H * H / PPT) conv5_kernel(const float* __restr
       }
     }
   }
+  if constexpr (KS > 1) {  // combine the K-split partials (slice order) through smem
+    __syncthreads();
+    float* red = sm;  // [KS][COB][H*H], fits in the input planes
+#pragma unroll
+    for (int c = 0; c < COB; ++c)
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) red[(ks * COB + c) * H * H + p0 + j] = acc[c][j];
+    __syncthreads();
+    if (ks != 0) return;
+#pragma unroll
+    for (int c = 0; c < COB; ++c)
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        float v = red[c * H * H + p0 + j];
+        for (int k = 1; k < KS; ++k) v += red[(k * COB + c) * H * H + p0 + j];
+        acc[c][j] = v;
+      }
+  }
   float* dst = out + static_cast<size_t>(n) * COUT * H * H;
 #pragma unroll
   for (int c = 0; c < COB; ++c) {
@@ -95,14 +119,19 @@ __global__ void __launch_bounds__(H * H / PPT) conv5_kernel(const float* __restr
   }
 }
 
-template <int CIN, int COUT, int H, int COB, int PPT>
+template <int CIN, int COUT, int H, int COB, int PPT, int KS>
 int launch_conv5(const float* in, const float* W, const float* b, float* out, uint32_t R, bool relu,
                  const uint32_t* gate, cudaStream_t s) {
   constexpr int HP = H + 4;
+  static_assert(KS == 1 || CIN * HP * HP >= KS * COB * H * H, "K-split combine must fit in the input planes");
   const size_t smem = (static_cast<size_t>(CIN) * HP * HP + static_cast<size_t>(CIN) * 25 * COB) * sizeof(float);
-  auto k = conv5_kernel<CIN, COUT, H, COB, PPT>;
-  DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  k<<<dim3(R, COUT / COB), H * H / PPT, smem, s>>>(in, W, b, out, relu, gate);
+  auto k = conv5_kernel<CIN, COUT, H, COB, PPT, KS>;
+  static bool attr = false;  // per instantiation, once per process
+  if (!attr) {
+    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = true;
+  }
+  k<<<dim3(R, COUT / COB), H * H / PPT * KS, smem, s>>>(in, W, b, out, relu, gate);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
@@ -293,37 +322,44 @@ __global__ void cnn_hits_kernel(const float* __restrict__ z, const uint32_t* __r
   if (hits && y && best == y[r]) atomicAdd(hits, 1ull);
 }
 
-// ---- convolution weight gradients ----------------------------------------------------
-// Partial sums over chunks of kCnnChunk samples: part[chunk][co][ci][25]. Thread =
-// (co in the CTA's CG group, ci, kh) with 5 kw accumulators and a sliding register window
-// along w. in_s holds the chunk sample's padded input planes, ds its dY planes.
-template <int CIN, int H, int CG>
+// ---- convolution weight (and bias) gradients ----------------------------------------
+// Partial sums over chunks of CHUNK samples: part[chunk][co][ci][25] and pb[chunk][co].
+// Thread = (co in the CTA's CG group, ci, kh) with 5 kw accumulators and a sliding
+// register window along w. xs holds the sample's padded input planes (row stride HP+1,
+// plane stride odd: the (ci, kh) lanes of a warp land in different banks), dsm its dY
+// planes. The bias partial of each co is a strided per-thread sum plus a fixed-order
+// combine over the group's threads.
+template <int CIN, int H, int CG, int CHUNK>
 __global__ void __launch_bounds__(CG * CIN * 5) conv5_bwd_w_kernel(const float* __restrict__ in,
                                                                   const float* __restrict__ dout, float* __restrict__ part,
-                                                                  uint32_t R, uint32_t cout, const uint32_t* gate) {
+                                                                  float* __restrict__ pb, uint32_t R, uint32_t cout,
+                                                                  const uint32_t* gate) {
   if (gate && *gate) return;
-  constexpr int HP = H + 4, NT = CG * CIN * 5;
+  constexpr int HP = H + 4, RS = HP + 1, PS = RS * HP + 1, NT = CG * CIN * 5, GT = CIN * 5;
   extern __shared__ __align__(16) float sm[];
-  float* xs = sm;                    // [CIN][HP][HP]
-  float* dsm = sm + CIN * HP * HP;   // [CG][H][H]
+  float* xs = sm;                   // [CIN][HP][RS] (plane stride PS)
+  float* dsm = sm + CIN * PS;       // [CG][H][H]
+  float* bred = dsm + CG * H * H;   // [NT]
   const int co0 = blockIdx.x * CG, chunk = blockIdx.y, tid = threadIdx.x;
-  const int g = tid / (CIN * 5), ci = (tid / 5) % CIN, kh = tid % 5;
+  const int g = tid / GT, ci = (tid / 5) % CIN, kh = tid % 5, gl = tid % GT;
   float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-  const uint32_t r0 = chunk * kCnnChunk, r1 = min(r0 + kCnnChunk, R);
+  float bacc = 0.0f;
+  const uint32_t r0 = chunk * CHUNK, r1 = min(r0 + CHUNK, R);
   for (uint32_t n = r0; n < r1; ++n) {
     __syncthreads();
     const float* src = in + static_cast<size_t>(n) * CIN * H * H;
     for (int i = tid; i < CIN * HP * HP; i += NT) {
       const int c = i / (HP * HP), rr = (i / HP) % HP, q = i % HP;
       const int y = rr - 2, x = q - 2;
-      xs[i] = (y >= 0 && y < H && x >= 0 && x < H) ? __ldg(src + (c * H + y) * H + x) : 0.0f;
+      xs[c * PS + rr * RS + q] = (y >= 0 && y < H && x >= 0 && x < H) ? __ldg(src + (c * H + y) * H + x) : 0.0f;
     }
     const float* dsrc = dout + (static_cast<size_t>(n) * cout + co0) * H * H;
     for (int i = tid; i < CG * H * H; i += NT) dsm[i] = __ldg(dsrc + i);
     __syncthreads();
     const float* dp = dsm + g * H * H;
+    for (int p = gl; p < H * H; p += GT) bacc += dp[p];
     for (int h = 0; h < H; ++h) {
-      const float* xr = xs + (ci * HP + h + kh) * HP;
+      const float* xr = xs + ci * PS + (h + kh) * RS;
       float win[5] = {xr[0], xr[1], xr[2], xr[3], 0.f};
 #pragma unroll 4
       for (int w = 0; w < H; ++w) {
@@ -339,6 +375,30 @@ __global__ void __launch_bounds__(CG * CIN * 5) conv5_bwd_w_kernel(const float* 
   float* dst = part + (static_cast<size_t>(chunk) * cout + co0 + g) * CIN * 25 + ci * 25 + kh * 5;
 #pragma unroll
   for (int kw = 0; kw < 5; ++kw) dst[kw] = acc[kw];
+  bred[tid] = bacc;
+  __syncthreads();
+  if (gl == 0) {
+    float b = 0.0f;
+    for (int k = 0; k < GT; ++k) b += bred[g * GT + k];
+    pb[static_cast<size_t>(chunk) * cout + co0 + g] = b;
+  }
+}
+
+template <int CIN, int H, int CG, int CHUNK>
+int launch_conv5_bwd_w(const float* in, const float* dout, float* part, float* pb, uint32_t R, uint32_t cout,
+                       const uint32_t* gate, cudaStream_t s) {
+  constexpr int HP = H + 4, PS = (HP + 1) * HP + 1;
+  const size_t smem = (static_cast<size_t>(CIN) * PS + CG * H * H + CG * CIN * 5) * sizeof(float);
+  auto k = conv5_bwd_w_kernel<CIN, H, CG, CHUNK>;
+  static bool attr = false;
+  if (!attr) {
+    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = true;
+  }
+  const uint32_t nch = (R + CHUNK - 1) / CHUNK;
+  k<<<dim3(cout / CG, nch), CG * CIN * 5, smem, s>>>(in, dout, part, pb, R, cout, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
 }
 
 // grad[j] = inv_b * sum_chunks part[chunk][j] (chunk order), j < n
@@ -352,24 +412,6 @@ __global__ void reduce_parts_kernel(const float* __restrict__ part, uint32_t nch
   const float g = s * inv_b;
   if (!isfinite(g)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
   grad[j] = g;
-}
-
-// gb[co] = inv_b * sum_{n,h,w} dY[n][co][h][w]; CTA per co, fixed-order tree
-__global__ void conv_bias_grad_kernel(const float* __restrict__ dout, uint32_t R, uint32_t cout, uint32_t HW,
-                                      float* __restrict__ gb, float inv_b, const uint32_t* gate) {
-  if (gate && *gate) return;
-  __shared__ float red[256];
-  const uint32_t co = blockIdx.x;
-  float s = 0.0f;
-  for (uint32_t n = 0; n < R; ++n)
-    for (uint32_t p = threadIdx.x; p < HW; p += 256) s += dout[(static_cast<size_t>(n) * cout + co) * HW + p];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (uint32_t k = 128; k > 0; k >>= 1) {
-    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) gb[co] = red[0] * inv_b;
 }
 
 __global__ void gather_cnn_rows_kernel(const float* __restrict__ X, const uint32_t* __restrict__ idx, uint32_t R,
@@ -395,7 +437,7 @@ __global__ void loss_mean_kernel(const double* __restrict__ loss_rows, uint32_t 
 struct CnnWs {
   float *x0, *c1, *p1, *c2, *p2, *c3, *p3, *h1, *z;       // forward
   float *dz, *dh1, *dp3, *dc3, *dp2, *dc2, *dr1, *dc1;    // backward
-  float *wt2, *wt3, *part;                                 // flipped weights, partial dW
+  float *wt2, *wt3, *part, *pb;                            // flipped weights, partial dW / db
   uint8_t* arg1;
   double* loss_rows;
   size_t bytes;
@@ -429,8 +471,9 @@ CnnWs carve(uint32_t R, uint32_t C, void* base) {
   w.dc1 = reinterpret_cast<float*>(take(R * 32768 * f));
   w.wt2 = reinterpret_cast<float*>(take(32 * 800 * f));
   w.wt3 = reinterpret_cast<float*>(take(64 * 800 * f));
-  const size_t nch = (R + kCnnChunk - 1) / kCnnChunk;
-  w.part = reinterpret_cast<float*>(take(nch * 64 * 800 * f));
+  // partials: conv1 per sample (100 x 2400), conv2/3 per 4 samples (25 x 51200)
+  w.part = reinterpret_cast<float*>(take(std::max<size_t>(R * 2400, ((R + 3) / 4) * 64 * 800) * f));
+  w.pb = reinterpret_cast<float*>(take(R * 64 * f));
   w.arg1 = reinterpret_cast<uint8_t*>(take(R * 8192));
   w.loss_rows = reinterpret_cast<double*>(take(R * sizeof(double)));
   w.bytes = off;
@@ -453,11 +496,11 @@ static int cnn_forward(const ModelInfo& m, const float* P, const float* X, const
     DS_CUDA_TRY(cudaGetLastError());
     x0 = w.x0;
   }
-  DS_TRY((launch_conv5<3, 32, 32, 16, 4>(x0, P + L[0].w_off, P + L[0].b_off, w.c1, R, false, gate, s)));
+  DS_TRY((launch_conv5<3, 32, 32, 16, 4, 1>(x0, P + L[0].w_off, P + L[0].b_off, w.c1, R, false, gate, s)));
   maxpool_relu_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.c1, w.p1, w.arg1, R * 32, 32, gate);
-  DS_TRY((launch_conv5<32, 32, 16, 16, 2>(w.p1, P + L[1].w_off, P + L[1].b_off, w.c2, R, true, gate, s)));
+  DS_TRY((launch_conv5<32, 32, 16, 16, 2, 2>(w.p1, P + L[1].w_off, P + L[1].b_off, w.c2, R, true, gate, s)));
   avepool_kernel<<<blocks(R * 32 * 64), 256, 0, s>>>(w.c2, w.p2, R * 32, 16, gate);
-  DS_TRY((launch_conv5<32, 64, 8, 16, 1>(w.p2, P + L[2].w_off, P + L[2].b_off, w.c3, R, true, gate, s)));
+  DS_TRY((launch_conv5<32, 64, 8, 16, 1, 4>(w.p2, P + L[2].w_off, P + L[2].b_off, w.c3, R, true, gate, s)));
   avepool_kernel<<<blocks(R * 64 * 16), 256, 0, s>>>(w.c3, w.p3, R * 64, 8, gate);
   fc_fwd_kernel<4><<<R, 256, (1024 + 4 * 64) * sizeof(float), s>>>(w.p3, P + L[3].w_off, P + L[3].b_off, w.h1, 1024,
                                                                    64, gate);
@@ -479,7 +522,7 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   DS_CUDA_TRY(cudaGetLastError());
   if (!grad) return DS_OK;
   const float inv_b = static_cast<float>(1.0 / static_cast<double>(R));
-  const uint32_t nch = (R + kCnnChunk - 1) / kCnnChunk;
+  const uint32_t nch4 = (R + 3) / 4;
   // ip2, ip1
   fc_bwd_w_kernel<<<blocks(C * 64), 256, 0, s>>>(w.dz, w.h1, grad + L[4].w_off, grad + L[4].b_off, R, 64, C, inv_b,
                                                  flags, gate);
@@ -490,47 +533,28 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   // pool3 -> relu3 -> conv3
   avepool_bwd_kernel<<<blocks(R * 64 * 64), 256, 0, s>>>(w.dp3, w.c3, w.dc3, R * 64, 8, gate);
   DS_CUDA_TRY(cudaGetLastError());
-  {
-    constexpr int HP = 12;
-    const size_t smem = (32 * HP * HP + 2 * 64) * sizeof(float);
-    auto k = conv5_bwd_w_kernel<32, 8, 2>;
-    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    k<<<dim3(64 / 2, nch), 2 * 32 * 5, smem, s>>>(w.p2, w.dc3, w.part, R, 64, gate);
-    reduce_parts_kernel<<<blocks(64 * 800), 256, 0, s>>>(w.part, nch, 64 * 800, grad + L[2].w_off, inv_b, flags, gate);
-    conv_bias_grad_kernel<<<64, 256, 0, s>>>(w.dc3, R, 64, 64, grad + L[2].b_off, inv_b, gate);
-    flip_transpose_kernel<<<blocks(64 * 800), 256, 0, s>>>(P + L[2].w_off, w.wt3, 64, 32, gate);
-    DS_CUDA_TRY(cudaGetLastError());
-    DS_TRY((launch_conv5<64, 32, 8, 16, 1>(w.dc3, w.wt3, nullptr, w.dp2, R, false, gate, s)));
-  }
+  DS_TRY((launch_conv5_bwd_w<32, 8, 2, 4>(w.p2, w.dc3, w.part, w.pb, R, 64, gate, s)));
+  reduce_parts_kernel<<<blocks(64 * 800), 256, 0, s>>>(w.part, nch4, 64 * 800, grad + L[2].w_off, inv_b, flags, gate);
+  reduce_parts_kernel<<<1, 64, 0, s>>>(w.pb, nch4, 64, grad + L[2].b_off, inv_b, flags, gate);
+  flip_transpose_kernel<<<blocks(64 * 800), 256, 0, s>>>(P + L[2].w_off, w.wt3, 64, 32, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  DS_TRY((launch_conv5<64, 32, 8, 16, 1, 4>(w.dc3, w.wt3, nullptr, w.dp2, R, false, gate, s)));
   // pool2 -> relu2 -> conv2
   avepool_bwd_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.dp2, w.c2, w.dc2, R * 32, 16, gate);
   DS_CUDA_TRY(cudaGetLastError());
-  {
-    constexpr int HP = 20;
-    const size_t smem = (32 * HP * HP + 2 * 256) * sizeof(float);
-    auto k = conv5_bwd_w_kernel<32, 16, 2>;
-    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    k<<<dim3(32 / 2, nch), 2 * 32 * 5, smem, s>>>(w.p1, w.dc2, w.part, R, 32, gate);
-    reduce_parts_kernel<<<blocks(32 * 800), 256, 0, s>>>(w.part, nch, 32 * 800, grad + L[1].w_off, inv_b, flags, gate);
-    conv_bias_grad_kernel<<<32, 256, 0, s>>>(w.dc2, R, 32, 256, grad + L[1].b_off, inv_b, gate);
-    flip_transpose_kernel<<<blocks(32 * 800), 256, 0, s>>>(P + L[1].w_off, w.wt2, 32, 32, gate);
-    DS_CUDA_TRY(cudaGetLastError());
-    DS_TRY((launch_conv5<32, 32, 16, 16, 2>(w.dc2, w.wt2, nullptr, w.dr1, R, false, gate, s)));
-  }
-  // relu1 -> pool1 (max) -> conv1 (weights only)
+  DS_TRY((launch_conv5_bwd_w<32, 16, 2, 4>(w.p1, w.dc2, w.part, w.pb, R, 32, gate, s)));
+  reduce_parts_kernel<<<blocks(32 * 800), 256, 0, s>>>(w.part, nch4, 32 * 800, grad + L[1].w_off, inv_b, flags, gate);
+  reduce_parts_kernel<<<1, 32, 0, s>>>(w.pb, nch4, 32, grad + L[1].b_off, inv_b, flags, gate);
+  flip_transpose_kernel<<<blocks(32 * 800), 256, 0, s>>>(P + L[1].w_off, w.wt2, 32, 32, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  DS_TRY((launch_conv5<32, 32, 16, 16, 2, 2>(w.dc2, w.wt2, nullptr, w.dr1, R, false, gate, s)));
+  // relu1 -> pool1 (max) -> conv1 (weights only), one sample per partial
   maxpool_relu_bwd_kernel<<<blocks(R * 32 * 1024), 256, 0, s>>>(w.dr1, w.arg1, w.dc1, R * 32, 32, gate);
   DS_CUDA_TRY(cudaGetLastError());
-  {
-    constexpr int HP = 36;
-    const size_t smem = (3 * HP * HP + 32 * 1024) * sizeof(float);
-    auto k = conv5_bwd_w_kernel<3, 32, 32>;
-    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const float* x0 = idx ? w.x0 : X;
-    k<<<dim3(1, nch), 32 * 3 * 5, smem, s>>>(x0, w.dc1, w.part, R, 32, gate);
-    reduce_parts_kernel<<<blocks(32 * 75), 256, 0, s>>>(w.part, nch, 32 * 75, grad + L[0].w_off, inv_b, flags, gate);
-    conv_bias_grad_kernel<<<32, 256, 0, s>>>(w.dc1, R, 32, 1024, grad + L[0].b_off, inv_b, gate);
-    DS_CUDA_TRY(cudaGetLastError());
-  }
+  DS_TRY((launch_conv5_bwd_w<3, 32, 32, 1>(idx ? w.x0 : X, w.dc1, w.part, w.pb, R, 32, gate, s)));
+  reduce_parts_kernel<<<blocks(32 * 75), 256, 0, s>>>(w.part, R, 32 * 75, grad + L[0].w_off, inv_b, flags, gate);
+  reduce_parts_kernel<<<1, 32, 0, s>>>(w.pb, R, 32, grad + L[0].b_off, inv_b, flags, gate);
+  DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
 

@@ -104,10 +104,16 @@ struct ds_engine {
   int fused_grid = 0;
   uint64_t launches = 0;
   // host-fed batches (ds_engine_step_host): staging rows, identity plan, row count
-  float* Xb = nullptr;
+  float* Xb = nullptr;              // current slot (one of Xb2)
   uint32_t* yb = nullptr;
   uint32_t* iota = nullptr;
   uint32_t* rows_dev = nullptr;
+  float* Xb2[2] = {};               // double-buffered staging for ds_engine_step_host_async
+  uint32_t* yb2[2] = {};
+  uint32_t* rows2[2] = {};
+  cudaEvent_t slot_ev[2] = {};
+  bool slot_armed[2] = {};
+  int slot = 0;
   uint32_t hostfed_rows = 0;
   bool hostfed = false;
 };
@@ -230,7 +236,7 @@ int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
     const uint32_t* idx = e->hostfed ? e->iota : e->plan + j * B;
     DS_TRY(launch_loss_and_grad(e->model, p, X, idx, y, R, e->grad, &e->st->loss, e->ws,
                                 &e->st->flags, &e->st->err, e->stream));
-    e->launches += 3 * e->model.layers.size() + 1;
+    e->launches += e->model.kind == DS_MODEL_CIFAR10_QUICK ? 31 : 3 * e->model.layers.size() + 1;
     DS_TRY(launch_sgd(p, p, e->grad, e->model.P, eta, wd, &e->st->flags, e->stream, &e->st->err));
     policy_kernel<<<1, 1, 0, e->stream>>>(e->st, e->log);
     e->launches += 2;
@@ -412,10 +418,16 @@ extern "C" int ds_engine_create(ds_engine** out, int device, const ds_model_desc
   if (err == cudaSuccess) err = cudaMalloc(&e->st, sizeof(dsb::DevState));
   if (err == cudaSuccess) err = cudaMalloc(&e->bar, 64 * sizeof(unsigned int));
   if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->plan_ev, cudaEventDisableTiming);
-  if (err == cudaSuccess) err = cudaMalloc(&e->Xb, B * F * sizeof(float));
-  if (err == cudaSuccess) err = cudaMalloc(&e->yb, B * sizeof(uint32_t));
+  for (int k = 0; k < 2; ++k) {
+    if (err == cudaSuccess) err = cudaMalloc(&e->Xb2[k], B * F * sizeof(float));
+    if (err == cudaSuccess) err = cudaMalloc(&e->yb2[k], B * sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMalloc(&e->rows2[k], sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->slot_ev[k], cudaEventDisableTiming);
+  }
+  e->Xb = e->Xb2[0];
+  e->yb = e->yb2[0];
+  e->rows_dev = e->rows2[0];
   if (err == cudaSuccess) err = cudaMalloc(&e->iota, B * sizeof(uint32_t));
-  if (err == cudaSuccess) err = cudaMalloc(&e->rows_dev, sizeof(uint32_t));
   if (err == cudaSuccess) {
     std::vector<uint32_t> id(B);
     std::iota(id.begin(), id.end(), 0u);
@@ -473,10 +485,13 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->plan);
   cudaFree(e->plan_rows);
   cudaFree(e->d_tickets);
-  cudaFree(e->Xb);
-  cudaFree(e->yb);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(e->Xb2[k]);
+    cudaFree(e->yb2[k]);
+    cudaFree(e->rows2[k]);
+    if (e->slot_ev[k]) cudaEventDestroy(e->slot_ev[k]);
+  }
   cudaFree(e->iota);
-  cudaFree(e->rows_dev);
   if (e->h_plan) cudaFreeHost(e->h_plan);
   if (e->h_rows) cudaFreeHost(e->h_rows);
   cudaFree(e->log.loss);
@@ -685,12 +700,19 @@ extern "C" int ds_engine_launches(ds_engine* e, uint64_t* launches) {
   return DS_OK;
 }
 
-extern "C" int ds_engine_step_host(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows,
-                                   double* loss_host) {
+namespace {
+// One host-fed iteration on the next staging slot. Waits (host) only when the slot's
+// previous user — the iteration two calls back — has not finished on the device.
+int step_host_enqueue(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows, double* loss_host) {
   if (!e || !X_host || !y_host) return set_error(DS_E_CONTRACT, "engine_step_host: null");
   if (rows == 0) return set_error(DS_E_CONTRACT, "loss_and_grad: empty batch");
   if (rows > e->hp.batch_size) return set_error(DS_E_CONTRACT, "engine_step_host: more rows than batch_size");
-  dsb::DeviceScope ds(e->device);
+  const int k = e->slot;
+  e->slot ^= 1;
+  if (e->slot_armed[k]) DS_CUDA_TRY(cudaEventSynchronize(e->slot_ev[k]));
+  e->Xb = e->Xb2[k];
+  e->yb = e->yb2[k];
+  e->rows_dev = e->rows2[k];
   const uint64_t F = e->model.n_features;
   DS_CUDA_TRY(cudaMemcpyAsync(e->Xb, X_host, rows * F * sizeof(float), cudaMemcpyDefault, e->stream));
   DS_CUDA_TRY(cudaMemcpyAsync(e->yb, y_host, rows * sizeof(uint32_t), cudaMemcpyDefault, e->stream));
@@ -700,11 +722,27 @@ extern "C" int ds_engine_step_host(ds_engine* e, const float* X_host, const uint
   const int rc = ds_engine_run(e, 1, 0, nullptr);
   e->hostfed = false;
   if (rc != DS_OK) return rc;
-  if (loss_host) {
-    // the loss row of this iteration: st->iter was advanced by the step
+  DS_CUDA_TRY(cudaEventRecord(e->slot_ev[k], e->stream));
+  e->slot_armed[k] = true;
+  if (loss_host)  // the loss row of this iteration: st->iter was advanced by the step
     DS_CUDA_TRY(cudaMemcpyAsync(loss_host, e->log.loss + (e->queued - 1), sizeof(double), cudaMemcpyDeviceToHost,
                                 e->stream));
-    DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
-  }
   return DS_OK;
+}
+}  // namespace
+
+extern "C" int ds_engine_step_host(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows,
+                                   double* loss_host) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine_step_host: null");
+  dsb::DeviceScope ds(e->device);
+  DS_TRY(step_host_enqueue(e, X_host, y_host, rows, loss_host));
+  if (loss_host) DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return DS_OK;
+}
+
+extern "C" int ds_engine_step_host_async(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows,
+                                         double* loss_host) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine_step_host: null");
+  dsb::DeviceScope ds(e->device);
+  return step_host_enqueue(e, X_host, y_host, rows, loss_host);
 }
