@@ -47,6 +47,7 @@ int ds_device_count(int* count);
 #define DS_FLAG_LOSS_NONFINITE 8u /* loss_and_grad: non-finite loss            (model.cpp:256) */
 #define DS_FLAG_GRAD_NONFINITE 16u /* loss_and_grad: non-finite gradient       (model.cpp:259) */
 #define DS_FLAG_LABEL_RANGE 32u   /* loss_and_grad: label out of range         (model.cpp:176-180) */
+#define DS_FLAG_STREAM_TIMEOUT 64u /* stream mode: no batch from the host for 20 s                  */
 
 /* ---------------------------------------------------------------------------------- */
 /* Elementwise updates — param_vector.hpp:21-38                                       */
@@ -262,6 +263,17 @@ int ds_engine_step_host(ds_engine* e, const float* X_host, const uint32_t* y_hos
  * calls later. The host blocks only when it runs two iterations ahead of the device. */
 int ds_engine_step_host_async(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows,
                               double* loss_host);
+/* Stream mode: ONE persistent launch trains `steps` iterations on batches the host pushes
+ * while it runs (a 4-slot device ring; the copy engine lands each batch and then its
+ * sequence word, the kernel waits for the word, frees the slot after its grid barrier).
+ * Every batch crosses PCIe as an H2D copy; each step's loss is written by the kernel to
+ * *loss_host[step] (pinned, mapped: zero-copy D2H), valid after ds_engine_stream_end.
+ * push blocks only while the ring is full. X_host/y_host of push s may be reused at push
+ * s+4. Fused one-hidden-layer engine, fixed-period policy. A host that stops pushing for
+ * 20 s makes the kernel finish with DS_FLAG_STREAM_TIMEOUT rather than hang. */
+int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss_host);
+int ds_engine_stream_push(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows);
+int ds_engine_stream_end(ds_engine* e);
 /* Block until the engine's queued work finished; returns DS_E_NUMERIC/DS_E_CONTRACT
  * if any step hit the reference's error conditions (message names the iteration). */
 int ds_engine_sync(ds_engine* e);

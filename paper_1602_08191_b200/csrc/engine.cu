@@ -15,6 +15,7 @@
 //
 // The policy is evaluated on the device (engine.cpp:35-48) so adaptive exchanges need
 // no host sync; the exchange kernels test the device-side fire flag themselves.
+#include <chrono>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -114,6 +115,17 @@ struct ds_engine {
   cudaEvent_t slot_ev[2] = {};
   bool slot_armed[2] = {};
   int slot = 0;
+  // stream mode (ds_engine_stream_*): host-fed ring consumed by one persistent launch
+  static constexpr uint32_t kRing = 4;
+  float* ring_X = nullptr;              // [kRing][B][F]
+  uint32_t* ring_y = nullptr;           // [kRing][B]
+  uint32_t* ring_words = nullptr;       // [kRing] rows, [kRing] ready sequence
+  uint32_t* ring_src = nullptr;         // pinned host: the same words' sources
+  unsigned long long* ring_consumed = nullptr;  // pinned host, written by the kernel
+  cudaStream_t copy_stream = nullptr;
+  bool ring_active = false;
+  uint64_t ring_steps = 0, ring_pushed = 0;
+  double* ring_loss = nullptr;
   uint32_t hostfed_rows = 0;
   bool hostfed = false;
 };
@@ -253,7 +265,7 @@ int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
 }
 
 int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
-  if (!e->hostfed) DS_TRY(upload_plan(e, steps));
+  if (!e->hostfed && !e->ring_active) DS_TRY(upload_plan(e, steps));
   FusedArgs a{};
   a.F = e->model.n_features;
   a.H = e->model.hidden.empty() ? 0 : e->model.hidden[0];
@@ -261,8 +273,8 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
   a.P = e->model.P;
   a.X = e->hostfed ? e->Xb : e->X;
   a.y = e->hostfed ? e->yb : e->y;
-  a.plan = e->hostfed ? e->iota : e->plan;
-  a.plan_rows = e->hostfed ? e->rows_dev : e->plan_rows;
+  a.plan = (e->hostfed || e->ring_active) ? e->iota : e->plan;
+  a.plan_rows = (e->hostfed || e->ring_active) ? e->rows_dev : e->plan_rows;
   a.B = e->hp.batch_size;
   a.steps = steps;
   a.params[0] = e->params[0];
@@ -292,6 +304,16 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
   if (prof) DS_CUDA_TRY(cudaMemsetAsync(prof, 0, prof_n * sizeof(unsigned long long), e->stream));
   a.prof = prof;
   a.prof_cta = prof ? prof + steps * kProfSlots : nullptr;
+  if (e->ring_active) {
+    a.ring = 1;
+    a.ring_slots = ds_engine::kRing;
+    a.ring_X = e->ring_X;
+    a.ring_y = e->ring_y;
+    a.ring_rows = e->ring_words;
+    a.ring_ready = e->ring_words + ds_engine::kRing;
+    a.ring_consumed = e->ring_consumed;
+    a.ring_loss = e->ring_loss;
+  }
   DS_TRY(launch_fused(a, e->fused_grid, e->stream));
   e->launches += 1;
   e->cur ^= static_cast<int>(steps & 1);
@@ -485,6 +507,12 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->plan);
   cudaFree(e->plan_rows);
   cudaFree(e->d_tickets);
+  cudaFree(e->ring_X);
+  cudaFree(e->ring_y);
+  cudaFree(e->ring_words);
+  cudaFreeHost(e->ring_src);
+  cudaFreeHost(e->ring_consumed);
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   for (int k = 0; k < 2; ++k) {
     cudaFree(e->Xb2[k]);
     cudaFree(e->yb2[k]);
@@ -745,4 +773,80 @@ extern "C" int ds_engine_step_host_async(ds_engine* e, const float* X_host, cons
   if (!e) return set_error(DS_E_CONTRACT, "engine_step_host: null");
   dsb::DeviceScope ds(e->device);
   return step_host_enqueue(e, X_host, y_host, rows, loss_host);
+}
+
+// ---- stream mode --------------------------------------------------------------------
+extern "C" int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss_host) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine_stream: null");
+  if (e->ring_active) return set_error(DS_E_STATE, "engine_stream: a stream is already open");
+  if (!e->fused || e->model.hidden.size() != 1 || (e->model.n_features % 4) != 0)
+    return set_error(DS_E_CONTRACT, "engine_stream: needs the fused one-hidden-layer engine and n_features %% 4 == 0");
+  if (e->hp.adaptive) return set_error(DS_E_CONTRACT, "engine_stream: fixed-period policy only");
+  if (steps == 0) return DS_OK;
+  dsb::DeviceScope ds(e->device);
+  const uint64_t B = e->hp.batch_size, F = e->model.n_features, K = ds_engine::kRing;
+  if (!e->ring_X) {
+    DS_CUDA_TRY(cudaMalloc(&e->ring_X, K * B * F * sizeof(float)));
+    DS_CUDA_TRY(cudaMalloc(&e->ring_y, K * B * sizeof(uint32_t)));
+    DS_CUDA_TRY(cudaMalloc(&e->ring_words, 2 * K * sizeof(uint32_t)));
+    DS_CUDA_TRY(cudaMallocHost(&e->ring_src, 2 * K * sizeof(uint32_t)));
+    DS_CUDA_TRY(cudaHostAlloc(&e->ring_consumed, sizeof(unsigned long long), cudaHostAllocMapped));
+    DS_CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+  }
+  DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  DS_CUDA_TRY(cudaMemsetAsync(e->ring_words, 0, 2 * K * sizeof(uint32_t), e->stream));
+  *reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) = 0;
+  DS_TRY(dsb::ensure_log(e, e->queued + steps));
+  e->ring_active = true;
+  e->ring_steps = steps;
+  e->ring_pushed = 0;
+  e->ring_loss = loss_host;
+  const int rc = ds_engine_run(e, steps, 0, nullptr);  // the launch waits on the ring
+  if (rc != DS_OK) e->ring_active = false;
+  return rc;
+}
+
+extern "C" int ds_engine_stream_push(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows) {
+  if (!e || !X_host || !y_host) return set_error(DS_E_CONTRACT, "engine_stream_push: null");
+  if (!e->ring_active) return set_error(DS_E_STATE, "engine_stream_push: no open stream");
+  if (e->ring_pushed >= e->ring_steps) return set_error(DS_E_STATE, "engine_stream_push: all steps already pushed");
+  if (rows == 0 || rows > e->hp.batch_size) return set_error(DS_E_CONTRACT, "engine_stream_push: bad row count");
+  dsb::DeviceScope ds(e->device);
+  const uint64_t s = e->ring_pushed, K = ds_engine::kRing, B = e->hp.batch_size, F = e->model.n_features;
+  const uint64_t slot = s % K;
+  if (s >= K) {  // the slot's previous step (s - K) must have been read by every CTA
+    const auto t0 = std::chrono::steady_clock::now();
+    while (*reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) < s - K + 1) {
+      if (cudaStreamQuery(e->stream) != cudaErrorNotReady)
+        return set_error(DS_E_STATE, "engine_stream_push: the stream kernel is no longer running");
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+        return set_error(DS_E_CUDA, "engine_stream_push: device stopped consuming");
+    }
+  }
+  e->ring_src[slot] = rows;
+  e->ring_src[K + slot] = static_cast<uint32_t>(s + 1);
+  cudaStream_t cs = e->copy_stream;
+  DS_CUDA_TRY(cudaMemcpyAsync(e->ring_X + slot * B * F, X_host, rows * F * sizeof(float), cudaMemcpyDefault, cs));
+  DS_CUDA_TRY(cudaMemcpyAsync(e->ring_y + slot * B, y_host, rows * sizeof(uint32_t), cudaMemcpyDefault, cs));
+  DS_CUDA_TRY(cudaMemcpyAsync(e->ring_words + slot, e->ring_src + slot, sizeof(uint32_t), cudaMemcpyHostToDevice, cs));
+  // the sequence word last: the kernel sees it only after the rows (same stream, in order)
+  DS_CUDA_TRY(cudaMemcpyAsync(e->ring_words + K + slot, e->ring_src + K + slot, sizeof(uint32_t),
+                              cudaMemcpyHostToDevice, cs));
+  ++e->ring_pushed;
+  return DS_OK;
+}
+
+extern "C" int ds_engine_stream_end(ds_engine* e) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine_stream_end: null");
+  if (!e->ring_active) return DS_OK;
+  dsb::DeviceScope ds(e->device);
+  if (e->ring_pushed < e->ring_steps)
+    return set_error(DS_E_STATE, "engine_stream_end: %llu of %llu steps pushed",
+                     static_cast<unsigned long long>(e->ring_pushed), static_cast<unsigned long long>(e->ring_steps));
+  const cudaError_t err = cudaStreamSynchronize(e->stream);
+  cudaStreamSynchronize(e->copy_stream);
+  e->ring_active = false;
+  e->ring_loss = nullptr;
+  if (err != cudaSuccess) return set_error(DS_E_CUDA, "engine_stream_end: %s", cudaGetErrorString(err));
+  return DS_OK;
 }

@@ -65,6 +65,15 @@ struct FusedArgs {
   unsigned int* bar;          // grid barrier words [2]
   unsigned long long* prof;   // optional: kProfSlots globaltimer stamps per step (CTA 0)
   unsigned long long* prof_cta;  // optional: [step][CTA][2] forward-done / grid-barrier-exit stamps
+  // stream mode (host-fed ring; MLP kernel only)
+  int ring;
+  uint32_t ring_slots;
+  const float* ring_X;              // [slots][B][F]
+  const uint32_t* ring_y;           // [slots][B]
+  const uint32_t* ring_rows;        // [slots]
+  const uint32_t* ring_ready;       // [slots] sequence words (step + 1), written by the copy engine
+  unsigned long long* ring_consumed;  // pinned host: steps whose ring slot is free again
+  double* ring_loss;                // pinned host: per-step batch loss (zero-copy), or null
 };
 
 constexpr int kProfSlots = 10;

@@ -1097,6 +1097,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   __shared__ unsigned int s_nbar;
   __shared__ PolicyLocal s_pol;
   __shared__ unsigned long long s_ticket;
+  __shared__ uint32_t s_rrows[2];  // stream mode: rows of steps s (s & 1)
 
   const uint64_t w1 = 0, b1 = static_cast<uint64_t>(H) * F;
   const uint64_t w2 = b1 + H, b2 = w2 + static_cast<uint64_t>(C) * H;
@@ -1143,31 +1144,70 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   // (One bulk copy per row-chunk would put ~R*nck serialized TMA issues on one warp.)
   // The caller has synced the block since the last generic access of Xs.
   // Ri holds the batch's shard rows (staged earlier, so no global load sits in this loop).
+  // Stream mode (host-fed ring, ds_engine_stream_*): step s's rows sit in ring slot
+  // s % ring_slots once the host's H2D copies have landed — the copy engine writes the
+  // slot's sequence word after the rows (same copy stream, in order). Thread 0 waits for
+  // it (bounded: a stalled host raises DS_FLAG_STREAM_TIMEOUT instead of hanging the GPU).
+  auto ring_wait = [&](uint64_t s) {
+    if (tid == 0) {
+      const uint32_t slot = static_cast<uint32_t>(s % A.ring_slots);
+      const uint32_t want = static_cast<uint32_t>(s + 1);
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      uint32_t rows = 1;
+      while (true) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(A.ring_ready + slot) : "memory");
+        if (v == want) {
+          rows = *reinterpret_cast<volatile const uint32_t*>(A.ring_rows + slot);
+          break;
+        }
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) {
+          atomicOr(&st->flags, DS_FLAG_STREAM_TIMEOUT);
+          break;
+        }
+        __nanosleep(64);
+      }
+      s_rrows[s & 1] = rows;
+    }
+    __syncthreads();
+  };
+  auto step_rows = [&](uint64_t s) -> uint32_t { return A.ring ? s_rrows[s & 1] : A.plan_rows[s]; };
+  auto step_x = [&](uint64_t s) -> const float* {
+    return A.ring ? A.ring_X + (s % A.ring_slots) * static_cast<uint64_t>(B) * F : A.X;
+  };
   auto issue_x = [&](uint64_t s) {
-    const uint32_t R = A.plan_rows[s];
+    if (A.ring) ring_wait(s);
+    const uint32_t R = step_rows(s);
+    const float* Xb = step_x(s);
     for (uint32_t k = 0; k < nck; ++k) {
       const uint32_t c = k * CW + 4 * lane;
       if (4 * lane < (F - k * CW < CW ? F - k * CW : CW))
         for (uint32_t r = warp; r < R; r += kFT / 32)
-          cp_async16(Xs + static_cast<size_t>(r) * Fs + c, A.X + static_cast<uint64_t>(Ri[r]) * F + c);
+          cp_async16(Xs + static_cast<size_t>(r) * Fs + c, Xb + static_cast<uint64_t>(Ri[r]) * F + c);
       cp_async_arrive(xbar + k);
     }
   };
   load_own_rows(A.params[cur]);
-  if (A.steps > 0)
+  if (A.ring) {
+    for (uint32_t r = tid; r < B; r += kFT) Ri[r] = r;
+  } else if (A.steps > 0) {
     for (uint32_t r = tid; r < A.plan_rows[0]; r += kFT) Ri[r] = A.plan[r];
+  }
   __syncthreads();
   if (vecx && A.steps > 0) issue_x(0);
 
   for (uint64_t step = 0; step < A.steps; ++step) {
-    const uint32_t R = A.plan_rows[step];
+    const uint32_t R = step_rows(step);
     const uint32_t* idx = A.plan + step * B;
     const float* P = A.params[cur];
     float* Pn = A.params[cur ^ 1];
     const double inv_b = 1.0 / static_cast<double>(R);
     stamp(A.prof, step, 0);
     if (tid == 0) s_bad = 0;
-    if (tid < R) Lab[tid] = A.y[idx[tid]];
+    if (tid < R) Lab[tid] = A.ring ? A.ring_y[(step % A.ring_slots) * B + tid] : A.y[idx[tid]];
 
     // ---- A: batch rows (TMA issued at the end of the previous step; generic path here) --
     if (!vecx) {
@@ -1209,6 +1249,8 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     if (tid == 0) {
       grid_arrive_wait(A.bar, s_nbar, G);
       s_flags = *reinterpret_cast<volatile uint32_t*>(&st->flags);
+      if (A.ring && blockIdx.x == 0)  // every CTA's loads of this step's ring slot have landed
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(A.ring_consumed), "l"(step + 1) : "memory");
       fence_proxy_async();
       if (!s_flags) {
         const uint32_t total = H * B * 8;
@@ -1297,13 +1339,14 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
       for (uint32_t r = 0; r < R; ++r) s = dadd(s, Lr[r]);
       s_loss = dmul(s, inv_b);
       if (!isfinite(s_loss)) atomicOr(&s_bad, DS_FLAG_LOSS_NONFINITE);
+      if (A.ring_loss && blockIdx.x == 0) A.ring_loss[step] = s_loss;  // zero-copy D2H of the result
     }
     for (uint32_t t = tid; t < R * C; t += kFT) {
       const uint32_t r = t / C, c = t - r * C;
       Z[t] = dsub(exp(dsub(Z[t], Lse[r])), c == Lab[r] ? 1.0 : 0.0);
     }
     __syncthreads();
-    if (step + 1 < A.steps)  // next batch's rows for issue_x (latency hidden by the backward)
+    if (!A.ring && step + 1 < A.steps)  // next batch's rows for issue_x (latency hidden by the backward)
       for (uint32_t r = tid; r < A.plan_rows[step + 1]; r += kFT) Ri[r] = A.plan[(step + 1) * B + r];
     // ---- C: backward. delta1 || W2 columns + b2 (different warps) ---------------------------
     stamp(A.prof, step, 6);

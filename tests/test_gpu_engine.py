@@ -181,3 +181,57 @@ def test_engine_numeric_error(L, orc, kind):
             L.check(L.lib.ds_engine_sync(e))
     finally:
         L.lib.ds_engine_destroy(e)
+
+
+@pytest.mark.parametrize("m,n,b,tau,steps", [(ModelSpec.mlp(20, [16], 3), 300, 16, 5, 45),
+                                             (ModelSpec.mlp(784, [256], 10), 2000, 32, 10, 120),
+                                             (ModelSpec.mlp(20, [33], 3), 70, 32, 4, 13)])  # ragged batches
+def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps):
+    """Stream mode (one persistent launch fed batch by batch from pinned host memory)
+    must reproduce the engine's own device-resident run on the same batch sequence (its
+    ShardSweeper order) bit for bit, including the exchanges and the per-step losses the
+    kernel writes to mapped host memory."""
+    import torch
+    X, y = orc.gen_synthetic(n, m.n_features, m.n_classes, 2.0, 1.5, 3)
+    init = orc.init_params(m, 9)
+    P = len(init)
+    hp = Hyper(eta=0.05, tau=tau, batch_size=b, i_max=steps)
+    master0 = orc.init_params(m, 10)
+    outs = []
+    for mode in ("run", "stream"):
+        e = make_engine(L, m, X, y, m.n_classes, hp, 31, init, 2)
+        mh = C.c_void_p()
+        L.check(L.lib.ds_master_create(C.byref(mh), 0, P, C.c_float(np.float32(hp.alpha)), L.DS_MODE_LOCKFREE,
+                                       master0.ctypes.data))
+        L.check(L.lib.ds_engine_attach_master(e, mh))
+        if mode == "run":
+            L.check(L.lib.ds_engine_run(e, steps, 0, None))
+            L.check(L.lib.ds_engine_sync(e))
+            loss = engine_log(L, e, steps)[0]
+        else:
+            from paper_1602_08191_b200.deepspark import DeepSpark
+            idx, sizes = DeepSpark().sweep_batches(len(y), b, 31, steps)
+            lossbuf = torch.zeros(steps, dtype=torch.float64, pin_memory=True)
+            bufs = [(torch.empty((b, m.n_features), dtype=torch.float32, pin_memory=True),
+                     torch.empty(b, dtype=torch.int32, pin_memory=True)) for _ in range(4)]
+            L.check(L.lib.ds_engine_stream_begin(e, steps, C.c_void_p(lossbuf.data_ptr())))
+            for s in range(steps):
+                xb, yb = bufs[s % 4]
+                r = int(sizes[s])
+                xb.numpy()[:r] = X[idx[s, :r]]
+                yb.numpy().view(np.uint32)[:r] = y[idx[s, :r]]
+                L.check(L.lib.ds_engine_stream_push(e, C.c_void_p(xb.data_ptr()), C.c_void_p(yb.data_ptr()), r))
+            L.check(L.lib.ds_engine_stream_end(e))
+            loss = lossbuf.numpy().copy()
+            assert np.array_equal(loss, engine_log(L, e, steps)[0])
+        outs.append((loss, engine_params(L, e, P), engine_log(L, e, steps)[2]))
+        snap = np.zeros(P, np.float32)
+        L.check(L.lib.ds_master_snapshot(mh, snap.ctypes.data))
+        outs[-1] += (snap,)
+        L.lib.ds_engine_destroy(e)
+        L.lib.ds_master_destroy(mh)
+    (l0, p0, x0, m0), (l1, p1, x1, m1) = outs
+    assert np.array_equal(l0, l1)
+    assert np.array_equal(x0, x1)
+    assert np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
+    assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
