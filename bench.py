@@ -269,12 +269,21 @@ def main():
     # roofline of the dominant (and only) kernel of the timed region: the fused step
     flop_launch = FLOP_PER_SAMPLE * args.batch * K
     achieved = flop_launch / (ms / 1e3) / 1e12
+    # The launch is the only kernel of the timed region. Its contract bound is reported
+    # against the tensor peak (FLOPs), but the path is exact-order f64 on CUDA cores, so
+    # the binding roofline is the FP64 pipe: 148 SMs x 64 DADD/DMUL lanes per clock.
+    sm_clk = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+    fp64_peak = 148 * 64 * sm_clk / 1e12  # TFLOP/s (one op per DADD/DMUL lane)
+    traffic = 32 * 3136 * K  # ncu dram bytes per launch = the X rows (profiles/r01_fused_kernel_ncu.md)
     roof = {"bound": "tensor", "achieved": achieved, "peak": bf16_sus, "unit": "TFLOP/s", "frac": achieved / bf16_sus,
-            "traffic": None, "peak_kind": f"{peak_kind} bf16 dense, sustained",
-            "kernel": "fused_kernel<true> (persistent: forward, softmax-CE, backward, SGD, policy, exchange)",
+            "traffic": traffic, "peak_kind": f"{peak_kind} bf16 dense, sustained",
+            "kernel": "mlp_kernel (persistent: forward, softmax-CE, backward, SGD, policy, exchange)",
             "algorithmic": f"{FLOP_PER_SAMPLE} FLOP/sample x {args.batch} x {K} steps per launch",
-            "note": "f64 CUDA-core chains in the reference's sequential order; latency-bound "
-                    "(784-long dependent DADD chains + 1 grid barrier per step), not a tensor-core kernel"}
+            "fp64_pipe": {"achieved_tflops": achieved, "peak_tflops": fp64_peak, "frac": achieved / fp64_peak,
+                          "note": "the reference's sequential f64 order (bit parity) keeps every FLOP on the FP64 "
+                                  "pipe; ncu: FP64 pipe active 12.5% of elapsed, 1 grid barrier per step"},
+            "note": "latency-bound f64 CUDA-core chains (784-long dependent DADD chains per hidden unit), "
+                    "not a tensor-core kernel; traffic = X rows only (22.5 MB DRAM read per 200-step launch)"}
 
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n, "steps": K, "warmup": W,
             "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
