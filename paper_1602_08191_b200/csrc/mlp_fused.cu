@@ -27,6 +27,7 @@
 // rounded to f32 once, and the update rounds like param_vector.cpp:33. The chains are
 // what bounds this kernel (latency, not bandwidth): 784 dependent DADDs per hidden
 // unit, 256 per logit.
+#include <algorithm>
 #include <cstdlib>
 
 #include "ds_common.cuh"
@@ -1062,6 +1063,17 @@ __device__ __forceinline__ void logit_chains(double* Z, const double* W2d, uint3
 
 constexpr uint32_t kBarFull = 2, kBarEmpty = 4;  // named barrier ids (+ buffer index)
 
+// Thread-block-cluster helpers: a store into a peer CTA's shared memory (DSMEM) and the
+// cluster barrier.
+__device__ __forceinline__ void st_cluster_f64(double* local, uint32_t rank, double v) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const unsigned int G = gridDim.x;
@@ -1074,6 +1086,9 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t cwarps = (B * U + 31) / 32;  // forward consumer (chain) warps
   const bool vecx = (F % 4) == 0 && (CW % 4) == 0;
+  uint32_t crank, csize;  // thread-block cluster: the CTAs of a cluster split the logits by rows
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
 
   float* Xs = reinterpret_cast<float*>(smem_raw + sp.xs);    // B x Fs batch rows (f32)
   float* Ws = reinterpret_cast<float*>(smem_raw + sp.w);     // own W1 rows f32 (the parameters)
@@ -1292,8 +1307,17 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     aph ^= 1;
     __syncthreads();
     stamp(A.prof, step, 4);
-    {  // logits: lane == row; a warp runs the chains of classes w, w+4, w+8, ... for its
-       // rows (4 class sets, one per SM sub-partition: the As reads stay 4x, not Cx)
+    // Logits and softmax-CE. Every CTA needs all rows' output deltas, but computing them
+    // is FP64-pipe bound (320 chains x 256 terms per CTA). The CTAs of a cluster split
+    // the rows: each computes logits, softmax and deltas for R/csize rows, then reads the
+    // others' rows from their shared memory (DSMEM) after one cluster barrier.
+    const uint32_t rpr = (R + csize - 1) / csize;
+    const uint32_t rlo = crank * rpr < R ? crank * rpr : R, rhi = rlo + rpr < R ? rlo + rpr : R;
+    if (csize > 1) {
+      for (uint32_t t = tid; t < (rhi - rlo) * C; t += kFT)
+        logit_chains<1>(Z, W2d, H2, As, B, H, P + b2, rlo + t / C, C, t % C);
+    } else {  // lane == row; a warp runs the chains of classes w, w+4, w+8, ... for its
+              // rows (4 class sets, one per SM sub-partition: the As reads stay 4x, not Cx)
       const uint32_t ngroups = (R + 31) / 32;
       for (uint32_t item = warp; item < ngroups * 4; item += kFT / 32) {
         const uint32_t r = (item >> 2) * 32 + lane, cs = item & 3;
@@ -1310,16 +1334,16 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
     }
     __syncthreads();
     stamp(A.prof, step, 5);
-    for (uint32_t r = tid; r < R; r += kFT) {
+    for (uint32_t r = rlo + tid; r < rhi; r += kFT) {
       const double* z = Z + static_cast<size_t>(r) * C;
       double zmax = z[0];
       for (uint32_t c = 1; c < C; ++c) zmax = z[c] > zmax ? z[c] : zmax;
       Zmax[r] = zmax;
     }
     __syncthreads();
-    for (uint32_t t = tid; t < R * C; t += kFT) E[t] = exp(dsub(Z[t], Zmax[t / C]));
+    for (uint32_t t = rlo * C + tid; t < rhi * C; t += kFT) E[t] = exp(dsub(Z[t], Zmax[t / C]));
     __syncthreads();
-    for (uint32_t r = tid; r < R; r += kFT) {
+    for (uint32_t r = rlo + tid; r < rhi; r += kFT) {
       const double* e = E + static_cast<size_t>(r) * C;
       double sum = 0.0;
       for (uint32_t c = 0; c < C; ++c) sum = dadd(sum, e[c]);
@@ -1334,6 +1358,20 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
       }
     }
     __syncthreads();
+    for (uint32_t t = rlo * C + tid; t < rhi * C; t += kFT) {
+      const uint32_t r = t / C, c = t - r * C;
+      const double d = dsub(exp(dsub(Z[t], Lse[r])), c == Lab[r] ? 1.0 : 0.0);
+      Z[t] = d;
+      for (uint32_t q = 1; q < csize; ++q) st_cluster_f64(Z + t, (crank + q) % csize, d);  // push to peers
+    }
+    if (csize > 1) {  // this rank's per-row losses to the peers, then one cluster barrier
+      for (uint32_t t = tid; t < (rhi - rlo) * (csize - 1); t += kFT) {
+        const uint32_t r = rlo + t % (rhi - rlo), q = 1 + t / (rhi - rlo);
+        st_cluster_f64(Lr + r, (crank + q) % csize, Lr[r]);
+      }
+      cluster_sync_all();
+    }
+    __syncthreads();
     if (tid == kFT - 1) {
       double s = 0.0;
       for (uint32_t r = 0; r < R; ++r) s = dadd(s, Lr[r]);
@@ -1341,11 +1379,6 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
       if (!isfinite(s_loss)) atomicOr(&s_bad, DS_FLAG_LOSS_NONFINITE);
       if (A.ring_loss && blockIdx.x == 0) A.ring_loss[step] = s_loss;  // zero-copy D2H of the result
     }
-    for (uint32_t t = tid; t < R * C; t += kFT) {
-      const uint32_t r = t / C, c = t - r * C;
-      Z[t] = dsub(exp(dsub(Z[t], Lse[r])), c == Lab[r] ? 1.0 : 0.0);
-    }
-    __syncthreads();
     if (!A.ring && step + 1 < A.steps)  // next batch's rows for issue_x (latency hidden by the backward)
       for (uint32_t r = tid; r < A.plan_rows[step + 1]; r += kFT) Ri[r] = A.plan[(step + 1) * B + r];
     // ---- C: backward. delta1 || W2 columns + b2 (different warps) ---------------------------
@@ -1529,7 +1562,59 @@ int launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
   void* args[] = {const_cast<FusedArgs*>(&a)};
   if (a.H > 0) {
     DS_CUDA_TRY(cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    DS_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mlp_kernel), dim3(grid), dim3(kFT), args, smem, s));
+    // Optional cooperative launch in thread-block clusters (DS_FUSED_CLUSTER=2|4|8): the
+    // CTAs of a cluster split the logits/softmax rows and exchange the deltas through
+    // DSMEM (see mlp_kernel). Measured neutral on B200 for 784-256-10 (the FP64 pipe work
+    // it saves is paid back in the cluster barrier and the exp/log latency), so the
+    // default is no clusters.
+    unsigned cap = 1;
+    if (const char* env = std::getenv("DS_FUSED_CLUSTER")) cap = static_cast<unsigned>(std::max(1, std::atoi(env)));
+    static int cached_grid = -1;
+    static size_t cached_smem = 0;
+    static unsigned cached_cap = 0, cached_cl = 1;
+    if (grid != cached_grid || smem != cached_smem || cap != cached_cap) {
+      unsigned pick = 1;
+      for (unsigned cl = 8; cl >= 2; cl /= 2) {
+        if (cl > cap || grid % cl) continue;
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(grid);
+        q.blockDim = dim3(kFT);
+        q.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        q.attrs = at;
+        q.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, mlp_kernel, &q) == cudaSuccess &&
+            nclusters * static_cast<int>(cl) >= grid) {
+          pick = cl;
+          break;
+        }
+        cudaGetLastError();
+      }
+      cached_grid = grid;
+      cached_smem = smem;
+      cached_cap = cap;
+      cached_cl = pick;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kFT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = cached_cl;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, mlp_kernel, a));
   } else {
     DS_CUDA_TRY(cudaFuncSetAttribute(fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DS_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fused_kernel<false>), dim3(1), dim3(kFT), args, smem, s));

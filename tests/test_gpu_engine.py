@@ -235,3 +235,22 @@ def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps):
     assert np.array_equal(x0, x1)
     assert np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
     assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
+
+
+def test_cluster_split_logits_bit_identical(L, orc, monkeypatch):
+    """DS_FUSED_CLUSTER=8: the CTAs of each 8-CTA cluster split the logits/softmax rows
+    and exchange deltas through DSMEM; the result must equal the default launch bit for bit."""
+    m = ModelSpec.mlp(784, [256], 10)
+    X, y = orc.gen_synthetic(600, 784, 10, 2.0, 1.5, 3)
+    init = orc.init_params(m, 9)
+    hp = Hyper(eta=0.05, tau=10, batch_size=32, i_max=40)
+    out = []
+    for cl in ("1", "8"):
+        monkeypatch.setenv("DS_FUSED_CLUSTER", cl)
+        e = make_engine(L, m, X, y, 10, hp, 31, init, 2)
+        L.check(L.lib.ds_engine_run(e, hp.i_max, 0, None))
+        L.check(L.lib.ds_engine_sync(e))
+        out.append((engine_log(L, e, hp.i_max)[0], engine_params(L, e, len(init))))
+        L.lib.ds_engine_destroy(e)
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1].view(np.uint32), out[1][1].view(np.uint32))
