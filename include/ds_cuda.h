@@ -77,6 +77,13 @@ int ds_sgd_update(float* out, const float* x, const float* g, uint64_t n, float 
 int ds_sgd_step_checked(float* out, const float* x, const float* g, uint64_t n, double eta,
                         void* stream);
 
+/* Momentum SGD — NOT IN THE REFERENCE (Hyperparams has no momentum), the
+ * Caffe solver's form: g' = g + f32(wd)*x; v = mu*v + g'; out = x - f32(eta)*v, f32 with
+ * separate roundings. mu == 0 is bit-identical to ds_sgd_update. `velocity` (device,
+ * n floats, zero-initialised by the caller) is updated in place. */
+int ds_sgd_momentum_update(float* out, const float* x, float* velocity, const float* g, uint64_t n,
+                           float eta, float mu, float wd, uint32_t* flags_dev, void* stream);
+
 /* ---------------------------------------------------------------------------------- */
 /* Synchronous data-parallel SGD — simulator.cpp:156-223 (and its NCCL form)          */
 /* ---------------------------------------------------------------------------------- */
@@ -249,6 +256,9 @@ int ds_engine_run(ds_engine* e, uint64_t steps, int stop_at_exchange, uint64_t* 
  * iterations so a following ds_engine_run(steps) allocates nothing (no implicit
  * device synchronisation inside a timed or latency-sensitive region). */
 int ds_engine_reserve(ds_engine* e, uint64_t steps);
+/* Momentum option (ds_sgd_momentum_update; layered engine only — the fused step keeps
+ * mu = 0): every following iteration uses the momentum update with this mu. */
+int ds_engine_set_momentum(ds_engine* e, float mu);
 /* Host-fed iteration (a data pipeline that owns the rows, like the reference worker's
  * ShardSweeper + gather_batch, engine.cpp:25-33 / model.cpp:12-21): copies `rows`
  * gathered rows (X_host row-major, y_host) from host memory — pinned for full speed —

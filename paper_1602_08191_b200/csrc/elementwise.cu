@@ -177,6 +177,39 @@ int launch_sgd(float* out, const float* x, const float* g, uint64_t n, float eta
   return DS_OK;
 }
 
+// Momentum SGD (SURVEY §8 a21 — NOT IN THE REFERENCE, whose Hyperparams has no mu):
+// g' = g + f32(wd)*x; v = mu*v + g'; out = x - eta*v, f32 with separate roundings.
+// mu == 0 gives v = g' and out = x - eta*g', i.e. exactly sgd_step (param_vector.cpp:33).
+__global__ void __launch_bounds__(kThreads) momentum_kernel(float* out, const float* x, float* v,
+                                                            const float* __restrict__ g, uint64_t n, float eta,
+                                                            float mu, float wd, uint32_t* flags,
+                                                            const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
+  uint32_t bad = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n; i += stride) {
+    const float xi = x[i];
+    float gi = g[i];
+    if (!finite_f(xi)) bad |= DS_FLAG_X_NONFINITE;
+    if (wd > 0.0f) gi = fadd(gi, fmul(wd, xi));
+    if (!finite_f(gi)) bad |= DS_FLAG_G_NONFINITE;
+    const float vi = mu != 0.0f ? fadd(fmul(mu, v[i]), gi) : gi;
+    v[i] = vi;
+    const float o = fsub(xi, fmul(eta, vi));
+    if (!finite_f(o)) bad |= DS_FLAG_OUT_NONFINITE;
+    out[i] = o;
+  }
+  flush_flags(bad, flags);
+}
+
+int launch_momentum(float* out, const float* x, float* v, const float* g, uint64_t n, float eta, float mu, float wd,
+                    uint32_t* flags, cudaStream_t s, const uint32_t* gate) {
+  if (n == 0) return DS_OK;
+  momentum_kernel<<<grid_for(n, current_sms()), kThreads, 0, s>>>(out, x, v, g, n, eta, mu, wd, flags, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
 }  // namespace dsb
 
 // ------------------------------------------------------------------------------------
@@ -301,4 +334,12 @@ extern "C" int ds_gather_rows(float* dst, uint32_t* y_dst, const float* X, const
   gather_rows_kernel<<<(rows + 7) / 8, 256, 0, dsb::as_stream(stream)>>>(dst, y_dst, X, y, idx, rows, features, vec);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
+}
+
+extern "C" int ds_sgd_momentum_update(float* out, const float* x, float* velocity, const float* g, uint64_t n,
+                                      float eta, float mu, float wd, uint32_t* flags_dev, void* stream) {
+  if (n && (!out || !x || !velocity || !g)) return dsb::set_error(DS_E_CONTRACT, "sgd_momentum: null pointer");
+  if (!(eta > 0.0f)) return dsb::set_error(DS_E_CONTRACT, "sgd_step: eta must be positive");
+  if (!(mu >= 0.0f && mu < 1.0f)) return dsb::set_error(DS_E_CONTRACT, "sgd_momentum: mu must be in [0,1)");
+  return dsb::launch_momentum(out, x, velocity, g, n, eta, mu, wd, flags_dev, dsb::as_stream(stream), nullptr);
 }

@@ -10,4 +10,6 @@ int launch_elastic(const float* w_in, float* w_out, float* m, uint64_t n, float 
 // out may equal x; flags may be null; gate (may be null): skip when *gate != 0.
 int launch_sgd(float* out, const float* x, const float* g, uint64_t n, float eta, float wd,
                uint32_t* flags, cudaStream_t s, const uint32_t* gate = nullptr);
+int launch_momentum(float* out, const float* x, float* v, const float* g, uint64_t n, float eta, float mu, float wd,
+                    uint32_t* flags, cudaStream_t s, const uint32_t* gate);
 }  // namespace dsb

@@ -126,6 +126,8 @@ struct ds_engine {
   bool ring_active = false;
   uint64_t ring_steps = 0, ring_pushed = 0;
   double* ring_loss = nullptr;
+  float mu = 0.0f;            // momentum (layered path), ds_engine_set_momentum
+  float* velocity = nullptr;
   uint32_t hostfed_rows = 0;
   bool hostfed = false;
 };
@@ -249,7 +251,11 @@ int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
     DS_TRY(launch_loss_and_grad(e->model, p, X, idx, y, R, e->grad, &e->st->loss, e->ws,
                                 &e->st->flags, &e->st->err, e->stream));
     e->launches += e->model.kind == DS_MODEL_CIFAR10_QUICK ? 31 : 3 * e->model.layers.size() + 1;
-    DS_TRY(launch_sgd(p, p, e->grad, e->model.P, eta, wd, &e->st->flags, e->stream, &e->st->err));
+    if (e->mu > 0.0f)
+      DS_TRY(launch_momentum(p, p, e->velocity, e->grad, e->model.P, eta, e->mu, wd, &e->st->flags, e->stream,
+                             &e->st->err));
+    else
+      DS_TRY(launch_sgd(p, p, e->grad, e->model.P, eta, wd, &e->st->flags, e->stream, &e->st->err));
     policy_kernel<<<1, 1, 0, e->stream>>>(e->st, e->log);
     e->launches += 2;
     if (e->hp.adaptive) {
@@ -507,6 +513,7 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->plan);
   cudaFree(e->plan_rows);
   cudaFree(e->d_tickets);
+  cudaFree(e->velocity);
   cudaFree(e->ring_X);
   cudaFree(e->ring_y);
   cudaFree(e->ring_words);
@@ -776,6 +783,19 @@ extern "C" int ds_engine_step_host_async(ds_engine* e, const float* X_host, cons
 }
 
 // ---- stream mode --------------------------------------------------------------------
+extern "C" int ds_engine_set_momentum(ds_engine* e, float mu) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine: null");
+  if (!(mu >= 0.0f && mu < 1.0f)) return set_error(DS_E_CONTRACT, "sgd_momentum: mu must be in [0,1)");
+  if (mu > 0.0f && e->fused) return set_error(DS_E_CONTRACT, "engine: momentum needs the layered engine");
+  dsb::DeviceScope ds(e->device);
+  if (mu > 0.0f && !e->velocity) {
+    DS_CUDA_TRY(cudaMalloc(&e->velocity, e->model.P * sizeof(float)));
+    DS_CUDA_TRY(cudaMemsetAsync(e->velocity, 0, e->model.P * sizeof(float), e->stream));
+  }
+  e->mu = mu;
+  return DS_OK;
+}
+
 extern "C" int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss_host) {
   if (!e) return set_error(DS_E_CONTRACT, "engine_stream: null");
   if (e->ring_active) return set_error(DS_E_STATE, "engine_stream: a stream is already open");

@@ -190,3 +190,31 @@ def test_label_out_of_range_flag(T, L, orc):
     m = ModelSpec.softmax(3, 2)
     _, _, fl = gpu_loss_and_grad(T, L, m, np.zeros(8, np.float32), np.ones((2, 3), np.float32), np.array([0, 2], np.uint32))
     assert fl & L.FLAG_LABEL_RANGE
+
+
+def test_momentum_update(T, L):
+    """SURVEY §8 a21 (not in the reference): mu = 0 is bit-identical to sgd_update; mu > 0
+    matches the Caffe-form recurrence evaluated with numpy float32 (separate roundings)."""
+    rng = np.random.default_rng(3)
+    n = 100003
+    x = rng.standard_normal(n).astype(np.float32)
+    g = rng.standard_normal(n).astype(np.float32)
+    v0 = rng.standard_normal(n).astype(np.float32)
+    eta, wd = np.float32(0.05), np.float32(0.01)
+    for mu in (0.0, 0.9):
+        xd, gd, vd = dev(T, x), dev(T, g), dev(T, v0.copy())
+        out = T.empty_like(xd)
+        fl = T.zeros(1, dtype=T.int32, device="cuda")
+        L.check(L.lib.ds_sgd_momentum_update(ptr(out), ptr(xd), ptr(vd), ptr(gd), n, C.c_float(eta), C.c_float(mu),
+                                             C.c_float(wd), ptr(fl), None))
+        T.cuda.synchronize()
+        g1 = (g + wd * x).astype(np.float32)
+        v = (np.float32(mu) * v0 + g1).astype(np.float32) if mu else g1
+        ref = (x - eta * v).astype(np.float32)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+        assert np.array_equal(vd.cpu().numpy().view(np.uint32), v.view(np.uint32))
+        if mu == 0.0:
+            out2 = T.empty_like(xd)
+            L.check(L.lib.ds_sgd_update(ptr(out2), ptr(xd), ptr(gd), n, C.c_float(eta), C.c_float(wd), ptr(fl), None))
+            T.cuda.synchronize()
+            assert T.equal(out, out2)
