@@ -1,0 +1,259 @@
+// conv_tc.cu — 5x5 pad-2 convolutions of the convnet as implicit GEMMs on the tcgen05
+// tensor cores (kind::tf32: f32 operands rounded to tf32 by the tensor core, f32
+// accumulation in TMEM).
+//
+// Forward / backward-data (conv5_tc_kernel): D[pixels x Cout] = A[pixels x K] * W[Cout x K]^T
+// with K = Cin*25 (k = ci*25 + kh*5 + kw) and A the im2col of the zero-padded input. One
+// CTA owns a 128-pixel tile (M = 128) of the flattened (sample, h, w) space; its input rows
+// are staged once in shared memory as f32, and 4 producer warps (one thread per tile row)
+// build 32-deep K chunks of A (im2col gather through a per-CTA offset table) in the
+// canonical K-major layout into an NS-stage ring, while each chunk of W — pre-packed in
+// that layout by pack_w_kernel — lands by one TMA bulk copy; a 5th warp (one elected
+// lane) issues four 128xCOUTx8 MMAs per chunk
+// into a TMEM accumulator and commits each stage back to the producers through an
+// mbarrier (the issuer must not share a warp with producers that it waits on). The
+// epilogue reads the 128xCOUT accumulator with tcgen05.ld, adds the bias, applies relu and
+// stores NCHW rows (coalesced over pixels).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "conv_tc.cuh"
+#include "ds_common.cuh"
+
+namespace dsb {
+namespace {
+
+constexpr int kTile = 128, kKC = 32, kNS = 4;  // pixels per CTA, K per chunk, ring stages
+
+// K order: with CIN % 32 == 0 the channels are innermost (k = (kh*5 + kw)*CIN + ci) and the
+// staged input is HWC with a padded channel stride CS, so a 32-deep chunk of one im2col row
+// is 8 aligned 16-byte runs (LDS.128 -> STS.128); otherwise (conv1, CIN = 3) the reference
+// order k = ci*25 + kh*5 + kw through an offset table. pack_w_kernel packs W to match.
+template <int CIN, int COUT, int H>
+struct ConvTcShape {
+  static constexpr int HW = H * H, HP = H + 4, K = CIN * 25, NKC = (K + kKC - 1) / kKC;
+  static constexpr bool kHWC = CIN % kKC == 0;  // a K chunk never straddles two (kh, kw)
+  static constexpr int CS = CIN + 4;                          // HWC channel stride (banks)
+  static constexpr bool kMulti = HW < kTile;                 // a tile spans several samples
+  static constexpr int SPT = kMulti ? kTile / HW : 1;         // samples per tile
+  static constexpr int ROWS = kMulti ? HP : kTile / H + 4;    // staged input rows per sample
+  static constexpr int XS = kHWC ? SPT * ROWS * HP * CS : SPT * CIN * ROWS * HP;  // staged input floats
+  static constexpr int A_BYTES = kTile * kKC * 4, B_BYTES = COUT * kKC * 4;
+  static constexpr size_t SMEM = static_cast<size_t>(XS) * 4 + kNS * (A_BYTES + B_BYTES) + NKC * kKC * 4 + 1024;
+};
+
+template <int CIN, int COUT, int H>
+__global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __restrict__ in, const float* __restrict__ Wpk,
+                                                            const float* __restrict__ bias, float* __restrict__ out,
+                                                            uint32_t R, bool relu, const uint32_t* gate) {
+  using S = ConvTcShape<CIN, COUT, H>;
+  if (gate && *gate) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* xs = reinterpret_cast<float*>(smem);
+  unsigned char* ring = smem + ((static_cast<size_t>(S::XS) * 4 + 127) & ~static_cast<size_t>(127));
+  int* koff = reinterpret_cast<int*>(ring + kNS * (S::A_BYTES + S::B_BYTES));  // [NKC*32] im2col offsets
+  __shared__ __align__(8) uint64_t full[kNS], empty[kNS], done;
+  __shared__ uint32_t tmem_base;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  const uint64_t total = static_cast<uint64_t>(R) * S::HW;
+  const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * kTile;
+  const uint32_t n0 = static_cast<uint32_t>(g0 / S::HW);
+  const uint32_t h0 = S::kMulti ? 0 : static_cast<uint32_t>((g0 % S::HW) / H);  // first output row
+
+  constexpr uint32_t kThreads = kTile + 32;
+  if (warp == 4) tc::tmem_alloc<(COUT < 32 ? 32 : COUT)>(&tmem_base);
+  if (tid == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      tc::mbar_init(&full[s], kTile);  // producer arrivals; thread 0 also adds W's tx bytes
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // stage the tile's zero-padded input rows: xs[s][ci][row][col], row r <-> image row
+  // h0 - 2 + r (or the whole padded image for multi-sample tiles)
+  // one (sample, channel, row) per thread and iteration: a coalesced, vectorised row read
+  for (uint32_t i = tid; i < static_cast<uint32_t>(S::SPT * CIN * S::ROWS); i += kThreads) {
+    uint32_t row, ci, sl;
+    if constexpr (S::kHWC) {  // channel fastest across threads: conflict-free HWC stores
+      ci = i % CIN;
+      row = (i / CIN) % S::ROWS;
+      sl = i / (CIN * S::ROWS);
+    } else {
+      row = i % S::ROWS;
+      ci = (i / S::ROWS) % CIN;
+      sl = i / (S::ROWS * CIN);
+    }
+    const int y = static_cast<int>(h0 + row) - 2;
+    const uint32_t n = n0 + sl;
+    // element col of this (sl, row, ci) line lives at dst[col * step]
+    float* dst = S::kHWC ? xs + (static_cast<size_t>(sl) * S::ROWS + row) * S::HP * S::CS + ci
+                         : xs + ((static_cast<size_t>(sl) * CIN + ci) * S::ROWS + row) * S::HP;
+    constexpr uint32_t step = S::kHWC ? S::CS : 1;
+    dst[0] = dst[step] = dst[(H + 2) * step] = dst[(H + 3) * step] = 0.0f;
+    if (n < R && y >= 0 && y < H) {
+      const float4* src = reinterpret_cast<const float4*>(in + ((static_cast<uint64_t>(n) * CIN + ci) * H + y) * H);
+      float4 v[H / 4];
+#pragma unroll
+      for (int q = 0; q < H / 4; ++q) v[q] = __ldg(src + q);
+#pragma unroll
+      for (int q = 0; q < H / 4; ++q) {
+        dst[(2 + 4 * q) * step] = v[q].x;
+        dst[(3 + 4 * q) * step] = v[q].y;
+        dst[(4 + 4 * q) * step] = v[q].z;
+        dst[(5 + 4 * q) * step] = v[q].w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < H; ++q) dst[(2 + q) * step] = 0.0f;
+    }
+  }
+  for (uint32_t k = tid; k < static_cast<uint32_t>(S::NKC * kKC); k += kThreads) {
+    const uint32_t ci = k / 25, r = k - ci * 25, kh = r / 5, kw = r - kh * 5;
+    koff[k] = k < static_cast<uint32_t>(S::K) ? static_cast<int>((ci * S::ROWS + kh) * S::HP + kw) : -1;
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  constexpr uint32_t a_lbo = kTile / 8 * 128, b_lbo = COUT / 8 * 128;
+  constexpr uint32_t idesc = tc::idesc_tf32(kTile, COUT);
+  if (warp == 4) {  // ---- MMA issuer (one lane) ----
+    if ((tid & 31) == 0) {
+      for (int i = 0; i < S::NKC; ++i) {
+        const int s = i % kNS;
+        unsigned char* As = ring + s * (S::A_BYTES + S::B_BYTES);
+        unsigned char* Bs = As + S::A_BYTES;
+        tc::mbar_wait(&full[s], (i / kNS) & 1);
+        tc::fence_after();
+#pragma unroll
+        for (int t = 0; t < kKC / 8; ++t)
+          tc::mma_tf32(tmem, tc::saddr(As) + t * 2 * a_lbo, a_lbo, tc::saddr(Bs) + t * 2 * b_lbo, b_lbo, idesc,
+                       i > 0 || t > 0);
+        tc::commit(&empty[s]);
+      }
+      tc::commit(&done);
+    }
+    __syncwarp();
+  } else {  // ---- producers: this thread's tile row ----
+    const uint64_t g = g0 + tid;
+    const bool valid = g < total;
+    const uint32_t sl = static_cast<uint32_t>((g / S::HW) - n0), p = static_cast<uint32_t>(g % S::HW);
+    const uint32_t ph = p / H - h0, pw = p % H;
+    const float* xrow = xs + static_cast<size_t>(sl) * CIN * S::ROWS * S::HP + ph * S::HP + pw;
+    for (int i = 0; i < S::NKC; ++i) {
+      const int s = i % kNS;
+      if (i >= kNS) tc::mbar_wait(&empty[s], ((i / kNS) - 1) & 1);
+      unsigned char* As = ring + s * (S::A_BYTES + S::B_BYTES);
+      unsigned char* Bs = As + S::A_BYTES;
+      const int k0 = i * kKC;
+      if (tid == 0) {  // W chunk i: one bulk copy of the pre-packed block
+        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(tc::saddr(&full[s])), "r"(S::B_BYTES)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                tc::saddr(Bs)),
+            "l"(Wpk + static_cast<size_t>(i) * COUT * kKC), "r"(S::B_BYTES), "r"(tc::saddr(&full[s]))
+            : "memory");
+      }
+      // A: this row's 32 K values (im2col), 16 bytes per core-matrix row
+      if constexpr (S::kHWC) {
+        const int khw = k0 / CIN, ci0 = k0 - khw * CIN, kh = khw / 5, kw = khw - kh * 5;
+        const float4* src = reinterpret_cast<const float4*>(
+            xs + ((static_cast<size_t>(sl) * S::ROWS + ph + kh) * S::HP + pw + kw) * S::CS + ci0);
+        float4 v[kKC / 4];
+#pragma unroll
+        for (int c = 0; c < kKC / 4; ++c) v[c] = valid ? src[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < kKC / 4; ++c) *reinterpret_cast<float4*>(As + tc::kmajor_off(tid, c * 4, kTile)) = v[c];
+      } else {
+#pragma unroll
+        for (int c = 0; c < kKC / 4; ++c) {
+          float4 v;
+          float* pv = reinterpret_cast<float*>(&v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int o = koff[k0 + c * 4 + j];
+            pv[j] = (valid && o >= 0) ? xrow[o] : 0.0f;
+          }
+          *reinterpret_cast<float4*>(As + tc::kmajor_off(tid, c * 4, kTile)) = v;
+        }
+      }
+      tc::fence_async_smem();
+      tc::mbar_arrive(&full[s]);
+    }
+    tc::mbar_wait(&done, 0);
+    tc::fence_after();
+    // epilogue: row tid of the accumulator -> out[n][co][p]
+    float* dst = out + (static_cast<uint64_t>(n0 + sl) * COUT) * S::HW + p;
+#pragma unroll
+    for (int cb = 0; cb < COUT; cb += 32) {
+      float v[32];
+      tc::tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cb, v);
+      if (valid) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float o = v[j] + (bias ? __ldg(bias + cb + j) : 0.0f);
+          if (relu) o = o > 0.0f ? o : 0.0f;
+          dst[static_cast<uint64_t>(cb + j) * S::HW] = o;
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 4) tc::tmem_free<(COUT < 32 ? 32 : COUT)>(tmem);
+}
+
+// Wpk[chunk][canonical K-major COUT x 32] = W[co][chunk*32 + kk] (0 beyond K): each K
+// chunk of the weights becomes one contiguous block for a single TMA bulk copy.
+__global__ void pack_w_kernel(const float* __restrict__ W, float* __restrict__ Wpk, uint32_t cout, uint32_t cin,
+                              uint32_t nkc, bool hwc, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nkc * cout * kKC) return;
+  const uint32_t K = cin * 25;
+  const uint32_t chunk = t / (cout * kKC), rem = t % (cout * kKC), co = rem / kKC, kk = rem % kKC;
+  const uint32_t k = chunk * kKC + kk;  // GEMM k; the weight's own index below
+  uint32_t kw_idx = k;
+  if (hwc && k < K) {  // k = (kh*5 + kw)*cin + ci  ->  ci*25 + kh*5 + kw
+    const uint32_t khw = k / cin, ci = k - khw * cin;
+    kw_idx = ci * 25 + khw;
+  }
+  Wpk[static_cast<size_t>(chunk) * cout * kKC + tc::kmajor_off(co, kk, cout) / 4] =
+      k < K ? W[static_cast<size_t>(co) * K + kw_idx] : 0.0f;
+}
+
+}  // namespace
+
+template <int CIN, int COUT, int H>
+int launch_conv5_tc(const float* in, const float* W, float* Wpk, const float* b, float* out, uint32_t R, bool relu,
+                    const uint32_t* gate, cudaStream_t s) {
+  using S = ConvTcShape<CIN, COUT, H>;
+  static_assert(COUT % 32 == 0 && COUT <= 256, "COUT: multiple of 32 (tcgen05 N, TMEM columns)");
+  static_assert(H % 4 == 0, "rows are staged as float4");
+  auto k = conv5_tc_kernel<CIN, COUT, H>;
+  static bool attr = false;
+  if (!attr) {
+    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::SMEM)));
+    attr = true;
+  }
+  const uint64_t tiles = (static_cast<uint64_t>(R) * S::HW + kTile - 1) / kTile;
+  const uint32_t n = S::NKC * COUT * kKC;
+  pack_w_kernel<<<(n + 255) / 256, 256, 0, s>>>(W, Wpk, COUT, CIN, S::NKC, S::kHWC, gate);
+  k<<<static_cast<unsigned>(tiles), kTile + 32, S::SMEM, s>>>(in, Wpk, b, out, R, relu, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+// the convnet's layers: forward (conv1..3) and backward-data (conv3 -> dp2, conv2 -> dr1)
+template int launch_conv5_tc<3, 32, 32>(const float*, const float*, float*, const float*, float*, uint32_t,
+                                        bool, const uint32_t*, cudaStream_t);
+template int launch_conv5_tc<32, 32, 16>(const float*, const float*, float*, const float*, float*, uint32_t,
+                                        bool, const uint32_t*, cudaStream_t);
+template int launch_conv5_tc<32, 64, 8>(const float*, const float*, float*, const float*, float*, uint32_t,
+                                        bool, const uint32_t*, cudaStream_t);
+template int launch_conv5_tc<64, 32, 8>(const float*, const float*, float*, const float*, float*, uint32_t,
+                                        bool, const uint32_t*, cudaStream_t);
+
+}  // namespace dsb

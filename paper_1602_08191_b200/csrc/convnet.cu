@@ -17,7 +17,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
+#include "conv_tc.cuh"
 #include "ds_common.cuh"
 #include "model.cuh"
 
@@ -438,6 +440,7 @@ struct CnnWs {
   float *x0, *c1, *p1, *c2, *p2, *c3, *p3, *h1, *z;       // forward
   float *dz, *dh1, *dp3, *dc3, *dp2, *dc2, *dr1, *dc1;    // backward
   float *wt2, *wt3, *part, *pb;                            // flipped weights, partial dW / db
+  float* wpk;                                              // tcgen05 packed weight chunks
   uint8_t* arg1;
   double* loss_rows;
   size_t bytes;
@@ -474,6 +477,7 @@ CnnWs carve(uint32_t R, uint32_t C, void* base) {
   // partials: conv1 per sample (100 x 2400), conv2/3 per 4 samples (25 x 51200)
   w.part = reinterpret_cast<float*>(take(std::max<size_t>(R * 2400, ((R + 3) / 4) * 64 * 800) * f));
   w.pb = reinterpret_cast<float*>(take(R * 64 * f));
+  w.wpk = reinterpret_cast<float*>(take(conv5_tc_wpk_floats(64, 32) * f));  // largest: 64x25 -> 32 (= 32x25 -> 64)
   w.arg1 = reinterpret_cast<uint8_t*>(take(R * 8192));
   w.loss_rows = reinterpret_cast<double*>(take(R * sizeof(double)));
   w.bytes = off;
@@ -481,6 +485,13 @@ CnnWs carve(uint32_t R, uint32_t C, void* base) {
 }
 
 unsigned blocks(uint64_t n, unsigned t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
+
+// Convolutions run as tcgen05 implicit GEMMs (tf32 operands, f32 accumulation) unless
+// DS_CNN_FFMA=1 selects the f32 CUDA-core kernels (a precision mode for parity checks).
+bool use_tensor_cores() {
+  const char* e = std::getenv("DS_CNN_FFMA");
+  return !(e && e[0] == '1');
+}
 
 }  // namespace
 
@@ -496,11 +507,21 @@ static int cnn_forward(const ModelInfo& m, const float* P, const float* X, const
     DS_CUDA_TRY(cudaGetLastError());
     x0 = w.x0;
   }
-  DS_TRY((launch_conv5<3, 32, 32, 16, 4, 1>(x0, P + L[0].w_off, P + L[0].b_off, w.c1, R, false, gate, s)));
+  const bool tcores = use_tensor_cores();
+  if (tcores)
+    DS_TRY((launch_conv5_tc<3, 32, 32>(x0, P + L[0].w_off, w.wpk, P + L[0].b_off, w.c1, R, false, gate, s)));
+  else
+    DS_TRY((launch_conv5<3, 32, 32, 16, 4, 1>(x0, P + L[0].w_off, P + L[0].b_off, w.c1, R, false, gate, s)));
   maxpool_relu_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.c1, w.p1, w.arg1, R * 32, 32, gate);
-  DS_TRY((launch_conv5<32, 32, 16, 16, 2, 2>(w.p1, P + L[1].w_off, P + L[1].b_off, w.c2, R, true, gate, s)));
+  if (tcores)
+    DS_TRY((launch_conv5_tc<32, 32, 16>(w.p1, P + L[1].w_off, w.wpk, P + L[1].b_off, w.c2, R, true, gate, s)));
+  else
+    DS_TRY((launch_conv5<32, 32, 16, 16, 2, 2>(w.p1, P + L[1].w_off, P + L[1].b_off, w.c2, R, true, gate, s)));
   avepool_kernel<<<blocks(R * 32 * 64), 256, 0, s>>>(w.c2, w.p2, R * 32, 16, gate);
-  DS_TRY((launch_conv5<32, 64, 8, 16, 1, 4>(w.p2, P + L[2].w_off, P + L[2].b_off, w.c3, R, true, gate, s)));
+  if (tcores)
+    DS_TRY((launch_conv5_tc<32, 64, 8>(w.p2, P + L[2].w_off, w.wpk, P + L[2].b_off, w.c3, R, true, gate, s)));
+  else
+    DS_TRY((launch_conv5<32, 64, 8, 16, 1, 4>(w.p2, P + L[2].w_off, P + L[2].b_off, w.c3, R, true, gate, s)));
   avepool_kernel<<<blocks(R * 64 * 16), 256, 0, s>>>(w.c3, w.p3, R * 64, 8, gate);
   fc_fwd_kernel<4><<<R, 256, (1024 + 4 * 64) * sizeof(float), s>>>(w.p3, P + L[3].w_off, P + L[3].b_off, w.h1, 1024,
                                                                    64, gate);
@@ -538,7 +559,10 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   reduce_parts_kernel<<<1, 64, 0, s>>>(w.pb, nch4, 64, grad + L[2].b_off, inv_b, flags, gate);
   flip_transpose_kernel<<<blocks(64 * 800), 256, 0, s>>>(P + L[2].w_off, w.wt3, 64, 32, gate);
   DS_CUDA_TRY(cudaGetLastError());
-  DS_TRY((launch_conv5<64, 32, 8, 16, 1, 4>(w.dc3, w.wt3, nullptr, w.dp2, R, false, gate, s)));
+  if (use_tensor_cores())
+    DS_TRY((launch_conv5_tc<64, 32, 8>(w.dc3, w.wt3, w.wpk, nullptr, w.dp2, R, false, gate, s)));
+  else
+    DS_TRY((launch_conv5<64, 32, 8, 16, 1, 4>(w.dc3, w.wt3, nullptr, w.dp2, R, false, gate, s)));
   // pool2 -> relu2 -> conv2
   avepool_bwd_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.dp2, w.c2, w.dc2, R * 32, 16, gate);
   DS_CUDA_TRY(cudaGetLastError());
@@ -547,7 +571,10 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   reduce_parts_kernel<<<1, 32, 0, s>>>(w.pb, nch4, 32, grad + L[1].b_off, inv_b, flags, gate);
   flip_transpose_kernel<<<blocks(32 * 800), 256, 0, s>>>(P + L[1].w_off, w.wt2, 32, 32, gate);
   DS_CUDA_TRY(cudaGetLastError());
-  DS_TRY((launch_conv5<32, 32, 16, 16, 2, 2>(w.dc2, w.wt2, nullptr, w.dr1, R, false, gate, s)));
+  if (use_tensor_cores())
+    DS_TRY((launch_conv5_tc<32, 32, 16>(w.dc2, w.wt2, w.wpk, nullptr, w.dr1, R, false, gate, s)));
+  else
+    DS_TRY((launch_conv5<32, 32, 16, 16, 2, 2>(w.dc2, w.wt2, nullptr, w.dr1, R, false, gate, s)));
   // relu1 -> pool1 (max) -> conv1 (weights only), one sample per partial
   maxpool_relu_bwd_kernel<<<blocks(R * 32 * 1024), 256, 0, s>>>(w.dr1, w.arg1, w.dc1, R * 32, 32, gate);
   DS_CUDA_TRY(cudaGetLastError());
