@@ -205,6 +205,196 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
   if (warp == 4) tc::tmem_free<(COUT < 32 ? 32 : COUT)>(tmem);
 }
 
+// ---- weight (and bias) gradients: D[k' x COUT] = A'[k' x pixels] * dY[COUT x pixels]^T --
+// k' in the HWC order (k' = (kh*5 + kw)*CIN + ci), one extra row k' = K of ones so row K of
+// D is the bias gradient. A' is the transpose of the forward's im2col, built K-major (one
+// thread per k' row gathers 4 pixels per 16-byte unit; MN-major tf32 operands are not
+// accepted by the MMA — tools/tc_gemm_test.cu); dY
+// rows land by LDGSTS straight into the K-major B layout; a producer arrives on a stage's
+// mbarrier one chunk later, after its copies for it completed and a proxy fence (LDGSTS
+// writes are generic-proxy data for the tensor core). CTA = (128-row k' tile, a split of
+// the batch); the per-split partials
+// part[split][K+1][COUT] are summed in split order by wgrad_reduce_kernel.
+template <int CIN, int COUT, int H, int SPS>
+struct WgradShape {
+  static constexpr int HW = H * H, HP = H + 4, CS = CIN + 4, K = CIN * 25, MT = (K + 1 + kTile - 1) / kTile;
+  static constexpr int XS = HP * HP * CS, CPS = HW / kKC;  // staged floats, pixel chunks per sample
+  static constexpr int A_BYTES = kTile * kKC * 4, B_BYTES = COUT * kKC * 4;
+  static constexpr size_t SMEM = static_cast<size_t>(XS) * 4 + kNS * (A_BYTES + B_BYTES) + 1024;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::saddr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int CIN, int COUT, int H, int SPS>
+__global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const float* __restrict__ in,
+                                                                       const float* __restrict__ dout,
+                                                                       float* __restrict__ part, uint32_t R,
+                                                                       const uint32_t* gate) {
+  using S = WgradShape<CIN, COUT, H, SPS>;
+  static_assert(CIN % 4 == 0 && S::HW % kKC == 0 && COUT % 32 == 0, "wgrad tiling");
+  if (gate && *gate) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* xs = reinterpret_cast<float*>(smem);
+  unsigned char* ring = smem + ((static_cast<size_t>(S::XS) * 4 + 127) & ~static_cast<size_t>(127));
+  __shared__ __align__(8) uint64_t full[kNS], empty[kNS], done;
+  __shared__ uint32_t tmem_base;
+  constexpr uint32_t kThreads = kTile + 32;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t mt = blockIdx.x, split = blockIdx.y;
+  const uint32_t n_lo = split * SPS, n_hi = min(n_lo + SPS, R);
+  const int nchunks = static_cast<int>(n_hi > n_lo ? (n_hi - n_lo) * S::CPS : 0);
+  if (warp == 4) tc::tmem_alloc<COUT>(&tmem_base);
+  if (tid == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      tc::mbar_init(&full[s], kTile);  // one arrival per producer thread
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  constexpr uint32_t a_lbo = kTile / 8 * 128;  // between 4-pixel halves (K-major A')
+  constexpr uint32_t b_lbo = COUT / 8 * 128;   // between 4-pixel halves (K-major B)
+  constexpr uint32_t idesc = tc::idesc_tf32(kTile, COUT);
+  if (warp == 4) {  // ---- MMA issuer ----
+    if ((tid & 31) == 0) {
+      for (int i = 0; i < nchunks; ++i) {
+        const int s = i % kNS;
+        unsigned char* As = ring + s * (S::A_BYTES + S::B_BYTES);
+        unsigned char* Bs = As + S::A_BYTES;
+        tc::mbar_wait(&full[s], (i / kNS) & 1);
+        tc::fence_after();
+#pragma unroll
+        for (int t = 0; t < kKC / 8; ++t) {
+          const uint64_t da = tc::sdesc(tc::saddr(As) + t * 2 * a_lbo, a_lbo, 128);
+          const uint64_t db = tc::sdesc(tc::saddr(Bs) + t * 2 * b_lbo, b_lbo, 128);
+          const uint32_t acc = (i > 0 || t > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+        tc::commit(&empty[s]);
+      }
+      tc::commit(&done);
+    }
+    __syncwarp();
+  } else {  // ---- producers ----
+    // this thread's row k' of the tile: (kh, kw, ci), the ones row (bias) or padding
+    const uint32_t krow = mt * kTile + tid;
+    const bool real = krow < static_cast<uint32_t>(S::K), ones = krow == static_cast<uint32_t>(S::K);
+    const uint32_t khw = real ? krow / CIN : 0, rci = real ? krow - khw * CIN : 0;
+    const uint32_t rkh = khw / 5, rkw = khw - rkh * 5;
+    for (int i = 0; i < nchunks; ++i) {
+      const uint32_t n = n_lo + i / S::CPS, p0 = (i % S::CPS) * kKC;
+      if (i % S::CPS == 0) {  // stage sample n as HWC (all producers; the ring holds copies)
+        asm volatile("bar.sync 1, %0;" ::"n"(kTile) : "memory");
+        for (uint32_t j = tid; j < static_cast<uint32_t>(CIN * S::HP); j += kTile) {
+          const uint32_t ci = j % CIN, row = j / CIN;
+          const int y = static_cast<int>(row) - 2;
+          float* dst = xs + static_cast<size_t>(row) * S::HP * S::CS + ci;
+          dst[0] = dst[S::CS] = dst[(H + 2) * S::CS] = dst[(H + 3) * S::CS] = 0.0f;
+          if (y >= 0 && y < H) {
+            const float4* src = reinterpret_cast<const float4*>(in + ((static_cast<uint64_t>(n) * CIN + ci) * H + y) * H);
+#pragma unroll
+            for (int q = 0; q < H / 4; ++q) {
+              const float4 v = __ldg(src + q);
+              dst[(2 + 4 * q) * S::CS] = v.x;
+              dst[(3 + 4 * q) * S::CS] = v.y;
+              dst[(4 + 4 * q) * S::CS] = v.z;
+              dst[(5 + 4 * q) * S::CS] = v.w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < H; ++q) dst[(2 + q) * S::CS] = 0.0f;
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTile) : "memory");
+      }
+      const int s = i % kNS;
+      if (i >= kNS) tc::mbar_wait(&empty[s], ((i / kNS) - 1) & 1);
+      unsigned char* As = ring + s * (S::A_BYTES + S::B_BYTES);
+      unsigned char* Bs = As + S::A_BYTES;
+      // B: dY[n][co][p0 .. p0+32) -> K-major rows co (LDGSTS, 16 bytes each)
+      for (uint32_t t = tid; t < static_cast<uint32_t>(COUT * (kKC / 4)); t += kTile) {
+        const uint32_t co = t / (kKC / 4), c = t % (kKC / 4);
+        cp_async16(Bs + tc::kmajor_off(co, c * 4, COUT),
+                   dout + (static_cast<uint64_t>(n) * COUT + co) * S::HW + p0 + c * 4);
+      }
+      // A': row k' x 32 pixels, 4 pixels (one image row, w..w+3) per 16-byte unit
+#pragma unroll
+      for (int j = 0; j < kKC / 4; ++j) {
+        const uint32_t pj = p0 + 4 * j, h = pj / H, w = pj % H;
+        float4 v;
+        if (real) {
+          const float* b = xs + ((h + rkh) * S::HP + w + rkw) * S::CS + rci;
+          v = make_float4(b[0], b[S::CS], b[2 * S::CS], b[3 * S::CS]);
+        } else {
+          const float o = ones ? 1.0f : 0.0f;
+          v = make_float4(o, o, o, o);
+        }
+        *reinterpret_cast<float4*>(As + tc::kmajor_off(tid, 4 * j, kTile)) = v;
+      }
+      cp_async_commit();
+      if (i > 0) {  // chunk i-1: its LDGSTS landed, A' stores done -> hand the stage over
+        cp_async_wait<1>();
+        tc::fence_async_smem();
+        tc::mbar_arrive(&full[(i - 1) % kNS]);
+      }
+    }
+    if (nchunks > 0) {
+      cp_async_wait<0>();
+      tc::fence_async_smem();
+      tc::mbar_arrive(&full[(nchunks - 1) % kNS]);
+      tc::mbar_wait(&done, 0);
+      tc::fence_after();
+    }
+    // epilogue: TMEM row tid = k' (tile mt) -> part[split][k'][co]
+    const uint32_t kp = mt * kTile + tid;
+#pragma unroll
+    for (int cb = 0; cb < COUT; cb += 32) {
+      float v[32];
+      tc::tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cb, v);
+      if (kp <= static_cast<uint32_t>(S::K)) {
+        float* dst = part + (static_cast<uint64_t>(split) * (S::K + 1) + kp) * COUT + cb;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dst[j] = nchunks > 0 ? v[j] : 0.0f;
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 4) tc::tmem_free<COUT>(tmem);
+}
+
+// grad W[co][ci*25 + kh*5 + kw] and b[co] from part[split][k'][co], splits summed in order
+__global__ void wgrad_reduce_kernel(const float* __restrict__ part, uint32_t nsplit, uint32_t cin, uint32_t cout,
+                                    float* __restrict__ gW, float* __restrict__ gb, float inv_b, uint32_t* flags,
+                                    const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t K = cin * 25, t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (K + 1) * cout) return;
+  const uint32_t kp = t / cout, co = t % cout;
+  float s = 0.0f;
+  for (uint32_t sp = 0; sp < nsplit; ++sp) s += part[(static_cast<uint64_t>(sp) * (K + 1) + kp) * cout + co];
+  const float g = s * inv_b;
+  if (!isfinite(g)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
+  if (kp == K) {
+    gb[co] = g;
+  } else {
+    const uint32_t khw = kp / cin, ci = kp - khw * cin;
+    gW[static_cast<uint64_t>(co) * K + ci * 25 + khw] = g;
+  }
+}
+
 // Wpk[chunk][canonical K-major COUT x 32] = W[co][chunk*32 + kk] (0 beyond K): each K
 // chunk of the weights becomes one contiguous block for a single TMA bulk copy.
 __global__ void pack_w_kernel(const float* __restrict__ W, float* __restrict__ Wpk, uint32_t cout, uint32_t cin,
@@ -255,5 +445,29 @@ template int launch_conv5_tc<32, 64, 8>(const float*, const float*, float*, cons
                                         bool, const uint32_t*, cudaStream_t);
 template int launch_conv5_tc<64, 32, 8>(const float*, const float*, float*, const float*, float*, uint32_t,
                                         bool, const uint32_t*, cudaStream_t);
+
+
+template <int CIN, int COUT, int H, int SPS>
+int launch_conv5_wgrad_tc(const float* in, const float* dout, float* part, float* gW, float* gb, uint32_t R,
+                          float inv_b, uint32_t* flags, const uint32_t* gate, cudaStream_t s) {
+  using S = WgradShape<CIN, COUT, H, SPS>;
+  auto k = conv5_wgrad_tc_kernel<CIN, COUT, H, SPS>;
+  static bool attr = false;
+  if (!attr) {
+    DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::SMEM)));
+    attr = true;
+  }
+  const uint32_t nsplit = (R + SPS - 1) / SPS;
+  k<<<dim3(S::MT, nsplit), kTile + 32, S::SMEM, s>>>(in, dout, part, R, gate);
+  const uint32_t n = (S::K + 1) * COUT;
+  wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(part, nsplit, CIN, COUT, gW, gb, inv_b, flags, gate);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+template int launch_conv5_wgrad_tc<32, 32, 16, 4>(const float*, const float*, float*, float*, float*, uint32_t, float,
+                                                   uint32_t*, const uint32_t*, cudaStream_t);
+template int launch_conv5_wgrad_tc<32, 64, 8, 8>(const float*, const float*, float*, float*, float*, uint32_t, float,
+                                                  uint32_t*, const uint32_t*, cudaStream_t);
 
 }  // namespace dsb

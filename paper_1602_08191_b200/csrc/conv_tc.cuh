@@ -105,6 +105,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 template <int CIN, int COUT, int H>
 int launch_conv5_tc(const float* in, const float* W, float* Wpk, const float* b, float* out, uint32_t R, bool relu,
                     const uint32_t* gate, cudaStream_t s);
+// conv_tc.cu: weight and bias gradients of a 5x5 pad-2 convolution as a tcgen05 GEMM over
+// the batch's pixels; part: scratch of conv5_wgrad_part_floats floats.
+template <int CIN, int COUT, int H, int SPS>
+int launch_conv5_wgrad_tc(const float* in, const float* dout, float* part, float* gW, float* gb, uint32_t R,
+                          float inv_b, uint32_t* flags, const uint32_t* gate, cudaStream_t s);
+inline constexpr uint64_t conv5_wgrad_part_floats(uint32_t cin, uint32_t cout, uint32_t R, uint32_t sps) {
+  return static_cast<uint64_t>((R + sps - 1) / sps) * (cin * 25 + 1) * cout;
+}
 inline constexpr uint32_t conv5_tc_wpk_floats(uint32_t cin, uint32_t cout) { return (cin * 25 + 31) / 32 * 32 * cout; }
 
 }  // namespace dsb

@@ -474,8 +474,11 @@ CnnWs carve(uint32_t R, uint32_t C, void* base) {
   w.dc1 = reinterpret_cast<float*>(take(R * 32768 * f));
   w.wt2 = reinterpret_cast<float*>(take(32 * 800 * f));
   w.wt3 = reinterpret_cast<float*>(take(64 * 800 * f));
-  // partials: conv1 per sample (100 x 2400), conv2/3 per 4 samples (25 x 51200)
-  w.part = reinterpret_cast<float*>(take(std::max<size_t>(R * 2400, ((R + 3) / 4) * 64 * 800) * f));
+  // partials: conv1 per sample (100 x 2400), conv2/3 per 4 samples (25 x 51200), or the
+  // tensor-core weight-gradient splits
+  w.part = reinterpret_cast<float*>(take(std::max<size_t>(
+      std::max<size_t>(R * 2400, ((R + 3) / 4) * 64 * 800),
+      std::max<size_t>(conv5_wgrad_part_floats(32, 32, R, 4), conv5_wgrad_part_floats(32, 64, R, 8))) * f));
   w.pb = reinterpret_cast<float*>(take(R * 64 * f));
   w.wpk = reinterpret_cast<float*>(take(conv5_tc_wpk_floats(64, 32) * f));  // largest: 64x25 -> 32 (= 32x25 -> 64)
   w.arg1 = reinterpret_cast<uint8_t*>(take(R * 8192));
@@ -554,9 +557,14 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   // pool3 -> relu3 -> conv3
   avepool_bwd_kernel<<<blocks(R * 64 * 64), 256, 0, s>>>(w.dp3, w.c3, w.dc3, R * 64, 8, gate);
   DS_CUDA_TRY(cudaGetLastError());
-  DS_TRY((launch_conv5_bwd_w<32, 8, 2, 4>(w.p2, w.dc3, w.part, w.pb, R, 64, gate, s)));
-  reduce_parts_kernel<<<blocks(64 * 800), 256, 0, s>>>(w.part, nch4, 64 * 800, grad + L[2].w_off, inv_b, flags, gate);
-  reduce_parts_kernel<<<1, 64, 0, s>>>(w.pb, nch4, 64, grad + L[2].b_off, inv_b, flags, gate);
+  if (use_tensor_cores()) {
+    DS_TRY((launch_conv5_wgrad_tc<32, 64, 8, 8>(w.p2, w.dc3, w.part, grad + L[2].w_off, grad + L[2].b_off, R, inv_b,
+                                                flags, gate, s)));
+  } else {
+    DS_TRY((launch_conv5_bwd_w<32, 8, 2, 4>(w.p2, w.dc3, w.part, w.pb, R, 64, gate, s)));
+    reduce_parts_kernel<<<blocks(64 * 800), 256, 0, s>>>(w.part, nch4, 64 * 800, grad + L[2].w_off, inv_b, flags, gate);
+    reduce_parts_kernel<<<1, 64, 0, s>>>(w.pb, nch4, 64, grad + L[2].b_off, inv_b, flags, gate);
+  }
   flip_transpose_kernel<<<blocks(64 * 800), 256, 0, s>>>(P + L[2].w_off, w.wt3, 64, 32, gate);
   DS_CUDA_TRY(cudaGetLastError());
   if (use_tensor_cores())
@@ -566,9 +574,14 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   // pool2 -> relu2 -> conv2
   avepool_bwd_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.dp2, w.c2, w.dc2, R * 32, 16, gate);
   DS_CUDA_TRY(cudaGetLastError());
-  DS_TRY((launch_conv5_bwd_w<32, 16, 2, 4>(w.p1, w.dc2, w.part, w.pb, R, 32, gate, s)));
-  reduce_parts_kernel<<<blocks(32 * 800), 256, 0, s>>>(w.part, nch4, 32 * 800, grad + L[1].w_off, inv_b, flags, gate);
-  reduce_parts_kernel<<<1, 32, 0, s>>>(w.pb, nch4, 32, grad + L[1].b_off, inv_b, flags, gate);
+  if (use_tensor_cores()) {
+    DS_TRY((launch_conv5_wgrad_tc<32, 32, 16, 4>(w.p1, w.dc2, w.part, grad + L[1].w_off, grad + L[1].b_off, R, inv_b,
+                                                 flags, gate, s)));
+  } else {
+    DS_TRY((launch_conv5_bwd_w<32, 16, 2, 4>(w.p1, w.dc2, w.part, w.pb, R, 32, gate, s)));
+    reduce_parts_kernel<<<blocks(32 * 800), 256, 0, s>>>(w.part, nch4, 32 * 800, grad + L[1].w_off, inv_b, flags, gate);
+    reduce_parts_kernel<<<1, 32, 0, s>>>(w.pb, nch4, 32, grad + L[1].b_off, inv_b, flags, gate);
+  }
   flip_transpose_kernel<<<blocks(32 * 800), 256, 0, s>>>(P + L[1].w_off, w.wt2, 32, 32, gate);
   DS_CUDA_TRY(cudaGetLastError());
   if (use_tensor_cores())

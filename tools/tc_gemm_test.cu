@@ -30,6 +30,7 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
          | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 
+template <int kAMN>
 __global__ void __launch_bounds__(128) tc_gemm(const float* A, const float* B, float* D) {
   __shared__ __align__(128) float sa[M * K];
   __shared__ __align__(128) float sb[N * K];
@@ -39,7 +40,11 @@ __global__ void __launch_bounds__(128) tc_gemm(const float* A, const float* B, f
   // operands -> canonical layout (chunks of 4 tf32 = 16 B)
   for (int i = tid; i < M * K; i += 128) {
     const int m = i / K, k = i % K, c = k / 4;
-    sa[(c * (M / 8) * 128 + (m / 8) * 128 + (m % 8) * 16) / 4 + k % 4] = A[i];
+    if (kAMN)  // MN-major: (m-quad, k): 16 B rows of 4 consecutive m; 8 k-rows per core matrix;
+               // m-quads 128 B apart (SBO), 8-k groups (M/4)*128 B apart (LBO)
+      sa[((m / 4) * 128 + (k / 8) * (M / 4) * 128 + (k % 8) * 16) / 4 + m % 4] = A[i];
+    else
+      sa[(c * (M / 8) * 128 + (m / 8) * 128 + (m % 8) * 16) / 4 + k % 4] = A[i];
   }
   for (int i = tid; i < N * K; i += 128) {
     const int n = i / K, k = i % K, c = k / 4;
@@ -59,9 +64,11 @@ __global__ void __launch_bounds__(128) tc_gemm(const float* A, const float* B, f
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   if (tid == 0) {
-    const uint32_t id = idesc_tf32(M, N);
+    const uint32_t id = idesc_tf32(M, N) | (kAMN ? (1u << 15) : 0u);
     for (int t = 0; t < K / 8; ++t) {  // K = 8 per tf32 MMA = 2 chunks
-      const uint64_t da = sdesc(smem_u32(sa) + 2 * t * (M / 8) * 128, (M / 8) * 128, 128);
+      const uint64_t da = kAMN == 1 ? sdesc(smem_u32(sa) + t * (M / 4) * 128, (M / 4) * 128, 128)
+                        : kAMN == 2 ? sdesc(smem_u32(sa) + t * (M / 4) * 128, 128, (M / 4) * 128)
+                                    : sdesc(smem_u32(sa) + 2 * t * (M / 8) * 128, (M / 8) * 128, 128);
       const uint64_t db = sdesc(smem_u32(sb) + 2 * t * (N / 8) * 128, (N / 8) * 128, 128);
       const uint32_t acc = t > 0;
       asm volatile(
@@ -106,7 +113,11 @@ int main() {
   cudaMemcpy(A, hA, M * K * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(B, hB, N * K * 4, cudaMemcpyHostToDevice);
   cudaMemset(D, 0, M * N * 4);
-  tc_gemm<<<1, 128>>>(A, B, D);
+  for (int mode = 0; mode < 3; ++mode) {
+  cudaMemset(D, 0, M * N * 4);
+  if (mode == 0) tc_gemm<0><<<1, 128>>>(A, B, D);
+  else if (mode == 1) tc_gemm<1><<<1, 128>>>(A, B, D);
+  else tc_gemm<2><<<1, 128>>>(A, B, D);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(hD, D, M * N * 4, cudaMemcpyDeviceToHost);
   double maxerr = 0, maxref = 0;
@@ -117,7 +128,8 @@ int main() {
       maxerr = fmax(maxerr, fabs(r - hD[m * N + n]));
       maxref = fmax(maxref, fabs(r));
     }
-  printf("tcgen05 tf32 GEMM %dx%dx%d: %s, max |err| %.3e (max |ref| %.3e), D[0]=%f D[last]=%f\n", M, N, K,
-         cudaGetErrorString(e), maxerr, maxref, hD[0], hD[M * N - 1]);
+  printf("tcgen05 tf32 GEMM %dx%dx%d A %s-major: %s, max |err| %.3e (max |ref| %.3e), D[0]=%f D[last]=%f\n", M, N,
+         K, mode == 0 ? "K" : (mode == 1 ? "MN(lbo=kgrp)" : "MN(lbo=128)"), cudaGetErrorString(e), maxerr, maxref, hD[0], hD[M * N - 1]);
+  }
   return 0;
 }
