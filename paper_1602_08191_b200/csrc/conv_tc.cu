@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
 template <int CIN, int COUT, int H, int SPS>
 struct WgradShape {
   static constexpr int HW = H * H, HP = H + 4, CS = CIN + 4, K = CIN * 25, MT = (K + 1 + kTile - 1) / kTile;
-  static constexpr int XS = HP * HP * CS, CPS = HW / kKC;  // staged floats, pixel chunks per sample
+  static constexpr bool kHWC = CIN % kKC == 0;  // else CHW staging and the reference k order (conv1)
+  static constexpr int XS = kHWC ? HP * HP * CS : CIN * HP * HP, CPS = HW / kKC;  // staged floats, chunks/sample
   static constexpr int A_BYTES = kTile * kKC * 4, B_BYTES = COUT * kKC * 4;
   static constexpr size_t SMEM = static_cast<size_t>(XS) * 4 + kNS * (A_BYTES + B_BYTES) + 1024;
 };
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
                                                                        float* __restrict__ part, uint32_t R,
                                                                        const uint32_t* gate) {
   using S = WgradShape<CIN, COUT, H, SPS>;
-  static_assert(CIN % 4 == 0 && S::HW % kKC == 0 && COUT % 32 == 0, "wgrad tiling");
+  static_assert(S::HW % kKC == 0 && COUT % 32 == 0, "wgrad tiling");
   if (gate && *gate) return;
   extern __shared__ __align__(128) unsigned char smem[];
   float* xs = reinterpret_cast<float*>(smem);
@@ -291,8 +292,20 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
     // this thread's row k' of the tile: (kh, kw, ci), the ones row (bias) or padding
     const uint32_t krow = mt * kTile + tid;
     const bool real = krow < static_cast<uint32_t>(S::K), ones = krow == static_cast<uint32_t>(S::K);
-    const uint32_t khw = real ? krow / CIN : 0, rci = real ? krow - khw * CIN : 0;
-    const uint32_t rkh = khw / 5, rkw = khw - rkh * 5;
+    uint32_t rci = 0, rkh = 0, rkw = 0;
+    if (real) {
+      if constexpr (S::kHWC) {
+        const uint32_t khw = krow / CIN;
+        rci = krow - khw * CIN;
+        rkh = khw / 5;
+        rkw = khw - rkh * 5;
+      } else {
+        rci = krow / 25;
+        const uint32_t r = krow - rci * 25;
+        rkh = r / 5;
+        rkw = r - rkh * 5;
+      }
+    }
     for (int i = 0; i < nchunks; ++i) {
       const uint32_t n = n_lo + i / S::CPS, p0 = (i % S::CPS) * kKC;
       if (i % S::CPS == 0) {  // stage sample n as HWC (all producers; the ring holds copies)
@@ -300,21 +313,23 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
         for (uint32_t j = tid; j < static_cast<uint32_t>(CIN * S::HP); j += kTile) {
           const uint32_t ci = j % CIN, row = j / CIN;
           const int y = static_cast<int>(row) - 2;
-          float* dst = xs + static_cast<size_t>(row) * S::HP * S::CS + ci;
-          dst[0] = dst[S::CS] = dst[(H + 2) * S::CS] = dst[(H + 3) * S::CS] = 0.0f;
+          constexpr uint32_t step = S::kHWC ? S::CS : 1;
+          float* dst = S::kHWC ? xs + static_cast<size_t>(row) * S::HP * S::CS + ci
+                               : xs + (static_cast<size_t>(ci) * S::HP + row) * S::HP;
+          dst[0] = dst[step] = dst[(H + 2) * step] = dst[(H + 3) * step] = 0.0f;
           if (y >= 0 && y < H) {
             const float4* src = reinterpret_cast<const float4*>(in + ((static_cast<uint64_t>(n) * CIN + ci) * H + y) * H);
 #pragma unroll
             for (int q = 0; q < H / 4; ++q) {
               const float4 v = __ldg(src + q);
-              dst[(2 + 4 * q) * S::CS] = v.x;
-              dst[(3 + 4 * q) * S::CS] = v.y;
-              dst[(4 + 4 * q) * S::CS] = v.z;
-              dst[(5 + 4 * q) * S::CS] = v.w;
+              dst[(2 + 4 * q) * step] = v.x;
+              dst[(3 + 4 * q) * step] = v.y;
+              dst[(4 + 4 * q) * step] = v.z;
+              dst[(5 + 4 * q) * step] = v.w;
             }
           } else {
 #pragma unroll
-            for (int q = 0; q < H; ++q) dst[(2 + q) * S::CS] = 0.0f;
+            for (int q = 0; q < H; ++q) dst[(2 + q) * step] = 0.0f;
           }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kTile) : "memory");
@@ -335,8 +350,13 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
         const uint32_t pj = p0 + 4 * j, h = pj / H, w = pj % H;
         float4 v;
         if (real) {
-          const float* b = xs + ((h + rkh) * S::HP + w + rkw) * S::CS + rci;
-          v = make_float4(b[0], b[S::CS], b[2 * S::CS], b[3 * S::CS]);
+          if constexpr (S::kHWC) {
+            const float* b = xs + ((h + rkh) * S::HP + w + rkw) * S::CS + rci;
+            v = make_float4(b[0], b[S::CS], b[2 * S::CS], b[3 * S::CS]);
+          } else {
+            const float* b = xs + (rci * S::HP + h + rkh) * S::HP + w + rkw;
+            v = make_float4(b[0], b[1], b[2], b[3]);
+          }
         } else {
           const float o = ones ? 1.0f : 0.0f;
           v = make_float4(o, o, o, o);
@@ -377,8 +397,8 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
 
 // grad W[co][ci*25 + kh*5 + kw] and b[co] from part[split][k'][co], splits summed in order
 __global__ void wgrad_reduce_kernel(const float* __restrict__ part, uint32_t nsplit, uint32_t cin, uint32_t cout,
-                                    float* __restrict__ gW, float* __restrict__ gb, float inv_b, uint32_t* flags,
-                                    const uint32_t* gate) {
+                                    bool hwc, float* __restrict__ gW, float* __restrict__ gb, float inv_b,
+                                    uint32_t* flags, const uint32_t* gate) {
   if (gate && *gate) return;
   const uint32_t K = cin * 25, t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (K + 1) * cout) return;
@@ -389,9 +409,11 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, uint32_t nsp
   if (!isfinite(g)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
   if (kp == K) {
     gb[co] = g;
-  } else {
+  } else if (hwc) {
     const uint32_t khw = kp / cin, ci = kp - khw * cin;
     gW[static_cast<uint64_t>(co) * K + ci * 25 + khw] = g;
+  } else {
+    gW[static_cast<uint64_t>(co) * K + kp] = g;
   }
 }
 
@@ -460,11 +482,13 @@ int launch_conv5_wgrad_tc(const float* in, const float* dout, float* part, float
   const uint32_t nsplit = (R + SPS - 1) / SPS;
   k<<<dim3(S::MT, nsplit), kTile + 32, S::SMEM, s>>>(in, dout, part, R, gate);
   const uint32_t n = (S::K + 1) * COUT;
-  wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(part, nsplit, CIN, COUT, gW, gb, inv_b, flags, gate);
+  wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(part, nsplit, CIN, COUT, S::kHWC, gW, gb, inv_b, flags, gate);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
 
+template int launch_conv5_wgrad_tc<3, 32, 32, 1>(const float*, const float*, float*, float*, float*, uint32_t, float,
+                                                  uint32_t*, const uint32_t*, cudaStream_t);
 template int launch_conv5_wgrad_tc<32, 32, 16, 4>(const float*, const float*, float*, float*, float*, uint32_t, float,
                                                    uint32_t*, const uint32_t*, cudaStream_t);
 template int launch_conv5_wgrad_tc<32, 64, 8, 8>(const float*, const float*, float*, float*, float*, uint32_t, float,

@@ -251,6 +251,52 @@ __global__ void fc_fwd_kernel(const float* __restrict__ a, const float* __restri
   }
 }
 
+// out[r][o] = b[o] + sum_i W[o][i] a[r][i] for 64 outputs, split over K: CTA = (16 rows,
+// one 128-wide K slice), thread = (row, 4 outputs), 64-wide tiles staged in smem (the W
+// tile is shared by the 16 rows); part[slice][r][o], summed in slice order by fc64_reduce.
+constexpr uint32_t kFcSlice = 128;
+__global__ void __launch_bounds__(256) fc64_fwd_kernel(const float* __restrict__ a, const float* __restrict__ W,
+                                                       float* __restrict__ part, uint32_t R, uint32_t in,
+                                                       const uint32_t* gate) {
+  if (gate && *gate) return;
+  __shared__ float as[16][65];
+  __shared__ float ws[64][65];
+  const uint32_t r0 = blockIdx.x * 16, tid = threadIdx.x, rl = tid >> 4, o4 = (tid & 15) * 4;
+  const uint32_t klo = blockIdx.y * kFcSlice, khi = min(klo + kFcSlice, in);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (uint32_t k0 = klo; k0 < khi; k0 += 64) {
+    for (uint32_t t = tid; t < 16 * 64; t += 256) {
+      const uint32_t r = t >> 6, k = t & 63;
+      as[r][k] = (r0 + r < R && k0 + k < khi) ? a[static_cast<size_t>(r0 + r) * in + k0 + k] : 0.0f;
+    }
+    for (uint32_t t = tid; t < 64 * 64; t += 256) {
+      const uint32_t o = t >> 6, k = t & 63;
+      ws[o][k] = k0 + k < khi ? __ldg(W + static_cast<size_t>(o) * in + k0 + k) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (uint32_t k = 0; k < 64; ++k) {
+      const float x = as[rl][k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] = fmaf(ws[o4 + j][k], x, acc[j]);
+    }
+    __syncthreads();
+  }
+  if (r0 + rl < R)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) part[(static_cast<size_t>(blockIdx.y) * R + r0 + rl) * 64 + o4 + j] = acc[j];
+}
+
+__global__ void fc64_reduce_kernel(const float* __restrict__ part, const float* __restrict__ b, float* __restrict__ out,
+                                   uint32_t R, uint32_t nslice, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= R * 64) return;
+  float s = b[t & 63];
+  for (uint32_t k = 0; k < nslice; ++k) s += part[static_cast<size_t>(k) * R * 64 + t];
+  out[t] = s;
+}
+
 // dW[o][i] = inv_b * sum_r d[r][o] a[r][i]; db[o] = inv_b * sum_r d[r][o] (threads i == 0
 // of each o also produce db). One thread per (o, i), rows in order.
 __global__ void fc_bwd_w_kernel(const float* __restrict__ d, const float* __restrict__ a, float* __restrict__ gW,
@@ -441,6 +487,7 @@ struct CnnWs {
   float *dz, *dh1, *dp3, *dc3, *dp2, *dc2, *dr1, *dc1;    // backward
   float *wt2, *wt3, *part, *pb;                            // flipped weights, partial dW / db
   float* wpk;                                              // tcgen05 packed weight chunks
+  float* fcpart;                                           // ip1 split-K partials
   uint8_t* arg1;
   double* loss_rows;
   size_t bytes;
@@ -480,7 +527,8 @@ CnnWs carve(uint32_t R, uint32_t C, void* base) {
       std::max<size_t>(R * 2400, ((R + 3) / 4) * 64 * 800),
       std::max<size_t>(conv5_wgrad_part_floats(32, 32, R, 4), conv5_wgrad_part_floats(32, 64, R, 8))) * f));
   w.pb = reinterpret_cast<float*>(take(R * 64 * f));
-  w.wpk = reinterpret_cast<float*>(take(conv5_tc_wpk_floats(64, 32) * f));  // largest: 64x25 -> 32 (= 32x25 -> 64)
+  w.wpk = reinterpret_cast<float*>(take(conv5_tc_wpk_floats(64, 32) * f));
+  w.fcpart = reinterpret_cast<float*>(take(static_cast<size_t>(R) * 64 * (1024 / kFcSlice) * f));  // largest: 64x25 -> 32 (= 32x25 -> 64)
   w.arg1 = reinterpret_cast<uint8_t*>(take(R * 8192));
   w.loss_rows = reinterpret_cast<double*>(take(R * sizeof(double)));
   w.bytes = off;
@@ -526,8 +574,8 @@ static int cnn_forward(const ModelInfo& m, const float* P, const float* X, const
   else
     DS_TRY((launch_conv5<32, 64, 8, 16, 1, 4>(w.p2, P + L[2].w_off, P + L[2].b_off, w.c3, R, true, gate, s)));
   avepool_kernel<<<blocks(R * 64 * 16), 256, 0, s>>>(w.c3, w.p3, R * 64, 8, gate);
-  fc_fwd_kernel<4><<<R, 256, (1024 + 4 * 64) * sizeof(float), s>>>(w.p3, P + L[3].w_off, P + L[3].b_off, w.h1, 1024,
-                                                                   64, gate);
+  fc64_fwd_kernel<<<dim3((R + 15) / 16, 1024 / kFcSlice), 256, 0, s>>>(w.p3, P + L[3].w_off, w.fcpart, R, 1024, gate);
+  fc64_reduce_kernel<<<blocks(R * 64), 256, 0, s>>>(w.fcpart, P + L[3].b_off, w.h1, R, 1024 / kFcSlice, gate);
   fc_fwd_kernel<1><<<R, 64, (64 + m.n_classes) * sizeof(float), s>>>(w.h1, P + L[4].w_off, P + L[4].b_off, w.z, 64,
                                                                      m.n_classes, gate);
   DS_CUDA_TRY(cudaGetLastError());
@@ -591,9 +639,14 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   // relu1 -> pool1 (max) -> conv1 (weights only), one sample per partial
   maxpool_relu_bwd_kernel<<<blocks(R * 32 * 1024), 256, 0, s>>>(w.dr1, w.arg1, w.dc1, R * 32, 32, gate);
   DS_CUDA_TRY(cudaGetLastError());
-  DS_TRY((launch_conv5_bwd_w<3, 32, 32, 1>(idx ? w.x0 : X, w.dc1, w.part, w.pb, R, 32, gate, s)));
-  reduce_parts_kernel<<<blocks(32 * 75), 256, 0, s>>>(w.part, R, 32 * 75, grad + L[0].w_off, inv_b, flags, gate);
-  reduce_parts_kernel<<<1, 32, 0, s>>>(w.pb, R, 32, grad + L[0].b_off, inv_b, flags, gate);
+  if (use_tensor_cores()) {
+    DS_TRY((launch_conv5_wgrad_tc<3, 32, 32, 1>(idx ? w.x0 : X, w.dc1, w.part, grad + L[0].w_off, grad + L[0].b_off, R,
+                                                inv_b, flags, gate, s)));
+  } else {
+    DS_TRY((launch_conv5_bwd_w<3, 32, 32, 1>(idx ? w.x0 : X, w.dc1, w.part, w.pb, R, 32, gate, s)));
+    reduce_parts_kernel<<<blocks(32 * 75), 256, 0, s>>>(w.part, R, 32 * 75, grad + L[0].w_off, inv_b, flags, gate);
+    reduce_parts_kernel<<<1, 32, 0, s>>>(w.pb, R, 32, grad + L[0].b_off, inv_b, flags, gate);
+  }
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
