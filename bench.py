@@ -471,7 +471,8 @@ def cifar_leg(args, L, api, torch, dist, world, rank, local):
     return {"metric": "train samples/s (cifar10_quick, BASELINE config 2 shape)", "value": world * B * K / (ms / 1e3),
             "unit": "samples/s", "ms_per_step": ms / K, "steps": K, "batch_per_worker": B, "tau": 10, "alpha": 0.1,
             "eta": 0.01, "workers": world, "exchange": "LockFree, center sharded over the GPUs" if world > 1 else
-            "LockFree, center on the same GPU", "dtype": "f32 (CUDA-core FFMA)", "data": "synthetic gen_synthetic "
+            "LockFree, center on the same GPU", "dtype": "tf32 tensor cores (tcgen05 implicit-GEMM convolutions, f32 "
+            "accumulation in TMEM), f32 elsewhere", "data": "synthetic gen_synthetic "
             "3072 features (3x32x32 CHW), 10 classes, 10,000 rows per GPU",
             "achieved_tflops": flop / (ms / 1e3) / 1e12, "gpu_launches": int(n1.value - n0.value),
             "loss_first_last": [float(loss[0]), float(loss[-1])],

@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
   constexpr uint32_t kThreads = kTile + 32;
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
   const uint32_t mt = blockIdx.x, split = blockIdx.y;
+  constexpr int kLag = 1;  // chunks of LDGSTS in flight per producer before it hands a stage over
   const uint32_t n_lo = split * SPS, n_hi = min(n_lo + SPS, R);
   const int nchunks = static_cast<int>(n_hi > n_lo ? (n_hi - n_lo) * S::CPS : 0);
   if (warp == 4) tc::tmem_alloc<COUT>(&tmem_base);
@@ -364,16 +365,16 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
         *reinterpret_cast<float4*>(As + tc::kmajor_off(tid, 4 * j, kTile)) = v;
       }
       cp_async_commit();
-      if (i > 0) {  // chunk i-1: its LDGSTS landed, A' stores done -> hand the stage over
-        cp_async_wait<1>();
+      if (i >= kLag) {  // chunk i-kLag: its LDGSTS landed, A' stores done -> hand the stage over
+        cp_async_wait<kLag>();
         tc::fence_async_smem();
-        tc::mbar_arrive(&full[(i - 1) % kNS]);
+        tc::mbar_arrive(&full[(i - kLag) % kNS]);
       }
     }
     if (nchunks > 0) {
       cp_async_wait<0>();
       tc::fence_async_smem();
-      tc::mbar_arrive(&full[(nchunks - 1) % kNS]);
+      for (int i = nchunks > kLag ? nchunks - kLag : 0; i < nchunks; ++i) tc::mbar_arrive(&full[i % kNS]);
       tc::mbar_wait(&done, 0);
       tc::fence_after();
     }
