@@ -17,4 +17,12 @@ if [ "${NO_NCU:-0}" != "1" ]; then
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:elastic -s 2 -c 1 \
       -o gpurun_out/${TAG}_prof_elastic python tools/prof_exchange.py > gpurun_out/${TAG}_ncu3.log 2>&1
 fi
+
+if [ "${NO_NCU:-0}" != "1" ]; then
+  timeout 300 python tools/prof_cnn.py --steps 20 > gpurun_out/${TAG}_cnn.log 2>&1 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_cnn_launches.csv \
+      python tools/prof_cnn.py --steps 20 > gpurun_out/${TAG}_ncu4.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv5_tc_kernel -s 1 -c 1 \
+      -o gpurun_out/${TAG}_prof_conv_tc python tools/prof_cnn.py --steps 5 > gpurun_out/${TAG}_ncu5.log 2>&1
+fi
 echo done
