@@ -39,7 +39,9 @@ struct ConvTcShape {
   static constexpr int ROWS = kMulti ? HP : kTile / H + 4;    // staged input rows per sample
   static constexpr int XS = kHWC ? SPT * ROWS * HP * CS : SPT * CIN * ROWS * HP;  // staged input floats
   static constexpr int A_BYTES = kTile * kKC * 4, B_BYTES = COUT * kKC * 4;
-  static constexpr size_t SMEM = static_cast<size_t>(XS) * 4 + kNS * (A_BYTES + B_BYTES) + NKC * kKC * 4 + 1024;
+  static constexpr size_t SMEM = static_cast<size_t>(XS) * 4 + kNS * B_BYTES + NKC * kKC * 4 + 1024;
+  // TMEM: accumulator (COUT columns) + the A ring (kNS x 32 columns)
+  static constexpr uint32_t TMEM_COLS = COUT + kNS * kKC <= 128 ? 128 : (COUT + kNS * kKC <= 256 ? 256 : 512);
 };
 
 template <int CIN, int COUT, int H>
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
   extern __shared__ __align__(128) unsigned char smem[];
   float* xs = reinterpret_cast<float*>(smem);
   unsigned char* ring = smem + ((static_cast<size_t>(S::XS) * 4 + 127) & ~static_cast<size_t>(127));
-  int* koff = reinterpret_cast<int*>(ring + kNS * (S::A_BYTES + S::B_BYTES));  // [NKC*32] im2col offsets
+  int* koff = reinterpret_cast<int*>(ring + kNS * S::B_BYTES);  // [NKC*32] im2col offsets
   __shared__ __align__(8) uint64_t full[kNS], empty[kNS], done;
   __shared__ uint32_t tmem_base;
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
@@ -61,7 +63,7 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
   const uint32_t h0 = S::kMulti ? 0 : static_cast<uint32_t>((g0 % S::HW) / H);  // first output row
 
   constexpr uint32_t kThreads = kTile + 32;
-  if (warp == 4) tc::tmem_alloc<(COUT < 32 ? 32 : COUT)>(&tmem_base);
+  if (warp == 4) tc::tmem_alloc<S::TMEM_COLS>(&tmem_base);
   if (tid == 0) {
     for (int s = 0; s < kNS; ++s) {
       tc::mbar_init(&full[s], kTile);  // producer arrivals; thread 0 also adds W's tx bytes
@@ -122,14 +124,13 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
     if ((tid & 31) == 0) {
       for (int i = 0; i < S::NKC; ++i) {
         const int s = i % kNS;
-        unsigned char* As = ring + s * (S::A_BYTES + S::B_BYTES);
-        unsigned char* Bs = As + S::A_BYTES;
+        unsigned char* Bs = ring + s * S::B_BYTES;
+        const uint32_t ta = tmem + COUT + s * kKC;  // A stage s: TMEM columns
         tc::mbar_wait(&full[s], (i / kNS) & 1);
         tc::fence_after();
 #pragma unroll
         for (int t = 0; t < kKC / 8; ++t)
-          tc::mma_tf32(tmem, tc::saddr(As) + t * 2 * a_lbo, a_lbo, tc::saddr(Bs) + t * 2 * b_lbo, b_lbo, idesc,
-                       i > 0 || t > 0);
+          tc::mma_tf32_ta(tmem, ta + t * 8, tc::saddr(Bs) + t * 2 * b_lbo, b_lbo, idesc, i > 0 || t > 0);
         tc::commit(&empty[s]);
       }
       tc::commit(&done);
@@ -144,8 +145,7 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
     for (int i = 0; i < S::NKC; ++i) {
       const int s = i % kNS;
       if (i >= kNS) tc::mbar_wait(&empty[s], ((i / kNS) - 1) & 1);
-      unsigned char* As = ring + s * (S::A_BYTES + S::B_BYTES);
-      unsigned char* Bs = As + S::A_BYTES;
+      unsigned char* Bs = ring + s * S::B_BYTES;
       const int k0 = i * kKC;
       if (tid == 0) {  // W chunk i: one bulk copy of the pre-packed block
         asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(tc::saddr(&full[s])), "r"(S::B_BYTES)
@@ -156,30 +156,29 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
             "l"(Wpk + static_cast<size_t>(i) * COUT * kKC), "r"(S::B_BYTES), "r"(tc::saddr(&full[s]))
             : "memory");
       }
-      // A: this row's 32 K values (im2col), 16 bytes per core-matrix row
+      // A: this row's 32 K values (im2col) -> TMEM lane tid, the stage's 32 columns
+      float av[kKC];
       if constexpr (S::kHWC) {
         const int khw = k0 / CIN, ci0 = k0 - khw * CIN, kh = khw / 5, kw = khw - kh * 5;
         const float4* src = reinterpret_cast<const float4*>(
             xs + ((static_cast<size_t>(sl) * S::ROWS + ph + kh) * S::HP + pw + kw) * S::CS + ci0);
-        float4 v[kKC / 4];
-#pragma unroll
-        for (int c = 0; c < kKC / 4; ++c) v[c] = valid ? src[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < kKC / 4; ++c) *reinterpret_cast<float4*>(As + tc::kmajor_off(tid, c * 4, kTile)) = v[c];
-      } else {
 #pragma unroll
         for (int c = 0; c < kKC / 4; ++c) {
-          float4 v;
-          float* pv = reinterpret_cast<float*>(&v);
+          const float4 v = valid ? src[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+          av[4 * c] = v.x;
+          av[4 * c + 1] = v.y;
+          av[4 * c + 2] = v.z;
+          av[4 * c + 3] = v.w;
+        }
+      } else {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int o = koff[k0 + c * 4 + j];
-            pv[j] = (valid && o >= 0) ? xrow[o] : 0.0f;
-          }
-          *reinterpret_cast<float4*>(As + tc::kmajor_off(tid, c * 4, kTile)) = v;
+        for (int j = 0; j < kKC; ++j) {
+          const int o = koff[k0 + j];
+          av[j] = (valid && o >= 0) ? xrow[o] : 0.0f;
         }
       }
-      tc::fence_async_smem();
+      tc::tmem_st32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + COUT + s * kKC, av);
+      tc::fence_before();
       tc::mbar_arrive(&full[s]);
     }
     tc::mbar_wait(&done, 0);
@@ -202,7 +201,7 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 4) tc::tmem_free<(COUT < 32 ? 32 : COUT)>(tmem);
+  if (warp == 4) tc::tmem_free<S::TMEM_COLS>(tmem);
 }
 
 // ---- weight (and bias) gradients: D[k' x COUT] = A'[k' x pixels] * dY[COUT x pixels]^T --
@@ -220,8 +219,9 @@ struct WgradShape {
   static constexpr int HW = H * H, HP = H + 4, CS = CIN + 4, K = CIN * 25, MT = (K + 1 + kTile - 1) / kTile;
   static constexpr bool kHWC = CIN % kKC == 0;  // else CHW staging and the reference k order (conv1)
   static constexpr int XS = kHWC ? HP * HP * CS : CIN * HP * HP, CPS = HW / kKC;  // staged floats, chunks/sample
-  static constexpr int A_BYTES = kTile * kKC * 4, B_BYTES = COUT * kKC * 4;
-  static constexpr size_t SMEM = static_cast<size_t>(XS) * 4 + kNS * (A_BYTES + B_BYTES) + 1024;
+  static constexpr int B_BYTES = COUT * kKC * 4;
+  static constexpr size_t SMEM = static_cast<size_t>(XS) * 4 + kNS * B_BYTES + 1024;
+  static constexpr uint32_t TMEM_COLS = COUT + kNS * kKC <= 128 ? 128 : (COUT + kNS * kKC <= 256 ? 256 : 512);
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
   constexpr int kLag = 1;  // chunks of LDGSTS in flight per producer before it hands a stage over
   const uint32_t n_lo = split * SPS, n_hi = min(n_lo + SPS, R);
   const int nchunks = static_cast<int>(n_hi > n_lo ? (n_hi - n_lo) * S::CPS : 0);
-  if (warp == 4) tc::tmem_alloc<COUT>(&tmem_base);
+  if (warp == 4) tc::tmem_alloc<S::TMEM_COLS>(&tmem_base);
   if (tid == 0) {
     for (int s = 0; s < kNS; ++s) {
       tc::mbar_init(&full[s], kTile);  // one arrival per producer thread
@@ -263,27 +263,19 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
-  constexpr uint32_t a_lbo = kTile / 8 * 128;  // between 4-pixel halves (K-major A')
   constexpr uint32_t b_lbo = COUT / 8 * 128;   // between 4-pixel halves (K-major B)
   constexpr uint32_t idesc = tc::idesc_tf32(kTile, COUT);
   if (warp == 4) {  // ---- MMA issuer ----
     if ((tid & 31) == 0) {
       for (int i = 0; i < nchunks; ++i) {
         const int s = i % kNS;
-        unsigned char* As = ring + s * (S::A_BYTES + S::B_BYTES);
-        unsigned char* Bs = As + S::A_BYTES;
+        unsigned char* Bs = ring + s * S::B_BYTES;
+        const uint32_t ta = tmem + COUT + s * kKC;  // A' stage s: TMEM columns
         tc::mbar_wait(&full[s], (i / kNS) & 1);
         tc::fence_after();
 #pragma unroll
-        for (int t = 0; t < kKC / 8; ++t) {
-          const uint64_t da = tc::sdesc(tc::saddr(As) + t * 2 * a_lbo, a_lbo, 128);
-          const uint64_t db = tc::sdesc(tc::saddr(Bs) + t * 2 * b_lbo, b_lbo, 128);
-          const uint32_t acc = (i > 0 || t > 0) ? 1u : 0u;
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-              "l"(da), "l"(db), "r"(idesc), "r"(acc));
-        }
+        for (int t = 0; t < kKC / 8; ++t)
+          tc::mma_tf32_ta(tmem, ta + t * 8, tc::saddr(Bs) + t * 2 * b_lbo, b_lbo, idesc, i > 0 || t > 0);
         tc::commit(&empty[s]);
       }
       tc::commit(&done);
@@ -337,33 +329,39 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
       }
       const int s = i % kNS;
       if (i >= kNS) tc::mbar_wait(&empty[s], ((i / kNS) - 1) & 1);
-      unsigned char* As = ring + s * (S::A_BYTES + S::B_BYTES);
-      unsigned char* Bs = As + S::A_BYTES;
+      unsigned char* Bs = ring + s * S::B_BYTES;
       // B: dY[n][co][p0 .. p0+32) -> K-major rows co (LDGSTS, 16 bytes each)
       for (uint32_t t = tid; t < static_cast<uint32_t>(COUT * (kKC / 4)); t += kTile) {
         const uint32_t co = t / (kKC / 4), c = t % (kKC / 4);
         cp_async16(Bs + tc::kmajor_off(co, c * 4, COUT),
                    dout + (static_cast<uint64_t>(n) * COUT + co) * S::HW + p0 + c * 4);
       }
-      // A': row k' x 32 pixels, 4 pixels (one image row, w..w+3) per 16-byte unit
+      // A': row k' x 32 pixels (4 per image row segment) -> TMEM lane tid, 32 columns
+      float av[kKC];
 #pragma unroll
       for (int j = 0; j < kKC / 4; ++j) {
         const uint32_t pj = p0 + 4 * j, h = pj / H, w = pj % H;
-        float4 v;
         if (real) {
           if constexpr (S::kHWC) {
             const float* b = xs + ((h + rkh) * S::HP + w + rkw) * S::CS + rci;
-            v = make_float4(b[0], b[S::CS], b[2 * S::CS], b[3 * S::CS]);
+            av[4 * j] = b[0];
+            av[4 * j + 1] = b[S::CS];
+            av[4 * j + 2] = b[2 * S::CS];
+            av[4 * j + 3] = b[3 * S::CS];
           } else {
             const float* b = xs + (rci * S::HP + h + rkh) * S::HP + w + rkw;
-            v = make_float4(b[0], b[1], b[2], b[3]);
+            av[4 * j] = b[0];
+            av[4 * j + 1] = b[1];
+            av[4 * j + 2] = b[2];
+            av[4 * j + 3] = b[3];
           }
         } else {
           const float o = ones ? 1.0f : 0.0f;
-          v = make_float4(o, o, o, o);
+          av[4 * j] = av[4 * j + 1] = av[4 * j + 2] = av[4 * j + 3] = o;
         }
-        *reinterpret_cast<float4*>(As + tc::kmajor_off(tid, 4 * j, kTile)) = v;
       }
+      tc::tmem_st32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + COUT + s * kKC, av);
+      tc::fence_before();
       cp_async_commit();
       if (i >= kLag) {  // chunk i-kLag: its LDGSTS landed, A' stores done -> hand the stage over
         cp_async_wait<kLag>();
@@ -393,7 +391,7 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 4) tc::tmem_free<COUT>(tmem);
+  if (warp == 4) tc::tmem_free<S::TMEM_COLS>(tmem);
 }
 
 // grad W[co][ci*25 + kh*5 + kw] and b[co] from part[split][k'][co], splits summed in order
