@@ -418,28 +418,37 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, uint32_t nsp
 
 // Wpk[chunk][canonical K-major COUT x 32] = W[co][chunk*32 + kk] (0 beyond K): each K
 // chunk of the weights becomes one contiguous block for a single TMA bulk copy.
+// flip: W is the forward weight of the layer whose backward-data this is ([cin][cout][5][5]
+// here); the packed operand is its transposed, 180-degree-rotated kernel
+// W'[co][ci][kh][kw] = W[ci][co][4-kh][4-kw] (no separate flip pass).
 __global__ void pack_w_kernel(const float* __restrict__ W, float* __restrict__ Wpk, uint32_t cout, uint32_t cin,
-                              uint32_t nkc, bool hwc, const uint32_t* gate) {
+                              uint32_t nkc, bool hwc, bool flip, const uint32_t* gate) {
   if (gate && *gate) return;
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nkc * cout * kKC) return;
   const uint32_t K = cin * 25;
   const uint32_t chunk = t / (cout * kKC), rem = t % (cout * kKC), co = rem / kKC, kk = rem % kKC;
   const uint32_t k = chunk * kKC + kk;  // GEMM k; the weight's own index below
-  uint32_t kw_idx = k;
-  if (hwc && k < K) {  // k = (kh*5 + kw)*cin + ci  ->  ci*25 + kh*5 + kw
-    const uint32_t khw = k / cin, ci = k - khw * cin;
-    kw_idx = ci * 25 + khw;
+  float v = 0.0f;
+  if (k < K) {
+    uint32_t ci, khw;
+    if (hwc) {  // k = (kh*5 + kw)*cin + ci
+      khw = k / cin;
+      ci = k - khw * cin;
+    } else {  // k = ci*25 + kh*5 + kw
+      ci = k / 25;
+      khw = k - ci * 25;
+    }
+    v = flip ? W[(static_cast<size_t>(ci) * cout + co) * 25 + (24 - khw)] : W[static_cast<size_t>(co) * K + ci * 25 + khw];
   }
-  Wpk[static_cast<size_t>(chunk) * cout * kKC + tc::kmajor_off(co, kk, cout) / 4] =
-      k < K ? W[static_cast<size_t>(co) * K + kw_idx] : 0.0f;
+  Wpk[static_cast<size_t>(chunk) * cout * kKC + tc::kmajor_off(co, kk, cout) / 4] = v;
 }
 
 }  // namespace
 
 template <int CIN, int COUT, int H>
-int launch_conv5_tc(const float* in, const float* W, float* Wpk, const float* b, float* out, uint32_t R, bool relu,
-                    const uint32_t* gate, cudaStream_t s) {
+int launch_conv5_tc(const float* in, const float* W, bool flip, float* Wpk, const float* b, float* out, uint32_t R,
+                    bool relu, const uint32_t* gate, cudaStream_t s) {
   using S = ConvTcShape<CIN, COUT, H>;
   static_assert(COUT % 32 == 0 && COUT <= 256, "COUT: multiple of 32 (tcgen05 N, TMEM columns)");
   static_assert(H % 4 == 0, "rows are staged as float4");
@@ -451,21 +460,21 @@ int launch_conv5_tc(const float* in, const float* W, float* Wpk, const float* b,
   }
   const uint64_t tiles = (static_cast<uint64_t>(R) * S::HW + kTile - 1) / kTile;
   const uint32_t n = S::NKC * COUT * kKC;
-  pack_w_kernel<<<(n + 255) / 256, 256, 0, s>>>(W, Wpk, COUT, CIN, S::NKC, S::kHWC, gate);
+  pack_w_kernel<<<(n + 255) / 256, 256, 0, s>>>(W, Wpk, COUT, CIN, S::NKC, S::kHWC, flip, gate);
   k<<<static_cast<unsigned>(tiles), kTile + 32, S::SMEM, s>>>(in, Wpk, b, out, R, relu, gate);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
 
 // the convnet's layers: forward (conv1..3) and backward-data (conv3 -> dp2, conv2 -> dr1)
-template int launch_conv5_tc<3, 32, 32>(const float*, const float*, float*, const float*, float*, uint32_t,
-                                        bool, const uint32_t*, cudaStream_t);
-template int launch_conv5_tc<32, 32, 16>(const float*, const float*, float*, const float*, float*, uint32_t,
-                                        bool, const uint32_t*, cudaStream_t);
-template int launch_conv5_tc<32, 64, 8>(const float*, const float*, float*, const float*, float*, uint32_t,
-                                        bool, const uint32_t*, cudaStream_t);
-template int launch_conv5_tc<64, 32, 8>(const float*, const float*, float*, const float*, float*, uint32_t,
-                                        bool, const uint32_t*, cudaStream_t);
+template int launch_conv5_tc<3, 32, 32>(const float*, const float*, bool, float*, const float*, float*,
+                                        uint32_t, bool, const uint32_t*, cudaStream_t);
+template int launch_conv5_tc<32, 32, 16>(const float*, const float*, bool, float*, const float*, float*,
+                                        uint32_t, bool, const uint32_t*, cudaStream_t);
+template int launch_conv5_tc<32, 64, 8>(const float*, const float*, bool, float*, const float*, float*,
+                                        uint32_t, bool, const uint32_t*, cudaStream_t);
+template int launch_conv5_tc<64, 32, 8>(const float*, const float*, bool, float*, const float*, float*,
+                                        uint32_t, bool, const uint32_t*, cudaStream_t);
 
 
 template <int CIN, int COUT, int H, int SPS>

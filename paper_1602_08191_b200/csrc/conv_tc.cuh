@@ -133,9 +133,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // conv_tc.cu: 5x5 pad-2 convolution (forward, or backward-data with flipped/transposed
 // weights) as a tcgen05 implicit GEMM; instantiated for the convnet's layer shapes. Wpk:
 // scratch of conv5_tc_wpk_floats(CIN, COUT) floats for the packed weight chunks.
+// flip: W is the forward weight of the layer being back-propagated ([COUT][CIN] swapped),
+// packed as its transposed, rotated kernel.
 template <int CIN, int COUT, int H>
-int launch_conv5_tc(const float* in, const float* W, float* Wpk, const float* b, float* out, uint32_t R, bool relu,
-                    const uint32_t* gate, cudaStream_t s);
+int launch_conv5_tc(const float* in, const float* W, bool flip, float* Wpk, const float* b, float* out, uint32_t R,
+                    bool relu, const uint32_t* gate, cudaStream_t s);
 // conv_tc.cu: weight and bias gradients of a 5x5 pad-2 convolution as a tcgen05 GEMM over
 // the batch's pixels; part: scratch of conv5_wgrad_part_floats floats.
 template <int CIN, int COUT, int H, int SPS>

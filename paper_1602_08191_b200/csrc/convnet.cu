@@ -560,17 +560,17 @@ static int cnn_forward(const ModelInfo& m, const float* P, const float* X, const
   }
   const bool tcores = use_tensor_cores();
   if (tcores)
-    DS_TRY((launch_conv5_tc<3, 32, 32>(x0, P + L[0].w_off, w.wpk, P + L[0].b_off, w.c1, R, false, gate, s)));
+    DS_TRY((launch_conv5_tc<3, 32, 32>(x0, P + L[0].w_off, false, w.wpk, P + L[0].b_off, w.c1, R, false, gate, s)));
   else
     DS_TRY((launch_conv5<3, 32, 32, 16, 4, 1>(x0, P + L[0].w_off, P + L[0].b_off, w.c1, R, false, gate, s)));
   maxpool_relu_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.c1, w.p1, w.arg1, R * 32, 32, gate);
   if (tcores)
-    DS_TRY((launch_conv5_tc<32, 32, 16>(w.p1, P + L[1].w_off, w.wpk, P + L[1].b_off, w.c2, R, true, gate, s)));
+    DS_TRY((launch_conv5_tc<32, 32, 16>(w.p1, P + L[1].w_off, false, w.wpk, P + L[1].b_off, w.c2, R, true, gate, s)));
   else
     DS_TRY((launch_conv5<32, 32, 16, 16, 2, 2>(w.p1, P + L[1].w_off, P + L[1].b_off, w.c2, R, true, gate, s)));
   avepool_kernel<<<blocks(R * 32 * 64), 256, 0, s>>>(w.c2, w.p2, R * 32, 16, gate);
   if (tcores)
-    DS_TRY((launch_conv5_tc<32, 64, 8>(w.p2, P + L[2].w_off, w.wpk, P + L[2].b_off, w.c3, R, true, gate, s)));
+    DS_TRY((launch_conv5_tc<32, 64, 8>(w.p2, P + L[2].w_off, false, w.wpk, P + L[2].b_off, w.c3, R, true, gate, s)));
   else
     DS_TRY((launch_conv5<32, 64, 8, 16, 1, 4>(w.p2, P + L[2].w_off, P + L[2].b_off, w.c3, R, true, gate, s)));
   avepool_kernel<<<blocks(R * 64 * 16), 256, 0, s>>>(w.c3, w.p3, R * 64, 8, gate);
@@ -613,10 +613,11 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
     reduce_parts_kernel<<<blocks(64 * 800), 256, 0, s>>>(w.part, nch4, 64 * 800, grad + L[2].w_off, inv_b, flags, gate);
     reduce_parts_kernel<<<1, 64, 0, s>>>(w.pb, nch4, 64, grad + L[2].b_off, inv_b, flags, gate);
   }
-  flip_transpose_kernel<<<blocks(64 * 800), 256, 0, s>>>(P + L[2].w_off, w.wt3, 64, 32, gate);
+  if (!use_tensor_cores())
+    flip_transpose_kernel<<<blocks(64 * 800), 256, 0, s>>>(P + L[2].w_off, w.wt3, 64, 32, gate);
   DS_CUDA_TRY(cudaGetLastError());
   if (use_tensor_cores())
-    DS_TRY((launch_conv5_tc<64, 32, 8>(w.dc3, w.wt3, w.wpk, nullptr, w.dp2, R, false, gate, s)));
+    DS_TRY((launch_conv5_tc<64, 32, 8>(w.dc3, P + L[2].w_off, true, w.wpk, nullptr, w.dp2, R, false, gate, s)));
   else
     DS_TRY((launch_conv5<64, 32, 8, 16, 1, 4>(w.dc3, w.wt3, nullptr, w.dp2, R, false, gate, s)));
   // pool2 -> relu2 -> conv2
@@ -630,10 +631,11 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
     reduce_parts_kernel<<<blocks(32 * 800), 256, 0, s>>>(w.part, nch4, 32 * 800, grad + L[1].w_off, inv_b, flags, gate);
     reduce_parts_kernel<<<1, 32, 0, s>>>(w.pb, nch4, 32, grad + L[1].b_off, inv_b, flags, gate);
   }
-  flip_transpose_kernel<<<blocks(32 * 800), 256, 0, s>>>(P + L[1].w_off, w.wt2, 32, 32, gate);
+  if (!use_tensor_cores())
+    flip_transpose_kernel<<<blocks(32 * 800), 256, 0, s>>>(P + L[1].w_off, w.wt2, 32, 32, gate);
   DS_CUDA_TRY(cudaGetLastError());
   if (use_tensor_cores())
-    DS_TRY((launch_conv5_tc<32, 32, 16>(w.dc2, w.wt2, w.wpk, nullptr, w.dr1, R, false, gate, s)));
+    DS_TRY((launch_conv5_tc<32, 32, 16>(w.dc2, P + L[1].w_off, true, w.wpk, nullptr, w.dr1, R, false, gate, s)));
   else
     DS_TRY((launch_conv5<32, 32, 16, 16, 2, 2>(w.dc2, w.wt2, nullptr, w.dr1, R, false, gate, s)));
   // relu1 -> pool1 (max) -> conv1 (weights only), one sample per partial
