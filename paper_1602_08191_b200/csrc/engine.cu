@@ -128,6 +128,12 @@ struct ds_engine {
   double* ring_loss = nullptr;
   float mu = 0.0f;            // momentum (layered path), ds_engine_set_momentum
   float* velocity = nullptr;
+  // layered path: one full-batch iteration captured as a CUDA graph (set_idx + loss/grad +
+  // update + policy), replayed per step; keyed by the pointers it captured
+  cudaGraphExec_t step_graph = nullptr;
+  const void* graph_key[3] = {};
+  uint32_t* cur_idx = nullptr;             // [B] the step's shard rows (set_idx_kernel)
+  unsigned long long* step_ctr = nullptr;  // device step counter within a run
   uint32_t hostfed_rows = 0;
   bool hostfed = false;
 };
@@ -236,28 +242,86 @@ int enqueue_exchange(ds_engine* e, float* p) {
 }
 
 // Layered iterations; with_master = perform fired exchanges against e->master.
+// cur_idx = plan[ctr*B .. +B); ++ctr (one CTA)
+__global__ void set_idx_kernel(const uint32_t* __restrict__ plan, uint32_t B, unsigned long long* ctr,
+                               uint32_t* __restrict__ cur_idx) {
+  const unsigned long long c = *reinterpret_cast<volatile unsigned long long*>(ctr);
+  for (uint32_t r = threadIdx.x; r < B; r += blockDim.x) cur_idx[r] = plan[c * B + r];
+  __syncthreads();
+  if (threadIdx.x == 0) *ctr = c + 1;
+}
+
+// One layered iteration (everything but the exchange) on e->stream.
+int layered_step(ds_engine* e, const float* X, const uint32_t* y, const uint32_t* idx, uint32_t R, bool set_idx) {
+  const uint64_t B = e->hp.batch_size;
+  const float eta = static_cast<float>(e->hp.eta);
+  const float wd = static_cast<float>(e->hp.weight_decay);
+  float* p = e->params[e->cur];
+  if (set_idx) {
+    set_idx_kernel<<<1, B < 1024 ? static_cast<unsigned>(B) : 1024u, 0, e->stream>>>(e->plan, static_cast<uint32_t>(B),
+                                                                                     e->step_ctr, e->cur_idx);
+    idx = e->cur_idx;
+  }
+  DS_TRY(launch_loss_and_grad(e->model, p, X, idx, y, R, e->grad, &e->st->loss, e->ws, &e->st->flags, &e->st->err,
+                              e->stream));
+  if (e->mu > 0.0f)
+    DS_TRY(launch_momentum(p, p, e->velocity, e->grad, e->model.P, eta, e->mu, wd, &e->st->flags, e->stream,
+                           &e->st->err));
+  else
+    DS_TRY(launch_sgd(p, p, e->grad, e->model.P, eta, wd, &e->st->flags, e->stream, &e->st->err));
+  policy_kernel<<<1, 1, 0, e->stream>>>(e->st, e->log);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+bool graphs_enabled() {
+  const char* v = std::getenv("DS_ENGINE_NO_GRAPH");
+  return !(v && v[0] == '1');
+}
+
 int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
   if (!e->hostfed) DS_TRY(upload_plan(e, steps));
   const uint64_t B = e->hp.batch_size;
   const float* X = e->hostfed ? e->Xb : e->X;
   const uint32_t* y = e->hostfed ? e->yb : e->y;
-  const float eta = static_cast<float>(e->hp.eta);
-  const float wd = static_cast<float>(e->hp.weight_decay);
   float* p = e->params[e->cur];
   const bool xm = with_master && e->master;
+  const uint64_t per_step = (e->model.kind == DS_MODEL_CIFAR10_QUICK ? 31 : 3 * e->model.layers.size() + 1) + 2;
+  if (!e->hostfed) {
+    if (!e->cur_idx) {
+      DS_CUDA_TRY(cudaMalloc(&e->cur_idx, B * sizeof(uint32_t)));
+      DS_CUDA_TRY(cudaMalloc(&e->step_ctr, sizeof(unsigned long long)));
+    }
+    DS_CUDA_TRY(cudaMemsetAsync(e->step_ctr, 0, sizeof(unsigned long long), e->stream));
+  }
+  const void* key[3] = {e->plan, p, e->velocity};
+  if (e->step_graph && (key[0] != e->graph_key[0] || key[1] != e->graph_key[1] || key[2] != e->graph_key[2] ||
+                        !graphs_enabled())) {
+    cudaGraphExecDestroy(e->step_graph);
+    e->step_graph = nullptr;
+  }
   for (uint64_t j = 0; j < steps; ++j) {
     const uint32_t R = e->hostfed ? e->hostfed_rows : e->h_rows[j];
-    const uint32_t* idx = e->hostfed ? e->iota : e->plan + j * B;
-    DS_TRY(launch_loss_and_grad(e->model, p, X, idx, y, R, e->grad, &e->st->loss, e->ws,
-                                &e->st->flags, &e->st->err, e->stream));
-    e->launches += e->model.kind == DS_MODEL_CIFAR10_QUICK ? 31 : 3 * e->model.layers.size() + 1;
-    if (e->mu > 0.0f)
-      DS_TRY(launch_momentum(p, p, e->velocity, e->grad, e->model.P, eta, e->mu, wd, &e->st->flags, e->stream,
-                             &e->st->err));
-    else
-      DS_TRY(launch_sgd(p, p, e->grad, e->model.P, eta, wd, &e->st->flags, e->stream, &e->st->err));
-    policy_kernel<<<1, 1, 0, e->stream>>>(e->st, e->log);
-    e->launches += 2;
+    if (e->hostfed) {
+      DS_TRY(layered_step(e, X, y, e->iota, R, false));
+    } else if (R == B && e->step_graph) {
+      DS_CUDA_TRY(cudaGraphLaunch(e->step_graph, e->stream));
+    } else {
+      DS_TRY(layered_step(e, X, y, nullptr, R, true));
+      if (R == B && graphs_enabled()) {  // first full batch ran eagerly (warm-up); capture the next ones
+        cudaGraph_t g = nullptr;
+        DS_CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = layered_step(e, X, y, nullptr, R, true);
+        const cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
+        if (rc != DS_OK) return rc;
+        if (ce != cudaSuccess) return set_error(DS_E_CUDA, "engine: step capture: %s", cudaGetErrorString(ce));
+        const cudaError_t ie = cudaGraphInstantiate(&e->step_graph, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) return set_error(DS_E_CUDA, "engine: step graph: %s", cudaGetErrorString(ie));
+        for (int k = 0; k < 3; ++k) e->graph_key[k] = key[k];
+      }
+    }
+    e->launches += per_step + (e->hostfed ? 0 : 1);
     if (e->hp.adaptive) {
       if (xm) DS_TRY(enqueue_exchange(e, p));  // conditional on the device fire flag
     } else if (++e->host_since == e->hp.tau) {
@@ -514,6 +578,9 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->plan_rows);
   cudaFree(e->d_tickets);
   cudaFree(e->velocity);
+  if (e->step_graph) cudaGraphExecDestroy(e->step_graph);
+  cudaFree(e->cur_idx);
+  cudaFree(e->step_ctr);
   cudaFree(e->ring_X);
   cudaFree(e->ring_y);
   cudaFree(e->ring_words);
