@@ -340,7 +340,7 @@ def e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n):
     t = torch.tensor([secs], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return {"value": n * B * K / t.item(), "unit": "samples/s", "h2d_bytes_per_step": B * F * 4 + B * 4 + 8,
+    return {"value": n * B * K / t.item(), "unit": "samples/s", "h2d_bytes_per_step": B * F * 4 + B * 4 + 4,
             "d2h_bytes_per_step": 8, "steps": K, "losses_finite": ok,
             "path": "ds_engine_stream_*: host gather into pinned memory + H2D copy per step into a 4-slot device "
                     "ring, one persistent fused launch (step + exchange every tau), per-step loss written to "

@@ -910,13 +910,11 @@ extern "C" int ds_engine_stream_push(ds_engine* e, const float* X_host, const ui
         return set_error(DS_E_CUDA, "engine_stream_push: device stopped consuming");
     }
   }
-  e->ring_src[slot] = rows;
-  e->ring_src[K + slot] = static_cast<uint32_t>(s + 1);
+  // one word carries the row count and the step (mod 2^20; slots are reused 4 steps apart)
+  e->ring_src[K + slot] = (rows << 20) | (static_cast<uint32_t>(s + 1) & 0xFFFFFu);
   cudaStream_t cs = e->copy_stream;
   DS_CUDA_TRY(cudaMemcpyAsync(e->ring_X + slot * B * F, X_host, rows * F * sizeof(float), cudaMemcpyDefault, cs));
   DS_CUDA_TRY(cudaMemcpyAsync(e->ring_y + slot * B, y_host, rows * sizeof(uint32_t), cudaMemcpyDefault, cs));
-  DS_CUDA_TRY(cudaMemcpyAsync(e->ring_words + slot, e->ring_src + slot, sizeof(uint32_t), cudaMemcpyHostToDevice, cs));
-  // the sequence word last: the kernel sees it only after the rows (same stream, in order)
   DS_CUDA_TRY(cudaMemcpyAsync(e->ring_words + K + slot, e->ring_src + K + slot, sizeof(uint32_t),
                               cudaMemcpyHostToDevice, cs));
   ++e->ring_pushed;

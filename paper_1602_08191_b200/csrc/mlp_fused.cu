@@ -1166,15 +1166,15 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
   auto ring_wait = [&](uint64_t s) {
     if (tid == 0) {
       const uint32_t slot = static_cast<uint32_t>(s % A.ring_slots);
-      const uint32_t want = static_cast<uint32_t>(s + 1);
+      const uint32_t want = static_cast<uint32_t>(s + 1) & 0xFFFFFu;  // sequence word: rows << 20 | step+1
       unsigned long long t0;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
       uint32_t rows = 1;
       while (true) {
         uint32_t v;
         asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(A.ring_ready + slot) : "memory");
-        if (v == want) {
-          rows = *reinterpret_cast<volatile const uint32_t*>(A.ring_rows + slot);
+        if ((v & 0xFFFFFu) == want) {
+          rows = v >> 20;
           break;
         }
         unsigned long long t;
