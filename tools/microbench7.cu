@@ -110,15 +110,20 @@ __global__ void fwd(double* out, long long* cyc, int busy) {
   long long t0 = clock64();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   double z = 0.25, z1 = 0.5;
-  constexpr int CW = kMode == 3 ? 1 : 2;  // consumer warps
+  constexpr int CW = kMode == 3 ? 1 : (kMode == 5 ? 4 : 2);  // consumer warps
   if (warp < CW) {
     if (kMode == 1 || kMode == 2) {
       const int c = threadIdx.x, r = (c / 2) % 16, u = c % 2;
       z = kMode == 1 ? f1(w + u * NP, x + r * NP, z) : f2(w + u * NP, x + r * NP, z);
     } else if (kMode == 3) {  // 1 warp, 2 chains per lane
       f3(w, w + NP, x + (lane % 16) * NP, z, z1);
-    } else {  // kMode 4: 2 warps x 16 lanes, 2 chains per lane
+    } else if (kMode == 4) {  // 2 warps x 16 lanes, 2 chains per lane
       if (lane < 16) f3(w, w + NP, x + lane * NP, z, z1);
+    } else {  // kMode 5: 4 warps x 16 lanes, 1 chain per lane (one warp per SM sub-partition)
+      if (lane < 16) {
+        const int c = warp * 16 + lane, r = (c / 2) % 16, u = c % 2;
+        z = f1(w + u * NP, x + r * NP, z);
+      }
     }
     __syncwarp();
     if (lane == 0) atomicAdd((int*)&done, 1);
@@ -228,6 +233,7 @@ int main() {
     runf(fwd<2>, "F2 1 chain/thread, loads 2 ahead, 2 warps", busy);
     runf(fwd<3>, "F3 2 chains/thread (shared x), 1 warp", busy);
     runf(fwd<4>, "F4 2 chains/thread, 2 warps x 16 lanes", busy);
+    runf(fwd<5>, "F5 1 chain/thread, 4 warps x 16 lanes", busy);
   }
   const size_t lsm = (H * B + C * H2 + B * C) * 8;
   auto runl = [&](auto k, const char* name) {
