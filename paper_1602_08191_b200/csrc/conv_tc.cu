@@ -403,7 +403,17 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, uint32_t nsp
   if (t >= (K + 1) * cout) return;
   const uint32_t kp = t / cout, co = t % cout;
   float s = 0.0f;
-  for (uint32_t sp = 0; sp < nsplit; ++sp) s += part[(static_cast<uint64_t>(sp) * (K + 1) + kp) * cout + co];
+  const uint64_t stride = static_cast<uint64_t>(K + 1) * cout;
+  const float* src = part + static_cast<uint64_t>(kp) * cout + co;
+  uint32_t sp = 0;
+  for (; sp + 8 <= nsplit; sp += 8) {  // loads batched, adds in split order
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = src[(sp + j) * stride];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+  }
+  for (; sp < nsplit; ++sp) s += src[sp * stride];
   const float g = s * inv_b;
   if (!isfinite(g)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
   if (kp == K) {
@@ -477,6 +487,32 @@ template int launch_conv5_tc<64, 32, 8>(const float*, const float*, bool, float*
                                         uint32_t, bool, const uint32_t*, cudaStream_t);
 
 
+// many splits (conv1: one per sample): a warp per output, lanes over the splits, fixed tree
+__global__ void wgrad_reduce_warp_kernel(const float* __restrict__ part, uint32_t nsplit, uint32_t cin, uint32_t cout,
+                                         bool hwc, float* __restrict__ gW, float* __restrict__ gb, float inv_b,
+                                         uint32_t* flags, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t K = cin * 25, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= (K + 1) * cout) return;
+  const uint32_t kp = w / cout, co = w % cout;
+  const uint64_t stride = static_cast<uint64_t>(K + 1) * cout;
+  float s = 0.0f;
+  for (uint32_t sp = lane; sp < nsplit; sp += 32) s += part[sp * stride + static_cast<uint64_t>(kp) * cout + co];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane != 0) return;
+  const float g = s * inv_b;
+  if (!isfinite(g)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
+  if (kp == K) {
+    gb[co] = g;
+  } else if (hwc) {
+    const uint32_t khw = kp / cin, ci = kp - khw * cin;
+    gW[static_cast<uint64_t>(co) * K + ci * 25 + khw] = g;
+  } else {
+    gW[static_cast<uint64_t>(co) * K + kp] = g;
+  }
+}
+
 template <int CIN, int COUT, int H, int SPS>
 int launch_conv5_wgrad_tc(const float* in, const float* dout, float* part, float* gW, float* gb, uint32_t R,
                           float inv_b, uint32_t* flags, const uint32_t* gate, cudaStream_t s) {
@@ -490,7 +526,11 @@ int launch_conv5_wgrad_tc(const float* in, const float* dout, float* part, float
   const uint32_t nsplit = (R + SPS - 1) / SPS;
   k<<<dim3(S::MT, nsplit), kTile + 32, S::SMEM, s>>>(in, dout, part, R, gate);
   const uint32_t n = (S::K + 1) * COUT;
-  wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(part, nsplit, CIN, COUT, S::kHWC, gW, gb, inv_b, flags, gate);
+  if (nsplit >= 32)
+    wgrad_reduce_warp_kernel<<<(n * 32 + 255) / 256, 256, 0, s>>>(part, nsplit, CIN, COUT, S::kHWC, gW, gb, inv_b, flags,
+                                                                   gate);
+  else
+    wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(part, nsplit, CIN, COUT, S::kHWC, gW, gb, inv_b, flags, gate);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }

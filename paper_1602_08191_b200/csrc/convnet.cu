@@ -222,6 +222,67 @@ __global__ void maxpool_relu_bwd_kernel(const float* __restrict__ dout, const ui
   din[i] = s;
 }
 
+// Even H (H = 2*Ho): one thread per 2x2 input block (ph, pw). Its pixels lie in windows
+// (ph-1|ph) x (pw-1|pw) only, so the thread reads those <= 4 pooled values once and
+// accumulates each pixel's contributions in ascending (ph, pw) order — the same sums, in
+// the same order, as the per-pixel gathers above.
+__global__ void maxpool_relu_bwd2_kernel(const float* __restrict__ dout, const uint8_t* __restrict__ arg,
+                                         float* __restrict__ din, uint32_t NC, uint32_t Ho, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= NC * Ho * Ho) return;
+  const uint32_t pw = i % Ho, ph = (i / Ho) % Ho, nc = i / (Ho * Ho), H = 2 * Ho;
+  float s[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+  for (int dh = -1; dh <= 0; ++dh)
+#pragma unroll
+    for (int dw = -1; dw <= 0; ++dw) {
+      const int wh = static_cast<int>(ph) + dh, ww = static_cast<int>(pw) + dw;
+      if (wh < 0 || ww < 0) continue;
+      const size_t o = (static_cast<size_t>(nc) * Ho + wh) * Ho + ww;
+      const uint32_t a = arg[o];
+      if (!(a & 0x10u)) continue;
+      const int hh = 2 * wh + static_cast<int>((a & 0xfu) / 3) - 2 * static_cast<int>(ph);
+      const int wc = 2 * ww + static_cast<int>((a & 0xfu) % 3) - 2 * static_cast<int>(pw);
+      if (hh >= 0 && hh < 2 && wc >= 0 && wc < 2) s[hh][wc] += dout[o];
+    }
+  float* d = din + (static_cast<size_t>(nc) * H + 2 * ph) * H + 2 * pw;
+  *reinterpret_cast<float2*>(d) = make_float2(s[0][0], s[0][1]);
+  *reinterpret_cast<float2*>(d + H) = make_float2(s[1][0], s[1][1]);
+}
+
+__global__ void avepool_bwd2_kernel(const float* __restrict__ dout, const float* __restrict__ act,
+                                    float* __restrict__ din, uint32_t NC, uint32_t Ho, const uint32_t* gate) {
+  if (gate && *gate) return;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= NC * Ho * Ho) return;
+  const uint32_t pw = i % Ho, ph = (i / Ho) % Ho, nc = i / (Ho * Ho), H = 2 * Ho;
+  float s[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+  for (int dh = -1; dh <= 0; ++dh)
+#pragma unroll
+    for (int dw = -1; dw <= 0; ++dw) {
+      const int wh = static_cast<int>(ph) + dh, ww = static_cast<int>(pw) + dw;
+      if (wh < 0 || ww < 0) continue;
+      const uint32_t hs = 2 * wh, ws = 2 * ww, he = min(hs + 3, H), we = min(ws + 3, H);
+      const float v = dout[(static_cast<size_t>(nc) * Ho + wh) * Ho + ww] / static_cast<float>((he - hs) * (we - ws));
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+          if (dh == 0 || a == 0)      // window ph-1 reaches only row 2ph
+            if (dw == 0 || b == 0) s[a][b] += v;
+    }
+  const size_t base = (static_cast<size_t>(nc) * H + 2 * ph) * H + 2 * pw;
+  float o[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) o[a][b] = (act && !(act[base + a * H + b] > 0.0f)) ? 0.0f : s[a][b];
+  *reinterpret_cast<float2*>(din + base) = make_float2(o[0][0], o[0][1]);
+  *reinterpret_cast<float2*>(din + base + H) = make_float2(o[1][0], o[1][1]);
+}
+
 // ---- fully connected ---------------------------------------------------------------
 // out[r][o] = b[o] + sum_i W[o][i] a[r][i]; CTA per row, KS-way split over i, fixed-order
 // combine of the KS partials.
@@ -603,7 +664,7 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
                                                     inv_b, flags, gate);
   fc_bwd_a_kernel<<<blocks(R * 1024), 256, 0, s>>>(w.dh1, P + L[3].w_off, w.dp3, R, 1024, 64, gate);
   // pool3 -> relu3 -> conv3
-  avepool_bwd_kernel<<<blocks(R * 64 * 64), 256, 0, s>>>(w.dp3, w.c3, w.dc3, R * 64, 8, gate);
+  avepool_bwd2_kernel<<<blocks(R * 64 * 16), 256, 0, s>>>(w.dp3, w.c3, w.dc3, R * 64, 4, gate);
   DS_CUDA_TRY(cudaGetLastError());
   if (use_tensor_cores()) {
     DS_TRY((launch_conv5_wgrad_tc<32, 64, 8, 8>(w.p2, w.dc3, w.part, grad + L[2].w_off, grad + L[2].b_off, R, inv_b,
@@ -621,7 +682,7 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   else
     DS_TRY((launch_conv5<64, 32, 8, 16, 1, 4>(w.dc3, w.wt3, nullptr, w.dp2, R, false, gate, s)));
   // pool2 -> relu2 -> conv2
-  avepool_bwd_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.dp2, w.c2, w.dc2, R * 32, 16, gate);
+  avepool_bwd2_kernel<<<blocks(R * 32 * 64), 256, 0, s>>>(w.dp2, w.c2, w.dc2, R * 32, 8, gate);
   DS_CUDA_TRY(cudaGetLastError());
   if (use_tensor_cores()) {
     DS_TRY((launch_conv5_wgrad_tc<32, 32, 16, 4>(w.p1, w.dc2, w.part, grad + L[1].w_off, grad + L[1].b_off, R, inv_b,
@@ -639,7 +700,7 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   else
     DS_TRY((launch_conv5<32, 32, 16, 16, 2, 2>(w.dc2, w.wt2, nullptr, w.dr1, R, false, gate, s)));
   // relu1 -> pool1 (max) -> conv1 (weights only), one sample per partial
-  maxpool_relu_bwd_kernel<<<blocks(R * 32 * 1024), 256, 0, s>>>(w.dr1, w.arg1, w.dc1, R * 32, 32, gate);
+  maxpool_relu_bwd2_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.dr1, w.arg1, w.dc1, R * 32, 16, gate);
   DS_CUDA_TRY(cudaGetLastError());
   if (use_tensor_cores()) {
     DS_TRY((launch_conv5_wgrad_tc<3, 32, 32, 1>(idx ? w.x0 : X, w.dc1, w.part, grad + L[0].w_off, grad + L[0].b_off, R,
