@@ -259,6 +259,10 @@ int ds_engine_reserve(ds_engine* e, uint64_t steps);
 /* Momentum option (ds_sgd_momentum_update; layered engine only — the fused step keeps
  * mu = 0): every following iteration uses the momentum update with this mu. */
 int ds_engine_set_momentum(ds_engine* e, float mu);
+/* Synchronous data-parallel mode (layered engine, no EASGD master): every iteration
+ * writes its gradient into the group's slot and applies ds_sync_reduce_update — the
+ * simulate_sync round (simulator.cpp:156-223) across the group's GPUs. NULL detaches. */
+int ds_engine_attach_sync(ds_engine* e, ds_sync* s);
 /* Host-fed iteration (a data pipeline that owns the rows, like the reference worker's
  * ShardSweeper + gather_batch, engine.cpp:25-33 / model.cpp:12-21): copies `rows`
  * gathered rows (X_host row-major, y_host) from host memory — pinned for full speed —

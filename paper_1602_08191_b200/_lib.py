@@ -102,6 +102,7 @@ _sig("ds_sgd_step_checked", VP, VP, VP, U64, C.c_double, VP)
 _sig("ds_grad_accumulate", VP, VP, U64, VP)
 _sig("ds_sgd_momentum_update", VP, VP, VP, VP, U64, C.c_float, C.c_float, C.c_float, VP, VP)
 _sig("ds_engine_set_momentum", VP, C.c_float)
+_sig("ds_engine_attach_sync", VP, VP)
 _sig("ds_grad_average", VP, VP, U64, U32, C.c_float, VP, VP)
 _sig("ds_device_alloc", C.c_int, U64, C.POINTER(VP))
 _sig("ds_device_free", VP)
@@ -159,7 +160,7 @@ _sig("ds_gather_rows", VP, VP, VP, VP, VP, U32, U32, VP)
 
 EXPORTED = [
     "ds_last_error", "ds_version", "ds_device_count", "ds_elastic_update", "ds_elastic_exchange",
-    "ds_sgd_update", "ds_sgd_step_checked", "ds_sgd_momentum_update", "ds_engine_set_momentum", "ds_grad_accumulate", "ds_grad_average", "ds_device_alloc",
+    "ds_sgd_update", "ds_sgd_step_checked", "ds_sgd_momentum_update", "ds_engine_set_momentum", "ds_engine_attach_sync", "ds_grad_accumulate", "ds_grad_average", "ds_device_alloc",
     "ds_device_free", "ds_memcpy", "ds_memset", "ds_stream_create", "ds_stream_destroy", "ds_stream_sync",
     "ds_param_dim", "ds_loss_and_grad_workspace",
     "ds_loss_and_grad", "ds_predict", "ds_count_hits", "ds_master_create", "ds_master_create_sharded",

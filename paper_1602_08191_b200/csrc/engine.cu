@@ -133,6 +133,7 @@ struct ds_engine {
   cudaGraphExec_t step_graph = nullptr;
   const void* graph_key[3] = {};
   uint32_t* cur_idx = nullptr;             // [B] the step's shard rows (set_idx_kernel)
+  ds_sync* sync = nullptr;                 // synchronous data-parallel mode (ds_engine_attach_sync)
   unsigned long long* step_ctr = nullptr;  // device step counter within a run
   uint32_t hostfed_rows = 0;
   bool hostfed = false;
@@ -262,6 +263,16 @@ int layered_step(ds_engine* e, const float* X, const uint32_t* y, const uint32_t
                                                                                      e->step_ctr, e->cur_idx);
     idx = e->cur_idx;
   }
+  if (e->sync) {  // simulate_sync (simulator.cpp:156-223) across the group's GPUs
+    float* slot = nullptr;
+    DS_TRY(ds_sync_begin(e->sync, &slot, e->stream));
+    DS_TRY(launch_loss_and_grad(e->model, p, X, idx, y, R, slot, &e->st->loss, e->ws, &e->st->flags, &e->st->err,
+                                e->stream));
+    DS_TRY(ds_sync_reduce_update(e->sync, p, eta, wd, &e->st->flags, e->stream));
+    policy_kernel<<<1, 1, 0, e->stream>>>(e->st, e->log);
+    DS_CUDA_TRY(cudaGetLastError());
+    return DS_OK;
+  }
   DS_TRY(launch_loss_and_grad(e->model, p, X, idx, y, R, e->grad, &e->st->loss, e->ws, &e->st->flags, &e->st->err,
                               e->stream));
   if (e->mu > 0.0f)
@@ -304,11 +315,11 @@ int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
     const uint32_t R = e->hostfed ? e->hostfed_rows : e->h_rows[j];
     if (e->hostfed) {
       DS_TRY(layered_step(e, X, y, e->iota, R, false));
-    } else if (R == B && e->step_graph) {
+    } else if (R == B && e->step_graph && !e->sync) {
       DS_CUDA_TRY(cudaGraphLaunch(e->step_graph, e->stream));
     } else {
       DS_TRY(layered_step(e, X, y, nullptr, R, true));
-      if (R == B && graphs_enabled()) {  // first full batch ran eagerly (warm-up); capture the next ones
+      if (R == B && graphs_enabled() && !e->sync) {  // first full batch ran eagerly; capture the next ones
         cudaGraph_t g = nullptr;
         DS_CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
         const int rc = layered_step(e, X, y, nullptr, R, true);
@@ -614,6 +625,7 @@ extern "C" int ds_engine_attach_master(ds_engine* e, ds_master* m) {
     if (dim != e->model.P) return set_error(DS_E_CONTRACT, "engine: master dim %llu != model dim %llu",
                                             (unsigned long long)dim, (unsigned long long)e->model.P);
     if (m->device != e->device) return set_error(DS_E_CONTRACT, "engine: master lives on another device");
+    if (e->sync) return set_error(DS_E_CONTRACT, "engine: synchronous mode replaces the EASGD master");
   }
   e->master = m;
   return DS_OK;
@@ -850,6 +862,15 @@ extern "C" int ds_engine_step_host_async(ds_engine* e, const float* X_host, cons
 }
 
 // ---- stream mode --------------------------------------------------------------------
+extern "C" int ds_engine_attach_sync(ds_engine* e, ds_sync* sg) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine: null");
+  if (sg && e->fused) return set_error(DS_E_CONTRACT, "engine: synchronous mode needs the layered engine");
+  if (sg && e->master) return set_error(DS_E_CONTRACT, "engine: synchronous mode replaces the EASGD master");
+  if (sg && e->mu > 0.0f) return set_error(DS_E_CONTRACT, "engine: synchronous mode has no momentum");
+  e->sync = sg;
+  return DS_OK;
+}
+
 extern "C" int ds_engine_set_momentum(ds_engine* e, float mu) {
   if (!e) return set_error(DS_E_CONTRACT, "engine: null");
   if (!(mu >= 0.0f && mu < 1.0f)) return set_error(DS_E_CONTRACT, "sgd_momentum: mu must be in [0,1)");

@@ -21,6 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--wd", type=float, default=0.0)
+    ap.add_argument("--engine", action="store_true", help="through ds_engine_attach_sync (device sweeper)")
     args = ap.parse_args()
 
     import torch
@@ -56,8 +57,27 @@ def main():
     hidden = (C.c_uint32 * 1)(*m.hidden)
     desc = L.ds_model_desc(1, m.n_features, m.n_classes, len(m.hidden), hidden)
     dist.barrier()
-    losses = D.run_sync_worker(L, api, desc, Xk, yk, m.n_classes, hp, D.sweep_seed(api, data_seed, rank), params,
-                               sg, local)
+    if args.engine:  # the engine's own ShardSweeper + layered kernels, sync group attached
+        h = L.ds_hyper(hp.eta, hp.alpha, hp.tau, hp.batch_size, hp.i_max, 0.0, hp.weight_decay, 0)
+        eng = C.c_void_p()
+        init_host = params.cpu().numpy()
+        yk32 = np.ascontiguousarray(yk, dtype=np.uint32)  # kept alive across the create call
+        Xk32 = np.ascontiguousarray(Xk, dtype=np.float32)
+        L.check(L.lib.ds_engine_create(C.byref(eng), local, C.byref(desc), Xk32.ctypes.data,
+                                       yk32.ctypes.data, len(yk), m.n_classes, C.byref(h),
+                                       D.sweep_seed(api, data_seed, rank), init_host.ctypes.data, L.DS_ENGINE_LAYERED))
+        L.check(L.lib.ds_engine_attach_sync(eng, sg))
+        L.check(L.lib.ds_engine_run(eng, hp.i_max, 0, None))
+        L.check(L.lib.ds_engine_sync(eng))
+        losses = np.zeros(hp.i_max)
+        L.check(L.lib.ds_engine_log(eng, 0, hp.i_max, losses.ctypes.data, None, None, None))
+        out = np.zeros(P, np.float32)
+        L.check(L.lib.ds_engine_get_params(eng, out.ctypes.data))
+        params.copy_(torch.from_numpy(out))
+        L.lib.ds_engine_destroy(eng)
+    else:
+        losses = D.run_sync_worker(L, api, desc, Xk, yk, m.n_classes, hp, D.sweep_seed(api, data_seed, rank), params,
+                                   sg, local)
     final = params.cpu().numpy()
     finals = D.gather_bytes(final.tobytes(), world)
     all_losses = D.gather_bytes(losses.tobytes(), world)

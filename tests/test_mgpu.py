@@ -79,3 +79,15 @@ def test_sync_config1_two_gpus():
     # Stated tolerance: <= 8 ulp per element, >= 99.99% of elements bit-identical.
     assert r["replicas_identical"] and r["loss_close"]
     assert r["master_max_ulp"] <= 8 and r["master_bit_identical"] >= 0.9999
+
+
+@pytest.mark.skipif(ngpus() < 1, reason="needs a GPU")
+def test_sync_engine_single_rank():
+    r = run(1, "--engine", script="mgpu_sync.py")
+    assert r["master_equal"] and r["loss_close"] and r["replicas_identical"]
+
+
+@pytest.mark.skipif(ngpus() < 2, reason="needs >= 2 GPUs")
+def test_sync_engine_multi_gpu():
+    r = run(min(ngpus(), 4), "--engine", script="mgpu_sync.py")
+    assert r["replicas_identical"] and r["master_equal"] and r["loss_close"]
