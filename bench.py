@@ -296,6 +296,8 @@ def main():
         line["exchange"] = exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind)
         if args.cifar_steps > 0:
             line["cifar10_quick"] = cifar_leg(args, L, api, torch, dist, world, rank, local)
+            line["cifar10_quick_config3"] = {k: cifar_leg(args, L, api, torch, dist, world, rank, local, k)
+                                             for k in ("sync", "adaptive")}
         if rank == 0 and world == 1:
             line["cpu_baseline"] = cpu_baseline(args, X, y)
     L.lib.ds_engine_destroy(eng)
@@ -409,11 +411,16 @@ def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind):
     return out
 
 
-def cifar_leg(args, L, api, torch, dist, world, rank, local):
-    """BASELINE config 2 shape: Caffe cifar10_quick on synthetic 3x32x32 CIFAR-10-shaped
-    data, async EASGD tau=10, batch 100 per worker, one worker per GPU, center sharded
-    over the GPUs (LockFree). NOT IN THE REFERENCE (no conv layers): f32 layered kernels
-    (csrc/convnet.cu), no CPU reference arm. Device-timed, max over ranks."""
+def cifar_leg(args, L, api, torch, dist, world, rank, local, mode="async"):
+    """BASELINE config 2 shape (mode "async"): Caffe cifar10_quick on synthetic 3x32x32
+    CIFAR-10-shaped data, async EASGD tau=10, batch 100 per worker, one worker per GPU,
+    center sharded over the GPUs (LockFree). Config 3 adds mode "adaptive" (async, the
+    Adaptive policy with resolve_loss_cut's cut = 20 x the first batch's loss,
+    worker.cpp:18-30) and mode "sync" (simulate_sync semantics, simulator.cpp:156-223:
+    every iteration the gradients of all GPUs are summed over NVLink and applied to the
+    replicated center, ds_engine_attach_sync). NOT IN THE REFERENCE (no conv layers): tf32
+    tensor-core layered kernels (csrc/conv_tc.cu, csrc/convnet.cu), no CPU reference arm.
+    Device-timed, max over ranks."""
     from paper_1602_08191_b200 import dist as D
     B, K, N = 100, args.cifar_steps, 10000
     Xc, yc = api.gen_synthetic(N, 3072, 10, 1.0, 1.0, 101 + rank)
@@ -425,19 +432,38 @@ def cifar_leg(args, L, api, torch, dist, world, rank, local):
     if world > 1:
         dist.broadcast(init, 0)
     torch.cuda.synchronize()
-    if world == 1:
+    hidden = (C.c_uint32 * 1)(0)
+    desc = L.ds_model_desc(2, 3072, 10, 0, hidden)
+    sweep = api.mix_seed(5, rank)
+
+    def make(hp):
+        e = C.c_void_p()
+        L.check(L.lib.ds_engine_create(C.byref(e), local, C.byref(desc), Xc.ctypes.data, yc.ctypes.data, len(yc),
+                                       10, C.byref(hp), sweep, C.c_void_p(init.data_ptr()), L.DS_ENGINE_AUTO))
+        return e
+
+    cut = 0.0
+    if mode == "adaptive":  # resolve_loss_cut: 20 x loss_only(first batch of a fresh sweeper, initial params)
+        probe = make(L.ds_hyper(0.01, 0.1, 10, B, 10 ** 9, 0.0, 0.0, 0))
+        L.check(L.lib.ds_engine_run(probe, 1, 0, None))
+        L.check(L.lib.ds_engine_sync(probe))
+        first = np.zeros(1)
+        L.check(L.lib.ds_engine_log(probe, 0, 1, first.ctypes.data, None, None, None))
+        L.lib.ds_engine_destroy(probe)
+        cut = 20.0 * float(first[0])
+    eng = make(L.ds_hyper(0.01, 0.1, 10, B, 10 ** 9, cut, 0.0, 1 if mode == "adaptive" else 0))
+    m = sg = None
+    if mode == "sync":
+        sg = D.sync_group(L, local, Pc, rank, world)
+        L.check(L.lib.ds_engine_attach_sync(eng, sg))
+    elif world == 1:
         m = C.c_void_p()
         L.check(L.lib.ds_master_create(C.byref(m), local, Pc, C.c_float(0.1), L.DS_MODE_LOCKFREE,
                                        C.c_void_p(init.data_ptr())))
     else:
         m = D.sharded_master(L, local, Pc, 0.1, L.DS_MODE_LOCKFREE, init.data_ptr(), rank, world)
-    hidden = (C.c_uint32 * 1)(0)
-    desc = L.ds_model_desc(2, 3072, 10, 0, hidden)
-    hp = L.ds_hyper(0.01, 0.1, 10, B, 10 ** 9, 0.0, 0.0, 0)
-    eng = C.c_void_p()
-    L.check(L.lib.ds_engine_create(C.byref(eng), local, C.byref(desc), Xc.ctypes.data, yc.ctypes.data, len(yc), 10,
-                                   C.byref(hp), api.mix_seed(5, rank), C.c_void_p(init.data_ptr()), L.DS_ENGINE_AUTO))
-    L.check(L.lib.ds_engine_attach_master(eng, m))
+    if m is not None:
+        L.check(L.lib.ds_engine_attach_master(eng, m))
     L.check(L.lib.ds_engine_reserve(eng, K + 5))
     L.check(L.lib.ds_engine_run(eng, 5, 0, None))
     L.check(L.lib.ds_engine_sync(eng))
@@ -462,21 +488,33 @@ def cifar_leg(args, L, api, torch, dist, world, rank, local):
     L.check(L.lib.ds_engine_launches(eng, C.byref(n1)))
     loss = np.zeros(K + 5)
     L.check(L.lib.ds_engine_log(eng, 0, K + 5, loss.ctypes.data, None, None, None))
+    exch = np.zeros(K + 5, np.uint8)
+    L.check(L.lib.ds_engine_log(eng, 0, K + 5, None, None, exch.ctypes.data, None))
     L.lib.ds_engine_destroy(eng)
     if world > 1:
         dist.barrier()
-    L.lib.ds_master_destroy(m)
+    if m is not None:
+        L.lib.ds_master_destroy(m)
+    if sg is not None:
+        L.lib.ds_sync_destroy(sg)
     ms = t.item()
     flop = 3 * 2 * 12_350_000 * B * K  # ~3x forward (fwd + dgrad + wgrad), 2 FLOP/MAC
-    return {"metric": "train samples/s (cifar10_quick, BASELINE config 2 shape)", "value": world * B * K / (ms / 1e3),
-            "unit": "samples/s", "ms_per_step": ms / K, "steps": K, "batch_per_worker": B, "tau": 10, "alpha": 0.1,
-            "eta": 0.01, "workers": world, "exchange": "LockFree, center sharded over the GPUs" if world > 1 else
-            "LockFree, center on the same GPU", "dtype": "tf32 tensor cores (tcgen05 implicit-GEMM convolutions, f32 "
-            "accumulation in TMEM), f32 elsewhere", "data": "synthetic gen_synthetic "
-            "3072 features (3x32x32 CHW), 10 classes, 10,000 rows per GPU",
-            "achieved_tflops": flop / (ms / 1e3) / 1e12, "gpu_launches": int(n1.value - n0.value),
-            "loss_first_last": [float(loss[0]), float(loss[-1])],
-            "reference_arm": "none: the reference has no conv layers (SURVEY §8 a20)"}
+    out = {"metric": "train samples/s (cifar10_quick, BASELINE config %d shape)" % (2 if mode == "async" else 3),
+           "value": world * B * K / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms / K, "steps": K,
+           "batch_per_worker": B, "eta": 0.01, "workers": world, "mode": mode,
+           "dtype": "tf32 tensor cores (tcgen05 implicit-GEMM convolutions, f32 accumulation in TMEM), f32 elsewhere",
+           "data": "synthetic gen_synthetic 3072 features (3x32x32 CHW), 10 classes, 10,000 rows per GPU",
+           "achieved_tflops": flop / (ms / 1e3) / 1e12, "gpu_launches": int(n1.value - n0.value),
+           "loss_first_last": [float(loss[0]), float(loss[-1])],
+           "reference_arm": "none: the reference has no conv layers (SURVEY §8 a20)"}
+    if mode == "sync":
+        out["exchange"] = "synchronous: f64 worker-ordered gradient sum over NVLink peers + SGD on every replica"
+    else:
+        out.update(tau=10, alpha=0.1, exchange="LockFree, center sharded over the GPUs" if world > 1 else
+                   "LockFree, center on the same GPU", exchanges_in_timed_steps=int(exch[5:].astype(bool).sum()))
+        if mode == "adaptive":
+            out["loss_cut"] = cut
+    return out
 
 
 def cpu_baseline(args, X, y):

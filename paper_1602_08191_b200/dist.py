@@ -31,6 +31,8 @@ def worker_tickets(order_workers: np.ndarray, rank: int) -> np.ndarray:
 
 
 def gather_bytes(blob: bytes, world: int, group=None):
+    if world == 1:  # a one-GPU group needs no process group
+        return [blob]
     import torch.distributed as dist
     out = [None] * world
     dist.all_gather_object(out, blob, group=group)
