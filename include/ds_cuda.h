@@ -32,7 +32,9 @@ typedef enum {
   DS_E_NUMERIC = 2,  /* deepspark::NumericError   (errors.hpp:16-19)  */
   DS_E_CUDA = 3,     /* CUDA runtime / driver failure, or no device      */
   DS_E_NOMEM = 4,    /* device allocation failed                         */
-  DS_E_STATE = 5     /* handle used in a state that does not allow it    */
+  DS_E_STATE = 5,    /* handle used in a state that does not allow it    */
+  DS_E_FORMAT = 6,   /* deepspark::FormatError    (errors.hpp:33-36)  */
+  DS_E_IO = 7        /* deepspark::IoError        (errors.hpp:56-59)  */
 } ds_status;
 
 const char* ds_last_error(void);
@@ -121,6 +123,26 @@ int ds_gather_rows(float* dst, uint32_t* y_dst, const float* X, const uint32_t* 
 
 /* ---------------------------------------------------------------------------------- */
 /* Device plumbing for hosts that do not link the CUDA runtime (C++/Go/Java/Python)   */
+/* ---------------------------------------------------------------------------------- */
+/* DSHD shards (shard.hpp:9-35, shard.cpp:75-125)                                     */
+/* ---------------------------------------------------------------------------------- */
+typedef struct ds_shard_info {
+  uint32_t n_samples;
+  uint32_t n_features;
+  uint32_t n_classes;
+  uint64_t seed; /* provenance seed (ShardData::seed) */
+} ds_shard_info;
+/* Header of a DSHD file, validated like read_shard (magic, version, dimensions, size
+ * arithmetic against the file length): DS_E_FORMAT / DS_E_IO with the reference's messages. */
+int ds_shard_info_read(const char* path, ds_shard_info* info);
+/* read_shard straight into device memory on the calling thread's current device: X_dev
+ * f32 [n x F] row-major, y_dev u32 [n] (capacity_rows >= n). The body streams through
+ * pinned double buffers and async copies and is unpacked and label-checked on the GPU;
+ * returns after the data is resident. A label >= n_classes is DS_E_FORMAT ("label L out
+ * of range at sample i"). */
+int ds_shard_load(const char* path, float* X_dev, uint32_t* y_dev, uint64_t capacity_rows, ds_shard_info* info_out,
+                  void* stream);
+
 /* ---------------------------------------------------------------------------------- */
 int ds_device_alloc(int device, uint64_t bytes, void** out);
 int ds_device_free(void* p);
@@ -237,6 +259,10 @@ typedef struct {
 int ds_engine_create(ds_engine** out, int device, const ds_model_desc* model, const float* X_host,
                      const uint32_t* y_host, uint64_t shard_n, uint32_t shard_classes,
                      const ds_hyper* hp, uint64_t sweep_seed, const float* init_host, int kind);
+/* SgdEngine over a DSHD shard file (shard.hpp:9-35), ingested straight into the engine's
+ * resident X/y (ds_shard_load): shard_n and shard_classes come from the file header. */
+int ds_engine_create_from_shard(ds_engine** out, int device, const ds_model_desc* model, const char* path,
+                                const ds_hyper* hp, uint64_t sweep_seed, const float* init_host, int kind);
 int ds_engine_destroy(ds_engine* e);
 /* Attach a master: the policy's exchanges run on-device against it (async/LockFree or
  * Locked as the master was created; deterministic when tickets are given). */

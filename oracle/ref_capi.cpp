@@ -19,6 +19,7 @@
 #include "deepspark/model.hpp"
 #include "deepspark/param_vector.hpp"
 #include "deepspark/rng.hpp"
+#include "deepspark/shard.hpp"
 #include "deepspark/simulator.hpp"
 #include "deepspark/worker.hpp"
 
@@ -190,6 +191,19 @@ int dsref_gen_synthetic(uint32_t n, uint32_t f, uint32_t c, double sep, double s
     const Dataset ds = gen_synthetic(s);
     std::memcpy(X, ds.features.data(), ds.features.size() * sizeof(float));
     std::memcpy(y, ds.labels.data(), ds.labels.size() * sizeof(uint32_t));
+  });
+}
+
+// write_shard (shard.cpp:40-73): golden DSHD files for the device ingestion tests
+int dsref_write_shard(const char* path, const float* X, const uint32_t* y, uint64_t n, uint32_t f, uint32_t c,
+                      uint64_t seed) {
+  return guarded([&] {
+    Dataset ds;
+    ds.n_features = f;
+    ds.n_classes = c;
+    ds.features.assign(X, X + n * f);
+    ds.labels.assign(y, y + n);
+    write_shard(ds, path, seed);
   });
 }
 

@@ -20,7 +20,7 @@ if not os.path.exists(LIB_PATH):
 
 lib = C.CDLL(LIB_PATH)
 
-DS_OK, DS_E_CONTRACT, DS_E_NUMERIC, DS_E_CUDA, DS_E_NOMEM, DS_E_STATE = range(6)
+DS_OK, DS_E_CONTRACT, DS_E_NUMERIC, DS_E_CUDA, DS_E_NOMEM, DS_E_STATE, DS_E_FORMAT, DS_E_IO = range(8)
 DS_MODE_LOCKED, DS_MODE_LOCKFREE = 0, 1
 DS_ENGINE_AUTO, DS_ENGINE_LAYERED, DS_ENGINE_FUSED = 0, 1, 2
 DS_IPC_RECORD_BYTES = 256
@@ -55,8 +55,18 @@ class StateError(DsError):
     code = DS_E_STATE
 
 
+class FormatError(DsError):
+    """deepspark::FormatError (errors.hpp:33-36): a malformed DSHD shard."""
+    code = DS_E_FORMAT
+
+
+class IoError(DsError):
+    """deepspark::IoError (errors.hpp:56-59)."""
+    code = DS_E_IO
+
+
 _ERRS = {DS_E_CONTRACT: ContractError, DS_E_NUMERIC: NumericError, DS_E_CUDA: CudaError,
-         DS_E_NOMEM: CudaError, DS_E_STATE: StateError}
+         DS_E_NOMEM: CudaError, DS_E_STATE: StateError, DS_E_FORMAT: FormatError, DS_E_IO: IoError}
 
 
 def check(rc: int) -> None:
@@ -68,6 +78,11 @@ def check(rc: int) -> None:
 class ds_model_desc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n_features", C.c_uint32), ("n_classes", C.c_uint32),
                 ("n_hidden", C.c_uint32), ("hidden", C.POINTER(C.c_uint32))]
+
+
+class ds_shard_info(C.Structure):
+    _fields_ = [("n_samples", C.c_uint32), ("n_features", C.c_uint32), ("n_classes", C.c_uint32),
+                ("seed", C.c_uint64)]
 
 
 class ds_hyper(C.Structure):
@@ -157,8 +172,13 @@ _sig("ds_sync_reduce_update", VP, VP, C.c_float, C.c_float, VP, VP)
 _sig("ds_sync_rounds", VP, P_U64)
 _sig("ds_sync_destroy", VP)
 _sig("ds_gather_rows", VP, VP, VP, VP, VP, U32, U32, VP)
+_sig("ds_shard_info_read", C.c_char_p, C.POINTER(ds_shard_info))
+_sig("ds_shard_load", C.c_char_p, VP, VP, U64, C.POINTER(ds_shard_info), VP)
+_sig("ds_engine_create_from_shard", C.POINTER(VP), C.c_int, C.POINTER(ds_model_desc), C.c_char_p,
+     C.POINTER(ds_hyper), U64, VP, C.c_int)
 
 EXPORTED = [
+    "ds_shard_info_read", "ds_shard_load", "ds_engine_create_from_shard",
     "ds_last_error", "ds_version", "ds_device_count", "ds_elastic_update", "ds_elastic_exchange",
     "ds_sgd_update", "ds_sgd_step_checked", "ds_sgd_momentum_update", "ds_engine_set_momentum", "ds_engine_attach_sync", "ds_grad_accumulate", "ds_grad_average", "ds_device_alloc",
     "ds_device_free", "ds_memcpy", "ds_memset", "ds_stream_create", "ds_stream_destroy", "ds_stream_sync",

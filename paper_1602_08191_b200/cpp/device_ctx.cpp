@@ -11,6 +11,8 @@ void throw_status(int status, const char* context) {
   switch (status) {
     case DS_E_CONTRACT: throw ContractError(ds_last_error());
     case DS_E_NUMERIC: throw NumericError(ds_last_error());
+    case DS_E_FORMAT: throw FormatError(ds_last_error());
+    case DS_E_IO: throw IoError(ds_last_error());
     default: throw CudaError(msg);
   }
 }

@@ -467,10 +467,13 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
 
 using dsb::set_error;
 
-extern "C" int ds_engine_create(ds_engine** out, int device, const ds_model_desc* model, const float* X_host,
-                                const uint32_t* y_host, uint64_t shard_n, uint32_t shard_classes, const ds_hyper* hp,
-                                uint64_t sweep_seed, const float* init_host, int kind) {
-  if (!out || !hp || !X_host || !y_host || !init_host) return set_error(DS_E_CONTRACT, "engine: null argument");
+// ds_engine_create / ds_engine_create_from_shard: the shard comes from host arrays, or
+// (shard_path != nullptr) from a DSHD file streamed straight into e->X / e->y.
+static int engine_create(ds_engine** out, int device, const ds_model_desc* model, const float* X_host,
+                         const uint32_t* y_host, uint64_t shard_n, uint32_t shard_classes, const ds_hyper* hp,
+                         uint64_t sweep_seed, const float* init_host, int kind, const char* shard_path) {
+  if (!out || !hp || (!shard_path && (!X_host || !y_host)) || !init_host)
+    return set_error(DS_E_CONTRACT, "engine: null argument");
   dsb::ModelInfo m;
   DS_TRY(dsb::model_from_desc(model, m));
   // Hyperparams::validate (hyperparams.cpp:7-18)
@@ -486,8 +489,9 @@ extern "C" int ds_engine_create(ds_engine** out, int device, const ds_model_desc
   if (shard_n > 0xFFFFFFFFull) return set_error(DS_E_CONTRACT, "engine: shard too large for u32 row indices");
   if (shard_classes == 0) return set_error(DS_E_CONTRACT, "dataset: n_classes must be positive");
   if (shard_classes > m.n_classes) return set_error(DS_E_CONTRACT, "engine: shard dims do not match model");
-  for (uint64_t i = 0; i < shard_n; ++i)
-    if (y_host[i] >= shard_classes) return set_error(DS_E_CONTRACT, "dataset: label out of range");
+  if (!shard_path)  // a shard file's labels are range-checked on the device as they land
+    for (uint64_t i = 0; i < shard_n; ++i)
+      if (y_host[i] >= shard_classes) return set_error(DS_E_CONTRACT, "dataset: label out of range");
   for (uint64_t i = 0; i < m.P; ++i)
     if (!std::isfinite(init_host[i])) {
       // sgd_step's require_finite(x) would reject the first step (param_vector.cpp:29)
@@ -536,13 +540,20 @@ extern "C" int ds_engine_create(ds_engine** out, int device, const ds_model_desc
     std::iota(id.begin(), id.end(), 0u);
     err = cudaMemcpy(e->iota, id.data(), B * sizeof(uint32_t), cudaMemcpyHostToDevice);
   }
-  if (err == cudaSuccess) err = cudaMemcpy(e->X, X_host, shard_n * F * sizeof(float), cudaMemcpyDefault);
-  if (err == cudaSuccess) err = cudaMemcpy(e->y, y_host, shard_n * sizeof(uint32_t), cudaMemcpyDefault);
+  if (err == cudaSuccess && !shard_path) err = cudaMemcpy(e->X, X_host, shard_n * F * sizeof(float), cudaMemcpyDefault);
+  if (err == cudaSuccess && !shard_path) err = cudaMemcpy(e->y, y_host, shard_n * sizeof(uint32_t), cudaMemcpyDefault);
   if (err == cudaSuccess) err = cudaMemcpy(e->params[0], init_host, m.P * sizeof(float), cudaMemcpyDefault);
   if (err == cudaSuccess) err = cudaMemcpy(e->params[1], init_host, m.P * sizeof(float), cudaMemcpyDefault);
   if (err == cudaSuccess) err = cudaMemset(e->bar, 0, 64 * sizeof(unsigned int));
   if (err != cudaSuccess)
     return fail(set_error(err == cudaErrorMemoryAllocation ? DS_E_NOMEM : DS_E_CUDA, "engine: %s", cudaGetErrorString(err)));
+  if (shard_path) {
+    ds_shard_info info{};
+    const int rc = ds_shard_load(shard_path, e->X, e->y, shard_n, &info, e->stream);
+    if (rc != DS_OK) return fail(rc);
+    if (info.n_samples != shard_n || info.n_features != F)
+      return fail(set_error(DS_E_FORMAT, "%s: changed while loading", shard_path));
+  }
   dsb::DevState s0{};
   s0.cut = hp->loss_cut;
   s0.tau = hp->tau;
@@ -569,6 +580,26 @@ extern "C" int ds_engine_create(ds_engine** out, int device, const ds_model_desc
   }
   *out = e;
   return DS_OK;
+}
+
+extern "C" int ds_engine_create(ds_engine** out, int device, const ds_model_desc* model, const float* X_host,
+                                const uint32_t* y_host, uint64_t shard_n, uint32_t shard_classes, const ds_hyper* hp,
+                                uint64_t sweep_seed, const float* init_host, int kind) {
+  return engine_create(out, device, model, X_host, y_host, shard_n, shard_classes, hp, sweep_seed, init_host, kind,
+                       nullptr);
+}
+
+extern "C" int ds_engine_create_from_shard(ds_engine** out, int device, const ds_model_desc* model, const char* path,
+                                           const ds_hyper* hp, uint64_t sweep_seed, const float* init_host, int kind) {
+  if (!path) return set_error(DS_E_CONTRACT, "engine: null argument");
+  ds_shard_info info{};
+  DS_TRY(ds_shard_info_read(path, &info));
+  dsb::ModelInfo m;
+  DS_TRY(dsb::model_from_desc(model, m));
+  if (info.n_features != m.n_features)
+    return set_error(DS_E_CONTRACT, "engine: shard has %u features, model expects %u", info.n_features, m.n_features);
+  return engine_create(out, device, model, nullptr, nullptr, info.n_samples, info.n_classes, hp, sweep_seed, init_host,
+                       kind, path);
 }
 
 extern "C" int ds_engine_destroy(ds_engine* e) {

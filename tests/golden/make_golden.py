@@ -69,6 +69,16 @@ def main():
         g[f"sim_{name}_virtual_total"] = np.array([o.virtual_total])
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(out, **g)
+    # a DSHD shard written by the reference's write_shard (shard.cpp:40-73): pins the
+    # device ingestion (ds_shard_load) and the header checks
+    import ctypes as C
+    Xs, ys = ref.gen_synthetic(37, 9, 4, 2.0, 1.0, 17)
+    fn = ref.lib.dsref_write_shard
+    fn.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64]
+    fn.restype = C.c_int
+    path = os.path.join(os.path.dirname(out), "ref_small.dshd")
+    assert fn(path.encode(), Xs.ctypes.data, ys.ctypes.data, len(ys), 9, 4, 0xFEED) == 0
+    np.savez_compressed(os.path.join(os.path.dirname(out), "ref_small_dshd.npz"), X=Xs, y=ys)
     print(f"wrote {out}: {len(g)} arrays, {os.path.getsize(out)} bytes")
 
 
