@@ -123,6 +123,17 @@ int ds_gather_rows(float* dst, uint32_t* y_dst, const float* X, const uint32_t* 
 
 /* ---------------------------------------------------------------------------------- */
 /* Device plumbing for hosts that do not link the CUDA runtime (C++/Go/Java/Python)   */
+/* D[M x N] = relu?( scale * A[M x K] . B[N x K]^T + bias_n[col] + bias_m[row] ) on the
+ * tcgen05 tensor cores (kind::tf32, f32 accumulation in TMEM; TMA SWIZZLE_128B tiles).
+ * A, B row-major with leading dimensions lda, ldb (multiples of 4, 16-byte aligned).
+ * Biases and ReLU optional (NULL / 0). splits > 1 cuts K into that many ranges whose
+ * partials (part: splits*M*N floats) are summed in a fixed order; D dense then. The
+ * contraction of the AlexNet-shaped convnet's convolution and FC layers (config 4; no
+ * reference counterpart). */
+int ds_gemm_tf32(const float* A, uint64_t lda, const float* B, uint64_t ldb, float* D, uint64_t ldd, uint32_t M,
+                 uint32_t N, uint32_t K, float scale, const float* bias_n, const float* bias_m, int relu,
+                 uint32_t splits, float* part, void* stream);
+
 /* ---------------------------------------------------------------------------------- */
 /* DSHD shards (shard.hpp:9-35, shard.cpp:75-125)                                     */
 /* ---------------------------------------------------------------------------------- */

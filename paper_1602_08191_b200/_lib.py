@@ -172,13 +172,14 @@ _sig("ds_sync_reduce_update", VP, VP, C.c_float, C.c_float, VP, VP)
 _sig("ds_sync_rounds", VP, P_U64)
 _sig("ds_sync_destroy", VP)
 _sig("ds_gather_rows", VP, VP, VP, VP, VP, U32, U32, VP)
+_sig("ds_gemm_tf32", VP, U64, VP, U64, VP, U64, U32, U32, U32, C.c_float, VP, VP, C.c_int, U32, VP, VP)
 _sig("ds_shard_info_read", C.c_char_p, C.POINTER(ds_shard_info))
 _sig("ds_shard_load", C.c_char_p, VP, VP, U64, C.POINTER(ds_shard_info), VP)
 _sig("ds_engine_create_from_shard", C.POINTER(VP), C.c_int, C.POINTER(ds_model_desc), C.c_char_p,
      C.POINTER(ds_hyper), U64, VP, C.c_int)
 
 EXPORTED = [
-    "ds_shard_info_read", "ds_shard_load", "ds_engine_create_from_shard",
+    "ds_gemm_tf32", "ds_shard_info_read", "ds_shard_load", "ds_engine_create_from_shard",
     "ds_last_error", "ds_version", "ds_device_count", "ds_elastic_update", "ds_elastic_exchange",
     "ds_sgd_update", "ds_sgd_step_checked", "ds_sgd_momentum_update", "ds_engine_set_momentum", "ds_engine_attach_sync", "ds_grad_accumulate", "ds_grad_average", "ds_device_alloc",
     "ds_device_free", "ds_memcpy", "ds_memset", "ds_stream_create", "ds_stream_destroy", "ds_stream_sync",

@@ -1,0 +1,27 @@
+// gemm_tc.cuh — TMA + tcgen05 tf32 GEMM (gemm_tc.cu): D = epi(scale * A . B^T), both
+// operands K-major row-major f32 (A [M x K] leading dimension lda, B [N x K] ldb; lda and
+// ldb multiples of 4, bases 16-byte aligned).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dsb {
+
+struct GemmEpilogue {
+  float* D = nullptr;
+  uint64_t ldd = 0;
+  uint64_t split_stride = 0;   // set internally for split-K slabs
+  float scale = 1.f;
+  const float* bias_n = nullptr;  // per output column
+  const float* bias_m = nullptr;  // per output row
+  bool relu = false;
+};
+
+// splits > 1: K is cut into `splits` ranges whose raw partials go to `part`
+// (splits * M * N floats) and are summed in split order (deterministic); D must then be
+// dense (ldd == N).
+int launch_gemm_tf32(const float* A, uint64_t lda, const float* B, uint64_t ldb, uint32_t M, uint32_t N, uint32_t K,
+                     const GemmEpilogue& ep, uint32_t splits, float* part, cudaStream_t s);
+uint32_t gemm_pick_bn(uint32_t N);
+
+}  // namespace dsb
