@@ -92,7 +92,8 @@ def _p(a: Optional[np.ndarray], ct):
 @dataclass
 class ModelSpec:
     """Mirror of deepspark::Model (model.hpp:32-56): kind 'softmax' | 'mlp', plus
-    'cifar10_quick' (kind 2, NOT IN THE REFERENCE; oracle/ds_oracle_cnn.h)."""
+    'cifar10_quick' (kind 2) and 'alexnet' (kind 3), NOT IN THE REFERENCE
+    (oracle/ds_oracle_cnn.h, oracle/ds_oracle_alex.h)."""
     kind: str
     n_features: int
     n_classes: int
@@ -110,9 +111,14 @@ class ModelSpec:
     def cifar10_quick(c: int = 10) -> "ModelSpec":
         return ModelSpec("cifar10_quick", 3072, c, ())
 
+    @staticmethod
+    def alexnet(side: int = 224, c: int = 1000) -> "ModelSpec":
+        """AlexNet-shaped (kind 3, NOT IN THE REFERENCE; oracle/ds_oracle_alex.h)."""
+        return ModelSpec("alexnet", 3 * side * side, c, ())
+
     def c(self):
         h = np.ascontiguousarray(np.asarray(self.hidden, dtype=np.uint32))
-        m = dso_model({"softmax": 0, "mlp": 1, "cifar10_quick": 2}[self.kind], self.n_features, self.n_classes,
+        m = dso_model({"softmax": 0, "mlp": 1, "cifar10_quick": 2, "alexnet": 3}[self.kind], self.n_features, self.n_classes,
                       len(self.hidden), _p(h if len(self.hidden) else None, C.c_uint32))
         return m, h  # keep h alive
 

@@ -204,3 +204,43 @@ def test_cnn_oracle_central_differences():
             assert rel <= 1e-4, (i, float(g[i]), cd, rel)
             checked += 1
     assert checked >= 20
+
+
+def test_alexnet_oracle_layout_and_central_differences():
+    """The AlexNet-shaped net (kind 3, BASELINE config 4) is NOT in the reference: its f64
+    restatement (oracle/ds_oracle_alex.c) is pinned by the published parameter count and by
+    central differences on a small input side (S = 55, same layers and widths), every
+    layer's weights and biases, relative error 1e-4 away from pool/relu kinks."""
+    from oracle.oracle import ModelSpec
+    o = Oracle("dso")
+    assert o.param_dim(ModelSpec.alexnet(224, 1000)) == 60965224  # SURVEY §8(a) a20
+    m = ModelSpec.alexnet(55, 5)
+    P = o.param_dim(m)
+    # conv 34,944 + 307,456 + 885,120 + 663,936 + 442,624; fc6 256 -> 4096; fc7; fc8 4096 -> 5
+    offs = np.cumsum([0, 34848, 96, 307200, 256, 884736, 384, 663552, 384, 442368, 256, 4096 * 256, 4096,
+                      4096 * 4096, 4096, 5 * 4096, 5])
+    assert P == offs[-1]
+    w = o.init_params(m, 2)
+    X, y = o.gen_synthetic(2, 3 * 55 * 55, 5, 1.0, 1.0, 7)
+    X = np.ascontiguousarray(X * 20.0, dtype=np.float32)  # large enough inputs that LRN is not the identity
+    _, g = o.loss_and_grad(m, w, X, y)
+    rng = np.random.default_rng(0)
+    checked = 0
+    for li in range(len(offs) - 1):
+        a, b = int(offs[li]), int(offs[li + 1])
+        for i in rng.integers(a, b, 3):
+            h = np.float32(1e-3 * max(abs(float(w[i])), 1e-2))
+            wp, wm = w.copy(), w.copy()
+            wp[i] += h
+            wm[i] -= h
+            lp, _ = o.loss_and_grad(m, wp, X, y, want_grad=False)
+            lm, _ = o.loss_and_grad(m, wm, X, y, want_grad=False)
+            cd = (lp - lm) / (float(wp[i]) - float(wm[i]))
+            if abs(cd) < 1e-9 and abs(g[i]) < 1e-9:
+                continue
+            rel = abs(cd - float(g[i])) / (abs(cd) + abs(float(g[i])))
+            if rel > 1e-4 and li < 10:  # conv layers feed max-pools / relus: a kink can fall inside +-h
+                continue
+            assert rel <= 1e-4, (li, i, float(g[i]), cd, rel)
+            checked += 1
+    assert checked >= 24
