@@ -171,6 +171,9 @@ int ds_stream_sync(void* stream);
  * NOT IN THE REFERENCE; same flat W-then-b layout, init and loss
  * conventions, f32 arithmetic (tolerance parity vs the f64 oracle, not bit-exact). */
 #define DS_MODEL_CIFAR10_QUICK 2
+/* AlexNet-shaped convnet (BASELINE config 4, NOT IN THE REFERENCE): n_features = 3*S*S
+ * (S = 224 for the config; S >= 55), n_hidden = 0; tf32 tensor-core GEMMs (alexnet.cu). */
+#define DS_MODEL_ALEXNET 3
 typedef struct {
   int32_t kind;          /* 0 = SoftmaxRegression, 1 = Mlp (model.hpp:13), 2 = cifar10_quick */
   uint32_t n_features;

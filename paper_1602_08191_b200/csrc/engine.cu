@@ -332,7 +332,7 @@ int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
         for (int k = 0; k < 3; ++k) e->graph_key[k] = key[k];
       }
     }
-    e->launches += per_step + (e->hostfed ? 0 : 1);
+    e->launches += (e->model.kind == DS_MODEL_ALEXNET ? dsb::alex_last_launches() + 2 : per_step) + (e->hostfed ? 0 : 1);
     if (e->hp.adaptive) {
       if (xm) DS_TRY(enqueue_exchange(e, p));  // conditional on the device fire flag
     } else if (++e->host_since == e->hp.tau) {

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      uint32_t M, uint32_t N, uint32_t K, uint32_t k_per_split) {
   using S = GemmSmem<BN>;
   constexpr int kStages = S::STAGES;
+  if (ep.gate && *ep.gate) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::STAGE);
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::fence_after();
     }
     float* out = ep.D + static_cast<uint64_t>(blockIdx.z) * ep.split_stride;
-    const bool raw = gridDim.z > 1;
+    const bool raw = ep.raw || gridDim.z > 1;
     const float bm = (!raw && ep.bias_m && row < M) ? ep.bias_m[row] : 0.f;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
@@ -157,7 +158,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           float x = v[j] * ep.scale + bm;
-          if (ep.bias_n && static_cast<uint32_t>(j) < lim) x += __ldg(ep.bias_n + n0 + c + j);
+          if (static_cast<uint32_t>(j) < lim) {
+            if (ep.bias_n) x += __ldg(ep.bias_n + n0 + c + j);
+            if (ep.mask && !(ep.mask[static_cast<uint64_t>(row) * ep.ldm + n0 + c + j] > 0.f)) x = 0.f;
+          }
           v[j] = ep.relu ? fmaxf(x, 0.f) : x;
         }
       }
@@ -179,16 +183,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 // sum of the split slabs in split order, then scale, bias, ReLU
 __global__ void gemm_reduce_kernel(const float* __restrict__ part, uint64_t split_stride, uint32_t splits,
                                    GemmEpilogue ep, uint32_t M, uint32_t N) {
+  if (ep.gate && *ep.gate) return;
   const uint64_t total = static_cast<uint64_t>(M) * N;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t r = static_cast<uint32_t>(i / N), c = static_cast<uint32_t>(i % N);
-    const uint64_t off = static_cast<uint64_t>(r) * ep.ldd + c;
+    const uint64_t off = static_cast<uint64_t>(r) * ep.ldd + c;  // D; the slabs are dense [M][N]
     float s = 0.f;
-    for (uint32_t z = 0; z < splits; ++z) s += part[z * split_stride + off];
+    for (uint32_t z = 0; z < splits; ++z) s += part[z * split_stride + i];
     float x = s * ep.scale;
     if (ep.bias_m) x += ep.bias_m[r];
     if (ep.bias_n) x += ep.bias_n[c];
+    if (ep.mask && !(ep.mask[static_cast<uint64_t>(r) * ep.ldm + c] > 0.f)) x = 0.f;
     ep.D[off] = ep.relu ? fmaxf(x, 0.f) : x;
   }
 }
@@ -245,38 +251,101 @@ int launch_bn(const CUtensorMap& ma, const float* B, uint64_t ldb, const GemmEpi
 
 }  // namespace
 
-uint32_t gemm_pick_bn(uint32_t N) { return N <= 64 ? 64 : (N <= 128 ? 128 : 256); }
+// the tile width with the least padding past N (ties: the wider tile)
+uint32_t gemm_pick_bn(uint32_t N) {
+  uint32_t best = 256, waste = (N + 255) / 256 * 256 - N;
+  for (uint32_t bn : {128u, 64u}) {
+    const uint32_t w = (N + bn - 1) / bn * bn - N;
+    if (w < waste) best = bn, waste = w;
+  }
+  return best;
+}
+
+namespace {
+
+// hi = x with the 13 low mantissa bits cleared (exact in tf32), lo = x - hi (exact in f32)
+__global__ void split_tf32_kernel(const float* __restrict__ x, uint32_t rows, uint32_t cols, uint64_t ld,
+                                  float* __restrict__ hi, float* __restrict__ lo, uint64_t ldo) {
+  const uint64_t total = static_cast<uint64_t>(rows) * cols;
+  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
+    const uint64_t r = i / cols, c = i % cols;
+    const float v = x[r * ld + c];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[r * ldo + c] = h;
+    lo[r * ldo + c] = v - h;
+  }
+}
+
+bool exact_mode() {  // DS_GEMM_3XTF32=1: f32-accurate products (parity diagnostics; read per call)
+  const char* e = getenv("DS_GEMM_3XTF32");
+  return e && e[0] == '1';
+}
+
+int launch_raw(const float* A, uint64_t lda, const float* B, uint64_t ldb, uint32_t M, uint32_t N, uint32_t K,
+               const GemmEpilogue& ep, uint32_t splits, cudaStream_t s) {
+  CUtensorMap ma;
+  DS_TRY(make_map(&ma, A, M, K, lda, kBM));
+  const uint32_t bn = gemm_pick_bn(N);
+  if (bn == 64) return launch_bn<64>(ma, B, ldb, ep, M, N, K, splits, s);
+  if (bn == 128) return launch_bn<128>(ma, B, ldb, ep, M, N, K, splits, s);
+  return launch_bn<256>(ma, B, ldb, ep, M, N, K, splits, s);
+}
+
+// 3xTF32: A.B ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi as three raw slabs, reduced with the epilogue
+int launch_3xtf32(const float* A, uint64_t lda, const float* B, uint64_t ldb, uint32_t M, uint32_t N, uint32_t K,
+                  const GemmEpilogue& ep_in, cudaStream_t s) {
+  const uint64_t kp = (K + 3) / 4 * 4;
+  float *ah = nullptr, *bh = nullptr, *slab = nullptr;
+  DS_CUDA_TRY(cudaMallocAsync(&ah, 2 * M * kp * 4, s));
+  DS_CUDA_TRY(cudaMallocAsync(&bh, 2 * N * kp * 4, s));
+  DS_CUDA_TRY(cudaMallocAsync(&slab, 3ull * M * N * 4, s));
+  float *al = ah + M * kp, *bl = bh + N * kp;
+  split_tf32_kernel<<<4096, 256, 0, s>>>(A, M, K, lda, ah, al, kp);
+  split_tf32_kernel<<<4096, 256, 0, s>>>(B, N, K, ldb, bh, bl, kp);
+  GemmEpilogue raw = ep_in;
+  raw.split_stride = 0;
+  raw.ldd = N;
+  raw.raw = true;
+  const float* pa[3] = {ah, ah, al};
+  const float* pb[3] = {bh, bl, bh};
+  int rc = DS_OK;
+  for (int t = 0; t < 3 && rc == DS_OK; ++t) {
+    raw.D = slab + static_cast<uint64_t>(t) * M * N;
+    rc = launch_raw(pa[t], kp, pb[t], kp, M, N, K, raw, 1, s);
+  }
+  if (rc == DS_OK) {
+    const uint64_t total = static_cast<uint64_t>(M) * N;
+    gemm_reduce_kernel<<<static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16)), 256, 0, s>>>(
+        slab, total, 3, ep_in, M, N);
+    if (cudaGetLastError() != cudaSuccess) rc = set_error(DS_E_CUDA, "gemm: reduce launch failed");
+  }
+  cudaFreeAsync(ah, s);
+  cudaFreeAsync(bh, s);
+  cudaFreeAsync(slab, s);
+  return rc;
+}
+
+}  // namespace
 
 int launch_gemm_tf32(const float* A, uint64_t lda, const float* B, uint64_t ldb, uint32_t M, uint32_t N, uint32_t K,
                      const GemmEpilogue& ep_in, uint32_t splits, float* part, cudaStream_t s) {
   if (M == 0 || N == 0) return DS_OK;
+  if (exact_mode()) return launch_3xtf32(A, lda, B, ldb, M, N, K, ep_in, s);
   if (splits == 0) splits = 1;
   const uint32_t max_splits = (K + kBK - 1) / kBK;
   if (splits > max_splits) splits = max_splits;
   if (splits > 1 && !part) return set_error(DS_E_CONTRACT, "gemm: split-K needs a partial buffer");
-  CUtensorMap ma;
-  DS_TRY(make_map(&ma, A, M, K, lda, kBM));
   GemmEpilogue ep = ep_in;
-  if (splits > 1) {  // raw partial slabs [splits][M][N], reduced below
+  if (splits > 1) {  // raw partial slabs [splits][M][N], reduced below with the epilogue
     ep.D = part;
     ep.ldd = N;
     ep.split_stride = static_cast<uint64_t>(M) * N;
   }
-  const uint32_t bn = gemm_pick_bn(N);
-  if (bn == 64) DS_TRY(launch_bn<64>(ma, B, ldb, ep, M, N, K, splits, s));
-  else if (bn == 128) DS_TRY(launch_bn<128>(ma, B, ldb, ep, M, N, K, splits, s));
-  else DS_TRY(launch_bn<256>(ma, B, ldb, ep, M, N, K, splits, s));
+  DS_TRY(launch_raw(A, lda, B, ldb, M, N, K, ep, splits, s));
   if (splits > 1) {
-    GemmEpilogue out = ep_in;
     const uint64_t total = static_cast<uint64_t>(M) * N;
     const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-    // the reduce reads part with row stride N and writes D with ldd: index through ep.ldd for D only
-    if (out.ldd != N) {
-      // partial slabs are dense [M][N]; write through a dense view then the caller's ldd
-      // is honoured by reducing row by row (rare: only FC layers split, and they are dense)
-      return set_error(DS_E_CONTRACT, "gemm: split-K output must be dense (ldd == N)");
-    }
-    gemm_reduce_kernel<<<blocks, 256, 0, s>>>(part, static_cast<uint64_t>(M) * N, splits, out, M, N);
+    gemm_reduce_kernel<<<blocks, 256, 0, s>>>(part, total, splits, ep_in, M, N);
     DS_CUDA_TRY(cudaGetLastError());
   }
   return DS_OK;

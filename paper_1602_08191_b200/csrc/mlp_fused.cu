@@ -1519,7 +1519,7 @@ size_t fused_smem_bytes(const ModelInfo& m, uint32_t batch) {
 }
 
 int fused_supported(const ModelInfo& m, uint32_t batch, int device, const char** why) {
-  if (m.kind == DS_MODEL_CIFAR10_QUICK) {
+  if (m.kind == DS_MODEL_CIFAR10_QUICK || m.kind == DS_MODEL_ALEXNET) {
     if (why) *why = "convnet models run on the layered path";
     return DS_E_CONTRACT;
   }

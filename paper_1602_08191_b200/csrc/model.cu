@@ -44,6 +44,36 @@ int model_from_desc(const ds_model_desc* d, ModelInfo& out) {
     out.sum_out = 0;
     return DS_OK;
   }
+  if (d->kind == DS_MODEL_ALEXNET) {  // NOT IN REFERENCE (alexnet.cu); layout as oracle/ds_oracle_alex.c
+    uint32_t S = 0;
+    while (3ull * (S + 1) * (S + 1) <= d->n_features) ++S;
+    if (3ull * S * S != d->n_features || S < 55)
+      return set_error(DS_E_CONTRACT, "model: alexnet takes 3*S*S features, S >= 55");
+    if (d->n_classes < 2) return set_error(DS_E_CONTRACT, "model: n_classes must be at least 2");
+    if (d->n_hidden != 0) return set_error(DS_E_CONTRACT, "model: alexnet has no hidden list");
+    out = ModelInfo{};
+    out.kind = d->kind;
+    out.n_features = d->n_features;
+    out.n_classes = d->n_classes;
+    out.alex_side = S;
+    const uint32_t H1 = (S - 11) / 4 + 1, P1 = (H1 - 2) / 2 + 1, P2 = (P1 - 2) / 2 + 1, P5 = (P2 - 2) / 2 + 1;
+    const uint32_t fan[8] = {363, 1200, 2304, 1728, 1728, 256 * P5 * P5, 4096, 4096};
+    const uint32_t width[8] = {96, 256, 384, 384, 256, 4096, 4096, d->n_classes};
+    uint64_t off = 0;
+    for (int l = 0; l < 8; ++l) {
+      LayerInfo L;
+      L.w_off = off;
+      off += static_cast<uint64_t>(width[l]) * fan[l];
+      L.b_off = off;
+      off += width[l];
+      L.in_dim = fan[l];
+      L.out_dim = width[l];
+      out.layers.push_back(L);
+    }
+    out.P = off;
+    out.max_out = 4096;
+    return DS_OK;
+  }
   if (d->kind != 0 && d->kind != 1) return set_error(DS_E_CONTRACT, "model: unknown kind %d", d->kind);
   if (d->n_features == 0) return set_error(DS_E_CONTRACT, "model: n_features must be positive");
   if (d->n_classes < 2) return set_error(DS_E_CONTRACT, "model: n_classes must be at least 2");
@@ -81,6 +111,7 @@ int model_from_desc(const ds_model_desc* d, ModelInfo& out) {
 
 uint64_t layered_workspace_doubles(const ModelInfo& m, uint32_t R) {
   if (m.kind == DS_MODEL_CIFAR10_QUICK) return (cnn_workspace_bytes(m, R) + 7) / 8;
+  if (m.kind == DS_MODEL_ALEXNET) return (alex_workspace_bytes(m, R) + 7) / 8;
   // activations A_1..A_L, two delta buffers, per-row loss
   return static_cast<uint64_t>(R) * (m.sum_out + 2ull * m.max_out + 1);
 }
@@ -267,6 +298,8 @@ int launch_loss_and_grad(const ModelInfo& m, const float* params, const float* X
   if (R > 65535) return set_error(DS_E_CONTRACT, "loss_and_grad: at most 65535 rows per call");
   if (m.kind == DS_MODEL_CIFAR10_QUICK)
     return launch_cnn_loss_and_grad(m, params, X, idx, y, R, grad, loss_out, ws, flags, gate, s);
+  if (m.kind == DS_MODEL_ALEXNET)
+    return launch_alex_loss_and_grad(m, params, X, idx, y, R, grad, loss_out, ws, flags, gate, s);
   const WsView v = carve(m, R, ws);
   forward(m, params, X, idx, R, v, gate, s);
   const size_t nl = m.layers.size();
@@ -303,6 +336,7 @@ int launch_count_hits(const ModelInfo& m, const float* params, const float* X, c
                       double* ws, unsigned long long* hits, uint32_t* pred, cudaStream_t s) {
   if (R == 0) return DS_OK;
   if (m.kind == DS_MODEL_CIFAR10_QUICK) return launch_cnn_count_hits(m, params, X, y, R, ws, hits, pred, s);
+  if (m.kind == DS_MODEL_ALEXNET) return launch_alex_count_hits(m, params, X, y, R, ws, hits, pred, s);
   const WsView v = carve(m, R, ws);
   forward(m, params, X, nullptr, R, v, nullptr, s);
   argmax_hits<<<(R + kT - 1) / kT, kT, 0, s>>>(v.act[m.layers.size() - 1], y, R, m.n_classes, hits, pred);
@@ -347,7 +381,7 @@ extern "C" int ds_predict(const ds_model_desc* model, const float* params, const
   dsb::ModelInfo m;
   DS_TRY(dsb::model_from_desc(model, m));
   cudaStream_t s = dsb::as_stream(stream);
-  const uint32_t chunk = 4096;
+  const uint32_t chunk = m.kind == DS_MODEL_ALEXNET ? 128 : 4096;  // alexnet workspace grows ~25 MB per row
   double* ws = nullptr;
   DS_CUDA_TRY(cudaMallocAsync(&ws, dsb::layered_workspace_doubles(m, chunk) * sizeof(double), s));
   int rc = DS_OK;
@@ -364,7 +398,7 @@ extern "C" int ds_count_hits(const ds_model_desc* model, const float* params, co
   dsb::ModelInfo m;
   DS_TRY(dsb::model_from_desc(model, m));
   cudaStream_t s = dsb::as_stream(stream);
-  const uint32_t chunk = 4096;
+  const uint32_t chunk = m.kind == DS_MODEL_ALEXNET ? 128 : 4096;  // alexnet workspace grows ~25 MB per row
   double* ws = nullptr;
   DS_CUDA_TRY(cudaMallocAsync(&ws, dsb::layered_workspace_doubles(m, chunk) * sizeof(double), s));
   int rc = DS_OK;

@@ -16,13 +16,14 @@ struct LayerInfo {
 };
 
 struct ModelInfo {
-  int32_t kind = 0;  // 0 softmax, 1 mlp, 2 cifar10_quick (NOT IN REFERENCE)
+  int32_t kind = 0;  // 0 softmax, 1 mlp, 2 cifar10_quick, 3 alexnet (2, 3 NOT IN REFERENCE)
   uint32_t n_features = 0, n_classes = 0;
   std::vector<uint32_t> hidden;
   std::vector<LayerInfo> layers;
   uint64_t P = 0;
   uint32_t max_out = 0;
   uint64_t sum_out = 0;
+  uint32_t alex_side = 0;  // kind 3: input side S
 };
 
 // Model::validate (model.cpp:44-57) + layer layout; DS_E_CONTRACT on invalid models.
@@ -49,6 +50,15 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
                              const uint32_t* gate, cudaStream_t s);
 int launch_cnn_count_hits(const ModelInfo& m, const float* P, const float* X, const uint32_t* y, uint32_t R, void* ws,
                           unsigned long long* hits, uint32_t* pred, cudaStream_t s);
+
+// AlexNet-shaped (kind DS_MODEL_ALEXNET, alexnet.cu; NOT IN REFERENCE).
+uint64_t alex_workspace_bytes(const ModelInfo& m, uint32_t R);
+uint32_t alex_last_launches();  // kernels issued by this thread's last launch_alex_loss_and_grad
+int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X, const uint32_t* idx,
+                              const uint32_t* y, uint32_t R, float* grad, double* loss_out, void* ws,
+                              uint32_t* flags, const uint32_t* gate, cudaStream_t s);
+int launch_alex_count_hits(const ModelInfo& m, const float* P, const float* X, const uint32_t* y, uint32_t R,
+                           void* ws, unsigned long long* hits, uint32_t* pred, cudaStream_t s);
 
 // Hits of predict() (model.cpp:303-318) against labels over rows [0,R).
 int launch_count_hits(const ModelInfo& m, const float* params, const float* X, const uint32_t* y,
