@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--exchange-params", type=int, default=256 * 1024 * 1024)
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / exchange sweep / cpu baseline (profiling)")
     ap.add_argument("--cifar-steps", type=int, default=200, help="timed steps of the cifar10_quick leg (0 = skip)")
+    ap.add_argument("--alexnet-steps", type=int, default=20, help="timed steps of the AlexNet leg (0 = skip)")
     return ap.parse_args()
 
 
@@ -294,10 +295,13 @@ def main():
     if not args.no_extras:
         line["e2e"] = e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n)
         line["exchange"] = exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind)
-        if args.cifar_steps > 0:
-            line["cifar10_quick"] = cifar_leg(args, L, api, torch, dist, world, rank, local)
-            line["cifar10_quick_config3"] = {k: cifar_leg(args, L, api, torch, dist, world, rank, local, k)
-                                             for k in ("sync", "adaptive")}
+    if args.cifar_steps > 0:
+        line["cifar10_quick"] = cifar_leg(args, L, api, torch, dist, world, rank, local)
+        line["cifar10_quick_config3"] = {k: cifar_leg(args, L, api, torch, dist, world, rank, local, k)
+                                         for k in ("sync", "adaptive")}
+    if args.alexnet_steps > 0:
+        line["alexnet"] = alexnet_leg(args, L, api, torch, dist, world, rank, local)
+    if not args.no_extras:
         if rank == 0 and world == 1:
             line["cpu_baseline"] = cpu_baseline(args, X, y)
     L.lib.ds_engine_destroy(eng)
@@ -515,6 +519,97 @@ def cifar_leg(args, L, api, torch, dist, world, rank, local, mode="async"):
         if mode == "adaptive":
             out["loss_cut"] = cut
     return out
+
+
+# multiply-adds per sample of the AlexNet-shaped net at S = 224 (oracle/ds_oracle_alex.h):
+# (MACs per output pixel x output pixels) per layer; training = forward + data gradient
+# (all but conv1) + weight gradient
+ALEX_FWD_MAC = [96 * 363 * 54 * 54, 256 * 1200 * 27 * 27, 384 * 2304 * 13 * 13, 384 * 1728 * 13 * 13,
+                256 * 1728 * 13 * 13, 4096 * 9216, 4096 * 4096, 1000 * 4096]
+ALEX_TRAIN_FLOP = 2 * (3 * sum(ALEX_FWD_MAC) - ALEX_FWD_MAC[0])
+
+
+def alexnet_leg(args, L, api, torch, dist, world, rank, local):
+    """BASELINE config 4: AlexNet-shaped CNN on synthetic 224x224x3 ImageNet-shaped rows,
+    1000 classes, batch 128 per worker, async EASGD tau=10 alpha=0.1 with the center sharded
+    over the GPUs (LockFree), one worker per GPU. NOT IN THE REFERENCE (no conv layers):
+    every convolution and FC contraction on the tcgen05 tensor cores (tf32, csrc/gemm_tc.cu),
+    NHWC layer kernels in csrc/alexnet.cu. Rows are N(0,1) generated on the device (the
+    reference's gen_synthetic is O(classes^2 x features) for 1000 x 150,528 and takes minutes);
+    labels uniform. Device-timed, max over ranks."""
+    from paper_1602_08191_b200 import dist as D
+    from paper_1602_08191_b200.deepspark import Model
+    B, K, N, S, Cls = 128, args.alexnet_steps, 512, 224, 1000
+    F = 3 * S * S
+    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    Xd = torch.randn(N, F, device="cuda", generator=g)  # 308 MB per GPU: larger than L2
+    yk = np.random.default_rng(2000 + rank).integers(0, Cls, N).astype(np.uint32)
+    m = Model.alexnet(S, Cls)
+    P = api.param_dim(m)
+    init = torch.empty(P, dtype=torch.float32, device="cuda")
+    if rank == 0:
+        init.copy_(torch.from_numpy(api.init_params(m, INIT_SEED)))
+    if world > 1:
+        dist.broadcast(init, 0)
+    torch.cuda.synchronize()
+    hidden = (C.c_uint32 * 1)(0)
+    desc = L.ds_model_desc(3, F, Cls, 0, hidden)
+    hp = L.ds_hyper(0.01, 0.1, 10, B, 10 ** 9, 0.0, 0.0, 0)
+    eng = C.c_void_p()
+    L.check(L.lib.ds_engine_create(C.byref(eng), local, C.byref(desc), C.c_void_p(Xd.data_ptr()), yk.ctypes.data, N,
+                                   Cls, C.byref(hp), api.mix_seed(7, rank), C.c_void_p(init.data_ptr()),
+                                   L.DS_ENGINE_AUTO))
+    del Xd
+    if world == 1:
+        mst = C.c_void_p()
+        L.check(L.lib.ds_master_create(C.byref(mst), local, P, C.c_float(0.1), L.DS_MODE_LOCKFREE,
+                                       C.c_void_p(init.data_ptr())))
+    else:
+        mst = D.sharded_master(L, local, P, 0.1, L.DS_MODE_LOCKFREE, init.data_ptr(), rank, world)
+    L.check(L.lib.ds_engine_attach_master(eng, mst))
+    W = 3
+    L.check(L.lib.ds_engine_reserve(eng, K + W))
+    L.check(L.lib.ds_engine_run(eng, W, 0, None))
+    L.check(L.lib.ds_engine_sync(eng))
+    sp = C.c_void_p()
+    L.check(L.lib.ds_engine_stream(eng, C.byref(sp)))
+    st = torch.cuda.ExternalStream(sp.value)
+    n0 = C.c_uint64()
+    L.check(L.lib.ds_engine_launches(eng, C.byref(n0)))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    L.check(L.lib.ds_engine_run(eng, K, 0, None))
+    e1.record(st)
+    L.check(L.lib.ds_engine_sync(eng))
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n1 = C.c_uint64()
+    L.check(L.lib.ds_engine_launches(eng, C.byref(n1)))
+    loss = np.zeros(K + W)
+    L.check(L.lib.ds_engine_log(eng, 0, K + W, loss.ctypes.data, None, None, None))
+    L.lib.ds_engine_destroy(eng)
+    if world > 1:
+        dist.barrier()
+    L.lib.ds_master_destroy(mst)
+    ms = t.item()
+    tflops = ALEX_TRAIN_FLOP * B * K / (ms / 1e3) / 1e12
+    return {"metric": "train samples/s (AlexNet-shaped, BASELINE config 4 shape)", "value": world * B * K / (ms / 1e3),
+            "unit": "samples/s", "ms_per_step": ms / K, "steps": K, "warmup": W, "batch_per_worker": B,
+            "tau": 10, "alpha": 0.1, "eta": 0.01, "workers": world, "params": P,
+            "exchange": "LockFree, center sharded over the GPUs" if world > 1 else "LockFree, center on the same GPU",
+            "dtype": "tf32 tensor cores (tcgen05 GEMMs, f32 accumulation in TMEM), f32 elsewhere",
+            "data": "synthetic N(0,1) rows 3x224x224 (CHW), uniform labels over 1000 classes, 512 rows per GPU "
+                    "(308 MB, larger than L2)",
+            "flop_per_sample": ALEX_TRAIN_FLOP, "achieved_tflops": tflops,
+            "tf32_peak_tflops": 823.4, "tf32_peak_kind": "measured bf16 dense burst (MEASURED_PEAKS.json) / 2; "
+            "nominal tf32 dense 1100", "tensor_frac": tflops / 823.4,
+            "gpu_launches": int(n1.value - n0.value), "loss_first_last": [float(loss[0]), float(loss[-1])],
+            "reference_arm": "none: the reference has no conv layers (SURVEY §8 a20)"}
 
 
 def cpu_baseline(args, X, y):

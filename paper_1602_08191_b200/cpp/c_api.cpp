@@ -42,7 +42,10 @@ int guard(F&& f) {
 
 Model model_of(const dsx_model* m) {
   Model out;
-  out.kind = m->kind == 0 ? ModelKind::SoftmaxRegression : (m->kind == 1 ? ModelKind::Mlp : ModelKind::Cifar10Quick);
+  out.kind = m->kind == 0 ? ModelKind::SoftmaxRegression
+             : m->kind == 1 ? ModelKind::Mlp
+             : m->kind == 2 ? ModelKind::Cifar10Quick
+                            : ModelKind::AlexNet;
   out.n_features = m->n_features;
   out.n_classes = m->n_classes;
   out.hidden.assign(m->hidden, m->hidden + m->n_hidden);

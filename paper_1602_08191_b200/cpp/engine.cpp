@@ -92,7 +92,7 @@ SgdEngine::SgdEngine(Model model, const Dataset& shard, const Hyperparams& hp, u
   if (shard.n_features != model_.n_features || shard.n_classes > model_.n_classes)
     throw ContractError("engine: shard dims do not match model");
   std::vector<uint32_t> hidden = model_.hidden;
-  ds_model_desc d{model_.kind == ModelKind::SoftmaxRegression ? 0 : (model_.kind == ModelKind::Mlp ? 1 : DS_MODEL_CIFAR10_QUICK), model_.n_features, model_.n_classes,
+  ds_model_desc d{model_kind_code(model_.kind), model_.n_features, model_.n_classes,
                   static_cast<uint32_t>(hidden.size()), hidden.data()};
   const ds_hyper h = to_ds(hp_);
   check_status(ds_engine_create(&h_, detail::default_device(), &d, shard.features.data(), shard.labels.data(),

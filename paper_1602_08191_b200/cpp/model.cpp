@@ -18,7 +18,7 @@ namespace {
 detail::ModelDesc desc_of(const Model& m) {
   detail::ModelDesc md;
   md.hidden = m.hidden;
-  md.d.kind = m.kind == ModelKind::SoftmaxRegression ? 0 : (m.kind == ModelKind::Mlp ? 1 : DS_MODEL_CIFAR10_QUICK);
+  md.d.kind = model_kind_code(m.kind);
   md.d.n_features = m.n_features;
   md.d.n_classes = m.n_classes;
   md.d.n_hidden = static_cast<uint32_t>(md.hidden.size());
@@ -116,7 +116,30 @@ Model Model::cifar10_quick(uint32_t n_classes) {
   return m;
 }
 
+Model Model::alexnet(uint32_t side, uint32_t n_classes) {
+  Model m;
+  m.kind = ModelKind::AlexNet;
+  m.n_features = 3 * side * side;
+  m.n_classes = n_classes;
+  m.validate();
+  return m;
+}
+
+namespace {
+uint32_t alex_side(uint32_t n_features) {  // S with 3*S*S == n_features and S >= 55, else 0
+  uint32_t s = 0;
+  while (3ull * (s + 1) * (s + 1) <= n_features) ++s;
+  return (3ull * s * s == n_features && s >= 55) ? s : 0;
+}
+}  // namespace
+
 void Model::validate() const {
+  if (kind == ModelKind::AlexNet) {
+    if (!alex_side(n_features)) throw ContractError("model: alexnet takes 3*S*S features, S >= 55");
+    if (n_classes < 2) throw ContractError("model: n_classes must be at least 2");
+    if (!hidden.empty()) throw ContractError("model: alexnet has no hidden list");
+    return;
+  }
   if (kind == ModelKind::Cifar10Quick) {
     if (n_features != 3072) throw ContractError("model: cifar10_quick takes 3072 features");
     if (n_classes < 2) throw ContractError("model: n_classes must be at least 2");
@@ -155,6 +178,11 @@ Model Model::parse(const std::string& text) {
     if (positive(parts[1]) != 3072) throw ContractError("model: cifar10_quick takes 3072 features");
     return cifar10_quick(positive(parts[2]));
   }
+  if (parts.size() == 3 && parts[0] == "alexnet") {
+    const uint32_t s = alex_side(positive(parts[1]));
+    if (!s) throw ContractError("model: alexnet takes 3*S*S features, S >= 55");
+    return alexnet(s, positive(parts[2]));
+  }
   if (parts.size() == 4 && parts[0] == "mlp") {
     std::vector<uint32_t> hidden;
     std::stringstream hs(parts[2]);
@@ -177,6 +205,10 @@ std::string Model::to_string() const {
     os << "cifar10_quick:" << n_features << ':' << n_classes;
     return os.str();
   }
+  if (kind == ModelKind::AlexNet) {
+    os << "alexnet:" << n_features << ':' << n_classes;
+    return os.str();
+  }
   os << "mlp:" << n_features << ':';
   for (size_t i = 0; i < hidden.size(); ++i) os << (i ? "," : "") << hidden[i];
   os << ':' << n_classes;
@@ -185,6 +217,19 @@ std::string Model::to_string() const {
 
 std::vector<Model::Layer> Model::layers() const {
   std::vector<Layer> out;
+  if (kind == ModelKind::AlexNet) {  // conv1..5 (fan_in = Cin/g * k * k), fc6..8 (oracle/ds_oracle_alex.h)
+    const uint32_t S = alex_side(n_features), H1 = (S - 11) / 4 + 1, P1 = (H1 - 2) / 2 + 1, P2 = (P1 - 2) / 2 + 1,
+                   P5 = (P2 - 2) / 2 + 1;
+    const uint32_t fan[8] = {363, 1200, 2304, 1728, 1728, 256 * P5 * P5, 4096, 4096};
+    const uint32_t width[8] = {96, 256, 384, 384, 256, 4096, 4096, n_classes};
+    size_t off = 0;
+    for (int l = 0; l < 8; ++l) {
+      Layer L{off, off + static_cast<size_t>(width[l]) * fan[l], fan[l], width[l]};
+      off = L.b_off + width[l];
+      out.push_back(L);
+    }
+    return out;
+  }
   if (kind == ModelKind::Cifar10Quick) {  // conv1..3 (fan_in = Cin*25), ip1, ip2
     const uint32_t fan[5] = {75, 800, 800, 1024, 64}, width[5] = {32, 32, 64, 64, n_classes};
     size_t off = 0;
@@ -221,7 +266,7 @@ uint64_t Model::fingerprint() const {
       h *= 0x100000001b3ULL;  // FNV prime
     }
   };
-  mix(kind == ModelKind::SoftmaxRegression ? 1 : (kind == ModelKind::Mlp ? 2 : 3), 1);
+  mix(static_cast<uint64_t>(model_kind_code(kind)) + 1, 1);
   mix(n_features, 4);
   mix(n_classes, 4);
   mix(hidden.size(), 4);

@@ -46,7 +46,7 @@ class DeviceHoldout {
     ctx.upload(y_.as<void>(), ds.labels.data(), ds.size() * sizeof(uint32_t));
     ctx.sync();
     hidden_ = m.hidden;
-    d_ = ds_model_desc{m.kind == ModelKind::SoftmaxRegression ? 0 : (m.kind == ModelKind::Mlp ? 1 : DS_MODEL_CIFAR10_QUICK), m.n_features, m.n_classes,
+    d_ = ds_model_desc{model_kind_code(m.kind), m.n_features, m.n_classes,
                        static_cast<uint32_t>(hidden_.size()), hidden_.data()};
   }
   double accuracy_of(const float* dparams) {
@@ -156,7 +156,7 @@ SimResult simulate_sync(const SimConfig& cfg, const std::vector<const Dataset*>&
 
   auto& ctx = detail::DeviceCtx::get();
   std::vector<uint32_t> hidden = cfg.model.hidden;
-  const ds_model_desc d{cfg.model.kind == ModelKind::SoftmaxRegression ? 0 : (cfg.model.kind == ModelKind::Mlp ? 1 : DS_MODEL_CIFAR10_QUICK), cfg.model.n_features,
+  const ds_model_desc d{model_kind_code(cfg.model.kind), cfg.model.n_features,
                         cfg.model.n_classes, static_cast<uint32_t>(hidden.size()), hidden.data()};
   uint64_t ws_bytes = 0;
   check_status(ds_loss_and_grad_workspace(&d, B, &ws_bytes), "simulate");

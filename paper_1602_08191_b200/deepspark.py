@@ -123,8 +123,8 @@ def _check(rc: int):
 
 @dataclass
 class Model:
-    """deepspark::Model (model.hpp:32-56): kind 'softmax' | 'mlp' | 'cifar10_quick' (the
-    last an extension, not in the reference)."""
+    """deepspark::Model (model.hpp:32-56): kind 'softmax' | 'mlp' | 'cifar10_quick' |
+    'alexnet' (the last two extensions, not in the reference)."""
     kind: str
     n_features: int
     n_classes: int
@@ -142,6 +142,10 @@ class Model:
     def cifar10_quick(c=10):
         return Model("cifar10_quick", 3072, c, ())
 
+    @staticmethod
+    def alexnet(side=224, c=1000):
+        return Model("alexnet", 3 * side * side, c, ())
+
 
 @dataclass
 class Hyperparams:
@@ -158,7 +162,7 @@ class Hyperparams:
 
 def _model(m):
     h = np.ascontiguousarray(np.asarray(tuple(m.hidden), dtype=np.uint32))
-    d = dsx_model({"softmax": 0, "mlp": 1, "cifar10_quick": 2}[m.kind], m.n_features, m.n_classes, len(m.hidden),
+    d = dsx_model({"softmax": 0, "mlp": 1, "cifar10_quick": 2, "alexnet": 3}[m.kind], m.n_features, m.n_classes, len(m.hidden),
                   _p(h if len(m.hidden) else None, C.c_uint32))
     return d, h
 

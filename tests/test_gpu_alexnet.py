@@ -152,3 +152,44 @@ def test_predict_matches_oracle(T, L, orc):
     got = pred.cpu().numpy()
     agree = (got == ref).mean()
     assert agree >= 0.9, agree
+
+
+def test_engine_training_tracks_oracle(T, L, orc, mode, monkeypatch):
+    """run_training_loop with a Locked master exchange every tau steps through the layered
+    engine (CUDA-graph replay in tf32 mode); exact mode tracks the f64 oracle to 1e-5."""
+    if mode == "exact":
+        monkeypatch.setenv("DS_ENGINE_NO_GRAPH", "1")
+    from oracle.oracle import Hyper
+    side, c = 55, 5
+    m = ModelSpec.alexnet(side, c)
+    X, y = orc.gen_synthetic(24, 3 * side * side, c, 1.0, 1.0, 7)
+    X = np.ascontiguousarray(X * 5.0, dtype=np.float32)
+    w = orc.init_params(m, 2)
+    hp = Hyper(eta=0.01, alpha=0.1, tau=3, batch_size=4, i_max=8)
+    d = desc(L, side, c)
+    h = L.ds_hyper(hp.eta, hp.alpha, hp.tau, hp.batch_size, hp.i_max, 0.0, 0.0, 0)
+    e = C.c_void_p()
+    yk = y.astype(np.uint32)
+    L.check(L.lib.ds_engine_create(C.byref(e), 0, C.byref(d), X.ctypes.data, yk.ctypes.data, len(y), c, C.byref(h),
+                                   99, w.ctypes.data, L.DS_ENGINE_AUTO))
+    mst = C.c_void_p()
+    L.check(L.lib.ds_master_create(C.byref(mst), 0, len(w), C.c_float(0.1), L.DS_MODE_LOCKED, w.ctypes.data))
+    L.check(L.lib.ds_engine_attach_master(e, mst))
+    L.check(L.lib.ds_engine_run(e, hp.i_max, 0, None))
+    L.check(L.lib.ds_engine_sync(e))
+    params = np.zeros_like(w)
+    L.check(L.lib.ds_engine_get_params(e, params.ctypes.data))
+    loss = np.zeros(hp.i_max)
+    ex = np.zeros(hp.i_max, np.uint8)
+    L.check(L.lib.ds_engine_log(e, 0, hp.i_max, loss.ctypes.data, None, ex.ctypes.data, None))
+    snap = np.zeros_like(w)
+    L.check(L.lib.ds_master_snapshot(mst, snap.ctypes.data))
+    L.lib.ds_engine_destroy(e)
+    L.lib.ds_master_destroy(mst)
+    ref = orc.run_training_loop(m, X, y, c, hp, 99, w, exchange_mode=2, master=w)
+    assert list(ex) == list(ref["exchanged"])
+    tol = 1e-5 if mode == "exact" else 5e-3
+    assert np.allclose(loss, ref["batch_loss"], rtol=tol, atol=0)
+    scale = np.abs(w).max()
+    assert np.abs(params - ref["final_params"]).max() <= tol * scale
+    assert np.abs(snap - ref["master"]).max() <= tol * scale
