@@ -2,17 +2,22 @@
 // DS_MODEL_ALEXNET; NOT IN THE REFERENCE, f64 oracle in
 // oracle/ds_oracle_alex.c). loss_and_grad for R rows.
 //
-// Layout: activations NHWC ([rows][y][x][c], channels contiguous), so every contraction is
-// a K-major GEMM on the tcgen05 tensor cores (gemm_tc.cu, tf32 with f32 accumulation):
-//   conv forward   col[M = R*Ho*Wo][g][ky][kx][cg] . Wp_g[Cout_g][ky][kx][cg]^T   (im2col)
-//   conv dgrad     dc_g[M][Cout_g] . WpT_g[K_g][Cout_g]^T -> dcol, then col2im (gather)
-//   conv wgrad     dcT_g[Cout_g][M] . colT_g[K_g][M]^T     (split-K over the pixels)
-//   fc forward     h[R][in] . W[out][in]^T ; dgrad dh . WT^T ; wgrad dhT . hT^T
-// conv1 reads the CHW input rows directly (k order = Caffe's (c, ky, kx)); conv2-5 use
-// (ky, kx, c) and their weights are repacked each step (tiny). LRN, max-pooling, ReLU
-// masks, softmax cross-entropy and the bias sums are HBM-bound elementwise kernels.
-// The gradient is the batch mean (scale 1/R in the GEMM epilogues), rounded to f32 like
-// the reference's Grad = f32(sum / b). Dropout is omitted (deterministic; see the oracle).
+// Every contraction is a tcgen05 GEMM (gemm_tc.cu, tf32 operands, f32 accumulation in
+// TMEM). Activations are NHWC ([rows][y][x][c], channels contiguous); the inputs of
+// conv2..conv5 live in spatially zero-padded maps (border = the conv's padding), so a
+// convolution is an implicit GEMM whose K loop walks the filter taps: tap (ky, kx) reads
+// the A tile at the pixel shift (ky-p)*Hp + (kx-p) (a TMA row coordinate), no im2col
+// matrix is written. Outputs are computed on the padded grid; the epilogue keeps interior
+// rows only. Per conv layer (group g, KK taps):
+//   forward  out[o] = sum_t in[o + d_t] . Wp_g[t]^T          (taps accumulate)
+//   dgrad    din[i] = sum_t dout[i - d_t] . WpT_g[t]^T       (taps accumulate, ReLU mask)
+//   wgrad    dW[t]  = doutT . inT(shifted by d_t)^T           (one output per tap, split-K)
+// wgrad contracts over pixels, so it reads transposed (pixel-contiguous) copies of dout and
+// the padded input: tf32 MMA operands must be K-major. conv1 (11x11 stride 4 on the CHW
+// input) keeps an explicit im2col. LRN, max-pooling, softmax cross-entropy and the bias
+// sums are HBM-bound elementwise kernels. The gradient is the batch mean (scale 1/R in the
+// GEMM epilogues), rounded to f32 like the reference's Grad = f32(sum / b). Dropout is
+// omitted (deterministic; see the oracle).
 #include <algorithm>
 
 #include "ds_common.cuh"
@@ -22,10 +27,10 @@
 namespace dsb {
 namespace {
 
+thread_local uint32_t t_launches = 0;  // kernels issued by the last loss_and_grad on this thread
+
 constexpr float kLrnAlpha = 1e-4f, kLrnBeta = 0.75f, kLrnK = 1.f;
 constexpr int kLrnN = 5;
-
-thread_local uint32_t t_launches = 0;  // kernels issued by the last loss_and_grad on this thread
 
 inline unsigned nblk(uint64_t n, unsigned t = 256) {
   return static_cast<unsigned>(std::min<uint64_t>((n + t - 1) / t, 148ull * 64));
@@ -34,48 +39,56 @@ inline uint32_t up4(uint32_t v) { return (v + 3) & ~3u; }
 
 struct Shape {
   uint32_t S, H1, P1, P2, P5, C, Cp;
-  uint64_t q5;  // fc6 fan-in
+  uint32_t Hp2, Hp3;  // padded sides of the conv2 input (pad 2) and the conv3..5 maps (pad 1)
+  uint64_t q5;        // fc6 fan-in
 };
 
 Shape shape_of(const ModelInfo& m) {
   Shape s{};
   s.S = m.alex_side;
   s.H1 = (s.S - 11) / 4 + 1;
-  auto pooled = [](uint32_t h) { return (h - 3 + 1) / 2 + 1; };  // ceil((h-3)/2)+1
+  auto pooled = [](uint32_t h) { return (h - 2) / 2 + 1; };  // ceil((h-3)/2)+1
   s.P1 = pooled(s.H1);
   s.P2 = pooled(s.P1);
   s.P5 = pooled(s.P2);
   s.C = m.n_classes;
   s.Cp = up4(s.C);
+  s.Hp2 = s.P1 + 4;
+  s.Hp3 = s.P2 + 2;
   s.q5 = 256ull * s.P5 * s.P5;
   return s;
 }
 
-// one conv layer of conv2..5 (NHWC input)
+// conv2..5 (stride 1, same padding, NHWC)
 struct ConvSpec {
-  uint32_t Cin, Cout, K, pad, g, H;  // H = input side = output side (stride 1, same padding)
+  uint32_t Cin, Cout, K, pad, g, H, Hp;
   uint32_t cig() const { return Cin / g; }
   uint32_t cog() const { return Cout / g; }
+  uint32_t KK() const { return K * K; }
   uint32_t Kg() const { return K * K * cig(); }
 };
 
-// ---- workspace ---------------------------------------------------------------------
-struct AlexWs {
-  float *a1, *n1, *p1, *a2, *n2, *p2, *a3, *a4, *a5, *p5, *h6, *h7, *z, *dz;
-  uint8_t *arg1, *arg2, *arg5;
-  float *dh7, *dh6, *dp5, *dA, *dB;  // dA/dB: ping-pong gradient maps (largest layer)
-  float *col, *tr, *part, *wtmp, *bpart;
-  float *w1p, *wp[4], *wpT[4], *w6T, *w7T, *w8T, *zT, *h7T, *h6T, *p5T, *dh7T, *dh6T;
-  double* loss_rows;
-};
-
-const ConvSpec kConv[4] = {{96, 256, 5, 2, 2, 0}, {256, 384, 3, 1, 1, 0}, {384, 384, 3, 1, 2, 0}, {384, 256, 3, 1, 2, 0}};
-
 ConvSpec conv_spec(const Shape& s, int l) {  // l = 0..3 -> conv2..conv5
+  static const ConvSpec kConv[4] = {{96, 256, 5, 2, 2, 0, 0}, {256, 384, 3, 1, 1, 0, 0}, {384, 384, 3, 1, 2, 0, 0},
+                                    {384, 256, 3, 1, 2, 0, 0}};
   ConvSpec c = kConv[l];
   c.H = l == 0 ? s.P1 : s.P2;
+  c.Hp = l == 0 ? s.Hp2 : s.Hp3;
   return c;
 }
+
+// ---- workspace ---------------------------------------------------------------------
+struct AlexWs {
+  // forward maps (p = spatially padded, zero border)
+  float *a1, *n1, *p1p, *a2, *n2, *p2p, *a3p, *a4p, *a5p, *p5, *h6, *h7, *z, *dz;
+  uint8_t *arg1, *arg2, *arg5;
+  // backward
+  float *dh7, *dh6, *dp5, *dc5p, *dc4p, *dc3p, *dp2p, *dn2, *dc2p, *dp1, *dn1, *dc1;
+  float *col, *trA, *trB, *part, *wtmp, *bpart;
+  float *w1p, *wp[4], *wpT[4], *w6T, *w7T, *w8T, *zT, *h7T, *h6T, *p5T, *dh7T, *dh6T;
+  double* loss_rows;
+  uint64_t end;
+};
 
 constexpr uint64_t kPartFloats = 24ull << 20;  // split-K slabs
 
@@ -84,22 +97,24 @@ AlexWs carve_ws(const ModelInfo& m, uint32_t R, void* base) {
   AlexWs ws{};
   uint8_t* b = static_cast<uint8_t*>(base);
   const Shape s = shape_of(m);
-  const uint64_t A1 = 1ull * R * s.H1 * s.H1 * 96, Q1 = 1ull * R * s.P1 * s.P1 * 96, A2 = 1ull * R * s.P1 * s.P1 * 256,
-                 Q2 = 1ull * R * s.P2 * s.P2 * 256, A3 = 1ull * R * s.P2 * s.P2 * 384, Q5 = R * s.q5;
   const uint64_t M1 = 1ull * R * s.H1 * s.H1, M2 = 1ull * R * s.P1 * s.P1, M3 = 1ull * R * s.P2 * s.P2;
-  const uint64_t col = std::max({up4(static_cast<uint32_t>(M1)) * 364ull, up4(static_cast<uint32_t>(M2)) * 2400ull,
-                                 up4(static_cast<uint32_t>(M3)) * 3456ull});
-  const uint64_t tr = std::max({96 * (M1 + 4), 256 * (M2 + 4), 384 * (M3 + 4)});
+  const uint64_t G2 = 1ull * R * s.Hp2 * s.Hp2, G3 = 1ull * R * s.Hp3 * s.Hp3;  // padded grids
+  const uint64_t Q5 = R * s.q5;
   const uint32_t Rp = up4(R);
   uint64_t off = 0;
   auto f = [&](float*& p, uint64_t n) { p = reinterpret_cast<float*>(b + off); off += (n * 4 + 255) & ~255ull; };
   auto u = [&](uint8_t*& p, uint64_t n) { p = b + off; off += (n + 255) & ~255ull; };
-  f(ws.a1, A1), f(ws.n1, A1), f(ws.p1, Q1), u(ws.arg1, Q1);
-  f(ws.a2, A2), f(ws.n2, A2), f(ws.p2, Q2), u(ws.arg2, Q2);
-  f(ws.a3, A3), f(ws.a4, A3), f(ws.a5, Q2), f(ws.p5, Q5), u(ws.arg5, Q5);
+  f(ws.a1, M1 * 96), f(ws.n1, M1 * 96), f(ws.p1p, G2 * 96), u(ws.arg1, M2 * 96);
+  f(ws.a2, M2 * 256), f(ws.n2, M2 * 256), f(ws.p2p, G3 * 256), u(ws.arg2, M3 * 256);
+  f(ws.a3p, G3 * 384), f(ws.a4p, G3 * 384), f(ws.a5p, G3 * 256), f(ws.p5, Q5), u(ws.arg5, Q5);
   f(ws.h6, 4096ull * R), f(ws.h7, 4096ull * R), f(ws.z, 1ull * s.Cp * R), f(ws.dz, 1ull * s.Cp * R);
-  f(ws.dh7, 4096ull * R), f(ws.dh6, 4096ull * R), f(ws.dp5, Q5), f(ws.dA, A1), f(ws.dB, A1);
-  f(ws.col, col), f(ws.tr, tr), f(ws.part, kPartFloats), f(ws.wtmp, 384ull * 2304), f(ws.bpart, 4096ull * 512);
+  f(ws.dh7, 4096ull * R), f(ws.dh6, 4096ull * R), f(ws.dp5, Q5);
+  f(ws.dc5p, G3 * 256), f(ws.dc4p, G3 * 384), f(ws.dc3p, G3 * 384), f(ws.dp2p, G3 * 256), f(ws.dn2, M2 * 256);
+  f(ws.dc2p, G2 * 256), f(ws.dp1, M2 * 96), f(ws.dn1, M1 * 96), f(ws.dc1, M1 * 96);
+  f(ws.col, 1ull * up4(static_cast<uint32_t>(M1)) * 364);
+  const uint64_t trA = std::max({384 * (G3 + 4), 256 * (G2 + 4), 96 * (M1 + 4)});
+  const uint64_t trB = 4 * std::max({384 * (G3 + 4), 96 * (G2 + 4)});
+  f(ws.trA, trA), f(ws.trB, trB), f(ws.part, kPartFloats), f(ws.wtmp, 384ull * 2304), f(ws.bpart, 4096ull * 512);
   f(ws.w1p, 96ull * 364);
   for (int l = 0; l < 4; ++l) {
     const ConvSpec c = conv_spec(s, l);
@@ -111,14 +126,8 @@ AlexWs carve_ws(const ModelInfo& m, uint32_t R, void* base) {
   f(ws.dh7T, 4096ull * Rp), f(ws.dh6T, 4096ull * Rp);
   ws.loss_rows = reinterpret_cast<double*>(b + off);
   off += (R * 8ull + 255) & ~255ull;
-  (void)off;
+  ws.end = off;
   return ws;
-}
-
-uint64_t ws_bytes(const ModelInfo& m, uint32_t R) {
-  // size = end offset of carve_ws's last buffer: carve against a null base
-  AlexWs w = carve_ws(m, R, nullptr);
-  return reinterpret_cast<uint64_t>(w.loss_rows) + ((R * 8ull + 255) & ~255ull);
 }
 
 // ---- kernels -------------------------------------------------------------------------
@@ -163,98 +172,6 @@ __global__ void im2colT_conv1_kernel(const float* __restrict__ X, const uint32_t
   }
 }
 
-// NHWC im2col, stride 1, same padding: col[m][g][ky][kx][cg] (ld = g*K*K*cg); float4 over c
-__global__ void im2col_nhwc_kernel(const float* __restrict__ in, uint32_t R, uint32_t H, uint32_t Cin, uint32_t K,
-                                   uint32_t pad, uint32_t g, float* __restrict__ col, const uint32_t* gate) {
-  GATE;
-  const uint32_t cg = Cin / g, cg4 = cg / 4, KK = K * K;
-  const uint64_t ld = 1ull * g * KK * cg;
-  const uint64_t total = 1ull * R * H * H * g * KK * cg4;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint32_t c4 = static_cast<uint32_t>(i % cg4);
-    uint64_t t = i / cg4;
-    const uint32_t kk = static_cast<uint32_t>(t % KK);
-    t /= KK;
-    const uint32_t gi = static_cast<uint32_t>(t % g);
-    const uint64_t m = t / g;
-    const uint32_t x = static_cast<uint32_t>(m % H), y = static_cast<uint32_t>((m / H) % H);
-    const uint64_t r = m / (1ull * H * H);
-    const int iy = static_cast<int>(y + kk / K) - static_cast<int>(pad), ix = static_cast<int>(x + kk % K) - static_cast<int>(pad);
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (iy >= 0 && iy < static_cast<int>(H) && ix >= 0 && ix < static_cast<int>(H))
-      v = __ldg(reinterpret_cast<const float4*>(in + ((r * H + iy) * H + ix) * Cin + gi * cg) + c4);
-    *reinterpret_cast<float4*>(col + m * ld + (1ull * gi * KK + kk) * cg + c4 * 4) = v;
-  }
-}
-
-// NHWC im2col transposed for one group: colT[k][m] (k = (ky*K+kx)*cg + c, ld ldT).
-// 32x32 smem tile: read along c (coalesced), write along m (coalesced).
-__global__ void im2colT_nhwc_kernel(const float* __restrict__ in, uint32_t R, uint32_t H, uint32_t Cin, uint32_t K,
-                                    uint32_t pad, uint32_t g, uint32_t gi, uint64_t ldT, float* __restrict__ colT,
-                                    const uint32_t* gate) {
-  GATE;
-  __shared__ float tile[32][33];
-  const uint32_t cg = Cin / g, Kg = K * K * cg;
-  const uint64_t M = 1ull * R * H * H;
-  const uint64_t m0 = blockIdx.x * 32ull;
-  const uint32_t k0 = blockIdx.y * 32;
-  // load: thread (ty, tx): m = m0 + ty (rows 0..31 in steps of 8), k = k0 + tx
-  for (uint32_t ty = threadIdx.y; ty < 32; ty += 8) {
-    const uint64_t m = m0 + ty;
-    const uint32_t k = k0 + threadIdx.x;
-    float v = 0.f;
-    if (m < M && k < Kg) {
-      const uint32_t c = k % cg, kk = k / cg;
-      const uint32_t x = static_cast<uint32_t>(m % H), y = static_cast<uint32_t>((m / H) % H);
-      const uint64_t r = m / (1ull * H * H);
-      const int iy = static_cast<int>(y + kk / K) - static_cast<int>(pad), ix = static_cast<int>(x + kk % K) - static_cast<int>(pad);
-      if (iy >= 0 && iy < static_cast<int>(H) && ix >= 0 && ix < static_cast<int>(H))
-        v = __ldg(in + ((r * H + iy) * H + ix) * Cin + gi * cg + c);
-    }
-    tile[ty][threadIdx.x] = v;
-  }
-  __syncthreads();
-  for (uint32_t ty = threadIdx.y; ty < 32; ty += 8) {
-    const uint32_t k = k0 + ty;
-    const uint64_t m = m0 + threadIdx.x;
-    if (k < Kg && m < M) colT[k * ldT + m] = tile[threadIdx.x][ty];
-  }
-}
-
-// col2im (gather) for stride-1 same-padding convs: dX[r][y][x][c] = sum over (ky, kx) of
-// dcol[(r, y+pad-ky, x+pad-kx)][g][ky][kx][c'] ; optional ReLU mask (forward activation)
-__global__ void col2im_nhwc_kernel(const float* __restrict__ dcol, uint32_t R, uint32_t H, uint32_t Cin, uint32_t K,
-                                   uint32_t pad, uint32_t g, const float* __restrict__ mask, float* __restrict__ dX,
-                                   const uint32_t* gate) {
-  GATE;
-  const uint32_t cg = Cin / g, KK = K * K;
-  const uint64_t ld = 1ull * g * KK * cg;
-  const uint64_t total = 1ull * R * H * H * Cin;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint32_t c = static_cast<uint32_t>(i % Cin);
-    const uint64_t p = i / Cin;
-    if (mask && !(mask[i] > 0.f)) {
-      dX[i] = 0.f;
-      continue;
-    }
-    const uint32_t x = static_cast<uint32_t>(p % H), y = static_cast<uint32_t>((p / H) % H);
-    const uint64_t r = p / (1ull * H * H);
-    const uint32_t gi = c / cg, cc = c % cg;
-    float s = 0.f;
-    for (uint32_t ky = 0; ky < K; ++ky) {
-      const int oy = static_cast<int>(y + pad) - static_cast<int>(ky);
-      if (oy < 0 || oy >= static_cast<int>(H)) continue;
-      for (uint32_t kx = 0; kx < K; ++kx) {
-        const int ox = static_cast<int>(x + pad) - static_cast<int>(kx);
-        if (ox < 0 || ox >= static_cast<int>(H)) continue;
-        const uint64_t m = (r * H + oy) * H + ox;
-        s += dcol[m * ld + (1ull * gi * KK + ky * K + kx) * cg + cc];
-      }
-    }
-    dX[i] = s;
-  }
-}
-
 // out[c][r] = in[r][c] for a [rows x cols] matrix (ld_in, ld_out), 32x32 tiles
 __global__ void transpose_kernel(const float* __restrict__ in, uint64_t rows, uint32_t cols, uint64_t ld_in,
                                  float* __restrict__ out, uint64_t ld_out, const uint32_t* gate) {
@@ -275,7 +192,30 @@ __global__ void transpose_kernel(const float* __restrict__ in, uint64_t rows, ui
   }
 }
 
-// Caffe conv weight [Cout][cg][K][K] -> Wp [Cout][K][K][cg] and per group WpT_g [Kg][Cout_g]
+// Four pixel-shifted transposed copies: out[s][c][m] = in[m + s][c] (0 past the last row),
+// m < ldT. TMA needs 16-byte aligned inner coordinates, so a weight-gradient tap with pixel
+// shift d reads copy (d mod 4) at the aligned offset d - (d mod 4).
+__global__ void transpose_shift4_kernel(const float* __restrict__ in, uint64_t rows, uint32_t cols,
+                                        float* __restrict__ out, uint64_t ldT, const uint32_t* gate) {
+  GATE;
+  __shared__ float tile[35][33];
+  const uint64_t r0 = blockIdx.x * 32ull;
+  const uint32_t c0 = blockIdx.y * 32;
+  for (uint32_t ty = threadIdx.y; ty < 35; ty += 8) {
+    const uint64_t r = r0 + ty;
+    const uint32_t c = c0 + threadIdx.x;
+    tile[ty][threadIdx.x] = (r < rows && c < cols) ? in[r * cols + c] : 0.f;
+  }
+  __syncthreads();
+  for (uint32_t sft = 0; sft < 4; ++sft)
+    for (uint32_t ty = threadIdx.y; ty < 32; ty += 8) {
+      const uint32_t c = c0 + ty;
+      const uint64_t m = r0 + threadIdx.x;
+      if (c < cols && m < ldT) out[(sft * cols + c) * ldT + m] = tile[threadIdx.x + sft][ty];
+    }
+}
+
+// Caffe conv weight [Cout][cg][K][K] -> Wp [Cout][K*K][cg] and per group WpT_g [K*K][cg][Cout_g]
 __global__ void pack_conv_kernel(const float* __restrict__ W, uint32_t Cout, uint32_t cg, uint32_t K, uint32_t g,
                                  float* __restrict__ Wp, float* __restrict__ WpT, const uint32_t* gate) {
   GATE;
@@ -301,67 +241,97 @@ __global__ void pack_conv1_kernel(const float* __restrict__ W, float* __restrict
   }
 }
 
-// packed weight gradient [Cout_g][(ky,kx,c)] of group gi -> Caffe order in grad
-__global__ void unpack_wgrad_kernel(const float* __restrict__ dWp, uint32_t cog, uint32_t cg, uint32_t K, uint32_t gi,
-                                    float* __restrict__ grad, const uint32_t* gate) {
+// packed weight gradient [Cout][(ky,kx,c)] -> Caffe order [Cout][c][ky][kx]
+__global__ void unpack_wgrad_kernel(const float* __restrict__ dWp, uint32_t rows, uint32_t cg, uint32_t K,
+                                    float* __restrict__ grad, uint32_t* flags, const uint32_t* gate) {
   GATE;
   const uint32_t KK = K * K, Kg = KK * cg;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < 1ull * cog * Kg; i += gridDim.x * 256ull) {
-    const uint32_t col = static_cast<uint32_t>(i / Kg), k = static_cast<uint32_t>(i % Kg);
+  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < 1ull * rows * Kg; i += gridDim.x * 256ull) {
+    const uint32_t co = static_cast<uint32_t>(i / Kg), k = static_cast<uint32_t>(i % Kg);
     const uint32_t kk = k / cg, c = k % cg;
-    grad[(1ull * (gi * cog + col) * cg + c) * KK + kk] = dWp[i];
+    const float v = dWp[i];
+    if (!isfinite(v)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
+    grad[(1ull * co * cg + c) * KK + kk] = v;
   }
 }
 
-// LRN across channels (NHWC): y = x * (k + a/n sum_{|c'-c|<=2} x_c'^2)^-b
+// LRN across channels (NHWC, 4 channels per thread): y = x * (k + a/n sum_{|c'-c|<=2} x_c'^2)^-b
 __global__ void lrn_fwd_kernel(const float* __restrict__ x, uint64_t pixels, uint32_t C, float* __restrict__ y,
                                const uint32_t* gate) {
   GATE;
-  const uint64_t total = pixels * C;
+  const uint32_t C4 = C / 4;
+  const uint64_t total = pixels * C4;
   for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint32_t c = static_cast<uint32_t>(i % C);
-    const float* px = x + (i - c);
-    float ss = 0.f;
-    const int lo = max(0, static_cast<int>(c) - kLrnN / 2), hi = min(static_cast<int>(C) - 1, static_cast<int>(c) + kLrnN / 2);
-    for (int j = lo; j <= hi; ++j) ss += px[j] * px[j];
-    const float sc = kLrnK + kLrnAlpha / kLrnN * ss;
-    y[i] = px[c] * __powf(sc, -kLrnBeta);
+    const uint32_t c0 = static_cast<uint32_t>(i % C4) * 4;
+    const float* px = x + (i / C4) * C;
+    float v[8];  // x[c0-2 .. c0+5]
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = static_cast<int>(c0) - 2 + j;
+      v[j] = (c >= 0 && c < static_cast<int>(C)) ? __ldg(px + c) : 0.f;
+    }
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float ss = v[j] * v[j] + v[j + 1] * v[j + 1] + v[j + 2] * v[j + 2] + v[j + 3] * v[j + 3] + v[j + 4] * v[j + 4];
+      o[j] = v[j + 2] * __powf(kLrnK + kLrnAlpha / kLrnN * ss, -kLrnBeta);
+    }
+    *reinterpret_cast<float4*>(y + (i / C4) * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
-// LRN backward, scale recomputed from x; the result is masked by ReLU (x = relu output > 0)
-__global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __restrict__ dy, uint64_t pixels,
-                                    uint32_t C, float* __restrict__ dx, const uint32_t* gate) {
+// LRN backward (scale recomputed from x), masked by the ReLU that produced x (x > 0):
+// dx_c = dy_c s_c^-b - (2 a b / n) x_c sum_{|j-c|<=2} dy_j x_j s_j^(-b-1)
+// dx is written at the same pixel of a map padded by `opad` (side H + 2 opad).
+__global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __restrict__ dy, uint32_t R, uint32_t H,
+                                    uint32_t C, uint32_t opad, float* __restrict__ dx, const uint32_t* gate) {
   GATE;
-  const uint64_t total = pixels * C;
+  const uint32_t C4 = C / 4, Ho = H + 2 * opad;
+  const uint64_t total = 1ull * R * H * H * C4;
   for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint32_t c = static_cast<uint32_t>(i % C);
-    const float* px = x + (i - c);
-    const float* pd = dy + (i - c);
-    if (!(px[c] > 0.f)) {
-      dx[i] = 0.f;
-      continue;
+    const uint32_t c0 = static_cast<uint32_t>(i % C4) * 4;
+    const uint64_t p = i / C4;
+    const float* px = x + p * C;
+    const float* pd = dy + p * C;
+    float xv[12], w[8], pw[8];  // x[c0-4 .. c0+7]; per j in [c0-2, c0+5]: dy x s^(-b-1), s^-b
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      const int c = static_cast<int>(c0) - 4 + j;
+      xv[j] = (c >= 0 && c < static_cast<int>(C)) ? __ldg(px + c) : 0.f;
     }
-    float acc = 0.f, own = 0.f;
-    const int lo = max(0, static_cast<int>(c) - kLrnN / 2), hi = min(static_cast<int>(C) - 1, static_cast<int>(c) + kLrnN / 2);
-    for (int j = lo; j <= hi; ++j) {
-      const int l2 = max(0, j - kLrnN / 2), h2 = min(static_cast<int>(C) - 1, j + kLrnN / 2);
-      float ss = 0.f;
-      for (int t = l2; t <= h2; ++t) ss += px[t] * px[t];
-      const float sc = kLrnK + kLrnAlpha / kLrnN * ss;
-      const float p = __powf(sc, -kLrnBeta);
-      if (j == static_cast<int>(c)) own = p;
-      acc += pd[j] * px[j] * p / sc;  // dy_j * y_j / scale_j
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = static_cast<int>(c0) - 2 + j;
+      const float ss = xv[j] * xv[j] + xv[j + 1] * xv[j + 1] + xv[j + 2] * xv[j + 2] + xv[j + 3] * xv[j + 3] +
+                       xv[j + 4] * xv[j + 4];
+      const float s = kLrnK + kLrnAlpha / kLrnN * ss;
+      const float sb = __powf(s, -kLrnBeta);
+      pw[j] = sb;
+      const float d = (c >= 0 && c < static_cast<int>(C)) ? __ldg(pd + c) : 0.f;
+      w[j] = d * xv[j + 2] * sb / s;
     }
-    dx[i] = pd[c] * own - 2.f * kLrnAlpha * kLrnBeta / kLrnN * px[c] * acc;
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float xc = xv[j + 4];
+      const float acc = w[j] + w[j + 1] + w[j + 2] + w[j + 3] + w[j + 4];
+      const float d = __ldg(pd + c0 + j);
+      o[j] = xc > 0.f ? d * pw[j + 2] - 2.f * kLrnAlpha * kLrnBeta / kLrnN * xc * acc : 0.f;
+    }
+    const uint32_t xx = static_cast<uint32_t>(p % H), yy = static_cast<uint32_t>((p / H) % H);
+    const uint64_t r = p / (1ull * H * H);
+    *reinterpret_cast<float4*>(dx + ((r * Ho + yy + opad) * Ho + xx + opad) * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
-// MAX 3x3/2 ceil-mode (NHWC in); out NHWC, or per-row CHW when chw != 0 (fc6 input).
-// arg = window position (0..8) of the first maximum in scan order.
+// MAX 3x3/2 ceil-mode over an NHWC map (input padded by ipad, output padded by opad, or
+// per-row CHW when chw != 0: the fc6 input). arg[r][py][px][c] (unpadded) = window position
+// (0..8) of the first maximum in scan order.
 __global__ void maxpool_fwd_kernel(const float* __restrict__ in, uint32_t R, uint32_t H, uint32_t C, uint32_t Ho,
-                                   int chw, float* __restrict__ out, uint8_t* __restrict__ arg, const uint32_t* gate) {
+                                   uint32_t ipad, uint32_t opad, int chw, float* __restrict__ out,
+                                   uint8_t* __restrict__ arg, const uint32_t* gate) {
   GATE;
+  const uint32_t Hi = H + 2 * ipad, Hq = Ho + 2 * opad;
   const uint64_t total = 1ull * R * Ho * Ho * C;
   for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
     const uint32_t c = static_cast<uint32_t>(i % C);
@@ -373,38 +343,42 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ in, uint32_t R, uin
     uint32_t bi = 0;
     for (uint32_t h = hs; h < he; ++h)
       for (uint32_t w = ws; w < we; ++w) {
-        const float v = in[((r * H + h) * H + w) * C + c];
+        const float v = in[((r * Hi + h + ipad) * Hi + w + ipad) * C + c];
         if (v > best) best = v, bi = (h - hs) * 3 + (w - ws);
       }
-    const uint64_t o = chw ? (r * C + c) * Ho * Ho + py * Ho + px : i;
+    const uint64_t o = chw ? (r * C + c) * Ho * Ho + py * Ho + px : ((r * Hq + py + opad) * Hq + px + opad) * C + c;
     out[o] = best;
-    arg[o] = static_cast<uint8_t>(bi);
+    arg[i] = static_cast<uint8_t>(bi);
   }
 }
 
-// gather form of the max-pool backward: din[r][y][x][c] = sum of dout over the windows
-// whose maximum sat at (y, x); optional ReLU mask (x > 0 of the pooled map's source)
+// gather form of the max-pool backward: din[r][y][x][c] = sum of dout over the windows whose
+// maximum sat at (y, x). dout: padded by opad (or per-row CHW), din/mask: padded by ipad;
+// mask (optional) zeroes din where the pooled map's source was not > 0 (ReLU).
 __global__ void maxpool_bwd_kernel(const float* __restrict__ dout, const uint8_t* __restrict__ arg, uint32_t R,
-                                   uint32_t H, uint32_t C, uint32_t Ho, int chw, const float* __restrict__ mask,
-                                   float* __restrict__ din, const uint32_t* gate) {
+                                   uint32_t H, uint32_t C, uint32_t Ho, uint32_t opad, int chw, uint32_t ipad,
+                                   const float* __restrict__ mask, float* __restrict__ din, const uint32_t* gate) {
   GATE;
+  const uint32_t Hi = H + 2 * ipad, Hq = Ho + 2 * opad;
   const uint64_t total = 1ull * R * H * H * C;
   for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
     const uint32_t c = static_cast<uint32_t>(i % C);
     const uint64_t p = i / C;
     const uint32_t x = static_cast<uint32_t>(p % H), y = static_cast<uint32_t>((p / H) % H);
     const uint64_t r = p / (1ull * H * H);
+    const uint64_t di = ((r * Hi + y + ipad) * Hi + x + ipad) * C + c;
     float s = 0.f;
-    if (!mask || mask[i] > 0.f) {
+    if (!mask || mask[di] > 0.f) {
       const uint32_t py0 = y >= 2 ? (y - 1) / 2 : 0, py1 = min(y / 2, Ho - 1);
       const uint32_t px0 = x >= 2 ? (x - 1) / 2 : 0, px1 = min(x / 2, Ho - 1);
       for (uint32_t py = py0; py <= py1; ++py)
         for (uint32_t px = px0; px <= px1; ++px) {
-          const uint64_t o = chw ? (r * C + c) * Ho * Ho + py * Ho + px : ((r * Ho + py) * Ho + px) * C + c;
-          if (arg[o] == (y - py * 2) * 3 + (x - px * 2)) s += dout[o];
+          const uint64_t a = ((r * Ho + py) * Ho + px) * C + c;
+          if (arg[a] == (y - py * 2) * 3 + (x - px * 2))
+            s += dout[chw ? (r * C + c) * Ho * Ho + py * Ho + px : ((r * Hq + py + opad) * Hq + px + opad) * C + c];
         }
     }
-    din[i] = s;
+    din[di] = s;
   }
 }
 
@@ -473,114 +447,7 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, uint32_t npa
   }
 }
 
-// ---- host helpers --------------------------------------------------------------------
-struct Ctx {
-  cudaStream_t s;
-  const uint32_t* gate;
-  float* part;
-  uint32_t* flags;
-};
-
-// splits so that tiles * splits covers the SMs, each split >= 4 k-steps, slabs fit `part`
-uint32_t pick_splits(uint32_t M, uint32_t N, uint32_t K) {
-  const uint32_t bn = gemm_pick_bn(N);
-  const uint64_t tiles = 1ull * ((N + bn - 1) / bn) * ((M + 127) / 128);
-  if (tiles >= 148) return 1;
-  uint32_t sp = static_cast<uint32_t>((148 + tiles - 1) / tiles);
-  sp = std::min<uint32_t>(sp, std::max<uint32_t>(1, K / 128));
-  while (sp > 1 && 1ull * sp * M * N > kPartFloats) --sp;
-  return sp;
-}
-
-int gemm(const Ctx& c, const float* A, uint64_t lda, const float* B, uint64_t ldb, float* D, uint64_t ldd, uint32_t M,
-         uint32_t N, uint32_t K, float scale, const float* bias_n, bool relu, const float* mask = nullptr,
-         uint64_t ldm = 0, bool allow_split = true) {
-  GemmEpilogue ep;
-  ep.D = D;
-  ep.ldd = ldd;
-  ep.scale = scale;
-  ep.bias_n = bias_n;
-  ep.relu = relu;
-  ep.mask = mask;
-  ep.ldm = ldm;
-  ep.gate = c.gate;
-  const uint32_t sp = allow_split ? pick_splits(M, N, K) : 1;
-  t_launches += sp > 1 ? 2 : 1;
-  return launch_gemm_tf32(A, lda, B, ldb, M, N, K, ep, sp, c.part, c.s);
-}
-
-int transpose(const Ctx& c, const float* in, uint64_t rows, uint32_t cols, uint64_t ld_in, float* out, uint64_t ld_out) {
-  dim3 grid(static_cast<unsigned>((rows + 31) / 32), (cols + 31) / 32);
-  transpose_kernel<<<grid, dim3(32, 8), 0, c.s>>>(in, rows, cols, ld_in, out, ld_out, c.gate); ++t_launches;
-  DS_CUDA_TRY(cudaGetLastError());
-  return DS_OK;
-}
-
-int colsum(const Ctx& c, const float* d, uint64_t rows, uint32_t N, uint64_t ld, float scale, float* out, float* bpart) {
-  const uint32_t nparts = static_cast<uint32_t>(std::min<uint64_t>(512, std::max<uint64_t>(1, rows / 64)));
-  const uint64_t rpb = (rows + nparts - 1) / nparts;
-  dim3 grid((N + 127) / 128, nparts);
-  colsum_part_kernel<<<grid, 128, 0, c.s>>>(d, rows, N, ld, rpb, bpart, c.gate); ++t_launches;
-  colsum_final_kernel<<<(N + 127) / 128, 128, 0, c.s>>>(bpart, nparts, N, scale, out, c.flags, c.gate); ++t_launches;
-  DS_CUDA_TRY(cudaGetLastError());
-  return DS_OK;
-}
-
-}  // namespace
-
-uint64_t alex_workspace_bytes(const ModelInfo& m, uint32_t R) { return ws_bytes(m, R); }
-uint32_t alex_last_launches() { return t_launches; }
-
-namespace {
-
-// forward to the logits w.z [R x Cp]
-int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint32_t* idx, uint32_t R, AlexWs& w,
-                 const Ctx& c) {
-  const Shape sh = shape_of(m);
-  const auto& L = m.layers;
-  const uint32_t F = m.n_features;
-  const uint64_t M1 = 1ull * R * sh.H1 * sh.H1, M2 = 1ull * R * sh.P1 * sh.P1, M3 = 1ull * R * sh.P2 * sh.P2;
-  cudaStream_t s = c.s;
-  const uint32_t* gate = c.gate;
-  pack_conv1_kernel<<<nblk(96 * 364), 256, 0, s>>>(P + L[0].w_off, w.w1p, gate); ++t_launches;
-  for (int l = 0; l < 4; ++l) {
-    const ConvSpec cs = conv_spec(sh, l);
-    pack_conv_kernel<<<nblk(1ull * cs.Cout * cs.Kg()), 256, 0, s>>>(P + L[l + 1].w_off, cs.Cout, cs.cig(), cs.K, cs.g,
-                                                                   w.wp[l], w.wpT[l], gate); ++t_launches;
-  }
-  // conv1 + relu
-  im2col_conv1_kernel<<<nblk(M1 * 364), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, M1, w.col, gate); ++t_launches;
-  DS_TRY(gemm(c, w.col, 364, w.w1p, 364, w.a1, 96, static_cast<uint32_t>(M1), 96, 364, 1.f, P + L[0].b_off, true));
-  lrn_fwd_kernel<<<nblk(M1 * 96), 256, 0, s>>>(w.a1, M1, 96, w.n1, gate); ++t_launches;
-  maxpool_fwd_kernel<<<nblk(M2 * 96), 256, 0, s>>>(w.n1, R, sh.H1, 96, sh.P1, 0, w.p1, w.arg1, gate); ++t_launches;
-  // conv2..5
-  const float* in_act[4] = {w.p1, w.p2, w.a3, w.a4};
-  float* out_act[4] = {w.a2, w.a3, w.a4, w.a5};
-  for (int l = 0; l < 4; ++l) {
-    const ConvSpec cs = conv_spec(sh, l);
-    const uint64_t Mx = l == 0 ? M2 : M3;
-    const uint32_t Kg = cs.Kg(), ldc = Kg * cs.g;
-    im2col_nhwc_kernel<<<nblk(Mx * ldc / 4), 256, 0, s>>>(in_act[l], R, cs.H, cs.Cin, cs.K, cs.pad, cs.g, w.col, gate); ++t_launches;
-    for (uint32_t gi = 0; gi < cs.g; ++gi)
-      DS_TRY(gemm(c, w.col + gi * Kg, ldc, w.wp[l] + 1ull * gi * cs.cog() * Kg, Kg, out_act[l] + gi * cs.cog(), cs.Cout,
-                  static_cast<uint32_t>(Mx), cs.cog(), Kg, 1.f, P + L[l + 1].b_off + gi * cs.cog(), true));
-    if (l == 0) {
-      lrn_fwd_kernel<<<nblk(M2 * 256), 256, 0, s>>>(w.a2, M2, 256, w.n2, gate); ++t_launches;
-      maxpool_fwd_kernel<<<nblk(M3 * 256), 256, 0, s>>>(w.n2, R, sh.P1, 256, sh.P2, 0, w.p2, w.arg2, gate); ++t_launches;
-    }
-  }
-  maxpool_fwd_kernel<<<nblk(R * sh.q5), 256, 0, s>>>(w.a5, R, sh.P2, 256, sh.P5, 1, w.p5, w.arg5, gate); ++t_launches;
-  // fc6, fc7 (+relu), fc8
-  DS_TRY(gemm(c, w.p5, sh.q5, P + L[5].w_off, sh.q5, w.h6, 4096, R, 4096, static_cast<uint32_t>(sh.q5), 1.f,
-              P + L[5].b_off, true));
-  DS_TRY(gemm(c, w.h6, 4096, P + L[6].w_off, 4096, w.h7, 4096, R, 4096, 4096, 1.f, P + L[6].b_off, true));
-  DS_TRY(gemm(c, w.h7, 4096, P + L[7].w_off, 4096, w.z, sh.Cp, R, sh.C, 4096, 1.f, P + L[7].b_off, false, nullptr, 0,
-              sh.Cp == sh.C));
-  DS_CUDA_TRY(cudaGetLastError());
-  return DS_OK;
-}
-
-// predict() (model.cpp:303-318): first maximal logit, hits against labels
+// argmax of the logits (first maximum), hits against labels (predict, model.cpp:303-318)
 __global__ void alex_hits_kernel(const float* __restrict__ z, uint32_t ldz, const uint32_t* __restrict__ y, uint32_t R,
                                  uint32_t C, uint32_t* pred, unsigned long long* hits) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -593,7 +460,236 @@ __global__ void alex_hits_kernel(const float* __restrict__ z, uint32_t ldz, cons
   if (hits && y && best == y[r]) atomicAdd(hits, 1ull);
 }
 
+// ---- host helpers --------------------------------------------------------------------
+// DS_DEBUG_SYNC=1: synchronize and check after every launch of this file (fault isolation)
+int debug_sync(cudaStream_t s, int line) {
+  static const bool on = [] {
+    const char* e = getenv("DS_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  if (!on) return DS_OK;
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_error(DS_E_CUDA, "alexnet.cu:%d: %s", line, cudaGetErrorString(e));
+  return DS_OK;
+}
+#define KDONE(n)                          \
+  do {                                    \
+    t_launches += (n);                    \
+    DS_TRY(debug_sync(s_, __LINE__));     \
+  } while (0)
+
+struct Ctx {
+  cudaStream_t s;
+  const uint32_t* gate;
+  float* part;
+  uint32_t* flags;
+};
+
+// splits so that tiles * splits covers the SMs twice, each split >= 4 k-steps, slabs fit
+uint32_t pick_splits(uint32_t M, uint32_t N, uint64_t K, uint32_t ntaps = 1) {
+  const uint32_t bn = gemm_pick_bn(N);
+  const uint64_t tiles = 1ull * ((N + bn - 1) / bn) * ((M + 127) / 128) * ntaps;
+  if (tiles >= 148) return 1;
+  uint32_t sp = static_cast<uint32_t>((2 * 148 + tiles - 1) / tiles);
+  sp = static_cast<uint32_t>(std::min<uint64_t>(sp, std::max<uint64_t>(1, K / 128)));
+  while (sp > 1 && 1ull * sp * M * N * ntaps > kPartFloats) --sp;
+  return sp;
+}
+
+GemmEpilogue epi(const Ctx& c, float* D, uint64_t ldd, float scale, const float* bias_n, bool relu,
+                 const float* mask = nullptr, uint64_t ldm = 0) {
+  GemmEpilogue ep;
+  ep.D = D;
+  ep.ldd = ldd;
+  ep.scale = scale;
+  ep.bias_n = bias_n;
+  ep.relu = relu;
+  ep.mask = mask;
+  ep.ldm = ldm;
+  ep.gate = c.gate;
+  return ep;
+}
+
+int gemm(const Ctx& c, const float* A, uint64_t lda, const float* B, uint64_t ldb, float* D, uint64_t ldd, uint32_t M,
+         uint32_t N, uint32_t K, float scale, const float* bias_n, bool relu, const float* mask = nullptr,
+         uint64_t ldm = 0) {
+  const uint32_t sp = pick_splits(M, N, K);
+  DS_TRY(launch_gemm_tf32(A, lda, B, ldb, M, N, K, epi(c, D, ldd, scale, bias_n, relu, mask, ldm), sp, c.part, c.s));
+  const cudaStream_t s_ = c.s;
+  KDONE(sp > 1 ? 2 : 1);
+  return DS_OK;
+}
+
+int transpose(const Ctx& c, const float* in, uint64_t rows, uint32_t cols, uint64_t ld_in, float* out, uint64_t ld_out) {
+  const cudaStream_t s_ = c.s;
+  dim3 grid(static_cast<unsigned>((rows + 31) / 32), (cols + 31) / 32);
+  transpose_kernel<<<grid, dim3(32, 8), 0, c.s>>>(in, rows, cols, ld_in, out, ld_out, c.gate);
+  KDONE(1);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+int colsum(const Ctx& c, const float* d, uint64_t rows, uint32_t N, uint64_t ld, float scale, float* out, float* bpart) {
+  const cudaStream_t s_ = c.s;
+  const uint32_t nparts = static_cast<uint32_t>(std::min<uint64_t>(512, std::max<uint64_t>(1, rows / 64)));
+  const uint64_t rpb = (rows + nparts - 1) / nparts;
+  dim3 grid((N + 127) / 128, nparts);
+  colsum_part_kernel<<<grid, 128, 0, c.s>>>(d, rows, N, ld, rpb, bpart, c.gate);
+  colsum_final_kernel<<<(N + 127) / 128, 128, 0, c.s>>>(bpart, nparts, N, scale, out, c.flags, c.gate);
+  KDONE(2);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+int zero(const Ctx& c, float* p, uint64_t floats) {
+  DS_CUDA_TRY(cudaMemsetAsync(p, 0, floats * 4, c.s));
+  return DS_OK;
+}
+
+// pixel shift of tap (ky, kx) on the padded grid of side Hp
+int32_t shift(const ConvSpec& cs, uint32_t t) {
+  return (static_cast<int32_t>(t / cs.K) - static_cast<int32_t>(cs.pad)) * static_cast<int32_t>(cs.Hp) +
+         (static_cast<int32_t>(t % cs.K) - static_cast<int32_t>(cs.pad));
+}
+
+// conv forward over the padded input `in` ([R*Hp*Hp][Cin]): out = relu(conv + b) at the
+// interior rows, unpadded (out_padded = false) or on the same padded grid
+int conv_fwd(const Ctx& c, const ConvSpec& cs, uint32_t R, const float* in, const float* Wp, const float* bias,
+             float* out, bool out_padded) {
+  const cudaStream_t s_ = c.s;
+  const uint32_t G = R * cs.Hp * cs.Hp, Kg = cs.Kg(), cog = cs.cog(), cig = cs.cig();
+  for (uint32_t gi = 0; gi < cs.g; ++gi) {
+    GemmTaps tp;
+    tp.n = static_cast<int32_t>(cs.KK());
+    tp.kt = cig;
+    for (uint32_t t = 0; t < cs.KK(); ++t) {
+      tp.a_row[t] = shift(cs, t);
+      tp.a_col[t] = static_cast<int32_t>(gi * cig);
+      tp.b_row[t] = 0;
+      tp.b_col[t] = static_cast<int32_t>(t * cig);
+    }
+    const GemmOperand A{in, G, cs.Cin, cs.Cin}, B{Wp + 1ull * gi * cog * Kg, cog, Kg, Kg};
+    GemmEpilogue ep = epi(c, out + gi * cog, cs.Cout, 1.f, bias + gi * cog, true);
+    ep.map_Hp = cs.Hp, ep.map_pad = cs.pad, ep.map_H = cs.H, ep.map_out_padded = out_padded;
+    DS_TRY(launch_gemm(A, B, G, cog, 0, &tp, ep, 1, nullptr, c.s));
+    KDONE(1);
+  }
+  return DS_OK;
+}
+
+// conv data gradient: din = sum_t dout[i - d_t] . WpT[t]^T (ReLU-masked by `mask`, same
+// layout as din), dout on the padded grid with a zero border; din at the interior rows
+int conv_dgrad(const Ctx& c, const ConvSpec& cs, uint32_t R, const float* dout, const float* WpT, float* din,
+               bool din_padded, const float* mask) {
+  const cudaStream_t s_ = c.s;
+  const uint32_t G = R * cs.Hp * cs.Hp, Kg = cs.Kg(), cog = cs.cog(), cig = cs.cig();
+  for (uint32_t gi = 0; gi < cs.g; ++gi) {
+    GemmTaps tp;
+    tp.n = static_cast<int32_t>(cs.KK());
+    tp.kt = cog;
+    for (uint32_t t = 0; t < cs.KK(); ++t) {
+      tp.a_row[t] = -shift(cs, t);
+      tp.a_col[t] = static_cast<int32_t>(gi * cog);
+      tp.b_row[t] = static_cast<int32_t>(t * cig);
+      tp.b_col[t] = 0;
+    }
+    const GemmOperand A{dout, G, cs.Cout, cs.Cout}, B{WpT + 1ull * gi * Kg * cog, Kg, cog, cog};
+    GemmEpilogue ep = epi(c, din + gi * cig, cs.Cin, 1.f, nullptr, false, mask ? mask + gi * cig : nullptr, cs.Cin);
+    ep.map_Hp = cs.Hp, ep.map_pad = cs.pad, ep.map_H = cs.H, ep.map_out_padded = din_padded;
+    DS_TRY(launch_gemm(A, B, G, cig, 0, &tp, ep, 1, nullptr, c.s));
+    KDONE(1);
+  }
+  return DS_OK;
+}
+
+// conv weight gradient from pixel-contiguous maps doutT [Cout][ldT] and the four shifted
+// copies inT4 [4][Cin][ldT] (padded grid): packed [Cout][KK][cig] into wtmp, then Caffe
+// order into grad
+int conv_wgrad(const Ctx& c, const ConvSpec& cs, uint32_t R, const float* doutT, const float* inT4, uint64_t ldT,
+               float scale, float* wtmp, float* grad) {
+  const cudaStream_t s_ = c.s;
+  const uint32_t G = R * cs.Hp * cs.Hp, Kg = cs.Kg(), cog = cs.cog(), cig = cs.cig();
+  for (uint32_t gi = 0; gi < cs.g; ++gi) {
+    GemmTaps tp;
+    tp.n = static_cast<int32_t>(cs.KK());
+    tp.per_z = 1;
+    tp.d_col_step = cig;
+    for (uint32_t t = 0; t < cs.KK(); ++t) {
+      const int32_t d = shift(cs, t), sft = ((d % 4) + 4) % 4;
+      tp.a_row[t] = 0;
+      tp.a_col[t] = 0;
+      tp.b_row[t] = sft * static_cast<int32_t>(cs.Cin) + static_cast<int32_t>(gi * cig);
+      tp.b_col[t] = d - sft;
+    }
+    const GemmOperand A{doutT + 1ull * gi * cog * ldT, cog, G, ldT}, B{inT4, 4ull * cs.Cin, G, ldT};
+    const uint32_t sp = pick_splits(cog, cig, G, cs.KK());
+    GemmEpilogue ep = epi(c, wtmp + 1ull * gi * cog * Kg, Kg, scale, nullptr, false);
+    DS_TRY(launch_gemm(A, B, cog, cig, G, &tp, ep, sp, c.part, c.s));
+    KDONE(sp > 1 ? 2 : 1);
+  }
+  unpack_wgrad_kernel<<<nblk(1ull * cs.Cout * Kg), 256, 0, c.s>>>(wtmp, cs.Cout, cig, cs.K, grad, c.flags, c.gate);
+  KDONE(1);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+// forward to the logits w.z [R x Cp]
+int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint32_t* idx, uint32_t R, AlexWs& w,
+                 const Ctx& c) {
+  const cudaStream_t s_ = c.s;
+  const Shape sh = shape_of(m);
+  const auto& L = m.layers;
+  const uint32_t F = m.n_features;
+  const uint64_t M1 = 1ull * R * sh.H1 * sh.H1, M2 = 1ull * R * sh.P1 * sh.P1;
+  const uint64_t G2 = 1ull * R * sh.Hp2 * sh.Hp2, G3 = 1ull * R * sh.Hp3 * sh.Hp3;
+  cudaStream_t s = c.s;
+  const uint32_t* gate = c.gate;
+  pack_conv1_kernel<<<nblk(96 * 364), 256, 0, s>>>(P + L[0].w_off, w.w1p, gate);
+  KDONE(1);
+  for (int l = 0; l < 4; ++l) {
+    const ConvSpec cs = conv_spec(sh, l);
+    pack_conv_kernel<<<nblk(1ull * cs.Cout * cs.Kg()), 256, 0, s>>>(P + L[l + 1].w_off, cs.Cout, cs.cig(), cs.K, cs.g,
+                                                                   w.wp[l], w.wpT[l], gate);
+    KDONE(1);
+  }
+  // padded maps: zero borders (interiors are rewritten below)
+  DS_TRY(zero(c, w.p1p, G2 * 96));
+  DS_TRY(zero(c, w.p2p, G3 * 256));
+  DS_TRY(zero(c, w.a3p, G3 * 384));
+  DS_TRY(zero(c, w.a4p, G3 * 384));
+  DS_TRY(zero(c, w.a5p, G3 * 256));
+  // conv1 (explicit im2col on the CHW input) + relu, LRN1, pool1 -> p1p (pad 2)
+  im2col_conv1_kernel<<<nblk(M1 * 364), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, M1, w.col, gate);
+  KDONE(1);
+  DS_TRY(gemm(c, w.col, 364, w.w1p, 364, w.a1, 96, static_cast<uint32_t>(M1), 96, 364, 1.f, P + L[0].b_off, true));
+  lrn_fwd_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, M1, 96, w.n1, gate);
+  maxpool_fwd_kernel<<<nblk(M2 * 96), 256, 0, s>>>(w.n1, R, sh.H1, 96, sh.P1, 0, 2, 0, w.p1p, w.arg1, gate);
+  KDONE(2);
+  // conv2 + relu -> a2 (unpadded), LRN2, pool2 -> p2p (pad 1)
+  DS_TRY(conv_fwd(c, conv_spec(sh, 0), R, w.p1p, w.wp[0], P + L[1].b_off, w.a2, false));
+  lrn_fwd_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, M2, 256, w.n2, gate);
+  maxpool_fwd_kernel<<<nblk(1ull * R * sh.P2 * sh.P2 * 256), 256, 0, s>>>(w.n2, R, sh.P1, 256, sh.P2, 0, 1, 0, w.p2p,
+                                                                         w.arg2, gate);
+  KDONE(2);
+  // conv3, conv4, conv5 on the pad-1 grid, pool5 -> p5 (per-row CHW)
+  DS_TRY(conv_fwd(c, conv_spec(sh, 1), R, w.p2p, w.wp[1], P + L[2].b_off, w.a3p, true));
+  DS_TRY(conv_fwd(c, conv_spec(sh, 2), R, w.a3p, w.wp[2], P + L[3].b_off, w.a4p, true));
+  DS_TRY(conv_fwd(c, conv_spec(sh, 3), R, w.a4p, w.wp[3], P + L[4].b_off, w.a5p, true));
+  maxpool_fwd_kernel<<<nblk(R * sh.q5), 256, 0, s>>>(w.a5p, R, sh.P2, 256, sh.P5, 1, 0, 1, w.p5, w.arg5, gate);
+  KDONE(1);
+  // fc6, fc7 (+relu), fc8
+  DS_TRY(gemm(c, w.p5, sh.q5, P + L[5].w_off, sh.q5, w.h6, 4096, R, 4096, static_cast<uint32_t>(sh.q5), 1.f,
+              P + L[5].b_off, true));
+  DS_TRY(gemm(c, w.h6, 4096, P + L[6].w_off, 4096, w.h7, 4096, R, 4096, 4096, 1.f, P + L[6].b_off, true));
+  DS_TRY(gemm(c, w.h7, 4096, P + L[7].w_off, 4096, w.z, sh.Cp, R, sh.C, 4096, 1.f, P + L[7].b_off, false));
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
 }  // namespace
+
+uint64_t alex_workspace_bytes(const ModelInfo& m, uint32_t R) { return carve_ws(m, R, nullptr).end; }
+uint32_t alex_last_launches() { return t_launches; }
 
 int launch_alex_count_hits(const ModelInfo& m, const float* P, const float* X, const uint32_t* y, uint32_t R,
                            void* ws_base, unsigned long long* hits, uint32_t* pred, cudaStream_t s) {
@@ -601,7 +697,7 @@ int launch_alex_count_hits(const ModelInfo& m, const float* P, const float* X, c
   Ctx c{s, nullptr, w.part, nullptr};
   DS_TRY(alex_forward(m, P, X, nullptr, R, w, c));
   const Shape sh = shape_of(m);
-  alex_hits_kernel<<<(R + 127) / 128, 128, 0, s>>>(w.z, sh.Cp, y, R, sh.C, pred, hits); ++t_launches;
+  alex_hits_kernel<<<(R + 127) / 128, 128, 0, s>>>(w.z, sh.Cp, y, R, sh.C, pred, hits);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
@@ -609,37 +705,37 @@ int launch_alex_count_hits(const ModelInfo& m, const float* P, const float* X, c
 int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X, const uint32_t* idx,
                               const uint32_t* y, uint32_t R, float* grad, double* loss_out, void* ws_base,
                               uint32_t* flags, const uint32_t* gate, cudaStream_t s) {
+  const cudaStream_t s_ = s;
   const Shape sh = shape_of(m);
   AlexWs w = carve_ws(m, R, ws_base);
   Ctx c{s, gate, w.part, flags};
   const auto& L = m.layers;
   const uint32_t F = m.n_features, Rp = up4(R);
   const uint64_t M1 = 1ull * R * sh.H1 * sh.H1, M2 = 1ull * R * sh.P1 * sh.P1, M3 = 1ull * R * sh.P2 * sh.P2;
+  const uint64_t G2 = 1ull * R * sh.Hp2 * sh.Hp2, G3 = 1ull * R * sh.Hp3 * sh.Hp3;
   const float inv_b = 1.f / static_cast<float>(R);
   t_launches = 0;
   DS_TRY(alex_forward(m, P, X, idx, R, w, c));
   softmax_ce_warp_kernel<<<(R + 7) / 8, 256, 0, s>>>(w.z, sh.Cp, y, idx, R, sh.C, w.loss_rows, grad ? w.dz : nullptr,
-                                                     flags, gate); ++t_launches;
-  alex_loss_mean_kernel<<<1, 1, 0, s>>>(w.loss_rows, R, loss_out, flags, gate); ++t_launches;
+                                                     flags, gate);
+  alex_loss_mean_kernel<<<1, 1, 0, s>>>(w.loss_rows, R, loss_out, flags, gate);
+  KDONE(2);
   DS_CUDA_TRY(cudaGetLastError());
   if (!grad) return DS_OK;
 
-  // ---------------- backward ----------------
-  // fc8: dW8 = dz^T h7 / R ; db8 ; dh7 = dz W8, masked by h7 > 0
+  // ---- fc8, fc7, fc6: dW = dh^T h / R ; db ; dh_prev = dh W, ReLU-masked -------------------
   DS_TRY(transpose(c, w.dz, R, sh.Cp, sh.Cp, w.zT, Rp));
   DS_TRY(transpose(c, w.h7, R, 4096, 4096, w.h7T, Rp));
   DS_TRY(gemm(c, w.zT, Rp, w.h7T, Rp, grad + L[7].w_off, 4096, sh.C, 4096, R, inv_b, nullptr, false));
   DS_TRY(colsum(c, w.dz, R, sh.C, sh.Cp, inv_b, grad + L[7].b_off, w.bpart));
   DS_TRY(transpose(c, P + L[7].w_off, sh.C, 4096, 4096, w.w8T, sh.Cp));
   DS_TRY(gemm(c, w.dz, sh.Cp, w.w8T, sh.Cp, w.dh7, 4096, R, 4096, sh.C, 1.f, nullptr, false, w.h7, 4096));
-  // fc7
   DS_TRY(transpose(c, w.dh7, R, 4096, 4096, w.dh7T, Rp));
   DS_TRY(transpose(c, w.h6, R, 4096, 4096, w.h6T, Rp));
   DS_TRY(gemm(c, w.dh7T, Rp, w.h6T, Rp, grad + L[6].w_off, 4096, 4096, 4096, R, inv_b, nullptr, false));
   DS_TRY(colsum(c, w.dh7, R, 4096, 4096, inv_b, grad + L[6].b_off, w.bpart));
   DS_TRY(transpose(c, P + L[6].w_off, 4096, 4096, 4096, w.w7T, 4096));
   DS_TRY(gemm(c, w.dh7, 4096, w.w7T, 4096, w.dh6, 4096, R, 4096, 4096, 1.f, nullptr, false, w.h6, 4096));
-  // fc6
   DS_TRY(transpose(c, w.dh6, R, 4096, 4096, w.dh6T, Rp));
   DS_TRY(transpose(c, w.p5, R, static_cast<uint32_t>(sh.q5), sh.q5, w.p5T, Rp));
   DS_TRY(gemm(c, w.dh6T, Rp, w.p5T, Rp, grad + L[5].w_off, sh.q5, 4096, static_cast<uint32_t>(sh.q5), R, inv_b,
@@ -647,59 +743,57 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   DS_TRY(colsum(c, w.dh6, R, 4096, 4096, inv_b, grad + L[5].b_off, w.bpart));
   DS_TRY(transpose(c, P + L[5].w_off, 4096, static_cast<uint32_t>(sh.q5), sh.q5, w.w6T, 4096));
   DS_TRY(gemm(c, w.dh6, 4096, w.w6T, 4096, w.dp5, sh.q5, R, static_cast<uint32_t>(sh.q5), 4096, 1.f, nullptr, false));
-  // pool5 backward (CHW pooled map), masked by a5 > 0 -> dc5 (NHWC)
-  float* dcur = w.dA;
-  float* dnext = w.dB;
-  maxpool_bwd_kernel<<<nblk(M3 * 256), 256, 0, s>>>(w.dp5, w.arg5, R, sh.P2, 256, sh.P5, 1, w.a5, dcur, gate); ++t_launches;
-  // conv5, conv4, conv3, conv2
-  const float* in_act[4] = {w.p1, w.p2, w.a3, w.a4};
-  const float* fwd_out[4] = {w.a2, w.a3, w.a4, w.a5};
+
+  // ---- conv5 .. conv2 on the padded grids ------------------------------------------------
+  DS_TRY(zero(c, w.dc5p, G3 * 256));
+  DS_TRY(zero(c, w.dc4p, G3 * 384));
+  DS_TRY(zero(c, w.dc3p, G3 * 384));
+  DS_TRY(zero(c, w.dc2p, G2 * 256));
+  // pool5 backward (per-row CHW pooled map) with the ReLU5 mask (a5p) -> dc5p
+  maxpool_bwd_kernel<<<nblk(M3 * 256), 256, 0, s>>>(w.dp5, w.arg5, R, sh.P2, 256, sh.P5, 0, 1, 1, w.a5p, w.dc5p,
+                                                    gate);
+  KDONE(1);
+  const float* in_maps[4] = {w.p1p, w.p2p, w.a3p, w.a4p};
+  float* dout_maps[4] = {w.dc2p, w.dc3p, w.dc4p, w.dc5p};
   for (int l = 3; l >= 0; --l) {
     const ConvSpec cs = conv_spec(sh, l);
-    const uint64_t Mx = l == 0 ? M2 : M3;
-    const uint32_t Kg = cs.Kg(), cog = cs.cog(), Mp = up4(static_cast<uint32_t>(Mx));
-    // bias gradient: column sums of dc
-    DS_TRY(colsum(c, dcur, Mx, cs.Cout, cs.Cout, inv_b, grad + L[l + 1].b_off, w.bpart));
-    // weight gradient per group: dcT_g [cog x M] . colT_g [Kg x M]^T
-    DS_TRY(transpose(c, dcur, Mx, cs.Cout, cs.Cout, w.tr, Mp));
-    for (uint32_t gi = 0; gi < cs.g; ++gi) {
-      dim3 grid(static_cast<unsigned>((Mx + 31) / 32), (Kg + 31) / 32);
-      im2colT_nhwc_kernel<<<grid, dim3(32, 8), 0, s>>>(in_act[l], R, cs.H, cs.Cin, cs.K, cs.pad, cs.g, gi, Mp, w.col,
-                                                       gate); ++t_launches;
-      DS_TRY(gemm(c, w.tr + 1ull * gi * cog * Mp, Mp, w.col, Mp, w.wtmp, Kg, cog, Kg, static_cast<uint32_t>(Mx), inv_b,
-                  nullptr, false));
-      unpack_wgrad_kernel<<<nblk(1ull * cog * Kg), 256, 0, s>>>(w.wtmp, cog, cs.cig(), cs.K, gi, grad + L[l + 1].w_off,
-                                                               gate); ++t_launches;
+    const uint64_t G = 1ull * R * cs.Hp * cs.Hp, ldT = up4(static_cast<uint32_t>(G));
+    float* dout = dout_maps[l];
+    // bias gradient (border rows are zero)
+    DS_TRY(colsum(c, dout, G, cs.Cout, cs.Cout, inv_b, grad + L[l + 1].b_off, w.bpart));
+    // weight gradient from pixel-contiguous copies
+    DS_TRY(transpose(c, dout, G, cs.Cout, cs.Cout, w.trA, ldT));
+    {
+      dim3 grid(static_cast<unsigned>((ldT + 31) / 32), (cs.Cin + 31) / 32);
+      transpose_shift4_kernel<<<grid, dim3(32, 8), 0, s>>>(in_maps[l], G, cs.Cin, w.trB, ldT, gate);
+      KDONE(1);
     }
-    // data gradient: dcol = dc_g . WpT_g^T, then col2im (+ ReLU mask of the input for conv3..5)
-    const uint32_t ldc = Kg * cs.g;
-    for (uint32_t gi = 0; gi < cs.g; ++gi)
-      DS_TRY(gemm(c, dcur + gi * cog, cs.Cout, w.wpT[l] + 1ull * gi * Kg * cog, cog, w.col + gi * Kg, ldc,
-                  static_cast<uint32_t>(Mx), Kg, cog, 1.f, nullptr, false));
-    if (l >= 2) {  // input of conv4/conv5 is relu(conv3/conv4): mask, stay in NHWC
-      col2im_nhwc_kernel<<<nblk(Mx * cs.Cin), 256, 0, s>>>(w.col, R, cs.H, cs.Cin, cs.K, cs.pad, cs.g, fwd_out[l - 1],
-                                                           dnext, gate); ++t_launches;
-      std::swap(dcur, dnext);
-    } else if (l == 1) {  // input of conv3 is pool2(LRN2(relu(conv2)))
-      col2im_nhwc_kernel<<<nblk(Mx * cs.Cin), 256, 0, s>>>(w.col, R, cs.H, cs.Cin, cs.K, cs.pad, cs.g, nullptr, dnext,
-                                                           gate); ++t_launches;
-      maxpool_bwd_kernel<<<nblk(M2 * 256), 256, 0, s>>>(dnext, w.arg2, R, sh.P1, 256, sh.P2, 0, nullptr, dcur, gate); ++t_launches;
-      lrn_bwd_relu_kernel<<<nblk(M2 * 256), 256, 0, s>>>(w.a2, dcur, M2, 256, dnext, gate); ++t_launches;
-      std::swap(dcur, dnext);
-    } else {  // input of conv2 is pool1(LRN1(relu(conv1)))
-      col2im_nhwc_kernel<<<nblk(Mx * cs.Cin), 256, 0, s>>>(w.col, R, cs.H, cs.Cin, cs.K, cs.pad, cs.g, nullptr, dnext,
-                                                           gate); ++t_launches;
-      maxpool_bwd_kernel<<<nblk(M1 * 96), 256, 0, s>>>(dnext, w.arg1, R, sh.H1, 96, sh.P1, 0, nullptr, dcur, gate); ++t_launches;
-      lrn_bwd_relu_kernel<<<nblk(M1 * 96), 256, 0, s>>>(w.a1, dcur, M1, 96, dnext, gate); ++t_launches;
-      std::swap(dcur, dnext);
+    DS_TRY(conv_wgrad(c, cs, R, w.trA, w.trB, ldT, inv_b, w.wtmp, grad + L[l + 1].w_off));
+    // data gradient
+    if (l >= 2) {  // into relu(conv3 / conv4): masked, same padded grid
+      DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], dout_maps[l - 1], true, in_maps[l]));
+    } else if (l == 1) {  // into pool2(LRN2(relu(conv2))): d(p2p), pool2 bwd, LRN2 bwd -> dc2p
+      DS_TRY(zero(c, w.dp2p, G3 * 256));
+      DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp2p, true, nullptr));
+      maxpool_bwd_kernel<<<nblk(M2 * 256), 256, 0, s>>>(w.dp2p, w.arg2, R, sh.P1, 256, sh.P2, 1, 0, 0, nullptr, w.dn2,
+                                                        gate);
+      lrn_bwd_relu_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, w.dn2, R, sh.P1, 256, 2, w.dc2p, gate);
+      KDONE(2);
+    } else {  // into pool1(LRN1(relu(conv1))): d(p1) unpadded, pool1 bwd, LRN1 bwd -> dc1
+      DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp1, false, nullptr));
+      maxpool_bwd_kernel<<<nblk(M1 * 96), 256, 0, s>>>(w.dp1, w.arg1, R, sh.H1, 96, sh.P1, 0, 0, 0, nullptr, w.dn1,
+                                                       gate);
+      lrn_bwd_relu_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, w.dn1, R, sh.H1, 96, 0, w.dc1, gate);
+      KDONE(2);
     }
   }
-  // conv1: bias and weight gradients (no data gradient)
-  DS_TRY(colsum(c, dcur, M1, 96, 96, inv_b, grad + L[0].b_off, w.bpart));
+  // ---- conv1: bias and weight gradients (no data gradient) ---------------------------------
+  DS_TRY(colsum(c, w.dc1, M1, 96, 96, inv_b, grad + L[0].b_off, w.bpart));
   const uint32_t M1p = up4(static_cast<uint32_t>(M1));
-  DS_TRY(transpose(c, dcur, M1, 96, 96, w.tr, M1p));
-  im2colT_conv1_kernel<<<nblk(363 * M1), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, M1, M1p, w.col, gate); ++t_launches;
-  DS_TRY(gemm(c, w.tr, M1p, w.col, M1p, grad + L[0].w_off, 363, 96, 363, static_cast<uint32_t>(M1), inv_b, nullptr,
+  DS_TRY(transpose(c, w.dc1, M1, 96, 96, w.trA, M1p));
+  im2colT_conv1_kernel<<<nblk(363 * M1), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, M1, M1p, w.col, gate);
+  KDONE(1);
+  DS_TRY(gemm(c, w.trA, M1p, w.col, M1p, grad + L[0].w_off, 363, 96, 363, static_cast<uint32_t>(M1), inv_b, nullptr,
               false));
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;

@@ -64,10 +64,22 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::saddr(b)), "r"(bytes) : "memory");
 }
 
+// Output row of accumulator row `row` under the epilogue's row map; -1 for a border row.
+__device__ __forceinline__ int64_t map_row(const GemmEpilogue& ep, uint32_t row) {
+  if (ep.map_Hp == 0) return row;
+  const uint32_t hp2 = ep.map_Hp * ep.map_Hp;
+  const uint32_t img = row / hp2, pix = row - img * hp2;
+  const uint32_t yp = pix / ep.map_Hp, xp = pix - yp * ep.map_Hp;
+  if (yp < ep.map_pad || xp < ep.map_pad || yp >= ep.map_pad + ep.map_H || xp >= ep.map_pad + ep.map_H) return -1;
+  if (ep.map_out_padded) return row;
+  return (static_cast<int64_t>(img) * ep.map_H + (yp - ep.map_pad)) * ep.map_H + (xp - ep.map_pad);
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmEpilogue ep,
-                     uint32_t M, uint32_t N, uint32_t K, uint32_t k_per_split) {
+    gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ GemmEpilogue ep, const __grid_constant__ GemmTaps tp, uint32_t M,
+                     uint32_t N, uint32_t K, uint32_t k_per_split, uint32_t splits) {
   using S = GemmSmem<BN>;
   constexpr int kStages = S::STAGES;
   if (ep.gate && *ep.gate) return;
@@ -79,9 +91,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM;
-  const uint32_t k_begin = blockIdx.z * k_per_split;
-  const uint32_t k_end = min(K, k_begin + k_per_split);
-  const uint32_t nk = (k_end > k_begin) ? (k_end - k_begin + kBK - 1) / kBK : 0;
+  const bool acc_taps = tp.n > 0 && !tp.per_z;
+  const int tap = (tp.n > 0 && tp.per_z) ? static_cast<int>(blockIdx.z / splits) : -1;
+  const uint32_t split = tap >= 0 ? blockIdx.z % splits : blockIdx.z;
+  uint32_t nk, nkt = 1, k_begin = 0;
+  if (acc_taps) {
+    nkt = (tp.kt + kBK - 1) / kBK;
+    nk = tp.n * nkt;
+  } else {
+    k_begin = split * k_per_split;
+    const uint32_t k_end = min(K, k_begin + k_per_split);
+    nk = (k_end > k_begin) ? (k_end - k_begin + kBK - 1) / kBK : 0;
+  }
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -106,9 +127,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
         uint8_t* sa = smem + s * S::STAGE;
         mbar_expect_tx(&full[s], S::STAGE);
-        const int kx = static_cast<int>(k_begin + i * kBK);
-        tma_load_2d(sa, &tmA, &full[s], kx, static_cast<int>(m0));
-        tma_load_2d(sa + S::A_BYTES, &tmB, &full[s], kx, static_cast<int>(n0));
+        int ax, ay, bx, by;
+        if (acc_taps) {
+          const uint32_t t = i / nkt, kc = i - t * nkt;
+          ax = tp.a_col[t] + static_cast<int>(kc * kBK);
+          ay = static_cast<int>(m0) + tp.a_row[t];
+          bx = tp.b_col[t] + static_cast<int>(kc * kBK);
+          by = static_cast<int>(n0) + tp.b_row[t];
+        } else {
+          ax = bx = static_cast<int>(k_begin + i * kBK);
+          ay = static_cast<int>(m0);
+          by = static_cast<int>(n0);
+          if (tap >= 0) ax += tp.a_col[tap], ay += tp.a_row[tap], bx += tp.b_col[tap], by += tp.b_row[tap];
+        }
+        tma_load_2d(sa, &tmA, &full[s], ax, ay);
+        tma_load_2d(sa + S::A_BYTES, &tmB, &full[s], bx, by);
       }
     }
   } else if (warp == 1) {
@@ -116,11 +149,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = tc::idesc_tf32(kBM, BN);
       for (uint32_t i = 0; i < nk; ++i) {
         const int s = i % kStages;
+        uint32_t nsub = kBK / 8;
+        if (acc_taps) {  // a tap's last chunk may be partial (kt multiple of 8)
+          const uint32_t rem = tp.kt - (i % nkt) * kBK;
+          nsub = rem >= kBK ? kBK / 8 : rem / 8;
+        }
         tc::mbar_wait(&full[s], (i / kStages) & 1);
         tc::fence_after();
         const uint32_t a = tc::saddr(smem + s * S::STAGE), b = a + S::A_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < kBK / 8; ++kk) {
+        for (uint32_t kk = 0; kk < nsub; ++kk) {
           const uint64_t da = sdesc_sw128(a + kk * 32), db = sdesc_sw128(b + kk * 32);
           const uint32_t acc = (i | kk) ? 1u : 0u;
           asm volatile(
@@ -139,9 +176,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(acc_full, 0);
       tc::fence_after();
     }
-    float* out = ep.D + static_cast<uint64_t>(blockIdx.z) * ep.split_stride;
-    const bool raw = ep.raw || gridDim.z > 1;
-    const float bm = (!raw && ep.bias_m && row < M) ? ep.bias_m[row] : 0.f;
+    const bool raw = ep.raw || (tap < 0 && gridDim.z > 1) || (tap >= 0 && splits > 1);
+    float* out = raw ? ep.D + static_cast<uint64_t>(blockIdx.z) * ep.split_stride
+                     : ep.D + (tap >= 0 ? static_cast<uint64_t>(tap) * tp.d_col_step : 0);
+    const int64_t orow = row < M ? (raw ? static_cast<int64_t>(row) : map_row(ep, row)) : -1;
+    const uint64_t ldo = raw ? N : ep.ldd;
+    const float bm = (!raw && ep.bias_m && orow >= 0) ? ep.bias_m[row] : 0.f;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       float v[32];
@@ -151,21 +191,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0.f;
       }
-      if (row >= M || n0 + c >= N) continue;
-      float* dst = out + static_cast<uint64_t>(row) * ep.ldd + n0 + c;
+      if (orow < 0 || n0 + c >= N) continue;
+      float* dst = out + static_cast<uint64_t>(orow) * ldo + n0 + c;
       const uint32_t lim = min(32u, N - (n0 + c));
       if (!raw) {
+        const float* mrow = ep.mask ? ep.mask + static_cast<uint64_t>(orow) * ep.ldm + n0 + c : nullptr;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           float x = v[j] * ep.scale + bm;
           if (static_cast<uint32_t>(j) < lim) {
             if (ep.bias_n) x += __ldg(ep.bias_n + n0 + c + j);
-            if (ep.mask && !(ep.mask[static_cast<uint64_t>(row) * ep.ldm + n0 + c + j] > 0.f)) x = 0.f;
+            if (mrow && !(mrow[j] > 0.f)) x = 0.f;
           }
           v[j] = ep.relu ? fmaxf(x, 0.f) : x;
         }
       }
-      if (lim == 32 && (ep.ldd % 4) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      if (lim == 32 && (ldo % 4) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       } else {
@@ -180,22 +221,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tc::tmem_free<S::TMEM_COLS>(tmem);
 }
 
-// sum of the split slabs in split order, then scale, bias, ReLU
-__global__ void gemm_reduce_kernel(const float* __restrict__ part, uint64_t split_stride, uint32_t splits,
-                                   GemmEpilogue ep, uint32_t M, uint32_t N) {
+// Sum of raw slabs in a fixed order, then the epilogue (row map, tap columns, scale,
+// biases, mask, ReLU). Slab (tap t, part p) starts at t * tap_stride + p * part_stride and
+// is dense [M][N].
+__global__ void gemm_reduce_kernel(const float* __restrict__ slabs, uint32_t ntaps, uint64_t tap_stride,
+                                   uint32_t nparts, uint64_t part_stride, uint32_t d_col_step, GemmEpilogue ep,
+                                   uint32_t M, uint32_t N) {
   if (ep.gate && *ep.gate) return;
-  const uint64_t total = static_cast<uint64_t>(M) * N;
+  const uint64_t total = static_cast<uint64_t>(ntaps) * M * N;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t r = static_cast<uint32_t>(i / N), c = static_cast<uint32_t>(i % N);
-    const uint64_t off = static_cast<uint64_t>(r) * ep.ldd + c;  // D; the slabs are dense [M][N]
+    const uint64_t mn = static_cast<uint64_t>(M) * N;
+    const uint32_t t = static_cast<uint32_t>(i / mn);
+    const uint64_t e = i - t * mn;
+    const uint32_t r = static_cast<uint32_t>(e / N), c = static_cast<uint32_t>(e % N);
+    const int64_t orow = map_row(ep, r);
+    if (orow < 0) continue;
     float s = 0.f;
-    for (uint32_t z = 0; z < splits; ++z) s += part[z * split_stride + i];
+    for (uint32_t p = 0; p < nparts; ++p) s += slabs[t * tap_stride + p * part_stride + e];
     float x = s * ep.scale;
     if (ep.bias_m) x += ep.bias_m[r];
     if (ep.bias_n) x += ep.bias_n[c];
-    if (ep.mask && !(ep.mask[static_cast<uint64_t>(r) * ep.ldm + c] > 0.f)) x = 0.f;
-    ep.D[off] = ep.relu ? fmaxf(x, 0.f) : x;
+    if (ep.mask && !(ep.mask[static_cast<uint64_t>(orow) * ep.ldm + c] > 0.f)) x = 0.f;
+    ep.D[static_cast<uint64_t>(orow) * ep.ldd + static_cast<uint64_t>(t) * d_col_step + c] = ep.relu ? fmaxf(x, 0.f) : x;
   }
 }
 
@@ -230,10 +278,11 @@ int make_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, ui
 }
 
 template <int BN>
-int launch_bn(const CUtensorMap& ma, const float* B, uint64_t ldb, const GemmEpilogue& ep, uint32_t M, uint32_t N,
-              uint32_t K, uint32_t splits, cudaStream_t s) {
-  CUtensorMap mb;
-  DS_TRY(make_map(&mb, B, N, K, ldb, BN));
+int launch_bn(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep, const GemmTaps& tp, uint32_t M,
+              uint32_t N, uint32_t K, uint32_t splits, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  DS_TRY(make_map(&ma, A.p, A.rows, A.cols, A.ld, kBM));
+  DS_TRY(make_map(&mb, B.p, B.rows, B.cols, B.ld, BN));
   static uint64_t attr_set = 0;  // per device
   int dev = 0;
   DS_CUDA_TRY(cudaGetDevice(&dev));
@@ -243,10 +292,76 @@ int launch_bn(const CUtensorMap& ma, const float* B, uint64_t ldb, const GemmEpi
     attr_set |= 1ull << (dev & 63);
   }
   const uint32_t kps = ((K + splits - 1) / splits + kBK - 1) / kBK * kBK;
-  dim3 grid((N + BN - 1) / BN, (M + kBM - 1) / kBM, splits);
-  gemm_tf32_kernel<BN><<<grid, kThreads, GemmSmem<BN>::TOTAL, s>>>(ma, mb, ep, M, N, K, kps);
+  const uint32_t zdim = (tp.n > 0 && tp.per_z) ? tp.n * splits : (tp.n > 0 ? 1 : splits);
+  dim3 grid((N + BN - 1) / BN, (M + kBM - 1) / kBM, zdim);
+  gemm_tf32_kernel<BN><<<grid, kThreads, GemmSmem<BN>::TOTAL, s>>>(ma, mb, ep, tp, M, N, K, kps, splits);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
+}
+
+int launch_any(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep, const GemmTaps& tp, uint32_t M,
+               uint32_t N, uint32_t K, uint32_t splits, cudaStream_t s) {
+  const uint32_t bn = gemm_pick_bn(N);
+  if (bn == 64) return launch_bn<64>(A, B, ep, tp, M, N, K, splits, s);
+  if (bn == 128) return launch_bn<128>(A, B, ep, tp, M, N, K, splits, s);
+  return launch_bn<256>(A, B, ep, tp, M, N, K, splits, s);
+}
+
+int launch_reduce(const float* slabs, uint32_t ntaps, uint64_t tap_stride, uint32_t nparts, uint64_t part_stride,
+                  uint32_t d_col_step, const GemmEpilogue& ep, uint32_t M, uint32_t N, cudaStream_t s) {
+  const uint64_t total = static_cast<uint64_t>(ntaps) * M * N;
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
+  gemm_reduce_kernel<<<blocks, 256, 0, s>>>(slabs, ntaps, tap_stride, nparts, part_stride, d_col_step, ep, M, N);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+// hi = x with the 13 low mantissa bits cleared (exact in tf32), lo = x - hi (exact in f32)
+__global__ void split_tf32_kernel(const float* __restrict__ x, uint64_t n, float* __restrict__ hi,
+                                  float* __restrict__ lo) {
+  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
+    const float v = x[i];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
+bool exact_mode() {  // DS_GEMM_3XTF32=1: f32-accurate products (parity diagnostics; read per call)
+  const char* e = getenv("DS_GEMM_3XTF32");
+  return e && e[0] == '1';
+}
+
+// 3xTF32: A.B ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi as three raw slab sets, reduced with the epilogue
+int launch_3xtf32(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32_t N, uint32_t K, const GemmTaps& tp,
+                  const GemmEpilogue& ep_in, cudaStream_t s) {
+  const uint64_t na = A.rows * A.ld, nb = B.rows * B.ld;
+  const uint32_t ntz = (tp.n > 0 && tp.per_z) ? tp.n : 1;
+  const uint64_t set = static_cast<uint64_t>(ntz) * M * N;
+  float *ab = nullptr, *bb = nullptr, *slab = nullptr;
+  DS_CUDA_TRY(cudaMallocAsync(&ab, 2 * na * 4, s));
+  DS_CUDA_TRY(cudaMallocAsync(&bb, 2 * nb * 4, s));
+  DS_CUDA_TRY(cudaMallocAsync(&slab, 3 * set * 4, s));
+  split_tf32_kernel<<<4096, 256, 0, s>>>(A.p, na, ab, ab + na);
+  split_tf32_kernel<<<4096, 256, 0, s>>>(B.p, nb, bb, bb + nb);
+  GemmEpilogue raw = ep_in;
+  raw.raw = true;
+  raw.split_stride = static_cast<uint64_t>(M) * N;
+  int rc = DS_OK;
+  const int ia[3] = {0, 0, 1}, ib[3] = {0, 1, 0};
+  for (int t = 0; t < 3 && rc == DS_OK; ++t) {
+    GemmOperand a = A, b = B;
+    a.p = ab + ia[t] * na;
+    b.p = bb + ib[t] * nb;
+    raw.D = slab + t * set;
+    rc = launch_any(a, b, raw, tp, M, N, K, 1, s);
+  }
+  if (rc == DS_OK) rc = launch_reduce(slab, ntz, static_cast<uint64_t>(M) * N, 3, set, tp.per_z ? tp.d_col_step : 0,
+                                      ep_in, M, N, s);
+  cudaFreeAsync(ab, s);
+  cudaFreeAsync(bb, s);
+  cudaFreeAsync(slab, s);
+  return rc;
 }
 
 }  // namespace
@@ -261,94 +376,42 @@ uint32_t gemm_pick_bn(uint32_t N) {
   return best;
 }
 
-namespace {
-
-// hi = x with the 13 low mantissa bits cleared (exact in tf32), lo = x - hi (exact in f32)
-__global__ void split_tf32_kernel(const float* __restrict__ x, uint32_t rows, uint32_t cols, uint64_t ld,
-                                  float* __restrict__ hi, float* __restrict__ lo, uint64_t ldo) {
-  const uint64_t total = static_cast<uint64_t>(rows) * cols;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint64_t r = i / cols, c = i % cols;
-    const float v = x[r * ld + c];
-    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-    hi[r * ldo + c] = h;
-    lo[r * ldo + c] = v - h;
-  }
-}
-
-bool exact_mode() {  // DS_GEMM_3XTF32=1: f32-accurate products (parity diagnostics; read per call)
-  const char* e = getenv("DS_GEMM_3XTF32");
-  return e && e[0] == '1';
-}
-
-int launch_raw(const float* A, uint64_t lda, const float* B, uint64_t ldb, uint32_t M, uint32_t N, uint32_t K,
-               const GemmEpilogue& ep, uint32_t splits, cudaStream_t s) {
-  CUtensorMap ma;
-  DS_TRY(make_map(&ma, A, M, K, lda, kBM));
-  const uint32_t bn = gemm_pick_bn(N);
-  if (bn == 64) return launch_bn<64>(ma, B, ldb, ep, M, N, K, splits, s);
-  if (bn == 128) return launch_bn<128>(ma, B, ldb, ep, M, N, K, splits, s);
-  return launch_bn<256>(ma, B, ldb, ep, M, N, K, splits, s);
-}
-
-// 3xTF32: A.B ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi as three raw slabs, reduced with the epilogue
-int launch_3xtf32(const float* A, uint64_t lda, const float* B, uint64_t ldb, uint32_t M, uint32_t N, uint32_t K,
-                  const GemmEpilogue& ep_in, cudaStream_t s) {
-  const uint64_t kp = (K + 3) / 4 * 4;
-  float *ah = nullptr, *bh = nullptr, *slab = nullptr;
-  DS_CUDA_TRY(cudaMallocAsync(&ah, 2 * M * kp * 4, s));
-  DS_CUDA_TRY(cudaMallocAsync(&bh, 2 * N * kp * 4, s));
-  DS_CUDA_TRY(cudaMallocAsync(&slab, 3ull * M * N * 4, s));
-  float *al = ah + M * kp, *bl = bh + N * kp;
-  split_tf32_kernel<<<4096, 256, 0, s>>>(A, M, K, lda, ah, al, kp);
-  split_tf32_kernel<<<4096, 256, 0, s>>>(B, N, K, ldb, bh, bl, kp);
-  GemmEpilogue raw = ep_in;
-  raw.split_stride = 0;
-  raw.ldd = N;
-  raw.raw = true;
-  const float* pa[3] = {ah, ah, al};
-  const float* pb[3] = {bh, bl, bh};
-  int rc = DS_OK;
-  for (int t = 0; t < 3 && rc == DS_OK; ++t) {
-    raw.D = slab + static_cast<uint64_t>(t) * M * N;
-    rc = launch_raw(pa[t], kp, pb[t], kp, M, N, K, raw, 1, s);
-  }
-  if (rc == DS_OK) {
-    const uint64_t total = static_cast<uint64_t>(M) * N;
-    gemm_reduce_kernel<<<static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16)), 256, 0, s>>>(
-        slab, total, 3, ep_in, M, N);
-    if (cudaGetLastError() != cudaSuccess) rc = set_error(DS_E_CUDA, "gemm: reduce launch failed");
-  }
-  cudaFreeAsync(ah, s);
-  cudaFreeAsync(bh, s);
-  cudaFreeAsync(slab, s);
-  return rc;
-}
-
-}  // namespace
-
-int launch_gemm_tf32(const float* A, uint64_t lda, const float* B, uint64_t ldb, uint32_t M, uint32_t N, uint32_t K,
-                     const GemmEpilogue& ep_in, uint32_t splits, float* part, cudaStream_t s) {
+int launch_gemm(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32_t N, uint32_t K, const GemmTaps* taps,
+                const GemmEpilogue& ep_in, uint32_t splits, float* part, cudaStream_t s) {
   if (M == 0 || N == 0) return DS_OK;
-  if (exact_mode()) return launch_3xtf32(A, lda, B, ldb, M, N, K, ep_in, s);
+  GemmTaps tp;
+  if (taps) tp = *taps;
+  if (tp.n < 0 || tp.n > kMaxTaps) return set_error(DS_E_CONTRACT, "gemm: at most %d taps", kMaxTaps);
+  if (tp.n > 0 && !tp.per_z && (tp.kt == 0 || tp.kt % 8)) return set_error(DS_E_CONTRACT, "gemm: tap width %% 8");
+  if (exact_mode()) return launch_3xtf32(A, B, M, N, K, tp, ep_in, s);
   if (splits == 0) splits = 1;
-  const uint32_t max_splits = (K + kBK - 1) / kBK;
-  if (splits > max_splits) splits = max_splits;
+  if (tp.n > 0 && !tp.per_z) {
+    splits = 1;  // K is given by the taps
+  } else {
+    const uint32_t max_splits = std::max<uint32_t>(1, (K + kBK - 1) / kBK);
+    if (splits > max_splits) splits = max_splits;
+  }
   if (splits > 1 && !part) return set_error(DS_E_CONTRACT, "gemm: split-K needs a partial buffer");
   GemmEpilogue ep = ep_in;
-  if (splits > 1) {  // raw partial slabs [splits][M][N], reduced below with the epilogue
+  const uint32_t ntz = (tp.n > 0 && tp.per_z) ? tp.n : 1;
+  if (splits > 1) {  // raw partial slabs [tap][split][M][N], reduced below with the epilogue
     ep.D = part;
-    ep.ldd = N;
+    ep.raw = true;
     ep.split_stride = static_cast<uint64_t>(M) * N;
   }
-  DS_TRY(launch_raw(A, lda, B, ldb, M, N, K, ep, splits, s));
-  if (splits > 1) {
-    const uint64_t total = static_cast<uint64_t>(M) * N;
-    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-    gemm_reduce_kernel<<<blocks, 256, 0, s>>>(part, total, splits, ep_in, M, N);
-    DS_CUDA_TRY(cudaGetLastError());
-  }
+  DS_TRY(launch_any(A, B, ep, tp, M, N, K, splits, s));
+  if (splits > 1)
+    DS_TRY(launch_reduce(part, ntz, static_cast<uint64_t>(splits) * M * N, splits, static_cast<uint64_t>(M) * N,
+                         tp.per_z ? tp.d_col_step : 0, ep_in, M, N, s));
   return DS_OK;
+}
+
+int launch_gemm_tf32(const float* A, uint64_t lda, const float* B, uint64_t ldb, uint32_t M, uint32_t N, uint32_t K,
+                     const GemmEpilogue& ep, uint32_t splits, float* part, cudaStream_t s) {
+  GemmOperand a, b;
+  a.p = A, a.rows = M, a.cols = K, a.ld = lda;
+  b.p = B, b.rows = N, b.cols = K, b.ld = ldb;
+  return launch_gemm(a, b, M, N, K, nullptr, ep, splits, part, s);
 }
 
 }  // namespace dsb
