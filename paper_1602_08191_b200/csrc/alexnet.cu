@@ -135,21 +135,19 @@ AlexWs carve_ws(const ModelInfo& m, uint32_t R, void* base) {
   if (gate && *gate) return
 
 // conv1 im2col from CHW input rows (row r = X[idx[r]]): col[m][k], k = (c*11+ky)*11+kx,
-// ld 364 (k = 363 zero)
+// ld 364 (k = 363 zero). 32-bit index math (the caller bounds M * 364 < 2^31).
 __global__ void im2col_conv1_kernel(const float* __restrict__ X, const uint32_t* __restrict__ idx, uint32_t F,
-                                    uint32_t S, uint32_t Ho, uint64_t M, float* __restrict__ col, const uint32_t* gate) {
+                                    uint32_t S, uint32_t Ho, uint32_t M, float* __restrict__ col, const uint32_t* gate) {
   GATE;
-  const uint64_t total = M * 364;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint64_t m = i / 364;
-    const uint32_t k = static_cast<uint32_t>(i % 364);
+  const uint32_t total = M * 364, HH = Ho * Ho;
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
+    const uint32_t m = i / 364, k = i - m * 364;
     float v = 0.f;
     if (k < 363) {
-      const uint32_t c = k / 121, ky = (k / 11) % 11, kx = k % 11;
-      const uint32_t r = static_cast<uint32_t>(m / (1ull * Ho * Ho)), pix = static_cast<uint32_t>(m % (1ull * Ho * Ho));
-      const uint32_t oy = pix / Ho, ox = pix % Ho;
+      const uint32_t c = k / 121, kyx = k - c * 121, ky = kyx / 11, kx = kyx - ky * 11;
+      const uint32_t r = m / HH, pix = m - r * HH, oy = pix / Ho, ox = pix - oy * Ho;
       const uint64_t row = idx ? idx[r] : r;
-      v = __ldg(X + row * F + (1ull * c * S + oy * 4 + ky) * S + ox * 4 + kx);
+      v = __ldg(X + row * F + (c * S + oy * 4 + ky) * S + ox * 4 + kx);
     }
     col[i] = v;
   }
@@ -157,18 +155,18 @@ __global__ void im2col_conv1_kernel(const float* __restrict__ X, const uint32_t*
 
 // conv1 im2col transposed: colT[k][m] (ld ldT), for the weight gradient
 __global__ void im2colT_conv1_kernel(const float* __restrict__ X, const uint32_t* __restrict__ idx, uint32_t F,
-                                     uint32_t S, uint32_t Ho, uint64_t M, uint64_t ldT, float* __restrict__ colT,
+                                     uint32_t S, uint32_t Ho, uint32_t M, uint32_t ldT, float* __restrict__ colT,
                                      const uint32_t* gate) {
   GATE;
-  const uint64_t total = 363ull * M;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint32_t k = static_cast<uint32_t>(i / M);
-    const uint64_t m = i % M;
-    const uint32_t c = k / 121, ky = (k / 11) % 11, kx = k % 11;
-    const uint32_t r = static_cast<uint32_t>(m / (1ull * Ho * Ho)), pix = static_cast<uint32_t>(m % (1ull * Ho * Ho));
-    const uint32_t oy = pix / Ho, ox = pix % Ho;
+  const uint32_t HH = Ho * Ho;
+  // grid-stride over (k, m) with m fastest: consecutive threads read input pixels 4 apart
+  const uint32_t total = 363 * M;
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
+    const uint32_t k = i / M, m = i - k * M;
+    const uint32_t c = k / 121, kyx = k - c * 121, ky = kyx / 11, kx = kyx - ky * 11;
+    const uint32_t r = m / HH, pix = m - r * HH, oy = pix / Ho, ox = pix - oy * Ho;
     const uint64_t row = idx ? idx[r] : r;
-    colT[k * ldT + m] = __ldg(X + row * F + (1ull * c * S + oy * 4 + ky) * S + ox * 4 + kx);
+    colT[static_cast<uint64_t>(k) * ldT + m] = __ldg(X + row * F + (c * S + oy * 4 + ky) * S + ox * 4 + kx);
   }
 }
 
@@ -256,14 +254,13 @@ __global__ void unpack_wgrad_kernel(const float* __restrict__ dWp, uint32_t rows
 }
 
 // LRN across channels (NHWC, 4 channels per thread): y = x * (k + a/n sum_{|c'-c|<=2} x_c'^2)^-b
-__global__ void lrn_fwd_kernel(const float* __restrict__ x, uint64_t pixels, uint32_t C, float* __restrict__ y,
+__global__ void lrn_fwd_kernel(const float* __restrict__ x, uint32_t pixels, uint32_t C, float* __restrict__ y,
                                const uint32_t* gate) {
   GATE;
-  const uint32_t C4 = C / 4;
-  const uint64_t total = pixels * C4;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint32_t c0 = static_cast<uint32_t>(i % C4) * 4;
-    const float* px = x + (i / C4) * C;
+  const uint32_t C4 = C / 4, total = pixels * C4;
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
+    const uint32_t p = i / C4, c0 = (i - p * C4) * 4;
+    const float* px = x + static_cast<uint64_t>(p) * C;
     float v[8];  // x[c0-2 .. c0+5]
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -276,7 +273,7 @@ __global__ void lrn_fwd_kernel(const float* __restrict__ x, uint64_t pixels, uin
       const float ss = v[j] * v[j] + v[j + 1] * v[j + 1] + v[j + 2] * v[j + 2] + v[j + 3] * v[j + 3] + v[j + 4] * v[j + 4];
       o[j] = v[j + 2] * __powf(kLrnK + kLrnAlpha / kLrnN * ss, -kLrnBeta);
     }
-    *reinterpret_cast<float4*>(y + (i / C4) * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(y + static_cast<uint64_t>(p) * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -286,13 +283,11 @@ __global__ void lrn_fwd_kernel(const float* __restrict__ x, uint64_t pixels, uin
 __global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __restrict__ dy, uint32_t R, uint32_t H,
                                     uint32_t C, uint32_t opad, float* __restrict__ dx, const uint32_t* gate) {
   GATE;
-  const uint32_t C4 = C / 4, Ho = H + 2 * opad;
-  const uint64_t total = 1ull * R * H * H * C4;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint32_t c0 = static_cast<uint32_t>(i % C4) * 4;
-    const uint64_t p = i / C4;
-    const float* px = x + p * C;
-    const float* pd = dy + p * C;
+  const uint32_t C4 = C / 4, Ho = H + 2 * opad, HH = H * H, total = R * HH * C4;
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
+    const uint32_t p = i / C4, c0 = (i - p * C4) * 4;
+    const float* px = x + static_cast<uint64_t>(p) * C;
+    const float* pd = dy + static_cast<uint64_t>(p) * C;
     float xv[12], w[8], pw[8];  // x[c0-4 .. c0+7]; per j in [c0-2, c0+5]: dy x s^(-b-1), s^-b
 #pragma unroll
     for (int j = 0; j < 12; ++j) {
@@ -304,11 +299,11 @@ __global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __
       const int c = static_cast<int>(c0) - 2 + j;
       const float ss = xv[j] * xv[j] + xv[j + 1] * xv[j + 1] + xv[j + 2] * xv[j + 2] + xv[j + 3] * xv[j + 3] +
                        xv[j + 4] * xv[j + 4];
-      const float s = kLrnK + kLrnAlpha / kLrnN * ss;
-      const float sb = __powf(s, -kLrnBeta);
+      const float sc = kLrnK + kLrnAlpha / kLrnN * ss;
+      const float sb = __powf(sc, -kLrnBeta);
       pw[j] = sb;
       const float d = (c >= 0 && c < static_cast<int>(C)) ? __ldg(pd + c) : 0.f;
-      w[j] = d * xv[j + 2] * sb / s;
+      w[j] = d * xv[j + 2] * sb / sc;
     }
     float o[4];
 #pragma unroll
@@ -318,9 +313,9 @@ __global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __
       const float d = __ldg(pd + c0 + j);
       o[j] = xc > 0.f ? d * pw[j + 2] - 2.f * kLrnAlpha * kLrnBeta / kLrnN * xc * acc : 0.f;
     }
-    const uint32_t xx = static_cast<uint32_t>(p % H), yy = static_cast<uint32_t>((p / H) % H);
-    const uint64_t r = p / (1ull * H * H);
-    *reinterpret_cast<float4*>(dx + ((r * Ho + yy + opad) * Ho + xx + opad) * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
+    const uint32_t r = p / HH, pix = p - r * HH, yy = pix / H, xx = pix - yy * H;
+    *reinterpret_cast<float4*>(dx + (static_cast<uint64_t>(r * Ho + yy + opad) * Ho + xx + opad) * C + c0) =
+        make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -331,22 +326,20 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ in, uint32_t R, uin
                                    uint32_t ipad, uint32_t opad, int chw, float* __restrict__ out,
                                    uint8_t* __restrict__ arg, const uint32_t* gate) {
   GATE;
-  const uint32_t Hi = H + 2 * ipad, Hq = Ho + 2 * opad;
-  const uint64_t total = 1ull * R * Ho * Ho * C;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint32_t c = static_cast<uint32_t>(i % C);
-    const uint64_t p = i / C;
-    const uint32_t px = static_cast<uint32_t>(p % Ho), py = static_cast<uint32_t>((p / Ho) % Ho);
-    const uint64_t r = p / (1ull * Ho * Ho);
+  const uint32_t Hi = H + 2 * ipad, Hq = Ho + 2 * opad, HoHo = Ho * Ho, total = R * HoHo * C;
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
+    const uint32_t p = i / C, c = i - p * C;
+    const uint32_t r = p / HoHo, pix = p - r * HoHo, py = pix / Ho, px = pix - py * Ho;
     const uint32_t hs = py * 2, ws = px * 2, he = min(hs + 3, H), we = min(ws + 3, H);
     float best = -INFINITY;
     uint32_t bi = 0;
     for (uint32_t h = hs; h < he; ++h)
       for (uint32_t w = ws; w < we; ++w) {
-        const float v = in[((r * Hi + h + ipad) * Hi + w + ipad) * C + c];
+        const float v = in[(static_cast<uint64_t>(r * Hi + h + ipad) * Hi + w + ipad) * C + c];
         if (v > best) best = v, bi = (h - hs) * 3 + (w - ws);
       }
-    const uint64_t o = chw ? (r * C + c) * Ho * Ho + py * Ho + px : ((r * Hq + py + opad) * Hq + px + opad) * C + c;
+    const uint64_t o = chw ? (static_cast<uint64_t>(r) * C + c) * HoHo + pix
+                           : (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c;
     out[o] = best;
     arg[i] = static_cast<uint8_t>(bi);
   }
@@ -359,23 +352,21 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ dout, const uint8_t
                                    uint32_t H, uint32_t C, uint32_t Ho, uint32_t opad, int chw, uint32_t ipad,
                                    const float* __restrict__ mask, float* __restrict__ din, const uint32_t* gate) {
   GATE;
-  const uint32_t Hi = H + 2 * ipad, Hq = Ho + 2 * opad;
-  const uint64_t total = 1ull * R * H * H * C;
-  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
-    const uint32_t c = static_cast<uint32_t>(i % C);
-    const uint64_t p = i / C;
-    const uint32_t x = static_cast<uint32_t>(p % H), y = static_cast<uint32_t>((p / H) % H);
-    const uint64_t r = p / (1ull * H * H);
-    const uint64_t di = ((r * Hi + y + ipad) * Hi + x + ipad) * C + c;
+  const uint32_t Hi = H + 2 * ipad, Hq = Ho + 2 * opad, HH = H * H, total = R * HH * C;
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
+    const uint32_t p = i / C, c = i - p * C;
+    const uint32_t r = p / HH, pix = p - r * HH, y = pix / H, x = pix - y * H;
+    const uint64_t di = (static_cast<uint64_t>(r * Hi + y + ipad) * Hi + x + ipad) * C + c;
     float s = 0.f;
     if (!mask || mask[di] > 0.f) {
       const uint32_t py0 = y >= 2 ? (y - 1) / 2 : 0, py1 = min(y / 2, Ho - 1);
       const uint32_t px0 = x >= 2 ? (x - 1) / 2 : 0, px1 = min(x / 2, Ho - 1);
       for (uint32_t py = py0; py <= py1; ++py)
         for (uint32_t px = px0; px <= px1; ++px) {
-          const uint64_t a = ((r * Ho + py) * Ho + px) * C + c;
+          const uint32_t a = ((r * Ho + py) * Ho + px) * C + c;
           if (arg[a] == (y - py * 2) * 3 + (x - px * 2))
-            s += dout[chw ? (r * C + c) * Ho * Ho + py * Ho + px : ((r * Hq + py + opad) * Hq + px + opad) * C + c];
+            s += dout[chw ? (static_cast<uint64_t>(r) * C + c) * Ho * Ho + py * Ho + px
+                          : (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c];
         }
     }
     din[di] = s;
@@ -424,23 +415,36 @@ __global__ void alex_loss_mean_kernel(const double* __restrict__ loss_rows, uint
   *loss_out = l;
 }
 
-// column sums of d[rows][N] (ld) -> part[block][N]; then fixed-order final sum * scale
+// column sums of d[rows][N] (ld): block (column tile of 32, part) with 8 row lanes per
+// column, reduced in shared memory -> part[part][N]; then one warp per column sums the parts
+// in a fixed order (deterministic) and scales
 __global__ void colsum_part_kernel(const float* __restrict__ d, uint64_t rows, uint32_t N, uint64_t ld,
-                                   uint64_t rows_per_block, float* __restrict__ part, const uint32_t* gate) {
+                                   uint64_t rows_per_part, float* __restrict__ part, const uint32_t* gate) {
   GATE;
-  const uint64_t r0 = blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
-  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (uint64_t r = r0; r < r1; ++r) s += d[r * ld + n];
-    part[1ull * blockIdx.y * N + n] = s;
+  __shared__ float red[8][33];
+  const uint32_t n = blockIdx.x * 32 + threadIdx.x;
+  const uint64_t r0 = blockIdx.y * rows_per_part, r1 = min(rows, r0 + rows_per_part);
+  float s = 0.f;
+  if (n < N)
+    for (uint64_t r = r0 + threadIdx.y; r < r1; r += 8) s += d[r * ld + n];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += red[j][threadIdx.x];
+    part[1ull * blockIdx.y * N + n] = t;
   }
 }
 __global__ void colsum_final_kernel(const float* __restrict__ part, uint32_t nparts, uint32_t N, float scale,
                                     float* __restrict__ out, uint32_t* flags, const uint32_t* gate) {
   GATE;
-  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (uint32_t p = 0; p < nparts; ++p) s += part[1ull * p * N + n];
+  const uint32_t n = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (n >= N) return;
+  float s = 0.f;
+  for (uint32_t p = lane; p < nparts; p += 32) s += part[1ull * p * N + n];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
     const float v = s * scale;
     if (!isfinite(v)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
     out[n] = v;
@@ -531,11 +535,13 @@ int transpose(const Ctx& c, const float* in, uint64_t rows, uint32_t cols, uint6
 
 int colsum(const Ctx& c, const float* d, uint64_t rows, uint32_t N, uint64_t ld, float scale, float* out, float* bpart) {
   const cudaStream_t s_ = c.s;
-  const uint32_t nparts = static_cast<uint32_t>(std::min<uint64_t>(512, std::max<uint64_t>(1, rows / 64)));
-  const uint64_t rpb = (rows + nparts - 1) / nparts;
-  dim3 grid((N + 127) / 128, nparts);
-  colsum_part_kernel<<<grid, 128, 0, c.s>>>(d, rows, N, ld, rpb, bpart, c.gate);
-  colsum_final_kernel<<<(N + 127) / 128, 128, 0, c.s>>>(bpart, nparts, N, scale, out, c.flags, c.gate);
+  const uint32_t ntile = (N + 31) / 32;
+  // about 4 blocks per SM, parts of >= 64 rows; bpart holds 4096 * 512 floats
+  uint32_t nparts = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(1, 592 / ntile), (rows + 63) / 64));
+  nparts = std::min<uint32_t>(nparts, (4096u * 512u) / N);
+  const uint64_t rpp = (rows + nparts - 1) / nparts;
+  colsum_part_kernel<<<dim3(ntile, nparts), dim3(32, 8), 0, c.s>>>(d, rows, N, ld, rpp, bpart, c.gate);
+  colsum_final_kernel<<<(N + 7) / 8, 256, 0, c.s>>>(bpart, nparts, N, scale, out, c.flags, c.gate);
   KDONE(2);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
@@ -659,15 +665,15 @@ int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint3
   DS_TRY(zero(c, w.a4p, G3 * 384));
   DS_TRY(zero(c, w.a5p, G3 * 256));
   // conv1 (explicit im2col on the CHW input) + relu, LRN1, pool1 -> p1p (pad 2)
-  im2col_conv1_kernel<<<nblk(M1 * 364), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, M1, w.col, gate);
+  im2col_conv1_kernel<<<nblk(M1 * 364), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, static_cast<uint32_t>(M1), w.col, gate);
   KDONE(1);
   DS_TRY(gemm(c, w.col, 364, w.w1p, 364, w.a1, 96, static_cast<uint32_t>(M1), 96, 364, 1.f, P + L[0].b_off, true));
-  lrn_fwd_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, M1, 96, w.n1, gate);
+  lrn_fwd_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, static_cast<uint32_t>(M1), 96, w.n1, gate);
   maxpool_fwd_kernel<<<nblk(M2 * 96), 256, 0, s>>>(w.n1, R, sh.H1, 96, sh.P1, 0, 2, 0, w.p1p, w.arg1, gate);
   KDONE(2);
   // conv2 + relu -> a2 (unpadded), LRN2, pool2 -> p2p (pad 1)
   DS_TRY(conv_fwd(c, conv_spec(sh, 0), R, w.p1p, w.wp[0], P + L[1].b_off, w.a2, false));
-  lrn_fwd_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, M2, 256, w.n2, gate);
+  lrn_fwd_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, static_cast<uint32_t>(M2), 256, w.n2, gate);
   maxpool_fwd_kernel<<<nblk(1ull * R * sh.P2 * sh.P2 * 256), 256, 0, s>>>(w.n2, R, sh.P1, 256, sh.P2, 0, 1, 0, w.p2p,
                                                                          w.arg2, gate);
   KDONE(2);
@@ -714,6 +720,8 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   const uint64_t M1 = 1ull * R * sh.H1 * sh.H1, M2 = 1ull * R * sh.P1 * sh.P1, M3 = 1ull * R * sh.P2 * sh.P2;
   const uint64_t G2 = 1ull * R * sh.Hp2 * sh.Hp2, G3 = 1ull * R * sh.Hp3 * sh.Hp3;
   const float inv_b = 1.f / static_cast<float>(R);
+  if (M1 * 364 >= (1ull << 31)) return set_error(DS_E_CONTRACT, "alexnet: at most %llu rows per call",
+                                                 static_cast<unsigned long long>((1ull << 31) / (364 * sh.H1 * sh.H1)));
   t_launches = 0;
   DS_TRY(alex_forward(m, P, X, idx, R, w, c));
   softmax_ce_warp_kernel<<<(R + 7) / 8, 256, 0, s>>>(w.z, sh.Cp, y, idx, R, sh.C, w.loss_rows, grad ? w.dz : nullptr,
@@ -791,7 +799,8 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   DS_TRY(colsum(c, w.dc1, M1, 96, 96, inv_b, grad + L[0].b_off, w.bpart));
   const uint32_t M1p = up4(static_cast<uint32_t>(M1));
   DS_TRY(transpose(c, w.dc1, M1, 96, 96, w.trA, M1p));
-  im2colT_conv1_kernel<<<nblk(363 * M1), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, M1, M1p, w.col, gate);
+  im2colT_conv1_kernel<<<nblk(363 * M1), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, static_cast<uint32_t>(M1), M1p, w.col,
+                                                      gate);
   KDONE(1);
   DS_TRY(gemm(c, w.trA, M1p, w.col, M1p, grad + L[0].w_off, 363, 96, 363, static_cast<uint32_t>(M1), inv_b, nullptr,
               false));

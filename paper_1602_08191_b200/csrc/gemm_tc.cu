@@ -37,7 +37,7 @@ struct GemmSmem {
   static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;  // 8 / 6 / 4 for BN 64/128/256
   static constexpr uint32_t TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;  // power of 2
 };
 
 // SWIZZLE_128B K-major descriptor: 8-row x 128 B atoms, atoms 1024 B apart (SBO); the
@@ -301,10 +301,14 @@ int launch_bn(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep
 
 int launch_any(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep, const GemmTaps& tp, uint32_t M,
                uint32_t N, uint32_t K, uint32_t splits, cudaStream_t s) {
-  const uint32_t bn = gemm_pick_bn(N);
-  if (bn == 64) return launch_bn<64>(A, B, ep, tp, M, N, K, splits, s);
-  if (bn == 128) return launch_bn<128>(A, B, ep, tp, M, N, K, splits, s);
-  return launch_bn<256>(A, B, ep, tp, M, N, K, splits, s);
+  switch (gemm_pick_bn(N)) {
+    case 48: return launch_bn<48>(A, B, ep, tp, M, N, K, splits, s);
+    case 64: return launch_bn<64>(A, B, ep, tp, M, N, K, splits, s);
+    case 96: return launch_bn<96>(A, B, ep, tp, M, N, K, splits, s);
+    case 128: return launch_bn<128>(A, B, ep, tp, M, N, K, splits, s);
+    case 192: return launch_bn<192>(A, B, ep, tp, M, N, K, splits, s);
+    default: return launch_bn<256>(A, B, ep, tp, M, N, K, splits, s);
+  }
 }
 
 int launch_reduce(const float* slabs, uint32_t ntaps, uint64_t tap_stride, uint32_t nparts, uint64_t part_stride,
@@ -366,10 +370,11 @@ int launch_3xtf32(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32
 
 }  // namespace
 
-// the tile width with the least padding past N (ties: the wider tile)
+// the tile width (MMA N) with the least padding past N; ties go to the wider tile, which
+// re-reads the A operand fewer times
 uint32_t gemm_pick_bn(uint32_t N) {
   uint32_t best = 256, waste = (N + 255) / 256 * 256 - N;
-  for (uint32_t bn : {128u, 64u}) {
+  for (uint32_t bn : {192u, 128u, 96u, 64u, 48u}) {
     const uint32_t w = (N + bn - 1) / bn * bn - N;
     if (w < waste) best = bn, waste = w;
   }

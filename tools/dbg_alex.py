@@ -8,10 +8,12 @@ import test_gpu_alexnet as t
 import torch
 from paper_1602_08191_b200 import _lib as L
 orc = Oracle("dso")
-for side, c, batch, scale in [(55, 5, 1, 5.0), (55, 5, 13, 5.0), (55, 5, 13, 1.0), (67, 10, 8, 1.0)]:
+import os
+cases = [(224, 1000, 2, 1.0)] if os.environ.get('DBG_FULL') else [(55, 5, 1, 5.0), (55, 5, 13, 5.0), (55, 5, 13, 1.0), (67, 10, 8, 1.0)]
+for side, c, batch, scale in cases:
     m = ModelSpec.alexnet(side, c)
-    w = orc.init_params(m, 3)
-    X, y = orc.gen_synthetic(batch, 3 * side * side, c, 1.0, 1.0, 21)
+    w = orc.init_params(m, 4 if side == 224 else 3)
+    X, y = orc.gen_synthetic(batch, 3 * side * side, c, 1.0, 1.0, 5 if side == 224 else 21)
     X = np.ascontiguousarray(X * scale, dtype=np.float32)
     lr, gr = orc.loss_and_grad(m, w, X, y)
     lg, gg, flags = t.gpu_lag(torch, L, t.desc(L, side, c), w, X, y)
