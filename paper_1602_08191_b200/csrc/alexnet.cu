@@ -14,7 +14,9 @@
 //   wgrad    dW[t]  = doutT . inT(shifted by d_t)^T           (one output per tap, split-K)
 // wgrad contracts over pixels, so it reads transposed (pixel-contiguous) copies of dout and
 // the padded input: tf32 MMA operands must be K-major. conv1 (11x11 stride 4 on the CHW
-// input) keeps an explicit im2col. LRN, max-pooling, softmax cross-entropy and the bias
+// input) becomes a 3x3 stride-1 convolution by space-to-depth: the input is regrouped into
+// 4x4 pixel blocks (48 channels on a ceil(S/4) grid) and the 11x11 kernel zero-extended to
+// 12x12 (1.19x the MACs, no im2col). LRN, max-pooling, softmax cross-entropy and the bias
 // sums are HBM-bound elementwise kernels. The gradient is the batch mean (scale 1/R in the
 // GEMM epilogues), rounded to f32 like the reference's Grad = f32(sum / b). Dropout is
 // omitted (deterministic; see the oracle).
@@ -39,6 +41,7 @@ inline uint32_t up4(uint32_t v) { return (v + 3) & ~3u; }
 
 struct Shape {
   uint32_t S, H1, P1, P2, P5, C, Cp;
+  uint32_t Hs;        // side of the space-to-depth grid of the input (conv1)
   uint32_t Hp2, Hp3;  // padded sides of the conv2 input (pad 2) and the conv3..5 maps (pad 1)
   uint64_t q5;        // fc6 fan-in
 };
@@ -53,6 +56,7 @@ Shape shape_of(const ModelInfo& m) {
   s.P5 = pooled(s.P2);
   s.C = m.n_classes;
   s.Cp = up4(s.C);
+  s.Hs = (s.S + 3) / 4;
   s.Hp2 = s.P1 + 4;
   s.Hp3 = s.P2 + 2;
   s.q5 = 256ull * s.P5 * s.P5;
@@ -67,6 +71,9 @@ struct ConvSpec {
   uint32_t KK() const { return K * K; }
   uint32_t Kg() const { return K * K * cig(); }
 };
+
+// conv1 after space-to-depth: 48 -> 96, 3x3 taps on the Hs grid, outputs at [1, 1 + H1)
+ConvSpec conv1_spec(const Shape& s) { return ConvSpec{48, 96, 3, 1, 1, s.H1, s.Hs}; }
 
 ConvSpec conv_spec(const Shape& s, int l) {  // l = 0..3 -> conv2..conv5
   static const ConvSpec kConv[4] = {{96, 256, 5, 2, 2, 0, 0}, {256, 384, 3, 1, 1, 0, 0}, {384, 384, 3, 1, 2, 0, 0},
@@ -83,8 +90,8 @@ struct AlexWs {
   float *a1, *n1, *p1p, *a2, *n2, *p2p, *a3p, *a4p, *a5p, *p5, *h6, *h7, *z, *dz;
   uint8_t *arg1, *arg2, *arg5;
   // backward
-  float *dh7, *dh6, *dp5, *dc5p, *dc4p, *dc3p, *dp2p, *dn2, *dc2p, *dp1, *dn1, *dc1;
-  float *col, *trA, *trB, *part, *wtmp, *bpart;
+  float *dh7, *dh6, *dp5, *dc5p, *dc4p, *dc3p, *dp2p, *dn2, *dc2p, *dp1, *dn1, *dc1p;
+  float *xs, *trA, *trB, *part, *wtmp, *bpart;
   float *w1p, *wp[4], *wpT[4], *w6T, *w7T, *w8T, *zT, *h7T, *h6T, *p5T, *dh7T, *dh6T;
   double* loss_rows;
   uint64_t end;
@@ -98,7 +105,7 @@ AlexWs carve_ws(const ModelInfo& m, uint32_t R, void* base) {
   uint8_t* b = static_cast<uint8_t*>(base);
   const Shape s = shape_of(m);
   const uint64_t M1 = 1ull * R * s.H1 * s.H1, M2 = 1ull * R * s.P1 * s.P1, M3 = 1ull * R * s.P2 * s.P2;
-  const uint64_t G2 = 1ull * R * s.Hp2 * s.Hp2, G3 = 1ull * R * s.Hp3 * s.Hp3;  // padded grids
+  const uint64_t G1 = 1ull * R * s.Hs * s.Hs, G2 = 1ull * R * s.Hp2 * s.Hp2, G3 = 1ull * R * s.Hp3 * s.Hp3;
   const uint64_t Q5 = R * s.q5;
   const uint32_t Rp = up4(R);
   uint64_t off = 0;
@@ -110,12 +117,12 @@ AlexWs carve_ws(const ModelInfo& m, uint32_t R, void* base) {
   f(ws.h6, 4096ull * R), f(ws.h7, 4096ull * R), f(ws.z, 1ull * s.Cp * R), f(ws.dz, 1ull * s.Cp * R);
   f(ws.dh7, 4096ull * R), f(ws.dh6, 4096ull * R), f(ws.dp5, Q5);
   f(ws.dc5p, G3 * 256), f(ws.dc4p, G3 * 384), f(ws.dc3p, G3 * 384), f(ws.dp2p, G3 * 256), f(ws.dn2, M2 * 256);
-  f(ws.dc2p, G2 * 256), f(ws.dp1, M2 * 96), f(ws.dn1, M1 * 96), f(ws.dc1, M1 * 96);
-  f(ws.col, 1ull * up4(static_cast<uint32_t>(M1)) * 364);
-  const uint64_t trA = std::max({384 * (G3 + 4), 256 * (G2 + 4), 96 * (M1 + 4)});
-  const uint64_t trB = 4 * std::max({384 * (G3 + 4), 96 * (G2 + 4)});
+  f(ws.dc2p, G2 * 256), f(ws.dp1, M2 * 96), f(ws.dn1, M1 * 96), f(ws.dc1p, G1 * 96);
+  f(ws.xs, G1 * 48);
+  const uint64_t trA = std::max({384 * (G3 + 8), 256 * (G2 + 8), 96 * (G1 + 8)});
+  const uint64_t trB = 4 * std::max({384 * (G3 + 8), 96 * (G2 + 8), 48 * (G1 + 8)});
   f(ws.trA, trA), f(ws.trB, trB), f(ws.part, kPartFloats), f(ws.wtmp, 384ull * 2304), f(ws.bpart, 4096ull * 512);
-  f(ws.w1p, 96ull * 364);
+  f(ws.w1p, 96ull * 9 * 48);
   for (int l = 0; l < 4; ++l) {
     const ConvSpec c = conv_spec(s, l);
     f(ws.wp[l], 1ull * c.Cout * c.Kg());
@@ -134,39 +141,47 @@ AlexWs carve_ws(const ModelInfo& m, uint32_t R, void* base) {
 #define GATE \
   if (gate && *gate) return
 
-// conv1 im2col from CHW input rows (row r = X[idx[r]]): col[m][k], k = (c*11+ky)*11+kx,
-// ld 364 (k = 363 zero). 32-bit index math (the caller bounds M * 364 < 2^31).
-__global__ void im2col_conv1_kernel(const float* __restrict__ X, const uint32_t* __restrict__ idx, uint32_t F,
-                                    uint32_t S, uint32_t Ho, uint32_t M, float* __restrict__ col, const uint32_t* gate) {
+// space-to-depth of the CHW input rows (row r = X[idx[r]]): xs[r][ys][xs][(dy*4+dx)*3+c] =
+// X[c][4ys+dy][4xs+dx] (0 past the image), on the Hs x Hs grid
+__global__ void s2d_kernel(const float* __restrict__ X, const uint32_t* __restrict__ idx, uint32_t F, uint32_t S,
+                           uint32_t R, uint32_t Hs, float* __restrict__ xs, const uint32_t* gate) {
   GATE;
-  const uint32_t total = M * 364, HH = Ho * Ho;
+  const uint32_t HH = Hs * Hs, total = R * HH * 48;
   for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
-    const uint32_t m = i / 364, k = i - m * 364;
+    const uint32_t p = i / 48, ch = i - p * 48;
+    const uint32_t r = p / HH, pix = p - r * HH, ys = pix / Hs, xq = pix - ys * Hs;
+    const uint32_t blk = ch / 3, c = ch - blk * 3, dy = blk / 4, dx = blk - dy * 4;
+    const uint32_t y = ys * 4 + dy, x = xq * 4 + dx;
     float v = 0.f;
-    if (k < 363) {
-      const uint32_t c = k / 121, kyx = k - c * 121, ky = kyx / 11, kx = kyx - ky * 11;
-      const uint32_t r = m / HH, pix = m - r * HH, oy = pix / Ho, ox = pix - oy * Ho;
+    if (y < S && x < S) {
       const uint64_t row = idx ? idx[r] : r;
-      v = __ldg(X + row * F + (c * S + oy * 4 + ky) * S + ox * 4 + kx);
+      v = __ldg(X + row * F + (c * S + y) * S + x);
     }
-    col[i] = v;
+    xs[i] = v;
   }
 }
 
-// conv1 im2col transposed: colT[k][m] (ld ldT), for the weight gradient
-__global__ void im2colT_conv1_kernel(const float* __restrict__ X, const uint32_t* __restrict__ idx, uint32_t F,
-                                     uint32_t S, uint32_t Ho, uint32_t M, uint32_t ldT, float* __restrict__ colT,
-                                     const uint32_t* gate) {
+// conv1 weights [96][3][11][11] -> Wp [96][9 taps (ty,tx)][48 (dy,dx,c)], zero past 11
+__global__ void pack_conv1_s2d_kernel(const float* __restrict__ W, float* __restrict__ Wp, const uint32_t* gate) {
   GATE;
-  const uint32_t HH = Ho * Ho;
-  // grid-stride over (k, m) with m fastest: consecutive threads read input pixels 4 apart
-  const uint32_t total = 363 * M;
-  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
-    const uint32_t k = i / M, m = i - k * M;
-    const uint32_t c = k / 121, kyx = k - c * 121, ky = kyx / 11, kx = kyx - ky * 11;
-    const uint32_t r = m / HH, pix = m - r * HH, oy = pix / Ho, ox = pix - oy * Ho;
-    const uint64_t row = idx ? idx[r] : r;
-    colT[static_cast<uint64_t>(k) * ldT + m] = __ldg(X + row * F + (c * S + oy * 4 + ky) * S + ox * 4 + kx);
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < 96 * 432; i += gridDim.x * 256) {
+    const uint32_t co = i / 432, rem = i - co * 432, t = rem / 48, ch = rem - t * 48;
+    const uint32_t ty = t / 3, tx = t - ty * 3, blk = ch / 3, c = ch - blk * 3, dy = blk / 4, dx = blk - dy * 4;
+    const uint32_t ky = ty * 4 + dy, kx = tx * 4 + dx;
+    Wp[i] = (ky < 11 && kx < 11) ? W[((co * 3 + c) * 11 + ky) * 11 + kx] : 0.f;
+  }
+}
+
+// packed conv1 weight gradient [96][9][48] -> Caffe [96][3][11][11]
+__global__ void unpack_conv1_s2d_kernel(const float* __restrict__ dWp, float* __restrict__ grad, uint32_t* flags,
+                                        const uint32_t* gate) {
+  GATE;
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < 96 * 363; i += gridDim.x * 256) {
+    const uint32_t co = i / 363, rem = i - co * 363, c = rem / 121, kyx = rem - c * 121, ky = kyx / 11, kx = kyx - ky * 11;
+    const uint32_t t = (ky / 4) * 3 + kx / 4, ch = ((ky % 4) * 4 + kx % 4) * 3 + c;
+    const float v = dWp[co * 432 + t * 48 + ch];
+    if (!isfinite(v)) atomicOr(flags, DS_FLAG_GRAD_NONFINITE);
+    grad[i] = v;
   }
 }
 
@@ -190,26 +205,27 @@ __global__ void transpose_kernel(const float* __restrict__ in, uint64_t rows, ui
   }
 }
 
-// Four pixel-shifted transposed copies: out[s][c][m] = in[m + s][c] (0 past the last row),
+// Four pixel-shifted transposed copies: out[s][c][m] = in[m - s][c] (0 outside the rows),
 // m < ldT. TMA needs 16-byte aligned inner coordinates, so a weight-gradient tap with pixel
-// shift d reads copy (d mod 4) at the aligned offset d - (d mod 4).
+// shift d reads copy s = (-d mod 4) at the aligned offset d + s: the shifted column is never
+// left of the unshifted one, so no needed pixel falls before column 0.
 __global__ void transpose_shift4_kernel(const float* __restrict__ in, uint64_t rows, uint32_t cols,
                                         float* __restrict__ out, uint64_t ldT, const uint32_t* gate) {
   GATE;
-  __shared__ float tile[35][33];
-  const uint64_t r0 = blockIdx.x * 32ull;
+  __shared__ float tile[35][33];  // rows r0-3 .. r0+31
+  const int64_t r0 = blockIdx.x * 32ll;
   const uint32_t c0 = blockIdx.y * 32;
   for (uint32_t ty = threadIdx.y; ty < 35; ty += 8) {
-    const uint64_t r = r0 + ty;
+    const int64_t r = r0 - 3 + ty;
     const uint32_t c = c0 + threadIdx.x;
-    tile[ty][threadIdx.x] = (r < rows && c < cols) ? in[r * cols + c] : 0.f;
+    tile[ty][threadIdx.x] = (r >= 0 && r < static_cast<int64_t>(rows) && c < cols) ? in[r * cols + c] : 0.f;
   }
   __syncthreads();
   for (uint32_t sft = 0; sft < 4; ++sft)
     for (uint32_t ty = threadIdx.y; ty < 32; ty += 8) {
       const uint32_t c = c0 + ty;
       const uint64_t m = r0 + threadIdx.x;
-      if (c < cols && m < ldT) out[(sft * cols + c) * ldT + m] = tile[threadIdx.x + sft][ty];
+      if (c < cols && m < ldT) out[(sft * cols + c) * ldT + m] = tile[threadIdx.x + 3 - sft][ty];
     }
 }
 
@@ -227,15 +243,6 @@ __global__ void pack_conv_kernel(const float* __restrict__ W, uint32_t Cout, uin
     Wp[1ull * co * Kg + k] = v;
     const uint32_t gi = co / cog, cl = co % cog;
     WpT[1ull * gi * Kg * cog + 1ull * k * cog + cl] = v;
-  }
-}
-
-// conv1 weights [96][363] -> [96][364] (zero pad)
-__global__ void pack_conv1_kernel(const float* __restrict__ W, float* __restrict__ Wp, const uint32_t* gate) {
-  GATE;
-  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < 96 * 364; i += gridDim.x * 256) {
-    const uint32_t co = i / 364, k = i % 364;
-    Wp[i] = k < 363 ? W[co * 363 + k] : 0.f;
   }
 }
 
@@ -279,11 +286,12 @@ __global__ void lrn_fwd_kernel(const float* __restrict__ x, uint32_t pixels, uin
 
 // LRN backward (scale recomputed from x), masked by the ReLU that produced x (x > 0):
 // dx_c = dy_c s_c^-b - (2 a b / n) x_c sum_{|j-c|<=2} dy_j x_j s_j^(-b-1)
-// dx is written at the same pixel of a map padded by `opad` (side H + 2 opad).
+// dx is written at pixel (y + opad, x + opad) of a map of side Ho.
 __global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __restrict__ dy, uint32_t R, uint32_t H,
-                                    uint32_t C, uint32_t opad, float* __restrict__ dx, const uint32_t* gate) {
+                                    uint32_t C, uint32_t opad, uint32_t Ho, float* __restrict__ dx,
+                                    const uint32_t* gate) {
   GATE;
-  const uint32_t C4 = C / 4, Ho = H + 2 * opad, HH = H * H, total = R * HH * C4;
+  const uint32_t C4 = C / 4, HH = H * H, total = R * HH * C4;
   for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
     const uint32_t p = i / C4, c0 = (i - p * C4) * 4;
     const float* px = x + static_cast<uint64_t>(p) * C;
@@ -609,10 +617,10 @@ int conv_dgrad(const Ctx& c, const ConvSpec& cs, uint32_t R, const float* dout, 
 }
 
 // conv weight gradient from pixel-contiguous maps doutT [Cout][ldT] and the four shifted
-// copies inT4 [4][Cin][ldT] (padded grid): packed [Cout][KK][cig] into wtmp, then Caffe
-// order into grad
+// copies inT4 [4][Cin][ldT] (padded grid, ldT >= G + 3): packed [Cout][KK][cig] into wtmp,
+// then Caffe order into grad
 int conv_wgrad(const Ctx& c, const ConvSpec& cs, uint32_t R, const float* doutT, const float* inT4, uint64_t ldT,
-               float scale, float* wtmp, float* grad) {
+               float scale, float* wtmp, float* grad, bool s2d = false) {
   const cudaStream_t s_ = c.s;
   const uint32_t G = R * cs.Hp * cs.Hp, Kg = cs.Kg(), cog = cs.cog(), cig = cs.cig();
   for (uint32_t gi = 0; gi < cs.g; ++gi) {
@@ -621,19 +629,22 @@ int conv_wgrad(const Ctx& c, const ConvSpec& cs, uint32_t R, const float* doutT,
     tp.per_z = 1;
     tp.d_col_step = cig;
     for (uint32_t t = 0; t < cs.KK(); ++t) {
-      const int32_t d = shift(cs, t), sft = ((d % 4) + 4) % 4;
+      const int32_t d = shift(cs, t), sft = (((-d) % 4) + 4) % 4;
       tp.a_row[t] = 0;
       tp.a_col[t] = 0;
       tp.b_row[t] = sft * static_cast<int32_t>(cs.Cin) + static_cast<int32_t>(gi * cig);
-      tp.b_col[t] = d - sft;
+      tp.b_col[t] = d + sft;
     }
-    const GemmOperand A{doutT + 1ull * gi * cog * ldT, cog, G, ldT}, B{inT4, 4ull * cs.Cin, G, ldT};
+    const GemmOperand A{doutT + 1ull * gi * cog * ldT, cog, G, ldT}, B{inT4, 4ull * cs.Cin, G + 3, ldT};
     const uint32_t sp = pick_splits(cog, cig, G, cs.KK());
     GemmEpilogue ep = epi(c, wtmp + 1ull * gi * cog * Kg, Kg, scale, nullptr, false);
     DS_TRY(launch_gemm(A, B, cog, cig, G, &tp, ep, sp, c.part, c.s));
     KDONE(sp > 1 ? 2 : 1);
   }
-  unpack_wgrad_kernel<<<nblk(1ull * cs.Cout * Kg), 256, 0, c.s>>>(wtmp, cs.Cout, cig, cs.K, grad, c.flags, c.gate);
+  if (s2d)
+    unpack_conv1_s2d_kernel<<<nblk(96 * 363), 256, 0, c.s>>>(wtmp, grad, c.flags, c.gate);
+  else
+    unpack_wgrad_kernel<<<nblk(1ull * cs.Cout * Kg), 256, 0, c.s>>>(wtmp, cs.Cout, cig, cs.K, grad, c.flags, c.gate);
   KDONE(1);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
@@ -650,7 +661,7 @@ int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint3
   const uint64_t G2 = 1ull * R * sh.Hp2 * sh.Hp2, G3 = 1ull * R * sh.Hp3 * sh.Hp3;
   cudaStream_t s = c.s;
   const uint32_t* gate = c.gate;
-  pack_conv1_kernel<<<nblk(96 * 364), 256, 0, s>>>(P + L[0].w_off, w.w1p, gate);
+  pack_conv1_s2d_kernel<<<nblk(96 * 432), 256, 0, s>>>(P + L[0].w_off, w.w1p, gate);
   KDONE(1);
   for (int l = 0; l < 4; ++l) {
     const ConvSpec cs = conv_spec(sh, l);
@@ -664,10 +675,10 @@ int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint3
   DS_TRY(zero(c, w.a3p, G3 * 384));
   DS_TRY(zero(c, w.a4p, G3 * 384));
   DS_TRY(zero(c, w.a5p, G3 * 256));
-  // conv1 (explicit im2col on the CHW input) + relu, LRN1, pool1 -> p1p (pad 2)
-  im2col_conv1_kernel<<<nblk(M1 * 364), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, static_cast<uint32_t>(M1), w.col, gate);
+  // conv1 (space-to-depth, 3x3 taps) + relu, LRN1, pool1 -> p1p (pad 2)
+  s2d_kernel<<<nblk(1ull * R * sh.Hs * sh.Hs * 48), 256, 0, s>>>(X, idx, F, sh.S, R, sh.Hs, w.xs, gate);
   KDONE(1);
-  DS_TRY(gemm(c, w.col, 364, w.w1p, 364, w.a1, 96, static_cast<uint32_t>(M1), 96, 364, 1.f, P + L[0].b_off, true));
+  DS_TRY(conv_fwd(c, conv1_spec(sh), R, w.xs, w.w1p, P + L[0].b_off, w.a1, false));
   lrn_fwd_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, static_cast<uint32_t>(M1), 96, w.n1, gate);
   maxpool_fwd_kernel<<<nblk(M2 * 96), 256, 0, s>>>(w.n1, R, sh.H1, 96, sh.P1, 0, 2, 0, w.p1p, w.arg1, gate);
   KDONE(2);
@@ -720,8 +731,9 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   const uint64_t M1 = 1ull * R * sh.H1 * sh.H1, M2 = 1ull * R * sh.P1 * sh.P1, M3 = 1ull * R * sh.P2 * sh.P2;
   const uint64_t G2 = 1ull * R * sh.Hp2 * sh.Hp2, G3 = 1ull * R * sh.Hp3 * sh.Hp3;
   const float inv_b = 1.f / static_cast<float>(R);
-  if (M1 * 364 >= (1ull << 31)) return set_error(DS_E_CONTRACT, "alexnet: at most %llu rows per call",
-                                                 static_cast<unsigned long long>((1ull << 31) / (364 * sh.H1 * sh.H1)));
+  if (1ull * R * sh.Hs * sh.Hs * 96 >= (1ull << 31))
+    return set_error(DS_E_CONTRACT, "alexnet: at most %llu rows per call",
+                     static_cast<unsigned long long>((1ull << 31) / (96ull * sh.Hs * sh.Hs)));
   t_launches = 0;
   DS_TRY(alex_forward(m, P, X, idx, R, w, c));
   softmax_ce_warp_kernel<<<(R + 7) / 8, 256, 0, s>>>(w.z, sh.Cp, y, idx, R, sh.C, w.loss_rows, grad ? w.dz : nullptr,
@@ -757,6 +769,7 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   DS_TRY(zero(c, w.dc4p, G3 * 384));
   DS_TRY(zero(c, w.dc3p, G3 * 384));
   DS_TRY(zero(c, w.dc2p, G2 * 256));
+  DS_TRY(zero(c, w.dc1p, 1ull * R * sh.Hs * sh.Hs * 96));
   // pool5 backward (per-row CHW pooled map) with the ReLU5 mask (a5p) -> dc5p
   maxpool_bwd_kernel<<<nblk(M3 * 256), 256, 0, s>>>(w.dp5, w.arg5, R, sh.P2, 256, sh.P5, 0, 1, 1, w.a5p, w.dc5p,
                                                     gate);
@@ -765,7 +778,7 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   float* dout_maps[4] = {w.dc2p, w.dc3p, w.dc4p, w.dc5p};
   for (int l = 3; l >= 0; --l) {
     const ConvSpec cs = conv_spec(sh, l);
-    const uint64_t G = 1ull * R * cs.Hp * cs.Hp, ldT = up4(static_cast<uint32_t>(G));
+    const uint64_t G = 1ull * R * cs.Hp * cs.Hp, ldT = up4(static_cast<uint32_t>(G + 3));
     float* dout = dout_maps[l];
     // bias gradient (border rows are zero)
     DS_TRY(colsum(c, dout, G, cs.Cout, cs.Cout, inv_b, grad + L[l + 1].b_off, w.bpart));
@@ -785,25 +798,27 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp2p, true, nullptr));
       maxpool_bwd_kernel<<<nblk(M2 * 256), 256, 0, s>>>(w.dp2p, w.arg2, R, sh.P1, 256, sh.P2, 1, 0, 0, nullptr, w.dn2,
                                                         gate);
-      lrn_bwd_relu_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, w.dn2, R, sh.P1, 256, 2, w.dc2p, gate);
+      lrn_bwd_relu_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, w.dn2, R, sh.P1, 256, 2, sh.Hp2, w.dc2p, gate);
       KDONE(2);
-    } else {  // into pool1(LRN1(relu(conv1))): d(p1) unpadded, pool1 bwd, LRN1 bwd -> dc1
+    } else {  // into pool1(LRN1(relu(conv1))): d(p1) unpadded, pool1 bwd, LRN1 bwd -> dc1p
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp1, false, nullptr));
       maxpool_bwd_kernel<<<nblk(M1 * 96), 256, 0, s>>>(w.dp1, w.arg1, R, sh.H1, 96, sh.P1, 0, 0, 0, nullptr, w.dn1,
                                                        gate);
-      lrn_bwd_relu_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, w.dn1, R, sh.H1, 96, 0, w.dc1, gate);
+      lrn_bwd_relu_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, w.dn1, R, sh.H1, 96, 1, sh.Hs, w.dc1p, gate);
       KDONE(2);
     }
   }
-  // ---- conv1: bias and weight gradients (no data gradient) ---------------------------------
-  DS_TRY(colsum(c, w.dc1, M1, 96, 96, inv_b, grad + L[0].b_off, w.bpart));
-  const uint32_t M1p = up4(static_cast<uint32_t>(M1));
-  DS_TRY(transpose(c, w.dc1, M1, 96, 96, w.trA, M1p));
-  im2colT_conv1_kernel<<<nblk(363 * M1), 256, 0, s>>>(X, idx, F, sh.S, sh.H1, static_cast<uint32_t>(M1), M1p, w.col,
-                                                      gate);
-  KDONE(1);
-  DS_TRY(gemm(c, w.trA, M1p, w.col, M1p, grad + L[0].w_off, 363, 96, 363, static_cast<uint32_t>(M1), inv_b, nullptr,
-              false));
+  // ---- conv1: bias and weight gradients on the space-to-depth grid (no data gradient) ------
+  {
+    const ConvSpec cs = conv1_spec(sh);
+    const uint64_t G1 = 1ull * R * sh.Hs * sh.Hs, ldT = up4(static_cast<uint32_t>(G1 + 3));
+    DS_TRY(colsum(c, w.dc1p, G1, 96, 96, inv_b, grad + L[0].b_off, w.bpart));
+    DS_TRY(transpose(c, w.dc1p, G1, 96, 96, w.trA, ldT));
+    dim3 grid(static_cast<unsigned>((ldT + 31) / 32), (48 + 31) / 32);
+    transpose_shift4_kernel<<<grid, dim3(32, 8), 0, s>>>(w.xs, G1, 48, w.trB, ldT, gate);
+    KDONE(1);
+    DS_TRY(conv_wgrad(c, cs, R, w.trA, w.trB, ldT, inv_b, w.wtmp, grad + L[0].w_off, true));
+  }
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
