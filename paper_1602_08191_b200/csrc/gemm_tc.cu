@@ -2,14 +2,14 @@
 // D[M x N] = epilogue( A[M x K] . B[N x K]^T ), f32 operands in HBM, tf32 tcgen05 MMA,
 // f32 accumulation in TMEM.
 //
-// Pipeline (one output tile per CTA, 192 threads, warp-specialised):
+// Pipeline (one output tile per CTA, 256 threads, warp-specialised):
 //   warp 0: TMA producer. Two 2-D tensor maps (SWIZZLE_128B, 32 f32 = 128 B inner box)
 //           stream [128 x 32] A and [BN x 32] B k-slices into a kStages-deep smem ring
 //           (full/empty mbarriers). Tails beyond M, N, K are zero-filled by TMA.
 //   warp 1: one elected lane issues 4 tcgen05.mma kind::tf32 (K = 8 each) per stage and
 //           frees the stage with tcgen05.commit; after the last stage commits the
 //           accumulator-full barrier.
-//   warps 2-5: epilogue. Each warp reads its TMEM lane quadrant (32 rows) 32 columns at a
+//   warps 4-7: epilogue. Each warp reads its TMEM lane quadrant (32 rows) 32 columns at a
 //           time (tcgen05.ld 32x32b.x32) and applies scale, bias and ReLU, then stores
 //           row-major D with leading dimension ldd. With split-K (gridDim.z > 1) each
 //           split stores raw partials to its own slab, and gemm_reduce_kernel sums the
@@ -28,14 +28,23 @@
 namespace dsb {
 namespace {
 
-constexpr int kBM = 128, kBK = 32, kThreads = 192;
+// 8 warps: 0 TMA producer, 1 MMA issuer, 2-3 idle, 4-7 epilogue. A multiple of 4 warps
+// keeps CTA-relative warp % 4 equal to the SM sub-partition when two CTAs share an SM, so
+// each epilogue warp reads its own TMEM lane quadrant.
+constexpr int kBM = 128, kBK = 32, kThreads = 256;
 
 template <int BN>
 struct GemmSmem {
   static constexpr uint32_t A_BYTES = kBM * kBK * 4;  // 16 KB
   static constexpr uint32_t B_BYTES = BN * kBK * 4;
   static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;  // 8 / 6 / 4 for BN 64/128/256
+  // BN <= 128: ~100 KB so two CTAs share an SM (one's epilogue overlaps the other's
+  // mainloop); wider tiles: one CTA with a deep ring
+#ifndef DS_GEMM_SMEM_SMALL
+#define DS_GEMM_SMEM_SMALL (100 * 1024)
+#endif
+  static constexpr uint32_t BUDGET = BN <= 128 ? DS_GEMM_SMEM_SMALL : 200 * 1024;
+  static constexpr int STAGES = BUDGET / STAGE > 8 ? 8 : BUDGET / STAGE;
   static constexpr uint32_t TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;  // power of 2
 };
@@ -76,7 +85,7 @@ __device__ __forceinline__ int64_t map_row(const GemmEpilogue& ep, uint32_t row)
 }
 
 template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, BN <= 128 ? 2 : 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmEpilogue ep, const __grid_constant__ GemmTaps tp, uint32_t M,
                      uint32_t N, uint32_t K, uint32_t k_per_split, uint32_t splits) {
@@ -169,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc::commit(acc_full);
     }
-  } else {  // epilogue warps 2..5: TMEM lane quadrant = warp % 4
+  } else if (warp >= 4) {  // epilogue warps 4..7: TMEM lane quadrant = warp % 4
     const int q = warp & 3;
     const uint32_t row = m0 + q * 32 + lane;
     if (nk > 0) {
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (orow < 0 || n0 + c >= N) continue;
       float* dst = out + static_cast<uint64_t>(orow) * ldo + n0 + c;
-      const uint32_t lim = min(32u, N - (n0 + c));
+      const uint32_t lim = min(min(32u, static_cast<uint32_t>(BN - c)), N - (n0 + c));  // BN = 48: last chunk is 16 wide
       if (!raw) {
         const float* mrow = ep.mask ? ep.mask + static_cast<uint64_t>(orow) * ep.ldm + n0 + c : nullptr;
 #pragma unroll

@@ -10,7 +10,7 @@ int main(int argc, char** argv) {
   const uint32_t M = argc > 1 ? atoi(argv[1]) : 128, N = argc > 2 ? atoi(argv[2]) : 192, K = argc > 3 ? atoi(argv[3]) : 50;
   const int T = argc > 4 ? atoi(argv[4]) : 9, splits = argc > 5 ? atoi(argv[5]) : 1;
   const uint64_t ld = (K + 3) / 4 * 4;
-  std::vector<float> A(M * ld), B(N * ld), D(M * N * T, -7.f);
+  std::vector<float> A(M * ld), B(N * ld), D(M * N * (T > 0 ? T : 1), -7.f);
   srand(1);
   for (auto& v : A) v = (rand() % 2001 - 1000) / 1000.f;
   for (auto& v : B) v = (rand() % 2001 - 1000) / 1000.f;
@@ -22,6 +22,23 @@ int main(int argc, char** argv) {
   cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dD, D.data(), D.size() * 4, cudaMemcpyHostToDevice);
+  if (T == 0) {  // plain GEMM, D [M x N]
+    GemmEpilogue ep0;
+    ep0.D = dD;
+    ep0.ldd = N;
+    int rc0 = launch_gemm_tf32(dA, ld, dB, ld, M, N, K, ep0, 1, nullptr, 0);
+    cudaError_t e0 = cudaDeviceSynchronize();
+    cudaMemcpy(D.data(), dD, 4ull * M * N, cudaMemcpyDeviceToHost);
+    double me = 0;
+    for (uint32_t m = 0; m < M; ++m)
+      for (uint32_t n = 0; n < N; ++n) {
+        double r = 0;
+        for (uint32_t k = 0; k < K; ++k) r += A[m * ld + k] * B[n * ld + k];
+        me = fmax(me, fabs(r - D[m * N + n]));
+      }
+    printf("plain M %u N %u K %u (rc %d, %s): max err %.3e\n", M, N, K, rc0, cudaGetErrorString(e0), me);
+    return 0;
+  }
   GemmTaps tp;
   tp.n = T;
   tp.per_z = 1;
