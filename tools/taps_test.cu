@@ -30,6 +30,7 @@ int main(int argc, char** argv) {
     cudaError_t e0 = cudaDeviceSynchronize();
     cudaMemcpy(D.data(), dD, 4ull * M * N, cudaMemcpyDeviceToHost);
     double me = 0;
+    if (1.0 * M * N * K < 1e9)
     for (uint32_t m = 0; m < M; ++m)
       for (uint32_t n = 0; n < N; ++n) {
         double r = 0;
@@ -37,6 +38,17 @@ int main(int argc, char** argv) {
         me = fmax(me, fabs(r - D[m * N + n]));
       }
     printf("plain M %u N %u K %u (rc %d, %s): max err %.3e\n", M, N, K, rc0, cudaGetErrorString(e0), me);
+    cudaEvent_t e1, e2;
+    cudaEventCreate(&e1);
+    cudaEventCreate(&e2);
+    for (int it = 0; it < 3; ++it) launch_gemm_tf32(dA, ld, dB, ld, M, N, K, ep0, 1, nullptr, 0);
+    cudaEventRecord(e1);
+    for (int it = 0; it < 20; ++it) launch_gemm_tf32(dA, ld, dB, ld, M, N, K, ep0, 1, nullptr, 0);
+    cudaEventRecord(e2);
+    cudaEventSynchronize(e2);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e1, e2);
+    printf("  %.1f TFLOP/s (bn %u)\n", 2.0 * M * N * K * 20 / (ms / 1e3) / 1e12, gemm_pick_bn(N));
     return 0;
   }
   GemmTaps tp;
