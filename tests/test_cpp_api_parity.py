@@ -64,7 +64,8 @@ def test_orders_bit_exact(orc, dev):
 
 
 @pytest.mark.parametrize("m", [ModelSpec.softmax(20, 2), ModelSpec.mlp(4, [8], 3), ModelSpec.mlp(784, [256], 10),
-                               ModelSpec.mlp(5, [6, 7], 4)])
+                               ModelSpec.mlp(5, [6, 7], 4), ModelSpec.cifar10_quick(10), ModelSpec.alexnet(55, 5),
+                               ModelSpec.alexnet(224, 1000)])
 def test_layout_init_fingerprint(orc, dev, m):
     assert orc.param_dim(m) == dev.param_dim(m)
     assert orc.fingerprint(m) == dev.fingerprint(m)
