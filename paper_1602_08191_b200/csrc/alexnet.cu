@@ -185,48 +185,73 @@ __global__ void unpack_conv1_s2d_kernel(const float* __restrict__ dWp, float* __
   }
 }
 
-// out[c][r] = in[r][c] for a [rows x cols] matrix (ld_in, ld_out), 32x32 tiles
-__global__ void transpose_kernel(const float* __restrict__ in, uint64_t rows, uint32_t cols, uint64_t ld_in,
-                                 float* __restrict__ out, uint64_t ld_out, const uint32_t* gate) {
+// out[c][r] = in[r][c] for a [rows x cols] matrix (ld_in, ld_out), 32x32 tiles, 256 threads:
+// float4 loads along c and float4 stores along r (scalar at ragged edges / odd strides)
+__global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict__ in, uint64_t rows, uint32_t cols,
+                                                        uint64_t ld_in, float* __restrict__ out, uint64_t ld_out,
+                                                        const uint32_t* gate) {
   GATE;
   __shared__ float tile[32][33];
   const uint64_t r0 = blockIdx.x * 32ull;
   const uint32_t c0 = blockIdx.y * 32;
-  for (uint32_t ty = threadIdx.y; ty < 32; ty += 8) {
-    const uint64_t r = r0 + ty;
-    const uint32_t c = c0 + threadIdx.x;
-    tile[ty][threadIdx.x] = (r < rows && c < cols) ? in[r * ld_in + c] : 0.f;
+  const uint32_t t = threadIdx.x, lr = t / 8, lc = (t % 8) * 4;  // load: row lr, cols lc..lc+3
+  const bool vin = (ld_in % 4) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  const uint64_t r = r0 + lr;
+  const uint32_t c = c0 + lc;
+  if (vin && r < rows && c + 3 < cols) {
+    const float4 v = *reinterpret_cast<const float4*>(in + r * ld_in + c);
+    tile[lr][lc] = v.x, tile[lr][lc + 1] = v.y, tile[lr][lc + 2] = v.z, tile[lr][lc + 3] = v.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tile[lr][lc + j] = (r < rows && c + j < cols) ? in[r * ld_in + c + j] : 0.f;
   }
   __syncthreads();
-  for (uint32_t ty = threadIdx.y; ty < 32; ty += 8) {
-    const uint32_t c = c0 + ty;
-    const uint64_t r = r0 + threadIdx.x;
-    if (c < cols && r < rows) out[c * ld_out + r] = tile[threadIdx.x][ty];
+  const uint32_t sc = t / 8, sr = (t % 8) * 4;  // store: out row c0 + sc, cols r0 + sr .. + 3
+  const uint32_t oc = c0 + sc;
+  const uint64_t orr = r0 + sr;
+  if (oc >= cols) return;
+  const bool vout = (ld_out % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (vout && orr + 3 < rows) {
+    *reinterpret_cast<float4*>(out + oc * ld_out + orr) =
+        make_float4(tile[sr][sc], tile[sr + 1][sc], tile[sr + 2][sc], tile[sr + 3][sc]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (orr + j < rows) out[oc * ld_out + orr + j] = tile[sr + j][sc];
   }
 }
 
 // Four pixel-shifted transposed copies: out[s][c][m] = in[m - s][c] (0 outside the rows),
 // m < ldT. TMA needs 16-byte aligned inner coordinates, so a weight-gradient tap with pixel
 // shift d reads copy s = (-d mod 4) at the aligned offset d + s: the shifted column is never
-// left of the unshifted one, so no needed pixel falls before column 0.
-__global__ void transpose_shift4_kernel(const float* __restrict__ in, uint64_t rows, uint32_t cols,
-                                        float* __restrict__ out, uint64_t ldT, const uint32_t* gate) {
+// left of the unshifted one, so no needed pixel falls before column 0. 32 m x 32 c per
+// block (256 threads), float4 loads along c (cols % 4 == 0) and float4 stores along m.
+__global__ void __launch_bounds__(256) transpose_shift4_kernel(const float* __restrict__ in, uint64_t rows,
+                                                               uint32_t cols, float* __restrict__ out, uint64_t ldT,
+                                                               const uint32_t* gate) {
   GATE;
-  __shared__ float tile[35][33];  // rows r0-3 .. r0+31
+  __shared__ float tile[36][33];  // rows r0-3 .. r0+32 (35 used)
   const int64_t r0 = blockIdx.x * 32ll;
   const uint32_t c0 = blockIdx.y * 32;
-  for (uint32_t ty = threadIdx.y; ty < 35; ty += 8) {
-    const int64_t r = r0 - 3 + ty;
-    const uint32_t c = c0 + threadIdx.x;
-    tile[ty][threadIdx.x] = (r >= 0 && r < static_cast<int64_t>(rows) && c < cols) ? in[r * cols + c] : 0.f;
+  const uint32_t t = threadIdx.x;
+  for (uint32_t i = t; i < 35 * 8; i += 256) {
+    const uint32_t lr = i / 8, lc = (i % 8) * 4;
+    const int64_t r = r0 - 3 + lr;
+    const uint32_t c = c0 + lc;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r >= 0 && r < static_cast<int64_t>(rows) && c < cols) v = *reinterpret_cast<const float4*>(in + r * cols + c);
+    tile[lr][lc] = v.x, tile[lr][lc + 1] = v.y, tile[lr][lc + 2] = v.z, tile[lr][lc + 3] = v.w;
   }
   __syncthreads();
-  for (uint32_t sft = 0; sft < 4; ++sft)
-    for (uint32_t ty = threadIdx.y; ty < 32; ty += 8) {
-      const uint32_t c = c0 + ty;
-      const uint64_t m = r0 + threadIdx.x;
-      if (c < cols && m < ldT) out[(sft * cols + c) * ldT + m] = tile[threadIdx.x + 3 - sft][ty];
-    }
+  for (uint32_t i = t; i < 4 * 32 * 8; i += 256) {  // (shift, c, 4-wide m group)
+    const uint32_t sft = i / 256, rem = i % 256, sc = rem / 8, sm = (rem % 8) * 4;
+    const uint32_t c = c0 + sc;
+    const uint64_t m = r0 + sm;
+    if (c >= cols || m >= ldT) continue;
+    const uint32_t tr = sm + 3 - sft;
+    *reinterpret_cast<float4*>(out + (sft * cols + c) * ldT + m) =
+        make_float4(tile[tr][sc], tile[tr + 1][sc], tile[tr + 2][sc], tile[tr + 3][sc]);
+  }
 }
 
 // Caffe conv weight [Cout][cg][K][K] -> Wp [Cout][K*K][cg] and per group WpT_g [K*K][cg][Cout_g]
@@ -535,7 +560,7 @@ int gemm(const Ctx& c, const float* A, uint64_t lda, const float* B, uint64_t ld
 int transpose(const Ctx& c, const float* in, uint64_t rows, uint32_t cols, uint64_t ld_in, float* out, uint64_t ld_out) {
   const cudaStream_t s_ = c.s;
   dim3 grid(static_cast<unsigned>((rows + 31) / 32), (cols + 31) / 32);
-  transpose_kernel<<<grid, dim3(32, 8), 0, c.s>>>(in, rows, cols, ld_in, out, ld_out, c.gate);
+  transpose_kernel<<<grid, 256, 0, c.s>>>(in, rows, cols, ld_in, out, ld_out, c.gate);
   KDONE(1);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
@@ -785,7 +810,7 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     DS_TRY(transpose(c, dout, G, cs.Cout, cs.Cout, w.trA, ldT));
     {
       dim3 grid(static_cast<unsigned>((ldT + 31) / 32), (cs.Cin + 31) / 32);
-      transpose_shift4_kernel<<<grid, dim3(32, 8), 0, s>>>(in_maps[l], G, cs.Cin, w.trB, ldT, gate);
+      transpose_shift4_kernel<<<grid, 256, 0, s>>>(in_maps[l], G, cs.Cin, w.trB, ldT, gate);
       KDONE(1);
     }
     DS_TRY(conv_wgrad(c, cs, R, w.trA, w.trB, ldT, inv_b, w.wtmp, grad + L[l + 1].w_off));
@@ -814,7 +839,7 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     DS_TRY(colsum(c, w.dc1p, G1, 96, 96, inv_b, grad + L[0].b_off, w.bpart));
     DS_TRY(transpose(c, w.dc1p, G1, 96, 96, w.trA, ldT));
     dim3 grid(static_cast<unsigned>((ldT + 31) / 32), (48 + 31) / 32);
-    transpose_shift4_kernel<<<grid, dim3(32, 8), 0, s>>>(w.xs, G1, 48, w.trB, ldT, gate);
+    transpose_shift4_kernel<<<grid, 256, 0, s>>>(w.xs, G1, 48, w.trB, ldT, gate);
     KDONE(1);
     DS_TRY(conv_wgrad(c, cs, R, w.trA, w.trB, ldT, inv_b, w.wtmp, grad + L[0].w_off, true));
   }
