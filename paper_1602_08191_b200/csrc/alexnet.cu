@@ -336,7 +336,7 @@ __global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __
       const float sb = __powf(sc, -kLrnBeta);
       pw[j] = sb;
       const float d = (c >= 0 && c < static_cast<int>(C)) ? __ldg(pd + c) : 0.f;
-      w[j] = d * xv[j + 2] * sb / sc;
+      w[j] = d * xv[j + 2] * sb * __frcp_rn(sc);
     }
     float o[4];
 #pragma unroll
@@ -354,16 +354,19 @@ __global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __
 
 // MAX 3x3/2 ceil-mode over an NHWC map (input padded by ipad, output padded by opad, or
 // per-row CHW when chw != 0: the fc6 input). arg[r][py][px][c] (unpadded) = window position
-// (0..8) of the first maximum in scan order. One block per pooled pixel, one thread per
-// channel (coalesced along c, the pixel decode is block-uniform).
-__global__ void maxpool_fwd_kernel(const float* __restrict__ in, uint32_t R, uint32_t H, uint32_t C, uint32_t Ho,
-                                   uint32_t ipad, uint32_t opad, int chw, float* __restrict__ out,
-                                   uint8_t* __restrict__ arg, const uint32_t* gate) {
+// (0..8) of the first maximum in scan order. One warp per pooled pixel (8 per block),
+// lanes across channels.
+__global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restrict__ in, uint32_t R, uint32_t H,
+                                                          uint32_t C, uint32_t Ho, uint32_t ipad, uint32_t opad,
+                                                          int chw, float* __restrict__ out,
+                                                          uint8_t* __restrict__ arg, const uint32_t* gate) {
   GATE;
   const uint32_t Hi = H + 2 * ipad, Hq = Ho + 2 * opad, HoHo = Ho * Ho;
-  const uint32_t p = blockIdx.x, r = p / HoHo, pix = p - r * HoHo, py = pix / Ho, px = pix - py * Ho;
+  const uint32_t p = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (p >= R * HoHo) return;
+  const uint32_t r = p / HoHo, pix = p - r * HoHo, py = pix / Ho, px = pix - py * Ho;
   const uint32_t hs = py * 2, ws = px * 2, he = min(hs + 3, H), we = min(ws + 3, H);
-  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+  for (uint32_t c = lane; c < C; c += 32) {
     float best = -INFINITY;
     uint32_t bi = 0;
     for (uint32_t h = hs; h < he; ++h)
@@ -380,28 +383,43 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ in, uint32_t R, uin
 
 // gather form of the max-pool backward: din[r][y][x][c] = sum of dout over the windows whose
 // maximum sat at (y, x). dout: padded by opad (or per-row CHW), din/mask: padded by ipad;
-// mask (optional) zeroes din where the pooled map's source was not > 0 (ReLU). One block
-// per input pixel, one thread per channel.
-__global__ void maxpool_bwd_kernel(const float* __restrict__ dout, const uint8_t* __restrict__ arg, uint32_t R,
-                                   uint32_t H, uint32_t C, uint32_t Ho, uint32_t opad, int chw, uint32_t ipad,
-                                   const float* __restrict__ mask, float* __restrict__ din, const uint32_t* gate) {
+// mask (optional) zeroes din where the pooled map's source was not > 0 (ReLU). One warp
+// per input pixel (8 per block), lanes across channels.
+__global__ void __launch_bounds__(256) maxpool_bwd_kernel(const float* __restrict__ dout,
+                                                          const uint8_t* __restrict__ arg, uint32_t R, uint32_t H,
+                                                          uint32_t C, uint32_t Ho, uint32_t opad, int chw,
+                                                          uint32_t ipad, const float* __restrict__ mask,
+                                                          float* __restrict__ din, const uint32_t* gate) {
   GATE;
   const uint32_t Hi = H + 2 * ipad, Hq = Ho + 2 * opad, HH = H * H;
-  const uint32_t p = blockIdx.x, r = p / HH, pix = p - r * HH, y = pix / H, x = pix - y * H;
+  const uint32_t p = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (p >= R * HH) return;
+  const uint32_t r = p / HH, pix = p - r * HH, y = pix / H, x = pix - y * H;
   const uint32_t py0 = y >= 2 ? (y - 1) / 2 : 0, py1 = min(y / 2, Ho - 1);
   const uint32_t px0 = x >= 2 ? (x - 1) / 2 : 0, px1 = min(x / 2, Ho - 1);
   const uint64_t dbase = (static_cast<uint64_t>(r * Hi + y + ipad) * Hi + x + ipad) * C;
-  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
-    float s = 0.f;
-    if (!mask || mask[dbase + c] > 0.f) {
-      for (uint32_t py = py0; py <= py1; ++py)
-        for (uint32_t px = px0; px <= px1; ++px) {
-          const uint32_t a = ((r * Ho + py) * Ho + px) * C + c;
-          if (arg[a] == (y - py * 2) * 3 + (x - px * 2))
-            s += dout[chw ? (static_cast<uint64_t>(r) * C + c) * Ho * Ho + py * Ho + px
-                          : (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c];
-        }
+  // up to 2 x 2 windows cover (y, x); their argmax bytes and gradients are loaded
+  // independently (no load waits on a comparison), then the matches are summed in window order
+  const bool two_y = py1 > py0, two_x = px1 > px0;
+  for (uint32_t c = lane; c < C; c += 32) {
+    uint32_t av[4];
+    float dv[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t py = py0 + (w >> 1), px = px0 + (w & 1);
+      const bool ok = ((w >> 1) == 0 || two_y) && ((w & 1) == 0 || two_x);
+      av[w] = ok ? arg[((r * Ho + py) * Ho + px) * C + c] : 255u;
+      dv[w] = ok ? dout[chw ? (static_cast<uint64_t>(r) * C + c) * Ho * Ho + py * Ho + px
+                            : (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c]
+                 : 0.f;
     }
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t py = py0 + (w >> 1), px = px0 + (w & 1);
+      if (av[w] == (y - py * 2) * 3 + (x - px * 2)) s += dv[w];
+    }
+    if (mask && !(mask[dbase + c] > 0.f)) s = 0.f;
     din[dbase + c] = s;
   }
 }
@@ -705,18 +723,18 @@ int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint3
   KDONE(1);
   DS_TRY(conv_fwd(c, conv1_spec(sh), R, w.xs, w.w1p, P + L[0].b_off, w.a1, false));
   lrn_fwd_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, static_cast<uint32_t>(M1), 96, w.n1, gate);
-  maxpool_fwd_kernel<<<static_cast<unsigned>(M2), 96, 0, s>>>(w.n1, R, sh.H1, 96, sh.P1, 0, 2, 0, w.p1p, w.arg1, gate);
+  maxpool_fwd_kernel<<<static_cast<unsigned>((M2 + 7) / 8), 256, 0, s>>>(w.n1, R, sh.H1, 96, sh.P1, 0, 2, 0, w.p1p, w.arg1, gate);
   KDONE(2);
   // conv2 + relu -> a2 (unpadded), LRN2, pool2 -> p2p (pad 1)
   DS_TRY(conv_fwd(c, conv_spec(sh, 0), R, w.p1p, w.wp[0], P + L[1].b_off, w.a2, false));
   lrn_fwd_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, static_cast<uint32_t>(M2), 256, w.n2, gate);
-  maxpool_fwd_kernel<<<R * sh.P2 * sh.P2, 256, 0, s>>>(w.n2, R, sh.P1, 256, sh.P2, 0, 1, 0, w.p2p, w.arg2, gate);
+  maxpool_fwd_kernel<<<(R * sh.P2 * sh.P2 + 7) / 8, 256, 0, s>>>(w.n2, R, sh.P1, 256, sh.P2, 0, 1, 0, w.p2p, w.arg2, gate);
   KDONE(2);
   // conv3, conv4, conv5 on the pad-1 grid, pool5 -> p5 (per-row CHW)
   DS_TRY(conv_fwd(c, conv_spec(sh, 1), R, w.p2p, w.wp[1], P + L[2].b_off, w.a3p, true));
   DS_TRY(conv_fwd(c, conv_spec(sh, 2), R, w.a3p, w.wp[2], P + L[3].b_off, w.a4p, true));
   DS_TRY(conv_fwd(c, conv_spec(sh, 3), R, w.a4p, w.wp[3], P + L[4].b_off, w.a5p, true));
-  maxpool_fwd_kernel<<<R * sh.P5 * sh.P5, 256, 0, s>>>(w.a5p, R, sh.P2, 256, sh.P5, 1, 0, 1, w.p5, w.arg5, gate);
+  maxpool_fwd_kernel<<<(R * sh.P5 * sh.P5 + 7) / 8, 256, 0, s>>>(w.a5p, R, sh.P2, 256, sh.P5, 1, 0, 1, w.p5, w.arg5, gate);
   KDONE(1);
   // fc6, fc7 (+relu), fc8
   DS_TRY(gemm(c, w.p5, sh.q5, P + L[5].w_off, sh.q5, w.h6, 4096, R, 4096, static_cast<uint32_t>(sh.q5), 1.f,
@@ -795,7 +813,7 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   DS_TRY(zero(c, w.dc2p, G2 * 256));
   DS_TRY(zero(c, w.dc1p, 1ull * R * sh.Hs * sh.Hs * 96));
   // pool5 backward (per-row CHW pooled map) with the ReLU5 mask (a5p) -> dc5p
-  maxpool_bwd_kernel<<<static_cast<unsigned>(M3), 256, 0, s>>>(w.dp5, w.arg5, R, sh.P2, 256, sh.P5, 0, 1, 1, w.a5p,
+  maxpool_bwd_kernel<<<static_cast<unsigned>((M3 + 7) / 8), 256, 0, s>>>(w.dp5, w.arg5, R, sh.P2, 256, sh.P5, 0, 1, 1, w.a5p,
                                                                 w.dc5p, gate);
   KDONE(1);
   const float* in_maps[4] = {w.p1p, w.p2p, w.a3p, w.a4p};
@@ -820,13 +838,13 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     } else if (l == 1) {  // into pool2(LRN2(relu(conv2))): d(p2p), pool2 bwd, LRN2 bwd -> dc2p
       DS_TRY(zero(c, w.dp2p, G3 * 256));
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp2p, true, nullptr));
-      maxpool_bwd_kernel<<<static_cast<unsigned>(M2), 256, 0, s>>>(w.dp2p, w.arg2, R, sh.P1, 256, sh.P2, 1, 0, 0,
+      maxpool_bwd_kernel<<<static_cast<unsigned>((M2 + 7) / 8), 256, 0, s>>>(w.dp2p, w.arg2, R, sh.P1, 256, sh.P2, 1, 0, 0,
                                                                     nullptr, w.dn2, gate);
       lrn_bwd_relu_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, w.dn2, R, sh.P1, 256, 2, sh.Hp2, w.dc2p, gate);
       KDONE(2);
     } else {  // into pool1(LRN1(relu(conv1))): d(p1) unpadded, pool1 bwd, LRN1 bwd -> dc1p
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp1, false, nullptr));
-      maxpool_bwd_kernel<<<static_cast<unsigned>(M1), 96, 0, s>>>(w.dp1, w.arg1, R, sh.H1, 96, sh.P1, 0, 0, 0, nullptr,
+      maxpool_bwd_kernel<<<static_cast<unsigned>((M1 + 7) / 8), 256, 0, s>>>(w.dp1, w.arg1, R, sh.H1, 96, sh.P1, 0, 0, 0, nullptr,
                                                                   w.dn1, gate);
       lrn_bwd_relu_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, w.dn1, R, sh.H1, 96, 1, sh.Hs, w.dc1p, gate);
       KDONE(2);
