@@ -679,7 +679,11 @@ int conv_wgrad(const Ctx& c, const ConvSpec& cs, uint32_t R, const float* doutT,
       tp.b_col[t] = d + sft;
     }
     const GemmOperand A{doutT + 1ull * gi * cog * ldT, cog, G, ldT}, B{inT4, 4ull * cs.Cin, G + 3, ldT};
-    const uint32_t sp = pick_splits(cog, cig, G, cs.KK());
+    // the GEMM stacks up to 256 / cig taps per CTA along N (launch_gemm); size the split-K
+    // for the resulting number of tap groups
+    uint32_t tpc = std::min<uint32_t>(cs.KK(), 256 / cig);
+    if (!(tpc > 1 && (tpc * cig == 192 || tpc * cig == 240 || tpc * cig == 256))) tpc = 1;
+    const uint32_t sp = pick_splits(cog, tpc * cig, G, (cs.KK() + tpc - 1) / tpc);
     GemmEpilogue ep = epi(c, wtmp + 1ull * gi * cog * Kg, Kg, scale, nullptr, false);
     DS_TRY(launch_gemm(A, B, cog, cig, G, &tp, ep, sp, c.part, c.s));
     KDONE(sp > 1 ? 2 : 1);

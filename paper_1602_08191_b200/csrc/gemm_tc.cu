@@ -101,8 +101,14 @@ __global__ void __launch_bounds__(kThreads, BN <= 192 ? 2 : 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM;
   const bool acc_taps = tp.n > 0 && !tp.per_z;
-  const int tap = (tp.n > 0 && tp.per_z) ? static_cast<int>(blockIdx.z / splits) : -1;
+  const int tap = (tp.n > 0 && tp.per_z) ? static_cast<int>(blockIdx.z / splits) : -1;  // tap group
   const uint32_t split = tap >= 0 ? blockIdx.z % splits : blockIdx.z;
+  // per_z with tpc > 1: taps tap*tpc .. + ntg - 1 share the A tile; their B tiles (n_tap rows
+  // each) are stacked along N in one BN-wide stage and one MMA covers them all
+  const uint32_t t0 = tap >= 0 ? static_cast<uint32_t>(tap) * tp.tpc : 0;
+  const uint32_t ntg = tap >= 0 ? min(tp.tpc, static_cast<uint32_t>(tp.n) - t0) : 1;
+  const uint32_t nvalid = (tap >= 0 && tp.tpc > 1) ? ntg * tp.n_tap : N;
+  const uint32_t stage_tx = (tap >= 0 && tp.tpc > 1) ? S::A_BYTES + ntg * tp.n_tap * kBK * 4 : S::STAGE;
   uint32_t nk, nkt = 1, k_begin = 0;
   if (acc_taps) {
     nkt = (tp.kt + kBK - 1) / kBK;
@@ -135,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, BN <= 192 ? 2 : 1)
         const int s = i % kStages;
         if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
         uint8_t* sa = smem + s * S::STAGE;
-        mbar_expect_tx(&full[s], S::STAGE);
+        mbar_expect_tx(&full[s], stage_tx);
         int ax, ay, bx, by;
         if (acc_taps) {
           const uint32_t t = i / nkt, kc = i - t * nkt;
@@ -147,7 +153,15 @@ __global__ void __launch_bounds__(kThreads, BN <= 192 ? 2 : 1)
           ax = bx = static_cast<int>(k_begin + i * kBK);
           ay = static_cast<int>(m0);
           by = static_cast<int>(n0);
-          if (tap >= 0) ax += tp.a_col[tap], ay += tp.a_row[tap], bx += tp.b_col[tap], by += tp.b_row[tap];
+          if (tap >= 0) {
+            ax += tp.a_col[t0], ay += tp.a_row[t0];
+            if (tp.tpc > 1) {  // one B sub-tile per tap of the group
+              for (uint32_t j = 1; j < ntg; ++j)
+                tma_load_2d(sa + S::A_BYTES + j * tp.n_tap * kBK * 4, &tmB, &full[s], bx + tp.b_col[t0 + j],
+                            by + tp.b_row[t0 + j]);
+            }
+            bx += tp.b_col[t0], by += tp.b_row[t0];
+          }
         }
         tma_load_2d(sa, &tmA, &full[s], ax, ay);
         tma_load_2d(sa + S::A_BYTES, &tmB, &full[s], bx, by);
@@ -187,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, BN <= 192 ? 2 : 1)
     }
     const bool raw = ep.raw || (tap < 0 && gridDim.z > 1) || (tap >= 0 && splits > 1);
     float* out = raw ? ep.D + static_cast<uint64_t>(blockIdx.z) * ep.split_stride
-                     : ep.D + (tap >= 0 ? static_cast<uint64_t>(tap) * tp.d_col_step : 0);
+                     : ep.D + (tap >= 0 ? static_cast<uint64_t>(t0) * tp.d_col_step : 0);
     const int64_t orow = row < M ? (raw ? static_cast<int64_t>(row) : map_row(ep, row)) : -1;
     const uint64_t ldo = raw ? N : ep.ldd;
     const float bm = (!raw && ep.bias_m && orow >= 0) ? ep.bias_m[row] : 0.f;
@@ -200,9 +214,9 @@ __global__ void __launch_bounds__(kThreads, BN <= 192 ? 2 : 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0.f;
       }
-      if (orow < 0 || n0 + c >= N) continue;
+      if (orow < 0 || n0 + c >= nvalid) continue;
       float* dst = out + static_cast<uint64_t>(orow) * ldo + n0 + c;
-      const uint32_t lim = min(min(32u, static_cast<uint32_t>(BN - c)), N - (n0 + c));  // BN = 48: last chunk is 16 wide
+      const uint32_t lim = min(min(32u, static_cast<uint32_t>(BN - c)), nvalid - (n0 + c));  // BN = 48: last chunk 16 wide
       if (!raw) {
         const float* mrow = ep.mask ? ep.mask + static_cast<uint64_t>(orow) * ep.ldm + n0 + c : nullptr;
 #pragma unroll
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, BN <= 192 ? 2 : 1)
 // is dense [M][N].
 __global__ void gemm_reduce_kernel(const float* __restrict__ slabs, uint32_t ntaps, uint64_t tap_stride,
                                    uint32_t nparts, uint64_t part_stride, uint32_t d_col_step, GemmEpilogue ep,
-                                   uint32_t M, uint32_t N) {
+                                   uint32_t M, uint32_t N, uint32_t col_limit) {
   if (ep.gate && *ep.gate) return;
   const uint64_t total = static_cast<uint64_t>(ntaps) * M * N;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -245,7 +259,7 @@ __global__ void gemm_reduce_kernel(const float* __restrict__ slabs, uint32_t nta
     const uint64_t e = i - t * mn;
     const uint32_t r = static_cast<uint32_t>(e / N), c = static_cast<uint32_t>(e % N);
     const int64_t orow = map_row(ep, r);
-    if (orow < 0) continue;
+    if (orow < 0 || static_cast<uint64_t>(t) * d_col_step + c >= col_limit) continue;
     float s = 0.f;
     for (uint32_t p = 0; p < nparts; ++p) s += slabs[t * tap_stride + p * part_stride + e];
     float x = s * ep.scale;
@@ -291,7 +305,7 @@ int launch_bn(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep
               uint32_t N, uint32_t K, uint32_t splits, cudaStream_t s) {
   CUtensorMap ma, mb;
   DS_TRY(make_map(&ma, A.p, A.rows, A.cols, A.ld, kBM));
-  DS_TRY(make_map(&mb, B.p, B.rows, B.cols, B.ld, BN));
+  DS_TRY(make_map(&mb, B.p, B.rows, B.cols, B.ld, (tp.per_z && tp.tpc > 1) ? tp.n_tap : BN));
   static uint64_t attr_set = 0;  // per device
   int dev = 0;
   DS_CUDA_TRY(cudaGetDevice(&dev));
@@ -301,7 +315,8 @@ int launch_bn(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep
     attr_set |= 1ull << (dev & 63);
   }
   const uint32_t kps = ((K + splits - 1) / splits + kBK - 1) / kBK * kBK;
-  const uint32_t zdim = (tp.n > 0 && tp.per_z) ? tp.n * splits : (tp.n > 0 ? 1 : splits);
+  const uint32_t ngroups = (tp.n > 0 && tp.per_z) ? (tp.n + tp.tpc - 1) / tp.tpc : 1;
+  const uint32_t zdim = (tp.n > 0 && tp.per_z) ? ngroups * splits : (tp.n > 0 ? 1 : splits);
   dim3 grid((N + BN - 1) / BN, (M + kBM - 1) / kBM, zdim);
   gemm_tf32_kernel<BN><<<grid, kThreads, GemmSmem<BN>::TOTAL, s>>>(ma, mb, ep, tp, M, N, K, kps, splits);
   DS_CUDA_TRY(cudaGetLastError());
@@ -310,6 +325,14 @@ int launch_bn(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep
 
 int launch_any(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep, const GemmTaps& tp, uint32_t M,
                uint32_t N, uint32_t K, uint32_t splits, cudaStream_t s) {
+  if (tp.per_z && tp.tpc > 1) {  // grouped taps: the tile is exactly tpc x n_tap wide
+    switch (tp.tpc * tp.n_tap) {
+      case 192: return launch_bn<192>(A, B, ep, tp, M, N, K, splits, s);
+      case 240: return launch_bn<240>(A, B, ep, tp, M, N, K, splits, s);
+      case 256: return launch_bn<256>(A, B, ep, tp, M, N, K, splits, s);
+      default: return set_error(DS_E_CONTRACT, "gemm: no tile for %u taps x %u", tp.tpc, tp.n_tap);
+    }
+  }
   switch (gemm_pick_bn(N)) {
     case 48: return launch_bn<48>(A, B, ep, tp, M, N, K, splits, s);
     case 64: return launch_bn<64>(A, B, ep, tp, M, N, K, splits, s);
@@ -321,10 +344,12 @@ int launch_any(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& e
 }
 
 int launch_reduce(const float* slabs, uint32_t ntaps, uint64_t tap_stride, uint32_t nparts, uint64_t part_stride,
-                  uint32_t d_col_step, const GemmEpilogue& ep, uint32_t M, uint32_t N, cudaStream_t s) {
+                  uint32_t d_col_step, const GemmEpilogue& ep, uint32_t M, uint32_t N, cudaStream_t s,
+                  uint32_t col_limit = 0xFFFFFFFFu) {
   const uint64_t total = static_cast<uint64_t>(ntaps) * M * N;
   const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-  gemm_reduce_kernel<<<blocks, 256, 0, s>>>(slabs, ntaps, tap_stride, nparts, part_stride, d_col_step, ep, M, N);
+  gemm_reduce_kernel<<<blocks, 256, 0, s>>>(slabs, ntaps, tap_stride, nparts, part_stride, d_col_step, ep, M, N,
+                                            col_limit);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
@@ -349,7 +374,7 @@ bool exact_mode() {  // DS_GEMM_3XTF32=1: f32-accurate products (parity diagnost
 int launch_3xtf32(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32_t N, uint32_t K, const GemmTaps& tp,
                   const GemmEpilogue& ep_in, cudaStream_t s) {
   const uint64_t na = A.rows * A.ld, nb = B.rows * B.ld;
-  const uint32_t ntz = (tp.n > 0 && tp.per_z) ? tp.n : 1;
+  const uint32_t ntz = (tp.n > 0 && tp.per_z) ? (tp.n + tp.tpc - 1) / tp.tpc : 1;
   const uint64_t set = static_cast<uint64_t>(ntz) * M * N;
   float *ab = nullptr, *bb = nullptr, *slab = nullptr;
   DS_CUDA_TRY(cudaMallocAsync(&ab, 2 * na * 4, s));
@@ -369,8 +394,9 @@ int launch_3xtf32(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32
     raw.D = slab + t * set;
     rc = launch_any(a, b, raw, tp, M, N, K, 1, s);
   }
-  if (rc == DS_OK) rc = launch_reduce(slab, ntz, static_cast<uint64_t>(M) * N, 3, set, tp.per_z ? tp.d_col_step : 0,
-                                      ep_in, M, N, s);
+  if (rc == DS_OK)
+    rc = launch_reduce(slab, ntz, static_cast<uint64_t>(M) * N, 3, set, tp.per_z ? tp.tpc * tp.d_col_step : 0, ep_in, M,
+                       N, s, tp.per_z ? tp.n * tp.d_col_step : 0xFFFFFFFFu);
   cudaFreeAsync(ab, s);
   cudaFreeAsync(bb, s);
   cudaFreeAsync(slab, s);
@@ -397,6 +423,15 @@ int launch_gemm(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32_t
   if (taps) tp = *taps;
   if (tp.n < 0 || tp.n > kMaxTaps) return set_error(DS_E_CONTRACT, "gemm: at most %d taps", kMaxTaps);
   if (tp.n > 0 && !tp.per_z && (tp.kt == 0 || tp.kt % 8)) return set_error(DS_E_CONTRACT, "gemm: tap width %% 8");
+  tp.tpc = 1;
+  tp.n_tap = N;
+  if (tp.n > 1 && tp.per_z && tp.d_col_step == N) {  // stack taps along N: one A tile feeds up to 256 columns
+    const uint32_t g = std::min<uint32_t>(static_cast<uint32_t>(tp.n), 256 / N);
+    if (g > 1 && (g * N == 192 || g * N == 240 || g * N == 256)) {
+      tp.tpc = g;
+      N = g * N;  // the kernel's N is the group width; columns past the last tap are clipped
+    }
+  }
   if (exact_mode()) return launch_3xtf32(A, B, M, N, K, tp, ep_in, s);
   if (splits == 0) splits = 1;
   if (tp.n > 0 && !tp.per_z) {
@@ -407,7 +442,7 @@ int launch_gemm(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32_t
   }
   if (splits > 1 && !part) return set_error(DS_E_CONTRACT, "gemm: split-K needs a partial buffer");
   GemmEpilogue ep = ep_in;
-  const uint32_t ntz = (tp.n > 0 && tp.per_z) ? tp.n : 1;
+  const uint32_t ntz = (tp.n > 0 && tp.per_z) ? (tp.n + tp.tpc - 1) / tp.tpc : 1;
   if (splits > 1) {  // raw partial slabs [tap][split][M][N], reduced below with the epilogue
     ep.D = part;
     ep.raw = true;
@@ -416,7 +451,8 @@ int launch_gemm(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32_t
   DS_TRY(launch_any(A, B, ep, tp, M, N, K, splits, s));
   if (splits > 1)
     DS_TRY(launch_reduce(part, ntz, static_cast<uint64_t>(splits) * M * N, splits, static_cast<uint64_t>(M) * N,
-                         tp.per_z ? tp.d_col_step : 0, ep_in, M, N, s));
+                         tp.per_z ? tp.tpc * tp.d_col_step : 0, ep_in, M, N, s,
+                         tp.per_z ? tp.n * tp.d_col_step : 0xFFFFFFFFu));
   return DS_OK;
 }
 
