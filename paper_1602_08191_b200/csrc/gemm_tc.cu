@@ -69,6 +69,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          tc::saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(tc::saddr(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::saddr(b)), "r"(bytes) : "memory");
 }
@@ -244,6 +252,150 @@ __global__ void __launch_bounds__(kThreads, BN <= 192 ? 2 : 1)
   if (warp == 1) tc::tmem_free<S::TMEM_COLS>(tmem);
 }
 
+// Halo variant of the accumulating taps mode (conv forward / data gradient; opt-in, see
+// halo_enabled), usable when the taps' A row shifts span <= 128 rows: per 32-channel chunk the CTA loads the A rows
+// [m0 + lo, m0 + 128 + hi) ONCE and every tap's MMA reads its 128-row window inside that
+// buffer; only the B tiles stream per tap. The halo uses the canonical no-swizzle K-major
+// layout [8 k-chunks][rows][16 B] (a 3-D TMA box {4 floats, rows, 8}), in which consecutive
+// rows are 16 bytes apart, so a tap's window is just the start address + 16 * shift.
+// A traffic per chunk drops from taps x 16 KB to halo_rows x 128 B.
+constexpr uint32_t kHaloBytes = 256 * 128;
+template <int BN>
+struct HaloSmem {
+  static constexpr uint32_t B_BYTES = BN * kBK * 4;
+  static constexpr int STAGES = (48 * 1024) / B_BYTES > 8 ? 8 : ((48 * 1024) / B_BYTES < 2 ? 2 : (48 * 1024) / B_BYTES);
+  static constexpr uint32_t TOTAL = 2 * kHaloBytes + STAGES * B_BYTES + 1024 + 512;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, HaloSmem<BN>::TOTAL <= 113 * 1024 ? 2 : 1)
+    gemm_halo_kernel(const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ GemmEpilogue ep, const __grid_constant__ GemmTaps tp, uint32_t M,
+                     uint32_t N) {
+  using S = HaloSmem<BN>;
+  using T = GemmSmem<BN>;
+  constexpr int kB = S::STAGES;
+  if (ep.gate && *ep.gate) return;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* halo = smem;                  // [2][kHaloBytes]
+  uint8_t* bst = smem + 2 * kHaloBytes;  // [kB][B_BYTES]
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(bst + kB * S::B_BYTES);
+  uint64_t* hempty = hfull + 2;
+  uint64_t* bfull = hempty + 2;
+  uint64_t* bempty = bfull + kB;
+  uint64_t* acc_full = bempty + kB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM;
+  const uint32_t nkc = (tp.kt + kBK - 1) / kBK, ntap = static_cast<uint32_t>(tp.n);
+  const uint32_t hrows = tp.halo_rows, lbo = hrows * 16;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA3)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int i = 0; i < 2; ++i) tc::mbar_init(&hfull[i], 1), tc::mbar_init(&hempty[i], 1);
+    for (int i = 0; i < kB; ++i) tc::mbar_init(&bfull[i], 1), tc::mbar_init(&bempty[i], 1);
+    tc::mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tc::tmem_alloc<T::TMEM_COLS>(tmem_slot);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: the chunk's halo, then its B tile per tap
+      uint32_t bi = 0;
+      for (uint32_t kc = 0; kc < nkc; ++kc) {
+        const uint32_t h = kc & 1;
+        if (kc >= 2) tc::mbar_wait(&hempty[h], ((kc >> 1) - 1) & 1);
+        mbar_expect_tx(&hfull[h], hrows * 128);
+        tma_load_3d(halo + h * kHaloBytes, &tmA3, &hfull[h], 0, static_cast<int>(m0) + tp.halo_lo,
+                    tp.a_col[0] / 4 + static_cast<int>(kc * 8));
+        for (uint32_t t = 0; t < ntap; ++t, ++bi) {
+          const uint32_t s = bi % kB;
+          if (bi >= kB) tc::mbar_wait(&bempty[s], ((bi / kB) - 1) & 1);
+          mbar_expect_tx(&bfull[s], S::B_BYTES);
+          tma_load_2d(bst + s * S::B_BYTES, &tmB, &bfull[s], tp.b_col[t] + static_cast<int>(kc * kBK),
+                      static_cast<int>(n0) + tp.b_row[t]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = tc::idesc_tf32(kBM, BN);
+      uint32_t bi = 0;
+      for (uint32_t kc = 0; kc < nkc; ++kc) {
+        const uint32_t h = kc & 1;
+        const uint32_t rem = tp.kt - kc * kBK, nsub = rem >= kBK ? kBK / 8 : rem / 8;
+        tc::mbar_wait(&hfull[h], (kc >> 1) & 1);
+        tc::fence_after();
+        const uint32_t abase = tc::saddr(halo + h * kHaloBytes);
+        for (uint32_t t = 0; t < ntap; ++t, ++bi) {
+          const uint32_t s = bi % kB;
+          tc::mbar_wait(&bfull[s], (bi / kB) & 1);
+          tc::fence_after();
+          const uint32_t a = abase + static_cast<uint32_t>(tp.a_row[t]) * 16, b = tc::saddr(bst + s * S::B_BYTES);
+          for (uint32_t kk = 0; kk < nsub; ++kk) {
+            const uint64_t da = tc::sdesc(a + kk * 2 * lbo, lbo, 128), db = sdesc_sw128(b + kk * 32);
+            const uint32_t acc = (kc | t | kk) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+          tc::commit(&bempty[s]);
+        }
+        tc::commit(&hempty[h]);
+      }
+      tc::commit(acc_full);
+    }
+  } else if (warp >= 4) {  // epilogue warps 4..7
+    const int q = warp & 3;
+    const uint32_t row = m0 + q * 32 + lane;
+    tc::mbar_wait(acc_full, 0);
+    tc::fence_after();
+    const bool raw = ep.raw;
+    float* out = raw ? ep.D + static_cast<uint64_t>(blockIdx.z) * ep.split_stride : ep.D;
+    const int64_t orow = row < M ? (raw ? static_cast<int64_t>(row) : map_row(ep, row)) : -1;
+    const uint64_t ldo = raw ? N : ep.ldd;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      tc::tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+      if (orow < 0 || n0 + c >= N) continue;
+      float* dst = out + static_cast<uint64_t>(orow) * ldo + n0 + c;
+      const uint32_t lim = min(min(32u, static_cast<uint32_t>(BN - c)), N - (n0 + c));
+      if (!raw) {
+        const float* mrow = ep.mask ? ep.mask + static_cast<uint64_t>(orow) * ep.ldm + n0 + c : nullptr;
+        const float bm = ep.bias_m ? ep.bias_m[row] : 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float x = v[j] * ep.scale + bm;
+          if (static_cast<uint32_t>(j) < lim) {
+            if (ep.bias_n) x += __ldg(ep.bias_n + n0 + c + j);
+            if (mrow && !(mrow[j] > 0.f)) x = 0.f;
+          }
+          v[j] = ep.relu ? fmaxf(x, 0.f) : x;
+        }
+      }
+      if (lim == 32 && (ldo % 4) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (static_cast<uint32_t>(j) < lim) dst[j] = v[j];
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_free<T::TMEM_COLS>(tmem);
+}
+
 // Sum of raw slabs in a fixed order, then the epilogue (row map, tap columns, scale,
 // biases, mask, ReLU). Slab (tap t, part p) starts at t * tap_stride + p * part_stride and
 // is dense [M][N].
@@ -300,6 +452,41 @@ int make_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, ui
   return DS_OK;
 }
 
+// A as [rows][cols/4 chunks][4] viewed 3-D {4, rows, cols/4}: the no-swizzle K-major halo box
+int make_map_halo(CUtensorMap* m, const GemmOperand& A, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(DS_E_CUDA, "gemm: cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {4, A.rows, A.cols / 4};
+  const cuuint64_t strides[2] = {A.ld * 4, 16};
+  const cuuint32_t box[3] = {4, box_rows, 8};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(A.p), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(DS_E_CUDA, "gemm: halo tensor map failed (%d)", static_cast<int>(r));
+  return DS_OK;
+}
+
+template <int BN>
+int launch_halo(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep, const GemmTaps& tp, uint32_t M,
+                uint32_t N, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  DS_TRY(make_map_halo(&ma, A, tp.halo_rows));
+  DS_TRY(make_map(&mb, B.p, B.rows, B.cols, B.ld, BN));
+  static uint64_t attr_set = 0;  // per device
+  int dev = 0;
+  DS_CUDA_TRY(cudaGetDevice(&dev));
+  if (!(attr_set >> (dev & 63) & 1)) {
+    DS_CUDA_TRY(cudaFuncSetAttribute(gemm_halo_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     HaloSmem<BN>::TOTAL));
+    attr_set |= 1ull << (dev & 63);
+  }
+  dim3 grid((N + BN - 1) / BN, (M + kBM - 1) / kBM, 1);
+  gemm_halo_kernel<BN><<<grid, kThreads, HaloSmem<BN>::TOTAL, s>>>(ma, mb, ep, tp, M, N);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
 template <int BN>
 int launch_bn(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep, const GemmTaps& tp, uint32_t M,
               uint32_t N, uint32_t K, uint32_t splits, cudaStream_t s) {
@@ -325,6 +512,16 @@ int launch_bn(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep
 
 int launch_any(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep, const GemmTaps& tp, uint32_t M,
                uint32_t N, uint32_t K, uint32_t splits, cudaStream_t s) {
+  if (tp.n > 0 && !tp.per_z && tp.halo_rows > 0) {
+    switch (gemm_pick_bn(N)) {
+      case 48: return launch_halo<48>(A, B, ep, tp, M, N, s);
+      case 64: return launch_halo<64>(A, B, ep, tp, M, N, s);
+      case 96: return launch_halo<96>(A, B, ep, tp, M, N, s);
+      case 128: return launch_halo<128>(A, B, ep, tp, M, N, s);
+      case 192: return launch_halo<192>(A, B, ep, tp, M, N, s);
+      default: return launch_halo<256>(A, B, ep, tp, M, N, s);
+    }
+  }
   if (tp.per_z && tp.tpc > 1) {  // grouped taps: the tile is exactly tpc x n_tap wide
     switch (tp.tpc * tp.n_tap) {
       case 192: return launch_bn<192>(A, B, ep, tp, M, N, K, splits, s);
@@ -363,6 +560,15 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, uint64_t n, float
     hi[i] = h;
     lo[i] = v - h;
   }
+}
+
+// DS_GEMM_HALO=1 enables the halo conv tiles. Off by default: measured on B200 it is exact
+// but 1.2x slower for the AlexNet layers (the no-swizzle halo needs a 3-D TMA box with a
+// 16-byte inner dimension, which streams far slower than the 128-byte swizzled boxes, and
+// its smem budget allows fewer B stages); kept for experiments. Read per call.
+bool halo_enabled() {
+  const char* e = getenv("DS_GEMM_HALO");
+  return e && e[0] == '1';
 }
 
 bool exact_mode() {  // DS_GEMM_3XTF32=1: f32-accurate products (parity diagnostics; read per call)
@@ -425,6 +631,22 @@ int launch_gemm(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32_t
   if (tp.n > 0 && !tp.per_z && (tp.kt == 0 || tp.kt % 8)) return set_error(DS_E_CONTRACT, "gemm: tap width %% 8");
   tp.tpc = 1;
   tp.n_tap = N;
+  tp.halo_rows = 0;
+  if (tp.n > 0 && !tp.per_z && halo_enabled() && A.cols % 4 == 0 && A.ld % 4 == 0) {
+    // halo mode: one A column offset, shifts within 128 rows (a_row becomes the row inside the halo)
+    int32_t lo = tp.a_row[0], hi = tp.a_row[0];
+    bool same_col = (tp.a_col[0] % 4) == 0;
+    for (int t = 1; t < tp.n; ++t) {
+      lo = std::min(lo, tp.a_row[t]);
+      hi = std::max(hi, tp.a_row[t]);
+      same_col = same_col && tp.a_col[t] == tp.a_col[0];
+    }
+    if (same_col && hi - lo <= 128) {
+      tp.halo_lo = lo;
+      tp.halo_rows = static_cast<uint32_t>(kBM + hi - lo);
+      for (int t = 0; t < tp.n; ++t) tp.a_row[t] -= lo;
+    }
+  }
   if (tp.n > 1 && tp.per_z && tp.d_col_step == N) {  // stack taps along N: one A tile feeds up to 256 columns
     const uint32_t g = std::min<uint32_t>(static_cast<uint32_t>(tp.n), 256 / N);
     if (g > 1 && (g * N == 192 || g * N == 240 || g * N == 256)) {

@@ -27,6 +27,8 @@ struct GemmTaps {
   uint32_t kt = 0;          // accumulate mode: K columns per tap (multiple of 8)
   uint32_t d_col_step = 0;  // per_z: D column offset per tap
   int32_t a_row[kMaxTaps], a_col[kMaxTaps], b_row[kMaxTaps], b_col[kMaxTaps];
+  int32_t halo_lo = 0;      // internal (halo mode): first A row of the halo relative to m0
+  uint32_t halo_rows = 0;   // internal: rows per halo load (0 = per-tap A loads)
   uint32_t tpc = 1;         // internal (per_z): taps per CTA, their B tiles stacked along N
   uint32_t n_tap = 0;       // internal (per_z, tpc > 1): N columns per tap
 };
