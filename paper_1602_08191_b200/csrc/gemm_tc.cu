@@ -38,12 +38,17 @@ struct GemmSmem {
   static constexpr uint32_t A_BYTES = kBM * kBK * 4;  // 16 KB
   static constexpr uint32_t B_BYTES = BN * kBK * 4;
   static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
-  // BN <= 192: ~100 KB so two CTAs share an SM (one's epilogue overlaps the other's
-  // mainloop); wider tiles: one CTA with a deep ring
+  // ~100 KB so two CTAs share an SM: one's epilogue and prologue overlap the other's
+  // mainloop (measured better than one CTA with a deep ring for every tile width; the
+  // 256-wide tile then has 2 stages of 48 KB)
 #ifndef DS_GEMM_SMEM_SMALL
 #define DS_GEMM_SMEM_SMALL (100 * 1024)
 #endif
-  static constexpr uint32_t BUDGET = BN <= 192 ? DS_GEMM_SMEM_SMALL : 200 * 1024;
+#ifndef DS_GEMM_TWO_CTA_MAX_BN
+#define DS_GEMM_TWO_CTA_MAX_BN 256
+#endif
+  static constexpr bool TWO_CTA = BN <= DS_GEMM_TWO_CTA_MAX_BN && BN != 240;  // 240: grouped taps, deep ring
+  static constexpr uint32_t BUDGET = TWO_CTA ? DS_GEMM_SMEM_SMALL : 200 * 1024;
   static constexpr int STAGES = BUDGET / STAGE > 8 ? 8 : BUDGET / STAGE;
   static constexpr uint32_t TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;  // power of 2
@@ -93,7 +98,7 @@ __device__ __forceinline__ int64_t map_row(const GemmEpilogue& ep, uint32_t row)
 }
 
 template <int BN>
-__global__ void __launch_bounds__(kThreads, BN <= 192 ? 2 : 1)
+__global__ void __launch_bounds__(kThreads, GemmSmem<BN>::TWO_CTA ? 2 : 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmEpilogue ep, const __grid_constant__ GemmTaps tp, uint32_t M,
                      uint32_t N, uint32_t K, uint32_t k_per_split, uint32_t splits) {
