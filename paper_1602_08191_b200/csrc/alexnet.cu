@@ -540,6 +540,31 @@ struct Ctx {
   uint32_t* flags;
 };
 
+// A second stream per device for work that can run beside the main chain (weight-gradient
+// GEMMs beside data-gradient GEMMs, FC weight transposes beside the forward). Fork and join
+// are event edges, so the pair is captured into the engine's CUDA graph as parallel branches.
+struct Side {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[16] = {};
+};
+int side_stream(Side** out) {
+  static Side sides[64];
+  int dev = 0;
+  DS_CUDA_TRY(cudaGetDevice(&dev));
+  Side& sd = sides[dev & 63];
+  if (!sd.s) {
+    DS_CUDA_TRY(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
+    for (auto& e : sd.ev) DS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  *out = &sd;
+  return DS_OK;
+}
+int edge(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {  // `to` waits for `from`'s work so far
+  DS_CUDA_TRY(cudaEventRecord(ev, from));
+  DS_CUDA_TRY(cudaStreamWaitEvent(to, ev, 0));
+  return DS_OK;
+}
+
 // splits so that tiles * splits covers the SMs twice, each split >= 4 k-steps, slabs fit
 uint32_t pick_splits(uint32_t M, uint32_t N, uint64_t K, uint32_t ntaps = 1) {
   const uint32_t bn = gemm_pick_bn(N);
@@ -781,6 +806,15 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     return set_error(DS_E_CONTRACT, "alexnet: at most %llu rows per call",
                      static_cast<unsigned long long>((1ull << 31) / (96ull * sh.Hs * sh.Hs)));
   t_launches = 0;
+  Side* sd = nullptr;
+  DS_TRY(side_stream(&sd));
+  Ctx c2{sd->s, gate, w.part, flags};
+  if (grad) {  // the FC backward's transposed weights depend only on P: build them beside the forward
+    DS_TRY(edge(s, c2.s, sd->ev[0]));
+    DS_TRY(transpose(c2, P + L[7].w_off, sh.C, 4096, 4096, w.w8T, sh.Cp));
+    DS_TRY(transpose(c2, P + L[6].w_off, 4096, 4096, 4096, w.w7T, 4096));
+    DS_TRY(transpose(c2, P + L[5].w_off, 4096, static_cast<uint32_t>(sh.q5), sh.q5, w.w6T, 4096));
+  }
   DS_TRY(alex_forward(m, P, X, idx, R, w, c));
   softmax_ce_warp_kernel<<<(R + 7) / 8, 256, 0, s>>>(w.z, sh.Cp, y, idx, R, sh.C, w.loss_rows, grad ? w.dz : nullptr,
                                                      flags, gate);
@@ -788,26 +822,24 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   KDONE(2);
   DS_CUDA_TRY(cudaGetLastError());
   if (!grad) return DS_OK;
+  DS_TRY(edge(c2.s, s, sd->ev[1]));  // join: the transposed FC weights are ready
 
   // ---- fc8, fc7, fc6: dW = dh^T h / R ; db ; dh_prev = dh W, ReLU-masked -------------------
   DS_TRY(transpose(c, w.dz, R, sh.Cp, sh.Cp, w.zT, Rp));
   DS_TRY(transpose(c, w.h7, R, 4096, 4096, w.h7T, Rp));
   DS_TRY(gemm(c, w.zT, Rp, w.h7T, Rp, grad + L[7].w_off, 4096, sh.C, 4096, R, inv_b, nullptr, false));
   DS_TRY(colsum(c, w.dz, R, sh.C, sh.Cp, inv_b, grad + L[7].b_off, w.bpart));
-  DS_TRY(transpose(c, P + L[7].w_off, sh.C, 4096, 4096, w.w8T, sh.Cp));
   DS_TRY(gemm(c, w.dz, sh.Cp, w.w8T, sh.Cp, w.dh7, 4096, R, 4096, sh.C, 1.f, nullptr, false, w.h7, 4096));
   DS_TRY(transpose(c, w.dh7, R, 4096, 4096, w.dh7T, Rp));
   DS_TRY(transpose(c, w.h6, R, 4096, 4096, w.h6T, Rp));
   DS_TRY(gemm(c, w.dh7T, Rp, w.h6T, Rp, grad + L[6].w_off, 4096, 4096, 4096, R, inv_b, nullptr, false));
   DS_TRY(colsum(c, w.dh7, R, 4096, 4096, inv_b, grad + L[6].b_off, w.bpart));
-  DS_TRY(transpose(c, P + L[6].w_off, 4096, 4096, 4096, w.w7T, 4096));
   DS_TRY(gemm(c, w.dh7, 4096, w.w7T, 4096, w.dh6, 4096, R, 4096, 4096, 1.f, nullptr, false, w.h6, 4096));
   DS_TRY(transpose(c, w.dh6, R, 4096, 4096, w.dh6T, Rp));
   DS_TRY(transpose(c, w.p5, R, static_cast<uint32_t>(sh.q5), sh.q5, w.p5T, Rp));
   DS_TRY(gemm(c, w.dh6T, Rp, w.p5T, Rp, grad + L[5].w_off, sh.q5, 4096, static_cast<uint32_t>(sh.q5), R, inv_b,
               nullptr, false));
   DS_TRY(colsum(c, w.dh6, R, 4096, 4096, inv_b, grad + L[5].b_off, w.bpart));
-  DS_TRY(transpose(c, P + L[5].w_off, 4096, static_cast<uint32_t>(sh.q5), sh.q5, w.w6T, 4096));
   DS_TRY(gemm(c, w.dh6, 4096, w.w6T, 4096, w.dp5, sh.q5, R, static_cast<uint32_t>(sh.q5), 4096, 1.f, nullptr, false));
 
   // ---- conv5 .. conv2 on the padded grids ------------------------------------------------
@@ -826,16 +858,17 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     const ConvSpec cs = conv_spec(sh, l);
     const uint64_t G = 1ull * R * cs.Hp * cs.Hp, ldT = up4(static_cast<uint32_t>(G + 3));
     float* dout = dout_maps[l];
-    // bias gradient (border rows are zero)
-    DS_TRY(colsum(c, dout, G, cs.Cout, cs.Cout, inv_b, grad + L[l + 1].b_off, w.bpart));
-    // weight gradient from pixel-contiguous copies
-    DS_TRY(transpose(c, dout, G, cs.Cout, cs.Cout, w.trA, ldT));
+    // side stream: bias gradient (border rows are zero) and the weight gradient from
+    // pixel-contiguous copies, beside the main stream's data gradient of the same layer
+    DS_TRY(edge(s, c2.s, sd->ev[2 + l]));
+    DS_TRY(colsum(c2, dout, G, cs.Cout, cs.Cout, inv_b, grad + L[l + 1].b_off, w.bpart));
+    DS_TRY(transpose(c2, dout, G, cs.Cout, cs.Cout, w.trA, ldT));
     {
       dim3 grid(static_cast<unsigned>((ldT + 31) / 32), (cs.Cin + 31) / 32);
-      transpose_shift4_kernel<<<grid, 256, 0, s>>>(in_maps[l], G, cs.Cin, w.trB, ldT, gate);
+      transpose_shift4_kernel<<<grid, 256, 0, c2.s>>>(in_maps[l], G, cs.Cin, w.trB, ldT, gate);
       KDONE(1);
     }
-    DS_TRY(conv_wgrad(c, cs, R, w.trA, w.trB, ldT, inv_b, w.wtmp, grad + L[l + 1].w_off));
+    DS_TRY(conv_wgrad(c2, cs, R, w.trA, w.trB, ldT, inv_b, w.wtmp, grad + L[l + 1].w_off));
     // data gradient
     if (l >= 2) {  // into relu(conv3 / conv4): masked, same padded grid
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], dout_maps[l - 1], true, in_maps[l]));
@@ -858,12 +891,14 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   {
     const ConvSpec cs = conv1_spec(sh);
     const uint64_t G1 = 1ull * R * sh.Hs * sh.Hs, ldT = up4(static_cast<uint32_t>(G1 + 3));
-    DS_TRY(colsum(c, w.dc1p, G1, 96, 96, inv_b, grad + L[0].b_off, w.bpart));
-    DS_TRY(transpose(c, w.dc1p, G1, 96, 96, w.trA, ldT));
+    DS_TRY(edge(s, c2.s, sd->ev[6]));
+    DS_TRY(colsum(c2, w.dc1p, G1, 96, 96, inv_b, grad + L[0].b_off, w.bpart));
+    DS_TRY(transpose(c2, w.dc1p, G1, 96, 96, w.trA, ldT));
     dim3 grid(static_cast<unsigned>((ldT + 31) / 32), (48 + 31) / 32);
-    transpose_shift4_kernel<<<grid, 256, 0, s>>>(w.xs, G1, 48, w.trB, ldT, gate);
+    transpose_shift4_kernel<<<grid, 256, 0, c2.s>>>(w.xs, G1, 48, w.trB, ldT, gate);
     KDONE(1);
-    DS_TRY(conv_wgrad(c, cs, R, w.trA, w.trB, ldT, inv_b, w.wtmp, grad + L[0].w_off, true));
+    DS_TRY(conv_wgrad(c2, cs, R, w.trA, w.trB, ldT, inv_b, w.wtmp, grad + L[0].w_off, true));
+    DS_TRY(edge(c2.s, s, sd->ev[7]));  // join: every gradient is written when the main stream moves on
   }
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
