@@ -91,7 +91,7 @@ struct AlexWs {
   uint8_t *arg1, *arg2, *arg5;
   // backward
   float *dh7, *dh6, *dp5, *dc5p, *dc4p, *dc3p, *dp2p, *dn2, *dc2p, *dp1, *dn1, *dc1p;
-  float *xs, *trA, *trB, *part, *wtmp, *bpart;
+  float *xs, *trA, *trB, *part, *part2, *wtmp, *bpart;
   float *w1p, *wp[4], *wpT[4], *w6T, *w7T, *w8T, *zT, *h7T, *h6T, *p5T, *dh7T, *dh6T;
   double* loss_rows;
   uint64_t end;
@@ -121,7 +121,8 @@ AlexWs carve_ws(const ModelInfo& m, uint32_t R, void* base) {
   f(ws.xs, G1 * 48);
   const uint64_t trA = std::max({384 * (G3 + 8), 256 * (G2 + 8), 96 * (G1 + 8)});
   const uint64_t trB = 4 * std::max({384 * (G3 + 8), 96 * (G2 + 8), 48 * (G1 + 8)});
-  f(ws.trA, trA), f(ws.trB, trB), f(ws.part, kPartFloats), f(ws.wtmp, 384ull * 2304), f(ws.bpart, 4096ull * 512);
+  f(ws.trA, trA), f(ws.trB, trB), f(ws.part, kPartFloats), f(ws.part2, kPartFloats), f(ws.wtmp, 384ull * 2304);
+  f(ws.bpart, 4096ull * 512);
   f(ws.w1p, 96ull * 9 * 48);
   for (int l = 0; l < 4; ++l) {
     const ConvSpec c = conv_spec(s, l);
@@ -808,7 +809,7 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   t_launches = 0;
   Side* sd = nullptr;
   DS_TRY(side_stream(&sd));
-  Ctx c2{sd->s, gate, w.part, flags};
+  Ctx c2{sd->s, gate, w.part2, flags};  // its own split-K slabs
   if (grad) {  // the FC backward's transposed weights depend only on P: build them beside the forward
     DS_TRY(edge(s, c2.s, sd->ev[0]));
     DS_TRY(transpose(c2, P + L[7].w_off, sh.C, 4096, 4096, w.w8T, sh.Cp));
@@ -824,22 +825,26 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   if (!grad) return DS_OK;
   DS_TRY(edge(c2.s, s, sd->ev[1]));  // join: the transposed FC weights are ready
 
-  // ---- fc8, fc7, fc6: dW = dh^T h / R ; db ; dh_prev = dh W, ReLU-masked -------------------
-  DS_TRY(transpose(c, w.dz, R, sh.Cp, sh.Cp, w.zT, Rp));
-  DS_TRY(transpose(c, w.h7, R, 4096, 4096, w.h7T, Rp));
-  DS_TRY(gemm(c, w.zT, Rp, w.h7T, Rp, grad + L[7].w_off, 4096, sh.C, 4096, R, inv_b, nullptr, false));
-  DS_TRY(colsum(c, w.dz, R, sh.C, sh.Cp, inv_b, grad + L[7].b_off, w.bpart));
+  // ---- fc8, fc7, fc6: dW = dh^T h / R and db on the side stream; dh_prev = dh W (ReLU-masked)
+  // on the main stream ---------------------------------------------------------------------
+  DS_TRY(edge(s, c2.s, sd->ev[8]));
+  DS_TRY(transpose(c2, w.dz, R, sh.Cp, sh.Cp, w.zT, Rp));
+  DS_TRY(transpose(c2, w.h7, R, 4096, 4096, w.h7T, Rp));
+  DS_TRY(gemm(c2, w.zT, Rp, w.h7T, Rp, grad + L[7].w_off, 4096, sh.C, 4096, R, inv_b, nullptr, false));
+  DS_TRY(colsum(c2, w.dz, R, sh.C, sh.Cp, inv_b, grad + L[7].b_off, w.bpart));
   DS_TRY(gemm(c, w.dz, sh.Cp, w.w8T, sh.Cp, w.dh7, 4096, R, 4096, sh.C, 1.f, nullptr, false, w.h7, 4096));
-  DS_TRY(transpose(c, w.dh7, R, 4096, 4096, w.dh7T, Rp));
-  DS_TRY(transpose(c, w.h6, R, 4096, 4096, w.h6T, Rp));
-  DS_TRY(gemm(c, w.dh7T, Rp, w.h6T, Rp, grad + L[6].w_off, 4096, 4096, 4096, R, inv_b, nullptr, false));
-  DS_TRY(colsum(c, w.dh7, R, 4096, 4096, inv_b, grad + L[6].b_off, w.bpart));
+  DS_TRY(edge(s, c2.s, sd->ev[9]));
+  DS_TRY(transpose(c2, w.dh7, R, 4096, 4096, w.dh7T, Rp));
+  DS_TRY(transpose(c2, w.h6, R, 4096, 4096, w.h6T, Rp));
+  DS_TRY(gemm(c2, w.dh7T, Rp, w.h6T, Rp, grad + L[6].w_off, 4096, 4096, 4096, R, inv_b, nullptr, false));
+  DS_TRY(colsum(c2, w.dh7, R, 4096, 4096, inv_b, grad + L[6].b_off, w.bpart));
   DS_TRY(gemm(c, w.dh7, 4096, w.w7T, 4096, w.dh6, 4096, R, 4096, 4096, 1.f, nullptr, false, w.h6, 4096));
-  DS_TRY(transpose(c, w.dh6, R, 4096, 4096, w.dh6T, Rp));
-  DS_TRY(transpose(c, w.p5, R, static_cast<uint32_t>(sh.q5), sh.q5, w.p5T, Rp));
-  DS_TRY(gemm(c, w.dh6T, Rp, w.p5T, Rp, grad + L[5].w_off, sh.q5, 4096, static_cast<uint32_t>(sh.q5), R, inv_b,
+  DS_TRY(edge(s, c2.s, sd->ev[10]));
+  DS_TRY(transpose(c2, w.dh6, R, 4096, 4096, w.dh6T, Rp));
+  DS_TRY(transpose(c2, w.p5, R, static_cast<uint32_t>(sh.q5), sh.q5, w.p5T, Rp));
+  DS_TRY(gemm(c2, w.dh6T, Rp, w.p5T, Rp, grad + L[5].w_off, sh.q5, 4096, static_cast<uint32_t>(sh.q5), R, inv_b,
               nullptr, false));
-  DS_TRY(colsum(c, w.dh6, R, 4096, 4096, inv_b, grad + L[5].b_off, w.bpart));
+  DS_TRY(colsum(c2, w.dh6, R, 4096, 4096, inv_b, grad + L[5].b_off, w.bpart));
   DS_TRY(gemm(c, w.dh6, 4096, w.w6T, 4096, w.dp5, sh.q5, R, static_cast<uint32_t>(sh.q5), 4096, 1.f, nullptr, false));
 
   // ---- conv5 .. conv2 on the padded grids ------------------------------------------------
