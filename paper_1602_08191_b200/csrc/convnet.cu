@@ -643,6 +643,33 @@ static int cnn_forward(const ModelInfo& m, const float* P, const float* X, const
   return DS_OK;
 }
 
+namespace {
+// Side stream per device for the weight-gradient chain (tensor-core path): it forks off
+// the main stream after each layer's output gradient and runs beside the data-gradient
+// chain; the event edges are captured into the engine's CUDA graph as parallel branches.
+struct CnnSide {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[8] = {};
+};
+int cnn_side(CnnSide** out) {
+  static CnnSide sides[64];
+  int dev = 0;
+  DS_CUDA_TRY(cudaGetDevice(&dev));
+  CnnSide& sd = sides[dev & 63];
+  if (!sd.s) {
+    DS_CUDA_TRY(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
+    for (auto& e : sd.ev) DS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  *out = &sd;
+  return DS_OK;
+}
+int cnn_edge(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
+  DS_CUDA_TRY(cudaEventRecord(ev, from));
+  DS_CUDA_TRY(cudaStreamWaitEvent(to, ev, 0));
+  return DS_OK;
+}
+}  // namespace
+
 int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X, const uint32_t* idx, const uint32_t* y,
                              uint32_t R, float* grad, double* loss_out, void* ws_base, uint32_t* flags,
                              const uint32_t* gate, cudaStream_t s) {
@@ -656,6 +683,39 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   if (!grad) return DS_OK;
   const float inv_b = static_cast<float>(1.0 / static_cast<double>(R));
   const uint32_t nch4 = (R + 3) / 4;
+  if (use_tensor_cores()) {  // two streams: weight gradients beside the data-gradient chain
+    CnnSide* sd = nullptr;
+    DS_TRY(cnn_side(&sd));
+    const cudaStream_t s2 = sd->s;
+    DS_TRY(cnn_edge(s, s2, sd->ev[0]));
+    fc_bwd_w_kernel<<<blocks(C * 64), 256, 0, s2>>>(w.dz, w.h1, grad + L[4].w_off, grad + L[4].b_off, R, 64, C, inv_b,
+                                                    flags, gate);
+    fc_bwd_a_kernel<<<blocks(R * 64), 256, 0, s>>>(w.dz, P + L[4].w_off, w.dh1, R, 64, C, gate);
+    DS_TRY(cnn_edge(s, s2, sd->ev[1]));
+    fc_bwd_w_kernel<<<blocks(64 * 1024), 256, 0, s2>>>(w.dh1, w.p3, grad + L[3].w_off, grad + L[3].b_off, R, 1024, 64,
+                                                       inv_b, flags, gate);
+    fc_bwd_a_kernel<<<blocks(R * 1024), 256, 0, s>>>(w.dh1, P + L[3].w_off, w.dp3, R, 1024, 64, gate);
+    avepool_bwd2_kernel<<<blocks(R * 64 * 16), 256, 0, s>>>(w.dp3, w.c3, w.dc3, R * 64, 4, gate);
+    DS_CUDA_TRY(cudaGetLastError());
+    DS_TRY(cnn_edge(s, s2, sd->ev[2]));
+    DS_TRY((launch_conv5_wgrad_tc<32, 64, 8, 8>(w.p2, w.dc3, w.part, grad + L[2].w_off, grad + L[2].b_off, R, inv_b,
+                                                flags, gate, s2)));
+    DS_TRY((launch_conv5_tc<64, 32, 8>(w.dc3, P + L[2].w_off, true, w.wpk, nullptr, w.dp2, R, false, gate, s)));
+    avepool_bwd2_kernel<<<blocks(R * 32 * 64), 256, 0, s>>>(w.dp2, w.c2, w.dc2, R * 32, 8, gate);
+    DS_CUDA_TRY(cudaGetLastError());
+    DS_TRY(cnn_edge(s, s2, sd->ev[3]));
+    DS_TRY((launch_conv5_wgrad_tc<32, 32, 16, 4>(w.p1, w.dc2, w.part, grad + L[1].w_off, grad + L[1].b_off, R, inv_b,
+                                                 flags, gate, s2)));
+    DS_TRY((launch_conv5_tc<32, 32, 16>(w.dc2, P + L[1].w_off, true, w.wpk, nullptr, w.dr1, R, false, gate, s)));
+    maxpool_relu_bwd2_kernel<<<blocks(R * 32 * 256), 256, 0, s>>>(w.dr1, w.arg1, w.dc1, R * 32, 16, gate);
+    DS_CUDA_TRY(cudaGetLastError());
+    DS_TRY(cnn_edge(s, s2, sd->ev[4]));
+    DS_TRY((launch_conv5_wgrad_tc<3, 32, 32, 1>(idx ? w.x0 : X, w.dc1, w.part, grad + L[0].w_off, grad + L[0].b_off, R,
+                                                inv_b, flags, gate, s2)));
+    DS_TRY(cnn_edge(s2, s, sd->ev[5]));  // join: all gradients written
+    DS_CUDA_TRY(cudaGetLastError());
+    return DS_OK;
+  }
   // ip2, ip1
   fc_bwd_w_kernel<<<blocks(C * 64), 256, 0, s>>>(w.dz, w.h1, grad + L[4].w_off, grad + L[4].b_off, R, 64, C, inv_b,
                                                  flags, gate);
