@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--tau", type=int, default=10)
-    ap.add_argument("--e2e-steps", type=int, default=500)
+    ap.add_argument("--e2e-steps", type=int, default=2000)
     ap.add_argument("--exchange-params", type=int, default=256 * 1024 * 1024)
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / exchange sweep / cpu baseline (profiling)")
     ap.add_argument("--cifar-steps", type=int, default=200, help="timed steps of the cifar10_quick leg (0 = skip)")
@@ -330,17 +330,23 @@ def e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n):
              torch.empty(B, dtype=torch.int32, pin_memory=True)) for _ in range(4)]
     views = [(xb.numpy(), yb.numpy().view(np.uint32)) for xb, yb in bufs]
     losses = torch.zeros(K, dtype=torch.float64, pin_memory=True)
+
+    def stream_run(steps):
+        L.check(L.lib.ds_engine_stream_begin(eng, steps, C.c_void_p(losses.data_ptr())))
+        for s in range(steps):
+            r, k = int(sizes[s]), s & 3
+            np.take(X, idx[s, :r], axis=0, out=views[k][0][:r])
+            np.take(y, idx[s, :r], out=views[k][1][:r])
+            L.check(L.lib.ds_engine_stream_push(eng, C.c_void_p(bufs[k][0].data_ptr()),
+                                                C.c_void_p(bufs[k][1].data_ptr()), r))
+        L.check(L.lib.ds_engine_stream_end(eng))
+
+    L.check(L.lib.ds_engine_reserve(eng, min(K, 100) + K))  # TrainLog room: no allocation while timed
+    stream_run(min(K, 100))  # warm-up session: first-touch of the pinned ring, host caches
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    L.check(L.lib.ds_engine_stream_begin(eng, K, C.c_void_p(losses.data_ptr())))
-    for s in range(K):
-        r, k = int(sizes[s]), s & 3
-        np.take(X, idx[s, :r], axis=0, out=views[k][0][:r])
-        np.take(y, idx[s, :r], out=views[k][1][:r])
-        L.check(L.lib.ds_engine_stream_push(eng, C.c_void_p(bufs[k][0].data_ptr()), C.c_void_p(bufs[k][1].data_ptr()),
-                                            r))
-    L.check(L.lib.ds_engine_stream_end(eng))
+    stream_run(K)
     secs = time.perf_counter() - t0
     ok = bool(np.isfinite(losses.numpy()).all())
     t = torch.tensor([secs], dtype=torch.float64, device="cuda")
