@@ -134,6 +134,12 @@ struct ds_engine {
   const void* graph_key[3] = {};
   uint32_t* cur_idx = nullptr;             // [B] the step's shard rows (set_idx_kernel)
   ds_sync* sync = nullptr;                 // synchronous data-parallel mode (ds_engine_attach_sync)
+  // sync mode: the gradient pass captured once per gradient slot (the group alternates two
+  // slots), replayed between the eager round kernels (wait / reduce+update / publish)
+  cudaGraphExec_t sync_graph[2] = {};
+  float* sync_slot[2] = {};
+  bool sync_eager[2] = {};
+  const void* sync_key[4] = {};
   unsigned long long* step_ctr = nullptr;  // device step counter within a run
   uint32_t hostfed_rows = 0;
   bool hostfed = false;
@@ -253,6 +259,8 @@ __global__ void set_idx_kernel(const uint32_t* __restrict__ plan, uint32_t B, un
 }
 
 // One layered iteration (everything but the exchange) on e->stream.
+bool graphs_enabled();
+
 int layered_step(ds_engine* e, const float* X, const uint32_t* y, const uint32_t* idx, uint32_t R, bool set_idx) {
   const uint64_t B = e->hp.batch_size;
   const float eta = static_cast<float>(e->hp.eta);
@@ -266,8 +274,41 @@ int layered_step(ds_engine* e, const float* X, const uint32_t* y, const uint32_t
   if (e->sync) {  // simulate_sync (simulator.cpp:156-223) across the group's GPUs
     float* slot = nullptr;
     DS_TRY(ds_sync_begin(e->sync, &slot, e->stream));
-    DS_TRY(launch_loss_and_grad(e->model, p, X, idx, y, R, slot, &e->st->loss, e->ws, &e->st->flags, &e->st->err,
-                                e->stream));
+    int k = -1;  // which captured gradient pass (per slot) applies, if any
+    if (set_idx && !e->hostfed && R == e->hp.batch_size && graphs_enabled()) {
+      const void* key[4] = {X, y, p, e->ws};
+      if (std::memcmp(key, e->sync_key, sizeof(key)) != 0) {  // buffers moved: drop the old captures
+        for (int q = 0; q < 2; ++q) {
+          if (e->sync_graph[q]) cudaGraphExecDestroy(e->sync_graph[q]);
+          e->sync_graph[q] = nullptr;
+          e->sync_slot[q] = nullptr;
+          e->sync_eager[q] = false;
+        }
+        std::memcpy(e->sync_key, key, sizeof(key));
+      }
+      for (int q = 0; q < 2 && k < 0; ++q)
+        if (e->sync_slot[q] == slot || !e->sync_slot[q]) k = q, e->sync_slot[q] = slot;
+    }
+    if (k >= 0 && e->sync_graph[k]) {
+      DS_CUDA_TRY(cudaGraphLaunch(e->sync_graph[k], e->stream));
+    } else {
+      DS_TRY(launch_loss_and_grad(e->model, p, X, idx, y, R, slot, &e->st->loss, e->ws, &e->st->flags, &e->st->err,
+                                  e->stream));
+      if (k >= 0 && e->sync_eager[k]) {  // second use of this slot: record the pass for replay
+        cudaGraph_t g = nullptr;
+        DS_CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = launch_loss_and_grad(e->model, p, X, idx, y, R, slot, &e->st->loss, e->ws, &e->st->flags,
+                                            &e->st->err, e->stream);
+        const cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
+        if (rc != DS_OK) return rc;
+        if (ce != cudaSuccess) return set_error(DS_E_CUDA, "engine: sync capture: %s", cudaGetErrorString(ce));
+        const cudaError_t ie = cudaGraphInstantiate(&e->sync_graph[k], g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) return set_error(DS_E_CUDA, "engine: sync graph: %s", cudaGetErrorString(ie));
+      } else if (k >= 0) {
+        e->sync_eager[k] = true;
+      }
+    }
     DS_TRY(ds_sync_reduce_update(e->sync, p, eta, wd, &e->st->flags, e->stream));
     policy_kernel<<<1, 1, 0, e->stream>>>(e->st, e->log);
     DS_CUDA_TRY(cudaGetLastError());
@@ -621,6 +662,8 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->d_tickets);
   cudaFree(e->velocity);
   if (e->step_graph) cudaGraphExecDestroy(e->step_graph);
+  for (auto& g : e->sync_graph)
+    if (g) cudaGraphExecDestroy(g);
   cudaFree(e->cur_idx);
   cudaFree(e->step_ctr);
   cudaFree(e->ring_X);
