@@ -198,6 +198,87 @@ __device__ void do_exchange(const FusedArgs& A, float* p, const Slice& sl, uint6
   }
 }
 
+// mlp_kernel's exchange: as do_exchange, but the CTA's own W1 rows (slice 0, contiguous,
+// 16-byte aligned) go four elements per thread with their loads issued up front, and the
+// updated values are written straight into the resident copies (Ws f32, Wd f64) instead of
+// re-reading the rows afterwards. The other slices (b1, W2 columns, b2) are tiny.
+__device__ void exchange_shard_mlp(float* p, const ShardTable& t, int s, const Slice& sl, float a, float* Ws,
+                                   double* Wd, uint32_t F, uint32_t Fd) {
+  const uint64_t b0 = t.begin[s], b1 = t.begin[s + 1];
+  const uint64_t lo = sl.lo[0];
+  const uint32_t n = sl.cols[0];  // Uo * F, one row
+  float* m0 = t.ptr[s] - b0;      // m0[g] = center element g
+  for (uint32_t j = threadIdx.x * 4; j < n; j += kFT * 4) {
+    const uint64_t g = lo + j;
+    float w[4], m[4], wo[4], mo[4];
+    bool in[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) in[q] = g + q >= b0 && g + q < b1 && j + q < n;
+    if (in[0] && in[3] && ((g - b0) & 3) == 0 && (g & 3) == 0) {
+      const float4 wv = *reinterpret_cast<const float4*>(p + g);
+      const float4 mv = __ldcg(reinterpret_cast<const float4*>(m0 + g));
+      w[0] = wv.x, w[1] = wv.y, w[2] = wv.z, w[3] = wv.w;
+      m[0] = mv.x, m[1] = mv.y, m[2] = mv.z, m[3] = mv.w;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) elastic_elem(w[q], m[q], a, wo[q], mo[q]);
+      *reinterpret_cast<float4*>(p + g) = make_float4(wo[0], wo[1], wo[2], wo[3]);
+      __stcg(reinterpret_cast<float4*>(m0 + g), make_float4(mo[0], mo[1], mo[2], mo[3]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!in[q]) continue;
+        elastic_elem(p[g + q], __ldcg(m0 + g + q), a, wo[q], mo[q]);
+        p[g + q] = wo[q];
+        __stcg(m0 + g + q, mo[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!in[q]) continue;
+      const uint32_t local = j + q, uu = local / F, i = local - uu * F;
+      Ws[local] = wo[q];
+      Wd[uu * Fd + i] = static_cast<double>(wo[q]);
+    }
+  }
+  for (int k = 1; k < sl.n; ++k) {
+    const uint32_t nk = sl.rows[k] * sl.cols[k];
+    for (uint32_t j = threadIdx.x; j < nk; j += kFT) {
+      const uint32_t r = j / sl.cols[k];
+      const uint64_t g = sl.lo[k] + r * sl.row_stride[k] + (j - r * sl.cols[k]);
+      if (g >= b0 && g < b1) exchange_elem(p, t, s, g, a);
+    }
+  }
+}
+
+__device__ void do_exchange_mlp(const FusedArgs& A, float* p, const Slice& sl, uint64_t ticket, unsigned int G,
+                                float* Ws, double* Wd, uint32_t F, uint32_t Fd) {
+  const ShardTable& t = A.table;
+  const bool ordered = ticket != kNoTicket;
+  for (int s = 0; s < t.n; ++s) {
+    if (ordered) {
+      if (threadIdx.x == 0)
+        while (ld_acquire_sys(reinterpret_cast<const uint64_t*>(&t.flags[s]->seq)) != ticket) nanosleep_ns(64);
+      __syncthreads();
+    }
+    exchange_shard_mlp(p, t, s, sl, A.alpha, Ws, Wd, F, Fd);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (ordered) {
+        __threadfence_system();
+        const unsigned long long old = atomicAdd_system(&t.flags[s]->done, 1ull);
+        if (old == G - 1) {
+          t.flags[s]->done = 0;
+          if (s == 0) t.flags[0]->exchanges += 1;
+          __threadfence_system();
+          st_release_sys(reinterpret_cast<uint64_t*>(&t.flags[s]->seq), ticket + 1);
+        }
+      } else if (s == 0 && blockIdx.x == 0) {
+        atomicAdd_system(&t.flags[0]->exchanges, 1ull);
+      }
+    }
+  }
+}
+
 struct PolicyLocal {
   double cum;
   double cut;       // launch constants (DevState), cached so the per-step update
@@ -1459,8 +1540,7 @@ __global__ void __launch_bounds__(kFT, 1) mlp_kernel(FusedArgs A) {
         __syncthreads();
         tk = s_ticket;
       }
-      do_exchange(A, Pn, sl, tk, G);
-      load_own_rows(Pn);  // the exchange moved the resident rows too
+      do_exchange_mlp(A, Pn, sl, tk, G, Ws, Wd, F, Fd);  // also refreshes the resident own rows
       ++xcount;
     }
     cur ^= 1;
