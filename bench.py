@@ -159,6 +159,20 @@ def run_reference(args):
         secs = time.perf_counter() - t0
         n = 1
     value = n * args.batch * steps / secs
+    all_cores = None
+    if kind == "reference":
+        # The same loop with one worker thread per host core (up to 64), for scale: the
+        # reference parallelises only across workers (each SgdEngine step is one thread),
+        # so this is its whole-box throughput; `value` stays on this arm's config.
+        W = max(1, min(os.cpu_count() or 1, 64))
+        if W > n:
+            small = (shards[0][0][:4800], shards[0][1][:4800])  # batch cost does not depend on shard size
+            steps_w = int(min(args.steps, max(10, 20.0 / per)))
+            secs_w = orc.workers_time(m, [small] * W, NCLS, hp, init, True, 3, steps_w)
+            all_cores = {"workers": W, "value": W * args.batch * steps_w / secs_w, "unit": "samples/s",
+                         "steps": steps_w,
+                         "note": "reference n-worker loop, one thread per host core, LockFree in-process "
+                                 "MasterState; not this arm's config (one worker per GPU)"}
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": steps,
             "warmup": warm, "ms_per_step": 1000.0 * secs / steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference gen_synthetic, per-worker seeds)",
@@ -168,6 +182,8 @@ def run_reference(args):
                              "sample": f"{steps} timed iterations per worker x {n} worker thread(s) "
                                        f"(+{warm} warmup), LockFree in-process MasterState, tau={args.tau}"},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if all_cores:
+        line["all_cores"] = all_cores
     print(json.dumps(line), flush=True)
     return 0
 
