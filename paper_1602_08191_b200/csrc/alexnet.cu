@@ -549,7 +549,9 @@ struct Side {
   cudaEvent_t ev[16] = {};
 };
 int side_stream(Side** out) {
-  static Side sides[64];
+  // per host thread: the fork/join events must not be shared between engines driven from
+  // different threads (an interleaved record would retarget another engine's wait)
+  thread_local Side sides[64];
   int dev = 0;
   DS_CUDA_TRY(cudaGetDevice(&dev));
   Side& sd = sides[dev & 63];

@@ -652,7 +652,7 @@ struct CnnSide {
   cudaEvent_t ev[8] = {};
 };
 int cnn_side(CnnSide** out) {
-  static CnnSide sides[64];
+  thread_local CnnSide sides[64];  // per host thread: events are not shared across threads
   int dev = 0;
   DS_CUDA_TRY(cudaGetDevice(&dev));
   CnnSide& sd = sides[dev & 63];
