@@ -258,12 +258,19 @@ __global__ void __launch_bounds__(kThreads, GemmSmem<BN>::TWO_CTA ? 2 : 1)
 }
 
 // Halo variant of the accumulating taps mode (conv forward / data gradient; opt-in, see
-// halo_enabled), usable when the taps' A row shifts span <= 128 rows: per 32-channel chunk the CTA loads the A rows
-// [m0 + lo, m0 + 128 + hi) ONCE and every tap's MMA reads its 128-row window inside that
-// buffer; only the B tiles stream per tap. The halo uses the canonical no-swizzle K-major
-// layout [8 k-chunks][rows][16 B] (a 3-D TMA box {4 floats, rows, 8}), in which consecutive
-// rows are 16 bytes apart, so a tap's window is just the start address + 16 * shift.
+// halo_enabled), usable when the taps' A row shifts span <= 128 rows: per 32-channel chunk
+// the CTA loads the A rows [m0 + lo, m0 + 128 + hi) ONCE and every tap's MMA reads its
+// 128-row window inside that buffer; only the B tiles stream per tap. Layout
+// (DS_HALO_SW128): 128-byte swizzled rows (a window starts 128 * shift bytes in), or the
+// canonical no-swizzle K-major layout [8 k-chunks][rows][16 B] (3-D TMA box), in which
+// consecutive rows are 16 bytes apart.
 // A traffic per chunk drops from taps x 16 KB to halo_rows x 128 B.
+#ifndef DS_HALO_SW128
+#define DS_HALO_SW128 1   // 128-byte swizzled halo rows; the start may sit anywhere in the 8-row atom (base offset 0)
+#endif
+#ifndef DS_HALO_BASEOFF
+#define DS_HALO_BASEOFF 0
+#endif
 constexpr uint32_t kHaloBytes = 256 * 128;
 template <int BN>
 struct HaloSmem {
@@ -317,8 +324,13 @@ __global__ void __launch_bounds__(kThreads, HaloSmem<BN>::TOTAL <= 113 * 1024 ? 
         const uint32_t h = kc & 1;
         if (kc >= 2) tc::mbar_wait(&hempty[h], ((kc >> 1) - 1) & 1);
         mbar_expect_tx(&hfull[h], hrows * 128);
+#if DS_HALO_SW128
+        tma_load_2d(halo + h * kHaloBytes, &tmA3, &hfull[h], tp.a_col[0] + static_cast<int>(kc * kBK),
+                    static_cast<int>(m0) + tp.halo_lo);
+#else
         tma_load_3d(halo + h * kHaloBytes, &tmA3, &hfull[h], 0, static_cast<int>(m0) + tp.halo_lo,
                     tp.a_col[0] / 4 + static_cast<int>(kc * 8));
+#endif
         for (uint32_t t = 0; t < ntap; ++t, ++bi) {
           const uint32_t s = bi % kB;
           if (bi >= kB) tc::mbar_wait(&bempty[s], ((bi / kB) - 1) & 1);
@@ -342,9 +354,24 @@ __global__ void __launch_bounds__(kThreads, HaloSmem<BN>::TOTAL <= 113 * 1024 ? 
           const uint32_t s = bi % kB;
           tc::mbar_wait(&bfull[s], (bi / kB) & 1);
           tc::fence_after();
+#if DS_HALO_SW128
+          // 128-byte swizzled rows: a tap's window starts whole rows into the halo
+          const uint32_t a = abase + static_cast<uint32_t>(tp.a_row[t]) * 128, b = tc::saddr(bst + s * S::B_BYTES);
+#else
           const uint32_t a = abase + static_cast<uint32_t>(tp.a_row[t]) * 16, b = tc::saddr(bst + s * S::B_BYTES);
+#endif
           for (uint32_t kk = 0; kk < nsub; ++kk) {
+#if DS_HALO_SW128
+            uint64_t da = sdesc_sw128(a + kk * 32);
+#if DS_HALO_BASEOFF == 1
+            da |= static_cast<uint64_t>(((a + kk * 32) >> 7) & 7) << 49;
+#elif DS_HALO_BASEOFF == 2
+            da |= static_cast<uint64_t>((8 - (((a + kk * 32) >> 7) & 7)) & 7) << 49;
+#endif
+            const uint64_t db = sdesc_sw128(b + kk * 32);
+#else
             const uint64_t da = tc::sdesc(a + kk * 2 * lbo, lbo, 128), db = sdesc_sw128(b + kk * 32);
+#endif
             const uint32_t acc = (kc | t | kk) ? 1u : 0u;
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -476,7 +503,11 @@ template <int BN>
 int launch_halo(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep, const GemmTaps& tp, uint32_t M,
                 uint32_t N, cudaStream_t s) {
   CUtensorMap ma, mb;
+#if DS_HALO_SW128
+  DS_TRY(make_map(&ma, A.p, A.rows, A.cols, A.ld, tp.halo_rows));
+#else
   DS_TRY(make_map_halo(&ma, A, tp.halo_rows));
+#endif
   DS_TRY(make_map(&mb, B.p, B.rows, B.cols, B.ld, BN));
   static uint64_t attr_set = 0;  // per device
   int dev = 0;
@@ -567,10 +598,12 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, uint64_t n, float
   }
 }
 
-// DS_GEMM_HALO=1 enables the halo conv tiles. Off by default: measured on B200 it is exact
-// but 1.2x slower for the AlexNet layers (the no-swizzle halo needs a 3-D TMA box with a
-// 16-byte inner dimension, which streams far slower than the 128-byte swizzled boxes, and
-// its smem budget allows fewer B stages); kept for experiments. Read per call.
+// DS_GEMM_HALO=1 enables the halo conv tiles. Off by default: measured on B200 both halo
+// layouts are exact but slower end to end for the AlexNet layers — the canonical no-swizzle
+// halo (3-D TMA box, 16-byte inner dimension) 1.2x, the 128-byte swizzled halo (tap windows
+// start at any row of the 8-row swizzle atom; the descriptor base offset stays 0 because the
+// hardware swizzles on absolute address bits — tools/taps_test.cu ACC_TAPS checks it) 1.15x:
+// the per-tap operand traffic it removes was not the limiter. Read per call.
 bool halo_enabled() {
   const char* e = getenv("DS_GEMM_HALO");
   return e && e[0] == '1';

@@ -51,6 +51,40 @@ int main(int argc, char** argv) {
     printf("  %.1f TFLOP/s (bn %u)\n", 2.0 * M * N * K * 20 / (ms / 1e3) / 1e12, gemm_pick_bn(N));
     return 0;
   }
+  if (getenv("ACC_TAPS")) {  // accumulate mode: D[m][n] = sum_t sum_k A[m + sh_t][k] B[n][t*K + k]
+    const int SH[9] = {-17, -16, -15, -1, 0, 1, 15, 16, 17};
+    std::vector<float> Bt(static_cast<size_t>(N) * T * K), Dt(static_cast<size_t>(M) * N, -7.f);
+    for (auto& v : Bt) v = (rand() % 2001 - 1000) / 1000.f;
+    float *dBt, *dDt;
+    cudaMalloc(&dBt, Bt.size() * 4);
+    cudaMalloc(&dDt, Dt.size() * 4);
+    cudaMemcpy(dBt, Bt.data(), Bt.size() * 4, cudaMemcpyHostToDevice);
+    GemmTaps ta;
+    ta.n = T;
+    ta.kt = K;
+    for (int t = 0; t < T; ++t) ta.a_row[t] = SH[t % 9], ta.a_col[t] = 0, ta.b_row[t] = 0, ta.b_col[t] = t * K;
+    GemmEpilogue e1;
+    e1.D = dDt;
+    e1.ldd = N;
+    GemmOperand a1{dA, M, K, ld}, b1{dBt, N, static_cast<uint64_t>(T) * K, static_cast<uint64_t>(T) * K};
+    int rc1 = launch_gemm(a1, b1, M, N, 0, &ta, e1, 1, nullptr, 0);
+    cudaError_t ee = cudaDeviceSynchronize();
+    cudaMemcpy(Dt.data(), dDt, Dt.size() * 4, cudaMemcpyDeviceToHost);
+    double me = 0;
+    for (uint32_t m = 0; m < M; ++m)
+      for (uint32_t n = 0; n < N; ++n) {
+        double r = 0;
+        for (int t = 0; t < T; ++t) {
+          const int mm = static_cast<int>(m) + SH[t % 9];
+          if (mm < 0 || mm >= static_cast<int>(M)) continue;
+          for (uint32_t k = 0; k < K; ++k) r += A[mm * ld + k] * Bt[(static_cast<size_t>(n) * T + t) * K + k];
+        }
+        me = fmax(me, fabs(r - Dt[m * N + n]));
+      }
+    printf("acc taps %d M %u N %u K %u (rc %d, %s, halo %s): max err %.3e\n", T, M, N, K, rc1, cudaGetErrorString(ee),
+           getenv("DS_GEMM_HALO") ? getenv("DS_GEMM_HALO") : "0", me);
+    return 0;
+  }
   GemmTaps tp;
   tp.n = T;
   tp.per_z = 1;
