@@ -342,19 +342,20 @@ def e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n):
     K = min(args.e2e_steps, args.steps)
     B = args.batch
     idx, sizes = api.sweep_batches(len(y), B, sweep_seed + 1, K)
-    bufs = [(torch.empty((B, F), dtype=torch.float32, pin_memory=True),
-             torch.empty(B, dtype=torch.int32, pin_memory=True)) for _ in range(4)]
-    views = [(xb.numpy(), yb.numpy().view(np.uint32)) for xb, yb in bufs]
+    idx = np.ascontiguousarray(idx, dtype=np.uint32)
+    Xh = np.ascontiguousarray(X, dtype=np.float32)
+    yh = np.ascontiguousarray(y, dtype=np.uint32)
     losses = torch.zeros(K, dtype=torch.float64, pin_memory=True)
+    push = L.lib.ds_engine_stream_push_rows
+    xp, yp = C.c_void_p(Xh.ctypes.data), C.c_void_p(yh.ctypes.data)
+    row_ptr = [C.c_void_p(idx[s].ctypes.data) for s in range(K)]
 
     def stream_run(steps):
+        # the host side of the reference worker loop: ShardSweeper order (precomputed above),
+        # gather_batch into the engine's pinned ring slot and push (ds_engine_stream_push_rows)
         L.check(L.lib.ds_engine_stream_begin(eng, steps, C.c_void_p(losses.data_ptr())))
         for s in range(steps):
-            r, k = int(sizes[s]), s & 3
-            np.take(X, idx[s, :r], axis=0, out=views[k][0][:r])
-            np.take(y, idx[s, :r], out=views[k][1][:r])
-            L.check(L.lib.ds_engine_stream_push(eng, C.c_void_p(bufs[k][0].data_ptr()),
-                                                C.c_void_p(bufs[k][1].data_ptr()), r))
+            L.check(push(eng, xp, yp, row_ptr[s], int(sizes[s])))
         L.check(L.lib.ds_engine_stream_end(eng))
 
     L.check(L.lib.ds_engine_reserve(eng, min(K, 100) + K))  # TrainLog room: no allocation while timed
@@ -370,9 +371,10 @@ def e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return {"value": n * B * K / t.item(), "unit": "samples/s", "h2d_bytes_per_step": B * F * 4 + B * 4 + 4,
             "d2h_bytes_per_step": 8, "steps": K, "losses_finite": ok,
-            "path": "ds_engine_stream_*: host gather into pinned memory + H2D copy per step into a 4-slot device "
-                    "ring, one persistent fused launch (step + exchange every tau), per-step loss written to "
-                    "mapped host memory; wall clock from stream_begin to stream_end"}
+            "path": "ds_engine_stream_*: per step ds_engine_stream_push_rows gathers the batch rows from the "
+                    "host shard into a pinned ring slot and copies it H2D into a 4-slot device ring; one "
+                    "persistent fused launch (step + exchange every tau) consumes it and writes each step's "
+                    "loss to mapped host memory; wall clock from stream_begin to stream_end"}
 
 
 def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind):

@@ -327,6 +327,11 @@ int ds_engine_step_host_async(ds_engine* e, const float* X_host, const uint32_t*
  * 20 s makes the kernel finish with DS_FLAG_STREAM_TIMEOUT rather than hang. */
 int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss_host);
 int ds_engine_stream_push(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows);
+/* As ds_engine_stream_push, but gathers the batch itself: rows idx[0..rows) of the host
+ * shard (X_host f32 [n x F], y_host u32 [n], any host memory) are copied into an
+ * engine-owned pinned staging slot (gather_batch, model.cpp:12-21) and pushed. */
+int ds_engine_stream_push_rows(ds_engine* e, const float* X_host, const uint32_t* y_host, const uint32_t* idx,
+                               uint32_t rows);
 int ds_engine_stream_end(ds_engine* e);
 /* Block until the engine's queued work finished; returns DS_E_NUMERIC/DS_E_CONTRACT
  * if any step hit the reference's error conditions (message names the iteration). */

@@ -125,6 +125,8 @@ struct ds_engine {
   cudaStream_t copy_stream = nullptr;
   bool ring_active = false;
   uint64_t ring_steps = 0, ring_pushed = 0;
+  float* ring_hX = nullptr;      // engine-owned pinned staging [kRing][B][F] (ds_engine_stream_push_rows)
+  uint32_t* ring_hy = nullptr;
   double* ring_loss = nullptr;
   float mu = 0.0f;            // momentum (layered path), ds_engine_set_momentum
   float* velocity = nullptr;
@@ -661,6 +663,8 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->plan_rows);
   cudaFree(e->d_tickets);
   cudaFree(e->velocity);
+  if (e->ring_hX) cudaFreeHost(e->ring_hX);
+  if (e->ring_hy) cudaFreeHost(e->ring_hy);
   if (e->step_graph) cudaGraphExecDestroy(e->step_graph);
   for (auto& g : e->sync_graph)
     if (g) cudaGraphExecDestroy(g);
@@ -988,15 +992,15 @@ extern "C" int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss
   return rc;
 }
 
-extern "C" int ds_engine_stream_push(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows) {
-  if (!e || !X_host || !y_host) return set_error(DS_E_CONTRACT, "engine_stream_push: null");
+namespace {
+// stream mode: validate a push and wait until ring slot (step % kRing) is free again (its
+// previous step has been read by every CTA, which also means its H2D copy completed)
+int stream_slot_ready(ds_engine* e, uint32_t rows) {
   if (!e->ring_active) return set_error(DS_E_STATE, "engine_stream_push: no open stream");
   if (e->ring_pushed >= e->ring_steps) return set_error(DS_E_STATE, "engine_stream_push: all steps already pushed");
   if (rows == 0 || rows > e->hp.batch_size) return set_error(DS_E_CONTRACT, "engine_stream_push: bad row count");
-  dsb::DeviceScope ds(e->device);
-  const uint64_t s = e->ring_pushed, K = ds_engine::kRing, B = e->hp.batch_size, F = e->model.n_features;
-  const uint64_t slot = s % K;
-  if (s >= K) {  // the slot's previous step (s - K) must have been read by every CTA
+  const uint64_t s = e->ring_pushed, K = ds_engine::kRing;
+  if (s >= K) {
     const auto t0 = std::chrono::steady_clock::now();
     while (*reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) < s - K + 1) {
       if (cudaStreamQuery(e->stream) != cudaErrorNotReady)
@@ -1005,6 +1009,12 @@ extern "C" int ds_engine_stream_push(ds_engine* e, const float* X_host, const ui
         return set_error(DS_E_CUDA, "engine_stream_push: device stopped consuming");
     }
   }
+  return DS_OK;
+}
+
+int stream_enqueue(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows) {
+  const uint64_t s = e->ring_pushed, K = ds_engine::kRing, B = e->hp.batch_size, F = e->model.n_features;
+  const uint64_t slot = s % K;
   // one word carries the row count and the step (mod 2^20; slots are reused 4 steps apart)
   e->ring_src[K + slot] = (rows << 20) | (static_cast<uint32_t>(s + 1) & 0xFFFFFu);
   cudaStream_t cs = e->copy_stream;
@@ -1014,6 +1024,34 @@ extern "C" int ds_engine_stream_push(ds_engine* e, const float* X_host, const ui
                               cudaMemcpyHostToDevice, cs));
   ++e->ring_pushed;
   return DS_OK;
+}
+}  // namespace
+
+extern "C" int ds_engine_stream_push(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows) {
+  if (!e || !X_host || !y_host) return set_error(DS_E_CONTRACT, "engine_stream_push: null");
+  dsb::DeviceScope ds(e->device);
+  DS_TRY(stream_slot_ready(e, rows));
+  return stream_enqueue(e, X_host, y_host, rows);
+}
+
+extern "C" int ds_engine_stream_push_rows(ds_engine* e, const float* X_host, const uint32_t* y_host,
+                                          const uint32_t* idx, uint32_t rows) {
+  if (!e || !X_host || !y_host || !idx) return set_error(DS_E_CONTRACT, "engine_stream_push_rows: null");
+  dsb::DeviceScope ds(e->device);
+  DS_TRY(stream_slot_ready(e, rows));
+  const uint64_t K = ds_engine::kRing, B = e->hp.batch_size, F = e->model.n_features;
+  if (!e->ring_hX) {
+    DS_CUDA_TRY(cudaHostAlloc(&e->ring_hX, K * B * F * sizeof(float), cudaHostAllocDefault));
+    DS_CUDA_TRY(cudaHostAlloc(&e->ring_hy, K * B * sizeof(uint32_t), cudaHostAllocDefault));
+  }
+  const uint64_t slot = e->ring_pushed % K;  // free: its previous copy has been consumed
+  float* hx = e->ring_hX + slot * B * F;
+  uint32_t* hy = e->ring_hy + slot * B;
+  for (uint32_t r = 0; r < rows; ++r) {  // gather_batch (model.cpp:12-21) into pinned staging
+    std::memcpy(hx + static_cast<uint64_t>(r) * F, X_host + static_cast<uint64_t>(idx[r]) * F, F * sizeof(float));
+    hy[r] = y_host[idx[r]];
+  }
+  return stream_enqueue(e, hx, hy, rows);
 }
 
 extern "C" int ds_engine_stream_end(ds_engine* e) {

@@ -198,7 +198,7 @@ def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps):
     hp = Hyper(eta=0.05, tau=tau, batch_size=b, i_max=steps)
     master0 = orc.init_params(m, 10)
     outs = []
-    for mode in ("run", "stream"):
+    for mode in ("run", "stream", "stream_rows"):
         e = make_engine(L, m, X, y, m.n_classes, hp, 31, init, 2)
         mh = C.c_void_p()
         L.check(L.lib.ds_master_create(C.byref(mh), 0, P, C.c_float(np.float32(hp.alpha)), L.DS_MODE_LOCKFREE,
@@ -208,6 +208,19 @@ def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps):
             L.check(L.lib.ds_engine_run(e, steps, 0, None))
             L.check(L.lib.ds_engine_sync(e))
             loss = engine_log(L, e, steps)[0]
+        elif mode == "stream_rows":  # the engine gathers the rows itself (ds_engine_stream_push_rows)
+            from paper_1602_08191_b200.deepspark import DeepSpark
+            idx, sizes = DeepSpark().sweep_batches(len(y), b, 31, steps)
+            idx = np.ascontiguousarray(idx, dtype=np.uint32)
+            yh = np.ascontiguousarray(y, dtype=np.uint32)
+            lossbuf = torch.zeros(steps, dtype=torch.float64, pin_memory=True)
+            L.check(L.lib.ds_engine_stream_begin(e, steps, C.c_void_p(lossbuf.data_ptr())))
+            for s in range(steps):
+                L.check(L.lib.ds_engine_stream_push_rows(e, C.c_void_p(X.ctypes.data), C.c_void_p(yh.ctypes.data),
+                                                         C.c_void_p(idx[s].ctypes.data), int(sizes[s])))
+            L.check(L.lib.ds_engine_stream_end(e))
+            loss = lossbuf.numpy().copy()
+            assert np.array_equal(loss, engine_log(L, e, steps)[0])
         else:
             from paper_1602_08191_b200.deepspark import DeepSpark
             idx, sizes = DeepSpark().sweep_batches(len(y), b, 31, steps)
@@ -230,11 +243,12 @@ def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps):
         outs[-1] += (snap,)
         L.lib.ds_engine_destroy(e)
         L.lib.ds_master_destroy(mh)
-    (l0, p0, x0, m0), (l1, p1, x1, m1) = outs
-    assert np.array_equal(l0, l1)
-    assert np.array_equal(x0, x1)
-    assert np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
-    assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
+    (l0, p0, x0, m0) = outs[0]
+    for (l1, p1, x1, m1) in outs[1:]:
+        assert np.array_equal(l0, l1)
+        assert np.array_equal(x0, x1)
+        assert np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
+        assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
 
 
 def test_cluster_split_logits_bit_identical(L, orc, monkeypatch):
