@@ -250,10 +250,69 @@ __device__ void exchange_shard_mlp(float* p, const ShardTable& t, int s, const S
   }
 }
 
+// Unordered (LockFree) exchange of the whole slice in one pass: every element goes to the
+// shard that holds it (no per-shard pass and barrier), so the remote loads of all shards
+// are in flight together.
+__device__ __forceinline__ int shard_of(const ShardTable& t, uint64_t g) {
+  int s = 0;
+  while (s + 1 < t.n && g >= t.begin[s + 1]) ++s;
+  return s;
+}
+
+__device__ void exchange_all_mlp(float* p, const ShardTable& t, const Slice& sl, float a, float* Ws, double* Wd,
+                                 uint32_t F, uint32_t Fd) {
+  const uint64_t lo = sl.lo[0];
+  const uint32_t n = sl.cols[0];  // own W1 rows: Uo * F, one row, 16-byte aligned
+  for (uint32_t j = threadIdx.x * 4; j < n; j += kFT * 4) {
+    const uint64_t g = lo + j;
+    const int s0 = shard_of(t, g), s3 = shard_of(t, g + 3);
+    float wo[4], mo[4];
+    if (s0 == s3 && ((g - t.begin[s0]) & 3) == 0) {
+      float* m = t.ptr[s0] + (g - t.begin[s0]);
+      const float4 wv = *reinterpret_cast<const float4*>(p + g);
+      const float4 mv = __ldcg(reinterpret_cast<const float4*>(m));
+      const float w[4] = {wv.x, wv.y, wv.z, wv.w}, mm[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) elastic_elem(w[q], mm[q], a, wo[q], mo[q]);
+      *reinterpret_cast<float4*>(p + g) = make_float4(wo[0], wo[1], wo[2], wo[3]);
+      __stcg(reinterpret_cast<float4*>(m), make_float4(mo[0], mo[1], mo[2], mo[3]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int sq = shard_of(t, g + q);
+        float* m = t.ptr[sq] + (g + q - t.begin[sq]);
+        elastic_elem(p[g + q], __ldcg(m), a, wo[q], mo[q]);
+        p[g + q] = wo[q];
+        __stcg(m, mo[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t local = j + q, uu = local / F, i = local - uu * F;
+      Ws[local] = wo[q];
+      Wd[uu * Fd + i] = static_cast<double>(wo[q]);
+    }
+  }
+  for (int k = 1; k < sl.n; ++k) {
+    const uint32_t nk = sl.rows[k] * sl.cols[k];
+    for (uint32_t j = threadIdx.x; j < nk; j += kFT) {
+      const uint32_t r = j / sl.cols[k];
+      const uint64_t g = sl.lo[k] + r * sl.row_stride[k] + (j - r * sl.cols[k]);
+      exchange_elem(p, t, shard_of(t, g), g, a);
+    }
+  }
+}
+
 __device__ void do_exchange_mlp(const FusedArgs& A, float* p, const Slice& sl, uint64_t ticket, unsigned int G,
                                 float* Ws, double* Wd, uint32_t F, uint32_t Fd) {
   const ShardTable& t = A.table;
   const bool ordered = ticket != kNoTicket;
+  if (!ordered) {
+    exchange_all_mlp(p, t, sl, A.alpha, Ws, Wd, F, Fd);
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd_system(&t.flags[0]->exchanges, 1ull);
+    return;
+  }
   for (int s = 0; s < t.n; ++s) {
     if (ordered) {
       if (threadIdx.x == 0)
