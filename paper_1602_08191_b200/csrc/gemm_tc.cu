@@ -652,8 +652,13 @@ int launch_3xtf32(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32
 // the tile width (MMA N) with the least padding past N; ties go to the wider tile, which
 // re-reads the A operand fewer times
 uint32_t gemm_pick_bn(uint32_t N) {
-  uint32_t best = 256, waste = (N + 255) / 256 * 256 - N;
-  for (uint32_t bn : {192u, 128u, 96u, 64u, 48u}) {
+  static const uint32_t cap = [] {  // DS_GEMM_MAXBN: cap the tile width (experiments)
+    const char* e = getenv("DS_GEMM_MAXBN");
+    return e ? static_cast<uint32_t>(atoi(e)) : 256u;
+  }();
+  uint32_t best = 0, waste = ~0u;
+  for (uint32_t bn : {256u, 192u, 128u, 96u, 64u, 48u}) {
+    if (bn > cap && bn != 48) continue;
     const uint32_t w = (N + bn - 1) / bn * bn - N;
     if (w < waste) best = bn, waste = w;
   }
