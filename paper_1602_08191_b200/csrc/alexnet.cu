@@ -367,14 +367,22 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restric
   if (p >= R * HoHo) return;
   const uint32_t r = p / HoHo, pix = p - r * HoHo, py = pix / Ho, px = pix - py * Ho;
   const uint32_t hs = py * 2, ws = px * 2, he = min(hs + 3, H), we = min(ws + 3, H);
+  // the window's 9 loads are independent and issued together (clipped taps are predicated
+  // off), then scanned in order: first maximum, strict >
+  const float* base = in + (static_cast<uint64_t>(r * Hi + hs + ipad) * Hi + ws + ipad) * C;
+  const uint32_t nh = he - hs, nw = we - ws, rowC = Hi * C;
   for (uint32_t c = lane; c < C; c += 32) {
-    float best = -INFINITY;
+    float v[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const uint32_t dh = k / 3, dw = k % 3;
+      v[k] = (dh < nh && dw < nw) ? base[dh * rowC + dw * C + c] : -INFINITY;
+    }
+    float best = v[0];
     uint32_t bi = 0;
-    for (uint32_t h = hs; h < he; ++h)
-      for (uint32_t w = ws; w < we; ++w) {
-        const float v = in[(static_cast<uint64_t>(r * Hi + h + ipad) * Hi + w + ipad) * C + c];
-        if (v > best) best = v, bi = (h - hs) * 3 + (w - ws);
-      }
+#pragma unroll
+    for (int k = 1; k < 9; ++k)
+      if (v[k] > best) best = v[k], bi = k;
     const uint64_t o = chw ? (static_cast<uint64_t>(r) * C + c) * HoHo + pix
                            : (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c;
     out[o] = best;
