@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restric
   // off), then scanned in order: first maximum, strict >
   const float* base = in + (static_cast<uint64_t>(r * Hi + hs + ipad) * Hi + ws + ipad) * C;
   const uint32_t nh = he - hs, nw = we - ws, rowC = Hi * C;
+#pragma unroll 4  // several channel groups' window loads in flight per lane
   for (uint32_t c = lane; c < C; c += 32) {
     float v[9];
 #pragma unroll
