@@ -372,7 +372,7 @@ def e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n):
     return {"value": n * B * K / t.item(), "unit": "samples/s", "h2d_bytes_per_step": B * F * 4 + B * 4 + 4,
             "d2h_bytes_per_step": 8, "steps": K, "losses_finite": ok,
             "path": "ds_engine_stream_*: per step ds_engine_stream_push_rows gathers the batch rows from the "
-                    "host shard into a pinned ring slot and copies it H2D into a 4-slot device ring; one "
+                    "host shard into a pinned ring slot and copies it H2D into an 8-slot device ring; one "
                     "persistent fused launch (step + exchange every tau) consumes it and writes each step's "
                     "loss to mapped host memory; wall clock from stream_begin to stream_end"}
 

@@ -317,13 +317,16 @@ int ds_engine_step_host(ds_engine* e, const float* X_host, const uint32_t* y_hos
  * calls later. The host blocks only when it runs two iterations ahead of the device. */
 int ds_engine_step_host_async(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows,
                               double* loss_host);
+/* Depth of the stream-mode ring: the host may run this many pushes ahead of the device. */
+#define DS_STREAM_RING 8
+
 /* Stream mode: ONE persistent launch trains `steps` iterations on batches the host pushes
- * while it runs (a 4-slot device ring; the copy engine lands each batch and then its
+ * while it runs (a DS_STREAM_RING-slot device ring; the copy engine lands each batch and then its
  * sequence word, the kernel waits for the word, frees the slot after its grid barrier).
  * Every batch crosses PCIe as an H2D copy; each step's loss is written by the kernel to
  * *loss_host[step] (pinned, mapped: zero-copy D2H), valid after ds_engine_stream_end.
  * push blocks only while the ring is full. X_host/y_host of push s may be reused at push
- * s+4. Fused one-hidden-layer engine, fixed-period policy. A host that stops pushing for
+ * s+DS_STREAM_RING. Fused one-hidden-layer engine, fixed-period policy. A host that stops pushing for
  * 20 s makes the kernel finish with DS_FLAG_STREAM_TIMEOUT rather than hang. */
 int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss_host);
 int ds_engine_stream_push(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows);

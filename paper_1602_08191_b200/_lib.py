@@ -24,6 +24,7 @@ DS_OK, DS_E_CONTRACT, DS_E_NUMERIC, DS_E_CUDA, DS_E_NOMEM, DS_E_STATE, DS_E_FORM
 DS_MODE_LOCKED, DS_MODE_LOCKFREE = 0, 1
 DS_ENGINE_AUTO, DS_ENGINE_LAYERED, DS_ENGINE_FUSED = 0, 1, 2
 DS_IPC_RECORD_BYTES = 256
+DS_STREAM_RING = 8  # include/ds_cuda.h
 
 FLAG_X_NONFINITE = 1
 FLAG_G_NONFINITE = 2

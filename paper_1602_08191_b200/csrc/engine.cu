@@ -116,7 +116,7 @@ struct ds_engine {
   bool slot_armed[2] = {};
   int slot = 0;
   // stream mode (ds_engine_stream_*): host-fed ring consumed by one persistent launch
-  static constexpr uint32_t kRing = 4;
+  static constexpr uint32_t kRing = DS_STREAM_RING;  // host may run this many steps ahead
   float* ring_X = nullptr;              // [kRing][B][F]
   uint32_t* ring_y = nullptr;           // [kRing][B]
   uint32_t* ring_words = nullptr;       // [kRing] rows, [kRing] ready sequence

@@ -225,11 +225,12 @@ def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps):
             from paper_1602_08191_b200.deepspark import DeepSpark
             idx, sizes = DeepSpark().sweep_batches(len(y), b, 31, steps)
             lossbuf = torch.zeros(steps, dtype=torch.float64, pin_memory=True)
+            ring = L.DS_STREAM_RING  # a pushed buffer may be reused DS_STREAM_RING pushes later
             bufs = [(torch.empty((b, m.n_features), dtype=torch.float32, pin_memory=True),
-                     torch.empty(b, dtype=torch.int32, pin_memory=True)) for _ in range(4)]
+                     torch.empty(b, dtype=torch.int32, pin_memory=True)) for _ in range(ring)]
             L.check(L.lib.ds_engine_stream_begin(e, steps, C.c_void_p(lossbuf.data_ptr())))
             for s in range(steps):
-                xb, yb = bufs[s % 4]
+                xb, yb = bufs[s % ring]
                 r = int(sizes[s])
                 xb.numpy()[:r] = X[idx[s, :r]]
                 yb.numpy().view(np.uint32)[:r] = y[idx[s, :r]]
