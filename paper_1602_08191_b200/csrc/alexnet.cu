@@ -328,16 +328,19 @@ __global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __
       const int c = static_cast<int>(c0) - 4 + j;
       xv[j] = (c >= 0 && c < static_cast<int>(C)) ? __ldg(px + c) : 0.f;
     }
+    float sq[12];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) sq[j] = xv[j] * xv[j];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int c = static_cast<int>(c0) - 2 + j;
-      const float ss = xv[j] * xv[j] + xv[j + 1] * xv[j + 1] + xv[j + 2] * xv[j + 2] + xv[j + 3] * xv[j + 3] +
-                       xv[j + 4] * xv[j + 4];
+      const float ss = ((sq[j] + sq[j + 1]) + (sq[j + 2] + sq[j + 3])) + sq[j + 4];
       const float sc = kLrnK + kLrnAlpha / kLrnN * ss;
-      const float sb = __powf(sc, -kLrnBeta);
+      const float l2 = __log2f(sc);  // s^-b and s^(-b-1) from one logarithm
+      const float sb = exp2f(-kLrnBeta * l2);
       pw[j] = sb;
       const float d = (c >= 0 && c < static_cast<int>(C)) ? __ldg(pd + c) : 0.f;
-      w[j] = d * xv[j + 2] * sb * __frcp_rn(sc);
+      w[j] = d * xv[j + 2] * exp2f(-(kLrnBeta + 1.f) * l2);
     }
     float o[4];
 #pragma unroll
