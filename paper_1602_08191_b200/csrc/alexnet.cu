@@ -412,26 +412,34 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const float* __restric
   const uint32_t px0 = x >= 2 ? (x - 1) / 2 : 0, px1 = min(x / 2, Ho - 1);
   const uint64_t dbase = (static_cast<uint64_t>(r * Hi + y + ipad) * Hi + x + ipad) * C;
   // up to 2 x 2 windows cover (y, x); their argmax bytes and gradients are loaded
-  // independently (no load waits on a comparison), then the matches are summed in window order
+  // independently (no load waits on a comparison), then the matches are summed in window
+  // order. Window offsets and expected argmax positions are channel-independent: hoisted.
   const bool two_y = py1 > py0, two_x = px1 > px0;
+  uint64_t aoff[4], doff[4];
+  uint32_t want[4];
+  bool ok[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t py = py0 + (w >> 1), px = px0 + (w & 1);
+    ok[w] = ((w >> 1) == 0 || two_y) && ((w & 1) == 0 || two_x);
+    aoff[w] = (static_cast<uint64_t>(r * Ho + py) * Ho + px) * C;
+    doff[w] = chw ? static_cast<uint64_t>(r) * C * Ho * Ho + py * Ho + px
+                  : (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C;
+    want[w] = (y - py * 2) * 3 + (x - px * 2);
+  }
+  const uint64_t dstride = chw ? static_cast<uint64_t>(Ho) * Ho : 1;  // channel step in dout
   for (uint32_t c = lane; c < C; c += 32) {
     uint32_t av[4];
     float dv[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      const uint32_t py = py0 + (w >> 1), px = px0 + (w & 1);
-      const bool ok = ((w >> 1) == 0 || two_y) && ((w & 1) == 0 || two_x);
-      av[w] = ok ? arg[((r * Ho + py) * Ho + px) * C + c] : 255u;
-      dv[w] = ok ? dout[chw ? (static_cast<uint64_t>(r) * C + c) * Ho * Ho + py * Ho + px
-                            : (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c]
-                 : 0.f;
+      av[w] = ok[w] ? arg[aoff[w] + c] : 255u;
+      dv[w] = ok[w] ? dout[doff[w] + c * dstride] : 0.f;
     }
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const uint32_t py = py0 + (w >> 1), px = px0 + (w & 1);
-      if (av[w] == (y - py * 2) * 3 + (x - px * 2)) s += dv[w];
-    }
+    for (int w = 0; w < 4; ++w)
+      if (av[w] == want[w]) s += dv[w];
     if (mask && !(mask[dbase + c] > 0.f)) s = 0.f;
     din[dbase + c] = s;
   }
