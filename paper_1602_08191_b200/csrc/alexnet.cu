@@ -415,26 +415,27 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const float* __restric
   // independently (no load waits on a comparison), then the matches are summed in window
   // order. Window offsets and expected argmax positions are channel-independent: hoisted.
   const bool two_y = py1 > py0, two_x = px1 > px0;
-  uint64_t aoff[4], doff[4];
+  // 32-bit offsets: the pooled maps hold < 2^32 elements (the caller bounds the batch)
+  const uint8_t* ap[4];
+  const float* dp[4];
   uint32_t want[4];
   bool ok[4];
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     const uint32_t py = py0 + (w >> 1), px = px0 + (w & 1);
     ok[w] = ((w >> 1) == 0 || two_y) && ((w & 1) == 0 || two_x);
-    aoff[w] = (static_cast<uint64_t>(r * Ho + py) * Ho + px) * C;
-    doff[w] = chw ? static_cast<uint64_t>(r) * C * Ho * Ho + py * Ho + px
-                  : (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C;
+    ap[w] = arg + ((r * Ho + py) * Ho + px) * C;
+    dp[w] = dout + (chw ? r * C * Ho * Ho + py * Ho + px : ((r * Hq + py + opad) * Hq + px + opad) * C);
     want[w] = (y - py * 2) * 3 + (x - px * 2);
   }
-  const uint64_t dstride = chw ? static_cast<uint64_t>(Ho) * Ho : 1;  // channel step in dout
+  const uint32_t dstride = chw ? Ho * Ho : 1;  // channel step in dout
   for (uint32_t c = lane; c < C; c += 32) {
     uint32_t av[4];
     float dv[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      av[w] = ok[w] ? arg[aoff[w] + c] : 255u;
-      dv[w] = ok[w] ? dout[doff[w] + c * dstride] : 0.f;
+      av[w] = ok[w] ? ap[w][c] : 255u;
+      dv[w] = ok[w] ? dp[w][c * dstride] : 0.f;
     }
     float s = 0.f;
 #pragma unroll
