@@ -293,7 +293,7 @@ __global__ void lrn_fwd_kernel(const float* __restrict__ x, uint32_t pixels, uin
   const uint32_t C4 = C / 4, total = pixels * C4;
   for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
     const uint32_t p = i / C4, c0 = (i - p * C4) * 4;
-    const float* px = x + static_cast<uint64_t>(p) * C;
+    const float* px = x + p * C;  // 32-bit: pixels * C < 2^32 (the caller bounds the batch)
     float v[8];  // x[c0-2 .. c0+5]
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -306,7 +306,7 @@ __global__ void lrn_fwd_kernel(const float* __restrict__ x, uint32_t pixels, uin
       const float ss = v[j] * v[j] + v[j + 1] * v[j + 1] + v[j + 2] * v[j + 2] + v[j + 3] * v[j + 3] + v[j + 4] * v[j + 4];
       o[j] = v[j + 2] * __powf(kLrnK + kLrnAlpha / kLrnN * ss, -kLrnBeta);
     }
-    *reinterpret_cast<float4*>(y + static_cast<uint64_t>(p) * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(y + p * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
