@@ -524,6 +524,23 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, uint32_t npa
   }
 }
 
+// Zero the border of a padded NHWC map [R][Hp][Hp][C] (everything outside rows and columns
+// [pad, pad + H)); the interior is rewritten every step, so only the border needs clearing.
+// One block per (image, row); interior rows clear only their 2 * pad... edge pixels.
+__global__ void zero_border_kernel(float* __restrict__ map, uint32_t Hp, uint32_t pad, uint32_t H, uint32_t C,
+                                   const uint32_t* gate) {
+  GATE;
+  const uint32_t r = blockIdx.x / Hp, yp = blockIdx.x - r * Hp;
+  float* row = map + (static_cast<uint64_t>(r) * Hp + yp) * Hp * C;
+  const bool full = yp < pad || yp >= pad + H;
+  const uint32_t n = full ? Hp * C : (Hp - H) * C;  // the row, or its left + right edges
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    uint32_t e = i;
+    if (!full && e >= pad * C) e += H * C;  // skip the interior columns
+    row[e] = 0.f;
+  }
+}
+
 // argmax of the logits (first maximum), hits against labels (predict, model.cpp:303-318)
 __global__ void alex_hits_kernel(const float* __restrict__ z, uint32_t ldz, const uint32_t* __restrict__ y, uint32_t R,
                                  uint32_t C, uint32_t* pred, unsigned long long* hits) {
@@ -652,6 +669,14 @@ int zero(const Ctx& c, float* p, uint64_t floats) {
   return DS_OK;
 }
 
+// clear only the border of a padded map (the interior is fully rewritten before it is read)
+int zero_border(const Ctx& c, float* p, uint32_t R, uint32_t Hp, uint32_t pad, uint32_t H, uint32_t C) {
+  zero_border_kernel<<<R * Hp, 256, 0, c.s>>>(p, Hp, pad, H, C, c.gate);
+  ++t_launches;
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
 // pixel shift of tap (ky, kx) on the padded grid of side Hp
 int32_t shift(const ConvSpec& cs, uint32_t t) {
   return (static_cast<int32_t>(t / cs.K) - static_cast<int32_t>(cs.pad)) * static_cast<int32_t>(cs.Hp) +
@@ -766,11 +791,11 @@ int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint3
     KDONE(1);
   }
   // padded maps: zero borders (interiors are rewritten below)
-  DS_TRY(zero(c, w.p1p, G2 * 96));
-  DS_TRY(zero(c, w.p2p, G3 * 256));
-  DS_TRY(zero(c, w.a3p, G3 * 384));
-  DS_TRY(zero(c, w.a4p, G3 * 384));
-  DS_TRY(zero(c, w.a5p, G3 * 256));
+  DS_TRY(zero_border(c, w.p1p, R, sh.Hp2, 2, sh.P1, 96));
+  DS_TRY(zero_border(c, w.p2p, R, sh.Hp3, 1, sh.P2, 256));
+  DS_TRY(zero_border(c, w.a3p, R, sh.Hp3, 1, sh.P2, 384));
+  DS_TRY(zero_border(c, w.a4p, R, sh.Hp3, 1, sh.P2, 384));
+  DS_TRY(zero_border(c, w.a5p, R, sh.Hp3, 1, sh.P2, 256));
   // conv1 (space-to-depth, 3x3 taps) + relu, LRN1, pool1 -> p1p (pad 2)
   s2d_kernel<<<nblk(1ull * R * sh.Hs * sh.Hs * 48), 256, 0, s>>>(X, idx, F, sh.S, R, sh.Hs, w.xs, gate);
   KDONE(1);
@@ -871,11 +896,11 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   DS_TRY(gemm(c, w.dh6, 4096, w.w6T, 4096, w.dp5, sh.q5, R, static_cast<uint32_t>(sh.q5), 4096, 1.f, nullptr, false));
 
   // ---- conv5 .. conv2 on the padded grids ------------------------------------------------
-  DS_TRY(zero(c, w.dc5p, G3 * 256));
-  DS_TRY(zero(c, w.dc4p, G3 * 384));
-  DS_TRY(zero(c, w.dc3p, G3 * 384));
-  DS_TRY(zero(c, w.dc2p, G2 * 256));
-  DS_TRY(zero(c, w.dc1p, 1ull * R * sh.Hs * sh.Hs * 96));
+  DS_TRY(zero_border(c, w.dc5p, R, sh.Hp3, 1, sh.P2, 256));
+  DS_TRY(zero_border(c, w.dc4p, R, sh.Hp3, 1, sh.P2, 384));
+  DS_TRY(zero_border(c, w.dc3p, R, sh.Hp3, 1, sh.P2, 384));
+  DS_TRY(zero_border(c, w.dc2p, R, sh.Hp2, 2, sh.P1, 256));
+  DS_TRY(zero_border(c, w.dc1p, R, sh.Hs, 1, sh.H1, 96));
   // pool5 backward (per-row CHW pooled map) with the ReLU5 mask (a5p) -> dc5p
   maxpool_bwd_kernel<<<static_cast<unsigned>((M3 + 7) / 8), 256, 0, s>>>(w.dp5, w.arg5, R, sh.P2, 256, sh.P5, 0, 1, 1, w.a5p,
                                                                 w.dc5p, gate);
@@ -901,7 +926,7 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     if (l >= 2) {  // into relu(conv3 / conv4): masked, same padded grid
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], dout_maps[l - 1], true, in_maps[l]));
     } else if (l == 1) {  // into pool2(LRN2(relu(conv2))): d(p2p), pool2 bwd, LRN2 bwd -> dc2p
-      DS_TRY(zero(c, w.dp2p, G3 * 256));
+      DS_TRY(zero_border(c, w.dp2p, R, sh.Hp3, 1, sh.P2, 256));
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp2p, true, nullptr));
       maxpool_bwd_kernel<<<static_cast<unsigned>((M2 + 7) / 8), 256, 0, s>>>(w.dp2p, w.arg2, R, sh.P1, 256, sh.P2, 1, 0, 0,
                                                                     nullptr, w.dn2, gate);
