@@ -222,6 +222,54 @@ __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict_
   }
 }
 
+// transpose_kernel fused with the first pass of colsum (the bias gradient) over the same
+// matrix: block (x, y) walks row tiles x, x + gridDim.x, ... of column tile y, so the
+// gradient map is read once for both; part[x][n] = sum of column n over the block's rows
+// (zero-filled beyond `rows`), reduced by colsum_final_kernel.
+__global__ void __launch_bounds__(256) transpose_colsum_kernel(const float* __restrict__ in, uint64_t rows,
+                                                               uint32_t cols, float* __restrict__ out,
+                                                               uint64_t ld_out, float* __restrict__ part,
+                                                               const uint32_t* gate) {
+  GATE;
+  __shared__ float tile[32][33];
+  const uint32_t c0 = blockIdx.y * 32;
+  const uint32_t t = threadIdx.x, lr = t / 8, lc = (t % 8) * 4;
+  const uint32_t sc = t / 8, sr = (t % 8) * 4;
+  const uint32_t c = c0 + lc, oc = c0 + sc;
+  const bool vin = (cols % 4) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  const bool vout = (ld_out % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  float acc = 0.f;
+  for (uint64_t r0 = blockIdx.x * 32ull; r0 < rows; r0 += gridDim.x * 32ull) {
+    const uint64_t r = r0 + lr;
+    if (vin && r < rows && c + 3 < cols) {
+      const float4 v = *reinterpret_cast<const float4*>(in + r * cols + c);
+      tile[lr][lc] = v.x, tile[lr][lc + 1] = v.y, tile[lr][lc + 2] = v.z, tile[lr][lc + 3] = v.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tile[lr][lc + j] = (r < rows && c + j < cols) ? in[r * cols + c + j] : 0.f;
+    }
+    __syncthreads();
+    const float a = tile[sr][sc], b = tile[sr + 1][sc], d = tile[sr + 2][sc], e = tile[sr + 3][sc];
+    acc += (a + b) + (d + e);
+    const uint64_t orr = r0 + sr;
+    if (oc < cols) {
+      if (vout && orr + 3 < rows) {
+        *reinterpret_cast<float4*>(out + oc * ld_out + orr) = make_float4(a, b, d, e);
+      } else {
+        const float q[4] = {a, b, d, e};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (orr + j < rows) out[oc * ld_out + orr + j] = q[j];
+      }
+    }
+    __syncthreads();
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  if ((t % 8) == 0 && oc < cols) part[1ull * blockIdx.x * cols + oc] = acc;
+}
+
 // Four pixel-shifted transposed copies: out[s][c][m] = in[m - s][c] (0 outside the rows),
 // m < ldT. TMA needs 16-byte aligned inner coordinates, so a weight-gradient tap with pixel
 // shift d reads copy s = (-d mod 4) at the aligned offset d + s: the shifted column is never
@@ -664,6 +712,24 @@ int colsum(const Ctx& c, const float* d, uint64_t rows, uint32_t N, uint64_t ld,
   return DS_OK;
 }
 
+// transpose (out[c][r] = in[r][c], ld_in = cols) and the bias gradient
+// bias[n] = scale * sum_r in[r][n] from one read of `in`
+int transpose_colsum(const Ctx& c, const float* in, uint64_t rows, uint32_t cols, float* out, uint64_t ld_out,
+                     float scale, float* bias, float* bpart) {
+  const cudaStream_t s_ = c.s;
+  const uint32_t ntile = (cols + 31) / 32;
+  uint64_t gx = std::max<uint32_t>(1, 1184 / ntile);  // ~8 resident blocks per SM
+  gx = std::min<uint64_t>(gx, (rows + 31) / 32);
+  gx = std::min<uint64_t>(gx, (4096ull * 512ull) / cols);
+  transpose_colsum_kernel<<<dim3(static_cast<unsigned>(gx), ntile), 256, 0, c.s>>>(in, rows, cols, out, ld_out, bpart,
+                                                                                    c.gate);
+  colsum_final_kernel<<<(cols + 7) / 8, 256, 0, c.s>>>(bpart, static_cast<uint32_t>(gx), cols, scale, bias, c.flags,
+                                                       c.gate);
+  KDONE(2);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
 int zero(const Ctx& c, float* p, uint64_t floats) {
   DS_CUDA_TRY(cudaMemsetAsync(p, 0, floats * 4, c.s));
   return DS_OK;
@@ -914,8 +980,7 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     // side stream: bias gradient (border rows are zero) and the weight gradient from
     // pixel-contiguous copies, beside the main stream's data gradient of the same layer
     DS_TRY(edge(s, c2.s, sd->ev[2 + l]));
-    DS_TRY(colsum(c2, dout, G, cs.Cout, cs.Cout, inv_b, grad + L[l + 1].b_off, w.bpart));
-    DS_TRY(transpose(c2, dout, G, cs.Cout, cs.Cout, w.trA, ldT));
+    DS_TRY(transpose_colsum(c2, dout, G, cs.Cout, w.trA, ldT, inv_b, grad + L[l + 1].b_off, w.bpart));
     {
       dim3 grid(static_cast<unsigned>((ldT + 31) / 32), (cs.Cin + 31) / 32);
       transpose_shift4_kernel<<<grid, 256, 0, c2.s>>>(in_maps[l], G, cs.Cin, w.trB, ldT, gate);
@@ -945,8 +1010,7 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     const ConvSpec cs = conv1_spec(sh);
     const uint64_t G1 = 1ull * R * sh.Hs * sh.Hs, ldT = up4(static_cast<uint32_t>(G1 + 3));
     DS_TRY(edge(s, c2.s, sd->ev[6]));
-    DS_TRY(colsum(c2, w.dc1p, G1, 96, 96, inv_b, grad + L[0].b_off, w.bpart));
-    DS_TRY(transpose(c2, w.dc1p, G1, 96, 96, w.trA, ldT));
+    DS_TRY(transpose_colsum(c2, w.dc1p, G1, 96, w.trA, ldT, inv_b, grad + L[0].b_off, w.bpart));
     dim3 grid(static_cast<unsigned>((ldT + 31) / 32), (48 + 31) / 32);
     transpose_shift4_kernel<<<grid, 256, 0, c2.s>>>(w.xs, G1, 48, w.trB, ldT, gate);
     KDONE(1);
