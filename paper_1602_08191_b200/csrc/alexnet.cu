@@ -422,23 +422,33 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restric
   // off), then scanned in order: first maximum, strict >
   const float* base = in + (static_cast<uint64_t>(r * Hi + hs + ipad) * Hi + ws + ipad) * C;
   const uint32_t nh = he - hs, nw = we - ws, rowC = Hi * C;
-#pragma unroll 4  // several channel groups' window loads in flight per lane
-  for (uint32_t c = lane; c < C; c += 32) {
-    float v[9];
+  // four channels per lane (C % 4 == 0 at every call site: 96, 256): float4 window loads,
+  // uchar4 argmax stores, float4 output stores (scalar into the CHW planes of pool5)
+#pragma unroll 2  // two channel groups' window loads in flight per lane
+  for (uint32_t c = lane * 4; c < C; c += 128) {
+    float4 v[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
       const uint32_t dh = k / 3, dw = k % 3;
-      v[k] = (dh < nh && dw < nw) ? base[dh * rowC + dw * C + c] : -INFINITY;
+      v[k] = (dh < nh && dw < nw) ? *reinterpret_cast<const float4*>(base + dh * rowC + dw * C + c)
+                                  : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     }
-    float best = v[0];
-    uint32_t bi = 0;
+    float4 best = v[0];
+    uchar4 bi = make_uchar4(0, 0, 0, 0);
 #pragma unroll
-    for (int k = 1; k < 9; ++k)
-      if (v[k] > best) best = v[k], bi = k;
-    const uint64_t o = chw ? (static_cast<uint64_t>(r) * C + c) * HoHo + pix
-                           : (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c;
-    out[o] = best;
-    arg[static_cast<uint64_t>(p) * C + c] = static_cast<uint8_t>(bi);
+    for (int k = 1; k < 9; ++k) {
+      if (v[k].x > best.x) best.x = v[k].x, bi.x = k;
+      if (v[k].y > best.y) best.y = v[k].y, bi.y = k;
+      if (v[k].z > best.z) best.z = v[k].z, bi.z = k;
+      if (v[k].w > best.w) best.w = v[k].w, bi.w = k;
+    }
+    if (chw) {
+      const uint64_t o = (static_cast<uint64_t>(r) * C + c) * HoHo + pix;
+      out[o] = best.x, out[o + HoHo] = best.y, out[o + 2 * HoHo] = best.z, out[o + 3 * HoHo] = best.w;
+    } else {
+      *reinterpret_cast<float4*>(out + (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c) = best;
+    }
+    *reinterpret_cast<uchar4*>(arg + static_cast<uint64_t>(p) * C + c) = bi;
   }
 }
 
@@ -476,21 +486,40 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const float* __restric
     dp[w] = dout + (chw ? r * C * Ho * Ho + py * Ho + px : ((r * Hq + py + opad) * Hq + px + opad) * C);
     want[w] = (y - py * 2) * 3 + (x - px * 2);
   }
+  // four channels per lane (C % 4 == 0 at every call site: 96, 256): uchar4 argmax loads,
+  // float4 gradient loads (scalar across the CHW planes of pool5) and float4 stores; the
+  // per-channel window order of the sum is unchanged
   const uint32_t dstride = chw ? Ho * Ho : 1;  // channel step in dout
-  for (uint32_t c = lane; c < C; c += 32) {
-    uint32_t av[4];
-    float dv[4];
+  for (uint32_t c = lane * 4; c < C; c += 128) {
+    uchar4 av[4];
+    float4 dv[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      av[w] = ok[w] ? ap[w][c] : 255u;
-      dv[w] = ok[w] ? dp[w][c * dstride] : 0.f;
+      av[w] = ok[w] ? *reinterpret_cast<const uchar4*>(ap[w] + c) : make_uchar4(255, 255, 255, 255);
+      if (!ok[w])
+        dv[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+      else if (chw)
+        dv[w] = make_float4(dp[w][c * dstride], dp[w][(c + 1) * dstride], dp[w][(c + 2) * dstride],
+                            dp[w][(c + 3) * dstride]);
+      else
+        dv[w] = *reinterpret_cast<const float4*>(dp[w] + c);
     }
-    float s = 0.f;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int w = 0; w < 4; ++w)
-      if (av[w] == want[w]) s += dv[w];
-    if (mask && !(mask[dbase + c] > 0.f)) s = 0.f;
-    din[dbase + c] = s;
+    for (int w = 0; w < 4; ++w) {
+      if (av[w].x == want[w]) s.x += dv[w].x;
+      if (av[w].y == want[w]) s.y += dv[w].y;
+      if (av[w].z == want[w]) s.z += dv[w].z;
+      if (av[w].w == want[w]) s.w += dv[w].w;
+    }
+    if (mask) {
+      const float4 mk = *reinterpret_cast<const float4*>(mask + dbase + c);
+      if (!(mk.x > 0.f)) s.x = 0.f;
+      if (!(mk.y > 0.f)) s.y = 0.f;
+      if (!(mk.z > 0.f)) s.z = 0.f;
+      if (!(mk.w > 0.f)) s.w = 0.f;
+    }
+    *reinterpret_cast<float4*>(din + dbase + c) = s;
   }
 }
 
