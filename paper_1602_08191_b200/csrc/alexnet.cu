@@ -523,6 +523,97 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const float* __restric
   }
 }
 
+// max-pool backward and LRN backward (ReLU-masked) fused, one warp per pixel of the LRN
+// input map x (unpadded [R][H][H][C], C % 4 == 0, C <= 256): the warp gathers the pooled
+// gradient of every channel of its pixel (maxpool_bwd_kernel's window order) into shared
+// memory, then applies lrn_bwd_relu_kernel's formula across the channel window from there,
+// so the LRN output gradient never round-trips through HBM. Results are bit-identical to
+// the two-kernel sequence. dout: pooled gradient padded by opad; dx written at pixel
+// (y + xpad, x + xpad) of a map of side Hx.
+__global__ void __launch_bounds__(256) pool_lrn_bwd_relu_kernel(const float* __restrict__ dout,
+                                                                const uint8_t* __restrict__ arg,
+                                                                const float* __restrict__ x, uint32_t R, uint32_t H,
+                                                                uint32_t C, uint32_t Ho, uint32_t opad, uint32_t xpad,
+                                                                uint32_t Hx, float* __restrict__ dx,
+                                                                const uint32_t* gate) {
+  GATE;
+  __shared__ float4 dys[8][66];  // per warp: channels -4 .. C + 3 (zero outside 0 .. C-1)
+  const uint32_t HH = H * H, Hq = Ho + 2 * opad, warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t p = blockIdx.x * 8 + warp;
+  if (p >= R * HH) return;
+  const uint32_t r = p / HH, pix = p - r * HH, y = pix / H, xx = pix - y * H;
+  const uint32_t py0 = y >= 2 ? (y - 1) / 2 : 0, py1 = min(y / 2, Ho - 1);
+  const uint32_t px0 = xx >= 2 ? (xx - 1) / 2 : 0, px1 = min(xx / 2, Ho - 1);
+  const bool two_y = py1 > py0, two_x = px1 > px0;
+  const uint8_t* ap[4];
+  const float* dp[4];
+  uint32_t want[4];
+  bool ok[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t py = py0 + (w >> 1), px = px0 + (w & 1);
+    ok[w] = ((w >> 1) == 0 || two_y) && ((w & 1) == 0 || two_x);
+    ap[w] = arg + ((r * Ho + py) * Ho + px) * C;
+    dp[w] = dout + ((r * Hq + py + opad) * Hq + px + opad) * C;
+    want[w] = (y - py * 2) * 3 + (xx - px * 2);
+  }
+  const uint32_t C4 = C / 4;
+  if (lane == 0) dys[warp][0] = make_float4(0.f, 0.f, 0.f, 0.f), dys[warp][C4 + 1] = dys[warp][0];
+  for (uint32_t q = lane; q < C4; q += 32) {
+    const uint32_t c = q * 4;
+    uchar4 av[4];
+    float4 dv[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      av[w] = ok[w] ? *reinterpret_cast<const uchar4*>(ap[w] + c) : make_uchar4(255, 255, 255, 255);
+      dv[w] = ok[w] ? *reinterpret_cast<const float4*>(dp[w] + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      if (av[w].x == want[w]) sum.x += dv[w].x;
+      if (av[w].y == want[w]) sum.y += dv[w].y;
+      if (av[w].z == want[w]) sum.z += dv[w].z;
+      if (av[w].w == want[w]) sum.w += dv[w].w;
+    }
+    dys[warp][q + 1] = sum;
+  }
+  __syncwarp();
+  const float* ds = reinterpret_cast<const float*>(&dys[warp][1]);  // ds[c], c in [-4, C + 4)
+  const float* px = x + static_cast<uint64_t>(p) * C;
+  for (uint32_t q = lane; q < C4; q += 32) {
+    const uint32_t c0 = q * 4;
+    float xv[12], w[8], pw[8];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      const int c = static_cast<int>(c0) - 4 + j;
+      xv[j] = (c >= 0 && c < static_cast<int>(C)) ? __ldg(px + c) : 0.f;
+    }
+    float sq[12];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) sq[j] = xv[j] * xv[j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = static_cast<int>(c0) - 2 + j;
+      const float ss = ((sq[j] + sq[j + 1]) + (sq[j + 2] + sq[j + 3])) + sq[j + 4];
+      const float sc = kLrnK + kLrnAlpha / kLrnN * ss;
+      const float l2 = __log2f(sc);
+      pw[j] = exp2f(-kLrnBeta * l2);
+      w[j] = ds[c] * xv[j + 2] * exp2f(-(kLrnBeta + 1.f) * l2);
+    }
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float xc = xv[j + 4];
+      const float acc = w[j] + w[j + 1] + w[j + 2] + w[j + 3] + w[j + 4];
+      const float d = ds[c0 + j];
+      o[j] = xc > 0.f ? d * pw[j + 2] - 2.f * kLrnAlpha * kLrnBeta / kLrnN * xc * acc : 0.f;
+    }
+    *reinterpret_cast<float4*>(dx + (static_cast<uint64_t>(r * Hx + y + xpad) * Hx + xx + xpad) * C + c0) =
+        make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // softmax cross-entropy, one warp per row: loss_rows[r], dz[r][c] = softmax - onehot
 // (f64 log-sum-exp as the reference's sample_loss_grad, model.cpp:205-214)
 __global__ void softmax_ce_warp_kernel(const float* __restrict__ z, uint32_t ldz, const uint32_t* __restrict__ y,
@@ -1022,16 +1113,14 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     } else if (l == 1) {  // into pool2(LRN2(relu(conv2))): d(p2p), pool2 bwd, LRN2 bwd -> dc2p
       DS_TRY(zero_border(c, w.dp2p, R, sh.Hp3, 1, sh.P2, 256));
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp2p, true, nullptr));
-      maxpool_bwd_kernel<<<static_cast<unsigned>((M2 + 7) / 8), 256, 0, s>>>(w.dp2p, w.arg2, R, sh.P1, 256, sh.P2, 1, 0, 0,
-                                                                    nullptr, w.dn2, gate);
-      lrn_bwd_relu_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, w.dn2, R, sh.P1, 256, 2, sh.Hp2, w.dc2p, gate);
-      KDONE(2);
+      pool_lrn_bwd_relu_kernel<<<static_cast<unsigned>((M2 + 7) / 8), 256, 0, s>>>(w.dp2p, w.arg2, w.a2, R, sh.P1, 256,
+                                                                             sh.P2, 1, 2, sh.Hp2, w.dc2p, gate);
+      KDONE(1);
     } else {  // into pool1(LRN1(relu(conv1))): d(p1) unpadded, pool1 bwd, LRN1 bwd -> dc1p
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp1, false, nullptr));
-      maxpool_bwd_kernel<<<static_cast<unsigned>((M1 + 7) / 8), 256, 0, s>>>(w.dp1, w.arg1, R, sh.H1, 96, sh.P1, 0, 0, 0, nullptr,
-                                                                  w.dn1, gate);
-      lrn_bwd_relu_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, w.dn1, R, sh.H1, 96, 1, sh.Hs, w.dc1p, gate);
-      KDONE(2);
+      pool_lrn_bwd_relu_kernel<<<static_cast<unsigned>((M1 + 7) / 8), 256, 0, s>>>(w.dp1, w.arg1, w.a1, R, sh.H1, 96,
+                                                                             sh.P1, 0, 1, sh.Hs, w.dc1p, gate);
+      KDONE(1);
     }
   }
   // ---- conv1: bias and weight gradients on the space-to-depth grid (no data gradient) ------
