@@ -90,7 +90,7 @@ struct AlexWs {
   float *a1, *n1, *p1p, *a2, *n2, *p2p, *a3p, *a4p, *a5p, *p5, *h6, *h7, *z, *dz;
   uint8_t *arg1, *arg2, *arg5;
   // backward
-  float *dh7, *dh6, *dp5, *dc5p, *dc4p, *dc3p, *dp2p, *dn2, *dc2p, *dp1, *dn1, *dc1p;
+  float *dh7, *dh6, *dp5, *dc5p, *dc4p, *dc3p, *dp2p, *dc2p, *dp1, *dc1p;
   float *xs, *trA, *trB, *part, *part2, *wtmp, *bpart;
   float *w1p, *wp[4], *wpT[4], *w6T, *w7T, *w8T, *zT, *h7T, *h6T, *p5T, *dh7T, *dh6T;
   double* loss_rows;
@@ -116,8 +116,8 @@ AlexWs carve_ws(const ModelInfo& m, uint32_t R, void* base) {
   f(ws.a3p, G3 * 384), f(ws.a4p, G3 * 384), f(ws.a5p, G3 * 256), f(ws.p5, Q5), u(ws.arg5, Q5);
   f(ws.h6, 4096ull * R), f(ws.h7, 4096ull * R), f(ws.z, 1ull * s.Cp * R), f(ws.dz, 1ull * s.Cp * R);
   f(ws.dh7, 4096ull * R), f(ws.dh6, 4096ull * R), f(ws.dp5, Q5);
-  f(ws.dc5p, G3 * 256), f(ws.dc4p, G3 * 384), f(ws.dc3p, G3 * 384), f(ws.dp2p, G3 * 256), f(ws.dn2, M2 * 256);
-  f(ws.dc2p, G2 * 256), f(ws.dp1, M2 * 96), f(ws.dn1, M1 * 96), f(ws.dc1p, G1 * 96);
+  f(ws.dc5p, G3 * 256), f(ws.dc4p, G3 * 384), f(ws.dc3p, G3 * 384), f(ws.dp2p, G3 * 256);
+  f(ws.dc2p, G2 * 256), f(ws.dp1, M2 * 96), f(ws.dc1p, G1 * 96);
   f(ws.xs, G1 * 48);
   const uint64_t trA = std::max({384 * (G3 + 8), 256 * (G2 + 8), 96 * (G1 + 8)});
   const uint64_t trB = 4 * std::max({384 * (G3 + 8), 96 * (G2 + 8), 48 * (G1 + 8)});
@@ -358,52 +358,6 @@ __global__ void lrn_fwd_kernel(const float* __restrict__ x, uint32_t pixels, uin
   }
 }
 
-// LRN backward (scale recomputed from x), masked by the ReLU that produced x (x > 0):
-// dx_c = dy_c s_c^-b - (2 a b / n) x_c sum_{|j-c|<=2} dy_j x_j s_j^(-b-1)
-// dx is written at pixel (y + opad, x + opad) of a map of side Ho.
-__global__ void lrn_bwd_relu_kernel(const float* __restrict__ x, const float* __restrict__ dy, uint32_t R, uint32_t H,
-                                    uint32_t C, uint32_t opad, uint32_t Ho, float* __restrict__ dx,
-                                    const uint32_t* gate) {
-  GATE;
-  const uint32_t C4 = C / 4, HH = H * H, total = R * HH * C4;
-  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
-    const uint32_t p = i / C4, c0 = (i - p * C4) * 4;
-    const float* px = x + static_cast<uint64_t>(p) * C;
-    const float* pd = dy + static_cast<uint64_t>(p) * C;
-    float xv[12], w[8], pw[8];  // x[c0-4 .. c0+7]; per j in [c0-2, c0+5]: dy x s^(-b-1), s^-b
-#pragma unroll
-    for (int j = 0; j < 12; ++j) {
-      const int c = static_cast<int>(c0) - 4 + j;
-      xv[j] = (c >= 0 && c < static_cast<int>(C)) ? __ldg(px + c) : 0.f;
-    }
-    float sq[12];
-#pragma unroll
-    for (int j = 0; j < 12; ++j) sq[j] = xv[j] * xv[j];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = static_cast<int>(c0) - 2 + j;
-      const float ss = ((sq[j] + sq[j + 1]) + (sq[j + 2] + sq[j + 3])) + sq[j + 4];
-      const float sc = kLrnK + kLrnAlpha / kLrnN * ss;
-      const float l2 = __log2f(sc);  // s^-b and s^(-b-1) from one logarithm
-      const float sb = exp2f(-kLrnBeta * l2);
-      pw[j] = sb;
-      const float d = (c >= 0 && c < static_cast<int>(C)) ? __ldg(pd + c) : 0.f;
-      w[j] = d * xv[j + 2] * exp2f(-(kLrnBeta + 1.f) * l2);
-    }
-    float o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float xc = xv[j + 4];
-      const float acc = w[j] + w[j + 1] + w[j + 2] + w[j + 3] + w[j + 4];
-      const float d = __ldg(pd + c0 + j);
-      o[j] = xc > 0.f ? d * pw[j + 2] - 2.f * kLrnAlpha * kLrnBeta / kLrnN * xc * acc : 0.f;
-    }
-    const uint32_t r = p / HH, pix = p - r * HH, yy = pix / H, xx = pix - yy * H;
-    *reinterpret_cast<float4*>(dx + (static_cast<uint64_t>(r * Ho + yy + opad) * Ho + xx + opad) * C + c0) =
-        make_float4(o[0], o[1], o[2], o[3]);
-  }
-}
-
 // MAX 3x3/2 ceil-mode over an NHWC map (input padded by ipad, output padded by opad, or
 // per-row CHW when chw != 0: the fc6 input). arg[r][py][px][c] (unpadded) = window position
 // (0..8) of the first maximum in scan order. One warp per pooled pixel (8 per block),
@@ -526,9 +480,10 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const float* __restric
 // max-pool backward and LRN backward (ReLU-masked) fused, one warp per pixel of the LRN
 // input map x (unpadded [R][H][H][C], C % 4 == 0, C <= 256): the warp gathers the pooled
 // gradient of every channel of its pixel (maxpool_bwd_kernel's window order) into shared
-// memory, then applies lrn_bwd_relu_kernel's formula across the channel window from there,
-// so the LRN output gradient never round-trips through HBM. Results are bit-identical to
-// the two-kernel sequence. dout: pooled gradient padded by opad; dx written at pixel
+// memory, then applies the LRN backward across the channel window from there (scale
+// recomputed from x, masked by the ReLU that produced x):
+//   dx_c = dy_c s_c^-b - (2 a b / n) x_c sum_{|j-c|<=2} dy_j x_j s_j^(-b-1)
+// so the LRN output gradient never round-trips through HBM. dout: pooled gradient padded by opad; dx written at pixel
 // (y + xpad, x + xpad) of a map of side Hx.
 __global__ void __launch_bounds__(256) pool_lrn_bwd_relu_kernel(const float* __restrict__ dout,
                                                                 const uint8_t* __restrict__ arg,
