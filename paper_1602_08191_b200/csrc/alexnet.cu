@@ -87,7 +87,7 @@ ConvSpec conv_spec(const Shape& s, int l) {  // l = 0..3 -> conv2..conv5
 // ---- workspace ---------------------------------------------------------------------
 struct AlexWs {
   // forward maps (p = spatially padded, zero border)
-  float *a1, *n1, *p1p, *a2, *n2, *p2p, *a3p, *a4p, *a5p, *p5, *h6, *h7, *z, *dz;
+  float *a1, *p1p, *a2, *p2p, *a3p, *a4p, *a5p, *p5, *h6, *h7, *z, *dz;
   uint8_t *arg1, *arg2, *arg5;
   // backward
   float *dh7, *dh6, *dp5, *dc5p, *dc4p, *dc3p, *dp2p, *dc2p, *dp1, *dc1p;
@@ -111,8 +111,8 @@ AlexWs carve_ws(const ModelInfo& m, uint32_t R, void* base) {
   uint64_t off = 0;
   auto f = [&](float*& p, uint64_t n) { p = reinterpret_cast<float*>(b + off); off += (n * 4 + 255) & ~255ull; };
   auto u = [&](uint8_t*& p, uint64_t n) { p = b + off; off += (n + 255) & ~255ull; };
-  f(ws.a1, M1 * 96), f(ws.n1, M1 * 96), f(ws.p1p, G2 * 96), u(ws.arg1, M2 * 96);
-  f(ws.a2, M2 * 256), f(ws.n2, M2 * 256), f(ws.p2p, G3 * 256), u(ws.arg2, M3 * 256);
+  f(ws.a1, M1 * 96), f(ws.p1p, G2 * 96), u(ws.arg1, M2 * 96);
+  f(ws.a2, M2 * 256), f(ws.p2p, G3 * 256), u(ws.arg2, M3 * 256);
   f(ws.a3p, G3 * 384), f(ws.a4p, G3 * 384), f(ws.a5p, G3 * 256), f(ws.p5, Q5), u(ws.arg5, Q5);
   f(ws.h6, 4096ull * R), f(ws.h7, 4096ull * R), f(ws.z, 1ull * s.Cp * R), f(ws.dz, 1ull * s.Cp * R);
   f(ws.dh7, 4096ull * R), f(ws.dh6, 4096ull * R), f(ws.dp5, Q5);
@@ -334,30 +334,6 @@ __global__ void unpack_wgrad_kernel(const float* __restrict__ dWp, uint32_t rows
   }
 }
 
-// LRN across channels (NHWC, 4 channels per thread): y = x * (k + a/n sum_{|c'-c|<=2} x_c'^2)^-b
-__global__ void lrn_fwd_kernel(const float* __restrict__ x, uint32_t pixels, uint32_t C, float* __restrict__ y,
-                               const uint32_t* gate) {
-  GATE;
-  const uint32_t C4 = C / 4, total = pixels * C4;
-  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
-    const uint32_t p = i / C4, c0 = (i - p * C4) * 4;
-    const float* px = x + p * C;  // 32-bit: pixels * C < 2^32 (the caller bounds the batch)
-    float v[8];  // x[c0-2 .. c0+5]
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = static_cast<int>(c0) - 2 + j;
-      v[j] = (c >= 0 && c < static_cast<int>(C)) ? __ldg(px + c) : 0.f;
-    }
-    float o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float ss = v[j] * v[j] + v[j + 1] * v[j + 1] + v[j + 2] * v[j + 2] + v[j + 3] * v[j + 3] + v[j + 4] * v[j + 4];
-      o[j] = v[j + 2] * __powf(kLrnK + kLrnAlpha / kLrnN * ss, -kLrnBeta);
-    }
-    *reinterpret_cast<float4*>(y + p * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
-  }
-}
-
 // MAX 3x3/2 ceil-mode over an NHWC map (input padded by ipad, output padded by opad, or
 // per-row CHW when chw != 0: the fc6 input). arg[r][py][px][c] (unpadded) = window position
 // (0..8) of the first maximum in scan order. One warp per pooled pixel (8 per block),
@@ -402,6 +378,59 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restric
     } else {
       *reinterpret_cast<float4*>(out + (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c) = best;
     }
+    *reinterpret_cast<uchar4*>(arg + static_cast<uint64_t>(p) * C + c) = bi;
+  }
+}
+
+// LRN across channels, y = x * (k + a/n sum_{|c'-c|<=2} x_c'^2)^-b, fused into the MAX 3x3/2 ceil-mode pool over its output:
+// one warp per pooled pixel, four channels per lane; each window tap's LRN output is
+// recomputed from x (channels c-2 .. c+5: float2 + float4 + float2 loads), so the LRN output
+// map is never written (the backward recomputes the LRN scale from x and pools by argmax).
+// x unpadded NHWC [R][H][H][C]; out padded by opad; arg as maxpool_fwd_kernel.
+__global__ void __launch_bounds__(256) lrn_maxpool_fwd_kernel(const float* __restrict__ x, uint32_t R, uint32_t H,
+                                                              uint32_t C, uint32_t Ho, uint32_t opad,
+                                                              float* __restrict__ out, uint8_t* __restrict__ arg,
+                                                              const uint32_t* gate) {
+  GATE;
+  const uint32_t Hq = Ho + 2 * opad, HoHo = Ho * Ho;
+  const uint32_t p = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (p >= R * HoHo) return;
+  const uint32_t r = p / HoHo, pix = p - r * HoHo, py = pix / Ho, px = pix - py * Ho;
+  const uint32_t hs = py * 2, ws = px * 2, he = min(hs + 3, H), we = min(ws + 3, H);
+  const float* base = x + (static_cast<uint64_t>(r * H + hs) * H + ws) * C;
+  const uint32_t nh = he - hs, nw = we - ws, rowC = H * C;
+  for (uint32_t c = lane * 4; c < C; c += 128) {
+    float4 best = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    uchar4 bi = make_uchar4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const uint32_t dh = k / 3, dw = k % 3;
+      float o[4];
+      if (dh < nh && dw < nw) {
+        const float* q = base + dh * rowC + dw * C + c;
+        const float4 m = *reinterpret_cast<const float4*>(q);
+        const float2 lo = c >= 2 ? *reinterpret_cast<const float2*>(q - 2) : make_float2(0.f, 0.f);
+        const float2 hi = c + 4 < C ? *reinterpret_cast<const float2*>(q + 4) : make_float2(0.f, 0.f);
+        const float v[8] = {lo.x, lo.y, m.x, m.y, m.z, m.w, hi.x, hi.y};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float ss =
+              v[j] * v[j] + v[j + 1] * v[j + 1] + v[j + 2] * v[j + 2] + v[j + 3] * v[j + 3] + v[j + 4] * v[j + 4];
+          o[j] = v[j + 2] * __powf(kLrnK + kLrnAlpha / kLrnN * ss, -kLrnBeta);
+        }
+      } else {
+        o[0] = o[1] = o[2] = o[3] = -INFINITY;
+      }
+      if (k == 0) {
+        best = make_float4(o[0], o[1], o[2], o[3]);
+      } else {  // first maximum in scan order, strict >
+        if (o[0] > best.x) best.x = o[0], bi.x = k;
+        if (o[1] > best.y) best.y = o[1], bi.y = k;
+        if (o[2] > best.z) best.z = o[2], bi.z = k;
+        if (o[3] > best.w) best.w = o[3], bi.w = k;
+      }
+    }
+    *reinterpret_cast<float4*>(out + (static_cast<uint64_t>(r * Hq + py + opad) * Hq + px + opad) * C + c) = best;
     *reinterpret_cast<uchar4*>(arg + static_cast<uint64_t>(p) * C + c) = bi;
   }
 }
@@ -919,7 +948,7 @@ int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint3
   const Shape sh = shape_of(m);
   const auto& L = m.layers;
   const uint32_t F = m.n_features;
-  const uint64_t M1 = 1ull * R * sh.H1 * sh.H1, M2 = 1ull * R * sh.P1 * sh.P1;
+  const uint64_t M2 = 1ull * R * sh.P1 * sh.P1;
   const uint64_t G2 = 1ull * R * sh.Hp2 * sh.Hp2, G3 = 1ull * R * sh.Hp3 * sh.Hp3;
   cudaStream_t s = c.s;
   const uint32_t* gate = c.gate;
@@ -941,14 +970,14 @@ int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint3
   s2d_kernel<<<nblk(1ull * R * sh.Hs * sh.Hs * 48), 256, 0, s>>>(X, idx, F, sh.S, R, sh.Hs, w.xs, gate);
   KDONE(1);
   DS_TRY(conv_fwd(c, conv1_spec(sh), R, w.xs, w.w1p, P + L[0].b_off, w.a1, false));
-  lrn_fwd_kernel<<<nblk(M1 * 24), 256, 0, s>>>(w.a1, static_cast<uint32_t>(M1), 96, w.n1, gate);
-  maxpool_fwd_kernel<<<static_cast<unsigned>((M2 + 7) / 8), 256, 0, s>>>(w.n1, R, sh.H1, 96, sh.P1, 0, 2, 0, w.p1p, w.arg1, gate);
-  KDONE(2);
+  lrn_maxpool_fwd_kernel<<<static_cast<unsigned>((M2 + 7) / 8), 256, 0, s>>>(w.a1, R, sh.H1, 96, sh.P1, 2, w.p1p,
+                                                                           w.arg1, gate);
+  KDONE(1);
   // conv2 + relu -> a2 (unpadded), LRN2, pool2 -> p2p (pad 1)
   DS_TRY(conv_fwd(c, conv_spec(sh, 0), R, w.p1p, w.wp[0], P + L[1].b_off, w.a2, false));
-  lrn_fwd_kernel<<<nblk(M2 * 64), 256, 0, s>>>(w.a2, static_cast<uint32_t>(M2), 256, w.n2, gate);
-  maxpool_fwd_kernel<<<(R * sh.P2 * sh.P2 + 7) / 8, 256, 0, s>>>(w.n2, R, sh.P1, 256, sh.P2, 0, 1, 0, w.p2p, w.arg2, gate);
-  KDONE(2);
+  lrn_maxpool_fwd_kernel<<<(R * sh.P2 * sh.P2 + 7) / 8, 256, 0, s>>>(w.a2, R, sh.P1, 256, sh.P2, 1, w.p2p, w.arg2,
+                                                                    gate);
+  KDONE(1);
   // conv3, conv4, conv5 on the pad-1 grid, pool5 -> p5 (per-row CHW)
   DS_TRY(conv_fwd(c, conv_spec(sh, 1), R, w.p2p, w.wp[1], P + L[2].b_off, w.a3p, true));
   DS_TRY(conv_fwd(c, conv_spec(sh, 2), R, w.a3p, w.wp[2], P + L[3].b_off, w.a4p, true));
