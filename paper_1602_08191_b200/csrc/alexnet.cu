@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(256) pool_lrn_bwd_relu_kernel(const float* __r
                                                                 const uint32_t* gate) {
   GATE;
   __shared__ float4 dys[8][66];  // per warp: channels -4 .. C + 3 (zero outside 0 .. C-1)
+  __shared__ float4 wts[8][66];  // per warp: LRN window terms, same channel range
   const uint32_t HH = H * H, Hq = Ho + 2 * opad, warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t p = blockIdx.x * 8 + warp;
   if (p >= R * HH) return;
@@ -564,34 +565,49 @@ __global__ void __launch_bounds__(256) pool_lrn_bwd_relu_kernel(const float* __r
   }
   __syncwarp();
   const float* ds = reinterpret_cast<const float*>(&dys[warp][1]);  // ds[c], c in [-4, C + 4)
+  // pass 1: each channel's scale once (one log2, two exp2): s_c^-b in registers and
+  // w_c = dy_c x_c s_c^(-b-1) in shared memory; pass 2 sums w over the 5-channel window
+  float* wsm = reinterpret_cast<float*>(&wts[warp][1]);  // wsm[c], c in [-4, C + 4)
+  if (lane == 0) wts[warp][0] = make_float4(0.f, 0.f, 0.f, 0.f), wts[warp][C4 + 1] = wts[warp][0];
   const float* px = x + static_cast<uint64_t>(p) * C;
-  for (uint32_t q = lane; q < C4; q += 32) {
+  float pwr[2][4], xcr[2][4];
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {  // C <= 256: at most two channel groups per lane
+    const uint32_t q = lane + it * 32;
+    if (q >= C4) continue;
     const uint32_t c0 = q * 4;
-    float xv[12], w[8], pw[8];
-#pragma unroll
-    for (int j = 0; j < 12; ++j) {
-      const int c = static_cast<int>(c0) - 4 + j;
-      xv[j] = (c >= 0 && c < static_cast<int>(C)) ? __ldg(px + c) : 0.f;
-    }
-    float sq[12];
-#pragma unroll
-    for (int j = 0; j < 12; ++j) sq[j] = xv[j] * xv[j];
+    float xv[8];  // x[c0-2 .. c0+5]
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int c = static_cast<int>(c0) - 2 + j;
+      xv[j] = (c >= 0 && c < static_cast<int>(C)) ? __ldg(px + c) : 0.f;
+    }
+    float sq[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sq[j] = xv[j] * xv[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
       const float ss = ((sq[j] + sq[j + 1]) + (sq[j + 2] + sq[j + 3])) + sq[j + 4];
       const float sc = kLrnK + kLrnAlpha / kLrnN * ss;
       const float l2 = __log2f(sc);
-      pw[j] = exp2f(-kLrnBeta * l2);
-      w[j] = ds[c] * xv[j + 2] * exp2f(-(kLrnBeta + 1.f) * l2);
+      pwr[it][j] = exp2f(-kLrnBeta * l2);
+      xcr[it][j] = xv[j + 2];
+      wsm[c0 + j] = ds[c0 + j] * xv[j + 2] * exp2f(-(kLrnBeta + 1.f) * l2);
     }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const uint32_t q = lane + it * 32;
+    if (q >= C4) continue;
+    const uint32_t c0 = q * 4;
     float o[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float xc = xv[j + 4];
-      const float acc = w[j] + w[j + 1] + w[j + 2] + w[j + 3] + w[j + 4];
-      const float d = ds[c0 + j];
-      o[j] = xc > 0.f ? d * pw[j + 2] - 2.f * kLrnAlpha * kLrnBeta / kLrnN * xc * acc : 0.f;
+      const uint32_t c = c0 + j;
+      const float xc = xcr[it][j];
+      const float acc = wsm[c - 2] + wsm[c - 1] + wsm[c] + wsm[c + 1] + wsm[c + 2];
+      o[j] = xc > 0.f ? ds[c] * pwr[it][j] - 2.f * kLrnAlpha * kLrnBeta / kLrnN * xc * acc : 0.f;
     }
     *reinterpret_cast<float4*>(dx + (static_cast<uint64_t>(r * Hx + y + xpad) * Hx + xx + xpad) * C + c0) =
         make_float4(o[0], o[1], o[2], o[3]);
