@@ -50,6 +50,7 @@ int ds_device_count(int* count);
 #define DS_FLAG_GRAD_NONFINITE 16u /* loss_and_grad: non-finite gradient       (model.cpp:259) */
 #define DS_FLAG_LABEL_RANGE 32u   /* loss_and_grad: label out of range         (model.cpp:176-180) */
 #define DS_FLAG_STREAM_TIMEOUT 64u /* stream mode: no batch from the host for 20 s                  */
+#define DS_FLAG_TICKET_TIMEOUT 128u /* ordered exchange: the previous ticket never completed (30 s) */
 
 /* ---------------------------------------------------------------------------------- */
 /* Elementwise updates — param_vector.hpp:21-38                                       */
@@ -265,6 +266,12 @@ typedef struct {
 #define DS_ENGINE_AUTO 0    /* fused persistent kernel when the model allows, else layered */
 #define DS_ENGINE_LAYERED 1 /* one kernel per layer pass; any depth                        */
 #define DS_ENGINE_FUSED 2   /* persistent single-kernel step (<= 1 hidden layer)            */
+/* Fast mode (NOT the reference's f64 order): the one-hidden-layer MLP step with its two
+ * dense contractions (forward X.W1^T, weight gradient X^T.delta1) on the tcgen05 tensor
+ * cores in bf16 with f32 accumulation, everything else f32; one thread-block cluster per
+ * worker (16 hidden units per CTA), so several engines train concurrently on one GPU.
+ * Every master mode exchanges in-kernel. Tolerance parity (tests/test_gpu_tc.py). */
+#define DS_ENGINE_TC 3
 
 /* SgdEngine(model, shard, hp, sweep_seed, initial) (engine.cpp:50-65): uploads the
  * shard (X row-major f32 [shard_n x n_features], y u32) to `device` once, keeps the

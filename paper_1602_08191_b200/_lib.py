@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libds_cuda.so")
+# DS_LIB_PATH: load an instrumented build of the same library (tools/ experiments)
+LIB_PATH = os.environ.get("DS_LIB_PATH") or os.path.join(HERE, "lib", "libds_cuda.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -22,7 +23,7 @@ lib = C.CDLL(LIB_PATH)
 
 DS_OK, DS_E_CONTRACT, DS_E_NUMERIC, DS_E_CUDA, DS_E_NOMEM, DS_E_STATE, DS_E_FORMAT, DS_E_IO = range(8)
 DS_MODE_LOCKED, DS_MODE_LOCKFREE = 0, 1
-DS_ENGINE_AUTO, DS_ENGINE_LAYERED, DS_ENGINE_FUSED = 0, 1, 2
+DS_ENGINE_AUTO, DS_ENGINE_LAYERED, DS_ENGINE_FUSED, DS_ENGINE_TC = 0, 1, 2, 3
 DS_IPC_RECORD_BYTES = 256
 DS_STREAM_RING = 8  # include/ds_cuda.h
 

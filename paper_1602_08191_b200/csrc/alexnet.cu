@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(256) pool_lrn_bwd_relu_kernel(const float* __r
     float o[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const uint32_t c = c0 + j;
+      const int c = static_cast<int>(c0) + j;  // signed: wsm[c - 2] at c < 2 is the zero guard
       const float xc = xcr[it][j];
       const float acc = wsm[c - 2] + wsm[c - 1] + wsm[c] + wsm[c + 1] + wsm[c + 2];
       o[j] = xc > 0.f ? ds[c] * pwr[it][j] - 2.f * kLrnAlpha * kLrnBeta / kLrnN * xc * acc : 0.f;

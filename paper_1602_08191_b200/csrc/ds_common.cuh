@@ -94,4 +94,23 @@ __device__ __forceinline__ unsigned long long atom_add_sys(unsigned long long* p
 }
 __device__ __forceinline__ void nanosleep_ns(unsigned ns) { __nanosleep(ns); }
 
+// Bounded acquire-wait until *p == want. Returns false after kSeqTimeoutNs: a peer that
+// stopped early (non-finite step) or died never advances the word, so the waiter raises
+// an error flag instead of hanging every GPU of the group.
+constexpr unsigned long long kSeqTimeoutNs = 30ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ bool wait_seq_eq(const uint64_t* p, uint64_t want, unsigned sleep_ns) {
+  if (ld_acquire_sys(p) == want) return true;
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_sys(p) != want) {
+    if (globaltimer_ns() - t0 > kSeqTimeoutNs) return false;
+    __nanosleep(sleep_ns);
+  }
+  return true;
+}
+
 }  // namespace dsb

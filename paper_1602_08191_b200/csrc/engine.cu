@@ -102,6 +102,13 @@ struct ds_engine {
   uint64_t* d_tickets = nullptr;
   int kind = DS_ENGINE_AUTO;
   bool fused = false;
+  bool tc = false;   // DS_ENGINE_TC: run_fused launches the tensor-core step (mlp_tc.cu)
+  int tc_nc = 0;     // its cluster size
+  // tensor-core step: bf16 copies of the batch sources ([rows][tc_pitch(F)]) + TMA maps
+  void* tc_shard = nullptr;   // the resident shard
+  void* tc_stage = nullptr;   // host-fed rows (ds_engine_step_host)
+  void* tc_ring = nullptr;    // stream-mode ring slots
+  CUtensorMap tm_shard{}, tm_stage{}, tm_ring{};
   int fused_grid = 0;
   uint64_t launches = 0;
   // host-fed batches (ds_engine_step_host): staging rows, identity plan, row count
@@ -238,6 +245,7 @@ uint64_t next_ticket(ds_engine* e) {
 bool in_kernel_ok(const ds_engine* e) {
   // the fused kernel may exchange itself when no host-side ordering is needed
   const ds_master* m = e->master;
+  if (e->tc) return m != nullptr;  // tickets / dispenser / plain stores, all in-kernel
   return m && (m->sharded || (m->mode == DS_MODE_LOCKFREE && e->tickets.empty()));
 }
 
@@ -417,13 +425,21 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
     a.table = e->master->table;
     a.lockfree = e->master->mode == DS_MODE_LOCKFREE && e->tickets.empty();
     a.tickets = e->tickets.empty() ? nullptr : e->d_tickets + e->host_exchanges;
+    if (a.tickets) {
+      // the kernel reads one ticket per exchange of this run: never past the array
+      const uint64_t need = (e->host_since + steps) / e->hp.tau;
+      if (e->host_exchanges + need > e->tickets.size())
+        return set_error(DS_E_STATE, "engine: ran out of deterministic exchange tickets (%llu needed, %llu left)",
+                         static_cast<unsigned long long>(need),
+                         static_cast<unsigned long long>(e->tickets.size() - std::min<uint64_t>(e->host_exchanges, e->tickets.size())));
+    }
     a.ticket_src = (!a.lockfree && !a.tickets) ? &e->master->table.flags[0]->next_ticket : nullptr;
   }
   // DS_FUSED_PROFILE=<file>: per-phase globaltimer stamps of CTA 0, medians appended
   const char* prof_path = std::getenv("DS_FUSED_PROFILE");
   unsigned long long* prof = nullptr;
   const uint64_t G = static_cast<uint64_t>(e->fused_grid);
-  const uint64_t prof_n = steps * (kProfSlots + 2 * G);
+  const uint64_t prof_n = steps * (kProfSlots + 2 * G) + 8;
   if (prof_path && steps >= 8) DS_CUDA_TRY(cudaMalloc(&prof, prof_n * sizeof(unsigned long long)));
   if (prof) DS_CUDA_TRY(cudaMemsetAsync(prof, 0, prof_n * sizeof(unsigned long long), e->stream));
   a.prof = prof;
@@ -438,7 +454,18 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
     a.ring_consumed = e->ring_consumed;
     a.ring_loss = e->ring_loss;
   }
-  DS_TRY(launch_fused(a, e->fused_grid, e->stream));
+  if (e->tc) {
+    const CUtensorMap* tm = &e->tm_shard;
+    if (e->ring_active) {
+      tm = &e->tm_ring;
+    } else if (e->hostfed) {  // this step's rows (staged f32 by step_host) as bf16
+      DS_TRY(tc_rows_to_bf16(e->Xb, e->hostfed_rows, e->model.n_features, e->tc_stage, e->stream));
+      tm = &e->tm_stage;
+    }
+    DS_TRY(launch_tc(a, e->tc_nc, *tm, e->stream));
+  }
+  else
+    DS_TRY(launch_fused(a, e->fused_grid, e->stream));
   e->launches += 1;
   e->cur ^= static_cast<int>(steps & 1);
   if (prof) {
@@ -446,11 +473,31 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
     DS_CUDA_TRY(cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream));
     DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
     cudaFree(prof);
-    const char* names[] = {"x_staged", "forward", "grid_barrier", "acts_staged", "logits", "softmax_loss",
-                           "backward_update", "policy_exchange", "bwd_head", "bwd_dW1"};
-    const int pairs[][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}, {6, 9}, {9, 7}};
+    const char* fnames[] = {"x_staged", "forward", "grid_barrier", "acts_staged", "logits", "softmax_loss",
+                            "backward_update", "policy_exchange", "bwd_head", "bwd_dW1"};
+    const int fpairs[][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}, {6, 9}, {9, 7}};
+    // tensor-core step (mlp_tc.cu): forward MMAs, tanh + partial logits, R phase, softmax +
+    // G phase, deltas + dW1 MMAs, W1 SGD, policy + exchange (then the next step's start)
+    const char* tnames[] = {"wait_fwd", "tanh_logits", "R_phase", "softmax_G", "unpack_delta1", "w2b_dW1_sgd",
+                            "exchange", "-", "start_to_G", "G_to_end"};
+    const int tpairs[][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 7}, {0, 4}, {4, 7}};
+    const char* const* names = e->tc ? tnames : fnames;
+    const int(*pairs)[2] = e->tc ? tpairs : fpairs;
+    static const int xpairs[][2] = {{0, 1}, {1, 6}, {6, 7}, {7, 8}, {8, 2}, {2, 3}, {3, 4}, {4, 5}, {1, 2}, {0, 5}};
+    static const char* xnames[] = {"arm", "round0_first_tile", "round0_rest", "round1", "wait_st", "small_fence",
+                                   "cbar", "release", "w1_all", "exchange_all"};
+    if (e->tc && std::getenv("DS_TC_PROF_X")) pairs = xpairs, names = xnames;
+    // MMA warp timeline: fwd(s) tiles (stamps 2,3,4 at sgdd waits of tiles 0,3,last; 5 commit),
+    // logits (6), delta1 ready (0) and dW1 issued (1); pairs are within the MMA loop's step s
+    static const int mpairs[][2] = {{2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 0}, {0, 1}, {2, 5}, {2, 0}, {0, 0}, {0, 0}};
+    static const char* mnames[] = {"fwd_t0_t3", "fwd_t3_t6", "fwd_last_commit", "logits_wait_a1",
+                                   "a1_to_d1rdy", "dW1_issue", "fwd_all", "fwd_to_d1", "-", "-"};
+    if (e->tc && std::getenv("DS_TC_PROF_M")) pairs = mpairs, names = mnames;
     if (FILE* f = std::fopen(prof_path, "a")) {
       std::fprintf(f, "steps=%llu", (unsigned long long)steps);
+      if (e->tc && h[steps * kProfSlots])
+        std::fprintf(f, " sm_clock=%.0fMHz", 1e3 * static_cast<double>(h[steps * kProfSlots + 1]) /
+                                                 static_cast<double>(h[steps * kProfSlots]));
       for (int k = 0; k < 10; ++k) {
         std::vector<double> d;
         for (uint64_t s = 2; s < steps; ++s) {
@@ -610,6 +657,24 @@ static int engine_create(ds_engine** out, int device, const ds_model_desc* model
   int rc = dsb::ensure_log(e, hp->i_max);
   if (rc != DS_OK) return fail(rc);
   const char* why = nullptr;
+  if (kind == DS_ENGINE_TC) {
+    if (dsb::tc_supported(m, static_cast<uint32_t>(B), device, &why) != DS_OK)
+      return fail(set_error(DS_E_CONTRACT, "engine: tensor-core path unavailable: %s", why));
+    e->fused = true;
+    e->tc = true;
+    e->tc_nc = dsb::tc_cluster(m);
+    const uint64_t pitch = dsb::tc_pitch(static_cast<uint32_t>(F));
+    err = cudaMalloc(&e->tc_shard, shard_n * pitch * 2);
+    if (err == cudaSuccess) err = cudaMalloc(&e->tc_stage, B * pitch * 2);
+    if (err == cudaSuccess) err = cudaMemset(e->tc_stage, 0, B * pitch * 2);
+    if (err != cudaSuccess) return fail(set_error(DS_E_NOMEM, "engine: %s", cudaGetErrorString(err)));
+    rc = dsb::tc_rows_to_bf16(e->X, shard_n, static_cast<uint32_t>(F), e->tc_shard, e->stream);
+    if (rc == DS_OK) rc = dsb::tc_make_map(&e->tm_shard, e->tc_shard, shard_n, static_cast<uint32_t>(F));
+    if (rc == DS_OK) rc = dsb::tc_make_map(&e->tm_stage, e->tc_stage, B, static_cast<uint32_t>(F));
+    if (rc != DS_OK) return fail(rc);
+    *out = e;
+    return DS_OK;
+  }
   const bool can_fuse = dsb::fused_supported(m, static_cast<uint32_t>(B), device, &why) == DS_OK;
   if (kind == DS_ENGINE_FUSED && !can_fuse) return fail(set_error(DS_E_CONTRACT, "engine: fused path unavailable: %s", why));
   e->fused = (kind == DS_ENGINE_FUSED) || (kind == DS_ENGINE_AUTO && can_fuse);
@@ -657,6 +722,9 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->ws);
   cudaFree(e->act);
   cudaFree(e->xb64);
+  cudaFree(e->tc_shard);
+  cudaFree(e->tc_stage);
+  cudaFree(e->tc_ring);
   cudaFree(e->st);
   cudaFree(e->bar);
   cudaFree(e->plan);
@@ -812,6 +880,10 @@ int engine_error(ds_engine* e) {
   if (f & DS_FLAG_X_NONFINITE) return set_error(DS_E_CONTRACT, "sgd_step: x contains a non-finite value (iteration %llu)", it);
   if (f & DS_FLAG_G_NONFINITE) return set_error(DS_E_CONTRACT, "sgd_step: grad contains a non-finite value (iteration %llu)", it);
   if (f & DS_FLAG_OUT_NONFINITE) return set_error(DS_E_NUMERIC, "sgd_step: non-finite result (iteration %llu)", it);
+  if (f & DS_FLAG_TICKET_TIMEOUT)
+    return set_error(DS_E_STATE, "exchange: timed out waiting for the previous ticket (a peer worker stopped early "
+                     "or died; iteration %llu)", it);
+  if (f & DS_FLAG_STREAM_TIMEOUT) return set_error(DS_E_STATE, "stream: no batch from the host for 20 s (iteration %llu)", it);
   return set_error(DS_E_NUMERIC, "engine: failure flags 0x%x (iteration %llu)", f, it);
 }
 }  // namespace
@@ -979,6 +1051,11 @@ extern "C" int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss
     DS_CUDA_TRY(cudaHostAlloc(&e->ring_consumed, sizeof(unsigned long long), cudaHostAllocMapped));
     DS_CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
   }
+  if (e->tc && !e->tc_ring) {  // bf16 copies of the slots, converted on the copy stream
+    DS_CUDA_TRY(cudaMalloc(&e->tc_ring, K * B * dsb::tc_pitch(static_cast<uint32_t>(F)) * 2));
+    DS_CUDA_TRY(cudaMemset(e->tc_ring, 0, K * B * dsb::tc_pitch(static_cast<uint32_t>(F)) * 2));
+    DS_TRY(dsb::tc_make_map(&e->tm_ring, e->tc_ring, K * B, static_cast<uint32_t>(F)));
+  }
   DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
   DS_CUDA_TRY(cudaMemsetAsync(e->ring_words, 0, 2 * K * sizeof(uint32_t), e->stream));
   *reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) = 0;
@@ -1019,6 +1096,9 @@ int stream_enqueue(ds_engine* e, const float* X_host, const uint32_t* y_host, ui
   e->ring_src[K + slot] = (rows << 20) | (static_cast<uint32_t>(s + 1) & 0xFFFFFu);
   cudaStream_t cs = e->copy_stream;
   DS_CUDA_TRY(cudaMemcpyAsync(e->ring_X + slot * B * F, X_host, rows * F * sizeof(float), cudaMemcpyDefault, cs));
+  if (e->tc)  // the tensor-core step gathers bf16 rows; convert the slot before its ready word
+    DS_TRY(dsb::tc_rows_to_bf16(e->ring_X + slot * B * F, rows, static_cast<uint32_t>(F),
+                                static_cast<char*>(e->tc_ring) + slot * B * dsb::tc_pitch(static_cast<uint32_t>(F)) * 2, cs));
   DS_CUDA_TRY(cudaMemcpyAsync(e->ring_y + slot * B, y_host, rows * sizeof(uint32_t), cudaMemcpyDefault, cs));
   DS_CUDA_TRY(cudaMemcpyAsync(e->ring_words + K + slot, e->ring_src + K + slot, sizeof(uint32_t),
                               cudaMemcpyHostToDevice, cs));

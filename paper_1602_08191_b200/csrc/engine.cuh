@@ -1,5 +1,6 @@
 // engine.cuh — device-resident SgdEngine / run_training_loop state (engine.hpp:17-105).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -79,6 +80,15 @@ struct FusedArgs {
 constexpr int kProfSlots = 10;
 
 int fused_supported(const ModelInfo& m, uint32_t batch, int device, const char** why);
+// mlp_tc.cu: the tensor-core (bf16 tcgen05, tolerance) fast step, one cluster per worker.
+int tc_supported(const ModelInfo& m, uint32_t batch, int device, const char** why);
+int tc_cluster(const ModelInfo& m);
+size_t tc_smem_bytes(const ModelInfo& m, uint32_t batch);
+int launch_tc(const FusedArgs& a, int nc, const CUtensorMap& batch_rows, cudaStream_t s);
+// the tensor-core step reads batches as bf16 rows of tc_pitch(F) elements through a TMA map
+uint32_t tc_pitch(uint32_t F);
+int tc_rows_to_bf16(const float* src, uint64_t rows, uint32_t F, void* dst, cudaStream_t s);
+int tc_make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t F);
 // Doubles of the f64 batch buffer (A.xb64) the MLP kernel needs.
 size_t fused_xb_doubles(const ModelInfo& m, uint32_t batch, int device);
 int launch_fused(const FusedArgs& a, int grid, cudaStream_t s);

@@ -37,20 +37,27 @@ __global__ void __launch_bounds__(kT) exchange_kernel(const float* w, float* out
                                                       uint64_t ticket, const unsigned long long* ticket_slot,
                                                       const uint32_t* fire, const uint32_t* gate, int cps,
                                                       int vec) {
-  if (fire && *fire == 0) return;
-  if (gate && *gate) return;
+  if (fire && *fire == 0) return;  // the policy did not fire: no exchange, no ticket
+  // An errored engine (gate) skips the data but still passes an explicit ticket on, so the
+  // peers waiting for the next ticket are not left hanging. A dispenser ticket was never
+  // taken when gated (take_ticket_kernel skips too).
+  const bool gated = gate && *gate;
+  if (gated && (ticket_slot || ticket == kNoTicket)) return;
   const int s = blockIdx.x % t.n;
   const int c = blockIdx.x / t.n;
   const uint64_t b0 = t.begin[s], b1 = t.begin[s + 1];
   const uint64_t tk = ticket_slot ? static_cast<uint64_t>(*ticket_slot) : ticket;
   const bool ordered = tk != kNoTicket;
   if (ordered) {
+    __shared__ int s_timeout;
     if (threadIdx.x == 0) {
-      while (ld_acquire_sys(reinterpret_cast<const uint64_t*>(&t.flags[s]->seq)) != tk) nanosleep_ns(100);
+      s_timeout = !wait_seq_eq(reinterpret_cast<const uint64_t*>(&t.flags[s]->seq), tk, 100);
+      if (s_timeout) atomicAdd_system(&t.flags[s]->timeouts, 1ull);
     }
     __syncthreads();
+    if (s_timeout) return;
   }
-  const uint64_t len = b1 - b0;
+  const uint64_t len = gated ? 0 : b1 - b0;
   const uint64_t per = ((len + cps - 1) / cps + 3) & ~3ull;
   const uint64_t lo = b0 + per * c;
   const uint64_t hi = lo + per < b1 ? lo + per : b1;
@@ -361,6 +368,12 @@ extern "C" int ds_master_exchange_count(ds_master* m, uint64_t* count) {
   dsb::DeviceScope ds(m->device);
   DS_CUDA_TRY(cudaDeviceSynchronize());
   dsb::ShardFlags f;
+  for (int k = 0; k < m->table.n; ++k) {
+    DS_CUDA_TRY(cudaMemcpy(&f, m->table.flags[k], sizeof(f), cudaMemcpyDefault));
+    if (f.timeouts)
+      return dsb::set_error(DS_E_STATE, "master: %llu ordered exchange(s) on shard %d timed out waiting for their "
+                            "ticket (a peer worker stopped early or died)", f.timeouts, k);
+  }
   DS_CUDA_TRY(cudaMemcpy(&f, m->table.flags[0], sizeof(f), cudaMemcpyDefault));
   *count = f.exchanges;
   return DS_OK;

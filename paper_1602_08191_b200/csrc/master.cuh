@@ -25,7 +25,8 @@ struct alignas(128) ShardFlags {
   unsigned long long done;       // CTAs finished for the current ticket
   unsigned long long next_ticket;  // ticket dispenser (Locked mode; rank 0's copy is used)
   unsigned long long exchanges;  // completed exchanges (counted on shard 0)
-  unsigned long long pad[12];
+  unsigned long long timeouts;   // ticket waits on this shard that gave up (wait_seq_eq)
+  unsigned long long pad[11];
 };
 
 // What an exchange kernel needs to reach every slice.

@@ -30,6 +30,10 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "ds_common.cuh"
 #include "engine.cuh"
 
@@ -175,9 +179,16 @@ __device__ void do_exchange(const FusedArgs& A, float* p, const Slice& sl, uint6
   const bool ordered = ticket != kNoTicket;
   for (int s = 0; s < t.n; ++s) {
     if (ordered) {
-      if (threadIdx.x == 0)
-        while (ld_acquire_sys(reinterpret_cast<const uint64_t*>(&t.flags[s]->seq)) != ticket) nanosleep_ns(64);
+      __shared__ int s_timeout;
+      if (threadIdx.x == 0) {
+        s_timeout = !wait_seq_eq(reinterpret_cast<const uint64_t*>(&t.flags[s]->seq), ticket, 64);
+        if (s_timeout) {
+          atomicAdd_system(&t.flags[s]->timeouts, 1ull);
+          atomicOr(&A.st->flags, DS_FLAG_TICKET_TIMEOUT);
+        }
+      }
       __syncthreads();
+      if (s_timeout) return;
     }
     exchange_shard(p, t, s, sl, A.alpha);
     __syncthreads();
@@ -265,9 +276,12 @@ __device__ void exchange_all_mlp(float* p, const ShardTable& t, const Slice& sl,
   const uint32_t n = sl.cols[0];  // own W1 rows: Uo * F, one row, 16-byte aligned
   for (uint32_t j = threadIdx.x * 4; j < n; j += kFT * 4) {
     const uint64_t g = lo + j;
+    bool in[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) in[q] = j + q < n;  // n % 4 != 0: the last group is partial
     const int s0 = shard_of(t, g), s3 = shard_of(t, g + 3);
     float wo[4], mo[4];
-    if (s0 == s3 && ((g - t.begin[s0]) & 3) == 0) {
+    if (in[3] && s0 == s3 && ((g - t.begin[s0]) & 3) == 0 && (g & 3) == 0) {
       float* m = t.ptr[s0] + (g - t.begin[s0]);
       const float4 wv = *reinterpret_cast<const float4*>(p + g);
       const float4 mv = __ldcg(reinterpret_cast<const float4*>(m));
@@ -279,6 +293,7 @@ __device__ void exchange_all_mlp(float* p, const ShardTable& t, const Slice& sl,
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
+        if (!in[q]) continue;
         const int sq = shard_of(t, g + q);
         float* m = t.ptr[sq] + (g + q - t.begin[sq]);
         elastic_elem(p[g + q], __ldcg(m), a, wo[q], mo[q]);
@@ -288,6 +303,7 @@ __device__ void exchange_all_mlp(float* p, const ShardTable& t, const Slice& sl,
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      if (!in[q]) continue;
       const uint32_t local = j + q, uu = local / F, i = local - uu * F;
       Ws[local] = wo[q];
       Wd[uu * Fd + i] = static_cast<double>(wo[q]);
@@ -315,9 +331,16 @@ __device__ void do_exchange_mlp(const FusedArgs& A, float* p, const Slice& sl, u
   }
   for (int s = 0; s < t.n; ++s) {
     if (ordered) {
-      if (threadIdx.x == 0)
-        while (ld_acquire_sys(reinterpret_cast<const uint64_t*>(&t.flags[s]->seq)) != ticket) nanosleep_ns(64);
+      __shared__ int s_timeout;
+      if (threadIdx.x == 0) {
+        s_timeout = !wait_seq_eq(reinterpret_cast<const uint64_t*>(&t.flags[s]->seq), ticket, 64);
+        if (s_timeout) {
+          atomicAdd_system(&t.flags[s]->timeouts, 1ull);
+          atomicOr(&A.st->flags, DS_FLAG_TICKET_TIMEOUT);
+        }
+      }
       __syncthreads();
+      if (s_timeout) return;
     }
     exchange_shard_mlp(p, t, s, sl, A.alpha, Ws, Wd, F, Fd);
     __syncthreads();
@@ -1708,10 +1731,21 @@ int launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
     // default is no clusters.
     unsigned cap = 1;
     if (const char* env = std::getenv("DS_FUSED_CLUSTER")) cap = static_cast<unsigned>(std::max(1, std::atoi(env)));
-    static int cached_grid = -1;
-    static size_t cached_smem = 0;
-    static unsigned cached_cap = 0, cached_cl = 1;
-    if (grid != cached_grid || smem != cached_smem || cap != cached_cap) {
+    // The cluster choice depends on (device, grid, smem, cap); engines on several threads
+    // or devices share this cache, so it is keyed and locked.
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::mutex cache_mu;
+    static std::map<std::tuple<int, int, size_t, unsigned>, unsigned> cache;
+    const auto key = std::make_tuple(dev, grid, smem, cap);
+    unsigned cached_cl = 1;
+    bool have = false;
+    {
+      std::lock_guard<std::mutex> lk(cache_mu);
+      auto it = cache.find(key);
+      if (it != cache.end()) cached_cl = it->second, have = true;
+    }
+    if (!have) {
       unsigned pick = 1;
       for (unsigned cl = 8; cl >= 2; cl /= 2) {
         if (cl > cap || grid % cl) continue;
@@ -1734,10 +1768,9 @@ int launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
         }
         cudaGetLastError();
       }
-      cached_grid = grid;
-      cached_smem = smem;
-      cached_cap = cap;
       cached_cl = pick;
+      std::lock_guard<std::mutex> lk(cache_mu);
+      cache[key] = pick;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

@@ -77,13 +77,16 @@ CASES = [
     ("mlp2layers", ModelSpec.mlp(12, [8, 6], 4), 200, 10, Hyper(eta=0.1, tau=3, batch_size=10, i_max=30)),
     ("mlp784", ModelSpec.mlp(784, [256], 10), 600, 32, Hyper(eta=0.05, tau=10, batch_size=32, i_max=60)),
     ("short-batch", ModelSpec.mlp(20, [33], 3), 70, 32, Hyper(eta=0.05, tau=4, batch_size=32, i_max=12)),
+    # F % 4 != 0: the fused exchange's last 4-element group of each W1 row block is partial
+    ("mlp13-odd", ModelSpec.mlp(13, [16], 3), 300, 16, Hyper(eta=0.05, tau=5, batch_size=16, i_max=40)),
 ]
 
 
 @pytest.mark.parametrize("kind", [1, 2])  # layered, fused
 @pytest.mark.parametrize("name,m,n,b,hp", CASES, ids=[c[0] for c in CASES])
-@pytest.mark.parametrize("with_master", [False, True])
+@pytest.mark.parametrize("with_master", [False, "locked", "lockfree"])
 def test_engine_matches_oracle(L, orc, kind, name, m, n, b, hp, with_master):
+    """A LockFree master with one writer must equal the Locked one (test_exchanger.cpp:228-242)."""
     if kind == 2 and len(m.hidden) > 1:
         pytest.skip("fused path covers <= 1 hidden layer")
     X, y = orc.gen_synthetic(n, m.n_features, m.n_classes, 2.0, 1.5, 3)
@@ -96,7 +99,8 @@ def test_engine_matches_oracle(L, orc, kind, name, m, n, b, hp, with_master):
     try:
         if with_master:
             mh = C.c_void_p()
-            L.check(L.lib.ds_master_create(C.byref(mh), 0, P, C.c_float(np.float32(hp.alpha)), L.DS_MODE_LOCKED,
+            mode = L.DS_MODE_LOCKED if with_master == "locked" else L.DS_MODE_LOCKFREE
+            L.check(L.lib.ds_master_create(C.byref(mh), 0, P, C.c_float(np.float32(hp.alpha)), mode,
                                            master0.ctypes.data))
             L.check(L.lib.ds_engine_attach_master(e, mh))
         L.check(L.lib.ds_engine_run(e, hp.i_max, 0, None))
