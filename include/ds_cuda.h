@@ -299,6 +299,14 @@ int ds_engine_set_tickets(ds_engine* e, const uint64_t* tickets, uint64_t count)
  * policy fires WITHOUT performing that exchange (for host ExchangeFn callbacks);
  * *ran_out (host, optional, synchronous when given) reports the iterations done. */
 int ds_engine_run(ds_engine* e, uint64_t steps, int stop_at_exchange, uint64_t* ran_out);
+/* Run `steps` iterations of several tensor-core engines (DS_ENGINE_TC; same device, model
+ * and batch size; <= 8) in ONE cooperative launch, one thread-block cluster per engine, all
+ * resident at once: the workers train concurrently and exchange with their masters
+ * in-kernel, so deterministic tickets across them are honoured on a single GPU (the
+ * reference's n-worker run_training_loop / simulate_async schedule, simulator.cpp:70-154).
+ * Equivalent to ds_engine_run(e, steps, 0, NULL) on each engine; enqueued on engine 0's
+ * stream, ordered after and before every engine's own stream work. */
+int ds_engine_run_group(ds_engine** engines, uint32_t n, uint64_t steps);
 /* Pre-size the engine's batch-plan and TrainLog buffers for the next `steps`
  * iterations so a following ds_engine_run(steps) allocates nothing (no implicit
  * device synchronisation inside a timed or latency-sensitive region). */

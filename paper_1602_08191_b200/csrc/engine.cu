@@ -396,9 +396,10 @@ int run_layered(ds_engine* e, uint64_t steps, bool with_master) {
   return DS_OK;
 }
 
-int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
+// The step kernels' arguments for the next `steps` iterations (uploads the batch plan).
+int fused_args(ds_engine* e, uint64_t steps, bool in_kernel_exchange, FusedArgs& a) {
   if (!e->hostfed && !e->ring_active) DS_TRY(upload_plan(e, steps));
-  FusedArgs a{};
+  a = FusedArgs{};
   a.F = e->model.n_features;
   a.H = e->model.hidden.empty() ? 0 : e->model.hidden[0];
   a.C = e->model.n_classes;
@@ -435,15 +436,6 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
     }
     a.ticket_src = (!a.lockfree && !a.tickets) ? &e->master->table.flags[0]->next_ticket : nullptr;
   }
-  // DS_FUSED_PROFILE=<file>: per-phase globaltimer stamps of CTA 0, medians appended
-  const char* prof_path = std::getenv("DS_FUSED_PROFILE");
-  unsigned long long* prof = nullptr;
-  const uint64_t G = static_cast<uint64_t>(e->fused_grid);
-  const uint64_t prof_n = steps * (kProfSlots + 2 * G) + 8;
-  if (prof_path && steps >= 8) DS_CUDA_TRY(cudaMalloc(&prof, prof_n * sizeof(unsigned long long)));
-  if (prof) DS_CUDA_TRY(cudaMemsetAsync(prof, 0, prof_n * sizeof(unsigned long long), e->stream));
-  a.prof = prof;
-  a.prof_cta = prof ? prof + steps * kProfSlots : nullptr;
   if (e->ring_active) {
     a.ring = 1;
     a.ring_slots = ds_engine::kRing;
@@ -454,6 +446,21 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
     a.ring_consumed = e->ring_consumed;
     a.ring_loss = e->ring_loss;
   }
+  return DS_OK;
+}
+
+int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
+  FusedArgs a;
+  DS_TRY(fused_args(e, steps, in_kernel_exchange, a));
+  // DS_FUSED_PROFILE=<file>: per-phase globaltimer stamps of CTA 0, medians appended
+  const char* prof_path = std::getenv("DS_FUSED_PROFILE");
+  unsigned long long* prof = nullptr;
+  const uint64_t G = static_cast<uint64_t>(e->fused_grid);
+  const uint64_t prof_n = steps * (kProfSlots + 2 * G) + 8;
+  if (prof_path && steps >= 8) DS_CUDA_TRY(cudaMalloc(&prof, prof_n * sizeof(unsigned long long)));
+  if (prof) DS_CUDA_TRY(cudaMemsetAsync(prof, 0, prof_n * sizeof(unsigned long long), e->stream));
+  a.prof = prof;
+  a.prof_cta = prof ? prof + steps * kProfSlots : nullptr;
   if (e->tc) {
     const CUtensorMap* tm = &e->tm_shard;
     if (e->ring_active) {
@@ -866,6 +873,59 @@ extern "C" int ds_engine_run(ds_engine* e, uint64_t steps, int stop_at_exchange,
   return DS_OK;
 }
 
+extern "C" int ds_engine_run_group(ds_engine** engines, uint32_t n, uint64_t steps) {
+  if (!engines || n == 0) return set_error(DS_E_CONTRACT, "engine_run_group: no engines");
+  if (n > 8) return set_error(DS_E_CONTRACT, "engine_run_group: at most 8 engines per launch");
+  ds_engine* e0 = engines[0];
+  for (uint32_t i = 0; i < n; ++i) {
+    ds_engine* e = engines[i];
+    if (!e) return set_error(DS_E_CONTRACT, "engine_run_group: null engine");
+    for (uint32_t k = 0; k < i; ++k)
+      if (engines[k] == e) return set_error(DS_E_CONTRACT, "engine_run_group: engine listed twice");
+    if (!e->tc) return set_error(DS_E_CONTRACT, "engine_run_group: needs tensor-core engines (DS_ENGINE_TC)");
+    if (e->device != e0->device || e->model.n_features != e0->model.n_features ||
+        e->model.hidden != e0->model.hidden || e->model.n_classes != e0->model.n_classes ||
+        e->hp.batch_size != e0->hp.batch_size)
+      return set_error(DS_E_CONTRACT, "engine_run_group: engines differ in device, model or batch size");
+    if (e->ring_active || e->hostfed) return set_error(DS_E_STATE, "engine_run_group: an engine is in stream mode");
+  }
+  if (steps == 0) return DS_OK;
+  dsb::DeviceScope ds(e0->device);
+  std::vector<dsb::FusedArgs> a(n);
+  std::vector<CUtensorMap> tm(n);
+  cudaEvent_t ev = nullptr;
+  DS_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t e;
+    ~EvGuard() { cudaEventDestroy(e); }
+  } guard{ev};
+  for (uint32_t i = 0; i < n; ++i) {
+    ds_engine* e = engines[i];
+    DS_TRY(dsb::ensure_log(e, e->queued + steps));
+    DS_TRY(dsb::fused_args(e, steps, e->master != nullptr, a[i]));
+    tm[i] = e->tm_shard;
+    if (i) {  // the launch (on engine 0's stream) follows every engine's queued work
+      DS_CUDA_TRY(cudaEventRecord(ev, e->stream));
+      DS_CUDA_TRY(cudaStreamWaitEvent(e0->stream, ev, 0));
+    }
+  }
+  DS_TRY(dsb::launch_tc_group(a.data(), tm.data(), n, e0->tc_nc, e0->stream));
+  DS_CUDA_TRY(cudaEventRecord(ev, e0->stream));
+  for (uint32_t i = 0; i < n; ++i) {
+    ds_engine* e = engines[i];
+    if (i) DS_CUDA_TRY(cudaStreamWaitEvent(e->stream, ev, 0));  // later work on each engine's stream
+    e->launches += 1;
+    e->cur ^= static_cast<int>(steps & 1);
+    if (!e->hp.adaptive) {
+      const uint64_t total = e->host_since + steps;
+      e->host_exchanges += total / e->hp.tau;
+      e->host_since = static_cast<uint32_t>(total % e->hp.tau);
+    }
+    e->queued += steps;
+  }
+  return DS_OK;
+}
+
 namespace {
 int engine_error(ds_engine* e) {
   dsb::DevState s;
@@ -1040,6 +1100,14 @@ extern "C" int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss
   if (!e->fused || e->model.hidden.size() != 1 || (e->model.n_features % 4) != 0)
     return set_error(DS_E_CONTRACT, "engine_stream: needs the fused one-hidden-layer engine and n_features %% 4 == 0");
   if (e->hp.adaptive) return set_error(DS_E_CONTRACT, "engine_stream: fixed-period policy only");
+  if (loss_host) {  // the kernel stores into it directly: it must be mapped (pinned) host memory
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, loss_host) != cudaSuccess || pa.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      return set_error(DS_E_CONTRACT, "engine_stream: loss_host must be pinned host memory (cudaHostAlloc / "
+                       "cudaHostRegister), the kernel writes it directly");
+    }
+  }
   if (steps == 0) return DS_OK;
   dsb::DeviceScope ds(e->device);
   const uint64_t B = e->hp.batch_size, F = e->model.n_features, K = ds_engine::kRing;

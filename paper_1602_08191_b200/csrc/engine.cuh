@@ -85,6 +85,8 @@ int tc_supported(const ModelInfo& m, uint32_t batch, int device, const char** wh
 int tc_cluster(const ModelInfo& m);
 size_t tc_smem_bytes(const ModelInfo& m, uint32_t batch);
 int launch_tc(const FusedArgs& a, int nc, const CUtensorMap& batch_rows, cudaStream_t s);
+// n workers (engines) in one cooperative launch, one cluster each (n <= 8)
+int launch_tc_group(const FusedArgs* a, const CUtensorMap* batch_rows, uint32_t n, int nc, cudaStream_t s);
 // the tensor-core step reads batches as bf16 rows of tc_pitch(F) elements through a TMA map
 uint32_t tc_pitch(uint32_t F);
 int tc_rows_to_bf16(const float* src, uint64_t rows, uint32_t F, void* dst, cudaStream_t s);

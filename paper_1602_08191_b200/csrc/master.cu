@@ -187,7 +187,8 @@ struct IpcRecord {
   cudaIpcMemHandle_t flags;
   uint64_t dim, slice_len, begin, end;
   int32_t rank, world, device, pid;
-  uint8_t pad[DS_IPC_RECORD_BYTES - 2 * sizeof(cudaIpcMemHandle_t) - 4 * 8 - 4 * 4];
+  uint64_t mem_ptr, flags_ptr;  // same-process peers (shards of one GPU) use these directly
+  uint8_t pad[DS_IPC_RECORD_BYTES - 2 * sizeof(cudaIpcMemHandle_t) - 6 * 8 - 4 * 4];
 };
 static_assert(sizeof(IpcRecord) == DS_IPC_RECORD_BYTES, "IPC record size");
 
@@ -278,6 +279,8 @@ extern "C" int ds_master_export(ds_master* m, void* record_out) {
   r.world = m->world;
   r.device = m->device;
   r.pid = static_cast<int32_t>(getpid());
+  r.mem_ptr = reinterpret_cast<uint64_t>(m->local);
+  r.flags_ptr = reinterpret_cast<uint64_t>(m->flags);
   std::memcpy(record_out, &r, sizeof(r));
   return DS_OK;
 }
@@ -300,10 +303,26 @@ extern "C" int ds_master_attach(ds_master* m, const void* records) {
     }
     void* pm = nullptr;
     void* pf = nullptr;
-    DS_CUDA_TRY(cudaIpcOpenMemHandle(&pm, r.mem, cudaIpcMemLazyEnablePeerAccess));
-    DS_CUDA_TRY(cudaIpcOpenMemHandle(&pf, r.flags, cudaIpcMemLazyEnablePeerAccess));
-    m->peer_mem[k] = pm;
-    m->peer_flags[k] = pf;
+    if (r.pid == static_cast<int32_t>(getpid())) {
+      // a shard of this process (several ranks emulated in one process): plain pointers;
+      // CUDA IPC handles cannot be opened by the process that exported them
+      pm = reinterpret_cast<void*>(r.mem_ptr);
+      pf = reinterpret_cast<void*>(r.flags_ptr);
+      if (r.device != m->device) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, m->device, r.device);
+        if (!can) return dsb::set_error(DS_E_CUDA, "master_attach: no peer access from device %d to %d", m->device, r.device);
+        const cudaError_t pe = cudaDeviceEnablePeerAccess(r.device, 0);
+        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+          return dsb::set_error(DS_E_CUDA, "master_attach: %s", cudaGetErrorString(pe));
+        cudaGetLastError();
+      }
+    } else {
+      DS_CUDA_TRY(cudaIpcOpenMemHandle(&pm, r.mem, cudaIpcMemLazyEnablePeerAccess));
+      DS_CUDA_TRY(cudaIpcOpenMemHandle(&pf, r.flags, cudaIpcMemLazyEnablePeerAccess));
+      m->peer_mem[k] = pm;  // opened here: closed by destroy
+      m->peer_flags[k] = pf;
+    }
     m->table.ptr[k] = static_cast<float*>(pm);
     m->table.flags[k] = static_cast<dsb::ShardFlags*>(pf);
   }

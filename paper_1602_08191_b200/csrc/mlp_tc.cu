@@ -282,6 +282,13 @@ __device__ __forceinline__ void tstamp_m(unsigned long long* prof, uint64_t step
 #endif
 
 
+constexpr int kMaxGroup = 8;  // workers per launch
+struct TcLaunch {
+  CUtensorMap maps[kMaxGroup];  // batch-row maps (64-byte aligned, first)
+  FusedArgs args[kMaxGroup];
+  uint32_t n;
+};
+
 struct PolicyTc {
   double cum, cut;
   uint32_t tau, since, fire, period;
@@ -302,13 +309,20 @@ __device__ __forceinline__ bool mbar_wait_or_quit(uint64_t* b, uint32_t parity, 
   }
 }
 
-__global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(FusedArgs A, const __grid_constant__ CUtensorMap tmx) {
+// One launch trains `n` workers (engines), one cluster each: worker w = cluster w. All
+// clusters are co-resident (cooperative launch when n > 1), so workers may wait on each
+// other's exchange tickets inside the kernel (the deterministic multi-worker schedule).
+__global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ TcLaunch P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // dynamic smem base must be 1 KB aligned for SWIZZLE_128B tiles
   unsigned char* sm = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
+  uint32_t NC;  // CTAs per worker = cluster size
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(NC));
+  const uint32_t wid = blockIdx.x / NC;
+  const FusedArgs& A = P.args[wid];
+  const CUtensorMap& tmx = P.maps[wid];
   const uint32_t F = A.F, H = A.H, C = A.C, B = A.B;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t NC = gridDim.x;  // = cluster size
   const TcSmem L = tc_smem(F, B, C, NC);
   const TcMsg M = tc_msg(B, C, NC);
   const uint32_t rank = cluster_rank();
@@ -1110,26 +1124,43 @@ int tc_make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t F) {
   return DS_OK;
 }
 
-int launch_tc(const FusedArgs& a, int nc, const CUtensorMap& tm, cudaStream_t s) {
+int launch_tc_group(const FusedArgs* a, const CUtensorMap* tm, uint32_t n, int nc, cudaStream_t s) {
   if (nc < 1 || nc > kMaxNC) return set_error(DS_E_CONTRACT, "tc: cluster size %d", nc);
-  const size_t smem = tc_smem(a.F, a.B, a.C, static_cast<uint32_t>(nc)).total + 1024;
+  if (n < 1 || n > static_cast<uint32_t>(kMaxGroup)) return set_error(DS_E_CONTRACT, "tc: %u workers per launch (1..%d)", n, kMaxGroup);
+  const size_t smem = tc_smem(a[0].F, a[0].B, a[0].C, static_cast<uint32_t>(nc)).total + 1024;
   DS_CUDA_TRY(cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   if (nc > 8) DS_CUDA_TRY(cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  static TcLaunch P;  // ~5 KB: kernel parameter, copied at launch
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  for (uint32_t i = 0; i < n; ++i) P.maps[i] = tm[i], P.args[i] = a[i];
+  P.n = n;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nc);
+  cfg.gridDim = dim3(n * nc);
   cfg.blockDim = dim3(kTT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = nc;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;  // every worker resident: workers wait on each other's tickets
+  at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
-  FusedArgs args = a;
-  DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, mlp_tc_kernel, args, tm));
+  cfg.numAttrs = n > 1 ? 2 : 1;
+  if (n > 1) {
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, mlp_tc_kernel, &cfg) == cudaSuccess && nclusters < static_cast<int>(n))
+      return set_error(DS_E_CONTRACT, "tc: %u workers of %d CTAs do not fit on the GPU at once (max %d)", n, nc, nclusters);
+    cudaGetLastError();
+  }
+  DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, mlp_tc_kernel, P));
   return DS_OK;
+}
+
+int launch_tc(const FusedArgs& a, int nc, const CUtensorMap& tm, cudaStream_t s) {
+  return launch_tc_group(&a, &tm, 1, nc, s);
 }
 
 }  // namespace dsb
