@@ -1,17 +1,25 @@
 #!/usr/bin/env python3
 """bench.py — throughput of the B200 EASGD hot path (BASELINE.json metric).
 
-Workload (config 1 shapes, one worker per GPU): MLP 784-256-10 (tanh), batch 32 per
-worker, async EASGD with tau=10, alpha=0.1, eta=0.05, on synthetic MNIST-shaped data
-made by the reference's own generator (gen_synthetic N=60000, sep 0.1, sigma 1.0; each
-GPU draws its own partition with seed 1+rank, the holdout split of the reference's
-simulator is removed, 48,000 rows = 150 MB stay resident per GPU, larger than L2).
+Workload (BASELINE config 1): MLP 784-256-10 (tanh), EASGD with tau=10, alpha=0.1,
+eta=0.05, batch 32 per worker, TWO workers per GPU (config 1's worker count), async
+LockFree exchanges with the center (sharded over the GPUs when N > 1), on synthetic
+MNIST-shaped data made by the reference's own generator (gen_synthetic N=60000, sep 0.1,
+sigma 1.0, seed 1+rank; the simulator's holdout split removed; the GPU's 48,000 rows are
+partitioned between its workers: 150 MB f32 + 75 MB bf16 resident, larger than L2).
 
-A "step" is one local SGD iteration on every GPU; every tau-th step also performs the
-elastic exchange with the center, which is sharded over all GPUs (LockFree, in-kernel
-P2P read-modify-write over NVLink). value = all samples processed / max-over-ranks
-device time. e2e = the same loop through the C-ABI with host buffers: every step
-copies its gathered batch from pinned host memory and reads the batch loss back.
+The headline step is the tensor-core fast step (DS_ENGINE_TC, csrc/mlp_tc.cu): both
+workers of a GPU train in ONE launch, one thread-block cluster each; the FC contractions
+run on tcgen05 (bf16 operands, tf32 logits, f32 accumulation) -- a stated-tolerance mode
+(tests/test_gpu_tc.py). The reference's exact f64 order (DS_ENGINE_FUSED, one worker per
+GPU) is measured beside it as "f64_exact".
+
+A "step" is one local SGD iteration of every worker; every tau-th step also performs the
+elastic exchange. value = all samples processed / max-over-ranks device time. The K-step
+launch is repeated until the device window is >= 200 ms ("repeats"). e2e = the same
+training through the C-ABI with HOST buffers (stream mode): every step of every worker
+gathers its batch on the host, copies it H2D from pinned memory, and the kernel writes the
+step's loss to mapped host memory (D2H).
 
   python bench.py [--gpus N --steps K --warmup W]          # our B200 arm
   python bench.py --impl reference [...]                   # the reference CPU arm
@@ -48,6 +56,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--tau", type=int, default=10)
+    ap.add_argument("--workers", type=int, default=2, help="EASGD workers per GPU (BASELINE config 1: 2)")
+    ap.add_argument("--min-window-ms", type=float, default=200.0, help="repeat the K-step launch up to this")
     ap.add_argument("--e2e-steps", type=int, default=2000)
     ap.add_argument("--exchange-params", type=int, default=256 * 1024 * 1024)
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / exchange sweep / cpu baseline (profiling)")
@@ -65,12 +75,16 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def worker_data(rank, api):
-    """Rank's synthetic partition: gen_synthetic (seed 1+rank) minus the simulator's holdout."""
+def worker_data(rank, api, workers=1):
+    """Rank's synthetic rows (gen_synthetic seed 1+rank, minus the simulator's holdout),
+    partitioned between the GPU's `workers` workers (contiguous blocks)."""
     X, y = api.gen_synthetic(N_SAMPLES, F, NCLS, SEP, SIGMA, 1 + rank)
     order, nh = api.split_holdout_order(N_SAMPLES, 0.2, api.mix_seed(DATA_SEED, 0x484f4c44))
     tr = order[nh:]
-    return np.ascontiguousarray(X[tr]), np.ascontiguousarray(y[tr])
+    Xr, yr = X[tr], y[tr]
+    n = len(yr) // workers
+    return [(np.ascontiguousarray(Xr[k * n:(k + 1) * n]), np.ascontiguousarray(yr[k * n:(k + 1) * n]))
+            for k in range(workers)]
 
 
 class ClockSampler:
@@ -137,10 +151,10 @@ def run_reference(args):
     from oracle.oracle import Oracle, ModelSpec, Hyper, available
     kind = "reference" if available("dsref") else "port"
     orc = Oracle("dsref" if kind == "reference" else "dso")
-    n = max(1, args.gpus)
+    n = max(1, args.gpus) * args.workers  # this arm's workers: `workers` per GPU
     m = ModelSpec.mlp(F, [H], NCLS)
     hp = Hyper(eta=0.05, alpha=0.1, tau=args.tau, batch_size=args.batch, i_max=10 ** 9)
-    shards = [worker_data(k, orc) for k in range(n)]
+    shards = [sh for g in range(max(1, args.gpus)) for sh in worker_data(g, orc, args.workers)]
     init = orc.init_params(m, INIT_SEED)
     if kind == "reference":
         probe = orc.workers_time(m, shards, NCLS, hp, init, True, 1, 5)  # calibrate: ~5 steps
@@ -172,12 +186,12 @@ def run_reference(args):
             all_cores = {"workers": W, "value": W * args.batch * steps_w / secs_w, "unit": "samples/s",
                          "steps": steps_w,
                          "note": "reference n-worker loop, one thread per host core, LockFree in-process "
-                                 "MasterState; not this arm's config (one worker per GPU)"}
+                                 "MasterState; not this arm's config (workers per GPU x GPUs)"}
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": steps,
             "warmup": warm, "ms_per_step": 1000.0 * secs / steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference gen_synthetic, per-worker seeds)",
             "impl": "reference",
-            "config": config_block(args, n),
+            "config": config_block(args, max(1, args.gpus)),
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": n, "kind": kind,
                              "sample": f"{steps} timed iterations per worker x {n} worker thread(s) "
                                        f"(+{warm} warmup), LockFree in-process MasterState, tau={args.tau}"},
@@ -189,14 +203,76 @@ def run_reference(args):
 
 
 def config_block(args, n):
-    return {"workload": "mlp784-256-10 async EASGD (BASELINE config 1 shapes, one worker per GPU)",
-            "model": "mlp:784:256:10 (tanh hidden, softmax CE)", "global_batch": args.batch * n,
+    w = args.workers * n
+    return {"workload": f"mlp784-256-10 EASGD, BASELINE config 1 ({args.workers} workers per GPU, async LockFree)",
+            "model": "mlp:784:256:10 (tanh hidden, softmax CE)", "global_batch": args.batch * w,
             "batch_per_worker": args.batch, "seq_len": None, "tau": args.tau, "alpha": 0.1, "eta": 0.05,
-            "workers": n, "parallelism": f"easgd-dp{n}",
+            "workers": w, "workers_per_gpu": args.workers, "parallelism": f"easgd-dp{w} ({args.workers} per GPU)",
             "exchange": "LockFree, center sharded over the GPUs, in-kernel P2P RMW" if n > 1 else
                         "LockFree, center on the same GPU, in-kernel",
-            "l2_policy": "inputs larger than L2: 48,000-row (150 MB) shard per GPU, random batches",
-            "numerics": "f64 accumulation in the reference's summation order, f32 params"}
+            "l2_policy": "inputs larger than L2: 48,000 rows per GPU (150 MB f32 + 75 MB bf16 copy), random batches",
+            "numerics": "tensor-core step: bf16 operands (forward, weight gradient), tf32 logits, f32 accumulation "
+                        "and parameters (stated tolerance, tests/test_gpu_tc.py); f64_exact: the reference's f64 order"}
+
+
+def make_master(L, dist, local, rank, world, P, init_ptr, mode):
+    master = C.c_void_p()
+    if world == 1:
+        L.check(L.lib.ds_master_create(C.byref(master), local, P, C.c_float(0.1), mode, C.c_void_p(init_ptr)))
+    else:
+        L.check(L.lib.ds_master_create_sharded(C.byref(master), local, P, C.c_float(0.1), mode, rank, world,
+                                               C.c_void_p(init_ptr)))
+        rec = (C.c_uint8 * L.DS_IPC_RECORD_BYTES)()
+        L.check(L.lib.ds_master_export(master, rec))
+        recs = [None] * world
+        dist.all_gather_object(recs, bytes(rec))
+        allrec = (C.c_uint8 * (L.DS_IPC_RECORD_BYTES * world)).from_buffer_copy(b"".join(recs))
+        L.check(L.lib.ds_master_attach(master, allrec))
+        dist.barrier()
+    return master
+
+
+def timed_runs(L, run, engines, stream, K, min_ms, clk_index, world, dist, torch):
+    """K-step launches, repeated until the device window reaches min_ms; CUDA events on the
+    launching stream, max over ranks. Returns (ms, repeats, launches, clocks)."""
+    e0 = engines[0]
+    for e in engines:  # TrainLog / plan room for the probe and every repeat: nothing allocated while timed
+        L.check(L.lib.ds_engine_reserve(e, K + 8))
+    probe = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    probe[0].record(stream)
+    run(K)
+    probe[1].record(stream)
+    for e in engines:
+        L.check(L.lib.ds_engine_sync(e))
+    torch.cuda.synchronize()
+    per = max(probe[0].elapsed_time(probe[1]), 1e-3)
+    reps = torch.tensor([max(1, min(4096, int(np.ceil(min_ms / per))))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(reps, op=dist.ReduceOp.MAX)
+    R = int(reps.item())
+    for e in engines:
+        L.check(L.lib.ds_engine_reserve(e, (R + 1) * K + 8))
+    n0 = C.c_uint64()
+    L.check(L.lib.ds_engine_launches(e0, C.byref(n0)))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(clk_index) as clk:
+        ev0.record(stream)
+        for _ in range(R):
+            run(K)
+        ev1.record(stream)
+        for e in engines:
+            L.check(L.lib.ds_engine_sync(e))
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    n1 = C.c_uint64()
+    L.check(L.lib.ds_engine_launches(e0, C.byref(n1)))
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item(), R, int(n1.value - n0.value), clk.summary()
 
 
 def main():
@@ -216,11 +292,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     api = DeepSpark()
-    n = world
+    n, Wk = world, args.workers
     hbm, bf16, bf16_sus, peak_kind = peaks()
 
-    # ---- data, init (NCCL broadcast), master, engine --------------------------------
-    X, y = worker_data(rank, api)
+    # ---- data, init (NCCL broadcast), center, engines -------------------------------
+    shards = worker_data(rank, api, Wk)
     P = (H * F + H) + (NCLS * H + NCLS)
     init = torch.empty(P, dtype=torch.float32, device="cuda")
     if rank == 0:
@@ -229,87 +305,71 @@ def main():
     if world > 1:
         dist.broadcast(init, 0)  # replaces FETCH_INIT (exchanger.cpp:266-270)
     torch.cuda.synchronize()
-
-    master = C.c_void_p()
-    if world == 1:
-        L.check(L.lib.ds_master_create(C.byref(master), local, P, C.c_float(0.1), L.DS_MODE_LOCKFREE,
-                                       C.c_void_p(init.data_ptr())))
-    else:
-        L.check(L.lib.ds_master_create_sharded(C.byref(master), local, P, C.c_float(0.1), L.DS_MODE_LOCKFREE,
-                                               rank, world, C.c_void_p(init.data_ptr())))
-        rec = (C.c_uint8 * L.DS_IPC_RECORD_BYTES)()
-        L.check(L.lib.ds_master_export(master, rec))
-        recs = [None] * world
-        dist.all_gather_object(recs, bytes(rec))
-        allrec = (C.c_uint8 * (L.DS_IPC_RECORD_BYTES * world)).from_buffer_copy(b"".join(recs))
-        L.check(L.lib.ds_master_attach(master, allrec))
-        dist.barrier()
+    master = make_master(L, dist, local, rank, world, P, init.data_ptr(), L.DS_MODE_LOCKFREE)
 
     hidden = (C.c_uint32 * 1)(H)
     desc = L.ds_model_desc(1, F, NCLS, 1, hidden)
     hp = L.ds_hyper(0.05, 0.1, args.tau, args.batch, 10 ** 9, 0.0, 0.0, 0)
-    sweep_seed = api.mix_seed(api.mix_seed(DATA_SEED, 0x53574550), rank)
-    eng = C.c_void_p()
-    L.check(L.lib.ds_engine_create(C.byref(eng), local, C.byref(desc), X.ctypes.data, y.ctypes.data, len(y), NCLS,
-                                   C.byref(hp), sweep_seed, C.c_void_p(init.data_ptr()), L.DS_ENGINE_AUTO))
-    L.check(L.lib.ds_engine_attach_master(eng, master))
+    seeds = [api.mix_seed(api.mix_seed(DATA_SEED, 0x53574550), rank * Wk + k) for k in range(Wk)]
+    engines = []
+    for k, (Xk, yk) in enumerate(shards):
+        e = C.c_void_p()
+        L.check(L.lib.ds_engine_create(C.byref(e), local, C.byref(desc), Xk.ctypes.data, yk.ctypes.data, len(yk),
+                                       NCLS, C.byref(hp), seeds[k], C.c_void_p(init.data_ptr()), L.DS_ENGINE_TC))
+        L.check(L.lib.ds_engine_attach_master(e, master))
+        engines.append(e)
+    arr = (C.c_void_p * Wk)(*[e.value for e in engines])
     sptr = C.c_void_p()
-    L.check(L.lib.ds_engine_stream(eng, C.byref(sptr)))
+    L.check(L.lib.ds_engine_stream(engines[0], C.byref(sptr)))
     stream = torch.cuda.ExternalStream(sptr.value)
 
-    # ---- warmup, then K timed steps in one device run -----------------------------------
-    W, K = max(3, args.warmup), args.steps
-    L.check(L.lib.ds_engine_reserve(eng, W + K))  # no allocation inside the timed region
-    L.check(L.lib.ds_engine_run(eng, W, 0, None))
-    L.check(L.lib.ds_engine_sync(eng))
-    launches0 = C.c_uint64()
-    L.check(L.lib.ds_engine_launches(eng, C.byref(launches0)))
+    def run_group(steps):
+        L.check(L.lib.ds_engine_run_group(arr, Wk, steps))
+
+    # ---- warmup, then the K-step group launch (repeated to a >= 200 ms window) ----------
+    Wu, K = max(3, args.warmup), args.steps
+    run_group(Wu)
+    for e in engines:
+        L.check(L.lib.ds_engine_sync(e))
+    ms, R, launches, clocks = timed_runs(L, run_group, engines, stream, K, args.min_window_ms, local, world, dist,
+                                         torch)
+    steps_done = K * R
+    value = n * Wk * args.batch * steps_done / (ms / 1e3)
+
+    # roofline of the only kernel of the timed region: mlp_tc_kernel. Algorithmic FLOPs:
+    # 818,176 per sample (fwd 203,264 MAC + dW 203,264 MAC + dX 2,560 MAC) x batch x workers x steps
+    flop = FLOP_PER_SAMPLE * args.batch * Wk * steps_done
+    achieved = flop / (ms / 1e3) / 1e12
+    peak, pk = (bf16, "burst") if ms < 1000.0 else (bf16_sus, "sustained")
+    # per worker and step the tensor pipe runs 49 forward MMAs (M64 N16 K16 bf16) + 2 logits MMAs
+    # (M64 N16 K8 tf32) + 14 weight-gradient MMAs (M128 N16 K16 bf16) on each of the cluster's CTAs
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "peak_kind": f"{peak_kind} bf16 dense, {pk} (device window {ms:.0f} ms)",
+            "kernel": "mlp_tc_kernel (one cluster of 16 CTAs per worker: TMA gather4 multicast batches, tcgen05 "
+                      "forward / logits / weight gradient, SGD from TMEM, policy, in-kernel exchange)",
+            "algorithmic": f"{FLOP_PER_SAMPLE} FLOP/sample x {args.batch} x {Wk} workers x {steps_done} steps",
+            "mma_per_cta_step": {"forward_bf16_m64n16k16": 49, "logits_tf32_m64n16k8": 2,
+                                 "weight_grad_bf16_m128n16k16": 14},
+            "sms_used": 16 * Wk,
+            "note": "latency-bound: 26 MFLOP per 32-sample step spread over 16 SMs per worker; each small "
+                    "tcgen05.mma costs ~55 cycles regardless of N (profiles/r02_umma_timing.md), plus two "
+                    "DSMEM phases per step"}
+
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n, "steps": K, "warmup": Wu,
+            "repeats": R, "ms_per_step": ms / steps_done, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference gen_synthetic, per-GPU seeds, partitioned between the GPU's workers)",
+            "config": config_block(args, n), "roofline": roof, "clocks": clocks, "gpu_launches": launches}
+    if not args.no_extras:
+        line["e2e"] = e2e_group_leg(args, L, api, engines, shards, seeds, rank, world, n)
+    for e in engines:
+        L.lib.ds_engine_destroy(e)
     if world > 1:
         dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        L.check(L.lib.ds_engine_run(eng, K, 0, None))
-        ev1.record(stream)
-        L.check(L.lib.ds_engine_sync(eng))
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    launches1 = C.c_uint64()
-    L.check(L.lib.ds_engine_launches(eng, C.byref(launches1)))
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = t.item()
-    value = n * args.batch * K / (ms_max / 1e3)
-
-    # roofline of the dominant (and only) kernel of the timed region: the fused step
-    flop_launch = FLOP_PER_SAMPLE * args.batch * K
-    achieved = flop_launch / (ms / 1e3) / 1e12
-    # The launch is the only kernel of the timed region. Its contract bound is reported
-    # against the tensor peak (FLOPs), but the path is exact-order f64 on CUDA cores, so
-    # the binding roofline is the FP64 pipe: 148 SMs x 64 DADD/DMUL lanes per clock.
-    sm_clk = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
-    fp64_peak = 148 * 64 * sm_clk / 1e12  # TFLOP/s (one op per DADD/DMUL lane)
-    traffic = 32 * 3136 * K  # ncu dram bytes per launch = the X rows (profiles/r01_fused_kernel_ncu.md)
-    roof = {"bound": "tensor", "achieved": achieved, "peak": bf16_sus, "unit": "TFLOP/s", "frac": achieved / bf16_sus,
-            "traffic": traffic, "peak_kind": f"{peak_kind} bf16 dense, sustained",
-            "kernel": "mlp_kernel (persistent: forward, softmax-CE, backward, SGD, policy, exchange)",
-            "algorithmic": f"{FLOP_PER_SAMPLE} FLOP/sample x {args.batch} x {K} steps per launch",
-            "fp64_pipe": {"achieved_tflops": achieved, "peak_tflops": fp64_peak, "frac": achieved / fp64_peak,
-                          "note": "the reference's sequential f64 order (bit parity) keeps every FLOP on the FP64 "
-                                  "pipe; ncu: FP64 pipe active 12.5% of elapsed, 1 grid barrier per step"},
-            "note": "latency-bound f64 CUDA-core chains (784-long dependent DADD chains per hidden unit), "
-                    "not a tensor-core kernel; traffic = X rows only (22.5 MB DRAM read per 200-step launch)"}
-
-    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n, "steps": K, "warmup": W,
-            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (reference gen_synthetic, per-GPU seeds)",
-            "config": config_block(args, n), "roofline": roof, "clocks": clk.summary(),
-            "gpu_launches": int(launches1.value - launches0.value)}
-
+    L.lib.ds_master_destroy(master)
     if not args.no_extras:
-        line["e2e"] = e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n)
+        line["f64_exact"] = f64_leg(args, L, api, torch, dist, world, rank, local, shards, init)
+        line["packed"] = packed_leg(args, L, api, torch, dist, world, rank, local, init)
         line["exchange"] = exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind)
     if args.cifar_steps > 0:
         line["cifar10_quick"] = cifar_leg(args, L, api, torch, dist, world, rank, local)
@@ -317,13 +377,8 @@ def main():
                                          for k in ("sync", "adaptive")}
     if args.alexnet_steps > 0:
         line["alexnet"] = alexnet_leg(args, L, api, torch, dist, world, rank, local)
-    if not args.no_extras:
-        if rank == 0 and world == 1:
-            line["cpu_baseline"] = cpu_baseline(args, X, y)
-    L.lib.ds_engine_destroy(eng)
-    if world > 1:
-        dist.barrier()
-    L.lib.ds_master_destroy(master)
+    if not args.no_extras and rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args, shards)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -331,50 +386,145 @@ def main():
     return 0
 
 
-def e2e_leg(args, L, api, eng, X, y, rank, world, sweep_seed, n):
-    """Same training through the C-ABI with HOST buffers (stream mode): one persistent
-    launch consumes batches the host gathers (the reference's ShardSweeper order) into
-    pinned memory and pushes as H2D copies while the device trains; the kernel writes
-    every step's batch loss to mapped pinned host memory (D2H). Host gather, H2D and
-    the device step overlap. Timed by wall clock from stream_begin to stream_end."""
+def f64_leg(args, L, api, torch, dist, world, rank, local, shards, init):
+    """The reference's exact f64 order (DS_ENGINE_FUSED: one persistent cooperative launch
+    per GPU, bit-identical to the reference), one worker per GPU (the GPU's first shard)."""
+    P = init.numel()
+    master = make_master(L, dist, local, rank, world, P, init.data_ptr(), L.DS_MODE_LOCKFREE)
+    hidden = (C.c_uint32 * 1)(H)
+    desc = L.ds_model_desc(1, F, NCLS, 1, hidden)
+    hp = L.ds_hyper(0.05, 0.1, args.tau, args.batch, 10 ** 9, 0.0, 0.0, 0)
+    Xk, yk = shards[0]
+    e = C.c_void_p()
+    L.check(L.lib.ds_engine_create(C.byref(e), local, C.byref(desc), Xk.ctypes.data, yk.ctypes.data, len(yk), NCLS,
+                                   C.byref(hp), api.mix_seed(9, rank), C.c_void_p(init.data_ptr()), L.DS_ENGINE_FUSED))
+    L.check(L.lib.ds_engine_attach_master(e, master))
+    sp = C.c_void_p()
+    L.check(L.lib.ds_engine_stream(e, C.byref(sp)))
+    st = torch.cuda.ExternalStream(sp.value)
+    L.check(L.lib.ds_engine_run(e, 10, 0, None))
+    L.check(L.lib.ds_engine_sync(e))
+    ms, R, launches, clocks = timed_runs(L, lambda k: L.check(L.lib.ds_engine_run(e, k, 0, None)), [e], st,
+                                         args.steps, args.min_window_ms, local, world, dist, torch)
+    L.lib.ds_engine_destroy(e)
+    if world > 1:
+        dist.barrier()
+    L.lib.ds_master_destroy(master)
+    steps = args.steps * R
+    achieved = FLOP_PER_SAMPLE * args.batch * steps / (ms / 1e3) / 1e12
+    sm_clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    fp64_peak = 148 * 64 * sm_clk / 1e12
+    return {"metric": METRIC, "value": world * args.batch * steps / (ms / 1e3), "unit": "samples/s",
+            "ms_per_step": ms / steps, "steps": args.steps, "repeats": R, "workers_per_gpu": 1, "dtype": "f64",
+            "gpu_launches": launches, "clocks": clocks,
+            "numerics": "the reference's f64 summation order: bit-identical trajectories (tests/test_gpu_engine.py)",
+            "kernel": "mlp_kernel (persistent cooperative, 128 CTAs, one grid barrier per step)",
+            "fp64_pipe": {"achieved_tflops": achieved, "peak_tflops": fp64_peak, "frac": achieved / fp64_peak}}
+
+
+def packed_leg(args, L, api, torch, dist, world, rank, local, init):
+    """As many concurrent workers as one launch holds (clusters of 16 CTAs co-resident on
+    the GPU): the GPU's aggregate tensor-core throughput at config 1's shapes."""
+    from paper_1602_08191_b200.deepspark import DeepSpark  # noqa: F401
+    Wp = 7
+    shards = worker_data(rank, api, Wp)
+    P = init.numel()
+    master = make_master(L, dist, local, rank, world, P, init.data_ptr(), L.DS_MODE_LOCKFREE)
+    hidden = (C.c_uint32 * 1)(H)
+    desc = L.ds_model_desc(1, F, NCLS, 1, hidden)
+    hp = L.ds_hyper(0.05, 0.1, args.tau, args.batch, 10 ** 9, 0.0, 0.0, 0)
+    engines = []
+    for k, (Xk, yk) in enumerate(shards):
+        e = C.c_void_p()
+        L.check(L.lib.ds_engine_create(C.byref(e), local, C.byref(desc), Xk.ctypes.data, yk.ctypes.data, len(yk),
+                                       NCLS, C.byref(hp), api.mix_seed(17, rank * Wp + k), C.c_void_p(init.data_ptr()),
+                                       L.DS_ENGINE_TC))
+        L.check(L.lib.ds_engine_attach_master(e, master))
+        engines.append(e)
+    arr = (C.c_void_p * Wp)(*[e.value for e in engines])
+    sp = C.c_void_p()
+    L.check(L.lib.ds_engine_stream(engines[0], C.byref(sp)))
+    st = torch.cuda.ExternalStream(sp.value)
+    out = {}
+    try:
+        L.check(L.lib.ds_engine_run_group(arr, Wp, 10))
+        ms, R, launches, clocks = timed_runs(L, lambda k: L.check(L.lib.ds_engine_run_group(arr, Wp, k)), engines, st,
+                                             args.steps, args.min_window_ms, local, world, dist, torch)
+        steps = args.steps * R
+        out = {"value": world * Wp * args.batch * steps / (ms / 1e3), "unit": "samples/s",
+               "workers_per_gpu": Wp, "ms_per_step": ms / steps, "steps": args.steps, "repeats": R,
+               "gpu_launches": launches, "clocks": clocks,
+               "note": "not config 1's worker count: the most 16-CTA clusters one B200 co-schedules"}
+    except Exception as ex:  # the GPU may not co-schedule 7 clusters of 16
+        out = {"unavailable": str(ex)}
+    for e in engines:
+        L.lib.ds_engine_destroy(e)
+    if world > 1:
+        dist.barrier()
+    L.lib.ds_master_destroy(master)
+    return out
+
+
+def e2e_group_leg(args, L, api, engines, shards, seeds, rank, world, n):
+    """The same training through the C-ABI with HOST buffers (stream mode): one launch
+    trains the GPU's workers while the host, per worker, runs the reference worker's
+    ShardSweeper (the epoch permutations are computed inside the timed window), gathers
+    each batch from the host shard into a pinned ring slot and pushes it (H2D) -- one host
+    thread per worker; the kernel writes every step's loss to mapped pinned host memory
+    (D2H). Wall clock from stream_begin to the last stream_end, max over ranks."""
     import torch
     import torch.distributed as dist
-    K = min(args.e2e_steps, args.steps)
-    B = args.batch
-    idx, sizes = api.sweep_batches(len(y), B, sweep_seed + 1, K)
-    idx = np.ascontiguousarray(idx, dtype=np.uint32)
-    Xh = np.ascontiguousarray(X, dtype=np.float32)
-    yh = np.ascontiguousarray(y, dtype=np.uint32)
-    losses = torch.zeros(K, dtype=torch.float64, pin_memory=True)
-    push = L.lib.ds_engine_stream_push_rows
-    xp, yp = C.c_void_p(Xh.ctypes.data), C.c_void_p(yh.ctypes.data)
-    row_ptr = [C.c_void_p(idx[s].ctypes.data) for s in range(K)]
+    K, B, Wk = min(args.e2e_steps, args.steps * 20), args.batch, len(engines)
+    losses = [torch.zeros(K, dtype=torch.float64, pin_memory=True) for _ in range(Wk)]
+    lp = (C.c_void_p * Wk)(*[lo.data_ptr() for lo in losses])
+    arr = (C.c_void_p * Wk)(*[e.value for e in engines])
+    host = [(np.ascontiguousarray(Xk, np.float32), np.ascontiguousarray(yk, np.uint32)) for Xk, yk in shards]
+    errs = []
 
-    def stream_run(steps):
-        # the host side of the reference worker loop: ShardSweeper order (precomputed above),
-        # gather_batch into the engine's pinned ring slot and push (ds_engine_stream_push_rows)
-        L.check(L.lib.ds_engine_stream_begin(eng, steps, C.c_void_p(losses.data_ptr())))
-        for s in range(steps):
-            L.check(push(eng, xp, yp, row_ptr[s], int(sizes[s])))
-        L.check(L.lib.ds_engine_stream_end(eng))
+    def feed(k, steps, seed):
+        try:
+            Xh, yh = host[k]
+            idx, sizes = api.sweep_batches(len(yh), B, seed, steps)  # ShardSweeper, inside the window
+            idx = np.ascontiguousarray(idx, dtype=np.uint32)
+            xp, yp = C.c_void_p(Xh.ctypes.data), C.c_void_p(yh.ctypes.data)
+            push = L.lib.ds_engine_stream_push_rows
+            for s in range(steps):
+                L.check(push(engines[k], xp, yp, C.c_void_p(idx[s].ctypes.data), int(sizes[s])))
+            L.check(L.lib.ds_engine_stream_end(engines[k]))
+        except Exception as ex:  # reported below
+            errs.append(str(ex))
 
-    L.check(L.lib.ds_engine_reserve(eng, min(K, 100) + K))  # TrainLog room: no allocation while timed
-    stream_run(min(K, 100))  # warm-up session: first-touch of the pinned ring, host caches
+    def session(steps, seed_off):
+        L.check(L.lib.ds_engine_stream_begin_group(arr, Wk, steps, lp))
+        th = [threading.Thread(target=feed, args=(k, steps, seeds[k] + seed_off)) for k in range(Wk)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    for e in engines:
+        L.check(L.lib.ds_engine_reserve(e, min(K, 100) + K + 8))
+    session(min(K, 100), 11)  # warm-up session: first touch of the pinned rings, host caches
+    if errs:
+        return {"value": None, "error": errs[0]}
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    stream_run(K)
+    session(K, 12)
     secs = time.perf_counter() - t0
-    ok = bool(np.isfinite(losses.numpy()).all())
+    if errs:
+        return {"value": None, "error": errs[0]}
+    ok = all(bool(np.isfinite(lo.numpy()).all()) for lo in losses)
     t = torch.tensor([secs], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return {"value": n * B * K / t.item(), "unit": "samples/s", "h2d_bytes_per_step": B * F * 4 + B * 4 + 4,
-            "d2h_bytes_per_step": 8, "steps": K, "losses_finite": ok,
-            "path": "ds_engine_stream_*: per step ds_engine_stream_push_rows gathers the batch rows from the "
-                    "host shard into a pinned ring slot and copies it H2D into an 8-slot device ring; one "
-                    "persistent fused launch (step + exchange every tau) consumes it and writes each step's "
-                    "loss to mapped host memory; wall clock from stream_begin to stream_end"}
+    return {"value": n * Wk * B * K / t.item(), "unit": "samples/s",
+            "h2d_bytes_per_step": Wk * (B * F * 4 + B * 4 + 4), "d2h_bytes_per_step": Wk * 8, "steps": K,
+            "losses_finite": ok,
+            "path": "ds_engine_stream_begin_group + per worker ds_engine_stream_push_rows (host ShardSweeper, "
+                    "gather_batch into a pinned ring slot, H2D copy, bf16 conversion on the copy stream) from one "
+                    "host thread per worker; one tensor-core launch trains all of the GPU's workers; per-step losses "
+                    "written to mapped host memory; wall clock from stream_begin to the last stream_end"}
 
 
 def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind):
@@ -636,9 +786,10 @@ def alexnet_leg(args, L, api, torch, dist, world, rank, local):
             "reference_arm": "none: the reference has no conv layers (SURVEY §8 a20)"}
 
 
-def cpu_baseline(args, X, y):
-    """The reference's own SgdEngine loop (oracle/_ref, unmodified) on this box's host,
-    one worker thread, a bounded sample (~15 s) of the same workload."""
+def cpu_baseline(args, shards):
+    """The reference's own n-worker loop (oracle/_ref, unmodified: SgdEngine + ExchangePolicy
+    + an in-process LockFree MasterState, one thread per worker) on this box's host, this
+    arm's workers, a bounded sample (~15 s) of the same workload."""
     try:
         from oracle.oracle import Oracle, ModelSpec, Hyper, available
     except Exception as e:  # pragma: no cover
@@ -648,18 +799,19 @@ def cpu_baseline(args, X, y):
     m = ModelSpec.mlp(F, [H], NCLS)
     hp = Hyper(eta=0.05, alpha=0.1, tau=args.tau, batch_size=args.batch, i_max=10 ** 9)
     init = orc.init_params(m, INIT_SEED)
+    Wk = len(shards)
     if kind == "reference":
-        probe = orc.workers_time(m, [(X, y)], NCLS, hp, init, True, 1, 5)
+        probe = orc.workers_time(m, shards, NCLS, hp, init, True, 1, 5)
         steps = int(max(20, min(2000, 15.0 / max(probe / 5, 1e-4))))
-        secs = orc.workers_time(m, [(X, y)], NCLS, hp, init, True, 3, steps)
+        secs = orc.workers_time(m, shards, NCLS, hp, init, True, 3, steps)
     else:
-        steps = 200
+        Wk, steps = 1, 200
         t0 = time.perf_counter()
-        orc.engine_steps(m, X, y, NCLS, hp, 7, init, steps)
+        orc.engine_steps(m, shards[0][0], shards[0][1], NCLS, hp, 7, init, steps)
         secs = time.perf_counter() - t0
-    return {"value": args.batch * steps / secs, "unit": "samples/s", "cores": 1, "kind": kind,
-            "sample": f"{steps} SgdEngine iterations (b={args.batch}, tau={args.tau} exchanges with an "
-                      f"in-process MasterState) on 1 host core of {os.cpu_count()}"}
+    return {"value": Wk * args.batch * steps / secs, "unit": "samples/s", "cores": Wk, "kind": kind,
+            "sample": f"{steps} iterations per worker x {Wk} worker thread(s) (b={args.batch}, tau={args.tau}, "
+                      f"LockFree in-process MasterState) on {Wk} of {os.cpu_count()} host cores"}
 
 
 if __name__ == "__main__":

@@ -351,6 +351,10 @@ int ds_engine_stream_push(ds_engine* e, const float* X_host, const uint32_t* y_h
 int ds_engine_stream_push_rows(ds_engine* e, const float* X_host, const uint32_t* y_host, const uint32_t* idx,
                                uint32_t rows);
 int ds_engine_stream_end(ds_engine* e);
+/* Stream mode for several tensor-core engines trained in ONE launch (ds_engine_run_group):
+ * each engine gets its own ring, pushes and ds_engine_stream_end as above; loss_host[i]
+ * (pinned, or a NULL array) receives engine i's per-step losses. */
+int ds_engine_stream_begin_group(ds_engine** engines, uint32_t n, uint64_t steps, double** loss_host);
 /* Block until the engine's queued work finished; returns DS_E_NUMERIC/DS_E_CONTRACT
  * if any step hit the reference's error conditions (message names the iteration). */
 int ds_engine_sync(ds_engine* e);

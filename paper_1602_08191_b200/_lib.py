@@ -152,6 +152,7 @@ _sig("ds_engine_attach_master", VP, VP)
 _sig("ds_engine_set_tickets", VP, VP, U64)
 _sig("ds_engine_run", VP, U64, C.c_int, P_U64)
 _sig("ds_engine_run_group", C.POINTER(VP), U32, U64)
+_sig("ds_engine_stream_begin_group", C.POINTER(VP), U32, U64, C.POINTER(VP))
 _sig("ds_engine_reserve", VP, U64)
 _sig("ds_engine_step_host", VP, VP, VP, U32, VP)
 _sig("ds_engine_step_host_async", VP, VP, VP, U32, VP)
@@ -192,7 +193,7 @@ EXPORTED = [
     "ds_master_export", "ds_master_attach", "ds_master_destroy", "ds_master_exchange",
     "ds_master_exchange_ticketed", "ds_master_snapshot", "ds_master_local_slice",
     "ds_master_exchange_count", "ds_master_dim", "ds_master_reset_tickets", "ds_engine_create",
-    "ds_engine_destroy", "ds_engine_attach_master", "ds_engine_set_tickets", "ds_engine_run", "ds_engine_run_group", "ds_engine_reserve", "ds_engine_step_host", "ds_engine_step_host_async",
+    "ds_engine_destroy", "ds_engine_attach_master", "ds_engine_set_tickets", "ds_engine_run", "ds_engine_run_group", "ds_engine_stream_begin_group", "ds_engine_reserve", "ds_engine_step_host", "ds_engine_step_host_async",
     "ds_engine_stream_begin", "ds_engine_stream_push", "ds_engine_stream_push_rows", "ds_engine_stream_end",
     "ds_engine_sync", "ds_engine_stream", "ds_engine_log", "ds_engine_iterations",
     "ds_engine_get_params", "ds_engine_set_params", "ds_engine_params_device", "ds_engine_policy",

@@ -563,6 +563,9 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
 }  // namespace dsb
 
 using dsb::set_error;
+namespace dsb {
+int run_group(ds_engine** engines, uint32_t n, uint64_t steps);
+}
 
 // ds_engine_create / ds_engine_create_from_shard: the shard comes from host arrays, or
 // (shard_path != nullptr) from a DSHD file streamed straight into e->X / e->y.
@@ -873,7 +876,8 @@ extern "C" int ds_engine_run(ds_engine* e, uint64_t steps, int stop_at_exchange,
   return DS_OK;
 }
 
-extern "C" int ds_engine_run_group(ds_engine** engines, uint32_t n, uint64_t steps) {
+namespace dsb {
+int run_group(ds_engine** engines, uint32_t n, uint64_t steps) {
   if (!engines || n == 0) return set_error(DS_E_CONTRACT, "engine_run_group: no engines");
   if (n > 8) return set_error(DS_E_CONTRACT, "engine_run_group: at most 8 engines per launch");
   ds_engine* e0 = engines[0];
@@ -887,7 +891,8 @@ extern "C" int ds_engine_run_group(ds_engine** engines, uint32_t n, uint64_t ste
         e->model.hidden != e0->model.hidden || e->model.n_classes != e0->model.n_classes ||
         e->hp.batch_size != e0->hp.batch_size)
       return set_error(DS_E_CONTRACT, "engine_run_group: engines differ in device, model or batch size");
-    if (e->ring_active || e->hostfed) return set_error(DS_E_STATE, "engine_run_group: an engine is in stream mode");
+    if (e->hostfed || e->ring_active != e0->ring_active)
+      return set_error(DS_E_STATE, "engine_run_group: engines differ in stream mode");
   }
   if (steps == 0) return DS_OK;
   dsb::DeviceScope ds(e0->device);
@@ -903,7 +908,7 @@ extern "C" int ds_engine_run_group(ds_engine** engines, uint32_t n, uint64_t ste
     ds_engine* e = engines[i];
     DS_TRY(dsb::ensure_log(e, e->queued + steps));
     DS_TRY(dsb::fused_args(e, steps, e->master != nullptr, a[i]));
-    tm[i] = e->tm_shard;
+    tm[i] = e->ring_active ? e->tm_ring : e->tm_shard;
     if (i) {  // the launch (on engine 0's stream) follows every engine's queued work
       DS_CUDA_TRY(cudaEventRecord(ev, e->stream));
       DS_CUDA_TRY(cudaStreamWaitEvent(e0->stream, ev, 0));
@@ -924,6 +929,14 @@ extern "C" int ds_engine_run_group(ds_engine** engines, uint32_t n, uint64_t ste
     e->queued += steps;
   }
   return DS_OK;
+}
+}  // namespace dsb
+
+extern "C" int ds_engine_run_group(ds_engine** engines, uint32_t n, uint64_t steps) {
+  for (uint32_t i = 0; engines && i < n; ++i)
+    if (engines[i] && engines[i]->ring_active)
+      return set_error(DS_E_STATE, "engine_run_group: an engine is in stream mode");
+  return dsb::run_group(engines, n, steps);
 }
 
 namespace {
@@ -1094,7 +1107,9 @@ extern "C" int ds_engine_set_momentum(ds_engine* e, float mu) {
   return DS_OK;
 }
 
-extern "C" int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss_host) {
+namespace {
+// stream mode set-up of one engine (everything but the launch)
+int stream_prepare(ds_engine* e, uint64_t steps, double* loss_host) {
   if (!e) return set_error(DS_E_CONTRACT, "engine_stream: null");
   if (e->ring_active) return set_error(DS_E_STATE, "engine_stream: a stream is already open");
   if (!e->fused || e->model.hidden.size() != 1 || (e->model.n_features % 4) != 0)
@@ -1132,8 +1147,35 @@ extern "C" int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss
   e->ring_steps = steps;
   e->ring_pushed = 0;
   e->ring_loss = loss_host;
+  return DS_OK;
+}
+}  // namespace
+
+extern "C" int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss_host) {
+  DS_TRY(stream_prepare(e, steps, loss_host));
+  if (steps == 0) return DS_OK;
+  dsb::DeviceScope ds(e->device);
   const int rc = ds_engine_run(e, steps, 0, nullptr);  // the launch waits on the ring
   if (rc != DS_OK) e->ring_active = false;
+  return rc;
+}
+
+extern "C" int ds_engine_stream_begin_group(ds_engine** engines, uint32_t n, uint64_t steps, double** loss_host) {
+  if (!engines || n == 0 || n > 8) return set_error(DS_E_CONTRACT, "engine_stream_group: 1..8 engines");
+  for (uint32_t i = 0; i < n; ++i)
+    if (!engines[i] || !engines[i]->tc)
+      return set_error(DS_E_CONTRACT, "engine_stream_group: needs tensor-core engines (DS_ENGINE_TC)");
+  for (uint32_t i = 0; i < n; ++i) {
+    const int rc = stream_prepare(engines[i], steps, loss_host ? loss_host[i] : nullptr);
+    if (rc != DS_OK) {
+      for (uint32_t k = 0; k < i; ++k) engines[k]->ring_active = false;
+      return rc;
+    }
+  }
+  if (steps == 0) return DS_OK;
+  const int rc = dsb::run_group(engines, n, steps);
+  if (rc != DS_OK)
+    for (uint32_t k = 0; k < n; ++k) engines[k]->ring_active = false;
   return rc;
 }
 
