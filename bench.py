@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--min-window-ms", type=float, default=200.0, help="repeat the K-step launch up to this")
     ap.add_argument("--e2e-steps", type=int, default=2000)
     ap.add_argument("--exchange-params", type=int, default=256 * 1024 * 1024)
+    ap.add_argument("--sync-params", type=int, default=62_378_344, help="synchronous round size (AlexNet's P)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / exchange sweep / cpu baseline (profiling)")
     ap.add_argument("--cifar-steps", type=int, default=200, help="timed steps of the cifar10_quick leg (0 = skip)")
     ap.add_argument("--alexnet-steps", type=int, default=20, help="timed steps of the AlexNet leg (0 = skip)")
@@ -370,7 +371,10 @@ def main():
     if not args.no_extras:
         line["f64_exact"] = f64_leg(args, L, api, torch, dist, world, rank, local, shards, init)
         line["packed"] = packed_leg(args, L, api, torch, dist, world, rank, local, init)
-        line["exchange"] = exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind)
+        nvl = nvlink_peak(L, torch, dist, world, rank, local) if world > 1 else None
+        line["exchange"] = exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind, nvl)
+        if world > 1:
+            line["sync_round"] = sync_leg(args, L, torch, dist, world, rank, local, nvl)
     if args.cifar_steps > 0:
         line["cifar10_quick"] = cifar_leg(args, L, api, torch, dist, world, rank, local)
         line["cifar10_quick_config3"] = {k: cifar_leg(args, L, api, torch, dist, world, rank, local, k)
@@ -527,7 +531,7 @@ def e2e_group_leg(args, L, api, engines, shards, seeds, rank, world, n):
                     "written to mapped host memory; wall clock from stream_begin to the last stream_end"}
 
 
-def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind):
+def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind, nvl=None):
     """Standalone elastic exchange (config 5 shape): fused in-place update streaming w and
     the center once, 16 B/param; with N>1 the center is sharded and the RMW crosses NVLink."""
     Pn = args.exchange_params
@@ -581,12 +585,115 @@ def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sms = t.item()
         remote = 8.0 * Ps * (world - 1) / world  # bytes each rank moves over NVLink per exchange, per direction x2
+        nv = remote / (sms / 1e3) / 1e9
         out.update({"sharded_params": Ps, "sharded_ms": sms, "sharded_gbs_per_gpu": 16.0 * Ps / (sms / 1e3) / 1e9,
-                    "nvlink_gbs_per_gpu": remote / (sms / 1e3) / 1e9,
+                    "sharded_frac_hbm": 16.0 * Ps / (sms / 1e3) / 1e9 / hbm,
+                    "exchanges_per_s_per_gpu": 1e3 / sms,
+                    "nvlink_gbs_per_gpu": nv, "nvlink_peak_gbs": nvl["gbs_per_gpu"] if nvl else None,
+                    "frac_nvlink_peak": nv / nvl["gbs_per_gpu"] if nvl else None,
                     "nvlink_note": "(G-1)/G x 8 B/param over NVLink per exchange, all ranks concurrent"})
         dist.barrier()
         L.lib.ds_master_destroy(mh)
     return out
+
+
+def nvlink_peak(L, torch, dist, world, rank, local, n_floats=64 * 1024 * 1024):
+    """In-run NVLink read peak with the all-gather's pattern: every rank concurrently copies
+    n floats split over all peers' memory into its own HBM (ds_sync_peer_read); per-GPU
+    GB/s = bytes read over NVLink / max-over-ranks device time."""
+    from paper_1602_08191_b200 import dist as D
+    dim = n_floats // 4 + 32
+    sg = D.sync_group(L, local, dim, rank, world)
+    dst = torch.empty(n_floats, device="cuda")
+    s = torch.cuda.current_stream()
+    st = C.c_void_p(s.cuda_stream)
+    for _ in range(3):
+        L.check(L.lib.ds_sync_peer_read(sg, C.c_void_p(dst.data_ptr()), n_floats, st))
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 20
+    e0.record(s)
+    for _ in range(iters):
+        L.check(L.lib.ds_sync_peer_read(sg, C.c_void_p(dst.data_ptr()), n_floats, st))
+    e1.record(s)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / iters], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    per = (n_floats // (world - 1)) & ~3
+    gbs = 4.0 * per * (world - 1) / (t.item() / 1e3) / 1e9
+    dist.barrier()
+    L.lib.ds_sync_destroy(sg)
+    return {"gbs_per_gpu": gbs, "bytes": 4 * per * (world - 1), "ms": t.item(),
+            "pattern": "every rank reads n/(G-1) floats from each peer concurrently (ds_sync_peer_read)"}
+
+
+def sync_leg(args, L, torch, dist, world, rank, local, nvl):
+    """Synchronous SGD round at AlexNet's parameter count over N GPUs: the worker-ordered
+    reduce-scatter + all-gather fused with the update (ds_sync_reduce_update), against the
+    in-run NVLink peak and against NCCL's all_reduce of the same vector (the library
+    baseline; its ring/tree order is not the reference's worker order)."""
+    from paper_1602_08191_b200 import dist as D
+    P = args.sync_params
+    sg = D.sync_group(L, local, P, rank, world)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    params = torch.randn(P, device="cuda", generator=g)
+    grad = torch.randn(P, device="cuda", generator=g) * 1e-3
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream()
+    st = C.c_void_p(s.cuda_stream)
+    slot = C.c_void_p()
+
+    def rnd():
+        L.check(L.lib.ds_sync_begin(sg, C.byref(slot), st))
+        L.check(L.lib.ds_sync_reduce_update(sg, C.c_void_p(params.data_ptr()), C.c_float(0.01), C.c_float(0.0),
+                                            C.c_void_p(flags.data_ptr()), st))
+    # the gradient is written once into both slot parities (the round's cost excludes the
+    # backward pass that would produce it)
+    for _ in range(2):
+        L.check(L.lib.ds_sync_begin(sg, C.byref(slot), st))
+        L.check(L.lib.ds_memcpy(slot, C.c_void_p(grad.data_ptr()), 4 * P, st))
+        L.check(L.lib.ds_sync_reduce_update(sg, C.c_void_p(params.data_ptr()), C.c_float(0.01), C.c_float(0.0),
+                                            C.c_void_p(flags.data_ptr()), st))
+    for _ in range(3):
+        rnd()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 20
+    e0.record(s)
+    for _ in range(iters):
+        rnd()
+    e1.record(s)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / iters], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    ok = int(flags.item()) == 0
+    dist.barrier()
+    L.lib.ds_sync_destroy(sg)
+    # NCCL all_reduce (sum) of the same f32 vector + the separate SGD update it would need
+    buf = grad.clone()
+    for _ in range(3):
+        dist.all_reduce(buf)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(s)
+    for _ in range(iters):
+        dist.all_reduce(buf)
+    e1.record(s)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / iters], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    nccl_ms = t.item()
+    nvl_bytes = 2.0 * (world - 1) / world * 4 * P
+    gbs = nvl_bytes / (ms / 1e3) / 1e9
+    return {"params": P, "round_ms": ms, "rounds_per_s": 1e3 / ms, "flags_clean": ok,
+            "nvlink_bytes_per_gpu": nvl_bytes, "nvlink_gbs_per_gpu": gbs,
+            "nvlink_peak_gbs": nvl["gbs_per_gpu"], "frac_nvlink_peak": gbs / nvl["gbs_per_gpu"],
+            "nccl_allreduce_ms": nccl_ms, "vs_nccl_allreduce": nccl_ms / ms,
+            "note": "ours = reduce-scatter (worker-ordered f64 sum) + SGD + all-gather, update included; "
+                    "NCCL = all_reduce alone (no update, not worker-ordered)"}
 
 
 def cifar_leg(args, L, api, torch, dist, world, rank, local, mode="async"):

@@ -99,21 +99,45 @@ int ds_grad_average(float* out, const double* gsum, uint64_t n, uint32_t n_worke
                     const float* x, void* stream);
 
 /* Multi-GPU synchronous SGD, one process per GPU (simulate_sync, simulator.cpp:156-223,
- * as the reference's "allreduce each iteration"). Each rank owns two peer-mapped f32
- * gradient slots; ds_sync_reduce_update reads every rank's slot over NVLink and sums in
- * f64 in worker order (simulator.cpp:192-200), divides by world, folds f32(wd)*x
- * (205-207) and applies sgd_step to `params` (the rank's replica of the master) in ONE
- * kernel — bit-identical to the single-process reference and identical on all ranks.
+ * as the reference's "allreduce each iteration"), as a worker-ordered reduce-scatter +
+ * all-gather over NVLink fused with the update: rank r owns the 128-byte aligned slice r;
+ * ds_sync_reduce_update sums every rank's gradient for that slice in f64 in worker order
+ * (simulator.cpp:192-200), divides by world, folds f32(wd)*x (205-207), applies sgd_step to
+ * its slice of `params` (the rank's replica of the master) and publishes it; then every
+ * rank copies the peers' new slices. Bit-identical to the single-process reference and on
+ * all ranks. NVLink bytes per rank and round: 2 (world-1)/world x 4 dim.
  *   create -> export (256-byte record) -> all-gather records -> attach
- *   per round: ds_sync_begin (slot free?) -> write the local gradient into *grad_slot on
- *   `stream` -> ds_sync_reduce_update(params, ...) on the same stream.
- * Non-finite conditions are OR-ed into *flags_dev (DS_FLAG_*). world <= 8. */
+ *   per round: ds_sync_begin -> write the local gradient into *grad_slot on `stream` ->
+ *   ds_sync_reduce_update(params, ...) on the same stream.
+ * Peer waits are bounded (30 s -> DS_FLAG_TICKET_TIMEOUT). Non-finite conditions are
+ * OR-ed into *flags_dev (DS_FLAG_*). world <= 8. Ranks of one process may share a device
+ * only through the *_group entry points (one kernel for all of them — never separate
+ * launches that wait on each other). */
 typedef struct ds_sync ds_sync;
 int ds_sync_create(ds_sync** out, int device, uint64_t dim, int rank, int world);
 int ds_sync_export(ds_sync* s, void* record_out);
 int ds_sync_attach(ds_sync* s, const void* records);
 int ds_sync_begin(ds_sync* s, float** grad_slot, void* stream);
 int ds_sync_reduce_update(ds_sync* s, float* params, float eta, float wd, uint32_t* flags_dev, void* stream);
+/* Synchronous EASGD (EXTENSION — not in the reference; the EASGD paper's synchronous
+ * variant, sharing the async path's elastic arithmetic param_vector.cpp:41-61): every
+ * rank holds a replica of the center `center` and its worker vector `worker`; one round:
+ *   e_k = f32(alpha * f32(x_k - c))        (all k, the OLD center)
+ *   x_k' = x_k - e_k                       (each rank its own worker)
+ *   c'   = c + f32(sum_k e_k in f64, worker order)
+ * Begins its own round (no ds_sync_begin). */
+int ds_sync_easgd_update(ds_sync* s, float* worker, float* center, float alpha, uint32_t* flags_dev, void* stream);
+/* Ranks 0..n-1 of one group living in THIS process on ONE device: one launch reduces every
+ * slice and writes every replica (params[k] / centers[k], workers[k]). Each rank's round
+ * must have been begun (ds_sync_begin, gradients written) for the SGD form. */
+int ds_sync_reduce_update_group(ds_sync** group, uint32_t n, float** params, float eta, float wd,
+                                uint32_t* flags_dev, void* stream);
+int ds_sync_easgd_update_group(ds_sync** group, uint32_t n, float** workers, float** centers, float alpha,
+                               uint32_t* flags_dev, void* stream);
+/* NVLink read probe with the all-gather's access pattern: n floats split evenly over every
+ * peer's exported region (<= 6 dim per peer), copied into dst (16-byte aligned). Timing
+ * it on all ranks concurrently gives the in-run NVLink peak the round is judged against. */
+int ds_sync_peer_read(ds_sync* s, float* dst, uint64_t n, void* stream);
 int ds_sync_rounds(ds_sync* s, uint64_t* out);
 int ds_sync_destroy(ds_sync* s);
 

@@ -319,6 +319,36 @@ class Oracle:
                                        _p(wo, C.c_float), _p(mo, C.c_float)))
         return wo, mo
 
+    @staticmethod
+    def sync_easgd_round(workers, center, alpha: float):
+        """Synchronous EASGD round (EXTENSION, not in the reference: the EASGD paper's
+        synchronous variant with the reference's elastic arithmetic, param_vector.cpp:41-61):
+        e_k = f32(alpha * f32(x_k - c)); x_k' = x_k - e_k; c' = c + f32(sum_k e_k), the sum
+        in f64 in worker order. numpy f32 operations round once each, like the C oracle."""
+        a = np.float32(alpha)
+        c = np.ascontiguousarray(center, np.float32)
+        s = np.zeros(c.shape, np.float64)
+        outs = []
+        for x in workers:
+            x = np.ascontiguousarray(x, np.float32)
+            e = (a * (x - c)).astype(np.float32)
+            s = s + e.astype(np.float64)
+            outs.append((x - e).astype(np.float32))
+        return outs, (c + s.astype(np.float32)).astype(np.float32)
+
+    @staticmethod
+    def sync_sgd_round(x, grads, eta: float, wd: float = 0.0):
+        """One simulate_sync master update (simulator.cpp:192-210): gsum in f64 in worker
+        order, gavg = f32(gsum / n), gavg += f32(wd) * x, sgd_step (param_vector.cpp:21-39)."""
+        x = np.ascontiguousarray(x, np.float32)
+        gs = np.zeros(x.shape, np.float64)
+        for g in grads:
+            gs = gs + np.asarray(g, np.float32).astype(np.float64)
+        g = (gs / np.float64(len(grads))).astype(np.float32)
+        if wd > 0:
+            g = (g + (np.float32(wd) * x).astype(np.float32)).astype(np.float32)
+        return (x - (np.float32(eta) * g).astype(np.float32)).astype(np.float32)
+
     def gen_synthetic(self, n, f, c, sep, sigma, seed):
         X = np.zeros((n, f), np.float32)
         y = np.zeros(n, np.uint32)

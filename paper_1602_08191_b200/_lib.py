@@ -174,6 +174,10 @@ _sig("ds_sync_export", VP, VP)
 _sig("ds_sync_attach", VP, VP)
 _sig("ds_sync_begin", VP, C.POINTER(VP), VP)
 _sig("ds_sync_reduce_update", VP, VP, C.c_float, C.c_float, VP, VP)
+_sig("ds_sync_easgd_update", VP, VP, VP, C.c_float, VP, VP)
+_sig("ds_sync_reduce_update_group", C.POINTER(VP), U32, C.POINTER(VP), C.c_float, C.c_float, VP, VP)
+_sig("ds_sync_easgd_update_group", C.POINTER(VP), U32, C.POINTER(VP), C.POINTER(VP), C.c_float, VP, VP)
+_sig("ds_sync_peer_read", VP, VP, U64, VP)
 _sig("ds_sync_rounds", VP, P_U64)
 _sig("ds_sync_destroy", VP)
 _sig("ds_gather_rows", VP, VP, VP, VP, VP, U32, U32, VP)
@@ -198,7 +202,8 @@ EXPORTED = [
     "ds_engine_sync", "ds_engine_stream", "ds_engine_log", "ds_engine_iterations",
     "ds_engine_get_params", "ds_engine_set_params", "ds_engine_params_device", "ds_engine_policy",
     "ds_engine_launches", "ds_sync_create", "ds_sync_export", "ds_sync_attach", "ds_sync_begin",
-    "ds_sync_reduce_update", "ds_sync_rounds", "ds_sync_destroy", "ds_gather_rows",
+    "ds_sync_reduce_update", "ds_sync_easgd_update", "ds_sync_reduce_update_group",
+    "ds_sync_easgd_update_group", "ds_sync_peer_read", "ds_sync_rounds", "ds_sync_destroy", "ds_gather_rows",
 ]
 
 

@@ -88,6 +88,75 @@ def sync_group(L, device: int, dim: int, rank: int, world: int, group=None):
     return s
 
 
+def local_sync_group(L, device: int, dim: int, world: int):
+    """`world` members of one synchronous group living in THIS process on one device (the
+    single-GPU form; drive them with ds_sync_*_group, one launch per round)."""
+    syncs = []
+    recs = []
+    for k in range(world):
+        s = C.c_void_p()
+        L.check(L.lib.ds_sync_create(C.byref(s), device, dim, k, world))
+        rec = (C.c_uint8 * L.DS_IPC_RECORD_BYTES)()
+        L.check(L.lib.ds_sync_export(s, rec))
+        syncs.append(s)
+        recs.append(bytes(rec))
+    allrec = (C.c_uint8 * (L.DS_IPC_RECORD_BYTES * world)).from_buffer_copy(b"".join(recs))
+    for s in syncs:
+        L.check(L.lib.ds_sync_attach(s, allrec))
+    return syncs
+
+
+def run_sync_group_local(L, api, model_desc, shards, n_classes: int, hp, sweep_seeds, params_devs, syncs,
+                         device: int, stream=None):
+    """simulate_sync (simulator.cpp:156-223) with all `world` ranks on ONE GPU: each round
+    every rank's ShardSweeper batch gives its gradient at its replica of the master (its
+    slot), then ONE ds_sync_reduce_update_group launch reduces every slice in worker order
+    and writes every replica. Returns the per-rank per-round batch losses ([world, i_max])."""
+    import torch
+    world = len(syncs)
+    B, i_max = hp.batch_size, hp.i_max
+    dev = torch.device("cuda", device)
+    ws_bytes = C.c_uint64()
+    L.check(L.lib.ds_loss_and_grad_workspace(C.byref(model_desc), B, C.byref(ws_bytes)))
+    per = []
+    for k, (Xk, yk) in enumerate(shards):
+        idx, rows = api.sweep_batches(len(yk), B, sweep_seeds[k], i_max)
+        F = Xk.shape[1]
+        per.append(dict(
+            F=F, rows=rows,
+            Xd=torch.from_numpy(np.ascontiguousarray(Xk)).to(dev),
+            yd=torch.from_numpy(np.ascontiguousarray(yk).astype(np.uint32).view(np.int32)).to(dev),
+            idx=torch.from_numpy(np.ascontiguousarray(idx).astype(np.uint32).view(np.int32)).to(dev),
+            bX=torch.empty((B, F), dtype=torch.float32, device=dev),
+            by=torch.empty(B, dtype=torch.int32, device=dev),
+            ws=torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device=dev)))
+    losses = torch.zeros((world, i_max), dtype=torch.float64, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = C.c_void_p(stream) if stream is not None else None
+    group = (C.c_void_p * world)(*[s.value for s in syncs])
+    preps = (C.c_void_p * world)(*[p.data_ptr() for p in params_devs])
+    slot = C.c_void_p()
+    for r in range(i_max):
+        for k in range(world):
+            w = per[k]
+            nr = int(w["rows"][r])
+            L.check(L.lib.ds_gather_rows(C.c_void_p(w["bX"].data_ptr()), C.c_void_p(w["by"].data_ptr()),
+                                         C.c_void_p(w["Xd"].data_ptr()), C.c_void_p(w["yd"].data_ptr()),
+                                         C.c_void_p(w["idx"][r, :nr].data_ptr()), nr, w["F"], st))
+            L.check(L.lib.ds_sync_begin(syncs[k], C.byref(slot), st))
+            L.check(L.lib.ds_loss_and_grad(C.byref(model_desc), C.c_void_p(params_devs[k].data_ptr()),
+                                           C.c_void_p(w["bX"].data_ptr()), C.c_void_p(w["by"].data_ptr()), nr, slot,
+                                           C.c_void_p(losses.data_ptr() + 8 * (k * i_max + r)),
+                                           C.c_void_p(w["ws"].data_ptr()), C.c_void_p(flags.data_ptr()), st))
+        L.check(L.lib.ds_sync_reduce_update_group(group, world, preps, C.c_float(hp.eta), C.c_float(hp.weight_decay),
+                                                  C.c_void_p(flags.data_ptr()), st))
+    torch.cuda.synchronize(dev)
+    fl = int(flags.item())
+    if fl:
+        raise RuntimeError(f"simulate_sync: device flags 0x{fl:x} (non-finite loss/grad/update or label range)")
+    return losses.cpu().numpy()
+
+
 def run_sync_worker(L, api, model_desc, Xk, yk, n_classes: int, hp, sweep_seed_k: int, params_dev, sg,
                     device: int, stream=None):
     """One rank of simulate_sync (simulator.cpp:156-223) on its own GPU: every round the
