@@ -724,6 +724,7 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   if (!e) return DS_OK;
   dsb::DeviceScope ds(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
+  if (e->master) dsb::master_remove_client(e->master, e->stream);
   cudaFree(e->X);
   cudaFree(e->y);
   cudaFree(e->params[0]);
@@ -783,6 +784,8 @@ extern "C" int ds_engine_attach_master(ds_engine* e, ds_master* m) {
     if (m->device != e->device) return set_error(DS_E_CONTRACT, "engine: master lives on another device");
     if (e->sync) return set_error(DS_E_CONTRACT, "engine: synchronous mode replaces the EASGD master");
   }
+  if (e->master && e->master != m) dsb::master_remove_client(e->master, e->stream);
+  if (m) dsb::master_add_client(m, e->stream);  // in-kernel exchanges run on the engine stream
   e->master = m;
   return DS_OK;
 }

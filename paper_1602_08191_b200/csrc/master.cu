@@ -14,6 +14,7 @@
 #include <unistd.h>
 
 #include <cstring>
+#include <set>
 
 #include "ds_common.cuh"
 #include "master.cuh"
@@ -138,9 +139,50 @@ int launch_exchange(const ShardTable& t, const float* worker, float* out, float 
   return DS_OK;
 }
 
+namespace {
+std::mutex g_live_mu;
+std::set<const ds_master*> g_live;  // masters not yet destroyed
+}  // namespace
+
+void master_add_client(ds_master* m, cudaStream_t s) {
+  if (s == m->stream) return;
+  std::lock_guard<std::mutex> lk(m->cmu);
+  for (cudaStream_t c : m->clients)
+    if (c == s) return;
+  m->clients.push_back(s);
+}
+
+void master_remove_client(ds_master* m, cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_live_mu);
+  if (!g_live.count(m)) return;
+  std::lock_guard<std::mutex> lk(m->cmu);
+  for (size_t i = 0; i < m->clients.size(); ++i)
+    if (m->clients[i] == s) {
+      m->clients.erase(m->clients.begin() + static_cast<long>(i));
+      return;
+    }
+}
+
+int master_quiesce(ds_master* m) {
+  DeviceScope ds(m->device);
+  DS_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  std::lock_guard<std::mutex> lk(m->cmu);
+  for (size_t i = 0; i < m->clients.size();) {
+    if (cudaEventRecord(m->ev_q, m->clients[i]) != cudaSuccess) {  // the stream was destroyed
+      cudaGetLastError();
+      m->clients.erase(m->clients.begin() + static_cast<long>(i));
+      continue;
+    }
+    DS_CUDA_TRY(cudaEventSynchronize(m->ev_q));
+    ++i;
+  }
+  return DS_OK;
+}
+
 int master_enqueue_exchange(ds_master* m, const float* worker, float* out, uint64_t ticket, const uint32_t* fire,
                             const uint32_t* gate, cudaStream_t caller) {
   DeviceScope ds(m->device);
+  master_add_client(m, caller);
   if (m->sharded && !m->attached) return set_error(DS_E_STATE, "master: sharded master not attached to peers");
   if (m->mode == DS_MODE_LOCKFREE && ticket == kNoTicket) {
     // LockFree: no serialization at all, straight on the caller's stream.
@@ -232,6 +274,7 @@ int create_common(ds_master** out, int device, uint64_t dim, float alpha, int mo
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->ev_in, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->ev_out, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->ev_q, cudaEventDisableTiming);
   if (e != cudaSuccess)
     return fail(dsb::set_error(e == cudaErrorMemoryAllocation ? DS_E_NOMEM : DS_E_CUDA, "master: %s", cudaGetErrorString(e)));
   // require_finite(initial) (exchanger.cpp:72), checked on the host copy of our slice
@@ -248,6 +291,10 @@ int create_common(ds_master** out, int device, uint64_t dim, float alpha, int mo
   m->table.begin[1] = dim;
   m->table.ptr[0] = m->local;
   m->table.flags[0] = m->flags;
+  {
+    std::lock_guard<std::mutex> g(dsb::g_live_mu);
+    dsb::g_live.insert(m);
+  }
   *out = m;
   return DS_OK;
 }
@@ -334,6 +381,10 @@ extern "C" int ds_master_attach(ds_master* m, const void* records) {
 extern "C" int ds_master_destroy(ds_master* m) {
   if (!m) return DS_OK;
   dsb::DeviceScope ds(m->device);
+  {
+    std::lock_guard<std::mutex> g(dsb::g_live_mu);
+    dsb::g_live.erase(m);
+  }
   cudaStreamSynchronize(m->stream);
   for (int k = 0; k < dsb::kMaxShards; ++k) {
     if (m->peer_mem[k]) cudaIpcCloseMemHandle(m->peer_mem[k]);
@@ -344,6 +395,7 @@ extern "C" int ds_master_destroy(ds_master* m) {
   cudaFree(m->ticket_slot);
   cudaEventDestroy(m->ev_in);
   cudaEventDestroy(m->ev_out);
+  cudaEventDestroy(m->ev_q);
   cudaStreamDestroy(m->stream);
   delete m;
   return DS_OK;
@@ -364,8 +416,7 @@ extern "C" int ds_master_exchange_ticketed(ds_master* m, const float* worker, fl
 extern "C" int ds_master_snapshot(ds_master* m, float* host_out) {
   if (!m || !host_out) return dsb::set_error(DS_E_CONTRACT, "master_snapshot: null");
   dsb::DeviceScope ds(m->device);
-  DS_CUDA_TRY(cudaStreamSynchronize(m->stream));
-  DS_CUDA_TRY(cudaDeviceSynchronize());
+  DS_TRY(dsb::master_quiesce(m));
   if (m->sharded && !m->attached) return dsb::set_error(DS_E_STATE, "master: sharded master not attached to peers");
   for (int k = 0; k < m->table.n; ++k) {
     const uint64_t b = m->table.begin[k], e = m->table.begin[k + 1];
@@ -385,7 +436,7 @@ extern "C" int ds_master_local_slice(ds_master* m, float** dev_ptr, uint64_t* be
 extern "C" int ds_master_exchange_count(ds_master* m, uint64_t* count) {
   if (!m || !count) return dsb::set_error(DS_E_CONTRACT, "master: null");
   dsb::DeviceScope ds(m->device);
-  DS_CUDA_TRY(cudaDeviceSynchronize());
+  DS_TRY(dsb::master_quiesce(m));
   dsb::ShardFlags f;
   for (int k = 0; k < m->table.n; ++k) {
     DS_CUDA_TRY(cudaMemcpy(&f, m->table.flags[k], sizeof(f), cudaMemcpyDefault));
@@ -407,7 +458,7 @@ extern "C" int ds_master_dim(ds_master* m, uint64_t* dim) {
 extern "C" int ds_master_reset_tickets(ds_master* m) {
   if (!m) return dsb::set_error(DS_E_CONTRACT, "master: null");
   dsb::DeviceScope ds(m->device);
-  DS_CUDA_TRY(cudaDeviceSynchronize());
+  DS_TRY(dsb::master_quiesce(m));
   DS_CUDA_TRY(cudaMemset(m->flags, 0, sizeof(dsb::ShardFlags)));
   std::lock_guard<std::mutex> lk(m->mu);
   m->next_host_ticket = 0;

@@ -12,6 +12,7 @@
 
 #include <condition_variable>
 #include <mutex>
+#include <vector>
 
 #include "ds_cuda.h"
 
@@ -69,6 +70,12 @@ struct ds_master {
   std::condition_variable cv;
   uint64_t next_host_ticket = 0;       // single-device deterministic ordering
   uint64_t host_exchanges = 0;
+  // streams that may carry work touching this center (callers' exchange streams, attached
+  // engines): snapshot / count / reset wait for these and the master stream only, never
+  // for the whole device
+  std::mutex cmu;
+  std::vector<cudaStream_t> clients;
+  cudaEvent_t ev_q = nullptr;
 };
 
 namespace dsb {
@@ -77,4 +84,9 @@ namespace dsb {
 // needs serialization and joins back into `caller`.
 int master_enqueue_exchange(ds_master* m, const float* worker, float* out, uint64_t ticket,
                             const uint32_t* fire, const uint32_t* gate, cudaStream_t caller);
+// client-stream registry (see ds_master::clients); remove is a no-op for a destroyed master
+void master_add_client(ds_master* m, cudaStream_t s);
+void master_remove_client(ds_master* m, cudaStream_t s);
+// wait for the master stream and every client stream's work enqueued so far
+int master_quiesce(ds_master* m);
 }  // namespace dsb
