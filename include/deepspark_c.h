@@ -116,6 +116,16 @@ int dsx_engine_steps(const dsx_model* m, const dsx_data* shard, const dsx_hyper*
  * (Locked, alpha = f32(hp.alpha)) initialised from / written back to master_inout. */
 int dsx_run_training_loop(const dsx_model* m, const dsx_data* shard, const dsx_hyper* hp, uint64_t sweep_seed,
                           const float* init, int exchange_mode, float* master_inout, dsx_loop_out* out);
+/* run_worker (worker.hpp) against a device center: the center is created from
+ * master_init with the model `master_model` bound to it (its handshake config: dim,
+ * fingerprint, alpha = f32(master_alpha)), mode 0 Locked / 1 LockFree. worker_model NULL
+ * = infer softmax from the shard. metrics_path NULL or "" = no dump. On return (also on
+ * the handshake errors, which leave the center untouched) master_out receives the
+ * center's snapshot and *master_exchanges its exchange count (either may be NULL). */
+int dsx_run_worker(const dsx_model* master_model, double master_alpha, int master_mode, const float* master_init,
+                   const dsx_model* worker_model, const char* shard_path, const dsx_hyper* hp, uint32_t worker_id,
+                   uint64_t rng_seed, const char* metrics_path, float* master_out, uint64_t* master_exchanges,
+                   dsx_loop_out* out);
 int dsx_resolve_loss_cut(const dsx_model* m, const dsx_data* shard, const dsx_hyper* hp, uint64_t sweep_seed,
                          const float* init, double* cut);
 int dsx_simulate(const dsx_sim_cfg* cfg, dsx_sim_out* out);

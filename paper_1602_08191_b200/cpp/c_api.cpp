@@ -254,6 +254,53 @@ int dsx_run_training_loop(const dsx_model* m, const dsx_data* shard, const dsx_h
   });
 }
 
+int dsx_run_worker(const dsx_model* master_model, double master_alpha, int master_mode, const float* master_init,
+                   const dsx_model* worker_model, const char* shard_path, const dsx_hyper* hp, uint32_t worker_id,
+                   uint64_t rng_seed, const char* metrics_path, float* master_out, uint64_t* master_exchanges,
+                   dsx_loop_out* out) {
+  return guard([&] {
+    if (!master_model || !master_init || !shard_path || !hp) throw ContractError("run_worker: null argument");
+    const Model served = model_of(master_model);
+    const size_t P = served.param_dim();
+    MasterState master(static_cast<uint32_t>(P), static_cast<float>(master_alpha),
+                       master_mode == 1 ? UpdateMode::LockFree : UpdateMode::Locked,
+                       ParamVector(master_init, master_init + P));
+    master.bind_model(served);
+    WorkerConfig cfg;
+    cfg.master = &master;
+    cfg.shard_path = shard_path;
+    cfg.hyper = hyper_of(hp);
+    cfg.worker_id = worker_id;
+    cfg.rng_seed = rng_seed;
+    cfg.metrics_path = metrics_path ? metrics_path : "";
+    if (worker_model) cfg.model = model_of(worker_model);
+    auto publish = [&] {
+      if (master_out) {
+        const ParamVector snap = master.snapshot();
+        std::memcpy(master_out, snap.data(), P * sizeof(float));
+      }
+      if (master_exchanges) *master_exchanges = master.exchange_count();
+    };
+    LocalRunResult r;
+    try {
+      r = run_worker(cfg);
+    } catch (...) {
+      publish();
+      throw;
+    }
+    publish();
+    if (out) {
+      if (out->final_params) std::memcpy(out->final_params, r.final_params.data(), r.final_params.size() * sizeof(float));
+      for (size_t i = 0; i < r.log.size(); ++i) {
+        if (out->batch_loss) out->batch_loss[i] = r.log[i].batch_loss;
+        if (out->cumulated) out->cumulated[i] = r.log[i].cumulated_loss;
+        if (out->exchanged) out->exchanged[i] = r.log[i].exchanged;
+        if (out->period_len) out->period_len[i] = r.log[i].period_len;
+      }
+    }
+  });
+}
+
 int dsx_resolve_loss_cut(const dsx_model* m, const dsx_data* shard, const dsx_hyper* hp, uint64_t sweep_seed,
                          const float* init, double* cut) {
   return guard([&] {

@@ -101,6 +101,9 @@ _SIGS = {
                                    C.c_uint64, P(C.c_float), P(C.c_double)]),
     "dsx_run_training_loop": (C.c_int, [P(dsx_model), P(dsx_data), P(dsx_hyper), C.c_uint64, P(C.c_float),
                                         C.c_int, P(C.c_float), P(dsx_loop_out)]),
+    "dsx_run_worker": (C.c_int, [P(dsx_model), C.c_double, C.c_int, P(C.c_float), P(dsx_model), C.c_char_p,
+                                 P(dsx_hyper), C.c_uint32, C.c_uint64, C.c_char_p, P(C.c_float), P(C.c_uint64),
+                                 P(dsx_loop_out)]),
     "dsx_resolve_loss_cut": (C.c_int, [P(dsx_model), P(dsx_data), P(dsx_hyper), C.c_uint64, P(C.c_float),
                                        P(C.c_double)]),
     "dsx_simulate": (C.c_int, [P(dsx_sim_cfg), P(dsx_sim_out)]),
@@ -301,6 +304,34 @@ class DeepSpark:
         _check(lib.dsx_run_training_loop(C.byref(d), C.byref(dd), C.byref(ch), sweep_seed, _p(init, C.c_float),
                                          exchange_mode, _p(master, C.c_float), C.byref(out)))
         res["master"] = master
+        return res
+
+    def run_worker(self, master_model, master_alpha, master_init, shard_path, hp, rng_seed, worker_model=None,
+                   worker_id=0, metrics_path=None, lockfree=False):
+        """run_worker (worker.cpp:52-98) against a device center serving `master_model`.
+        Returns the LocalRunResult fields plus the center's snapshot ("master") and
+        exchange count ("exchanges"); on a handshake error raises ContractError."""
+        d, _h = _model(master_model)
+        wd = None
+        if worker_model is not None:
+            wd, _wh = _model(worker_model)
+        ch = _hyper(hp)
+        init = np.ascontiguousarray(master_init, np.float32)
+        I = hp.i_max
+        res = dict(final_params=np.zeros_like(init), batch_loss=np.zeros(I), cumulated=np.zeros(I),
+                   exchanged=np.zeros(I, np.uint8), period_len=np.zeros(I, np.uint32),
+                   master=np.zeros_like(init))
+        if worker_model is not None:
+            res["final_params"] = np.zeros(self.param_dim(worker_model), np.float32)
+        out = dsx_loop_out(_p(res["final_params"], C.c_float), _p(res["batch_loss"], C.c_double),
+                           _p(res["cumulated"], C.c_double), _p(res["exchanged"], C.c_uint8),
+                           _p(res["period_len"], C.c_uint32))
+        cnt = C.c_uint64()
+        _check(lib.dsx_run_worker(C.byref(d), master_alpha, 1 if lockfree else 0, _p(init, C.c_float),
+                                  C.byref(wd) if wd is not None else None, str(shard_path).encode(), C.byref(ch),
+                                  worker_id, rng_seed, metrics_path.encode() if metrics_path else None,
+                                  _p(res["master"], C.c_float), C.byref(cnt), C.byref(out)))
+        res["exchanges"] = cnt.value
         return res
 
     def resolve_loss_cut(self, m, X, y, n_classes, hp, sweep_seed, init):

@@ -173,3 +173,98 @@ def test_config1_two_worker_deterministic(orc, dev):
     assert np.array_equal(a.eval_acc, b["eval_acc"])
     print(f"config1: {a.n_snaps} exchanges, snapshots bit-identical fraction {np.mean(d == 0):.7f}, "
           f"final acc {b['eval_acc'][-1]:.4f}")
+
+
+# ---- run_worker over the device path (worker.cpp:52-98; test_worker.cpp:122-260) ---------
+
+def _worker_fixture(orc, tmp_path, sep=10.0, sigma=0.5, name="shard_0.dshd"):
+    """test_worker.cpp's Fixture: standard_benchmark(12) with 120 samples, softmax model,
+    the shard spilled to DSHD (seed 7)."""
+    from test_shard import write_dshd
+    X, y = orc.gen_synthetic(120, 20, 2, sep, sigma, 12)
+    path = str(tmp_path / name)
+    write_dshd(path, X, y, seed=7, c=2)
+    return X, y, path
+
+
+@pytest.mark.gpu
+def test_run_worker_equals_in_process_loop(orc, dev, tmp_path):
+    """test_worker.cpp:122-147: the worker through the device exchanger equals the
+    in-process training loop with exchanges applied to a local master copy."""
+    X, y, path = _worker_fixture(orc, tmp_path)
+    m = ModelSpec.softmax(20, 2)
+    init = orc.init_params(m, 55)
+    hp = Hyper(eta=0.05, alpha=0.1, tau=5, batch_size=16, i_max=20)
+    got = dev.run_worker(m, 0.1, init, path, hp, rng_seed=3, metrics_path=str(tmp_path / "w.csv"))
+    ref = orc.run_training_loop(m, X, y, 2, hp, 3, init, 2, init)  # ExchangeFn on a host master
+    np.testing.assert_allclose(got["batch_loss"], ref["batch_loss"], rtol=1e-13)
+    assert np.array_equal(got["exchanged"], ref["exchanged"]) and np.array_equal(got["period_len"],
+                                                                                 ref["period_len"])
+    assert ulps(got["final_params"], ref["final_params"]).max() <= 1
+    assert ulps(got["master"], ref["master"]).max() <= 1
+    assert got["exchanges"] == 4  # iterations 5, 10, 15, 20
+
+
+@pytest.mark.gpu
+def test_run_worker_writes_metrics_and_params(orc, dev, tmp_path):
+    """test_worker.cpp:149-165 + the byte-identical-logs case (167-182)."""
+    import csv
+    X, y, path = _worker_fixture(orc, tmp_path)
+    m = ModelSpec.softmax(20, 2)
+    init = orc.init_params(m, 55)
+    hp = Hyper(eta=0.05, alpha=0.1, tau=5, batch_size=16, i_max=20)
+    res = dev.run_worker(m, 0.1, init, path, hp, rng_seed=3, metrics_path=str(tmp_path / "run.csv"))
+    rows = list(csv.DictReader(open(tmp_path / "run.csv")))
+    assert len(rows) == 20
+    for i, r in enumerate(rows):
+        assert int(r["exchanged"]) == ((i + 1) % 5 == 0)
+        assert float(r["batch_loss"]) == res["batch_loss"][i]  # shortest round-trip text
+        assert float(r["cumulated_loss"]) == res["cumulated"][i]
+    params = np.array([float(v) for v in open(tmp_path / "run.params").read().split()], np.float32)
+    assert np.array_equal(params.view(np.uint32), res["final_params"].view(np.uint32))
+    dev.run_worker(m, 0.1, init, path, hp, rng_seed=3, metrics_path=str(tmp_path / "run2.csv"))
+    strip = lambda p: [",".join(l.split(",")[:1] + l.split(",")[2:]) for l in open(p).read().splitlines()]
+    assert strip(tmp_path / "run.csv") == strip(tmp_path / "run2.csv")  # wall_ms column aside
+
+
+@pytest.mark.gpu
+def test_run_worker_adaptive_resolves_cut(orc, dev, tmp_path):
+    """test_worker.cpp:184-214: a hard shard, loss_cut resolved from the first batch."""
+    X, y, path = _worker_fixture(orc, tmp_path, sep=0.5, sigma=3.0, name="shard_9.dshd")
+    m = ModelSpec.softmax(20, 2)
+    init = orc.init_params(m, 55)
+    hp = Hyper(eta=0.05, alpha=0.1, tau=5, batch_size=16, i_max=100, adaptive=True, loss_cut=0.0)
+    res = dev.run_worker(m, 0.1, init, path, hp, rng_seed=3)
+    ref = orc.run_training_loop(m, X, y, 2, Hyper(eta=0.05, alpha=0.1, tau=5, batch_size=16, i_max=100,
+                                                   adaptive=True,
+                                                   loss_cut=orc.resolve_loss_cut(m, X, y, 2, hp, 3, init)),
+                                3, init, 2, init)
+    assert int(res["exchanged"].sum()) == res["exchanges"] >= 1
+    assert np.array_equal(res["exchanged"], ref["exchanged"])
+    np.testing.assert_allclose(res["batch_loss"], ref["batch_loss"], rtol=1e-13)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["alpha", "model", "shard", "no_master_dim"])
+def test_run_worker_handshake_errors(orc, dev, tmp_path, case):
+    """test_worker.cpp:216-242: disagreement with the exchanger is fatal before training
+    (the center is untouched, no exchange happened)."""
+    from paper_1602_08191_b200.deepspark import ContractError
+    X, y, path = _worker_fixture(orc, tmp_path)
+    m = ModelSpec.softmax(20, 2)
+    init = orc.init_params(m, 55)
+    hp = Hyper(eta=0.05, alpha=0.1, tau=5, batch_size=16, i_max=20)
+    kw = {}
+    served = m
+    if case == "alpha":
+        hp = Hyper(eta=0.05, alpha=0.2, tau=5, batch_size=16, i_max=20)  # server says 0.1
+    elif case == "model":
+        kw["worker_model"] = ModelSpec.mlp(20, [4], 2)  # different fingerprint (and dim)
+    elif case == "shard":
+        kw["worker_model"] = ModelSpec.softmax(21, 2)
+    else:  # same fingerprint family, different dim served: softmax(20, 3)
+        served = ModelSpec.softmax(20, 3)
+        init = orc.init_params(served, 55)
+        kw["worker_model"] = m
+    with pytest.raises(ContractError):
+        dev.run_worker(served, 0.1, init, path, hp, rng_seed=3, **kw)

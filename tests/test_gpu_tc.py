@@ -323,8 +323,19 @@ def test_tc_errors(L, orc):
             L.check(L.lib.ds_engine_sync(e))
     finally:
         L.lib.ds_engine_destroy(e)
-    hp_big = Hyper(eta=1e30, tau=5, batch_size=16, i_max=10)  # the update overflows: NumericError
-    e = make_engine(L, m, X, y, 3, hp_big, 31, init)
+    # a non-finite batch makes the loss non-finite (model.cpp:256): NumericError
+    e = make_engine(L, m, X, y, 3, hp, 31, init)
+    try:
+        xb = np.full((16, 20), np.nan, np.float32)
+        yb = np.ascontiguousarray(y[:16], np.uint32)
+        L.check(L.lib.ds_engine_step_host(e, xb.ctypes.data, yb.ctypes.data, 16, None))
+        with pytest.raises(L.NumericError):
+            L.check(L.lib.ds_engine_sync(e))
+    finally:
+        L.lib.ds_engine_destroy(e)
+    # an update that overflows f32 (huge weights, weight decay folded in): NumericError
+    hp_big = Hyper(eta=5.0, tau=5, batch_size=16, i_max=10, weight_decay=1.0)
+    e = make_engine(L, m, X, y, 3, hp_big, 31, (init * np.float32(1e37)).astype(np.float32))
     try:
         L.check(L.lib.ds_engine_run(e, 10, 0, None))
         with pytest.raises(L.NumericError):
