@@ -3,9 +3,11 @@
 Each rank is one worker with its simulate() partition; the center is sharded over all
 GPUs and every exchange is an in-kernel P2P read-modify-write of all slices.
 
-  --mode det   deterministic: global tickets from the replayed simulate_async order;
-               rank 0 checks the final master and every worker against the CPU oracle
-               (<= 1 ulp per element).
+  --mode det   deterministic: global tickets from the replayed simulate_async order; the
+               run is cut into tau-step chunks and after every chunk (= every round of
+               `world` exchanges, tickets [c*world, (c+1)*world)) rank 0 snapshots the
+               center and compares it with the oracle's per-exchange snapshot of that
+               ticket; rank 0 also checks the final master and every worker (<= 1 ulp).
   --mode async LockFree, no tickets; rank 0 checks the master is finite and its holdout
                accuracy lies within a band of the oracle's deterministic run.
 Prints one line `MGPU_RESULT {json}` on rank 0.
@@ -75,7 +77,25 @@ def main():
         tk = D.worker_tickets(order_w, rank)
         L.check(L.lib.ds_engine_set_tickets(eng, tk.ctypes.data, len(tk)))
     dist.barrier()
-    L.check(L.lib.ds_engine_run(eng, hp.i_max, 0, None))
+    snaps = []  # (global exchange index, center) after every round of exchanges
+    if args.mode == "det":
+        order_w, _ = api.exchange_order(world, hp.tau, hp.i_max, sched_seed)
+        rounds = hp.i_max // hp.tau
+        assert all(sorted(order_w[c * world:(c + 1) * world]) == list(range(world)) for c in range(rounds))
+        for c in range(rounds):
+            L.check(L.lib.ds_engine_run(eng, hp.tau, 0, None))
+            L.check(L.lib.ds_engine_sync(eng))
+            dist.barrier()  # every rank finished its c-th exchange: tickets < (c+1)*world done
+            if rank == 0:
+                sn = np.zeros(P, np.float32)
+                L.check(L.lib.ds_master_snapshot(master, sn.ctypes.data))
+                snaps.append(((c + 1) * world - 1, sn))
+            dist.barrier()
+        rest = hp.i_max - rounds * hp.tau
+        if rest:
+            L.check(L.lib.ds_engine_run(eng, rest, 0, None))
+    else:
+        L.check(L.lib.ds_engine_run(eng, hp.i_max, 0, None))
     L.check(L.lib.ds_engine_sync(eng))
     params = np.zeros(P, np.float32)
     L.check(L.lib.ds_engine_get_params(eng, params.ctypes.data))
@@ -93,7 +113,7 @@ def main():
     if rank == 0:
         orc = Oracle("dso")
         s = SimSpec(world, hp, m, X, y, ncls, schedule_seed=sched_seed, init_seed=init_seed, data_seed=data_seed,
-                    eval_every=10 ** 6, record_master_snaps=False)
+                    eval_every=10 ** 6, record_master_snaps=args.mode == "det")
         ref = orc.simulate(s)
 
         def ulps(a, b):
@@ -117,6 +137,9 @@ def main():
                 wk = np.frombuffer(all_params[k], np.float32)
                 wmax = max(wmax, int(ulps(wk, ref.worker_final[k]).max()))
             res["workers_max_ulp"] = wmax
+            # per-round center snapshots against the oracle's snapshot after that ticket
+            res["snapshots_compared"] = len(snaps)
+            res["snapshots_max_ulp"] = max((int(ulps(sn, ref.snap_params[g]).max()) for g, sn in snaps), default=-1)
         print("MGPU_RESULT " + json.dumps(res), flush=True)
     dist.destroy_process_group()
 

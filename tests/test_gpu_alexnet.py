@@ -6,15 +6,20 @@ tcgen05 tensor cores with tf32 operands and f32 accumulation (csrc/gemm_tc.cu,
 csrc/alexnet.cu). Two bars:
   * f32-accurate products (DS_GEMM_3XTF32=1: each GEMM as three tf32 GEMMs on hi/lo
     operand splits) isolate the implementation from tf32 rounding: batch loss within 2e-5
-    relative, every layer's gradient within 1e-3 relative norm (cosine >= 0.99999) of the
-    f64 oracle — the evidence that the layer algebra is right. (The tensor core's f32
-    accumulation is not IEEE round-to-nearest, so the residual grows with K: measured
-    relnorm 3e-5 at S = 55, 2e-4 .. 3.2e-4 at S = 224 with K up to 9216.);
-  * the production tf32 path: batch loss within 2e-3 relative; per layer relative norm
-    <= 0.15 and cosine >= 0.99. tf32 rounding flips ReLU masks and max-pool winners, and
-    each flip moves a whole row of a weight gradient (measured: relnorm 3e-3 .. 1.2e-1);
-  * predictions: argmax equal to the oracle's wherever the oracle's top-2 logit margin is
-    clear of tf32 noise;
+    relative, every layer's gradient within 2e-4 relative norm (cosine >= 0.99999) of the
+    f64 oracle — the evidence that the layer algebra is right (measured, tools/alex_tol.py:
+    1.4e-5 .. 5e-5 at S = 55 and S = 224; the tensor core's f32 accumulation is not IEEE
+    round-to-nearest, so the residual grows with K);
+  * the production tf32 path: batch loss within 5e-5 relative (measured 9e-7 .. 5e-6);
+    the classifier layer's gradient within 1e-2 relative norm (measured 3e-3 .. 6e-3);
+    every other layer within 0.12 relative norm, cosine >= 0.99 (measured 0.036 .. 0.090,
+    the same against the f64 oracle as against the GPU's own 3xTF32 products, and the
+    same at batch 2, 13, 32 and 64). That residual is not accumulation error: tf32 operand
+    rounding (2^-11) flips ReLU masks and max-pool winners whose pre-activations tie to
+    within 5e-4, and each flip moves one position's whole gradient contribution — a flip
+    rate of ~1e-3 gives sqrt(2e-3) ~ 5% relative norm independent of batch. Only
+    f32-accurate forward products remove it (the 3xTF32 bar above);
+  * predictions: argmax agreement with the oracle >= 0.99 (measured 1.0 on 200 rows);
   * determinism: two identical calls are bit-identical (fixed-order split-K reductions).
 """
 import ctypes as C
@@ -81,15 +86,18 @@ def gpu_lag(T, L, d, params, X, y, want_grad=True):
 
 
 def compare(orc, side, c, lg, gg, lr, gr, exact):
-    assert abs(lg - lr) <= (2e-5 if exact else 2e-3) * abs(lr), (lg, lr)
-    for li, (a, b) in enumerate(layer_bounds(orc, side, c)):
+    assert abs(lg - lr) <= (2e-5 if exact else 5e-5) * abs(lr), (lg, lr)
+    bounds = layer_bounds(orc, side, c)
+    for li, (a, b) in enumerate(bounds):
         ref, got = gr[a:b].astype(np.float64), gg[a:b].astype(np.float64)
         rn = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         cos = float(ref @ got / (np.linalg.norm(ref) * np.linalg.norm(got) + 1e-300))
         if exact:
-            assert rn <= 1e-3 and cos >= 0.99999, (li, rn, cos)
+            assert rn <= 2e-4 and cos >= 0.99999, (li, rn, cos)
+        elif li == len(bounds) - 1:  # classifier: no ReLU / pool downstream of its inputs' use
+            assert rn <= 1e-2 and cos >= 0.9999, (li, rn, cos)
         else:
-            assert rn <= 0.15 and cos >= 0.99, (li, rn, cos)
+            assert rn <= 0.12 and cos >= 0.99, (li, rn, cos)
 
 
 @pytest.fixture(params=["tf32", "exact"])
@@ -141,7 +149,7 @@ def test_predict_matches_oracle(T, L, orc):
     side, c = 55, 7
     m = ModelSpec.alexnet(side, c)
     w = orc.init_params(m, 6)
-    X, y = orc.gen_synthetic(40, 3 * side * side, c, 1.0, 1.0, 9)
+    X, y = orc.gen_synthetic(200, 3 * side * side, c, 1.0, 1.0, 9)
     X = np.ascontiguousarray(X * 5.0, dtype=np.float32)
     ref = orc.predict(m, w, X)
     d = desc(L, side, c)
@@ -153,7 +161,7 @@ def test_predict_matches_oracle(T, L, orc):
     T.cuda.synchronize()
     got = pred.cpu().numpy()
     agree = (got == ref).mean()
-    assert agree >= 0.9, agree
+    assert agree >= 0.99, agree
 
 
 def test_engine_training_tracks_oracle(T, L, orc, mode, monkeypatch):

@@ -37,6 +37,7 @@ def test_deterministic_sharded_center(kind):
     r = run(min(ngpus(), 4), "--mode", "det", "--kind", str(kind))
     assert r["exchanges"] == r["expected_exchanges"]
     assert r["master_max_ulp"] <= 1 and r["workers_max_ulp"] <= 1
+    assert r["snapshots_compared"] == 60 // 5 and r["snapshots_max_ulp"] <= 1
     assert r["acc_dev"] == r["acc_ref"]
 
 
@@ -44,13 +45,16 @@ def test_deterministic_sharded_center(kind):
 def test_deterministic_config1_two_gpus():
     r = run(2, "--mode", "det", "--big")
     assert r["master_max_ulp"] <= 1 and r["workers_max_ulp"] <= 1
+    assert r["snapshots_compared"] == 200 // 10 and r["snapshots_max_ulp"] <= 1
 
 
 @pytest.mark.skipif(ngpus() < 2, reason="needs >= 2 GPUs")
 def test_async_lockfree_band():
-    r = run(min(ngpus(), 4), "--mode", "async")
+    # BASELINE config 1's model and data (784-256-10, sep 0.1): accuracy is not saturated
+    r = run(min(ngpus(), 4), "--mode", "async", "--big")
     assert r["finite"] and r["exchanges"] == r["expected_exchanges"]
-    assert abs(r["acc_dev"] - r["acc_ref"]) <= 0.05
+    assert r["acc_ref"] < 0.99, "band test on a saturated run proves nothing"
+    assert abs(r["acc_dev"] - r["acc_ref"]) <= 0.03
 
 
 # ---- synchronous SGD: gradient "allreduce" fused into the update kernel over NVLink ----
