@@ -1145,11 +1145,16 @@ int launch_tc_group(const FusedArgs* a, const CUtensorMap* tm, uint32_t n, int n
   at[0].val.clusterDim.x = nc;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeCooperative;  // every worker resident: workers wait on each other's tickets
+  // co-residency is needed only when workers wait on each other (ordered exchanges:
+  // Locked arrival tickets or deterministic tickets); LockFree and master-less groups
+  // launch as plain cluster grids (which profilers can also replay)
+  bool waits = false;
+  for (uint32_t i = 0; i < n; ++i) waits = waits || (a[i].has_master && !a[i].lockfree);
+  at[1].id = cudaLaunchAttributeCooperative;
   at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = n > 1 ? 2 : 1;
-  if (n > 1) {
+  cfg.numAttrs = (n > 1 && waits) ? 2 : 1;
+  if (n > 1 && waits) {
     int nclusters = 0;
     if (cudaOccupancyMaxActiveClusters(&nclusters, mlp_tc_kernel, &cfg) == cudaSuccess && nclusters < static_cast<int>(n))
       return set_error(DS_E_CONTRACT, "tc: %u workers of %d CTAs do not fit on the GPU at once (max %d)", n, nc, nclusters);
