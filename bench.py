@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--workers", type=int, default=2, help="EASGD workers per GPU (BASELINE config 1: 2)")
     ap.add_argument("--min-window-ms", type=float, default=200.0, help="repeat the K-step launch up to this")
     ap.add_argument("--e2e-steps", type=int, default=2000)
+    ap.add_argument("--det-steps", type=int, default=20000, help="timed steps of the deterministic config-1 leg")
     ap.add_argument("--exchange-params", type=int, default=256 * 1024 * 1024)
     ap.add_argument("--sync-params", type=int, default=62_378_344, help="synchronous round size (AlexNet's P)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / exchange sweep / cpu baseline (profiling)")
@@ -371,6 +372,8 @@ def main():
     if not args.no_extras:
         line["f64_exact"] = f64_leg(args, L, api, torch, dist, world, rank, local, shards, init)
         line["packed"] = packed_leg(args, L, api, torch, dist, world, rank, local, init)
+        if world == 1:
+            line["config1_deterministic"] = det_leg(args, L, api, torch, shards, seeds, init)
         nvl = nvlink_peak(L, torch, dist, world, rank, local) if world > 1 else None
         line["exchange"] = exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind, nvl)
         if world > 1:
@@ -466,6 +469,65 @@ def packed_leg(args, L, api, torch, dist, world, rank, local, init):
     if world > 1:
         dist.barrier()
     L.lib.ds_master_destroy(master)
+    return out
+
+
+def det_leg(args, L, api, torch, shards, seeds, init):
+    """BASELINE config 1 as the reference's simulator runs it: 2 workers, DETERMINISTIC
+    exchange order (simulate_async's replayed global order, simulator.cpp:91-143) — both
+    workers in ONE tensor-core launch, the center serialised by the replayed tickets in
+    the kernel (bit-reproducible run to run; tests/test_gpu_tc.py)."""
+    P = init.numel()
+    Wd = 2
+    warm, steps = 300, args.det_steps
+    order_w, _ = api.exchange_order(Wd, args.tau, warm + steps, 1)
+    mh = C.c_void_p()
+    L.check(L.lib.ds_master_create(C.byref(mh), 0, P, C.c_float(0.1), L.DS_MODE_LOCKED,
+                                   C.c_void_p(init.data_ptr())))
+    hidden = (C.c_uint32 * 1)(H)
+    desc = L.ds_model_desc(1, F, NCLS, 1, hidden)
+    hp = L.ds_hyper(0.05, 0.1, args.tau, args.batch, warm + steps, 0.0, 0.0, 0)
+    engines = []
+    out = {}
+    try:
+        for k in range(Wd):
+            Xk, yk = shards[k % len(shards)]
+            e = C.c_void_p()
+            L.check(L.lib.ds_engine_create(C.byref(e), 0, C.byref(desc), Xk.ctypes.data, yk.ctypes.data, len(yk),
+                                           NCLS, C.byref(hp), seeds[k % len(seeds)], C.c_void_p(init.data_ptr()),
+                                           L.DS_ENGINE_TC))
+            engines.append(e)
+            L.check(L.lib.ds_engine_attach_master(e, mh))
+            tk = np.nonzero(np.asarray(order_w) == k)[0].astype(np.uint64)
+            L.check(L.lib.ds_engine_set_tickets(e, tk.ctypes.data, len(tk)))
+            L.check(L.lib.ds_engine_reserve(e, warm + steps + 8))
+        arr = (C.c_void_p * Wd)(*[e.value for e in engines])
+        sp = C.c_void_p()
+        L.check(L.lib.ds_engine_stream(engines[0], C.byref(sp)))
+        st = torch.cuda.ExternalStream(sp.value)
+        L.check(L.lib.ds_engine_run_group(arr, Wd, warm))
+        for e in engines:
+            L.check(L.lib.ds_engine_sync(e))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(0) as clk:
+            e0.record(st)
+            L.check(L.lib.ds_engine_run_group(arr, Wd, steps))
+            e1.record(st)
+            for e in engines:
+                L.check(L.lib.ds_engine_sync(e))
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        cnt = C.c_uint64()
+        L.check(L.lib.ds_master_exchange_count(mh, C.byref(cnt)))
+        out = {"value": Wd * args.batch * steps / (ms / 1e3), "unit": "samples/s", "workers": Wd,
+               "ms_per_step": ms / steps, "steps": steps, "exchanges": int(cnt.value),
+               "expected_exchanges": Wd * ((warm + steps) // args.tau), "clocks": clk.summary(),
+               "mode": "Locked center, deterministic tickets replayed from simulate_async's order"}
+    finally:
+        for e in engines:
+            L.lib.ds_engine_destroy(e)
+        L.lib.ds_master_destroy(mh)
     return out
 
 

@@ -4,6 +4,7 @@
 // (ds_engine_*), whose own sweep plan and policy reproduce the same order on the GPU.
 #include "deepspark/engine.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <numeric>
 
@@ -185,6 +186,9 @@ LocalRunResult run_training_loop(const Model& model, const Dataset& shard, const
                                  ParamVector initial, const ExchangeFn& exchange) {
   hp.validate();
   SgdEngine engine(model, shard, hp, sweep_seed, std::move(initial));
+  // the TrainLog rows and sweep plan are allocated before the clock starts (wall_ms
+  // measures training, as the reference's host loop does)
+  check_status(ds_engine_reserve(engine.handle(), std::min<uint64_t>(hp.i_max, 1u << 16)), "run_training_loop");
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<int64_t> wall(hp.i_max, 0);
   uint64_t done = 0;
@@ -222,6 +226,7 @@ LocalRunResult run_training_loop(const Model& model, const Dataset& shard, const
   if (master.dim() != model.param_dim()) throw ContractError("run_training_loop: master dim does not match model");
   SgdEngine engine(model, shard, hp, sweep_seed, std::move(initial));
   engine.attach_master(&master);
+  check_status(ds_engine_reserve(engine.handle(), std::min<uint64_t>(hp.i_max, 1u << 16)), "run_training_loop");
   const auto t0 = std::chrono::steady_clock::now();
   engine.run(hp.i_max, false);
   engine.sync();

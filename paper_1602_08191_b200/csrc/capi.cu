@@ -2,6 +2,7 @@
 #include <mutex>
 
 #include "ds_common.cuh"
+#include "master.cuh"
 
 namespace dsb {
 
@@ -100,6 +101,7 @@ extern "C" int ds_stream_create(int device, void** stream) {
 }
 
 extern "C" int ds_stream_destroy(void* stream) {
+  if (stream) dsb::master_forget_stream(dsb::as_stream(stream));  // no master may record on it later
   if (stream) DS_CUDA_TRY(cudaStreamDestroy(dsb::as_stream(stream)));
   return DS_OK;
 }

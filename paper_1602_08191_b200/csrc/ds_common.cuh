@@ -6,6 +6,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <initializer_list>
 #include <string>
 
 #include "ds_cuda.h"
@@ -55,6 +56,21 @@ struct DeviceScope {
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count(int device);
+
+// Loads kernels now (CUDA lazy loading otherwise loads each on its first launch, which
+// lands inside the caller's first timed step): cudaFuncGetAttributes forces the load.
+template <typename... K>
+inline void load_kernels(K... k) {
+  cudaFuncAttributes a;
+  (void)std::initializer_list<int>{(cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k)), 0)...};
+  cudaGetLastError();
+}
+// Per-file warmers (engine / master creation call the ones their paths launch).
+void warm_model_kernels();
+void warm_elementwise_kernels();
+void warm_fused_kernels();
+void warm_tc_kernels();
+void warm_master_kernels();
 
 // ---------------------------------------------------------------------------------
 // Device arithmetic with the reference's rounding points. The reference is compiled

@@ -343,3 +343,8 @@ extern "C" int ds_sgd_momentum_update(float* out, const float* x, float* velocit
   if (!(mu >= 0.0f && mu < 1.0f)) return dsb::set_error(DS_E_CONTRACT, "sgd_momentum: mu must be in [0,1)");
   return dsb::launch_momentum(out, x, velocity, g, n, eta, mu, wd, flags_dev, dsb::as_stream(stream), nullptr);
 }
+
+void dsb::warm_elementwise_kernels() {
+  dsb::load_kernels(dsb::elastic_vec_kernel, dsb::elastic_scalar_kernel, dsb::sgd_vec_kernel, dsb::sgd_scalar_kernel,
+                    dsb::momentum_kernel, grad_accumulate_kernel, grad_average_kernel, gather_rows_kernel);
+}

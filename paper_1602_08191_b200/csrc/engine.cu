@@ -21,7 +21,9 @@
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <numeric>
+#include <set>
 
 #include "deepspark/rng.hpp"
 #include "ds_common.cuh"
@@ -569,6 +571,23 @@ int run_group(ds_engine** engines, uint32_t n, uint64_t steps);
 
 // ds_engine_create / ds_engine_create_from_shard: the shard comes from host arrays, or
 // (shard_path != nullptr) from a DSHD file streamed straight into e->X / e->y.
+// Load the step kernels once per device at engine creation, so no timed step pays CUDA's
+// lazy module loading (the reference's TrainLog wall_ms would otherwise differ between a
+// cold and a warm run of the same training).
+static void warm_step_kernels(int device) {
+  static std::mutex mu;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert(device).second) return;
+  dsb::DeviceScope ds(device);
+  dsb::load_kernels(dsb::policy_kernel, dsb::set_idx_kernel);
+  dsb::warm_model_kernels();
+  dsb::warm_elementwise_kernels();
+  dsb::warm_fused_kernels();
+  dsb::warm_tc_kernels();
+  dsb::warm_master_kernels();
+}
+
 static int engine_create(ds_engine** out, int device, const ds_model_desc* model, const float* X_host,
                          const uint32_t* y_host, uint64_t shard_n, uint32_t shard_classes, const ds_hyper* hp,
                          uint64_t sweep_seed, const float* init_host, int kind, const char* shard_path) {
@@ -576,6 +595,7 @@ static int engine_create(ds_engine** out, int device, const ds_model_desc* model
     return set_error(DS_E_CONTRACT, "engine: null argument");
   dsb::ModelInfo m;
   DS_TRY(dsb::model_from_desc(model, m));
+  if (device >= 0) warm_step_kernels(device);
   // Hyperparams::validate (hyperparams.cpp:7-18)
   if (!(hp->eta > 0.0)) return set_error(DS_E_CONTRACT, "hyperparams: eta must be positive");
   if (!(hp->alpha > 0.0 && hp->alpha < 1.0)) return set_error(DS_E_CONTRACT, "hyperparams: alpha must lie in (0,1)");
@@ -724,7 +744,7 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   if (!e) return DS_OK;
   dsb::DeviceScope ds(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
-  if (e->master) dsb::master_remove_client(e->master, e->stream);
+  if (e->stream) dsb::master_forget_stream(e->stream);
   cudaFree(e->X);
   cudaFree(e->y);
   cudaFree(e->params[0]);

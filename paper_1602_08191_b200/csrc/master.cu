@@ -163,6 +163,19 @@ void master_remove_client(ds_master* m, cudaStream_t s) {
     }
 }
 
+void master_forget_stream(cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_live_mu);
+  for (const ds_master* cm : g_live) {
+    ds_master* m = const_cast<ds_master*>(cm);
+    std::lock_guard<std::mutex> lk(m->cmu);
+    for (size_t i = 0; i < m->clients.size(); ++i)
+      if (m->clients[i] == s) {
+        m->clients.erase(m->clients.begin() + static_cast<long>(i));
+        break;
+      }
+  }
+}
+
 int master_quiesce(ds_master* m) {
   DeviceScope ds(m->device);
   DS_CUDA_TRY(cudaStreamSynchronize(m->stream));
@@ -266,6 +279,7 @@ int create_common(ds_master** out, int device, uint64_t dim, float alpha, int mo
     delete m;
     return rc;
   };
+  dsb::warm_master_kernels();  // no first exchange pays lazy module loading
   cudaError_t e = cudaMalloc(&m->local, (own ? own : 1) * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&m->flags, sizeof(dsb::ShardFlags));
   if (e == cudaSuccess) e = cudaMalloc(&m->ticket_slot, sizeof(unsigned long long));
@@ -464,3 +478,5 @@ extern "C" int ds_master_reset_tickets(ds_master* m) {
   m->next_host_ticket = 0;
   return DS_OK;
 }
+
+void dsb::warm_master_kernels() { dsb::load_kernels(dsb::exchange_kernel, dsb::take_ticket_kernel); }

@@ -87,6 +87,8 @@ int master_enqueue_exchange(ds_master* m, const float* worker, float* out, uint6
 // client-stream registry (see ds_master::clients); remove is a no-op for a destroyed master
 void master_add_client(ds_master* m, cudaStream_t s);
 void master_remove_client(ds_master* m, cudaStream_t s);
+// drop `s` from every live master's registry (the stream is about to be destroyed)
+void master_forget_stream(cudaStream_t s);
 // wait for the master stream and every client stream's work enqueued so far
 int master_quiesce(ds_master* m);
 }  // namespace dsb

@@ -1795,3 +1795,5 @@ int launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
 }
 
 }  // namespace dsb
+
+void dsb::warm_fused_kernels() { dsb::load_kernels(dsb::fused_kernel<false>, dsb::fused_kernel<true>, dsb::mlp_kernel); }

@@ -1169,3 +1169,5 @@ int launch_tc(const FusedArgs& a, int nc, const CUtensorMap& tm, cudaStream_t s)
 }
 
 }  // namespace dsb
+
+void dsb::warm_tc_kernels() { dsb::load_kernels(dsb::mlp_tc_kernel, dsb::rows_to_bf16_kernel); }

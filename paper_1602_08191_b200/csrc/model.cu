@@ -409,3 +409,8 @@ extern "C" int ds_count_hits(const ds_model_desc* model, const float* params, co
   cudaFreeAsync(ws, s);
   return rc;
 }
+
+void dsb::warm_model_kernels() {
+  dsb::load_kernels(dsb::fwd_layer<true>, dsb::fwd_layer<false>, dsb::softmax_ce, dsb::loss_reduce, dsb::bwd_delta,
+                    dsb::grad_layer<true>, dsb::grad_layer<false>, dsb::argmax_hits);
+}

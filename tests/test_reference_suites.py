@@ -1,4 +1,5 @@
-"""The reference's own unit suites (proj/tests/test_{params,model,engine,simulator,data}.cpp),
+"""The reference's own unit suites (proj/tests/test_{params,model,engine,simulator,data,
+protocol,exchanger,worker}.cpp),
 compiled UNMODIFIED against include/deepspark/ and linked with the B200 library
 (oracle/Makefile `reftests`), run on the GPU. Every assertion the reference makes about
 its own API — bit-exact one-step equality, replay of the elastic kernel, sync averaging,
@@ -22,14 +23,16 @@ def run_suite(suite):
     return p
 
 
-def test_data_suite_host_only():
-    """test_data.cpp needs no GPU: dataset generation, partition, holdout, CSV, DSHD."""
-    p = run_suite("data")
+@pytest.mark.parametrize("suite", ["data", "protocol"])
+def test_host_only_suites(suite):
+    """test_data.cpp (dataset generation, partition, holdout, CSV, DSHD) and
+    test_protocol.cpp (the DSPR wire codec) need no GPU."""
+    p = run_suite(suite)
     assert p.returncode == 0, p.stderr[-2000:]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["params", "model", "engine", "simulator"])
+@pytest.mark.parametrize("suite", ["params", "model", "engine", "simulator", "exchanger", "worker"])
 def test_reference_suite_on_b200(suite):
     p = run_suite(suite)
     assert p.returncode == 0, p.stderr[-3000:]
