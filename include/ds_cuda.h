@@ -365,7 +365,8 @@ int ds_engine_step_host_async(ds_engine* e, const float* X_host, const uint32_t*
  * Every batch crosses PCIe as an H2D copy; each step's loss is written by the kernel to
  * *loss_host[step] (pinned, mapped: zero-copy D2H), valid after ds_engine_stream_end.
  * push blocks only while the ring is full. X_host/y_host of push s may be reused at push
- * s+DS_STREAM_RING. Fused one-hidden-layer engine, fixed-period policy. A host that stops pushing for
+ * s+DS_STREAM_RING. Fused one-hidden-layer engine; a Fixed or Adaptive policy (Adaptive needs the
+ * in-kernel exchange: no master, a LockFree/sharded one, or a TC engine). A host that stops pushing for
  * 20 s makes the kernel finish with DS_FLAG_STREAM_TIMEOUT rather than hang. */
 int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss_host);
 int ds_engine_stream_push(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows);

@@ -1137,7 +1137,11 @@ int stream_prepare(ds_engine* e, uint64_t steps, double* loss_host) {
   if (e->ring_active) return set_error(DS_E_STATE, "engine_stream: a stream is already open");
   if (!e->fused || e->model.hidden.size() != 1 || (e->model.n_features % 4) != 0)
     return set_error(DS_E_CONTRACT, "engine_stream: needs the fused one-hidden-layer engine and n_features %% 4 == 0");
-  if (e->hp.adaptive) return set_error(DS_E_CONTRACT, "engine_stream: fixed-period policy only");
+  // the adaptive policy (engine.cpp:35-48) runs in the kernel; it needs the exchange to be
+  // in-kernel too (a host-ordered master would split the launch at value-dependent points)
+  if (e->hp.adaptive && e->master && !dsb::in_kernel_ok(e))
+    return set_error(DS_E_CONTRACT, "engine_stream: an adaptive policy needs an in-kernel exchange (LockFree or "
+                     "sharded master, or a tensor-core engine)");
   if (loss_host) {  // the kernel stores into it directly: it must be mapped (pinned) host memory
     cudaPointerAttributes pa{};
     if (cudaPointerGetAttributes(&pa, loss_host) != cudaSuccess || pa.type != cudaMemoryTypeHost) {

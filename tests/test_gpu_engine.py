@@ -187,10 +187,12 @@ def test_engine_numeric_error(L, orc, kind):
         L.lib.ds_engine_destroy(e)
 
 
-@pytest.mark.parametrize("m,n,b,tau,steps", [(ModelSpec.mlp(20, [16], 3), 300, 16, 5, 45),
-                                             (ModelSpec.mlp(784, [256], 10), 2000, 32, 10, 120),
-                                             (ModelSpec.mlp(20, [33], 3), 70, 32, 4, 13)])  # ragged batches
-def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps):
+@pytest.mark.parametrize("m,n,b,tau,steps,adaptive", [(ModelSpec.mlp(20, [16], 3), 300, 16, 5, 45, False),
+                                                      (ModelSpec.mlp(784, [256], 10), 2000, 32, 10, 120, False),
+                                                      (ModelSpec.mlp(20, [33], 3), 70, 32, 4, 13, False),  # ragged
+                                                      (ModelSpec.mlp(20, [16], 3), 300, 16, 5, 90, True),
+                                                      (ModelSpec.mlp(784, [256], 10), 2000, 32, 10, 120, True)])
+def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps, adaptive):
     """Stream mode (one persistent launch fed batch by batch from pinned host memory)
     must reproduce the engine's own device-resident run on the same batch sequence (its
     ShardSweeper order) bit for bit, including the exchanges and the per-step losses the
@@ -200,6 +202,10 @@ def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps):
     init = orc.init_params(m, 9)
     P = len(init)
     hp = Hyper(eta=0.05, tau=tau, batch_size=b, i_max=steps)
+    if adaptive:  # the reference's adaptive rule (engine.cpp:35-48), cut = 0.5 x the first batch's loss
+        cut = orc.resolve_loss_cut(m, X, y, m.n_classes, Hyper(eta=0.05, tau=tau, batch_size=b, i_max=steps,
+                                                               adaptive=True), 31, init) * 0.5 / 20.0
+        hp = Hyper(eta=0.05, tau=tau, batch_size=b, i_max=steps, adaptive=True, loss_cut=cut)
     master0 = orc.init_params(m, 10)
     outs = []
     for mode in ("run", "stream", "stream_rows"):
@@ -254,6 +260,8 @@ def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps):
         assert np.array_equal(x0, x1)
         assert np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
         assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
+    if adaptive:  # the rule really fired, at value-dependent points
+        assert 1 <= int(x0.sum()) < steps // 2
 
 
 def test_cluster_split_logits_bit_identical(L, orc, monkeypatch):

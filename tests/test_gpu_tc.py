@@ -150,19 +150,28 @@ def test_tc_split_runs_equal_one_run(L, orc):
         assert np.array_equal(p, out[0][0]) and np.array_equal(s, out[0][1]) and np.array_equal(lo, out[0][2])
 
 
-def test_tc_stream_and_host_steps_equal_device_run(L, orc, api):
+@pytest.mark.parametrize("adaptive", [False, True])
+def test_tc_stream_and_host_steps_equal_device_run(L, orc, api, adaptive):
     """Host-fed batches (stream mode, the e2e path; and ds_engine_step_host) give exactly the
-    device-resident run's trajectory on the same batches."""
+    device-resident run's trajectory on the same batches — with the Fixed and the Adaptive
+    policy (engine.cpp:35-48, evaluated in the kernel)."""
     m = ModelSpec.mlp(784, [256], 10)
     X, y = orc.gen_synthetic(1000, 784, 10, 0.1, 1.0, 3)
     init = orc.init_params(m, 9)
     P, steps, B = len(init), 40, 32
     hp = Hyper(eta=0.05, tau=10, batch_size=B, i_max=steps)
+    if adaptive:
+        cut = 3.0 / 20.0 * orc.resolve_loss_cut(m, X, y, 10, Hyper(eta=0.05, tau=10, batch_size=B, i_max=steps,
+                                                                    adaptive=True), 31, init)
+        hp = Hyper(eta=0.05, tau=10, batch_size=B, i_max=steps, adaptive=True, loss_cut=cut)
     idx, rows = api.sweep_batches(len(y), B, 31, steps)
     e0 = make_engine(L, m, X, y, 10, hp, 31, init)
     L.check(L.lib.ds_engine_run(e0, steps, 0, None))
     L.check(L.lib.ds_engine_sync(e0))
     ref_p, ref_l = params_of(L, e0, P), engine_log(L, e0, 0, steps)[0]
+    ref_x = engine_log(L, e0, 0, steps)[2]
+    if adaptive:
+        assert 2 <= int(ref_x.sum()) < steps // 2
     L.lib.ds_engine_destroy(e0)
     # stream mode with host gathers
     import torch
@@ -178,6 +187,7 @@ def test_tc_stream_and_host_steps_equal_device_run(L, orc, api):
     L.check(L.lib.ds_engine_stream_end(e1))
     assert np.array_equal(params_of(L, e1, P), ref_p) and np.array_equal(engine_log(L, e1, 0, steps)[0], ref_l)
     assert np.array_equal(loss_h.numpy(), ref_l)  # the zero-copy per-step losses
+    assert np.array_equal(engine_log(L, e1, 0, steps)[2], ref_x)
     L.lib.ds_engine_destroy(e1)
     # one host step at a time
     e2 = make_engine(L, m, X, y, 10, hp, 31, init)
