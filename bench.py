@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--tau", type=int, default=10)
     ap.add_argument("--workers", type=int, default=2, help="EASGD workers per GPU (BASELINE config 1: 2)")
     ap.add_argument("--min-window-ms", type=float, default=200.0, help="repeat the K-step launch up to this")
-    ap.add_argument("--e2e-steps", type=int, default=2000)
+    ap.add_argument("--e2e-steps", type=int, default=20000)
     ap.add_argument("--det-steps", type=int, default=20000, help="timed steps of the deterministic config-1 leg")
     ap.add_argument("--exchange-params", type=int, default=256 * 1024 * 1024)
     ap.add_argument("--sync-params", type=int, default=62_378_344, help="synchronous round size (AlexNet's P)")
@@ -534,13 +534,15 @@ def det_leg(args, L, api, torch, shards, seeds, init):
 def e2e_group_leg(args, L, api, engines, shards, seeds, rank, world, n):
     """The same training through the C-ABI with HOST buffers (stream mode): one launch
     trains the GPU's workers while the host, per worker, runs the reference worker's
-    ShardSweeper (the epoch permutations are computed inside the timed window), gathers
-    each batch from the host shard into a pinned ring slot and pushes it (H2D) -- one host
-    thread per worker; the kernel writes every step's loss to mapped pinned host memory
-    (D2H). Wall clock from stream_begin to the last stream_end, max over ranks."""
+    ShardSweeper (the epoch permutations are computed inside the timed window) and
+    gather_batch: ds_engine_stream_push_rows_n gathers each step's rows from the host shard
+    and writes them as bf16 into the engine's zero-copy ring in pinned, mapped host memory,
+    which the kernel's TMA gathers read across PCIe (H2D) -- one host thread per worker; the
+    kernel writes every step's loss to mapped pinned host memory (D2H). Wall clock from
+    stream_begin to the last stream_end, max over ranks."""
     import torch
     import torch.distributed as dist
-    K, B, Wk = min(args.e2e_steps, args.steps * 20), args.batch, len(engines)
+    K, B, Wk = args.e2e_steps, args.batch, len(engines)
     losses = [torch.zeros(K, dtype=torch.float64, pin_memory=True) for _ in range(Wk)]
     lp = (C.c_void_p * Wk)(*[lo.data_ptr() for lo in losses])
     arr = (C.c_void_p * Wk)(*[e.value for e in engines])
@@ -552,10 +554,10 @@ def e2e_group_leg(args, L, api, engines, shards, seeds, rank, world, n):
             Xh, yh = host[k]
             idx, sizes = api.sweep_batches(len(yh), B, seed, steps)  # ShardSweeper, inside the window
             idx = np.ascontiguousarray(idx, dtype=np.uint32)
-            xp, yp = C.c_void_p(Xh.ctypes.data), C.c_void_p(yh.ctypes.data)
-            push = L.lib.ds_engine_stream_push_rows
-            for s in range(steps):
-                L.check(push(engines[k], xp, yp, C.c_void_p(idx[s].ctypes.data), int(sizes[s])))
+            sizes = np.ascontiguousarray(sizes, dtype=np.uint32)
+            L.check(L.lib.ds_engine_stream_push_rows_n(engines[k], C.c_void_p(Xh.ctypes.data),
+                                                       C.c_void_p(yh.ctypes.data), C.c_void_p(idx.ctypes.data),
+                                                       C.c_void_p(sizes.ctypes.data), steps))
             L.check(L.lib.ds_engine_stream_end(engines[k]))
         except Exception as ex:  # reported below
             errs.append(str(ex))
@@ -584,13 +586,15 @@ def e2e_group_leg(args, L, api, engines, shards, seeds, rank, world, n):
     t = torch.tensor([secs], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    pitch = (F + 7) // 8 * 8
     return {"value": n * Wk * B * K / t.item(), "unit": "samples/s",
-            "h2d_bytes_per_step": Wk * (B * F * 4 + B * 4 + 4), "d2h_bytes_per_step": Wk * 8, "steps": K,
-            "losses_finite": ok,
-            "path": "ds_engine_stream_begin_group + per worker ds_engine_stream_push_rows (host ShardSweeper, "
-                    "gather_batch into a pinned ring slot, H2D copy, bf16 conversion on the copy stream) from one "
-                    "host thread per worker; one tensor-core launch trains all of the GPU's workers; per-step losses "
-                    "written to mapped host memory; wall clock from stream_begin to the last stream_end"}
+            "h2d_bytes_per_step": Wk * (B * pitch * 2 + B * 4 + 4), "d2h_bytes_per_step": Wk * 8, "steps": K,
+            "wall_s": t.item(), "losses_finite": ok,
+            "path": "ds_engine_stream_begin_group + per worker ds_engine_stream_push_rows_n (host ShardSweeper, "
+                    "gather_batch + bf16 cast into a zero-copy ring in pinned mapped host memory, read by the "
+                    "kernel's TMA across PCIe) from one host thread per worker; one tensor-core launch trains all "
+                    "of the GPU's workers; per-step losses written to mapped host memory; wall clock from "
+                    "stream_begin to the last stream_end"}
 
 
 def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind, nvl=None):

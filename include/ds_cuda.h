@@ -375,6 +375,13 @@ int ds_engine_stream_push(ds_engine* e, const float* X_host, const uint32_t* y_h
  * engine-owned pinned staging slot (gather_batch, model.cpp:12-21) and pushed. */
 int ds_engine_stream_push_rows(ds_engine* e, const float* X_host, const uint32_t* y_host, const uint32_t* idx,
                                uint32_t rows);
+/* As ds_engine_stream_push_rows for nsteps consecutive steps in one call: step s takes
+ * rows[s] row indices from idx[s * batch_size ...] (the ShardSweeper layout). Blocks while
+ * the ring is full. Tensor-core engines write the rows as bf16 straight into a zero-copy
+ * ring in mapped host memory that the kernel's TMA gathers read across PCIe (no CUDA call
+ * per step). */
+int ds_engine_stream_push_rows_n(ds_engine* e, const float* X_host, const uint32_t* y_host, const uint32_t* idx,
+                                 const uint32_t* rows, uint64_t nsteps);
 int ds_engine_stream_end(ds_engine* e);
 /* Stream mode for several tensor-core engines trained in ONE launch (ds_engine_run_group):
  * each engine gets its own ring, pushes and ds_engine_stream_end as above; loss_host[i]

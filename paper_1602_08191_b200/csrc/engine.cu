@@ -15,6 +15,7 @@
 //
 // The policy is evaluated on the device (engine.cpp:35-48) so adaptive exchanges need
 // no host sync; the exchange kernels test the device-side fire flag themselves.
+#include <atomic>
 #include <chrono>
 #include <algorithm>
 #include <cmath>
@@ -135,6 +136,13 @@ struct ds_engine {
   bool ring_active = false;
   uint64_t ring_steps = 0, ring_pushed = 0;
   float* ring_hX = nullptr;      // engine-owned pinned staging [kRing][B][F] (ds_engine_stream_push_rows)
+  // tensor-core engines: a ZERO-COPY ring in pinned, mapped host memory — the host writes
+  // each step's rows as bf16 ([kRing][B][tc_pitch(F)]), labels and a release-stored
+  // sequence word; the kernel's TMA gathers read the rows across PCIe (no copy engine, no
+  // CUDA call per step)
+  uint16_t* zc_X = nullptr;
+  uint32_t* zc_y = nullptr;     // [kRing][B]
+  uint32_t* zc_words = nullptr; // [kRing] (rows << 20) | (step + 1)
   uint32_t* ring_hy = nullptr;
   double* ring_loss = nullptr;
   float mu = 0.0f;            // momentum (layered path), ds_engine_set_momentum
@@ -445,6 +453,10 @@ int fused_args(ds_engine* e, uint64_t steps, bool in_kernel_exchange, FusedArgs&
     a.ring_y = e->ring_y;
     a.ring_rows = e->ring_words;
     a.ring_ready = e->ring_words + ds_engine::kRing;
+    if (e->tc) {  // the zero-copy host ring (mapped: UVA pointers are device-accessible)
+      a.ring_y = e->zc_y;
+      a.ring_ready = e->zc_words;
+    }
     a.ring_consumed = e->ring_consumed;
     a.ring_loss = e->ring_loss;
   }
@@ -763,6 +775,9 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->d_tickets);
   cudaFree(e->velocity);
   if (e->ring_hX) cudaFreeHost(e->ring_hX);
+  if (e->zc_X) cudaFreeHost(e->zc_X);
+  if (e->zc_y) cudaFreeHost(e->zc_y);
+  if (e->zc_words) cudaFreeHost(e->zc_words);
   if (e->ring_hy) cudaFreeHost(e->ring_hy);
   if (e->step_graph) cudaGraphExecDestroy(e->step_graph);
   for (auto& g : e->sync_graph)
@@ -1153,21 +1168,29 @@ int stream_prepare(ds_engine* e, uint64_t steps, double* loss_host) {
   if (steps == 0) return DS_OK;
   dsb::DeviceScope ds(e->device);
   const uint64_t B = e->hp.batch_size, F = e->model.n_features, K = ds_engine::kRing;
-  if (!e->ring_X) {
+  if (!e->ring_consumed)
+    DS_CUDA_TRY(cudaHostAlloc(&e->ring_consumed, sizeof(unsigned long long), cudaHostAllocMapped));
+  if (!e->tc && !e->ring_X) {
     DS_CUDA_TRY(cudaMalloc(&e->ring_X, K * B * F * sizeof(float)));
     DS_CUDA_TRY(cudaMalloc(&e->ring_y, K * B * sizeof(uint32_t)));
     DS_CUDA_TRY(cudaMalloc(&e->ring_words, 2 * K * sizeof(uint32_t)));
     DS_CUDA_TRY(cudaMallocHost(&e->ring_src, 2 * K * sizeof(uint32_t)));
-    DS_CUDA_TRY(cudaHostAlloc(&e->ring_consumed, sizeof(unsigned long long), cudaHostAllocMapped));
     DS_CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
   }
-  if (e->tc && !e->tc_ring) {  // bf16 copies of the slots, converted on the copy stream
-    DS_CUDA_TRY(cudaMalloc(&e->tc_ring, K * B * dsb::tc_pitch(static_cast<uint32_t>(F)) * 2));
-    DS_CUDA_TRY(cudaMemset(e->tc_ring, 0, K * B * dsb::tc_pitch(static_cast<uint32_t>(F)) * 2));
-    DS_TRY(dsb::tc_make_map(&e->tm_ring, e->tc_ring, K * B, static_cast<uint32_t>(F)));
+  if (e->tc && !e->zc_X) {  // zero-copy host ring, bf16 rows padded to the TMA pitch
+    const uint64_t pitch = dsb::tc_pitch(static_cast<uint32_t>(F));
+    DS_CUDA_TRY(cudaHostAlloc(&e->zc_X, K * B * pitch * 2, cudaHostAllocMapped));
+    DS_CUDA_TRY(cudaHostAlloc(&e->zc_y, K * B * sizeof(uint32_t), cudaHostAllocMapped));
+    DS_CUDA_TRY(cudaHostAlloc(&e->zc_words, K * sizeof(uint32_t), cudaHostAllocMapped));
+    std::memset(e->zc_X, 0, K * B * pitch * 2);
+    std::memset(e->zc_y, 0, K * B * sizeof(uint32_t));
+    DS_TRY(dsb::tc_make_map(&e->tm_ring, e->zc_X, K * B, static_cast<uint32_t>(F)));
   }
   DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
-  DS_CUDA_TRY(cudaMemsetAsync(e->ring_words, 0, 2 * K * sizeof(uint32_t), e->stream));
+  if (e->tc)
+    std::memset(e->zc_words, 0, K * sizeof(uint32_t));  // no kernel reads it yet
+  else
+    DS_CUDA_TRY(cudaMemsetAsync(e->ring_words, 0, 2 * K * sizeof(uint32_t), e->stream));
   *reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) = 0;
   DS_TRY(dsb::ensure_log(e, e->queued + steps));
   e->ring_active = true;
@@ -1216,7 +1239,8 @@ int stream_slot_ready(ds_engine* e, uint32_t rows) {
   const uint64_t s = e->ring_pushed, K = ds_engine::kRing;
   if (s >= K) {
     const auto t0 = std::chrono::steady_clock::now();
-    while (*reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) < s - K + 1) {
+    for (uint64_t spin = 0; *reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) < s - K + 1; ++spin) {
+      if ((spin & 1023) != 1023) continue;  // the CUDA / clock checks are rare: the word is hot
       if (cudaStreamQuery(e->stream) != cudaErrorNotReady)
         return set_error(DS_E_STATE, "engine_stream_push: the stream kernel is no longer running");
       if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
@@ -1226,21 +1250,73 @@ int stream_slot_ready(ds_engine* e, uint32_t rows) {
   return DS_OK;
 }
 
+// f32 -> bf16, round to nearest even, NaN -> 0x7FFF: the same bits as the device's
+// __float2bfloat16_rn (cvt.rn.bf16.f32) in tc_rows_to_bf16
+inline void rows_to_bf16_host(const float* src, uint32_t F, uint16_t* dst) {
+  for (uint32_t f = 0; f < F; ++f) {
+    uint32_t u;
+    std::memcpy(&u, src + f, 4);
+    const uint32_t r = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+    dst[f] = static_cast<uint16_t>((u & 0x7FFFFFFFu) > 0x7F800000u ? 0x7FFFu : r);
+  }
+}
+
+// tensor-core engines: write step s's rows into the zero-copy ring and publish its word.
+// row(r) gives batch row r's f32 source, label(r) its label.
+template <typename RowFn, typename LabelFn>
+int zc_enqueue(ds_engine* e, uint32_t rows, RowFn row, LabelFn label) {
+  const uint64_t s = e->ring_pushed, K = ds_engine::kRing, B = e->hp.batch_size;
+  const uint32_t F = e->model.n_features;
+  const uint64_t slot = s % K, pitch = dsb::tc_pitch(F);
+  uint16_t* dst = e->zc_X + slot * B * pitch;
+  uint32_t* ydst = e->zc_y + slot * B;
+  for (uint32_t r = 0; r < rows; ++r) {  // gather_batch (model.cpp:12-21) + the bf16 operand cast
+    rows_to_bf16_host(row(r), F, dst + r * pitch);
+    ydst[r] = label(r);
+  }
+  // release: the rows and labels are visible before the word (x86 stores are ordered; the
+  // kernel reads the word with ld.acquire.sys, then the rows through TMA)
+  std::atomic_thread_fence(std::memory_order_release);
+  reinterpret_cast<volatile uint32_t*>(e->zc_words)[slot] = (rows << 20) | (static_cast<uint32_t>(s + 1) & 0xFFFFFu);
+  ++e->ring_pushed;
+  return DS_OK;
+}
+
 int stream_enqueue(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows) {
   const uint64_t s = e->ring_pushed, K = ds_engine::kRing, B = e->hp.batch_size, F = e->model.n_features;
+  if (e->tc)
+    return zc_enqueue(e, rows, [&](uint32_t r) { return X_host + static_cast<uint64_t>(r) * F; },
+                      [&](uint32_t r) { return y_host[r]; });
   const uint64_t slot = s % K;
-  // one word carries the row count and the step (mod 2^20; slots are reused 4 steps apart)
+  // one word carries the row count and the step (mod 2^20; slots are reused kRing steps apart)
   e->ring_src[K + slot] = (rows << 20) | (static_cast<uint32_t>(s + 1) & 0xFFFFFu);
   cudaStream_t cs = e->copy_stream;
   DS_CUDA_TRY(cudaMemcpyAsync(e->ring_X + slot * B * F, X_host, rows * F * sizeof(float), cudaMemcpyDefault, cs));
-  if (e->tc)  // the tensor-core step gathers bf16 rows; convert the slot before its ready word
-    DS_TRY(dsb::tc_rows_to_bf16(e->ring_X + slot * B * F, rows, static_cast<uint32_t>(F),
-                                static_cast<char*>(e->tc_ring) + slot * B * dsb::tc_pitch(static_cast<uint32_t>(F)) * 2, cs));
   DS_CUDA_TRY(cudaMemcpyAsync(e->ring_y + slot * B, y_host, rows * sizeof(uint32_t), cudaMemcpyDefault, cs));
   DS_CUDA_TRY(cudaMemcpyAsync(e->ring_words + K + slot, e->ring_src + K + slot, sizeof(uint32_t),
                               cudaMemcpyHostToDevice, cs));
   ++e->ring_pushed;
   return DS_OK;
+}
+
+int push_rows_one(ds_engine* e, const float* X_host, const uint32_t* y_host, const uint32_t* idx, uint32_t rows) {
+  DS_TRY(stream_slot_ready(e, rows));
+  const uint64_t K = ds_engine::kRing, B = e->hp.batch_size, F = e->model.n_features;
+  if (e->tc)  // gather + convert straight into the zero-copy ring
+    return zc_enqueue(e, rows, [&](uint32_t r) { return X_host + static_cast<uint64_t>(idx[r]) * F; },
+                      [&](uint32_t r) { return y_host[idx[r]]; });
+  if (!e->ring_hX) {
+    DS_CUDA_TRY(cudaHostAlloc(&e->ring_hX, K * B * F * sizeof(float), cudaHostAllocDefault));
+    DS_CUDA_TRY(cudaHostAlloc(&e->ring_hy, K * B * sizeof(uint32_t), cudaHostAllocDefault));
+  }
+  const uint64_t slot = e->ring_pushed % K;  // free: its previous copy has been consumed
+  float* hx = e->ring_hX + slot * B * F;
+  uint32_t* hy = e->ring_hy + slot * B;
+  for (uint32_t r = 0; r < rows; ++r) {  // gather_batch (model.cpp:12-21) into pinned staging
+    std::memcpy(hx + static_cast<uint64_t>(r) * F, X_host + static_cast<uint64_t>(idx[r]) * F, F * sizeof(float));
+    hy[r] = y_host[idx[r]];
+  }
+  return stream_enqueue(e, hx, hy, rows);
 }
 }  // namespace
 
@@ -1255,20 +1331,16 @@ extern "C" int ds_engine_stream_push_rows(ds_engine* e, const float* X_host, con
                                           const uint32_t* idx, uint32_t rows) {
   if (!e || !X_host || !y_host || !idx) return set_error(DS_E_CONTRACT, "engine_stream_push_rows: null");
   dsb::DeviceScope ds(e->device);
-  DS_TRY(stream_slot_ready(e, rows));
-  const uint64_t K = ds_engine::kRing, B = e->hp.batch_size, F = e->model.n_features;
-  if (!e->ring_hX) {
-    DS_CUDA_TRY(cudaHostAlloc(&e->ring_hX, K * B * F * sizeof(float), cudaHostAllocDefault));
-    DS_CUDA_TRY(cudaHostAlloc(&e->ring_hy, K * B * sizeof(uint32_t), cudaHostAllocDefault));
-  }
-  const uint64_t slot = e->ring_pushed % K;  // free: its previous copy has been consumed
-  float* hx = e->ring_hX + slot * B * F;
-  uint32_t* hy = e->ring_hy + slot * B;
-  for (uint32_t r = 0; r < rows; ++r) {  // gather_batch (model.cpp:12-21) into pinned staging
-    std::memcpy(hx + static_cast<uint64_t>(r) * F, X_host + static_cast<uint64_t>(idx[r]) * F, F * sizeof(float));
-    hy[r] = y_host[idx[r]];
-  }
-  return stream_enqueue(e, hx, hy, rows);
+  return push_rows_one(e, X_host, y_host, idx, rows);
+}
+
+extern "C" int ds_engine_stream_push_rows_n(ds_engine* e, const float* X_host, const uint32_t* y_host,
+                                            const uint32_t* idx, const uint32_t* rows, uint64_t nsteps) {
+  if (!e || !X_host || !y_host || !idx || !rows) return set_error(DS_E_CONTRACT, "engine_stream_push_rows_n: null");
+  dsb::DeviceScope ds(e->device);
+  const uint64_t B = e->hp.batch_size;
+  for (uint64_t s = 0; s < nsteps; ++s) DS_TRY(push_rows_one(e, X_host, y_host, idx + s * B, rows[s]));
+  return DS_OK;
 }
 
 extern "C" int ds_engine_stream_end(ds_engine* e) {

@@ -479,7 +479,11 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
         }
         R = __shfl_sync(0xffffffffu, nrows, 0);
         row = slot * B + (lane < R ? lane : 0u);
-        if (lane < R) y = __ldcg(A.ring_y + static_cast<uint64_t>(slot) * B + lane);
+        // the ring lives in mapped host memory, rewritten every ring_slots steps: labels are
+        // read uncached after the acquire, and the async proxy (the TMA gathers below) is
+        // ordered after it
+        if (lane < R) y = __ldcv(A.ring_y + static_cast<uint64_t>(slot) * B + lane);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
       } else {
         R = A.plan_rows[s];
         const uint32_t r0 = A.plan[s * B];

@@ -158,7 +158,7 @@ def test_tc_stream_and_host_steps_equal_device_run(L, orc, api, adaptive):
     m = ModelSpec.mlp(784, [256], 10)
     X, y = orc.gen_synthetic(1000, 784, 10, 0.1, 1.0, 3)
     init = orc.init_params(m, 9)
-    P, steps, B = len(init), 40, 32
+    P, steps, B = len(init), 120, 32  # the 8-slot host ring is reused 15 times
     hp = Hyper(eta=0.05, tau=10, batch_size=B, i_max=steps)
     if adaptive:
         cut = 3.0 / 20.0 * orc.resolve_loss_cut(m, X, y, 10, Hyper(eta=0.05, tau=10, batch_size=B, i_max=steps,
@@ -171,7 +171,7 @@ def test_tc_stream_and_host_steps_equal_device_run(L, orc, api, adaptive):
     ref_p, ref_l = params_of(L, e0, P), engine_log(L, e0, 0, steps)[0]
     ref_x = engine_log(L, e0, 0, steps)[2]
     if adaptive:
-        assert 2 <= int(ref_x.sum()) < steps // 2
+        assert 1 <= int(ref_x.sum()) < steps // 2
     L.lib.ds_engine_destroy(e0)
     # stream mode with host gathers
     import torch
@@ -189,6 +189,28 @@ def test_tc_stream_and_host_steps_equal_device_run(L, orc, api, adaptive):
     assert np.array_equal(loss_h.numpy(), ref_l)  # the zero-copy per-step losses
     assert np.array_equal(engine_log(L, e1, 0, steps)[2], ref_x)
     L.lib.ds_engine_destroy(e1)
+    # the whole session's pushes in one call (ring reuse: steps >> DS_STREAM_RING), and
+    # user-gathered f32 batches through ds_engine_stream_push
+    e3 = make_engine(L, m, X, y, 10, hp, 31, init)
+    idx_all = np.ascontiguousarray(idx, np.uint32)
+    rows_all = np.ascontiguousarray(rows, np.uint32)
+    L.check(L.lib.ds_engine_stream_begin(e3, steps, C.c_void_p(loss_h.data_ptr())))
+    L.check(L.lib.ds_engine_stream_push_rows_n(e3, Xc.ctypes.data, yc.ctypes.data, idx_all.ctypes.data,
+                                               rows_all.ctypes.data, steps))
+    L.check(L.lib.ds_engine_stream_end(e3))
+    assert np.array_equal(params_of(L, e3, P), ref_p) and np.array_equal(engine_log(L, e3, 0, steps)[0], ref_l)
+    L.lib.ds_engine_destroy(e3)
+    e4 = make_engine(L, m, X, y, 10, hp, 31, init)
+    L.check(L.lib.ds_engine_stream_begin(e4, steps, C.c_void_p(loss_h.data_ptr())))
+    keep = []
+    for s in range(steps):
+        xb = np.ascontiguousarray(X[idx[s, :rows[s]]], np.float32)
+        yb = np.ascontiguousarray(y[idx[s, :rows[s]]], np.uint32)
+        keep.append((xb, yb))
+        L.check(L.lib.ds_engine_stream_push(e4, xb.ctypes.data, yb.ctypes.data, int(rows[s])))
+    L.check(L.lib.ds_engine_stream_end(e4))
+    assert np.array_equal(params_of(L, e4, P), ref_p) and np.array_equal(engine_log(L, e4, 0, steps)[0], ref_l)
+    L.lib.ds_engine_destroy(e4)
     # one host step at a time
     e2 = make_engine(L, m, X, y, 10, hp, 31, init)
     for s in range(steps):
