@@ -25,6 +25,9 @@
 #include <mutex>
 #include <numeric>
 #include <set>
+#include <string>
+#include <thread>
+#include <vector>
 
 #include "deepspark/rng.hpp"
 #include "ds_common.cuh"
@@ -136,13 +139,17 @@ struct ds_engine {
   bool ring_active = false;
   uint64_t ring_steps = 0, ring_pushed = 0;
   float* ring_hX = nullptr;      // engine-owned pinned staging [kRing][B][F] (ds_engine_stream_push_rows)
-  // tensor-core engines: a ZERO-COPY ring in pinned, mapped host memory — the host writes
-  // each step's rows as bf16 ([kRing][B][tc_pitch(F)]), labels and a release-stored
-  // sequence word; the kernel's TMA gathers read the rows across PCIe (no copy engine, no
-  // CUDA call per step)
-  uint16_t* zc_X = nullptr;
-  uint32_t* zc_y = nullptr;     // [kRing][B]
-  uint32_t* zc_words = nullptr; // [kRing] (rows << 20) | (step + 1)
+  // tensor-core engines: the stream ring tc_ring is [kTcRing][B + 1][tc_pitch(F)] bf16 in
+  // HBM (row B of a slot holds its labels). The host gathers each step's rows straight into
+  // a pinned twin as bf16 and the copy engine moves a group of slots per DMA, then the
+  // group's sequence words (ring_words): two CUDA calls per group of steps
+  static constexpr uint32_t kTcRing = 16, kTcGroup = 4;
+  uint16_t* tch_ring = nullptr;   // pinned host twin of tc_ring
+  uint32_t* tch_words = nullptr;  // pinned host sources of ring_words
+  // a DS_FUSED_PROFILE buffer of a stream-mode launch, reported at ds_engine_stream_end
+  unsigned long long* prof_pending = nullptr;
+  uint64_t prof_steps = 0, prof_n = 0;
+  const char* prof_path = nullptr;
   uint32_t* ring_hy = nullptr;
   double* ring_loss = nullptr;
   float mu = 0.0f;            // momentum (layered path), ds_engine_set_momentum
@@ -453,9 +460,15 @@ int fused_args(ds_engine* e, uint64_t steps, bool in_kernel_exchange, FusedArgs&
     a.ring_y = e->ring_y;
     a.ring_rows = e->ring_words;
     a.ring_ready = e->ring_words + ds_engine::kRing;
-    if (e->tc) {  // the zero-copy host ring (mapped: UVA pointers are device-accessible)
-      a.ring_y = e->zc_y;
-      a.ring_ready = e->zc_words;
+    a.ring_slot_rows = static_cast<uint32_t>(e->hp.batch_size);
+    a.ring_y_stride = static_cast<uint32_t>(e->hp.batch_size);
+    if (e->tc) {  // bf16 slots of B + 1 rows, the labels in the last row
+      const uint64_t B = e->hp.batch_size, pitch = tc_pitch(e->model.n_features);
+      a.ring_slots = ds_engine::kTcRing;
+      a.ring_slot_rows = static_cast<uint32_t>(B + 1);
+      a.ring_y = reinterpret_cast<const uint32_t*>(static_cast<const char*>(e->tc_ring) + B * pitch * 2);
+      a.ring_y_stride = static_cast<uint32_t>((B + 1) * pitch / 2);
+      a.ring_ready = e->ring_words;
     }
     a.ring_consumed = e->ring_consumed;
     a.ring_loss = e->ring_loss;
@@ -463,33 +476,10 @@ int fused_args(ds_engine* e, uint64_t steps, bool in_kernel_exchange, FusedArgs&
   return DS_OK;
 }
 
-int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
-  FusedArgs a;
-  DS_TRY(fused_args(e, steps, in_kernel_exchange, a));
-  // DS_FUSED_PROFILE=<file>: per-phase globaltimer stamps of CTA 0, medians appended
-  const char* prof_path = std::getenv("DS_FUSED_PROFILE");
-  unsigned long long* prof = nullptr;
+// Per-phase medians of a DS_FUSED_PROFILE run (stream mode: at stream_end, once the
+// launch is done).
+int dump_profile(ds_engine* e, unsigned long long* prof, uint64_t steps, uint64_t prof_n, const char* prof_path) {
   const uint64_t G = static_cast<uint64_t>(e->fused_grid);
-  const uint64_t prof_n = steps * (kProfSlots + 2 * G) + 8;
-  if (prof_path && steps >= 8) DS_CUDA_TRY(cudaMalloc(&prof, prof_n * sizeof(unsigned long long)));
-  if (prof) DS_CUDA_TRY(cudaMemsetAsync(prof, 0, prof_n * sizeof(unsigned long long), e->stream));
-  a.prof = prof;
-  a.prof_cta = prof ? prof + steps * kProfSlots : nullptr;
-  if (e->tc) {
-    const CUtensorMap* tm = &e->tm_shard;
-    if (e->ring_active) {
-      tm = &e->tm_ring;
-    } else if (e->hostfed) {  // this step's rows (staged f32 by step_host) as bf16
-      DS_TRY(tc_rows_to_bf16(e->Xb, e->hostfed_rows, e->model.n_features, e->tc_stage, e->stream));
-      tm = &e->tm_stage;
-    }
-    DS_TRY(launch_tc(a, e->tc_nc, *tm, e->stream));
-  }
-  else
-    DS_TRY(launch_fused(a, e->fused_grid, e->stream));
-  e->launches += 1;
-  e->cur ^= static_cast<int>(steps & 1);
-  if (prof) {
     std::vector<unsigned long long> h(prof_n);
     DS_CUDA_TRY(cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream));
     DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
@@ -514,6 +504,12 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
     static const char* mnames[] = {"fwd_t0_t3", "fwd_t3_t6", "fwd_last_commit", "logits_wait_a1",
                                    "a1_to_d1rdy", "dW1_issue", "fwd_all", "fwd_to_d1", "-", "-"};
     if (e->tc && std::getenv("DS_TC_PROF_M")) pairs = mpairs, names = mnames;
+    // TMA warp timeline (DS_TC_PROF_T build): poll word, labels, wait for the X buffer,
+    // issue, and the MMA warp's arrival of the gathered rows
+    static const int tpairs2[][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {3, 5}, {0, 5}, {0, 3}, {0, 0}, {0, 0}};
+    static const char* tnames2[] = {"poll_word", "labels", "wait_xbuf", "issue", "issue_to_landed", "stage_to_landed",
+                                    "start_to_landed", "start_to_stage", "-", "-"};
+    if (e->tc && std::getenv("DS_TC_PROF_T")) pairs = tpairs2, names = tnames2;
     if (FILE* f = std::fopen(prof_path, "a")) {
       std::fprintf(f, "steps=%llu", (unsigned long long)steps);
       if (e->tc && h[steps * kProfSlots])
@@ -569,6 +565,42 @@ int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
       std::fprintf(f, "\n");
       std::fclose(f);
     }
+  return DS_OK;
+}
+
+int run_fused(ds_engine* e, uint64_t steps, bool in_kernel_exchange) {
+  FusedArgs a;
+  DS_TRY(fused_args(e, steps, in_kernel_exchange, a));
+  // DS_FUSED_PROFILE=<file>: per-phase globaltimer stamps of CTA 0, medians appended
+  const char* prof_path = std::getenv("DS_FUSED_PROFILE");
+  unsigned long long* prof = nullptr;
+  const uint64_t G = static_cast<uint64_t>(e->fused_grid);
+  const uint64_t prof_n = steps * (kProfSlots + 2 * G) + 8;
+  if (prof_path && steps >= 8) DS_CUDA_TRY(cudaMalloc(&prof, prof_n * sizeof(unsigned long long)));
+  if (prof) DS_CUDA_TRY(cudaMemsetAsync(prof, 0, prof_n * sizeof(unsigned long long), e->stream));
+  a.prof = prof;
+  a.prof_cta = prof ? prof + steps * kProfSlots : nullptr;
+  if (e->tc) {
+    const CUtensorMap* tm = &e->tm_shard;
+    if (e->ring_active) {
+      tm = &e->tm_ring;
+    } else if (e->hostfed) {  // this step's rows (staged f32 by step_host) as bf16
+      DS_TRY(tc_rows_to_bf16(e->Xb, e->hostfed_rows, e->model.n_features, e->tc_stage, e->stream));
+      tm = &e->tm_stage;
+    }
+    DS_TRY(launch_tc(a, e->tc_nc, *tm, e->stream));
+  }
+  else
+    DS_TRY(launch_fused(a, e->fused_grid, e->stream));
+  e->launches += 1;
+  e->cur ^= static_cast<int>(steps & 1);
+  if (prof && e->ring_active) {  // the launch waits on host pushes: report at stream_end
+    e->prof_pending = prof;
+    e->prof_steps = steps;
+    e->prof_n = prof_n;
+    e->prof_path = prof_path;
+  } else if (prof) {
+    DS_TRY(dump_profile(e, prof, steps, prof_n, prof_path));
   }
   return DS_OK;
 }
@@ -775,9 +807,8 @@ extern "C" int ds_engine_destroy(ds_engine* e) {
   cudaFree(e->d_tickets);
   cudaFree(e->velocity);
   if (e->ring_hX) cudaFreeHost(e->ring_hX);
-  if (e->zc_X) cudaFreeHost(e->zc_X);
-  if (e->zc_y) cudaFreeHost(e->zc_y);
-  if (e->zc_words) cudaFreeHost(e->zc_words);
+  if (e->tch_ring) cudaFreeHost(e->tch_ring);
+  if (e->tch_words) cudaFreeHost(e->tch_words);
   if (e->ring_hy) cudaFreeHost(e->ring_hy);
   if (e->step_graph) cudaGraphExecDestroy(e->step_graph);
   for (auto& g : e->sync_graph)
@@ -1177,20 +1208,20 @@ int stream_prepare(ds_engine* e, uint64_t steps, double* loss_host) {
     DS_CUDA_TRY(cudaMallocHost(&e->ring_src, 2 * K * sizeof(uint32_t)));
     DS_CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
   }
-  if (e->tc && !e->zc_X) {  // zero-copy host ring, bf16 rows padded to the TMA pitch
-    const uint64_t pitch = dsb::tc_pitch(static_cast<uint32_t>(F));
-    DS_CUDA_TRY(cudaHostAlloc(&e->zc_X, K * B * pitch * 2, cudaHostAllocMapped));
-    DS_CUDA_TRY(cudaHostAlloc(&e->zc_y, K * B * sizeof(uint32_t), cudaHostAllocMapped));
-    DS_CUDA_TRY(cudaHostAlloc(&e->zc_words, K * sizeof(uint32_t), cudaHostAllocMapped));
-    std::memset(e->zc_X, 0, K * B * pitch * 2);
-    std::memset(e->zc_y, 0, K * B * sizeof(uint32_t));
-    DS_TRY(dsb::tc_make_map(&e->tm_ring, e->zc_X, K * B, static_cast<uint32_t>(F)));
+  if (e->tc && !e->tc_ring) {
+    const uint64_t KT = ds_engine::kTcRing, pitch = dsb::tc_pitch(static_cast<uint32_t>(F));
+    const uint64_t sb = (B + 1) * pitch * 2;  // bytes per slot
+    DS_CUDA_TRY(cudaMalloc(&e->tc_ring, KT * sb));
+    DS_CUDA_TRY(cudaMemset(e->tc_ring, 0, KT * sb));
+    DS_CUDA_TRY(cudaMalloc(&e->ring_words, KT * sizeof(uint32_t)));
+    DS_CUDA_TRY(cudaHostAlloc(&e->tch_ring, KT * sb, cudaHostAllocDefault));
+    DS_CUDA_TRY(cudaHostAlloc(&e->tch_words, KT * sizeof(uint32_t), cudaHostAllocDefault));
+    std::memset(e->tch_ring, 0, KT * sb);
+    DS_CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+    DS_TRY(dsb::tc_make_map(&e->tm_ring, e->tc_ring, KT * (B + 1), static_cast<uint32_t>(F)));
   }
   DS_CUDA_TRY(cudaStreamSynchronize(e->stream));
-  if (e->tc)
-    std::memset(e->zc_words, 0, K * sizeof(uint32_t));  // no kernel reads it yet
-  else
-    DS_CUDA_TRY(cudaMemsetAsync(e->ring_words, 0, 2 * K * sizeof(uint32_t), e->stream));
+  DS_CUDA_TRY(cudaMemsetAsync(e->ring_words, 0, (e->tc ? ds_engine::kTcRing : 2 * K) * sizeof(uint32_t), e->stream));
   *reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) = 0;
   DS_TRY(dsb::ensure_log(e, e->queued + steps));
   e->ring_active = true;
@@ -1232,61 +1263,63 @@ extern "C" int ds_engine_stream_begin_group(ds_engine** engines, uint32_t n, uin
 namespace {
 // stream mode: validate a push and wait until ring slot (step % kRing) is free again (its
 // previous step has been read by every CTA, which also means its H2D copy completed)
-int stream_slot_ready(ds_engine* e, uint32_t rows) {
-  if (!e->ring_active) return set_error(DS_E_STATE, "engine_stream_push: no open stream");
-  if (e->ring_pushed >= e->ring_steps) return set_error(DS_E_STATE, "engine_stream_push: all steps already pushed");
-  if (rows == 0 || rows > e->hp.batch_size) return set_error(DS_E_CONTRACT, "engine_stream_push: bad row count");
-  const uint64_t s = e->ring_pushed, K = ds_engine::kRing;
-  if (s >= K) {
-    const auto t0 = std::chrono::steady_clock::now();
-    for (uint64_t spin = 0; *reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) < s - K + 1; ++spin) {
-      if ((spin & 1023) != 1023) continue;  // the CUDA / clock checks are rare: the word is hot
-      if (cudaStreamQuery(e->stream) != cudaErrorNotReady)
-        return set_error(DS_E_STATE, "engine_stream_push: the stream kernel is no longer running");
-      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
-        return set_error(DS_E_CUDA, "engine_stream_push: device stopped consuming");
-    }
+// wait until ring slot (step % kRing) is free again: step - kRing has been read by every
+// CTA (which also means its H2D copy completed)
+int wait_slot(ds_engine* e, uint64_t step) {
+  const uint64_t K = e->tc ? ds_engine::kTcRing : ds_engine::kRing;
+  if (step < K) return DS_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t spin = 0; *reinterpret_cast<volatile unsigned long long*>(e->ring_consumed) < step - K + 1; ++spin) {
+    if ((spin & 1023) != 1023) continue;  // the CUDA / clock checks are rare: the word is hot
+    if (cudaStreamQuery(e->stream) != cudaErrorNotReady)
+      return set_error(DS_E_STATE, "engine_stream_push: the stream kernel is no longer running");
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+      return set_error(DS_E_CUDA, "engine_stream_push: device stopped consuming");
   }
   return DS_OK;
 }
 
-// f32 -> bf16, round to nearest even, NaN -> 0x7FFF: the same bits as the device's
-// __float2bfloat16_rn (cvt.rn.bf16.f32) in tc_rows_to_bf16
-inline void rows_to_bf16_host(const float* src, uint32_t F, uint16_t* dst) {
-  for (uint32_t f = 0; f < F; ++f) {
-    uint32_t u;
-    std::memcpy(&u, src + f, 4);
-    const uint32_t r = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
-    dst[f] = static_cast<uint16_t>((u & 0x7FFFFFFFu) > 0x7F800000u ? 0x7FFFu : r);
-  }
+// stream mode: validate a push and wait for its slot
+int stream_slot_ready(ds_engine* e, uint32_t rows) {
+  if (!e->ring_active) return set_error(DS_E_STATE, "engine_stream_push: no open stream");
+  if (e->ring_pushed >= e->ring_steps) return set_error(DS_E_STATE, "engine_stream_push: all steps already pushed");
+  if (rows == 0 || rows > e->hp.batch_size) return set_error(DS_E_CONTRACT, "engine_stream_push: bad row count");
+  return wait_slot(e, e->ring_pushed);
 }
 
-// tensor-core engines: write step s's rows into the zero-copy ring and publish its word.
-// row(r) gives batch row r's f32 source, label(r) its label.
-template <typename RowFn, typename LabelFn>
-int zc_enqueue(ds_engine* e, uint32_t rows, RowFn row, LabelFn label) {
-  const uint64_t s = e->ring_pushed, K = ds_engine::kRing, B = e->hp.batch_size;
+// tensor-core engines: gather step `step`'s rows (X + idx[r] * F, or X + r * F when idx is
+// null) as bf16 into its slot of the pinned twin, labels in the slot's last row, and set
+// the slot's word. The caller waited for the slot; tc_flush moves it to the device.
+void tc_fill(ds_engine* e, uint64_t step, const float* X, const uint32_t* y, const uint32_t* idx, uint32_t rows) {
+  const uint64_t KT = ds_engine::kTcRing, B = e->hp.batch_size;
   const uint32_t F = e->model.n_features;
-  const uint64_t slot = s % K, pitch = dsb::tc_pitch(F);
-  uint16_t* dst = e->zc_X + slot * B * pitch;
-  uint32_t* ydst = e->zc_y + slot * B;
-  for (uint32_t r = 0; r < rows; ++r) {  // gather_batch (model.cpp:12-21) + the bf16 operand cast
-    rows_to_bf16_host(row(r), F, dst + r * pitch);
-    ydst[r] = label(r);
-  }
-  // release: the rows and labels are visible before the word (x86 stores are ordered; the
-  // kernel reads the word with ld.acquire.sys, then the rows through TMA)
-  std::atomic_thread_fence(std::memory_order_release);
-  reinterpret_cast<volatile uint32_t*>(e->zc_words)[slot] = (rows << 20) | (static_cast<uint32_t>(s + 1) & 0xFFFFFu);
-  ++e->ring_pushed;
+  const uint64_t slot = step % KT, pitch = dsb::tc_pitch(F);
+  uint16_t* base = e->tch_ring + slot * (B + 1) * pitch;
+  dsb::gather_rows_bf16_host(X, F, idx, rows, base, pitch);  // gather_batch + the bf16 operand cast
+  uint32_t* lab = reinterpret_cast<uint32_t*>(base + B * pitch);
+  for (uint32_t r = 0; r < rows; ++r) lab[r] = y[idx ? idx[r] : r];
+  e->tch_words[slot] = (rows << 20) | (static_cast<uint32_t>(step + 1) & 0xFFFFFu);
+}
+
+// DMA steps [s0, s1) (one group: contiguous slots) and then their words, on the copy stream
+int tc_flush(ds_engine* e, uint64_t s0, uint64_t s1) {
+  const uint64_t KT = ds_engine::kTcRing, B = e->hp.batch_size;
+  const uint64_t sb = (B + 1) * dsb::tc_pitch(e->model.n_features) * 2, slot0 = s0 % KT, n = s1 - s0;
+  DS_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(e->tc_ring) + slot0 * sb, reinterpret_cast<char*>(e->tch_ring) + slot0 * sb,
+                              n * sb, cudaMemcpyHostToDevice, e->copy_stream));
+  DS_CUDA_TRY(cudaMemcpyAsync(e->ring_words + slot0, e->tch_words + slot0, n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                              e->copy_stream));
   return DS_OK;
 }
 
 int stream_enqueue(ds_engine* e, const float* X_host, const uint32_t* y_host, uint32_t rows) {
   const uint64_t s = e->ring_pushed, K = ds_engine::kRing, B = e->hp.batch_size, F = e->model.n_features;
-  if (e->tc)
-    return zc_enqueue(e, rows, [&](uint32_t r) { return X_host + static_cast<uint64_t>(r) * F; },
-                      [&](uint32_t r) { return y_host[r]; });
+  if (e->tc) {
+    tc_fill(e, s, X_host, y_host, nullptr, rows);
+    DS_TRY(tc_flush(e, s, s + 1));
+    ++e->ring_pushed;
+    return DS_OK;
+  }
   const uint64_t slot = s % K;
   // one word carries the row count and the step (mod 2^20; slots are reused kRing steps apart)
   e->ring_src[K + slot] = (rows << 20) | (static_cast<uint32_t>(s + 1) & 0xFFFFFu);
@@ -1302,9 +1335,12 @@ int stream_enqueue(ds_engine* e, const float* X_host, const uint32_t* y_host, ui
 int push_rows_one(ds_engine* e, const float* X_host, const uint32_t* y_host, const uint32_t* idx, uint32_t rows) {
   DS_TRY(stream_slot_ready(e, rows));
   const uint64_t K = ds_engine::kRing, B = e->hp.batch_size, F = e->model.n_features;
-  if (e->tc)  // gather + convert straight into the zero-copy ring
-    return zc_enqueue(e, rows, [&](uint32_t r) { return X_host + static_cast<uint64_t>(idx[r]) * F; },
-                      [&](uint32_t r) { return y_host[idx[r]]; });
+  if (e->tc) {  // gather + bf16 cast straight into the pinned twin, then one DMA
+    tc_fill(e, e->ring_pushed, X_host, y_host, idx, rows);
+    DS_TRY(tc_flush(e, e->ring_pushed, e->ring_pushed + 1));
+    ++e->ring_pushed;
+    return DS_OK;
+  }
   if (!e->ring_hX) {
     DS_CUDA_TRY(cudaHostAlloc(&e->ring_hX, K * B * F * sizeof(float), cudaHostAllocDefault));
     DS_CUDA_TRY(cudaHostAlloc(&e->ring_hy, K * B * sizeof(uint32_t), cudaHostAllocDefault));
@@ -1338,8 +1374,51 @@ extern "C" int ds_engine_stream_push_rows_n(ds_engine* e, const float* X_host, c
                                             const uint32_t* idx, const uint32_t* rows, uint64_t nsteps) {
   if (!e || !X_host || !y_host || !idx || !rows) return set_error(DS_E_CONTRACT, "engine_stream_push_rows_n: null");
   dsb::DeviceScope ds(e->device);
-  const uint64_t B = e->hp.batch_size;
-  for (uint64_t s = 0; s < nsteps; ++s) DS_TRY(push_rows_one(e, X_host, y_host, idx + s * B, rows[s]));
+  const uint64_t B = e->hp.batch_size, K = ds_engine::kRing;
+  if (!e->ring_active) return set_error(DS_E_STATE, "engine_stream_push: no open stream");
+  if (e->ring_pushed + nsteps > e->ring_steps)
+    return set_error(DS_E_STATE, "engine_stream_push_rows_n: %llu steps exceed the %llu the stream was opened for",
+                     static_cast<unsigned long long>(e->ring_pushed + nsteps),
+                     static_cast<unsigned long long>(e->ring_steps));
+  for (uint64_t s = 0; s < nsteps; ++s)
+    if (rows[s] == 0 || rows[s] > B) return set_error(DS_E_CONTRACT, "engine_stream_push: bad row count at step %llu",
+                                                      static_cast<unsigned long long>(s));
+  if (!e->tc) {
+    for (uint64_t s = 0; s < nsteps; ++s) DS_TRY(push_rows_one(e, X_host, y_host, idx + s * B, rows[s]));
+    return DS_OK;
+  }
+  // groups of kTcGroup steps, one DMA each; T producer threads take groups g = t, t + T, ...
+  // (the host's gather is memory-latency bound: one thread cannot keep up with the kernel)
+  const uint64_t G = ds_engine::kTcGroup, base = e->ring_pushed;
+  uint32_t T = 2;
+  if (const char* env = std::getenv("DS_STREAM_FEED_THREADS")) T = static_cast<uint32_t>(std::max(1, std::atoi(env)));
+  // groups in flight <= ring slots / G; a group starts at a multiple of G so it never wraps
+  const uint64_t first = std::min<uint64_t>(nsteps, (G - base % G) % G);  // steps before the next boundary
+  for (uint64_t s = 0; s < first; ++s) DS_TRY(push_rows_one(e, X_host, y_host, idx + s * B, rows[s]));
+  const uint64_t rest = nsteps - first, b0 = base + first, ngroups = (rest + G - 1) / G;
+  T = static_cast<uint32_t>(std::min<uint64_t>({T, ds_engine::kTcRing / G, std::max<uint64_t>(ngroups, 1)}));
+  std::vector<int> rc(T, DS_OK);
+  std::vector<std::string> msg(T);
+  auto work = [&](uint32_t t) {
+    for (uint64_t g = t; g < ngroups; g += T) {
+      const uint64_t s0 = b0 + g * G, s1 = std::min(s0 + G, base + nsteps);
+      int r = wait_slot(e, s1 - 1);
+      for (uint64_t s = s0; r == DS_OK && s < s1; ++s) tc_fill(e, s, X_host, y_host, idx + (s - base) * B, rows[s - base]);
+      if (r == DS_OK) r = tc_flush(e, s0, s1);
+      if (r != DS_OK) {
+        rc[t] = r;
+        msg[t] = ds_last_error();
+        return;
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (uint32_t t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  e->ring_pushed = base + nsteps;
+  for (uint32_t t = 0; t < T; ++t)
+    if (rc[t] != DS_OK) return set_error(rc[t], "%s", msg[t].c_str());
   return DS_OK;
 }
 
@@ -1351,8 +1430,13 @@ extern "C" int ds_engine_stream_end(ds_engine* e) {
     return set_error(DS_E_STATE, "engine_stream_end: %llu of %llu steps pushed",
                      static_cast<unsigned long long>(e->ring_pushed), static_cast<unsigned long long>(e->ring_steps));
   const cudaError_t err = cudaStreamSynchronize(e->stream);
-  cudaStreamSynchronize(e->copy_stream);
+  if (e->copy_stream) cudaStreamSynchronize(e->copy_stream);
   e->ring_active = false;
+  if (e->prof_pending && err == cudaSuccess) {
+    unsigned long long* p = e->prof_pending;
+    e->prof_pending = nullptr;
+    DS_TRY(dsb::dump_profile(e, p, e->prof_steps, e->prof_n, e->prof_path));
+  }
   e->ring_loss = nullptr;
   if (err != cudaSuccess) return set_error(DS_E_CUDA, "engine_stream_end: %s", cudaGetErrorString(err));
   return DS_OK;

@@ -73,6 +73,8 @@ struct FusedArgs {
   const uint32_t* ring_y;           // [slots][B]
   const uint32_t* ring_rows;        // [slots]
   const uint32_t* ring_ready;       // [slots] sequence words (step + 1), written by the copy engine
+  uint32_t ring_slot_rows;          // TC ring: rows per slot (B + 1: the labels ride in the last)
+  uint32_t ring_y_stride;           // TC ring: u32 stride between slots' labels
   unsigned long long* ring_consumed;  // pinned host: steps whose ring slot is free again
   double* ring_loss;                // pinned host: per-step batch loss (zero-copy), or null
 };
@@ -89,6 +91,10 @@ int launch_tc(const FusedArgs& a, int nc, const CUtensorMap& batch_rows, cudaStr
 int launch_tc_group(const FusedArgs* a, const CUtensorMap* batch_rows, uint32_t n, int nc, cudaStream_t s);
 // the tensor-core step reads batches as bf16 rows of tc_pitch(F) elements through a TMA map
 uint32_t tc_pitch(uint32_t F);
+// host_rows.cpp: gather + bf16 cast of host rows (the zero-copy stream ring's producer);
+// idx == nullptr: X is the batch itself
+void gather_rows_bf16_host(const float* X, uint32_t F, const uint32_t* idx, uint32_t rows, uint16_t* dst,
+                           uint64_t pitch);
 int tc_rows_to_bf16(const float* src, uint64_t rows, uint32_t F, void* dst, cudaStream_t s);
 int tc_make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t F);
 // Doubles of the f64 batch buffer (A.xb64) the MLP kernel needs.

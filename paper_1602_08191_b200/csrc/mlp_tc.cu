@@ -267,7 +267,16 @@ __device__ __forceinline__ void tstamp(unsigned long long* prof, uint64_t step, 
 __device__ __forceinline__ void tstamp_m(unsigned long long* prof, uint64_t step, int slot, uint32_t rank) {
   if (prof && rank == 0 && threadIdx.x == (kCW + 1) * 32) prof[step * kProfSlots + slot] = globaltimer_ns();
 }
-#if defined(DS_TC_PROF_X)
+__device__ __forceinline__ void tstamp_t(unsigned long long* prof, uint64_t step, int slot, uint32_t rank) {
+  if (prof && rank == 0 && threadIdx.x == kCW * 32) prof[step * kProfSlots + slot] = globaltimer_ns();
+}
+#if defined(DS_TC_PROF_T)
+#define TSTAMP_MAIN(...)
+#define TSTAMP_X(...)
+#define TSTAMP_M(...)
+#define TSTAMP_T(...) tstamp_t(__VA_ARGS__)
+#define TSTAMP_TM(...) tstamp_m(__VA_ARGS__)
+#elif defined(DS_TC_PROF_X)
 #define TSTAMP_MAIN(...)
 #define TSTAMP_X(...) tstamp(__VA_ARGS__)
 #define TSTAMP_M(...)
@@ -279,6 +288,10 @@ __device__ __forceinline__ void tstamp_m(unsigned long long* prof, uint64_t step
 #define TSTAMP_MAIN(...) tstamp(__VA_ARGS__)
 #define TSTAMP_X(...)
 #define TSTAMP_M(...)
+#endif
+#ifndef TSTAMP_T
+#define TSTAMP_T(...)
+#define TSTAMP_TM(...)
 #endif
 
 
@@ -452,11 +465,10 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
     const uint32_t xbytes_step = kBM * L.NA * 128;
     for (uint64_t s = 0; s < A.steps && !s_stop; ++s) {
       const uint32_t buf = static_cast<uint32_t>(s & 1);
-      if (lane == 0)  // every CTA finished the dW1 MMAs that last read X[buf]
-        while (*reinterpret_cast<volatile unsigned long long*>(&s_can_stage) < s && !*quitp) __nanosleep(32);
-      __syncwarp();
-      if (*quitp) break;
       uint32_t R, row, y = 0;
+      TSTAMP_T(A.prof, s, 0, rank);
+      // the batch description first (host ring: a PCIe round trip for the word and one for
+      // the labels), while the X buffer is still being read by step s-2's dW1 MMAs
       if (A.ring) {
         const uint32_t slot = static_cast<uint32_t>(s % A.ring_slots);
         uint32_t nrows = 1;
@@ -477,19 +489,26 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
             __nanosleep(64);
           }
         }
+        TSTAMP_T(A.prof, s, 1, rank);
         R = __shfl_sync(0xffffffffu, nrows, 0);
-        row = slot * B + (lane < R ? lane : 0u);
-        // the ring lives in mapped host memory, rewritten every ring_slots steps: labels are
-        // read uncached after the acquire, and the async proxy (the TMA gathers below) is
-        // ordered after it
-        if (lane < R) y = __ldcv(A.ring_y + static_cast<uint64_t>(slot) * B + lane);
+        row = slot * A.ring_slot_rows + (lane < R ? lane : 0u);
+        // the slot was written by the copy engine before its word: labels after the acquire,
+        // and the async proxy (the TMA gathers below) ordered after it
+        if (lane < R) y = __ldcg(A.ring_y + static_cast<uint64_t>(slot) * A.ring_y_stride + lane);
         asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (y == 0xFFFFFFFFu) TSTAMP_T(A.prof, s, 9, rank);  // (keeps the label load before the stamp)
+        TSTAMP_T(A.prof, s, 2, rank);
       } else {
         R = A.plan_rows[s];
         const uint32_t r0 = A.plan[s * B];
         row = lane < R ? A.plan[s * B + lane] : r0;  // padding rows repeat a valid row
         if (lane < R) y = __ldg(A.y + row);
       }
+      if (lane == 0)  // every CTA finished the dW1 MMAs that last read X[buf]
+        while (*reinterpret_cast<volatile unsigned long long*>(&s_can_stage) < s && !*quitp) __nanosleep(32);
+      __syncwarp();
+      if (*quitp) break;
+      TSTAMP_T(A.prof, s, 3, rank);
       lab[buf * kBM + lane] = y;
       if (lane == 0) {
         s_rows[buf] = R;
@@ -523,6 +542,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
                 : "memory");
         }
       }
+      TSTAMP_T(A.prof, s, 4, rank);
     }
   } else if (warp == kCW + 1) {
     // ================= MMA warp: every tcgen05.mma of the step ============================
@@ -541,6 +561,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
       const uint32_t buf = static_cast<uint32_t>(s & 1);
       const uint32_t pp = static_cast<uint32_t>((s - 1) & 1);  // phase parity of step s-1's barriers
       if (!mbar_wait_or_quit(xbar + buf, static_cast<uint32_t>((s >> 1) & 1), quitp)) break;
+      TSTAMP_TM(A.prof, s, 5, rank);
       if (s > 0 && prev_fired) {
         if (!mbar_wait_or_quit(exdone, xph, quitp)) break;
         xph ^= 1;
@@ -831,10 +852,10 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
           A.log.period[row] = pl.period;
         }
         if (A.ring_loss) A.ring_loss[step] = s_loss;
-        if (A.ring && A.ring_consumed) {  // every CTA staged this step's rows before its R phase
-          __threadfence_system();
-          *reinterpret_cast<volatile unsigned long long*>(A.ring_consumed) = step + 1;
-        }
+        if (A.ring && A.ring_consumed)  // every CTA's gathers of this step's slot have landed
+          // relaxed: nothing written before needs to be visible to the host with it (a system
+          // fence here would stall this warp for a PCIe round trip every step)
+          asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(A.ring_consumed), "l"(step + 1) : "memory");
       }
       done = step + 1;
       if (s_pol.fire && A.has_master) {
