@@ -536,10 +536,11 @@ def e2e_group_leg(args, L, api, engines, shards, seeds, rank, world, n):
     trains the GPU's workers while the host, per worker, runs the reference worker's
     ShardSweeper (the epoch permutations are computed inside the timed window) and
     gather_batch: ds_engine_stream_push_rows_n gathers each step's rows from the host shard
-    and writes them as bf16 into the engine's zero-copy ring in pinned, mapped host memory,
-    which the kernel's TMA gathers read across PCIe (H2D) -- one host thread per worker; the
-    kernel writes every step's loss to mapped pinned host memory (D2H). Wall clock from
-    stream_begin to the last stream_end, max over ranks."""
+    as bf16 into a pinned staging ring (labels in each slot's last row) and the copy engine
+    moves groups of 4 steps per DMA into the kernel's HBM ring (H2D) -- one host thread per
+    worker (plus helpers inside the call); the kernel writes every step's loss to mapped
+    pinned host memory (D2H). Wall clock from stream_begin to the last stream_end, max over
+    ranks."""
     import torch
     import torch.distributed as dist
     K, B, Wk = args.e2e_steps, args.batch, len(engines)
@@ -588,13 +589,13 @@ def e2e_group_leg(args, L, api, engines, shards, seeds, rank, world, n):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     pitch = (F + 7) // 8 * 8
     return {"value": n * Wk * B * K / t.item(), "unit": "samples/s",
-            "h2d_bytes_per_step": Wk * (B * pitch * 2 + B * 4 + 4), "d2h_bytes_per_step": Wk * 8, "steps": K,
+            "h2d_bytes_per_step": Wk * ((B + 1) * pitch * 2 + 4), "d2h_bytes_per_step": Wk * 8, "steps": K,
             "wall_s": t.item(), "losses_finite": ok,
             "path": "ds_engine_stream_begin_group + per worker ds_engine_stream_push_rows_n (host ShardSweeper, "
-                    "gather_batch + bf16 cast into a zero-copy ring in pinned mapped host memory, read by the "
-                    "kernel's TMA across PCIe) from one host thread per worker; one tensor-core launch trains all "
-                    "of the GPU's workers; per-step losses written to mapped host memory; wall clock from "
-                    "stream_begin to the last stream_end"}
+                    "gather_batch + bf16 cast into a pinned staging ring, one H2D DMA per 4 steps into the "
+                    "kernel's HBM ring) from one host thread per worker; one tensor-core launch trains all of the "
+                    "GPU's workers; per-step losses written to mapped host memory; wall clock from stream_begin "
+                    "to the last stream_end"}
 
 
 def exchange_leg(args, L, torch, dist, world, rank, local, hbm, peak_kind, nvl=None):

@@ -377,9 +377,9 @@ int ds_engine_stream_push_rows(ds_engine* e, const float* X_host, const uint32_t
                                uint32_t rows);
 /* As ds_engine_stream_push_rows for nsteps consecutive steps in one call: step s takes
  * rows[s] row indices from idx[s * batch_size ...] (the ShardSweeper layout). Blocks while
- * the ring is full. Tensor-core engines write the rows as bf16 straight into a zero-copy
- * ring in mapped host memory that the kernel's TMA gathers read across PCIe (no CUDA call
- * per step). */
+ * the ring is full. Tensor-core engines gather the rows as bf16 into a pinned staging ring
+ * (labels in each slot's extra row) with helper threads and move groups of 4 steps per H2D
+ * DMA (two CUDA calls per group). */
 int ds_engine_stream_push_rows_n(ds_engine* e, const float* X_host, const uint32_t* y_host, const uint32_t* idx,
                                  const uint32_t* rows, uint64_t nsteps);
 int ds_engine_stream_end(ds_engine* e);
