@@ -498,6 +498,11 @@ int dump_profile(ds_engine* e, unsigned long long* prof, uint64_t steps, uint64_
     static const char* xnames[] = {"arm", "round0_first_tile", "round0_rest", "round1", "wait_st", "small_fence",
                                    "cbar", "release", "w1_all", "exchange_all"};
     if (e->tc && std::getenv("DS_TC_PROF_X")) pairs = xpairs, names = xnames;
+    // the one-shard bulk exchange: ticket, bulk load landed, W1 updated, stored, rest
+    static const int bpairs[][2] = {{0, 1}, {1, 6}, {6, 7}, {7, 8}, {8, 3}, {3, 5}, {0, 5}, {0, 0}, {0, 0}, {0, 0}};
+    static const char* bnames[] = {"ticket", "bulk_load", "w1_update", "small_store", "fence_sync", "b2_release",
+                                   "exchange_all", "-", "-", "-"};
+    if (e->tc && std::getenv("DS_TC_PROF_B")) pairs = bpairs, names = bnames;
     // MMA warp timeline: fwd(s) tiles (stamps 2,3,4 at sgdd waits of tiles 0,3,last; 5 commit),
     // logits (6), delta1 ready (0) and dW1 issued (1); pairs are within the MMA loop's step s
     static const int mpairs[][2] = {{2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 0}, {0, 1}, {2, 5}, {2, 0}, {0, 0}, {0, 0}};

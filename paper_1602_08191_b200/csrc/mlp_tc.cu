@@ -73,7 +73,7 @@ constexpr int kMaxC = 16;      // classes: the logits MMA's N
 constexpr int kMaxNC = 16;     // CTAs per cluster (non-portable size above 8)
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kBarCompute = 1;  // named barrier of the compute warps
-constexpr uint32_t kNumBars = 27;
+constexpr uint32_t kNumBars = 28;
 
 // ---------------------------------------------------------------------------------
 // PTX helpers
@@ -158,6 +158,19 @@ __device__ __forceinline__ float ld_center(const float* p) {
   float v;
   asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
   return v;
+}
+// TMA bulk copies of the CTA's center rows (one-shard exchange): global -> shared with an
+// mbarrier transaction count, and back shared -> global as a bulk group
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes)
+               : "memory");
 }
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -375,6 +388,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
   uint64_t* lgbar = bars + 10;  // partial logits in TMEM (MMA warp -> warps 0, 1)
   uint64_t* dtile = bars + 11;  // [8] dW1 MMAs of 128-feature tile t done (MMA warp -> compute)
   uint64_t* sgdd = bars + 19;   // [8] W1 SGD of tile t done by all compute warps (-> MMA warp)
+  uint64_t* cxbar = bars + 27;  // the CTA's center rows staged for a one-shard exchange
   __shared__ uint32_t s_tmem, s_bad, s_stop, s_quit, s_rows[2];
   __shared__ unsigned long long s_can_stage;  // the TMA warp may stage steps <= s_can_stage
   __shared__ double s_loss;
@@ -391,7 +405,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
   // ---- setup ---------------------------------------------------------------------
   if (warp == 0) tc::tmem_alloc<kTmemCols>(&s_tmem);
   if (tid == 0) {
-    for (uint32_t i = 0; i < kNumBars; ++i) tc::mbar_init(bars + i, i >= 19 ? kCW : (i == 9 ? 2u : 1u));
+    for (uint32_t i = 0; i < kNumBars; ++i) tc::mbar_init(bars + i, (i >= 19 && i < 27) ? kCW : (i == 9 ? 2u : 1u));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_pol.cum = st->cum;
     s_pol.cut = st->cut;
@@ -611,6 +625,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
     // ================= compute warps ======================================================
     uint32_t ph = 0;   // fbar / dtile / rbar / gbar / d1rdy parity: one completion per step
     uint32_t eph = 0;  // ebar / cbar parity: completions per exchange
+    uint32_t cxph = 0;  // cxbar parity: one completion per bulk exchange
     for (uint64_t step = 0; step < A.steps && !s_stop; ++step) {
       const uint32_t buf = static_cast<uint32_t>(step & 1);
       TSTAMP_MAIN(A.prof, step, 0, rank);
@@ -905,7 +920,77 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
           while (s + 1 < T.n && g >= T.begin[s + 1]) ++s;
           return T.ptr[s] + (g - T.begin[s]);
         };
-        if (!(s_bad & DS_FLAG_TICKET_TIMEOUT)) {
+        // the small slices (own W2 columns, own b1, b2 on CTA 0): thread tid < nsmall owns one
+        const uint32_t nsmall = C * HU + HU + (rank == 0 ? C : 0u);
+        auto small_slice = [&](float*& mp, float*& wp) {
+          if (tid < C * HU) {
+            const uint32_t k = tid / HU, j = tid - k * HU;
+            mp = center(w2o + static_cast<uint64_t>(k) * H + u0 + j);
+            wp = W2cc + w2c_idx(k, j);
+          } else if (tid < C * HU + HU) {
+            mp = center(b1o + u0 + (tid - C * HU));
+            wp = b1c + (tid - C * HU);
+          } else {
+            mp = center(b2o + (tid - C * HU - HU));
+            wp = b2s + (tid - C * HU - HU);
+          }
+        };
+        if (!(s_bad & DS_FLAG_TICKET_TIMEOUT) && one_shard && (F & 3u) == 0 && HU > 0) {
+          // own W1 rows, one-shard center: the HU center rows (contiguous, F floats each)
+          // come in by TMA bulk copies into this step's X buffer (free: dW1(step) is done and
+          // step+2 is staged only after the next R phase), are updated in place next to the
+          // TMEM master, and go back by bulk stores — one latency each way instead of a
+          // dependent load round per tile pair
+          const uint64_t g0 = w1o + static_cast<uint64_t>(u0) * F;
+          float* cst = reinterpret_cast<float*>(Xbuf(static_cast<uint32_t>(step & 1)));
+          if (tid == 0) {
+            mbar_expect_tx(cxbar, HU * F * 4);
+            for (uint32_t j = 0; j < HU; ++j) bulk_g2s(cst + j * F, c0p + g0 + static_cast<uint64_t>(j) * F, F * 4, cxbar);
+          }
+          float* smp = nullptr;
+          float* swp = nullptr;
+          float smv = 0.f;
+          if (tid < nsmall) {  // the small slice's center load overlaps the bulk copies
+            small_slice(smp, swp);
+            smv = ld_center(smp);
+          }
+          tc::mbar_wait(cxbar, cxph);
+          cxph ^= 1;
+          TSTAMP_X(A.prof, step, 6, rank);
+          for (uint32_t t = 0; t < L.NT; ++t) {
+            const uint32_t f = t * 128 + quarter * 32 + lane;
+            float o[8];
+            tmem_ld8(tmem + lane_base + kColW1 + t * kHC + chalf * 8, o);
+            if (f < F) {
+#pragma unroll
+              for (uint32_t i = 0; i < 8; ++i) {
+                const uint32_t j = chalf * 8 + i;
+                if (j < HU) {
+                  float mo;
+                  elastic_elem(o[i], cst[j * F + f], a, o[i], mo);
+                  cst[j * F + f] = mo;
+                }
+              }
+            }
+            tmem_st8(tmem + lane_base + kColW1 + t * kHC + chalf * 8, o);
+            if (f < F) store_wbf_half(Wbf, f, chalf, o);
+          }
+          tmem_wait_st();
+          TSTAMP_X(A.prof, step, 7, rank);
+          if (tid < nsmall) {
+            float mo;
+            elastic_elem(*swp, smv, a, *swp, mo);
+            *smp = mo;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the updates, to the bulk stores
+          csync();
+          if (tid == 0) {
+            for (uint32_t j = 0; j < HU; ++j) bulk_s2g(c0p + g0 + static_cast<uint64_t>(j) * F, cst + j * F, F * 4);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // written (and the buffer free again)
+          }
+          TSTAMP_X(A.prof, step, 8, rank);
+        } else if (!(s_bad & DS_FLAG_TICKET_TIMEOUT)) {
           // own W1 rows: thread = feature of a tile (its TMEM lane), 8 units (its column
           // half); per unit the center row is contiguous in f (coalesced). Two tiles per
           // round: all 16 center loads of a thread are issued before any update.
@@ -948,21 +1033,10 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
           tmem_wait_st();
           // the small slices: own W2 columns, own b1, b2 (CTA 0): loads first, then updates
           TSTAMP_X(A.prof, step, 2, rank);
-          const uint32_t nsmall = C * HU + HU + (rank == 0 ? C : 0u);
           if (tid < nsmall) {
             float* mp;
             float* wp;
-            if (tid < C * HU) {
-              const uint32_t k = tid / HU, j = tid - k * HU;
-              mp = center(w2o + static_cast<uint64_t>(k) * H + u0 + j);
-              wp = W2cc + w2c_idx(k, j);
-            } else if (tid < C * HU + HU) {
-              mp = center(b1o + u0 + (tid - C * HU));
-              wp = b1c + (tid - C * HU);
-            } else {
-              mp = center(b2o + (tid - C * HU - HU));
-              wp = b2s + (tid - C * HU - HU);
-            }
+            small_slice(mp, wp);
             float mo;
             elastic_elem(*wp, ld_center(mp), a, *wp, mo);
             *mp = mo;
