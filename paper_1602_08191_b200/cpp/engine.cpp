@@ -75,11 +75,12 @@ ds_hyper to_ds(const Hyperparams& hp) {
 }
 
 int engine_kind() {
-  const char* env = std::getenv("DEEPSPARK_ENGINE");  // auto | layered | fused
+  const char* env = std::getenv("DEEPSPARK_ENGINE");  // auto | layered | fused | tc
   if (!env) return DS_ENGINE_AUTO;
   const std::string v(env);
   if (v == "layered") return DS_ENGINE_LAYERED;
   if (v == "fused") return DS_ENGINE_FUSED;
+  if (v == "tc") return DS_ENGINE_TC;  // the tensor-core step (stated tolerance, one hidden layer)
   return DS_ENGINE_AUTO;
 }
 
