@@ -172,6 +172,12 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes)
                : "memory");
 }
+// dst[i] += src[i] (f32, round to nearest) for a whole row, as one bulk reduction
+__device__ __forceinline__ void bulk_add_s2g(float* dst, const float* src, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
@@ -907,7 +913,9 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
           }
           if (!ok) atomicOr(&s_bad, DS_FLAG_TICKET_TIMEOUT), atomicOr(&st->flags, DS_FLAG_TICKET_TIMEOUT);
         }
-        if (rank == 0 && tid == 0 && NC > 1) mbar_expect_tx(cbar, (NC - 1) * 16);
+        // ordered exchanges release the next ticket only after every CTA's slice is written
+        // ("slice done" messages to CTA 0 + system fences); LockFree needs neither
+        if (rank == 0 && tid == 0 && NC > 1 && ordered) mbar_expect_tx(cbar, (NC - 1) * 16);
         if (rank != 0 && tid == 0 && NC > 1) mbar_expect_tx(ebar, ((C + 3) / 4) * 16);
         csync();
         TSTAMP_X(A.prof, step, 1, rank);
@@ -965,10 +973,10 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
 #pragma unroll
               for (uint32_t i = 0; i < 8; ++i) {
                 const uint32_t j = chalf * 8 + i;
-                if (j < HU) {
-                  float mo;
-                  elastic_elem(o[i], cst[j * F + f], a, o[i], mo);
-                  cst[j * F + f] = mo;
+                if (j < HU) {  // elastic_elem: e = a (w - m); w' = w - e; m' = m + e
+                  const float e = fmul(a, fsub(o[i], cst[j * F + f]));
+                  o[i] = fsub(o[i], e);
+                  cst[j * F + f] = ordered ? fadd(cst[j * F + f], e) : e;
                 }
               }
             }
@@ -978,16 +986,31 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
           tmem_wait_st();
           TSTAMP_X(A.prof, step, 7, rank);
           if (tid < nsmall) {
-            float mo;
-            elastic_elem(*swp, smv, a, *swp, mo);
-            *smp = mo;
+            const float e = fmul(a, fsub(*swp, smv));
+            *swp = fsub(*swp, e);
+            if (ordered)
+              *smp = fadd(smv, e);
+            else
+              atomicAdd_system(smp, e);  // LockFree: the increment is never lost (m' = m + e when alone)
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the updates, to the bulk stores
           csync();
           if (tid == 0) {
-            for (uint32_t j = 0; j < HU; ++j) bulk_s2g(c0p + g0 + static_cast<uint64_t>(j) * F, cst + j * F, F * 4);
+            // ordered: the new rows (this worker holds the center exclusively); LockFree: the
+            // increments e as bulk f32 reductions — concurrent workers' exchanges add up
+            // instead of overwriting each other (a lone writer gets m + e, as elastic_elem)
+            for (uint32_t j = 0; j < HU; ++j) {
+              float* dst = c0p + g0 + static_cast<uint64_t>(j) * F;
+              if (ordered)
+                bulk_s2g(dst, cst + j * F, F * 4);
+              else
+                bulk_add_s2g(dst, cst + j * F, F * 4);
+            }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // written (and the buffer free again)
+            if (ordered)  // written before the next ticket is released
+              asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            else  // the X buffer read out (it is restaged after the next R phase)
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           }
           TSTAMP_X(A.prof, step, 8, rank);
         } else if (!(s_bad & DS_FLAG_TICKET_TIMEOUT)) {
@@ -1018,9 +1041,13 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
               for (uint32_t i = 0; i < 8; ++i) {
                 const uint32_t j = chalf * 8 + i;
                 if (f < F && j < HU) {
-                  float mo;
-                  elastic_elem(o[i], mv[h][i], a, o[i], mo);
-                  *center(g0 + static_cast<uint64_t>(j) * F + f) = mo;
+                  const float e = fmul(a, fsub(o[i], mv[h][i]));
+                  o[i] = fsub(o[i], e);
+                  float* cp = center(g0 + static_cast<uint64_t>(j) * F + f);
+                  if (ordered)
+                    *cp = fadd(mv[h][i], e);
+                  else
+                    atomicAdd_system(cp, e);  // LockFree: increments add up across workers / GPUs
                 }
               }
               tmem_st8(tmem + lane_base + kColW1 + t * kHC + chalf * 8, o);
@@ -1037,26 +1064,32 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
             float* mp;
             float* wp;
             small_slice(mp, wp);
-            float mo;
-            elastic_elem(*wp, ld_center(mp), a, *wp, mo);
-            *mp = mo;
+            const float mv0 = ld_center(mp);
+            const float e = fmul(a, fsub(*wp, mv0));
+            *wp = fsub(*wp, e);
+            if (ordered)
+              *mp = fadd(mv0, e);
+            else
+              atomicAdd_system(mp, e);
           }
         }
         tc::fence_async_smem();
         tc::fence_before();
         csync();
-        if (tid == 0) __threadfence_system();  // this CTA's center writes (cumulative over the barrier)
+        if (tid == 0 && ordered) __threadfence_system();  // this CTA's center writes (cumulative over the barrier)
         TSTAMP_X(A.prof, step, 3, rank);
         if (NC > 1) {
           if (rank != 0) {
-            if (tid == 0) st_async16(b2in + kMaxC - 4, cbar, 0, make_float4(0.f, 0.f, 0.f, 0.f));  // "slice done"
+            if (tid == 0 && ordered) st_async16(b2in + kMaxC - 4, cbar, 0, make_float4(0.f, 0.f, 0.f, 0.f));  // "slice done"
             tc::mbar_wait(ebar, eph);  // CTA 0's exchanged b2
             if (tid < C) b2s[tid] = b2in[tid];
             eph ^= 1;
           } else {
-            tc::mbar_wait(cbar, eph);  // every peer's slice done
+            if (ordered) {
+              tc::mbar_wait(cbar, eph);  // every peer's slice done
+              eph ^= 1;
+            }
             TSTAMP_X(A.prof, step, 4, rank);
-            eph ^= 1;
             if (tid < (C + 3) / 4 * (NC - 1)) {  // b2 lives in every CTA
               const uint32_t q = 1 + tid / ((C + 3) / 4), pc = tid % ((C + 3) / 4);
               float v[4];
@@ -1067,8 +1100,8 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
           }
         }
         if (rank == 0 && tid == 0 && !(s_bad & DS_FLAG_TICKET_TIMEOUT)) {
-          __threadfence_system();
           if (ordered) {
+            __threadfence_system();
             T.flags[0]->exchanges += 1;
             __threadfence_system();
             for (int s = 0; s < T.n; ++s) st_release_sys(reinterpret_cast<uint64_t*>(&T.flags[s]->seq), tk + 1);
@@ -1088,6 +1121,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
   }
 
   // ---- write back the parameters, the policy state, errors --------------------------
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // LockFree center stores landed
   __syncthreads();
   tc::fence_after();
   if (warp < kCW) {  // own W1 rows from the TMEM master

@@ -315,11 +315,11 @@ def test_tc_group_async_band_config1(L, orc, api, mode, n_slices):
 
     * Locked (exchanges serialized in arrival order by the device ticket dispenser, the
       reference's UpdateMode::Locked): |d acc| <= 0.02 and |d loss| <= 3% relative.
-    * LockFree (plain per-element loads/stores, UpdateMode::LockFree, "lost updates
-      allowed"): the two workers run in lockstep on one GPU, so their exchanges collide and
-      one worker's elastic term is usually overwritten -- the center moves about half as
-      fast (measured: accuracy 0.82-0.87 vs 0.92). Stated band: |d acc| <= 0.12, holdout loss
-      within 35%."""
+    * LockFree (UpdateMode::LockFree: no ordering): the two workers run in lockstep on one
+      GPU, so their exchanges overlap. The center's increments are f32 atomic adds (bulk
+      TMA reductions for a one-GPU center), so overlapping exchanges add up rather than
+      overwrite each other (a lone writer gets exactly m + e) — measured: accuracy 0.920 vs
+      0.918, holdout loss within 2%. Same band as Locked."""
     m, X, y, hp, shards, hold, seeds, init = _config1(orc, api, 2, 120)
     ref = orc.simulate(SimSpec(2, hp, m, X, y, 10, schedule_seed=1, init_seed=2, data_seed=3,
                                eval_every=10 ** 6, record_master_snaps=False))
@@ -333,12 +333,8 @@ def test_tc_group_async_band_config1(L, orc, api, mode, n_slices):
           f"holdout loss {loss_dev:.5f} vs {loss_ref:.5f}")
     assert cnt == 2 * (hp.i_max // hp.tau) and np.isfinite(snap).all()
     assert 0.8 <= acc_ref <= 0.97  # the band is tested away from saturation
-    if mode == "locked":
-        assert abs(acc_dev - acc_ref) <= 0.02
-        assert abs(loss_dev - loss_ref) <= 0.03 * loss_ref
-    else:
-        assert abs(acc_dev - acc_ref) <= 0.12
-        assert abs(loss_dev - loss_ref) <= 0.35 * loss_ref
+    assert abs(acc_dev - acc_ref) <= 0.02
+    assert abs(loss_dev - loss_ref) <= 0.03 * loss_ref
 
 
 def test_tc_errors(L, orc):
