@@ -383,6 +383,12 @@ int ds_engine_stream_push_rows(ds_engine* e, const float* X_host, const uint32_t
 int ds_engine_stream_push_rows_n(ds_engine* e, const float* X_host, const uint32_t* y_host, const uint32_t* idx,
                                  const uint32_t* rows, uint64_t nsteps);
 int ds_engine_stream_end(ds_engine* e);
+/* Host-side gather + bf16 cast the tensor-core stream ring uses (no GPU involved): rows x F
+ * floats, row r from X + idx[r] * F (idx NULL: X + r * F), into dst rows of `pitch` bf16
+ * (padding untouched); round to nearest even, NaN -> 0x7FFF, denormals kept — the device's
+ * __float2bfloat16_rn bits. DS_E_CONTRACT on null pointers or pitch < F. */
+int ds_host_rows_to_bf16(const float* X, uint32_t F, const uint32_t* idx, uint32_t rows, uint16_t* dst,
+                         uint64_t pitch);
 /* Stream mode for several tensor-core engines trained in ONE launch (ds_engine_run_group):
  * each engine gets its own ring, pushes and ds_engine_stream_end as above; loss_host[i]
  * (pinned, or a NULL array) receives engine i's per-step losses. */

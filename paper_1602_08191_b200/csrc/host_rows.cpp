@@ -68,3 +68,12 @@ void gather_rows_bf16_host(const float* X, uint32_t F, const uint32_t* idx, uint
 }
 
 }  // namespace dsb
+
+// C-ABI (ds_cuda.h): the host half of the tensor-core stream mode, exported for pipelines
+// that stage their own batches (and testable without a GPU)
+extern "C" int ds_host_rows_to_bf16(const float* X, uint32_t F, const uint32_t* idx, uint32_t rows, uint16_t* dst,
+                                    uint64_t pitch) {
+  if (!X || !dst || F == 0 || pitch < F) return 1;  // DS_E_CONTRACT
+  dsb::gather_rows_bf16_host(X, F, idx, rows, dst, pitch);
+  return 0;
+}

@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
   uint64_t* cbar = bars + 6;    // (CTA 0) every peer finished its exchange slice
   uint64_t* d1rdy = bars + 7;   // delta1 of the step written (compute -> MMA warp)
   uint64_t* exdone = bars + 8;  // the step's exchange done (compute -> MMA warp)
-  uint64_t* a1rdy = bars + 9;   // A1 of the step written (warps 0, 1 -> MMA warp)
+  uint64_t* a1rdy = bars + 9;   // A1 of the step written (warps 0, 1, 4, 5 -> MMA warp)
   uint64_t* lgbar = bars + 10;  // partial logits in TMEM (MMA warp -> warps 0, 1)
   uint64_t* dtile = bars + 11;  // [8] dW1 MMAs of 128-feature tile t done (MMA warp -> compute)
   uint64_t* sgdd = bars + 19;   // [8] W1 SGD of tile t done by all compute warps (-> MMA warp)
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
   // ---- setup ---------------------------------------------------------------------
   if (warp == 0) tc::tmem_alloc<kTmemCols>(&s_tmem);
   if (tid == 0) {
-    for (uint32_t i = 0; i < kNumBars; ++i) tc::mbar_init(bars + i, (i >= 19 && i < 27) ? kCW : (i == 9 ? 2u : 1u));
+    for (uint32_t i = 0; i < kNumBars; ++i) tc::mbar_init(bars + i, (i >= 19 && i < 27) ? kCW : (i == 9 ? 4u : 1u));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_pol.cum = st->cum;
     s_pol.cut = st->cut;
@@ -575,25 +575,26 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
     const uint32_t idesc_lg = tc::idesc_tf32(64, kMaxC);
     const uint64_t dw_b = sdesc_sw(saddr(D1b), 16, 1024, kSw128);
     const uint64_t fwd_b = sdesc_sw(saddr(Wbf), 0, 256, kSw32);
-    bool prev_fired = false;
     uint32_t xph = 0;  // exdone parity
     for (uint64_t s = 0; s < A.steps && !s_stop; ++s) {
       const uint32_t buf = static_cast<uint32_t>(s & 1);
       const uint32_t pp = static_cast<uint32_t>((s - 1) & 1);  // phase parity of step s-1's barriers
       if (!mbar_wait_or_quit(xbar + buf, static_cast<uint32_t>((s >> 1) & 1), quitp)) break;
       TSTAMP_TM(A.prof, s, 5, rank);
-      if (s > 0 && prev_fired) {
+      // the whole W1 update of step s-1 first: forward MMAs issued while the compute warps
+      // still run the SGD (TMEM / smem traffic) were measured at half the tensor-pipe rate
+      bool quit = false;
+      if (s > 0)
+        for (uint32_t t = 0; t < L.NT && !quit; ++t) quit = !mbar_wait_or_quit(sgdd + t, pp, quitp);
+      if (quit) break;
+      // step s-1's policy decision is final (computed before the compute warps' SGD arrivals)
+      const bool prev_fired = s > 0 && s_pol.fire && A.has_master;
+      if (prev_fired) {
         if (!mbar_wait_or_quit(exdone, xph, quitp)) break;
         xph ^= 1;
       }
       tc::fence_after();
       const uint64_t da0 = sdesc_sw(saddr(Xbuf(buf)), 16, 1024, kSw128);
-      // the whole W1 update of step s-1 first: forward MMAs issued while the compute warps
-      // still run the SGD (TMEM / smem traffic) were measured at half the tensor-pipe rate
-      bool quit = false;
-      if (s > 0 && !prev_fired)
-        for (uint32_t t = 0; t < L.NT && !quit; ++t) quit = !mbar_wait_or_quit(sgdd + t, pp, quitp);
-      if (quit) break;
       tc::fence_after();
       for (uint32_t t = 0; t < L.NT; ++t) {
         if (t == 0) TSTAMP_M(A.prof, s, 2, rank);
@@ -616,7 +617,6 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
       TSTAMP_M(A.prof, s, 6, rank);
       if (!mbar_wait_or_quit(d1rdy, buf, quitp)) break;  // delta1(s) in D1b; the policy decided
       TSTAMP_M(A.prof, s, 0, rank);
-      prev_fired = s_pol.fire && A.has_master;
       tc::fence_after();
       const uint64_t dx0 = sdesc_sw(saddr(Xbuf(buf)), 4096, 1024, kSw128);
       for (uint32_t t = 0; t < L.NT; ++t) {
@@ -643,25 +643,32 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
       // ---- hidden activations (warps 0, 1; lane = row) -> A1c; logits on the tensor core -
       // tanh(x) = 1 - 2 / (exp(2x) + 1) (saturates correctly at +-inf); the MMA warp then
       // computes the CTA's partial logits P[64 x 16] = A1[64 x 16] . W2c[16 x 16]^T (tf32)
-      if (warp < 2) {
-        float z[16];
-        tmem_ld16(tmem + ((warp * 32u) << 16), z);
-        const uint32_t r = warp * 16 + lane;
+      if (warp < 2 || warp == 4 || warp == 5) {
+        // warps 0/4 rows 0-15, 1/5 rows 16-31 (TMEM lanes 0-15 / 32-47); warps 0, 1 the
+        // units 0-7, warps 4, 5 the units 8-15
+        const uint32_t rw = warp & 1u, uh = warp >> 2;
+        float z[8];
+        tmem_ld8(tmem + ((rw * 32u) << 16) + uh * 8, z);
+        const uint32_t r = rw * 16 + lane;
         if (lane < 16) {
-          float a[kHC];
+          float a[8];
 #pragma unroll
-          for (int j = 0; j < kHC; ++j) {
-            const float x = z[j] + b1c[j];
+          for (int j = 0; j < 8; ++j) {
+            const float x = z[j] + b1c[uh * 8 + j];
             a[j] = r < R ? 1.f - __fdividef(2.f, __expf(2.f * x) + 1.f) : 0.f;
           }
 #pragma unroll
-          for (int c = 0; c < kHC / 4; ++c)
-            *reinterpret_cast<float4*>(A1c + a1c_idx(r, 4 * c)) = make_float4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]);
+          for (int c = 0; c < 2; ++c)
+            *reinterpret_cast<float4*>(A1c + a1c_idx(r, uh * 8 + 4 * c)) =
+                make_float4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]);
         }
         tc::fence_async_smem();
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(a1rdy);
+      }
+      if (warp < 2) {
+        const uint32_t r = warp * 16 + lane;
         tc::mbar_wait(lgbar, ph);
         tc::fence_after();
         float lg[16];
@@ -766,22 +773,6 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
       }
       // delta2 / per-row loss of row r straight from the gathered messages (slot r / RP)
       auto D2 = [&](uint32_t r, uint32_t k) -> float { return fs[d2off[r] + k]; };
-      if (warp == kCW - 1) {  // batch loss (mean over rows) and the policy (engine.cpp:35-48)
-        const uint32_t p = lane / RP;
-        double l = (lane < R && p < NC) ? static_cast<double>(inG[p * MG + RP * Cp + (lane - p * RP)]) : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-        if (lane == 0) {
-          s_loss = l / static_cast<double>(R);
-          PolicyTc& pl = s_pol;
-          pl.cum += s_loss;
-          pl.since += 1;
-          const bool fire = pl.adaptive ? (pl.cum > pl.cut) : (pl.since == pl.tau);
-          pl.period = fire ? pl.since : 0u;
-          pl.fire = fire ? 1u : 0u;
-          if (fire) pl.cum = 0.0, pl.since = 0;
-        }
-      }
       // ---- delta1 = (delta2 . W2[:, own]) * (1 - a^2): thread = (row r, 2 units) --------
       {
         const uint32_t r = tid >> 3, j0 = (tid & 7) * 2;
@@ -804,6 +795,25 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
       csync();
       if (tid == 0) tc::mbar_arrive(d1rdy);  // the MMA warp issues dW1(s)
       TSTAMP_MAIN(A.prof, step, 5, rank);
+      // the batch loss and the policy, off the path to the dW1 MMAs: the MMA warp reads the
+      // decision only at the next step, after every compute warp's SGD arrivals
+      if (warp == kCW - 1) {  // batch loss (mean over rows) and the policy (engine.cpp:35-48)
+        const uint32_t p = lane / RP;
+        double l = (lane < R && p < NC) ? static_cast<double>(inG[p * MG + RP * Cp + (lane - p * RP)]) : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+        if (lane == 0) {
+          s_loss = l / static_cast<double>(R);
+          PolicyTc& pl = s_pol;
+          pl.cum += s_loss;
+          pl.since += 1;
+          const bool fire = pl.adaptive ? (pl.cum > pl.cut) : (pl.since == pl.tau);
+          pl.period = fire ? pl.since : 0u;
+          pl.fire = fire ? 1u : 0u;
+          if (fire) pl.cum = 0.0, pl.since = 0;
+        }
+      }
+
       // ---- W2 / b1 / b2 SGD (overlaps the dW1 MMAs) --------------------------------------
       uint32_t ubad = 0;
       for (uint32_t o = tid; o < kHC * C + kHC + C; o += kCT) {
@@ -943,17 +953,42 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
             wp = b2s + (tid - C * HU - HU);
           }
         };
-        if (!(s_bad & DS_FLAG_TICKET_TIMEOUT) && one_shard && (F & 3u) == 0 && HU > 0) {
-          // own W1 rows, one-shard center: the HU center rows (contiguous, F floats each)
-          // come in by TMA bulk copies into this step's X buffer (free: dW1(step) is done and
+        if (!(s_bad & DS_FLAG_TICKET_TIMEOUT) && (F & 3u) == 0 && HU > 0) {
+          // own W1 rows: the HU center rows (contiguous, F floats each; split where a shard
+          // boundary — 32-float aligned — crosses a row, the remote pieces over NVLink) come
+          // in by TMA bulk copies into this step's X buffer (free: dW1(step) is done and
           // step+2 is staged only after the next R phase), are updated in place next to the
-          // TMEM master, and go back by bulk stores — one latency each way instead of a
-          // dependent load round per tile pair
+          // TMEM master, and go back by bulk stores / bulk f32 reductions — one latency each
+          // way instead of a dependent load round per tile pair
           const uint64_t g0 = w1o + static_cast<uint64_t>(u0) * F;
           float* cst = reinterpret_cast<float*>(Xbuf(static_cast<uint32_t>(step & 1)));
+          // row j's pieces: [lo, hi) of the global vector inside shard k (one piece, the
+          // whole row, for a one-GPU center). mode 0: load, 1: store, 2: reduce-add
+          auto pieces = [&](int mode) {
+#pragma unroll 1
+            for (uint32_t j = 0; j < HU; ++j) {
+              const uint64_t r0 = g0 + static_cast<uint64_t>(j) * F;
+#pragma unroll
+              for (int k = 0; k < kMaxShards; ++k) {  // static indices: the table stays in the parameter bank
+                if (k >= T.n) break;
+                const uint64_t b0 = one_shard ? 0 : T.begin[k], b1 = one_shard ? ~0ull : T.begin[k + 1];
+                const uint64_t lo = r0 > b0 ? r0 : b0, hi = r0 + F < b1 ? r0 + F : b1;
+                if (lo >= hi) continue;
+                float* g = (one_shard ? c0p : T.ptr[k]) + (lo - b0);
+                float* sp = cst + j * F + (lo - r0);
+                const uint32_t bytes = static_cast<uint32_t>(hi - lo) * 4u;
+                if (mode == 0)
+                  bulk_g2s(sp, g, bytes, cxbar);
+                else if (mode == 1)
+                  bulk_s2g(g, sp, bytes);
+                else
+                  bulk_add_s2g(g, sp, bytes);
+              }
+            }
+          };
           if (tid == 0) {
             mbar_expect_tx(cxbar, HU * F * 4);
-            for (uint32_t j = 0; j < HU; ++j) bulk_g2s(cst + j * F, c0p + g0 + static_cast<uint64_t>(j) * F, F * 4, cxbar);
+            pieces(0);
           }
           float* smp = nullptr;
           float* swp = nullptr;
@@ -999,13 +1034,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
             // ordered: the new rows (this worker holds the center exclusively); LockFree: the
             // increments e as bulk f32 reductions — concurrent workers' exchanges add up
             // instead of overwriting each other (a lone writer gets m + e, as elastic_elem)
-            for (uint32_t j = 0; j < HU; ++j) {
-              float* dst = c0p + g0 + static_cast<uint64_t>(j) * F;
-              if (ordered)
-                bulk_s2g(dst, cst + j * F, F * 4);
-              else
-                bulk_add_s2g(dst, cst + j * F, F * 4);
-            }
+            pieces(ordered ? 1 : 2);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             if (ordered)  // written before the next ticket is released
               asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
