@@ -221,6 +221,20 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+// tcgen05.ld without the wait, and a wait that names the destination registers (so no use
+// of them can be scheduled above it): two loads in flight behind one wait
+__device__ __forceinline__ void tmem_ld8_raw(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld2(uint32_t (&a)[8], uint32_t (&b)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+                 "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7])
+               :
+               : "memory");
+}
 // 8 units (half h) of feature f's bf16 row in the MN-major SW32 W1 copy
 __device__ __forceinline__ void store_wbf_half(unsigned char* Wbf, uint32_t f, uint32_t h, const float (&o)[8]) {
   *reinterpret_cast<uint4*>(Wbf + wbf_chunk(f, h)) =
@@ -850,25 +864,29 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
       // ---- W1 SGD per tile from the TMEM dW1 tile and master; release the tile to the
       // MMA warp (forward of step s+1 reads the bf16 copy) ------------------------------
       for (uint32_t t = 0; t < L.NT; ++t) {
+        uint32_t gr[8], wr[8];
+        // the master tile first (only these threads write it), then the MMA's dW1 tile
+        tmem_ld8_raw(tmem + lane_base + kColW1 + t * kHC + chalf * 8, wr);
         tc::mbar_wait(dtile + t, ph);
         tc::fence_after();
-        float g[8], o[8];
-        tmem_ld8(tmem + lane_base + kColDw + t * kHC + chalf * 8, g);
-        tmem_ld8(tmem + lane_base + kColW1 + t * kHC + chalf * 8, o);
+        tmem_ld8_raw(tmem + lane_base + kColDw + t * kHC + chalf * 8, gr);
+        tmem_wait_ld2(wr, gr);
         const uint32_t f = t * 128 + quarter * 32 + lane;
+        float o[8];
 #pragma unroll
         for (uint32_t i = 0; i < 8; ++i) {
-          o[i] = chalf * 8 + i < HU ? fmaf(-eta, fmaf(wd, o[i], g[i]), o[i]) : 0.f;  // padding units stay zero
+          const float w = __uint_as_float(wr[i]), g = __uint_as_float(gr[i]);
+          o[i] = chalf * 8 + i < HU ? fmaf(-eta, fmaf(wd, w, g), w) : 0.f;  // padding units stay zero
           if (f < F && !isfinite(o[i])) ubad |= DS_FLAG_OUT_NONFINITE;
         }
         tmem_st8(tmem + lane_base + kColW1 + t * kHC + chalf * 8, o);
         if (f < F) store_wbf_half(Wbf, f, chalf, o);
-        tmem_wait_st();
         tc::fence_async_smem();
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(sgdd + t);
       }
+      tmem_wait_st();  // the master's stores (read by this thread again: next step or exchange)
       ubad = __reduce_or_sync(0xffffffffu, ubad);
       if (ubad && lane == 0) atomicOr(&s_bad, ubad);
       TSTAMP_MAIN(A.prof, step, 6, rank);
