@@ -246,25 +246,25 @@ __global__ void __launch_bounds__(kT) gather_kernel(SyncTable t, int self, unsig
 }
 
 // NVLink read probe (the all-gather's access pattern): n floats split over every peer's
-// slot region, copied into dst.
+// slot region, copied into dst. The CTAs are dealt round-robin to the peers, starting at a
+// rank-dependent peer, so every link is busy at once (a peer-after-peer walk would have all
+// ranks read the same peer together).
 __global__ void __launch_bounds__(kT) peer_read_kernel(SyncTable t, int self, uint64_t per, float* dst) {
-  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  int q = 0;
-  for (int k = 0; k < t.world; ++k) {
-    if (k == self) continue;
-    const float4* p4 = reinterpret_cast<const float4*>(t.slot[k]);
-    float4* d4 = reinterpret_cast<float4*>(dst + q * per);
-    const uint64_t nv = per / 4;
-    uint64_t u = tid;
-    for (; u + 3 * stride < nv; u += 4 * stride) {
-      const float4 v0 = __ldcg(p4 + u), v1 = __ldcg(p4 + u + stride), v2 = __ldcg(p4 + u + 2 * stride),
-                   v3 = __ldcg(p4 + u + 3 * stride);
-      d4[u] = v0, d4[u + stride] = v1, d4[u + 2 * stride] = v2, d4[u + 3 * stride] = v3;
-    }
-    for (; u < nv; u += stride) d4[u] = __ldcg(p4 + u);
-    ++q;
+  const uint32_t np = static_cast<uint32_t>(t.world - 1);
+  const uint32_t q = blockIdx.x % np, cq = blockIdx.x / np, nq = gridDim.x / np;
+  if (cq >= nq) return;
+  const int k = (self + 1 + static_cast<int>(q)) % t.world;  // never self
+  const float4* p4 = reinterpret_cast<const float4*>(t.slot[k]);
+  float4* d4 = reinterpret_cast<float4*>(dst + q * per);
+  const uint64_t nv = per / 4;
+  const uint64_t stride = static_cast<uint64_t>(nq) * blockDim.x;
+  uint64_t u = static_cast<uint64_t>(cq) * blockDim.x + threadIdx.x;
+  for (; u + 3 * stride < nv; u += 4 * stride) {
+    const float4 v0 = __ldcg(p4 + u), v1 = __ldcg(p4 + u + stride), v2 = __ldcg(p4 + u + 2 * stride),
+                 v3 = __ldcg(p4 + u + 3 * stride);
+    d4[u] = v0, d4[u + stride] = v1, d4[u + 2 * stride] = v2, d4[u + 3 * stride] = v3;
   }
+  for (; u < nv; u += stride) d4[u] = __ldcg(p4 + u);
 }
 
 struct IpcRecord {
