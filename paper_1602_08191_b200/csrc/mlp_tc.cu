@@ -98,11 +98,26 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem, uint64_t da, uint64_t db
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
       "l"(da), "l"(db), "r"(id), "r"(acc));
 }
+// one thread issues (the caller picks it): no per-MMA elect in a long chain
+__device__ __forceinline__ void mma_bf16_1(uint32_t tmem, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+                   tmem),
+               "l"(da), "l"(db), "r"(id), "r"(acc));
+}
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
       "l"(da), "l"(db), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit_1(uint64_t* mbar) {  // one thread (the caller picks it)
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void mma_tf32_1(uint32_t tmem, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+                   tmem),
+               "l"(da), "l"(db), "r"(id), "r"(acc));
 }
 __device__ __forceinline__ void commit_elect(uint64_t* mbar) {
   asm volatile(
@@ -610,35 +625,44 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
       tc::fence_after();
       const uint64_t da0 = sdesc_sw(saddr(Xbuf(buf)), 16, 1024, kSw128);
       tc::fence_after();
-      for (uint32_t t = 0; t < L.NT; ++t) {
-        if (t == 0) TSTAMP_M(A.prof, s, 2, rank);
-        if (t == 3) TSTAMP_M(A.prof, s, 3, rank);
-        if (t == L.NT - 1) TSTAMP_M(A.prof, s, 4, rank);
-        const uint32_t k1 = min(8 * (t + 1), L.NK);
-        for (uint32_t k = 8 * t; k < k1; ++k)  // +4096 B per 4 steps (next atom), +32 B inside
-          mma_bf16(tmem, da0 + (k >> 2) * 256 + (k & 3) * 2, fwd_b + k * 32, idesc_fwd, k > 0);
+      TSTAMP_M(A.prof, s, 2, rank);
+      if (lane == 0) {  // +4096 B per 4 K steps (next atom), +32 B inside; B +512 B per K step
+        uint64_t a = da0, b = fwd_b;
+#pragma unroll 4
+        for (uint32_t k = 0; k < L.NK; ++k, b += 32) {
+          mma_bf16_1(tmem, a + (k & 3) * 2, b, idesc_fwd, k > 0);
+          if ((k & 3) == 3) a += 256;
+        }
       }
-      commit_elect(fbar);
+      if (lane == 0) commit_1(fbar);
+      __syncwarp();
+      TSTAMP_M(A.prof, s, 4, rank);
       TSTAMP_M(A.prof, s, 5, rank);
       // the CTA's partial logits: P[64 x 16] = A1[64 x 16] . W2c[16 x 16]^T, tf32, K = 8 x 2
       if (!mbar_wait_or_quit(a1rdy, buf, quitp)) break;
       tc::fence_after();
+      if (lane == 0) {
 #pragma unroll
-      for (uint32_t kk = 0; kk < 2; ++kk)
-        mma_tf32(tmem + kColLg, sdesc_sw(saddr(A1c) + kk * 2048, 1024, 128, 0),
-                 sdesc_sw(saddr(W2cc) + kk * 512, 256, 128, 0), idesc_lg, kk > 0);
-      commit_elect(lgbar);
+        for (uint32_t kk = 0; kk < 2; ++kk)
+          mma_tf32_1(tmem + kColLg, sdesc_sw(saddr(A1c) + kk * 2048, 1024, 128, 0),
+                     sdesc_sw(saddr(W2cc) + kk * 512, 256, 128, 0), idesc_lg, kk > 0);
+        commit_1(lgbar);
+      }
+      __syncwarp();
       TSTAMP_M(A.prof, s, 6, rank);
       if (!mbar_wait_or_quit(d1rdy, buf, quitp)) break;  // delta1(s) in D1b; the policy decided
       TSTAMP_M(A.prof, s, 0, rank);
       tc::fence_after();
       const uint64_t dx0 = sdesc_sw(saddr(Xbuf(buf)), 4096, 1024, kSw128);
-      for (uint32_t t = 0; t < L.NT; ++t) {
+      if (lane == 0) {
+        for (uint32_t t = 0; t < L.NT; ++t) {
 #pragma unroll
-        for (uint32_t kk = 0; kk < 2; ++kk)  // K = 16 batch rows per MMA (2 row groups)
-          mma_bf16(tmem + kColDw + t * kHC, dx0 + t * 512 + kk * 128, dw_b + kk * 2, idesc_dw, kk > 0);
-        commit_elect(dtile + t);
+          for (uint32_t kk = 0; kk < 2; ++kk)  // K = 16 batch rows per MMA (2 row groups)
+            mma_bf16_1(tmem + kColDw + t * kHC, dx0 + t * 512 + kk * 128, dw_b + kk * 2, idesc_dw, kk > 0);
+          commit_1(dtile + t);
+        }
       }
+      __syncwarp();
       TSTAMP_M(A.prof, s, 1, rank);
     }
   } else {
