@@ -73,6 +73,7 @@ constexpr int kMaxC = 16;      // classes: the logits MMA's N
 constexpr int kMaxNC = 16;     // CTAs per cluster (non-portable size above 8)
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kBarCompute = 1;  // named barrier of the compute warps
+constexpr uint32_t kBarAct = 2;      // named barrier of compute warps 0, 1, 4, 5 (activations, W2 / b SGD)
 constexpr uint32_t kNumBars = 28;
 
 // ---------------------------------------------------------------------------------
@@ -852,39 +853,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
         }
       }
 
-      // ---- W2 / b1 / b2 SGD (overlaps the dW1 MMAs) --------------------------------------
       uint32_t ubad = 0;
-      for (uint32_t o = tid; o < kHC * C + kHC + C; o += kCT) {
-        float g0 = 0.f, g1 = 0.f;
-        float* dst;
-        if (o < kHC * C) {  // own W2 column entry (k, j) (model.cpp:219-221)
-          const uint32_t k = o >> 4, j = o & 15;
-          if (j >= HU) continue;
-#pragma unroll
-          for (int r = 0; r < kBM; r += 2) {
-            g0 = fmaf(D2(r, k), A1c[a1c_idx(r, j)], g0);
-            g1 = fmaf(D2(r + 1, k), A1c[a1c_idx(r + 1, j)], g1);
-          }
-          dst = W2cc + w2c_idx(k, j);
-        } else if (o < kHC * C + kHC) {  // own b1
-          const uint32_t j = o - kHC * C;
-          if (j >= HU) continue;
-#pragma unroll
-          for (int r = 0; r < kBM; r += 2) g0 += D1[r * 17 + j], g1 += D1[(r + 1) * 17 + j];
-          dst = b1c + j;
-        } else {  // b2, replicated in every CTA (same arithmetic)
-          const uint32_t k = o - kHC * C - kHC;
-#pragma unroll
-          for (int r = 0; r < kBM; r += 2) g0 += D2(r, k), g1 += D2(r + 1, k);
-          dst = b2s + k;
-        }
-        const float w = *dst;
-        const float out = fmaf(-eta, fmaf(wd, w, g0 + g1), w);
-        if (!isfinite(out)) ubad |= DS_FLAG_OUT_NONFINITE;
-        *dst = out;
-      }
-      tc::fence_async_smem();  // W2c is the next step's logits operand
-      csync();
       // ---- W1 SGD per tile from the TMEM dW1 tile and master; release the tile to the
       // MMA warp (forward of step s+1 reads the bf16 copy) ------------------------------
       for (uint32_t t = 0; t < L.NT; ++t) {
@@ -911,6 +880,43 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
         if (lane == 0) tc::mbar_arrive(sgdd + t);
       }
       tmem_wait_st();  // the master's stores (read by this thread again: next step or exchange)
+      // ---- W2 / b1 / b2 SGD, off the path to the next forward: warps 0, 1, 4, 5 — the
+      // ones that write the next step's activations and arrive on a1rdy, so their W2c /
+      // b1 updates are ordered before the next logits MMA and tanh -------------------------
+      if (warp < 2 || warp == 4 || warp == 5) {
+        const uint32_t gi = ((warp & 1u) | ((warp >> 2) << 1)) * 32 + lane;  // 0..127
+        for (uint32_t o = gi; o < kHC * C + kHC + C; o += 128) {
+          float g0 = 0.f, g1 = 0.f;
+          float* dst;
+          if (o < kHC * C) {  // own W2 column entry (k, j) (model.cpp:219-221)
+            const uint32_t k = o >> 4, j = o & 15;
+            if (j >= HU) continue;
+#pragma unroll
+            for (int r = 0; r < kBM; r += 2) {
+              g0 = fmaf(D2(r, k), A1c[a1c_idx(r, j)], g0);
+              g1 = fmaf(D2(r + 1, k), A1c[a1c_idx(r + 1, j)], g1);
+            }
+            dst = W2cc + w2c_idx(k, j);
+          } else if (o < kHC * C + kHC) {  // own b1
+            const uint32_t j = o - kHC * C;
+            if (j >= HU) continue;
+#pragma unroll
+            for (int r = 0; r < kBM; r += 2) g0 += D1[r * 17 + j], g1 += D1[(r + 1) * 17 + j];
+            dst = b1c + j;
+          } else {  // b2, replicated in every CTA (same arithmetic)
+            const uint32_t k = o - kHC * C - kHC;
+#pragma unroll
+            for (int r = 0; r < kBM; r += 2) g0 += D2(r, k), g1 += D2(r + 1, k);
+            dst = b2s + k;
+          }
+          const float w = *dst;
+          const float out = fmaf(-eta, fmaf(wd, w, g0 + g1), w);
+          if (!isfinite(out)) ubad |= DS_FLAG_OUT_NONFINITE;
+          *dst = out;
+        }
+        tc::fence_async_smem();  // W2c is the next step's logits operand
+        named_sync(kBarAct, 128);  // b1 / W2c complete before any of the four warps' next tanh
+      }
       ubad = __reduce_or_sync(0xffffffffu, ubad);
       if (ubad && lane == 0) atomicOr(&s_bad, ubad);
       TSTAMP_MAIN(A.prof, step, 6, rank);
