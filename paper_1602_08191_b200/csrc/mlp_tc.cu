@@ -1036,7 +1036,11 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
           };
           if (tid == 0) {
             mbar_expect_tx(cxbar, HU * F * 4);
-            pieces(0);
+            if (one_shard) {
+              for (uint32_t j = 0; j < HU; ++j) bulk_g2s(cst + j * F, c0p + g0 + static_cast<uint64_t>(j) * F, F * 4, cxbar);
+            } else {
+              pieces(0);
+            }
           }
           float* smp = nullptr;
           float* swp = nullptr;
@@ -1082,7 +1086,17 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
             // ordered: the new rows (this worker holds the center exclusively); LockFree: the
             // increments e as bulk f32 reductions — concurrent workers' exchanges add up
             // instead of overwriting each other (a lone writer gets m + e, as elastic_elem)
-            pieces(ordered ? 1 : 2);
+            if (one_shard) {
+              for (uint32_t j = 0; j < HU; ++j) {
+                float* dst = c0p + g0 + static_cast<uint64_t>(j) * F;
+                if (ordered)
+                  bulk_s2g(dst, cst + j * F, F * 4);
+                else
+                  bulk_add_s2g(dst, cst + j * F, F * 4);
+              }
+            } else {
+              pieces(ordered ? 1 : 2);
+            }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             if (ordered)  // written before the next ticket is released
               asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
