@@ -266,7 +266,7 @@ __host__ __device__ inline TcMsg tc_msg(uint32_t B, uint32_t C, uint32_t NC) {
   m.RP = (B + NC - 1) / NC;
   m.Cp = (C + 3) & ~3u;                                // a row's classes, padded to 16 bytes
   m.MR = m.RP * m.Cp + 4;                              // [RP][Cp] partial logits, flags piece
-  m.MG = m.RP * m.Cp + ((m.RP + 3) & ~3u) + 4;         // [RP][Cp] deltas, [RP] losses, flags
+  m.MG = m.RP * (m.Cp + 4);                           // per row: [Cp] deltas, loss, flags, 2 pad
   return m;
 }
 
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
   for (uint32_t i = tid; i < tc_small_floats(NC, M); i += kTT) fs[i] = 0.f;  // inboxes: pad words stay 0
   if (tid < kBM) {
     const uint32_t p = tid / RP;
-    d2off[tid] = p < NC ? static_cast<uint32_t>(inG - fs) + p * MG + (tid - p * RP) * Cp
+    d2off[tid] = p < NC ? static_cast<uint32_t>(inG - fs) + p * MG + (tid - p * RP) * (Cp + 4)
                         : static_cast<uint32_t>(zblk - fs);
     zblk[tid] = 0.f;
   }
@@ -755,10 +755,12 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
         break;
       }
       // ---- softmax-CE for the CTA's own rows (one warp per row, lane = class) -----------
-      uint32_t bad = 0;
-      for (uint32_t rr = warp; rr < RP && rank * RP + rr < kBM; rr += kCW) {
+      // Each row's warp sends the row's record — [Cp] deltas, loss, flags — straight from
+      // registers to every peer (G phase: every CTA gets every row), and writes its own copy.
+      const uint32_t nch = Cp / 4 + 1;  // float4 chunks per row record
+      for (uint32_t rr = warp; rr < RP; rr += kCW) {
         const uint32_t r = rank * RP + rr;
-        const bool valid = r < R;
+        const bool valid = r < R;  // rows past the batch (or past kBM) send zero records
         float z = -INFINITY;
         if (lane < C) {
           float acc[4] = {b2s[lane], 0.f, 0.f, 0.f};
@@ -774,36 +776,37 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
         float se = ez;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-        const uint32_t y = valid ? lab[buf * kBM + r] : 0u;
+        const uint32_t y = valid ? lab[buf * kBM + (r < kBM ? r : 0u)] : 0u;
+        uint32_t bad = 0;
         if (valid && y >= C) bad |= DS_FLAG_LABEL_RANGE;
         const float lse = mx + __logf(se);
         const float zy = __shfl_sync(0xffffffffu, z, y < C ? y : 0);
         const float loss = valid ? lse - zy : 0.f;
         if (valid && !isfinite(loss)) bad |= DS_FLAG_LOSS_NONFINITE;
         const float d = valid && lane < C ? (ez / se - (lane == y ? 1.f : 0.f)) / static_cast<float>(R) : 0.f;
-        // our own slot of the G inbox doubles as the staging of the message
-        if (lane < C) inG[rank * MG + rr * Cp + lane] = d;
-        if (lane == 0) inG[rank * MG + RP * Cp + rr] = loss;
-      }
-      bad = __reduce_or_sync(0xffffffffu, bad);
-      if (bad && lane == 0) atomicOr(&s_bad, bad);
-      csync();
-      // ---- G phase: every CTA gets every row's delta2 and loss ---------------------------
-      if (tid == 0) inG[rank * MG + MG - 4] = __uint_as_float(s_bad);
-      csync();
-      for (uint32_t i = tid; i < (NC - 1) * (MG / 4); i += kCT) {
-        uint32_t q = i / (MG / 4);
-        const uint32_t w0 = (i - q * (MG / 4)) * 4;
-        q += q >= rank ? 1u : 0u;  // every peer but us
-        st_async16(inG + rank * MG + w0, gbar, q, *reinterpret_cast<const float4*>(inG + rank * MG + w0));
+        const float fl = __uint_as_float(__reduce_or_sync(0xffffffffu, bad));
+        float* own = inG + rank * MG + rr * (Cp + 4);
+        if (lane < Cp) own[lane] = d;
+        if (lane == 0) own[Cp] = loss, own[Cp + 1] = fl;
+        for (uint32_t i0 = 0; i0 < (NC - 1) * nch; i0 += 32) {  // warp-uniform trips (shuffles)
+          const uint32_t i = i0 + lane;
+          const uint32_t c = i % nch, qi = i / nch;
+          const uint32_t src = c * 4 < Cp ? c * 4 : 0u;
+          const float v0 = __shfl_sync(0xffffffffu, d, src), v1 = __shfl_sync(0xffffffffu, d, (src + 1) & 31),
+                      v2 = __shfl_sync(0xffffffffu, d, (src + 2) & 31), v3 = __shfl_sync(0xffffffffu, d, (src + 3) & 31);
+          const float lz = __shfl_sync(0xffffffffu, loss, 0);
+          if (i < (NC - 1) * nch) {
+            const uint32_t q = qi + (qi >= rank ? 1u : 0u);  // every peer but us
+            const float4 v = c * 4 < Cp ? make_float4(v0, v1, v2, v3) : make_float4(lz, fl, 0.f, 0.f);
+            st_async16(own + c * 4, gbar, q, v);
+          }
+        }
       }
       if (NC > 1) tc::mbar_wait(gbar, ph);
       csync();
       TSTAMP_MAIN(A.prof, step, 4, rank);
-      uint32_t gbad = 0;
-#pragma unroll
-      for (uint32_t p = 0; p < kMaxNC; ++p)
-        if (p < NC) gbad |= __float_as_uint(inG[p * MG + MG - 4]);
+      uint32_t gbad = __float_as_uint(fs[d2off[lane] + Cp + 1]);  // lane = row (zero records past R)
+      gbad = __reduce_or_sync(0xffffffffu, gbad);
       if (gbad) {  // label / loss failure in loss_and_grad: stop before the update (model.cpp:176-181, 256)
         failed = true;
         bad_iter_step = static_cast<uint32_t>(step + 1);
@@ -838,7 +841,7 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
       // decision only at the next step, after every compute warp's SGD arrivals
       if (warp == kCW - 1) {  // batch loss (mean over rows) and the policy (engine.cpp:35-48)
         const uint32_t p = lane / RP;
-        double l = (lane < R && p < NC) ? static_cast<double>(inG[p * MG + RP * Cp + (lane - p * RP)]) : 0.0;
+        double l = (lane < R && p < NC) ? static_cast<double>(fs[d2off[lane] + Cp]) : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
         if (lane == 0) {
