@@ -364,8 +364,9 @@ int ds_engine_step_host_async(ds_engine* e, const float* X_host, const uint32_t*
  * sequence word, the kernel waits for the word, frees the slot after its grid barrier).
  * Every batch crosses PCIe as an H2D copy; each step's loss is written by the kernel to
  * *loss_host[step] (pinned, mapped: zero-copy D2H), valid after ds_engine_stream_end.
- * push blocks only while the ring is full. X_host/y_host of push s may be reused at push
- * s+DS_STREAM_RING. Fused one-hidden-layer engine; a Fixed or Adaptive policy (Adaptive needs the
+ * push blocks only while the ring is full. X_host/y_host of push s may be rewritten once
+ * push s+DS_STREAM_RING has returned (tensor-core engines copy them before push returns).
+ * Fused one-hidden-layer engine; a Fixed or Adaptive policy (Adaptive needs the
  * in-kernel exchange: no master, a LockFree/sharded one, or a TC engine). A host that stops pushing for
  * 20 s makes the kernel finish with DS_FLAG_STREAM_TIMEOUT rather than hang. */
 int ds_engine_stream_begin(ds_engine* e, uint64_t steps, double* loss_host);

@@ -235,7 +235,9 @@ def test_stream_mode_matches_device_sweep(L, orc, m, n, b, tau, steps, adaptive)
             from paper_1602_08191_b200.deepspark import DeepSpark
             idx, sizes = DeepSpark().sweep_batches(len(y), b, 31, steps)
             lossbuf = torch.zeros(steps, dtype=torch.float64, pin_memory=True)
-            ring = L.DS_STREAM_RING  # a pushed buffer may be reused DS_STREAM_RING pushes later
+            # the buffers of push s may be rewritten once push s + DS_STREAM_RING has RETURNED:
+            # rewriting them just before that push (ring buffers) races the copy of step s
+            ring = 2 * L.DS_STREAM_RING
             bufs = [(torch.empty((b, m.n_features), dtype=torch.float32, pin_memory=True),
                      torch.empty(b, dtype=torch.int32, pin_memory=True)) for _ in range(ring)]
             L.check(L.lib.ds_engine_stream_begin(e, steps, C.c_void_p(lossbuf.data_ptr())))
