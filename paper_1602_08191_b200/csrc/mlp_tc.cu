@@ -859,14 +859,17 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
       uint32_t ubad = 0;
       // ---- W1 SGD per tile from the TMEM dW1 tile and master; release the tile to the
       // MMA warp (forward of step s+1 reads the bf16 copy) ------------------------------
+      uint32_t wn[8];  // the next tile's master, loaded while this tile is processed
+      tmem_ld8_raw(tmem + lane_base + kColW1 + chalf * 8, wn);
       for (uint32_t t = 0; t < L.NT; ++t) {
         uint32_t gr[8], wr[8];
-        // the master tile first (only these threads write it), then the MMA's dW1 tile
-        tmem_ld8_raw(tmem + lane_base + kColW1 + t * kHC + chalf * 8, wr);
         tc::mbar_wait(dtile + t, ph);
         tc::fence_after();
         tmem_ld8_raw(tmem + lane_base + kColDw + t * kHC + chalf * 8, gr);
-        tmem_wait_ld2(wr, gr);
+        tmem_wait_ld2(wn, gr);  // also completes the master load issued last iteration
+#pragma unroll
+        for (int i = 0; i < 8; ++i) wr[i] = wn[i];
+        if (t + 1 < L.NT) tmem_ld8_raw(tmem + lane_base + kColW1 + (t + 1) * kHC + chalf * 8, wn);
         const uint32_t f = t * 128 + quarter * 32 + lane;
         float o[8];
 #pragma unroll
