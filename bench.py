@@ -546,7 +546,7 @@ def e2e_group_leg(args, L, api, engines, shards, seeds, rank, world, n):
     K, B, Wk = args.e2e_steps, args.batch, len(engines)
     # the host cores are shared by every rank's feeders: producer threads per worker
     local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
-    os.environ.setdefault("DS_STREAM_FEED_THREADS", str(max(1, min(4, (os.cpu_count() or 2) // (local * Wk) - 1))))
+    os.environ.setdefault("DS_STREAM_FEED_THREADS", str(max(1, min(4, (os.cpu_count() or 2) // (local * Wk)))))
     losses = [torch.zeros(K, dtype=torch.float64, pin_memory=True) for _ in range(Wk)]
     lp = (C.c_void_p * Wk)(*[lo.data_ptr() for lo in losses])
     arr = (C.c_void_p * Wk)(*[e.value for e in engines])
