@@ -1,7 +1,8 @@
 /* ds_oracle_alex.h — TEST INFRASTRUCTURE ONLY (see ds_oracle.c). f64 CPU restatement of
  * an AlexNet-shaped convnet for model kind 3 (BASELINE config 4; NOT IN
- * THE REFERENCE — parity unpinned; checked by central differences in
- * tests/test_oracle.py, not against a reference implementation).
+ * THE REFERENCE — no reference to pin against; checked by central differences in
+ * tests/test_oracle.py and against an independent PyTorch float64 autograd implementation
+ * of the same layers in tests/test_oracle_cnn_torch.py: loss to 1e-12, grads to 1 ulp).
  *
  * Conventions follow the reference's models (model.cpp:103-159): flat parameters, per
  * layer W[out x fan_in] row-major then b[out] (conv W in Caffe order [Cout][Cin/g][kh][kw]);

@@ -1,7 +1,8 @@
 /* ds_oracle_cnn.h — TEST INFRASTRUCTURE ONLY (see ds_oracle.c). f64 CPU restatement of
  * the Caffe cifar10_quick network for model kind 2 (NOT IN THE
- * REFERENCE — parity unpinned; this restatement is checked by central differences in
- * tests/test_oracle.py, not against a reference implementation).
+ * REFERENCE — no reference to pin against; this restatement is checked by central
+ * differences in tests/test_oracle.py and against an independent PyTorch float64 autograd
+ * implementation in tests/test_oracle_cnn_torch.py: loss to 1e-12, grads bit-exact).
  *
  * Conventions follow the reference's models (model.cpp:103-159): flat parameters, per
  * layer W[out x fan_in] row-major then b[out]; init U(+-1/sqrt(fan_in)) for weights and

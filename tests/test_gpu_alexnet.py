@@ -1,7 +1,8 @@
 """AlexNet-shaped convnet (model kind 3, BASELINE config 4) on the B200 against the f64 CPU
-restatement (oracle/ds_oracle_alex.c, pinned by central differences in test_oracle.py).
+restatement (oracle/ds_oracle_alex.c, pinned by central differences in test_oracle.py and
+against PyTorch float64 autograd to 1 ulp in test_oracle_cnn_torch.py).
 
-NOT IN THE REFERENCE (parity unpinned). Every contraction runs on the
+NOT IN THE REFERENCE (no reference implementation to pin against). Every contraction runs on the
 tcgen05 tensor cores with tf32 operands and f32 accumulation (csrc/gemm_tc.cu,
 csrc/alexnet.cu). Two bars:
   * f32-accurate products (DS_GEMM_3XTF32=1: each GEMM as three tf32 GEMMs on hi/lo
