@@ -345,8 +345,19 @@ def main():
     peak, pk = (bf16, "burst") if ms < 1000.0 else (bf16_sus, "sustained")
     # per worker and step the tensor pipe runs 49 forward MMAs (M64 N16 K16 bf16) + 2 logits MMAs
     # (M64 N16 K8 tf32) + 14 weight-gradient MMAs (M128 N16 K16 bf16) on each of the cluster's CTAs
+    # traffic: DRAM bytes per launch of the dominant kernel, from the committed ncu --set full
+    # capture (bytes per worker-step there) scaled to this run's launch (Wk workers x K steps)
+    traffic, traffic_note = None, None
+    dram_f = os.path.join(ROOT, "profiles", "r02_mlp_tc_dram.json")
+    if os.path.exists(dram_f):
+        with open(dram_f) as f:
+            dj = json.load(f)
+        traffic = dj["dram_bytes_per_worker_step"] * Wk * K
+        traffic_note = (f"bytes per launch ({Wk} workers x {K} steps) from {dj['source']}: "
+                        f"{dj['dram_bytes_per_worker_step']} B per worker-step vs "
+                        f"{dj['algorithmic_bytes_per_worker_step']} B algorithmic ({dj['algorithmic']})")
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": None, "peak_kind": f"{peak_kind} bf16 dense, {pk} (device window {ms:.0f} ms)",
+            "traffic": traffic, "traffic_note": traffic_note, "peak_kind": f"{peak_kind} bf16 dense, {pk} (device window {ms:.0f} ms)",
             "kernel": "mlp_tc_kernel (one cluster of 16 CTAs per worker: TMA gather4 multicast batches, tcgen05 "
                       "forward / logits / weight gradient, SGD from TMEM, policy, in-kernel exchange)",
             "algorithmic": f"{FLOP_PER_SAMPLE} FLOP/sample x {args.batch} x {Wk} workers x {steps_done} steps",
