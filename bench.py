@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--sync-params", type=int, default=62_378_344, help="synchronous round size (AlexNet's P)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / exchange sweep / cpu baseline (profiling)")
     ap.add_argument("--cifar-steps", type=int, default=200, help="timed steps of the cifar10_quick leg (0 = skip)")
+    ap.add_argument("--cifar-workers", type=int, default=8, help="workers on one GPU in the packed cifar10_quick leg")
     ap.add_argument("--alexnet-steps", type=int, default=20, help="timed steps of the AlexNet leg (0 = skip)")
     return ap.parse_args()
 
@@ -391,6 +392,7 @@ def main():
             line["sync_round"] = sync_leg(args, L, torch, dist, world, rank, local, nvl)
     if args.cifar_steps > 0:
         line["cifar10_quick"] = cifar_leg(args, L, api, torch, dist, world, rank, local)
+        line["cifar10_quick_packed"] = cifar_packed_leg(args, L, api, torch, dist, world, rank, local, args.cifar_workers)
         line["cifar10_quick_config3"] = {k: cifar_leg(args, L, api, torch, dist, world, rank, local, k)
                                          for k in ("sync", "adaptive")}
     if args.alexnet_steps > 0:
@@ -882,6 +884,96 @@ def cifar_leg(args, L, api, torch, dist, world, rank, local, mode="async"):
             out["loss_cut"] = cut
     return out
 
+
+
+def cifar_packed_leg(args, L, api, torch, dist, world, rank, local, workers=8):
+    """BASELINE config 2 with its largest worker count on ONE GPU: `workers` cifar10_quick
+    engines (batch 100 each, own stream and CUDA graphs, own data partition) training
+    asynchronously against one LockFree center on the same GPU (tau = 10). The engines'
+    launches overlap on the device. Device-timed: an event on engine 0's stream opens the
+    window (every other stream waits on it), engine 0's stream waits on every stream's end
+    event before the closing event. NOT IN THE REFERENCE (no conv layers)."""
+    B, K, N = 100, args.cifar_steps, 10000
+    Pc = 145578
+    from paper_1602_08191_b200.deepspark import Model
+    init_h = api.init_params(Model.cifar10_quick(10), INIT_SEED)
+    init = torch.from_numpy(init_h).to("cuda")
+    hidden = (C.c_uint32 * 1)(0)
+    desc = L.ds_model_desc(2, 3072, 10, 0, hidden)
+    m = C.c_void_p()
+    L.check(L.lib.ds_master_create(C.byref(m), local, Pc, C.c_float(0.1), L.DS_MODE_LOCKFREE,
+                                   C.c_void_p(init.data_ptr())))
+    engines, data = [], []
+    for w in range(workers):
+        Xc, yc = api.gen_synthetic(N, 3072, 10, 1.0, 1.0, 101 + rank * workers + w)
+        data.append((Xc, yc))
+        e = C.c_void_p()
+        hp = L.ds_hyper(0.01, 0.1, 10, B, 10 ** 9, 0.0, 0.0, 0)
+        L.check(L.lib.ds_engine_create(C.byref(e), local, C.byref(desc), Xc.ctypes.data, yc.ctypes.data, len(yc),
+                                       10, C.byref(hp), api.mix_seed(5, rank * workers + w),
+                                       C.c_void_p(init.data_ptr()), L.DS_ENGINE_AUTO))
+        L.check(L.lib.ds_engine_attach_master(e, m))
+        L.check(L.lib.ds_engine_reserve(e, K + 5))
+        engines.append(e)
+    for e in engines:
+        L.check(L.lib.ds_engine_run(e, 5, 0, None))
+    for e in engines:
+        L.check(L.lib.ds_engine_sync(e))
+    streams = []
+    for e in engines:
+        sp = C.c_void_p()
+        L.check(L.lib.ds_engine_stream(e, C.byref(sp)))
+        streams.append(torch.cuda.ExternalStream(sp.value))
+    n0 = []
+    for e in engines:
+        v = C.c_uint64()
+        L.check(L.lib.ds_engine_launches(e, C.byref(v)))
+        n0.append(v.value)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(streams[0])
+    for st in streams[1:]:
+        st.wait_event(e0)
+    chunk = 10
+    for k in range(0, K, chunk):  # interleaved enqueue keeps every stream fed
+        for e in engines:
+            L.check(L.lib.ds_engine_run(e, min(chunk, K - k), 0, None))
+    for st in streams[1:]:
+        ev = torch.cuda.Event()
+        ev.record(st)
+        streams[0].wait_event(ev)
+    e1.record(streams[0])
+    for e in engines:
+        L.check(L.lib.ds_engine_sync(e))
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    launches = 0
+    finite = True
+    for e, a in zip(engines, n0):
+        v = C.c_uint64()
+        L.check(L.lib.ds_engine_launches(e, C.byref(v)))
+        launches += int(v.value - a)
+        loss = np.zeros(K + 5)
+        L.check(L.lib.ds_engine_log(e, 0, K + 5, loss.ctypes.data, None, None, None))
+        finite = finite and bool(np.isfinite(loss).all())
+        L.lib.ds_engine_destroy(e)
+    xcount = C.c_uint64()
+    L.check(L.lib.ds_master_exchange_count(m, C.byref(xcount)))
+    L.lib.ds_master_destroy(m)
+    ms = t.item()
+    flop = 3 * 2 * 12_350_000 * B * K * workers
+    return {"metric": "train samples/s (cifar10_quick, BASELINE config 2: %d workers on one GPU)" % workers,
+            "value": world * workers * B * K / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms / K,
+            "steps": K, "batch_per_worker": B, "workers_per_gpu": workers, "tau": 10, "alpha": 0.1, "eta": 0.01,
+            "exchange": "LockFree, one center per GPU shared by its workers", "center_exchanges": int(xcount.value),
+            "achieved_tflops": flop / (ms / 1e3) / 1e12, "gpu_launches": launches, "losses_finite": finite,
+            "dtype": "tf32 tensor cores (tcgen05 implicit-GEMM convolutions), f32 elsewhere",
+            "data": "synthetic gen_synthetic 3072 features, 10,000 rows per worker",
+            "reference_arm": "none: the reference has no conv layers (SURVEY §8 a20)"}
 
 # multiply-adds per sample of the AlexNet-shaped net at S = 224 (oracle/ds_oracle_alex.h):
 # (MACs per output pixel x output pixels) per layer; training = forward + data gradient
