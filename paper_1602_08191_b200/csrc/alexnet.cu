@@ -774,12 +774,17 @@ int edge(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {  // `to` waits fo
   return DS_OK;
 }
 
-// splits so that tiles * splits covers the SMs twice, each split >= 4 k-steps, slabs fit
-uint32_t pick_splits(uint32_t M, uint32_t N, uint64_t K, uint32_t ntaps = 1) {
-  const uint32_t bn = gemm_pick_bn(N);
+// splits so that tiles * splits fills ONE wave of co-resident CTAs (148 SMs x the tile
+// width's CTAs per SM) without spilling over it — a few CTAs past a full wave run as a
+// whole extra CTA duration (conv4's weight gradient was 306 CTAs on 296 slots); each split
+// >= 4 k-steps, slabs fit. `bn` = the kernel's tile width (0: gemm_pick_bn(N)); the stacked
+// weight-gradient taps run ONE N-wide tile (240 = 5 taps x 48), not N / gemm_pick_bn(N).
+uint32_t pick_splits(uint32_t M, uint32_t N, uint64_t K, uint32_t ntaps = 1, uint32_t bn = 0) {
+  if (bn == 0) bn = gemm_pick_bn(N);
   const uint64_t tiles = 1ull * ((N + bn - 1) / bn) * ((M + 127) / 128) * ntaps;
+  const uint64_t slots = 148ull * gemm_ctas_per_sm(bn);
   if (tiles >= 148) return 1;
-  uint32_t sp = static_cast<uint32_t>((2 * 148 + tiles - 1) / tiles);
+  uint32_t sp = static_cast<uint32_t>(std::max<uint64_t>(1, slots / tiles));
   sp = static_cast<uint32_t>(std::min<uint64_t>(sp, std::max<uint64_t>(1, K / 128)));
   while (sp > 1 && 1ull * sp * M * N * ntaps > kPartFloats) --sp;
   return sp;
@@ -943,7 +948,7 @@ int conv_wgrad(const Ctx& c, const ConvSpec& cs, uint32_t R, const float* doutT,
     // for the resulting number of tap groups
     uint32_t tpc = std::min<uint32_t>(cs.KK(), 256 / cig);
     if (!(tpc > 1 && (tpc * cig == 192 || tpc * cig == 240 || tpc * cig == 256))) tpc = 1;
-    const uint32_t sp = pick_splits(cog, tpc * cig, G, (cs.KK() + tpc - 1) / tpc);
+    const uint32_t sp = pick_splits(cog, tpc * cig, G, (cs.KK() + tpc - 1) / tpc, tpc > 1 ? tpc * cig : 0);
     GemmEpilogue ep = epi(c, wtmp + 1ull * gi * cog * Kg, Kg, scale, nullptr, false);
     DS_TRY(launch_gemm(A, B, cog, cig, G, &tp, ep, sp, c.part, c.s));
     KDONE(sp > 1 ? 2 : 1);

@@ -657,6 +657,18 @@ int launch_3xtf32(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32
 
 // the tile width (MMA N) with the least padding past N; ties go to the wider tile, which
 // re-reads the A operand fewer times
+uint32_t gemm_ctas_per_sm(uint32_t bn) {  // co-resident CTAs of one tile width (GemmSmem<BN>::CTAS)
+  switch (bn) {
+    case 48: return GemmSmem<48>::CTAS;
+    case 64: return GemmSmem<64>::CTAS;
+    case 96: return GemmSmem<96>::CTAS;
+    case 128: return GemmSmem<128>::CTAS;
+    case 192: return GemmSmem<192>::CTAS;
+    case 240: return GemmSmem<240>::CTAS;
+    default: return GemmSmem<256>::CTAS;
+  }
+}
+
 uint32_t gemm_pick_bn(uint32_t N) {
   static const uint32_t cap = [] {  // DS_GEMM_MAXBN: cap the tile width (experiments)
     const char* e = getenv("DS_GEMM_MAXBN");

@@ -64,5 +64,6 @@ int launch_gemm(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32_t
 int launch_gemm_tf32(const float* A, uint64_t lda, const float* B, uint64_t ldb, uint32_t M, uint32_t N, uint32_t K,
                      const GemmEpilogue& ep, uint32_t splits, float* part, cudaStream_t s);
 uint32_t gemm_pick_bn(uint32_t N);
+uint32_t gemm_ctas_per_sm(uint32_t bn);
 
 }  // namespace dsb
