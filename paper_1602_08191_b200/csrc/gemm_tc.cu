@@ -47,7 +47,13 @@ struct GemmSmem {
 #ifndef DS_GEMM_TWO_CTA_MAX_BN
 #define DS_GEMM_TWO_CTA_MAX_BN 256
 #endif
-  static constexpr bool TWO_CTA = BN <= DS_GEMM_TWO_CTA_MAX_BN && BN != 240;  // 240: grouped taps, deep ring
+  // up to 128 wide: two (three up to 64) persistent CTAs per SM; 192 / 240 / 256 wide: one
+  // CTA with a deep ring, two accumulator buffers and eight epilogue warps (two CTAs with one
+  // buffer each, or one CTA with four epilogue warps, were slower: the epilogue of these
+  // tiles is as long as a short-K mainloop)
+  static constexpr bool TWO_CTA = BN <= DS_GEMM_TWO_CTA_MAX_BN && BN <= 128;
+  static constexpr int THREADS = BN <= 128 ? 256 : 384;  // warps 4.. are the epilogue
+  static constexpr int EPI_WARPS = THREADS / 32 - 4;
 #ifndef DS_GEMM_THREE_CTA_MAX_BN
 #define DS_GEMM_THREE_CTA_MAX_BN 64
 #endif
@@ -58,6 +64,11 @@ struct GemmSmem {
   static constexpr int STAGES = BUDGET / STAGE > 8 ? 8 : BUDGET / STAGE;
   static constexpr uint32_t TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;  // power of 2
+  // accumulator buffers per CTA: two (the epilogue of tile j overlaps the MMAs of tile j + 1)
+  // when every co-resident CTA's pair fits in the 512 TMEM columns, else one (192 / 256-wide
+  // tiles: two CTAs per SM overlap each other's epilogues instead — measured faster than one
+  // CTA per SM with two buffers, whose four epilogue warps could not keep up)
+  static constexpr uint32_t NBUF = CTAS * 2 * TMEM_COLS <= 512 ? 2 : 1;
 };
 
 // SWIZZLE_128B K-major descriptor: 8-row x 128 B atoms, atoms 1024 B apart (SBO); the
@@ -103,40 +114,68 @@ __device__ __forceinline__ int64_t map_row(const GemmEpilogue& ep, uint32_t row)
   return (static_cast<int64_t>(img) * ep.map_H + (yp - ep.map_pad)) * ep.map_H + (xp - ep.map_pad);
 }
 
+// One output tile's coordinates and k-loop (blockIdx of the one-tile-per-CTA grid).
+struct TileJob {
+  uint32_t n0, m0, z, split, t0, ntg, nvalid, stage_tx, nk, nkt, k_begin;
+  int tap;
+};
 template <int BN>
-__global__ void __launch_bounds__(kThreads, GemmSmem<BN>::CTAS)
+__device__ __forceinline__ TileJob tile_job(uint32_t T, uint32_t gx, uint32_t gy, const GemmTaps& tp, uint32_t N,
+                                            uint32_t K, uint32_t k_per_split, uint32_t splits) {
+  using S = GemmSmem<BN>;
+  TileJob j;
+  const uint32_t bx = T % gx, rest = T / gx, by = rest % gy;
+  j.z = rest / gy;
+  j.n0 = bx * BN;
+  j.m0 = by * kBM;
+  const bool acc_taps = tp.n > 0 && !tp.per_z;
+  j.tap = (tp.n > 0 && tp.per_z) ? static_cast<int>(j.z / splits) : -1;  // tap group
+  j.split = j.tap >= 0 ? j.z % splits : j.z;
+  // per_z with tpc > 1: taps tap*tpc .. + ntg - 1 share the A tile; their B tiles (n_tap rows
+  // each) are stacked along N in one BN-wide stage and one MMA covers them all
+  j.t0 = j.tap >= 0 ? static_cast<uint32_t>(j.tap) * tp.tpc : 0;
+  j.ntg = j.tap >= 0 ? min(tp.tpc, static_cast<uint32_t>(tp.n) - j.t0) : 1;
+  j.nvalid = (j.tap >= 0 && tp.tpc > 1) ? j.ntg * tp.n_tap : N;
+  j.stage_tx = (j.tap >= 0 && tp.tpc > 1) ? S::A_BYTES + j.ntg * tp.n_tap * kBK * 4 : S::STAGE;
+  j.nkt = 1;
+  j.k_begin = 0;
+  if (acc_taps) {
+    j.nkt = (tp.kt + kBK - 1) / kBK;
+    j.nk = tp.n * j.nkt;
+  } else {
+    j.k_begin = j.split * k_per_split;
+    const uint32_t k_end = min(K, j.k_begin + k_per_split);
+    j.nk = (k_end > j.k_begin) ? (k_end - j.k_begin + kBK - 1) / kBK : 0;
+  }
+  return j;
+}
+
+// Persistent: gridDim.x CTAs walk the tiles T = blockIdx.x, + gridDim.x, ... of the logical
+// (gx, gy, gz) grid (x fastest, so concurrently running CTAs share A tiles in L2). The TMA
+// ring runs on across tiles, and the accumulator is double-buffered in TMEM where it fits
+// (NBUF): the MMA warp fills buffer j % NBUF for tile j while the epilogue warps drain the
+// previous tile from the other.
+template <int BN>
+__global__ void __launch_bounds__(GemmSmem<BN>::THREADS, GemmSmem<BN>::CTAS)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmEpilogue ep, const __grid_constant__ GemmTaps tp, uint32_t M,
-                     uint32_t N, uint32_t K, uint32_t k_per_split, uint32_t splits) {
+                     uint32_t N, uint32_t K, uint32_t k_per_split, uint32_t splits, uint32_t gx, uint32_t gy,
+                     uint32_t ntiles) {
   using S = GemmSmem<BN>;
   constexpr int kStages = S::STAGES;
+  constexpr uint32_t kAcc = S::TMEM_COLS;  // columns per accumulator buffer
+  constexpr uint32_t kNB = S::NBUF;
   if (ep.gate && *ep.gate) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::STAGE);
   uint64_t* empty = full + kStages;
-  uint64_t* acc_full = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* acc_full = empty + kStages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2], one arrival per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM;
   const bool acc_taps = tp.n > 0 && !tp.per_z;
-  const int tap = (tp.n > 0 && tp.per_z) ? static_cast<int>(blockIdx.z / splits) : -1;  // tap group
-  const uint32_t split = tap >= 0 ? blockIdx.z % splits : blockIdx.z;
-  // per_z with tpc > 1: taps tap*tpc .. + ntg - 1 share the A tile; their B tiles (n_tap rows
-  // each) are stacked along N in one BN-wide stage and one MMA covers them all
-  const uint32_t t0 = tap >= 0 ? static_cast<uint32_t>(tap) * tp.tpc : 0;
-  const uint32_t ntg = tap >= 0 ? min(tp.tpc, static_cast<uint32_t>(tp.n) - t0) : 1;
-  const uint32_t nvalid = (tap >= 0 && tp.tpc > 1) ? ntg * tp.n_tap : N;
-  const uint32_t stage_tx = (tap >= 0 && tp.tpc > 1) ? S::A_BYTES + ntg * tp.n_tap * kBK * 4 : S::STAGE;
-  uint32_t nk, nkt = 1, k_begin = 0;
-  if (acc_taps) {
-    nkt = (tp.kt + kBK - 1) / kBK;
-    nk = tp.n * nkt;
-  } else {
-    k_begin = split * k_per_split;
-    const uint32_t k_end = min(K, k_begin + k_per_split);
-    nk = (k_end > k_begin) ? (k_end - k_begin + kBK - 1) / kBK : 0;
-  }
+  const uint32_t gz_total = ntiles / (gx * gy);
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -145,122 +184,149 @@ __global__ void __launch_bounds__(kThreads, GemmSmem<BN>::CTAS)
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    tc::mbar_init(acc_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], S::EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tc::tmem_alloc<S::TMEM_COLS>(tmem_slot);
+  if (warp == 1) tc::tmem_alloc<kNB * kAcc>(tmem_slot);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // TMA producer
-      for (uint32_t i = 0; i < nk; ++i) {
-        const int s = i % kStages;
-        if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-        uint8_t* sa = smem + s * S::STAGE;
-        mbar_expect_tx(&full[s], stage_tx);
-        int ax, ay, bx, by;
-        if (acc_taps) {
-          const uint32_t t = i / nkt, kc = i - t * nkt;
-          ax = tp.a_col[t] + static_cast<int>(kc * kBK);
-          ay = static_cast<int>(m0) + tp.a_row[t];
-          bx = tp.b_col[t] + static_cast<int>(kc * kBK);
-          by = static_cast<int>(n0) + tp.b_row[t];
-        } else {
-          ax = bx = static_cast<int>(k_begin + i * kBK);
-          ay = static_cast<int>(m0);
-          by = static_cast<int>(n0);
-          if (tap >= 0) {
-            ax += tp.a_col[t0], ay += tp.a_row[t0];
-            if (tp.tpc > 1) {  // one B sub-tile per tap of the group
-              for (uint32_t j = 1; j < ntg; ++j)
-                tma_load_2d(sa + S::A_BYTES + j * tp.n_tap * kBK * 4, &tmB, &full[s], bx + tp.b_col[t0 + j],
-                            by + tp.b_row[t0 + j]);
+    if (lane == 0) {  // TMA producer; the ring index i runs on across tiles
+      uint32_t i = 0;
+      for (uint32_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
+        const TileJob j = tile_job<BN>(T, gx, gy, tp, N, K, k_per_split, splits);
+        for (uint32_t kk = 0; kk < j.nk; ++kk, ++i) {
+          const int s = i % kStages;
+          if (i >= kStages) tc::mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+          uint8_t* sa = smem + s * S::STAGE;
+          mbar_expect_tx(&full[s], j.stage_tx);
+          int ax, ay, bx, by;
+          if (acc_taps) {
+            const uint32_t t = kk / j.nkt, kc = kk - t * j.nkt;
+            ax = tp.a_col[t] + static_cast<int>(kc * kBK);
+            ay = static_cast<int>(j.m0) + tp.a_row[t];
+            bx = tp.b_col[t] + static_cast<int>(kc * kBK);
+            by = static_cast<int>(j.n0) + tp.b_row[t];
+          } else {
+            ax = bx = static_cast<int>(j.k_begin + kk * kBK);
+            ay = static_cast<int>(j.m0);
+            by = static_cast<int>(j.n0);
+            if (j.tap >= 0) {
+              ax += tp.a_col[j.t0], ay += tp.a_row[j.t0];
+              if (tp.tpc > 1) {  // one B sub-tile per tap of the group
+                for (uint32_t g = 1; g < j.ntg; ++g)
+                  tma_load_2d(sa + S::A_BYTES + g * tp.n_tap * kBK * 4, &tmB, &full[s], bx + tp.b_col[j.t0 + g],
+                              by + tp.b_row[j.t0 + g]);
+              }
+              bx += tp.b_col[j.t0], by += tp.b_row[j.t0];
             }
-            bx += tp.b_col[t0], by += tp.b_row[t0];
           }
+          tma_load_2d(sa, &tmA, &full[s], ax, ay);
+          tma_load_2d(sa + S::A_BYTES, &tmB, &full[s], bx, by);
         }
-        tma_load_2d(sa, &tmA, &full[s], ax, ay);
-        tma_load_2d(sa + S::A_BYTES, &tmB, &full[s], bx, by);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       constexpr uint32_t idesc = tc::idesc_tf32(kBM, BN);
-      for (uint32_t i = 0; i < nk; ++i) {
-        const int s = i % kStages;
-        uint32_t nsub = kBK / 8;
-        if (acc_taps) {  // a tap's last chunk may be partial (kt multiple of 8)
-          const uint32_t rem = tp.kt - (i % nkt) * kBK;
-          nsub = rem >= kBK ? kBK / 8 : rem / 8;
-        }
-        tc::mbar_wait(&full[s], (i / kStages) & 1);
+      uint32_t i = 0, jt = 0;
+      for (uint32_t T = blockIdx.x; T < ntiles; T += gridDim.x, ++jt) {
+        const TileJob j = tile_job<BN>(T, gx, gy, tp, N, K, k_per_split, splits);
+        const uint32_t ab = jt % kNB;
+        if (jt >= kNB) tc::mbar_wait(&acc_empty[ab], ((jt / kNB) - 1) & 1);  // tile jt - kNB drained
         tc::fence_after();
-        const uint32_t a = tc::saddr(smem + s * S::STAGE), b = a + S::A_BYTES;
-        for (uint32_t kk = 0; kk < nsub; ++kk) {
-          const uint64_t da = sdesc_sw128(a + kk * 32), db = sdesc_sw128(b + kk * 32);
-          const uint32_t acc = (i | kk) ? 1u : 0u;
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-              "l"(da), "l"(db), "r"(idesc), "r"(acc));
-        }
-        tc::commit(&empty[s]);
-      }
-      tc::commit(acc_full);
-    }
-  } else if (warp >= 4) {  // epilogue warps 4..7: TMEM lane quadrant = warp % 4
-    const int q = warp & 3;
-    const uint32_t row = m0 + q * 32 + lane;
-    if (nk > 0) {
-      tc::mbar_wait(acc_full, 0);
-      tc::fence_after();
-    }
-    const bool raw = ep.raw || (tap < 0 && gridDim.z > 1) || (tap >= 0 && splits > 1);
-    float* out = raw ? ep.D + static_cast<uint64_t>(blockIdx.z) * ep.split_stride
-                     : ep.D + (tap >= 0 ? static_cast<uint64_t>(t0) * tp.d_col_step : 0);
-    const int64_t orow = row < M ? (raw ? static_cast<int64_t>(row) : map_row(ep, row)) : -1;
-    const uint64_t ldo = raw ? N : ep.ldd;
-    const float bm = (!raw && ep.bias_m && orow >= 0) ? ep.bias_m[row] : 0.f;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      float v[32];
-      if (nk > 0) {
-        tc::tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;
-      }
-      if (orow < 0 || n0 + c >= nvalid) continue;
-      float* dst = out + static_cast<uint64_t>(orow) * ldo + n0 + c;
-      const uint32_t lim = min(min(32u, static_cast<uint32_t>(BN - c)), nvalid - (n0 + c));  // BN = 48: last chunk 16 wide
-      if (!raw) {
-        const float* mrow = ep.mask ? ep.mask + static_cast<uint64_t>(orow) * ep.ldm + n0 + c : nullptr;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float x = v[j] * ep.scale + bm;
-          if (static_cast<uint32_t>(j) < lim) {
-            if (ep.bias_n) x += __ldg(ep.bias_n + n0 + c + j);
-            if (mrow && !(mrow[j] > 0.f)) x = 0.f;
+        const uint32_t acc_t = tmem + ab * kAcc;
+        for (uint32_t kk = 0; kk < j.nk; ++kk, ++i) {
+          const int s = i % kStages;
+          uint32_t nsub = kBK / 8;
+          if (acc_taps) {  // a tap's last chunk may be partial (kt multiple of 8)
+            const uint32_t rem = tp.kt - (kk % j.nkt) * kBK;
+            nsub = rem >= kBK ? kBK / 8 : rem / 8;
           }
-          v[j] = ep.relu ? fmaxf(x, 0.f) : x;
+          tc::mbar_wait(&full[s], (i / kStages) & 1);
+          tc::fence_after();
+          const uint32_t a = tc::saddr(smem + s * S::STAGE), b = a + S::A_BYTES;
+          for (uint32_t q = 0; q < nsub; ++q) {
+            const uint64_t da = sdesc_sw128(a + q * 32), db = sdesc_sw128(b + q * 32);
+            const uint32_t acc = (kk | q) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_t),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+          tc::commit(&empty[s]);
+        }
+        tc::commit(&acc_full[ab]);  // (a tile without k-steps: arrives once earlier MMAs are done)
+      }
+    }
+  } else if (warp >= 4) {  // epilogue warps: TMEM lane quadrant = warp % 4; with eight, column halves
+    const int q = warp & 3;
+    constexpr int kHalf = (BN / 2 + 31) / 32 * 32;
+    const int c_beg = S::EPI_WARPS == 8 && warp >= 8 ? kHalf : 0;
+    const int c_end = S::EPI_WARPS == 8 && warp < 8 ? kHalf : BN;
+    uint32_t jt = 0;
+    for (uint32_t T = blockIdx.x; T < ntiles; T += gridDim.x, ++jt) {
+      const TileJob j = tile_job<BN>(T, gx, gy, tp, N, K, k_per_split, splits);
+      const uint32_t ab = jt % kNB;
+      tc::mbar_wait(&acc_full[ab], (jt / kNB) & 1);
+      tc::fence_after();
+      const uint32_t acc_t = tmem + ab * kAcc;
+      const uint32_t row = j.m0 + q * 32 + lane;
+      const bool raw = ep.raw || (j.tap < 0 && gz_total > 1) || (j.tap >= 0 && splits > 1);
+      float* out = raw ? ep.D + static_cast<uint64_t>(j.z) * ep.split_stride
+                       : ep.D + (j.tap >= 0 ? static_cast<uint64_t>(j.t0) * tp.d_col_step : 0);
+      const int64_t orow = row < M ? (raw ? static_cast<int64_t>(row) : map_row(ep, row)) : -1;
+      const uint64_t ldo = raw ? N : ep.ldd;
+      const float bm = (!raw && ep.bias_m && orow >= 0) ? ep.bias_m[row] : 0.f;
+      const uint32_t n0 = j.n0, nvalid = j.nvalid;
+#pragma unroll 1
+      for (int c = c_beg; c < c_end; c += 32) {
+        float v[32];
+        if (j.nk > 0) {
+          tc::tmem_ld32(acc_t + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+        } else {
+#pragma unroll
+          for (int x = 0; x < 32; ++x) v[x] = 0.f;
+        }
+        if (orow < 0 || n0 + c >= nvalid) continue;
+        float* dst = out + static_cast<uint64_t>(orow) * ldo + n0 + c;
+        // BN = 48: last chunk 16 wide; 240: the second half's last chunk 16 wide
+        const uint32_t lim = min(min(32u, static_cast<uint32_t>(c_end - c)), nvalid - (n0 + c));
+        if (!raw) {
+          const float* mrow = ep.mask ? ep.mask + static_cast<uint64_t>(orow) * ep.ldm + n0 + c : nullptr;
+#pragma unroll
+          for (int x = 0; x < 32; ++x) {
+            float y = v[x] * ep.scale + bm;
+            if (static_cast<uint32_t>(x) < lim) {
+              if (ep.bias_n) y += __ldg(ep.bias_n + n0 + c + x);
+              if (mrow && !(mrow[x] > 0.f)) y = 0.f;
+            }
+            v[x] = ep.relu ? fmaxf(y, 0.f) : y;
+          }
+        }
+        if (lim == 32 && (ldo % 4) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+          for (int x = 0; x < 32; x += 4) *reinterpret_cast<float4*>(dst + x) = make_float4(v[x], v[x + 1], v[x + 2], v[x + 3]);
+        } else {
+#pragma unroll
+          for (int x = 0; x < 32; ++x)
+            if (static_cast<uint32_t>(x) < lim) dst[x] = v[x];
         }
       }
-      if (lim == 32 && (ldo % 4) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (static_cast<uint32_t>(j) < lim) dst[j] = v[j];
-      }
+      tc::fence_before();  // this warp's TMEM reads of the buffer are complete
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acc_empty[ab]);
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_free<S::TMEM_COLS>(tmem);
+  if (warp == 1) tc::tmem_free<kNB * kAcc>(tmem);
 }
 
 // Halo variant of the accumulating taps mode (conv forward / data gradient; opt-in, see
@@ -546,8 +612,16 @@ int launch_bn(const GemmOperand& A, const GemmOperand& B, const GemmEpilogue& ep
   const uint32_t kps = ((K + splits - 1) / splits + kBK - 1) / kBK * kBK;
   const uint32_t ngroups = (tp.n > 0 && tp.per_z) ? (tp.n + tp.tpc - 1) / tp.tpc : 1;
   const uint32_t zdim = (tp.n > 0 && tp.per_z) ? ngroups * splits : (tp.n > 0 ? 1 : splits);
-  dim3 grid((N + BN - 1) / BN, (M + kBM - 1) / kBM, zdim);
-  gemm_tf32_kernel<BN><<<grid, kThreads, GemmSmem<BN>::TOTAL, s>>>(ma, mb, ep, tp, M, N, K, kps, splits);
+  const uint32_t gx = (N + BN - 1) / BN, gy = (M + kBM - 1) / kBM;
+  const uint64_t ntiles = 1ull * gx * gy * zdim;
+  if (ntiles == 0) return DS_OK;
+  if (ntiles > 0xFFFFFFFFull) return set_error(DS_E_CONTRACT, "gemm: too many tiles");
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t slots = static_cast<uint64_t>(nsm) * GemmSmem<BN>::CTAS;  // persistent CTAs
+  const uint32_t grid = static_cast<uint32_t>(ntiles < slots ? ntiles : slots);
+  gemm_tf32_kernel<BN><<<grid, GemmSmem<BN>::THREADS, GemmSmem<BN>::TOTAL, s>>>(ma, mb, ep, tp, M, N, K, kps, splits, gx, gy,
+                                                                   static_cast<uint32_t>(ntiles));
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
