@@ -300,12 +300,25 @@ __global__ void __launch_bounds__(GemmSmem<BN>::THREADS, GemmSmem<BN>::CTAS)
         const uint32_t lim = min(min(32u, static_cast<uint32_t>(c_end - c)), nvalid - (n0 + c));
         if (!raw) {
           const float* mrow = ep.mask ? ep.mask + static_cast<uint64_t>(orow) * ep.ldm + n0 + c : nullptr;
+          float mk[32];  // the ReLU mask row (data gradient), 16-byte loads when aligned
+          if (mrow) {
+            if (lim == 32 && (reinterpret_cast<uintptr_t>(mrow) & 15) == 0) {
+#pragma unroll
+              for (int x = 0; x < 32; x += 4) {
+                const float4 m4 = __ldg(reinterpret_cast<const float4*>(mrow + x));
+                mk[x] = m4.x, mk[x + 1] = m4.y, mk[x + 2] = m4.z, mk[x + 3] = m4.w;
+              }
+            } else {
+#pragma unroll
+              for (int x = 0; x < 32; ++x) mk[x] = static_cast<uint32_t>(x) < lim ? mrow[x] : 1.f;
+            }
+          }
 #pragma unroll
           for (int x = 0; x < 32; ++x) {
             float y = v[x] * ep.scale + bm;
             if (static_cast<uint32_t>(x) < lim) {
               if (ep.bias_n) y += __ldg(ep.bias_n + n0 + c + x);
-              if (mrow && !(mrow[x] > 0.f)) y = 0.f;
+              if (mrow && !(mk[x] > 0.f)) y = 0.f;
             }
             v[x] = ep.relu ? fmaxf(y, 0.f) : y;
           }
