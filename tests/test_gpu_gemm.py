@@ -64,6 +64,16 @@ def test_epilogue_and_strides(L):
     run(L, torch, 190, 100, 96, bias_m=True, scale=-2.0)
 
 
+@pytest.mark.parametrize("M,N,K", [(128 * 500, 48, 64), (128 * 700 + 5, 96, 72), (128 * 320, 128, 40),
+                                   (128 * 300 + 17, 192, 96), (128 * 300, 256, 64), (128 * 3, 200, 5000)])
+def test_persistent_tiles(L, M, N, K):
+    """More tiles than co-resident CTAs for every tile width (each persistent CTA walks several
+    tiles through both TMEM accumulator buffers), ragged M, short and long K."""
+    import torch
+    lda = (K + 3) // 4 * 4
+    run(L, torch, M, N, K, lda=lda, ldb=lda, bias_n=True, relu=True, seed=M % 7)
+
+
 @pytest.mark.parametrize("splits", [2, 4, 9])
 def test_split_k(L, splits):
     import torch
