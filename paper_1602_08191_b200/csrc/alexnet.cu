@@ -21,6 +21,7 @@
 // GEMM epilogues), rounded to f32 like the reference's Grad = f32(sum / b). Dropout is
 // omitted (deterministic; see the oracle).
 #include <algorithm>
+#include <initializer_list>
 
 #include "ds_common.cuh"
 #include "gemm_tc.cuh"
@@ -709,6 +710,29 @@ __global__ void zero_border_kernel(float* __restrict__ map, uint32_t Hp, uint32_
   }
 }
 
+// Several maps' borders in one launch (blocks [first[i], first[i + 1]) clear map i): the
+// per-step border clears were 11 launches of ~7 us each, latency not bandwidth
+struct BorderMaps {
+  float* p[6];
+  uint32_t Hp[6], pad[6], H[6], C[6], first[7];
+  uint32_t n;
+};
+__global__ void zero_borders_kernel(const __grid_constant__ BorderMaps bm, const uint32_t* gate) {
+  GATE;
+  uint32_t i = 0;
+  while (i + 1 < bm.n && blockIdx.x >= bm.first[i + 1]) ++i;
+  const uint32_t b = blockIdx.x - bm.first[i], Hp = bm.Hp[i], pad = bm.pad[i], H = bm.H[i], C = bm.C[i];
+  const uint32_t r = b / Hp, yp = b - r * Hp;
+  float* row = bm.p[i] + (static_cast<uint64_t>(r) * Hp + yp) * Hp * C;
+  const bool full = yp < pad || yp >= pad + H;
+  const uint32_t n = full ? Hp * C : (Hp - H) * C;  // the row, or its left + right edges
+  for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+    uint32_t e = k;
+    if (!full && e >= pad * C) e += H * C;  // skip the interior columns
+    row[e] = 0.f;
+  }
+}
+
 // argmax of the logits (first maximum), hits against labels (predict, model.cpp:303-318)
 __global__ void alex_hits_kernel(const float* __restrict__ z, uint32_t ldz, const uint32_t* __restrict__ y, uint32_t R,
                                  uint32_t C, uint32_t* pred, unsigned long long* hits) {
@@ -860,7 +884,28 @@ int zero(const Ctx& c, float* p, uint64_t floats) {
   return DS_OK;
 }
 
-// clear only the border of a padded map (the interior is fully rewritten before it is read)
+struct BorderSpec {
+  float* p;
+  uint32_t Hp, pad, H, C;
+};
+// clear only the borders of padded maps (the interiors are fully rewritten before they are read)
+int zero_borders(const Ctx& c, uint32_t R, std::initializer_list<BorderSpec> maps) {
+  BorderMaps bm{};
+  uint32_t blocks = 0;
+  for (const BorderSpec& m : maps) {
+    if (bm.n == 6) return set_error(DS_E_CONTRACT, "zero_borders: at most 6 maps");
+    bm.p[bm.n] = m.p, bm.Hp[bm.n] = m.Hp, bm.pad[bm.n] = m.pad, bm.H[bm.n] = m.H, bm.C[bm.n] = m.C;
+    bm.first[bm.n] = blocks;
+    blocks += R * m.Hp;
+    ++bm.n;
+  }
+  bm.first[bm.n] = blocks;
+  zero_borders_kernel<<<blocks, 256, 0, c.s>>>(bm, c.gate);
+  ++t_launches;
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
 int zero_border(const Ctx& c, float* p, uint32_t R, uint32_t Hp, uint32_t pad, uint32_t H, uint32_t C) {
   zero_border_kernel<<<R * Hp, 256, 0, c.s>>>(p, Hp, pad, H, C, c.gate);
   ++t_launches;
@@ -982,11 +1027,9 @@ int alex_forward(const ModelInfo& m, const float* P, const float* X, const uint3
     KDONE(1);
   }
   // padded maps: zero borders (interiors are rewritten below)
-  DS_TRY(zero_border(c, w.p1p, R, sh.Hp2, 2, sh.P1, 96));
-  DS_TRY(zero_border(c, w.p2p, R, sh.Hp3, 1, sh.P2, 256));
-  DS_TRY(zero_border(c, w.a3p, R, sh.Hp3, 1, sh.P2, 384));
-  DS_TRY(zero_border(c, w.a4p, R, sh.Hp3, 1, sh.P2, 384));
-  DS_TRY(zero_border(c, w.a5p, R, sh.Hp3, 1, sh.P2, 256));
+  DS_TRY(zero_borders(c, R, {{w.p1p, sh.Hp2, 2, sh.P1, 96}, {w.p2p, sh.Hp3, 1, sh.P2, 256},
+                             {w.a3p, sh.Hp3, 1, sh.P2, 384}, {w.a4p, sh.Hp3, 1, sh.P2, 384},
+                             {w.a5p, sh.Hp3, 1, sh.P2, 256}}));
   // conv1 (space-to-depth, 3x3 taps) + relu, LRN1, pool1 -> p1p (pad 2)
   s2d_kernel<<<nblk(1ull * R * sh.Hs * sh.Hs * 48), 256, 0, s>>>(X, idx, F, sh.S, R, sh.Hs, w.xs, gate);
   KDONE(1);
@@ -1087,11 +1130,9 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
   DS_TRY(gemm(c, w.dh6, 4096, w.w6T, 4096, w.dp5, sh.q5, R, static_cast<uint32_t>(sh.q5), 4096, 1.f, nullptr, false));
 
   // ---- conv5 .. conv2 on the padded grids ------------------------------------------------
-  DS_TRY(zero_border(c, w.dc5p, R, sh.Hp3, 1, sh.P2, 256));
-  DS_TRY(zero_border(c, w.dc4p, R, sh.Hp3, 1, sh.P2, 384));
-  DS_TRY(zero_border(c, w.dc3p, R, sh.Hp3, 1, sh.P2, 384));
-  DS_TRY(zero_border(c, w.dc2p, R, sh.Hp2, 2, sh.P1, 256));
-  DS_TRY(zero_border(c, w.dc1p, R, sh.Hs, 1, sh.H1, 96));
+  DS_TRY(zero_borders(c, R, {{w.dc5p, sh.Hp3, 1, sh.P2, 256}, {w.dc4p, sh.Hp3, 1, sh.P2, 384},
+                             {w.dc3p, sh.Hp3, 1, sh.P2, 384}, {w.dc2p, sh.Hp2, 2, sh.P1, 256},
+                             {w.dc1p, sh.Hs, 1, sh.H1, 96}, {w.dp2p, sh.Hp3, 1, sh.P2, 256}}));
   // pool5 backward (per-row CHW pooled map) with the ReLU5 mask (a5p) -> dc5p
   maxpool_bwd_kernel<<<static_cast<unsigned>((M3 + 7) / 8), 256, 0, s>>>(w.dp5, w.arg5, R, sh.P2, 256, sh.P5, 0, 1, 1, w.a5p,
                                                                 w.dc5p, gate);
@@ -1116,7 +1157,6 @@ int launch_alex_loss_and_grad(const ModelInfo& m, const float* P, const float* X
     if (l >= 2) {  // into relu(conv3 / conv4): masked, same padded grid
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], dout_maps[l - 1], true, in_maps[l]));
     } else if (l == 1) {  // into pool2(LRN2(relu(conv2))): d(p2p), pool2 bwd, LRN2 bwd -> dc2p
-      DS_TRY(zero_border(c, w.dp2p, R, sh.Hp3, 1, sh.P2, 256));
       DS_TRY(conv_dgrad(c, cs, R, dout, w.wpT[l], w.dp2p, true, nullptr));
       pool_lrn_bwd_relu_kernel<<<static_cast<unsigned>((M2 + 7) / 8), 256, 0, s>>>(w.dp2p, w.arg2, w.a2, R, sh.P1, 256,
                                                                              sh.P2, 1, 2, sh.Hp2, w.dc2p, gate);
