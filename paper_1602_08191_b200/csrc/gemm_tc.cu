@@ -742,8 +742,6 @@ int launch_3xtf32(const GemmOperand& A, const GemmOperand& B, uint32_t M, uint32
 
 }  // namespace
 
-// the tile width (MMA N) with the least padding past N; ties go to the wider tile, which
-// re-reads the A operand fewer times
 uint32_t gemm_ctas_per_sm(uint32_t bn) {  // co-resident CTAs of one tile width (GemmSmem<BN>::CTAS)
   switch (bn) {
     case 48: return GemmSmem<48>::CTAS;
@@ -756,6 +754,8 @@ uint32_t gemm_ctas_per_sm(uint32_t bn) {  // co-resident CTAs of one tile width 
   }
 }
 
+// the tile width (MMA N) with the least padding past N; ties go to the wider tile, which
+// re-reads the A operand fewer times
 uint32_t gemm_pick_bn(uint32_t N) {
   static const uint32_t cap = [] {  // DS_GEMM_MAXBN: cap the tile width (experiments)
     const char* e = getenv("DS_GEMM_MAXBN");
