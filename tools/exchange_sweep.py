@@ -30,6 +30,12 @@ def main():
     except Exception:
         peak = 6552.3
     s = torch.cuda.current_stream()
+    nvl = None
+    if world > 1:  # in-run NVLink read peak (bench.py's probe: every rank reads its peers concurrently)
+        import bench
+        nvl = bench.nvlink_peak(L, torch, dist, world, rank, local)
+        if rank == 0:
+            print(json.dumps({"nvlink_peak": nvl}), flush=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for P in (1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20, 500 * (1 << 20)):
         g = torch.Generator(device="cuda").manual_seed(7 + rank)
@@ -60,8 +66,35 @@ def main():
         ms = t.item()
         rec = {"gpus": world, "params": P, "ms": ms, "exchanges_per_s_per_gpu": 1e3 / ms,
                "gbs_per_gpu": 16.0 * P / (ms / 1e3) / 1e9, "frac_hbm": 16.0 * P / (ms / 1e3) / 1e9 / peak}
+        # tau: one period = tau local SGD updates of the worker vector (ds_sgd_update in place,
+        # 12 B/param, the update a worker applies between exchanges) + one exchange
+        gbuf = torch.rand(P, device="cuda", generator=g) * 1e-3
+        sgd = lambda: L.check(L.lib.ds_sgd_update(C.c_void_p(w.data_ptr()), C.c_void_p(w.data_ptr()),  # noqa: E731
+                                                  C.c_void_p(gbuf.data_ptr()), P, C.c_float(1e-3), C.c_float(0.0),
+                                                  None, C.c_void_p(s.cuda_stream)))
+        for tau in (1, 4, 16):
+            reps = max(2, iters // tau)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0.record(s)
+            for _ in range(reps):
+                for _ in range(tau):
+                    sgd()
+                call()
+            e1.record(s)
+            torch.cuda.synchronize()
+            tt = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            rec[f"tau{tau}"] = {"ms_per_period": tt.item(), "exchanges_per_s_per_gpu": 1e3 / tt.item(),
+                                "exchange_share": ms / tt.item()}
+        del gbuf
         if world > 1:
             rec["nvlink_gbs_per_gpu_per_dir"] = 8.0 * P * (world - 1) / world / (ms / 1e3) / 1e9
+            pk = nvl.get("gbs_per_gpu") if isinstance(nvl, dict) else nvl
+            if pk:
+                rec["frac_nvlink_peak"] = rec["nvlink_gbs_per_gpu_per_dir"] / pk
             dist.barrier()
             L.lib.ds_master_destroy(mh)
             del init
