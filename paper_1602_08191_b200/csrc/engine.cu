@@ -441,6 +441,7 @@ int fused_args(ds_engine* e, uint64_t steps, bool in_kernel_exchange, FusedArgs&
   a.has_master = (e->master && in_kernel_exchange) ? 1 : 0;
   if (a.has_master) {
     a.table = e->master->table;
+    a.center_local = (!e->master->sharded && e->master->world == 1) ? 1 : 0;
     a.lockfree = e->master->mode == DS_MODE_LOCKFREE && e->tickets.empty();
     a.tickets = e->tickets.empty() ? nullptr : e->d_tickets + e->host_exchanges;
     if (a.tickets) {
@@ -988,7 +989,18 @@ int run_group(ds_engine** engines, uint32_t n, uint64_t steps) {
       DS_CUDA_TRY(cudaStreamWaitEvent(e0->stream, ev, 0));
     }
   }
+  // DS_FUSED_PROFILE=<file>: per-phase stamps of worker 0's CTA 0 (as run_fused)
+  const char* prof_path = std::getenv("DS_FUSED_PROFILE");
+  unsigned long long* prof = nullptr;
+  const uint64_t prof_n = steps * (kProfSlots + 2 * static_cast<uint64_t>(e0->fused_grid)) + 8;
+  if (prof_path && steps >= 8 && !e0->ring_active) {
+    DS_CUDA_TRY(cudaMalloc(&prof, prof_n * sizeof(unsigned long long)));
+    DS_CUDA_TRY(cudaMemsetAsync(prof, 0, prof_n * sizeof(unsigned long long), e0->stream));
+    a[0].prof = prof;
+    a[0].prof_cta = prof + steps * kProfSlots;
+  }
   DS_TRY(dsb::launch_tc_group(a.data(), tm.data(), n, e0->tc_nc, e0->stream));
+  if (prof) DS_TRY(dump_profile(e0, prof, steps, prof_n, prof_path));
   DS_CUDA_TRY(cudaEventRecord(ev, e0->stream));
   for (uint32_t i = 0; i < n; ++i) {
     ds_engine* e = engines[i];

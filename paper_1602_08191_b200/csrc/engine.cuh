@@ -60,6 +60,7 @@ struct FusedArgs {
   int has_master;
   ShardTable table;
   int lockfree;               // plain stores, no tickets
+  int center_local;           // the center and its control words are touched by this GPU only (gpu-scope fences)
   const uint64_t* tickets;    // per-exchange global tickets (deterministic), or null
   unsigned long long* ticket_src;  // Locked: dispenser (shard 0 flags.next_ticket)
   int stop_at_exchange;

@@ -1173,7 +1173,9 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
         tc::fence_async_smem();
         tc::fence_before();
         csync();
-        if (tid == 0 && ordered) __threadfence_system();  // this CTA's center writes (cumulative over the barrier)
+        // this CTA's center writes (cumulative over the barrier); a center that only this GPU
+        // touches needs gpu scope — the system-scope fences cost ~4 us per ordered exchange
+        if (tid == 0 && ordered) A.center_local ? __threadfence() : __threadfence_system();
         TSTAMP_X(A.prof, step, 3, rank);
         if (NC > 1) {
           if (rank != 0) {
@@ -1198,10 +1200,16 @@ __global__ void __launch_bounds__(kTT, 1) mlp_tc_kernel(const __grid_constant__ 
         }
         if (rank == 0 && tid == 0 && !(s_bad & DS_FLAG_TICKET_TIMEOUT)) {
           if (ordered) {
-            __threadfence_system();
-            T.flags[0]->exchanges += 1;
-            __threadfence_system();
-            for (int s = 0; s < T.n; ++s) st_release_sys(reinterpret_cast<uint64_t*>(&T.flags[s]->seq), tk + 1);
+            if (A.center_local) {
+              __threadfence();
+              T.flags[0]->exchanges += 1;
+              asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&T.flags[0]->seq), "l"(tk + 1) : "memory");
+            } else {
+              __threadfence_system();
+              T.flags[0]->exchanges += 1;
+              __threadfence_system();
+              for (int s = 0; s < T.n; ++s) st_release_sys(reinterpret_cast<uint64_t*>(&T.flags[s]->seq), tk + 1);
+            }
           } else {
             atomicAdd_system(&T.flags[0]->exchanges, 1ull);
           }
