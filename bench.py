@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--tau", type=int, default=10)
     ap.add_argument("--workers", type=int, default=2, help="EASGD workers per GPU (BASELINE config 1: 2)")
     ap.add_argument("--min-window-ms", type=float, default=200.0, help="repeat the K-step launch up to this")
-    ap.add_argument("--e2e-steps", type=int, default=20000)
+    ap.add_argument("--e2e-steps", type=int, default=60000, help="e2e steps per worker (a window of ~0.5 s: short host windows are noisy)")
     ap.add_argument("--det-steps", type=int, default=20000, help="timed steps of the deterministic config-1 leg")
     ap.add_argument("--exchange-params", type=int, default=256 * 1024 * 1024)
     ap.add_argument("--sync-params", type=int, default=62_378_344, help="synchronous round size (AlexNet's P)")
