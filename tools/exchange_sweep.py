@@ -104,6 +104,23 @@ def main():
         torch.cuda.empty_cache()
         if rank == 0:
             print(json.dumps(rec), flush=True)
+    if world == 1 and os.environ.get("SWEEP_CPU_REF", "1") == "1":
+        # the reference's own exchange beside it: MasterState::exchange
+        # of the UNMODIFIED reference (oracle/_ref) in-process on this host — 1 thread Locked,
+        # and T threads LockFree; seconds per exchange and GB/s at 16 B/param
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from oracle.oracle import Oracle
+        ref = Oracle("dsref")
+        T = os.cpu_count() or 1
+        for P in (1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20):
+            it = max(1, (64 << 20) // P)
+            for lockfree, threads in ((False, 1), (True, T)):
+                if threads > 1 and P > (64 << 20):
+                    continue  # T private worker vectors of 1 GB each
+                sec = ref.master_exchange_time(P, lockfree, threads, it) / it
+                print(json.dumps({"cpu_reference": True, "params": P, "mode": "LockFree" if lockfree else "Locked",
+                                  "threads": threads, "ms_per_exchange_per_thread": sec * 1e3,
+                                  "gbs_total": 16.0 * P * threads / sec / 1e9}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
