@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "conv_tc.cuh"
 #include "ds_common.cuh"
 
@@ -235,7 +237,7 @@ template <int CIN, int COUT, int H, int SPS>
 __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const float* __restrict__ in,
                                                                        const float* __restrict__ dout,
                                                                        float* __restrict__ part, uint32_t R,
-                                                                       const uint32_t* gate) {
+                                                                       uint32_t sps, const uint32_t* gate) {
   using S = WgradShape<CIN, COUT, H, SPS>;
   static_assert(S::HW % kKC == 0 && COUT % 32 == 0, "wgrad tiling");
   if (gate && *gate) return;
@@ -248,7 +250,7 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
   const uint32_t mt = blockIdx.x, split = blockIdx.y;
   constexpr int kLag = 1;  // chunks of LDGSTS in flight per producer before it hands a stage over
-  const uint32_t n_lo = split * SPS, n_hi = min(n_lo + SPS, R);
+  const uint32_t n_lo = split * sps, n_hi = min(n_lo + sps, R);
   const int nchunks = static_cast<int>(n_hi > n_lo ? (n_hi - n_lo) * S::CPS : 0);
   if (warp == 4) tc::tmem_alloc<S::TMEM_COLS>(&tmem_base);
   if (tid == 0) {
@@ -523,8 +525,16 @@ int launch_conv5_wgrad_tc(const float* in, const float* dout, float* part, float
     DS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::SMEM)));
     attr = true;
   }
-  const uint32_t nsplit = (R + SPS - 1) / SPS;
-  k<<<dim3(S::MT, nsplit), kTile + 32, S::SMEM, s>>>(in, dout, part, R, gate);
+  // samples per split: as few as fill ONE wave of CTAs (S::MT x nsplit <= 148; conv2's 7 x 25
+  // = 175 CTAs ran a second wave for 27 of them), never fewer than SPS (the partials buffer
+  // holds ceil(R / SPS) splits)
+  int nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t per_wave = std::max<uint32_t>(1, static_cast<uint32_t>(nsm) / S::MT);
+  const uint32_t sps = std::max<uint32_t>(SPS, (R + per_wave - 1) / per_wave);
+  const uint32_t nsplit = (R + sps - 1) / sps;
+  k<<<dim3(S::MT, nsplit), kTile + 32, S::SMEM, s>>>(in, dout, part, R, sps, gate);
   const uint32_t n = (S::K + 1) * COUT;
   if (nsplit >= 32)
     wgrad_reduce_warp_kernel<<<(n * 32 + 255) / 256, 256, 0, s>>>(part, nsplit, CIN, COUT, S::kHWC, gW, gb, inv_b, flags,
@@ -539,7 +549,7 @@ template int launch_conv5_wgrad_tc<3, 32, 32, 1>(const float*, const float*, flo
                                                   uint32_t*, const uint32_t*, cudaStream_t);
 template int launch_conv5_wgrad_tc<32, 32, 16, 4>(const float*, const float*, float*, float*, float*, uint32_t, float,
                                                    uint32_t*, const uint32_t*, cudaStream_t);
-template int launch_conv5_wgrad_tc<32, 64, 8, 8>(const float*, const float*, float*, float*, float*, uint32_t, float,
+template int launch_conv5_wgrad_tc<32, 64, 8, 4>(const float*, const float*, float*, float*, float*, uint32_t, float,
                                                   uint32_t*, const uint32_t*, cudaStream_t);
 
 }  // namespace dsb

@@ -585,8 +585,8 @@ CnnWs carve(uint32_t R, uint32_t C, void* base) {
   // partials: conv1 per sample (100 x 2400), conv2/3 per 4 samples (25 x 51200), or the
   // tensor-core weight-gradient splits
   w.part = reinterpret_cast<float*>(take(std::max<size_t>(
-      std::max<size_t>(R * 2400, ((R + 3) / 4) * 64 * 800),
-      std::max<size_t>(conv5_wgrad_part_floats(32, 32, R, 4), conv5_wgrad_part_floats(32, 64, R, 8))) * f));
+      std::max<size_t>(std::max<size_t>(R * 2400, conv5_wgrad_part_floats(3, 32, R, 1)), ((R + 3) / 4) * 64 * 800),
+      std::max<size_t>(conv5_wgrad_part_floats(32, 32, R, 4), conv5_wgrad_part_floats(32, 64, R, 4))) * f));
   w.pb = reinterpret_cast<float*>(take(R * 64 * f));
   w.wpk = reinterpret_cast<float*>(take(conv5_tc_wpk_floats(64, 32) * f));
   w.fcpart = reinterpret_cast<float*>(take(static_cast<size_t>(R) * 64 * (1024 / kFcSlice) * f));  // largest: 64x25 -> 32 (= 32x25 -> 64)
@@ -698,7 +698,7 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
     avepool_bwd2_kernel<<<blocks(R * 64 * 16), 256, 0, s>>>(w.dp3, w.c3, w.dc3, R * 64, 4, gate);
     DS_CUDA_TRY(cudaGetLastError());
     DS_TRY(cnn_edge(s, s2, sd->ev[2]));
-    DS_TRY((launch_conv5_wgrad_tc<32, 64, 8, 8>(w.p2, w.dc3, w.part, grad + L[2].w_off, grad + L[2].b_off, R, inv_b,
+    DS_TRY((launch_conv5_wgrad_tc<32, 64, 8, 4>(w.p2, w.dc3, w.part, grad + L[2].w_off, grad + L[2].b_off, R, inv_b,
                                                 flags, gate, s2)));
     DS_TRY((launch_conv5_tc<64, 32, 8>(w.dc3, P + L[2].w_off, true, w.wpk, nullptr, w.dp2, R, false, gate, s)));
     avepool_bwd2_kernel<<<blocks(R * 32 * 64), 256, 0, s>>>(w.dp2, w.c2, w.dc2, R * 32, 8, gate);
@@ -727,7 +727,7 @@ int launch_cnn_loss_and_grad(const ModelInfo& m, const float* P, const float* X,
   avepool_bwd2_kernel<<<blocks(R * 64 * 16), 256, 0, s>>>(w.dp3, w.c3, w.dc3, R * 64, 4, gate);
   DS_CUDA_TRY(cudaGetLastError());
   if (use_tensor_cores()) {
-    DS_TRY((launch_conv5_wgrad_tc<32, 64, 8, 8>(w.p2, w.dc3, w.part, grad + L[2].w_off, grad + L[2].b_off, R, inv_b,
+    DS_TRY((launch_conv5_wgrad_tc<32, 64, 8, 4>(w.p2, w.dc3, w.part, grad + L[2].w_off, grad + L[2].b_off, R, inv_b,
                                                 flags, gate, s)));
   } else {
     DS_TRY((launch_conv5_bwd_w<32, 8, 2, 4>(w.p2, w.dc3, w.part, w.pb, R, 64, gate, s)));
