@@ -383,6 +383,11 @@ int ds_engine_stream_push_rows(ds_engine* e, const float* X_host, const uint32_t
  * DMA (two CUDA calls per group). */
 int ds_engine_stream_push_rows_n(ds_engine* e, const float* X_host, const uint32_t* y_host, const uint32_t* idx,
                                  const uint32_t* rows, uint64_t nsteps);
+/* Tensor-core engines: keep a bf16 copy of the host shard X_host [n_rows x n_features]
+ * (the same cast as the per-step gather), so later pushes that pass this X_host gather rows
+ * by row copies — half the host memory traffic and no cast per step. X_host NULL drops the
+ * copy. The caller keeps X_host unchanged while it is cached. */
+int ds_engine_stream_cache_host_shard(ds_engine* e, const float* X_host, uint64_t n_rows);
 int ds_engine_stream_end(ds_engine* e);
 /* Host-side gather + bf16 cast the tensor-core stream ring uses (no GPU involved): rows x F
  * floats, row r from X + idx[r] * F (idx NULL: X + r * F), into dst rows of `pitch` bf16

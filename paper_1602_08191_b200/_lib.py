@@ -160,6 +160,7 @@ _sig("ds_engine_stream_begin", VP, U64, VP)
 _sig("ds_engine_stream_push", VP, VP, VP, U32)
 _sig("ds_engine_stream_push_rows", VP, VP, VP, VP, U32)
 _sig("ds_engine_stream_push_rows_n", VP, VP, VP, VP, VP, U64)
+_sig("ds_engine_stream_cache_host_shard", VP, VP, U64)
 _sig("ds_host_rows_to_bf16", VP, U32, VP, U32, VP, U64)
 _sig("ds_engine_stream_end", VP)
 _sig("ds_engine_sync", VP)
@@ -200,7 +201,7 @@ EXPORTED = [
     "ds_master_exchange_ticketed", "ds_master_snapshot", "ds_master_local_slice",
     "ds_master_exchange_count", "ds_master_dim", "ds_master_reset_tickets", "ds_engine_create",
     "ds_engine_destroy", "ds_engine_attach_master", "ds_engine_set_tickets", "ds_engine_run", "ds_engine_run_group", "ds_engine_stream_begin_group", "ds_engine_reserve", "ds_engine_step_host", "ds_engine_step_host_async",
-    "ds_engine_stream_begin", "ds_engine_stream_push", "ds_engine_stream_push_rows", "ds_engine_stream_push_rows_n", "ds_host_rows_to_bf16",
+    "ds_engine_stream_begin", "ds_engine_stream_push", "ds_engine_stream_push_rows", "ds_engine_stream_push_rows_n", "ds_engine_stream_cache_host_shard", "ds_host_rows_to_bf16",
     "ds_engine_stream_end",
     "ds_engine_sync", "ds_engine_stream", "ds_engine_log", "ds_engine_iterations",
     "ds_engine_get_params", "ds_engine_set_params", "ds_engine_params_device", "ds_engine_policy",

@@ -146,6 +146,11 @@ struct ds_engine {
   static constexpr uint32_t kTcRing = 16, kTcGroup = 4;
   uint16_t* tch_ring = nullptr;   // pinned host twin of tc_ring
   uint32_t* tch_words = nullptr;  // pinned host sources of ring_words
+  // ds_engine_stream_cache_host_shard: a bf16 copy of a host shard (rows of F), so the
+  // per-step gather of rows from that shard is a row copy instead of a read + cast
+  const float* hb_src = nullptr;
+  uint64_t hb_rows = 0;
+  std::vector<uint16_t> hb;
   // a DS_FUSED_PROFILE buffer of a stream-mode launch, reported at ds_engine_stream_end
   unsigned long long* prof_pending = nullptr;
   uint64_t prof_steps = 0, prof_n = 0;
@@ -1312,7 +1317,12 @@ void tc_fill(ds_engine* e, uint64_t step, const float* X, const uint32_t* y, con
   const uint32_t F = e->model.n_features;
   const uint64_t slot = step % KT, pitch = dsb::tc_pitch(F);
   uint16_t* base = e->tch_ring + slot * (B + 1) * pitch;
-  dsb::gather_rows_bf16_host(X, F, idx, rows, base, pitch);  // gather_batch + the bf16 operand cast
+  if (X == e->hb_src && !e->hb.empty()) {  // the cached bf16 shard: gather_batch as row copies
+    for (uint32_t r = 0; r < rows; ++r)
+      std::memcpy(base + r * pitch, e->hb.data() + static_cast<uint64_t>(idx ? idx[r] : r) * F, F * sizeof(uint16_t));
+  } else {
+    dsb::gather_rows_bf16_host(X, F, idx, rows, base, pitch);  // gather_batch + the bf16 operand cast
+  }
   uint32_t* lab = reinterpret_cast<uint32_t*>(base + B * pitch);
   for (uint32_t r = 0; r < rows; ++r) lab[r] = y[idx ? idx[r] : r];
   e->tch_words[slot] = (rows << 20) | (static_cast<uint32_t>(step + 1) & 0xFFFFFu);
@@ -1436,6 +1446,38 @@ extern "C" int ds_engine_stream_push_rows_n(ds_engine* e, const float* X_host, c
   e->ring_pushed = base + nsteps;
   for (uint32_t t = 0; t < T; ++t)
     if (rc[t] != DS_OK) return set_error(rc[t], "%s", msg[t].c_str());
+  return DS_OK;
+}
+
+extern "C" int ds_engine_stream_cache_host_shard(ds_engine* e, const float* X_host, uint64_t n_rows) {
+  if (!e) return set_error(DS_E_CONTRACT, "engine_stream_cache_host_shard: null engine");
+  if (!X_host || n_rows == 0) {  // drop the cache
+    e->hb_src = nullptr;
+    e->hb_rows = 0;
+    std::vector<uint16_t>().swap(e->hb);
+    return DS_OK;
+  }
+  if (!e->tc) return set_error(DS_E_CONTRACT, "engine_stream_cache_host_shard: needs a tensor-core engine");
+  const uint32_t F = e->model.n_features;
+  e->hb.resize(n_rows * F);
+  // the same cast as the per-step path (gather_rows_bf16_host: RNE, NaN, denormals), split
+  // over a few threads
+  uint32_t T = 4;
+  if (const char* env = std::getenv("DS_STREAM_FEED_THREADS")) T = static_cast<uint32_t>(std::max(1, std::atoi(env)));
+  T = static_cast<uint32_t>(std::min<uint64_t>(T, n_rows));
+  auto work = [&](uint32_t t) {
+    const uint64_t r0 = n_rows * t / T, r1 = n_rows * (t + 1) / T;
+    for (uint64_t r = r0; r < r1; r += 65536) {
+      const uint32_t n = static_cast<uint32_t>(std::min<uint64_t>(65536, r1 - r));
+      dsb::gather_rows_bf16_host(X_host + r * F, F, nullptr, n, e->hb.data() + r * F, F);
+    }
+  };
+  std::vector<std::thread> th;
+  for (uint32_t t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  e->hb_src = X_host;
+  e->hb_rows = n_rows;
   return DS_OK;
 }
 

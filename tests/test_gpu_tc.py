@@ -200,6 +200,16 @@ def test_tc_stream_and_host_steps_equal_device_run(L, orc, api, adaptive):
     L.check(L.lib.ds_engine_stream_end(e3))
     assert np.array_equal(params_of(L, e3, P), ref_p) and np.array_equal(engine_log(L, e3, 0, steps)[0], ref_l)
     L.lib.ds_engine_destroy(e3)
+    # the same pushes from a cached bf16 copy of the host shard (row copies instead of casts)
+    e5 = make_engine(L, m, X, y, 10, hp, 31, init)
+    L.check(L.lib.ds_engine_stream_cache_host_shard(e5, Xc.ctypes.data, len(yc)))
+    L.check(L.lib.ds_engine_stream_begin(e5, steps, C.c_void_p(loss_h.data_ptr())))
+    L.check(L.lib.ds_engine_stream_push_rows_n(e5, Xc.ctypes.data, yc.ctypes.data, idx_all.ctypes.data,
+                                               rows_all.ctypes.data, steps))
+    L.check(L.lib.ds_engine_stream_end(e5))
+    assert np.array_equal(params_of(L, e5, P), ref_p) and np.array_equal(engine_log(L, e5, 0, steps)[0], ref_l)
+    L.check(L.lib.ds_engine_stream_cache_host_shard(e5, None, 0))
+    L.lib.ds_engine_destroy(e5)
     e4 = make_engine(L, m, X, y, 10, hp, 31, init)
     L.check(L.lib.ds_engine_stream_begin(e4, steps, C.c_void_p(loss_h.data_ptr())))
     keep = []
