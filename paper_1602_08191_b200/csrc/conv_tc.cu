@@ -304,27 +304,35 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_wgrad_tc_kernel(const flo
     for (int i = 0; i < nchunks; ++i) {
       const uint32_t n = n_lo + i / S::CPS, p0 = (i % S::CPS) * kKC;
       if (i % S::CPS == 0) {  // stage sample n as HWC (all producers; the ring holds copies)
-        asm volatile("bar.sync 1, %0;" ::"n"(kTile) : "memory");
-        for (uint32_t j = tid; j < static_cast<uint32_t>(CIN * S::HP); j += kTile) {
-          const uint32_t ci = j % CIN, row = j / CIN;
+        // every global load of the sample is issued before the first shared store (one
+        // memory round trip per sample instead of one per (channel, row) line a thread owns)
+        constexpr int kLines = (CIN * S::HP + kTile - 1) / kTile;  // lines per thread
+        float4 v[kLines][H / 4];
+#pragma unroll
+        for (int li = 0; li < kLines; ++li) {
+          const uint32_t j = tid + li * kTile, ci = j % CIN, row = j / CIN;
           const int y = static_cast<int>(row) - 2;
+          const bool live = j < static_cast<uint32_t>(CIN * S::HP) && y >= 0 && y < H;
+          const float4* src = reinterpret_cast<const float4*>(in + ((static_cast<uint64_t>(n) * CIN + ci) * H + (live ? y : 0)) * H);
+#pragma unroll
+          for (int q = 0; q < H / 4; ++q) v[li][q] = live ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTile) : "memory");
+#pragma unroll
+        for (int li = 0; li < kLines; ++li) {
+          const uint32_t j = tid + li * kTile;
+          if (j >= static_cast<uint32_t>(CIN * S::HP)) break;
+          const uint32_t ci = j % CIN, row = j / CIN;
           constexpr uint32_t step = S::kHWC ? S::CS : 1;
           float* dst = S::kHWC ? xs + static_cast<size_t>(row) * S::HP * S::CS + ci
                                : xs + (static_cast<size_t>(ci) * S::HP + row) * S::HP;
           dst[0] = dst[step] = dst[(H + 2) * step] = dst[(H + 3) * step] = 0.0f;
-          if (y >= 0 && y < H) {
-            const float4* src = reinterpret_cast<const float4*>(in + ((static_cast<uint64_t>(n) * CIN + ci) * H + y) * H);
 #pragma unroll
-            for (int q = 0; q < H / 4; ++q) {
-              const float4 v = __ldg(src + q);
-              dst[(2 + 4 * q) * step] = v.x;
-              dst[(3 + 4 * q) * step] = v.y;
-              dst[(4 + 4 * q) * step] = v.z;
-              dst[(5 + 4 * q) * step] = v.w;
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < H; ++q) dst[(2 + q) * step] = 0.0f;
+          for (int q = 0; q < H / 4; ++q) {
+            dst[(2 + 4 * q) * step] = v[li][q].x;
+            dst[(3 + 4 * q) * step] = v[li][q].y;
+            dst[(4 + 4 * q) * step] = v[li][q].z;
+            dst[(5 + 4 * q) * step] = v[li][q].w;
           }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kTile) : "memory");
