@@ -77,8 +77,11 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
   // stage the tile's zero-padded input rows: xs[s][ci][row][col], row r <-> image row
   // h0 - 2 + r (or the whole padded image for multi-sample tiles)
   // one (sample, channel, row) per thread and iteration: a coalesced, vectorised row read
-  for (uint32_t i = tid; i < static_cast<uint32_t>(S::SPT * CIN * S::ROWS); i += kThreads) {
-    uint32_t row, ci, sl;
+  // all of a thread's line loads are issued before its first shared store (one memory
+  // round trip instead of one per line)
+  constexpr int kLines = (S::SPT * CIN * S::ROWS + kThreads - 1) / kThreads;
+  float4 v[kLines][H / 4];
+  auto line = [&](uint32_t i, uint32_t& row, uint32_t& ci, uint32_t& sl) {
     if constexpr (S::kHWC) {  // channel fastest across threads: conflict-free HWC stores
       ci = i % CIN;
       row = (i / CIN) % S::ROWS;
@@ -88,28 +91,37 @@ __global__ void __launch_bounds__(kTile + 32, 1) conv5_tc_kernel(const float* __
       ci = (i / S::ROWS) % CIN;
       sl = i / (S::ROWS * CIN);
     }
+  };
+#pragma unroll
+  for (int li = 0; li < kLines; ++li) {
+    const uint32_t i = tid + li * kThreads;
+    uint32_t row, ci, sl;
+    line(i, row, ci, sl);
     const int y = static_cast<int>(h0 + row) - 2;
     const uint32_t n = n0 + sl;
+    const bool live = i < static_cast<uint32_t>(S::SPT * CIN * S::ROWS) && n < R && y >= 0 && y < H;
+    const float4* src =
+        reinterpret_cast<const float4*>(in + ((static_cast<uint64_t>(live ? n : 0) * CIN + ci) * H + (live ? y : 0)) * H);
+#pragma unroll
+    for (int q = 0; q < H / 4; ++q) v[li][q] = live ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int li = 0; li < kLines; ++li) {
+    const uint32_t i = tid + li * kThreads;
+    if (i >= static_cast<uint32_t>(S::SPT * CIN * S::ROWS)) break;
+    uint32_t row, ci, sl;
+    line(i, row, ci, sl);
     // element col of this (sl, row, ci) line lives at dst[col * step]
     float* dst = S::kHWC ? xs + (static_cast<size_t>(sl) * S::ROWS + row) * S::HP * S::CS + ci
                          : xs + ((static_cast<size_t>(sl) * CIN + ci) * S::ROWS + row) * S::HP;
     constexpr uint32_t step = S::kHWC ? S::CS : 1;
     dst[0] = dst[step] = dst[(H + 2) * step] = dst[(H + 3) * step] = 0.0f;
-    if (n < R && y >= 0 && y < H) {
-      const float4* src = reinterpret_cast<const float4*>(in + ((static_cast<uint64_t>(n) * CIN + ci) * H + y) * H);
-      float4 v[H / 4];
 #pragma unroll
-      for (int q = 0; q < H / 4; ++q) v[q] = __ldg(src + q);
-#pragma unroll
-      for (int q = 0; q < H / 4; ++q) {
-        dst[(2 + 4 * q) * step] = v[q].x;
-        dst[(3 + 4 * q) * step] = v[q].y;
-        dst[(4 + 4 * q) * step] = v[q].z;
-        dst[(5 + 4 * q) * step] = v[q].w;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < H; ++q) dst[(2 + q) * step] = 0.0f;
+    for (int q = 0; q < H / 4; ++q) {
+      dst[(2 + 4 * q) * step] = v[li][q].x;
+      dst[(3 + 4 * q) * step] = v[li][q].y;
+      dst[(4 + 4 * q) * step] = v[li][q].z;
+      dst[(5 + 4 * q) * step] = v[li][q].w;
     }
   }
   for (uint32_t k = tid; k < static_cast<uint32_t>(S::NKC * kKC); k += kThreads) {
