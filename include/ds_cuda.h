@@ -386,7 +386,8 @@ int ds_engine_stream_push_rows_n(ds_engine* e, const float* X_host, const uint32
 /* Tensor-core engines: keep a bf16 copy of the host shard X_host [n_rows x n_features]
  * (the same cast as the per-step gather), so later pushes that pass this X_host gather rows
  * by row copies — half the host memory traffic and no cast per step. X_host NULL drops the
- * copy. The caller keeps X_host unchanged while it is cached. */
+ * copy. Not while a stream is open (DS_E_STATE); the caller keeps X_host unchanged while it
+ * is cached. */
 int ds_engine_stream_cache_host_shard(ds_engine* e, const float* X_host, uint64_t n_rows);
 int ds_engine_stream_end(ds_engine* e);
 /* Host-side gather + bf16 cast the tensor-core stream ring uses (no GPU involved): rows x F

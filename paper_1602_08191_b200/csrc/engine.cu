@@ -26,6 +26,7 @@
 #include <numeric>
 #include <set>
 #include <string>
+#include <new>
 #include <thread>
 #include <vector>
 
@@ -1451,6 +1452,7 @@ extern "C" int ds_engine_stream_push_rows_n(ds_engine* e, const float* X_host, c
 
 extern "C" int ds_engine_stream_cache_host_shard(ds_engine* e, const float* X_host, uint64_t n_rows) {
   if (!e) return set_error(DS_E_CONTRACT, "engine_stream_cache_host_shard: null engine");
+  if (e->ring_active) return set_error(DS_E_STATE, "engine_stream_cache_host_shard: not while a stream is open");
   if (!X_host || n_rows == 0) {  // drop the cache
     e->hb_src = nullptr;
     e->hb_rows = 0;
@@ -1459,7 +1461,13 @@ extern "C" int ds_engine_stream_cache_host_shard(ds_engine* e, const float* X_ho
   }
   if (!e->tc) return set_error(DS_E_CONTRACT, "engine_stream_cache_host_shard: needs a tensor-core engine");
   const uint32_t F = e->model.n_features;
-  e->hb.resize(n_rows * F);
+  try {
+    e->hb.resize(n_rows * F);
+  } catch (const std::bad_alloc&) {
+    e->hb_src = nullptr;
+    return set_error(DS_E_NOMEM, "engine_stream_cache_host_shard: %llu bf16 rows do not fit in host memory",
+                     static_cast<unsigned long long>(n_rows));
+  }
   // the same cast as the per-step path (gather_rows_bf16_host: RNE, NaN, denormals), split
   // over a few threads
   uint32_t T = 4;

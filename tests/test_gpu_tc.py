@@ -204,6 +204,8 @@ def test_tc_stream_and_host_steps_equal_device_run(L, orc, api, adaptive):
     e5 = make_engine(L, m, X, y, 10, hp, 31, init)
     L.check(L.lib.ds_engine_stream_cache_host_shard(e5, Xc.ctypes.data, len(yc)))
     L.check(L.lib.ds_engine_stream_begin(e5, steps, C.c_void_p(loss_h.data_ptr())))
+    with pytest.raises(L.StateError, match="stream is open"):  # the pushes may be reading the copy
+        L.check(L.lib.ds_engine_stream_cache_host_shard(e5, Xc.ctypes.data, len(yc)))
     L.check(L.lib.ds_engine_stream_push_rows_n(e5, Xc.ctypes.data, yc.ctypes.data, idx_all.ctypes.data,
                                                rows_all.ctypes.data, steps))
     L.check(L.lib.ds_engine_stream_end(e5))
@@ -352,6 +354,17 @@ def test_tc_errors(L, orc):
     X, y = orc.gen_synthetic(300, 20, 3, 2.0, 1.5, 3)
     init = orc.init_params(m, 9)
     hp = Hyper(eta=0.05, tau=5, batch_size=16, i_max=10)
+    # the bf16 host-shard cache: contract errors on a null engine / a non-tensor-core engine;
+    # dropping a cache that does not exist is a no-op
+    with pytest.raises(L.ContractError):
+        L.check(L.lib.ds_engine_stream_cache_host_shard(None, X.ctypes.data, len(y)))
+    e = make_engine(L, m, X, y, 3, hp, 31, init, kind=L.DS_ENGINE_FUSED)
+    try:
+        with pytest.raises(L.ContractError, match="tensor-core"):
+            L.check(L.lib.ds_engine_stream_cache_host_shard(e, X.ctypes.data, len(y)))
+        L.check(L.lib.ds_engine_stream_cache_host_shard(e, None, 0))
+    finally:
+        L.lib.ds_engine_destroy(e)
     e = make_engine(L, m, X, y, 3, hp, 31, init)
     try:  # a host-fed batch with a label out of range, caught in the kernel (model.cpp:176-180)
         xb = np.ascontiguousarray(X[:16], np.float32)
